@@ -1,0 +1,471 @@
+"""Pins of the fp64 oracle against things other than itself (all CPU, -m "not gpu").
+
+Each test names what fixes the expected value: a closed form, a textbook special
+case, a library routine, a hand-derived golden value (tests/golden/), brute
+force, or an invariant the paper states.  A plausible mistake anywhere in the
+oracle (dropped term, wrong sign or index, transposed operand, wrong pairing,
+off-by-one position, wrong GQA map, missing sink, wrong eviction) fails at
+least one of them.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import dscache_synth as synth
+from oracle import dscache_oracle as O
+from oracle.workload import StreamInputs, oracle_step, step_schedule
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "schedule_spot_values.json")
+RNG = np.random.default_rng(12345)
+
+
+# --------------------------------------------------------------------------- RoPE
+def test_rope_position_zero_is_identity_bitwise():
+    # SPEC.md:113 "any x at position 0 -> x unchanged"; cos 0 = 1, sin 0 = 0 exactly.
+    x = RNG.standard_normal((7, 3, 128))
+    for style in (O.SPLIT_HALF, O.ADJACENT):
+        assert np.array_equal(O.rope(x, np.zeros(7), 1e6, style), x)
+
+
+def test_rope_d2_is_textbook_rotation():
+    # d = 2 has one pair with theta_0 = base^0 = 1: (1, 0) at position p -> (cos p, sin p).
+    for p in [0, 1, 2, 5, 17, 1000]:
+        y = O.rope(np.array([[1.0, 0.0]]), np.array([p]), 1e4)
+        assert np.allclose(y[0], [math.cos(p), math.sin(p)], atol=1e-15, rtol=0)
+        y = O.rope(np.array([[0.0, 1.0]]), np.array([p]), 1e4)
+        assert np.allclose(y[0], [-math.sin(p), math.cos(p)], atol=1e-15, rtol=0)
+
+
+def test_rope_split_half_pairing():
+    # e_i (i < d/2) only mixes with e_{i+d/2}: a mistaken adjacent pairing fails here.
+    d, p, base = 128, 9, 1e6
+    for i in [0, 1, 37, 63]:
+        e = np.zeros((1, d)); e[0, i] = 1.0
+        y = O.rope(e, np.array([p]), base)[0]
+        nz = set(np.nonzero(np.abs(y) > 1e-300)[0].tolist())
+        assert nz <= {i, i + d // 2}
+        assert abs(y[i] ** 2 + y[i + d // 2] ** 2 - 1.0) < 1e-14
+
+
+def test_rope_matches_qwen2_library_rotary():
+    # Library routine: transformers' Qwen2 rotary embedding (the LLaVA-OV-7B LM) computes
+    # inv_freq = 1 / base^(arange(0, d, 2)/d) and rotate_half pairing; its cos/sin are fp32.
+    from transformers import Qwen2Config
+    from transformers.models.qwen2 import modeling_qwen2 as m
+    hcfg = Qwen2Config(hidden_size=28 * 128, num_attention_heads=28, num_key_value_heads=4, rope_theta=1e6)
+    rot = m.Qwen2RotaryEmbedding(hcfg)
+    n = 40
+    pos = torch.arange(n)[None]
+    cos, sin = rot(torch.zeros(1, 1, n, 128, dtype=torch.float64), pos)
+    q = torch.randn(1, 28, n, 128, dtype=torch.float64)
+    k = torch.randn(1, 4, n, 128, dtype=torch.float64)
+    qe, ke = m.apply_rotary_pos_emb(q, k, cos.double(), sin.double())
+    ours_q = O.rope(q[0].permute(1, 0, 2).numpy(), np.arange(n), 1e6)
+    ours_k = O.rope(k[0].permute(1, 0, 2).numpy(), np.arange(n), 1e6)
+    assert np.abs(ours_q - qe[0].permute(1, 0, 2).numpy()).max() < 2e-5   # fp32 angle error at p < 40
+    assert np.abs(ours_k - ke[0].permute(1, 0, 2).numpy()).max() < 2e-5
+
+
+def test_rope_isometry():
+    x = RNG.standard_normal((500, 128))
+    p = RNG.integers(0, 30000, 500)
+    y = O.rope(x, p, 1e6)
+    assert np.allclose(np.linalg.norm(y, axis=1), np.linalg.norm(x, axis=1), rtol=1e-13, atol=0)
+
+
+def test_rope_group_property():
+    # R(p2) R(p1) = R(p1 + p2): rotations compose additively.
+    x = RNG.standard_normal((300, 64))
+    p1 = RNG.integers(0, 20000, 300); p2 = RNG.integers(0, 20000, 300)
+    for style in (O.SPLIT_HALF, O.ADJACENT):
+        a = O.rope(O.rope(x, p1, 1e4, style), p2, 1e4, style)
+        b = O.rope(x, p1 + p2, 1e4, style)
+        assert np.abs(a - b).max() < 1e-9
+
+
+def test_rope_shift_invariance_1e5_trials():
+    # PAPER.md:662-664 <f(q,i), f(k,j)> = g(q, k, i-j); SPEC.md:137 bound 1e-10 (we hold 1e-10).
+    n = 100_000
+    q = RNG.standard_normal((n, 64)); k = RNG.standard_normal((n, 64))
+    j = RNG.integers(0, 4000, n); i = j + RNG.integers(0, 4000, n); s = RNG.integers(-j, 4000)
+    a = np.sum(O.rope(q, i, 1e4) * O.rope(k, j, 1e4), axis=1)
+    b = np.sum(O.rope(q, i + s, 1e4) * O.rope(k, j + s, 1e4), axis=1)
+    assert np.abs(a - b).max() <= 1e-10
+    # and i == j gives <q, k> (both rotations cancel)
+    c = np.sum(O.rope(q, j, 1e4) * O.rope(k, j, 1e4), axis=1)
+    assert np.abs(c - np.sum(q * k, axis=1)).max() <= 1e-10
+
+
+# --------------------------------------------------------------------------- schedule (Eq. 3/5/6)
+def closed_form(cfg, t):
+    """Independent derivation of the FIFO state (SURVEY §8(a)2 closed form)."""
+    lI, lU, tpf = cfg.instant_frames, cfg.past_frames, cfg.tokens_per_frame
+    inst = list(range(max(0, t - lI + 1), t + 1))
+    past = list(range(max(0, t - lI - lU + 1), t - lI + 1))
+    ev = [t - lI - lU] if t - lI - lU >= 0 else []
+    return inst, past, ev
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
+def test_fifo_matches_closed_form_every_step(name):
+    cfg = synth.CONFIGS[name]
+    for t in range(cfg.num_frames):
+        sch = step_schedule(cfg, t)
+        inst, past, ev = closed_form(cfg, t)
+        assert sch.instant_frames == inst and sch.past_frames == past and sch.evicted == ev, t
+
+
+def test_fifo_matches_closed_form_c4_sampled():
+    cfg = synth.CONFIGS["c4"]
+    for t in [0, 7, 8, 135, 136, 137, 272, 1000, 2047, 4095]:
+        sch = step_schedule(cfg, t)
+        inst, past, ev = closed_form(cfg, t)
+        assert sch.instant_frames == inst and sch.past_frames == past and sch.evicted == ev, t
+
+
+def test_schedule_golden_spot_values():
+    g = json.load(open(GOLDEN))
+    for name in ("c1", "c2"):
+        cfg = synth.CONFIGS[name]
+        for t, v in g[name]["P_t"].items():
+            assert step_schedule(cfg, int(t)).P_t == v
+        for t, v in g[name]["C_t"].items():
+            assert step_schedule(cfg, int(t)).C_t == v
+        fe = g[name]["first_eviction"]
+        assert step_schedule(cfg, fe["step"]).evicted == [fe["frame"]]
+        assert step_schedule(cfg, fe["step"] - 1).evicted == []
+    for name in ("c1", "c2", "c4"):
+        cfg = synth.CONFIGS[name]
+        t = cfg.num_frames - 1
+        sch = step_schedule(cfg, t)
+        bk, bq, ak, aq = O.position_ids(sch, cfg.query_tokens)
+        ctx_max = int(ak[-1 - cfg.query_tokens])
+        assert ctx_max == g[name]["max_context_key_id"]
+        assert int(aq.max()) == g[name]["max_query_id"]
+        assert int(aq.max()) < cfg.max_position
+    c4 = synth.CONFIGS["c4"]
+    assert c4.sink_tokens + c4.num_frames * c4.tokens_per_frame == g["c4"]["total_tokens"]
+
+
+def test_ring_slack_frame_is_next_frames_slots():
+    # R = (l_U + l_I + 1) tpf: the frame evicted at t occupies exactly the slots frame t+1 will
+    # take (the slack frame), and the window frames never collide.
+    for name in ("c1", "c2", "c5"):
+        cfg = synth.CONFIGS[name]
+        for t in range(cfg.num_frames - 1):
+            sch = step_schedule(cfg, t)
+            used = np.concatenate([O.ring_slots(f, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames)
+                                   for f in sch.past_frames + sch.instant_frames])
+            assert len(set(used.tolist())) == len(used)
+            for e in sch.evicted:
+                assert np.array_equal(
+                    O.ring_slots(e, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames),
+                    O.ring_slots(t + 1, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames))
+
+
+def test_position_ids_bounded_for_every_config():
+    # PAPER.md:236 "positional indices remain bounded"; north_star: below W+C+sink for keys.
+    for cfg in synth.CONFIGS.values():
+        for t in (0, cfg.num_frames - 1):
+            sch = step_schedule(cfg, t)
+            bk, bq, ak, aq = O.position_ids(sch, cfg.query_tokens)
+            assert ak[: len(ak) - cfg.query_tokens].max() < cfg.sink_tokens + cfg.W + cfg.C
+            assert aq.max() < cfg.sink_tokens + cfg.W + cfg.C + cfg.query_tokens <= cfg.max_position
+
+
+# --------------------------------------------------------------------------- attention core
+def test_softmax_attention_matches_torch_sdpa_fp64():
+    # Library routine: torch scaled_dot_product_attention with a boolean mask (fp64, CPU).
+    nq, nk, d = 37, 91, 64
+    q = RNG.standard_normal((nq, d)); k = RNG.standard_normal((nk, d)); v = RNG.standard_normal((nk, 48))
+    vis = RNG.random((nq, nk)) < 0.6
+    vis[:, 0] = True
+    ours = O.softmax_attention(q, k, v, vis)
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(q)[None], torch.from_numpy(k)[None], torch.from_numpy(v)[None],
+        attn_mask=torch.from_numpy(vis)[None])[0].numpy()
+    assert np.abs(ours - ref).max() < 1e-13
+
+
+def test_gqa_head_map_matches_repeat_kv_sdpa():
+    # HF repeat_kv convention (reading Q10): query head h uses kv head h // (Hq/Hkv).
+    nq, hq, hkv, d = 5, 28, 4, 32
+    q = RNG.standard_normal((nq, hq, d)); k = RNG.standard_normal((11, hkv, d)); v = RNG.standard_normal((11, hkv, d))
+    pos_k = np.arange(11); pos_q = 6 + np.arange(5)
+    ours = O.gqa_attention(q, pos_q, k, v, pos_k, 1e4)
+    qr = torch.from_numpy(O.rope(q, pos_q, 1e4)).permute(1, 0, 2)
+    kr = torch.from_numpy(O.rope(k, pos_k, 1e4)).permute(1, 0, 2).repeat_interleave(hq // hkv, 0)
+    vv = torch.from_numpy(v).permute(1, 0, 2).repeat_interleave(hq // hkv, 0)
+    mask = torch.from_numpy(pos_k[None, :] <= pos_q[:, None])
+    ref = torch.nn.functional.scaled_dot_product_attention(qr, kr, vv, attn_mask=mask).permute(1, 0, 2).numpy()
+    assert np.abs(ours - ref).max() < 1e-13
+
+
+# --------------------------------------------------------------------------- closed forms on the step
+def _zero_q_inputs(cfg, id_in_v):
+    """Inputs with Q = 0 (uniform softmax) and V[.][0] = position id if id_in_v."""
+    inp = StreamInputs(cfg, 0, 0)
+
+    class Z(StreamInputs):
+        pass
+    z = Z(cfg, 0, 0)
+    z.instant_q = lambda t, n: np.zeros((n, cfg.num_q_heads, cfg.head_dim))
+    base_query = inp.query
+    z.query = lambda t, n_q=None: (np.zeros_like(base_query(t, n_q)[0]),) + base_query(t, n_q)[1:]
+    return z
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_zero_query_gives_mean_of_visible_values(name):
+    # Q = 0 -> every score 0 -> O = mean of the visible V.  Build row i sees A + i + 1 keys,
+    # attend row i sees A + P_t + C_t + i + 1 keys (sink, past, instant, self[0..i]).
+    cfg = synth.CONFIGS[name].replace(num_frames=12)
+    z = _zero_q_inputs(cfg, False)
+    for t in (0, 1, 4, 11):
+        sch, o_inst, o = oracle_step(cfg, 0, 0, t, inputs=z)
+        sk, sv = z.sink()
+        vals = [sv] + [z.frame_kv(f)[1] for f in sch.past_frames + sch.instant_frames]
+        ctx = np.concatenate(vals)
+        _, _, vself = z.query(t)
+        grp = cfg.num_q_heads // cfg.num_kv_heads
+        for h in (0, cfg.num_q_heads - 1):
+            g = h // grp
+            allv = np.concatenate([ctx[:, g], vself[:, g]])
+            L = len(ctx)
+            for i in (0, cfg.query_tokens - 1):
+                assert np.abs(o[i, h] - allv[: L + i + 1].mean(0)).max() < 1e-12
+            inst_v = np.concatenate([sv] + [z.frame_kv(f)[1] for f in sch.instant_frames])[:, g]
+            for i in (0, sch.C_t - 1):
+                assert np.abs(o_inst[i, h] - inst_v[: cfg.sink_tokens + i + 1].mean(0)).max() < 1e-12
+
+
+def test_zero_query_position_id_encoding():
+    # V[j][0] = id(j), Q = 0  ->  O[i][0] = mean(0..lim_i) = lim_i / 2 exactly; pins the visible
+    # *set* and the ids (an off-by-one position or a dropped sink shifts the mean).
+    cfg = synth.CONFIGS["c1"]
+    A, tpf = cfg.sink_tokens, cfg.tokens_per_frame
+    for t in (0, 3, 7, 19):
+        sch = step_schedule(cfg, t)
+        d, hkv = cfg.head_dim, cfg.num_kv_heads
+        def fr(f):
+            k = np.zeros((tpf, hkv, d)); v = np.zeros((tpf, hkv, d))
+            return k, v
+        # value column 0 carries the id the *context* assigns: fill after concatenation
+        frames = sch.past_frames + sch.instant_frames
+        id_of = {}
+        for n, f in enumerate(frames):
+            id_of[f] = A + n * tpf + np.arange(tpf)
+        def frv(f):
+            k, v = fr(f)
+            v[:, :, 0] = id_of[f][:, None]
+            return k, v
+        sink = (np.zeros((A, hkv, d)), np.zeros((A, hkv, d)))
+        sink[1][:, :, 0] = np.arange(A)[:, None]
+        nq = cfg.query_tokens
+        L = A + sch.P_t + sch.C_t
+        vself = np.zeros((nq, hkv, d)); vself[:, :, 0] = (L + np.arange(nq))[:, None]
+        o = O.attend_output(sch, sink, frv, np.zeros((nq, cfg.num_q_heads, d)), np.zeros((nq, hkv, d)),
+                            vself, cfg.rope_theta)
+        assert np.abs(o[:, :, 0] - ((L + np.arange(nq)) / 2.0)[:, None]).max() < 1e-12
+        # instant build: ids A + i inside [sink | instant] only
+        id_of = {f: A + n * tpf + np.arange(tpf) for n, f in enumerate(sch.instant_frames)}
+        oi = O.instant_cache_output(sch, sink, frv, np.zeros((sch.C_t, cfg.num_q_heads, d)), cfg.rope_theta)
+        assert np.abs(oi[:, :, 0] - ((A + np.arange(sch.C_t)) / 2.0)[:, None]).max() < 1e-12
+
+
+def test_single_visible_key_returns_its_value():
+    # A = 0: instant row 0 sees only instant key 0 -> O_inst[0] = v_0 for every head.
+    cfg = synth.CONFIGS["c1"].replace(sink_tokens=0)
+    inp = StreamInputs(cfg, 0, 0)
+    for t in (0, 6):
+        sch, o_inst, _ = oracle_step(cfg, 0, 0, t, inputs=inp)
+        v0 = inp.frame_kv(sch.instant_frames[0])[1][0]
+        for h in range(cfg.num_q_heads):
+            assert np.abs(o_inst[0, h] - v0[h // (cfg.num_q_heads // cfg.num_kv_heads)]).max() < 1e-15
+
+
+# --------------------------------------------------------------------------- brute force
+def _brute_rope(vec, p, base):
+    d = len(vec); h = d // 2
+    out = list(vec)
+    for i in range(h):
+        th = base ** (-2.0 * i / d)
+        c, s = math.cos(p * th), math.sin(p * th)
+        a, b = vec[i], vec[i + h]
+        out[i] = a * c - b * s
+        out[i + h] = a * s + b * c
+    return out
+
+
+def _brute_attend(qv, qpos, keys, base):
+    """keys: list of (pos, k, v); pure-Python softmax over keys with pos <= qpos."""
+    qr = _brute_rope(qv, qpos, base)
+    sc = []
+    for (p, k, v) in keys:
+        if p <= qpos:
+            kr = _brute_rope(k, p, base)
+            sc.append((sum(a * b for a, b in zip(qr, kr)) / math.sqrt(len(qv)), v))
+    m = max(s for s, _ in sc)
+    w = [math.exp(s - m) for s, _ in sc]
+    den = sum(w)
+    return [sum(wi * v[c] for wi, (_, v) in zip(w, sc)) / den for c in range(len(sc[0][1]))]
+
+
+def test_brute_force_full_history_tiny_stream():
+    """Keep EVERY token ever appended (full history); slice the window from the end of the
+    history as PAPER.md:113-114 / Eq. 6 describe (the last l_W = (l_U + l_I) frames behind
+    the sink), and recompute both attentions with pure-Python loops."""
+    cfg = synth.StreamConfig("tiny", 99, 1, 1, 4, 2, 8, 1e4, 3, 2, 2, 2, 3, 9, "fp32", 1.0)
+    inp = StreamInputs(cfg, 0, 0)
+    sk, sv = inp.sink()
+    A, tpf, lI, lU = cfg.sink_tokens, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames
+    grp = cfg.num_q_heads // cfg.num_kv_heads
+    history = []   # (frame, k [Hkv,d], v)
+    for t in range(cfg.num_frames):
+        fk, fv = inp.frame_kv(t)
+        history += [(t, fk[j], fv[j]) for j in range(tpf)]
+        sch, o_inst, o = oracle_step(cfg, 0, 0, t, inputs=inp)
+        window = history[-(lU + lI) * tpf:]                 # P_{l_P - l_W : l_P}
+        inst = history[-lI * tpf:]                          # the buffer B_t
+        q, ks, vs = inp.query(t)
+        nq = q.shape[0]
+        for h in range(cfg.num_q_heads):
+            g = h // grp
+            keys = [(j, list(sk[j, g]), list(sv[j, g])) for j in range(A)]
+            keys += [(A + n, list(k[g]), list(v[g])) for n, (_, k, v) in enumerate(window)]
+            L = len(keys)
+            keys += [(L + i, list(ks[i, g]), list(vs[i, g])) for i in range(nq)]
+            for i in range(nq):
+                ref = _brute_attend(list(q[i, h]), L + i, keys, cfg.rope_theta)
+                assert np.abs(np.array(ref) - o[i, h]).max() < 1e-12
+            ikeys = [(j, list(sk[j, g]), list(sv[j, g])) for j in range(A)]
+            ikeys += [(A + n, list(k[g]), list(v[g])) for n, (_, k, v) in enumerate(inst)]
+            qi = inp.instant_q(t, sch.C_t)
+            for i in range(sch.C_t):
+                ref = _brute_attend(list(qi[i, h]), A + i, ikeys, cfg.rope_theta)
+                assert np.abs(np.array(ref) - o_inst[i, h]).max() < 1e-12
+
+
+# --------------------------------------------------------------------------- paper invariants
+def _abs_attend(cfg, sch, inp, t, pos_mode):
+    """Attend computed with *absolute* ids (standard cache, Eq. 1 / App. B): stream token
+    a has id a (A = 0), the query chunk follows the newest frame."""
+    tpf = cfg.tokens_per_frame
+    frames = sch.past_frames + sch.instant_frames
+    ks = np.concatenate([inp.frame_kv(f)[0] for f in frames])
+    vs = np.concatenate([inp.frame_kv(f)[1] for f in frames])
+    pk = np.concatenate([f * tpf + np.arange(tpf) for f in frames])
+    q, kq, vq = inp.query(t)
+    nq = q.shape[0]
+    pq = (t + 1) * tpf + np.arange(nq)
+    if pos_mode == "shuffled":
+        pk = RNG.permutation(pk)
+    kk = np.concatenate([ks, kq]); vv = np.concatenate([vs, vq]); pp = np.concatenate([pk, pq])
+    return O.gqa_attention(q, pq, kk, vv, pp, cfg.rope_theta)
+
+
+def test_proposition_rebased_equals_absolute_ids_with_eviction():
+    # Proposition 3.2 (proof "Case eviction" PAPER.md:647-684): with no sink
+    # (A = 0) the contiguous re-basing is a distance-preserving shift of the absolute ids,
+    # so outputs are identical; a shuffled-position negative control must differ.
+    cfg = synth.CONFIGS["c1"].replace(sink_tokens=0, num_frames=12)
+    inp = StreamInputs(cfg, 0, 0)
+    for t in (2, 5, 6, 11):               # before and after the first eviction (t = 5)
+        sch, _, o = oracle_step(cfg, 0, 0, t, inputs=inp)
+        assert np.abs(o - _abs_attend(cfg, sch, inp, t, "abs")).max() < 1e-12
+    sch, _, o = oracle_step(cfg, 0, 0, 11, inputs=inp)
+    assert np.abs(o - _abs_attend(cfg, sch, inp, 11, "shuffled")).max() > 1e-3
+
+
+def test_proposition_with_sink_before_first_eviction():
+    # Before any eviction the contiguous ids ARE the absolute ids (sink 0..A-1, then the stream).
+    cfg = synth.CONFIGS["c1"]
+    inp = StreamInputs(cfg, 0, 0)
+    A, tpf = cfg.sink_tokens, cfg.tokens_per_frame
+    for t in (0, 2, 4):
+        sch, _, o = oracle_step(cfg, 0, 0, t, inputs=inp)
+        assert not sch.evicted and sch.past_frames[:1] in ([], [0])
+        sk, sv = inp.sink()
+        frames = sch.past_frames + sch.instant_frames
+        q, kq, vq = inp.query(t)
+        kk = np.concatenate([sk] + [inp.frame_kv(f)[0] for f in frames] + [kq])
+        vv = np.concatenate([sv] + [inp.frame_kv(f)[1] for f in frames] + [vq])
+        pk = np.concatenate([np.arange(A)] + [A + f * tpf + np.arange(tpf) for f in frames]
+                            + [A + (t + 1) * tpf + np.arange(len(q))])
+        ref = O.gqa_attention(q, pk[-len(q):], kk, vv, pk, cfg.rope_theta)
+        assert np.abs(o - ref).max() < 1e-12
+
+
+def test_rerotation_invariant():
+    # north_star: raw (position-agnostic) keys rotated at the reassigned ids == keys stored
+    # rotated at absolute ids (Eq. 1) and explicitly re-rotated by (new - abs).
+    cfg = synth.CONFIGS["c2"].replace(num_frames=40)
+    inp = StreamInputs(cfg, 0, 0)
+    t = 39
+    sch = step_schedule(cfg, t)
+    A, tpf = cfg.sink_tokens, cfg.tokens_per_frame
+    frames = sch.past_frames + sch.instant_frames
+    k_raw = np.concatenate([inp.frame_kv(f)[0] for f in frames])
+    abs_id = np.concatenate([A + f * tpf + np.arange(tpf) for f in frames])
+    new_id = A + np.arange(len(abs_id))
+    k_abs = O.rope(k_raw, abs_id, cfg.rope_theta)                     # standard cache
+    k_re = O.rope(k_abs, new_id - abs_id, cfg.rope_theta)             # re-rotated
+    assert np.abs(k_re - O.rope(k_raw, new_id, cfg.rope_theta)).max() < 1e-9
+
+
+def _uniform_window_attend(cfg, t, inp, n_tokens):
+    """Reference for the reductions: the sink + the last n_tokens stream tokens (a plain
+    sliding window), then the query chunk."""
+    tpf, A = cfg.tokens_per_frame, cfg.sink_tokens
+    toks_k = np.concatenate([inp.frame_kv(f)[0] for f in range(t + 1)])
+    toks_v = np.concatenate([inp.frame_kv(f)[1] for f in range(t + 1)])
+    wk, wv = toks_k[len(toks_k) - min(n_tokens, len(toks_k)):], toks_v[len(toks_v) - min(n_tokens, len(toks_v)):]
+    sk, sv = inp.sink()
+    q, kq, vq = inp.query(t)
+    kk = np.concatenate([sk, wk, kq]); vv = np.concatenate([sv, wv, vq])
+    pk = np.arange(len(kk))
+    return O.gqa_attention(q, pk[-len(q):], kk, vv, pk, cfg.rope_theta)
+
+
+def test_reduction_lI0_is_uniform_cache():
+    # PAPER.md:295 / 488: DSCache with l_I = 0 is the uniform streaming cache (window l_U).
+    cfg = synth.CONFIGS["c1"].replace(instant_frames=0, past_frames=5)
+    inp = StreamInputs(cfg, 0, 0)
+    for t in (0, 3, 9, 19):
+        sch, o_inst, o = oracle_step(cfg, 0, 0, t, inputs=inp)
+        assert sch.C_t == 0 and o_inst.shape[0] == 0
+        assert np.abs(o - _uniform_window_attend(cfg, t, inp, cfg.W)).max() < 1e-12
+
+
+def test_reduction_lU0_is_sliding_window():
+    # l_U = 0 degenerates to a sliding-window model over the buffer.
+    cfg = synth.CONFIGS["c1"].replace(instant_frames=3, past_frames=0)
+    inp = StreamInputs(cfg, 0, 0)
+    for t in (0, 2, 8, 19):
+        sch, _, o = oracle_step(cfg, 0, 0, t, inputs=inp)
+        assert sch.P_t == 0
+        assert np.abs(o - _uniform_window_attend(cfg, t, inp, cfg.C)).max() < 1e-12
+
+
+def test_instant_cache_decoupled_from_past():
+    # Eq. 7 / PAPER.md:221,226: I is built from the buffer and sink alone -> bitwise unchanged
+    # when every past frame's K/V is replaced by garbage; the final attend does change.
+    cfg = synth.CONFIGS["c1"]
+    inp = StreamInputs(cfg, 0, 0)
+    t = 15
+    sch, o_inst, o = oracle_step(cfg, 0, 0, t, inputs=inp)
+
+    class Garbage(StreamInputs):
+        def _frame_kv(self, f):
+            k, v = StreamInputs._frame_kv(self, f)
+            if f in sch.past_frames:
+                return 1e3 * RNG.standard_normal(k.shape), 1e3 * RNG.standard_normal(v.shape)
+            return k, v
+    g = Garbage(cfg, 0, 0)
+    sch2, o_inst2, o2 = oracle_step(cfg, 0, 0, t, inputs=g)
+    assert np.array_equal(o_inst, o_inst2)
+    assert np.abs(o - o2).max() > 1e-3

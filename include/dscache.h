@@ -1,0 +1,192 @@
+/*
+ * dscache.h -- C ABI of the B200 (sm_100a) DSCache streaming hot path.
+ *
+ * DSCache ("Decouple and Cache: KV Cache Construction for Streaming Video
+ * Understanding", arxiv 2605.01858; text in PAPER.md) keeps, per stream and per
+ * transformer layer, attention-sink K/V C_a, a FIFO cumulative
+ * past cache U with budget l_U (Eq. 5-6), a feature buffer of
+ * the newest l_I inputs (Eq. 3), builds an instant cache
+ * I = phi(B, C_a) on demand (Eq. 7) and answers queries over
+ * [C_a, U, I] (Eq. 8).  Keys are stored un-rotated
+ * (position-agnostic encoding, Def. 4.1) and RoPE is applied
+ * at use time with consecutive position ids from 0 over the active cache
+ * (PAPER.md:236), so ids stay bounded on unbounded streams.
+ *
+ * One handle owns the device state of S independent streams x N layers x Hkv
+ * KV heads (one GPU).  In the synthetic setting of this library the operator
+ * phi of Eq. 4 is the caller's per-layer K/V: append_frame receives a frame's
+ * raw K/V, the frame stays in the instant window for l_I steps, then becomes
+ * part of the past window (reading Q2: disjoint windows in one ring).
+ *
+ * Conventions (all calls):
+ *  - Tensor arguments are DEVICE pointers owned by the caller, dense row-major
+ *    in the layouts stated per call; element type = config.dtype (bf16 or fp32).
+ *    Base pointers must be 16-byte aligned.
+ *  - Work is stream-ordered on `stream` (a cudaStream_t passed as void*; NULL =
+ *    legacy default stream).  No call synchronises the host except create,
+ *    destroy, copy_ring, copy_sink.  Inputs may be reused once `stream` has
+ *    passed the call.
+ *  - Errors never cross the ABI as exceptions: every call returns a
+ *    dscache_status; dscache_last_error() gives a thread-local message.
+ *    Launch errors return DSCACHE_E_CUDA; asynchronous kernel faults surface at
+ *    the caller's next synchronisation.
+ *  - A handle is single-threaded (one host thread at a time).  Handles are
+ *    independent (one per GPU / rank in multi-GPU runs).
+ *  - All streams of a handle advance in lockstep (one frame per append per
+ *    layer); layers may be advanced separately (layer_begin/layer_count), e.g.
+ *    layer by layer as a real model produces them.
+ */
+#ifndef DSCACHE_H_
+#define DSCACHE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dscache_s* dscache_t;   /* opaque; owns all device memory it allocates */
+
+typedef enum {
+  DSCACHE_OK = 0,
+  DSCACHE_E_ARG = -1,           /* bad argument (null pointer, size, layer range, n_tokens)        */
+  DSCACHE_E_CONFIG = -2,        /* invalid configuration at create                                  */
+  DSCACHE_E_POS_OVERFLOW = -3,  /* A+W+C+q_max > max_position (SPEC.md:112's overflow error, raised
+                                   at create: re-based ids never exceed this bound afterwards)      */
+  DSCACHE_E_STATE = -4,         /* call out of order (attend before the sink, layers not in step)  */
+  DSCACHE_E_CUDA = -5,          /* CUDA runtime error (launch / memcpy)                             */
+  DSCACHE_E_OOM = -6            /* device allocation failed                                         */
+} dscache_status;
+
+enum { DSCACHE_DTYPE_BF16 = 0, DSCACHE_DTYPE_FP32 = 1 };
+enum { DSCACHE_ROPE_SPLIT_HALF = 0,   /* pairs (i, i+d/2): Qwen2 / LLaVA-OV-7B (reading Q7, default) */
+       DSCACHE_ROPE_ADJACENT = 1 };   /* pairs (2i, 2i+1)                                            */
+enum { DSCACHE_IMPL_AUTO = 0,         /* tcgen05 kernel when eligible, else the SIMT kernel          */
+       DSCACHE_IMPL_TC = 1,           /* force tcgen05 (E_CONFIG if the shape is not eligible)       */
+       DSCACHE_IMPL_SIMT = 2 };       /* force the fp32 CUDA-core kernel                             */
+
+typedef struct {
+  int32_t num_streams;      /* S: independent video streams held by this handle                    */
+  int32_t num_layers;       /* N: transformer layers                                               */
+  int32_t num_q_heads;      /* Hq held by this handle (after any KV-head split)                    */
+  int32_t num_kv_heads;     /* Hkv held by this handle; Hq % Hkv == 0; q head h reads kv head
+                               h / (Hq/Hkv) (HF repeat_kv, reading Q10)                            */
+  int32_t head_dim;         /* d in {64, 128}                                                      */
+  int32_t kv_head_offset;   /* first global KV head of this handle (KV-head split); bookkeeping only */
+  int32_t tokens_per_frame; /* tpf (196 for LLaVA-OV-7B)                             */
+  int32_t sink_tokens;      /* A = l_A; 0 = no sink                                 */
+  int32_t past_frames;      /* l_U: cumulative past budget in frames (W = l_U*tpf tokens)          */
+  int32_t instant_frames;   /* l_I: feature-buffer / instant window in frames (C = l_I*tpf)        */
+  int32_t max_query_tokens; /* q_max: largest n_q passed to attend                                 */
+  int32_t max_position;     /* training length; create fails with E_POS_OVERFLOW if
+                               A + W + C + q_max > max_position                                   */
+  double  rope_theta;       /* RoPE base; theta_i = base^(-2i/d)                                   */
+  int32_t rope_style;       /* DSCACHE_ROPE_*                                                      */
+  int32_t dtype;            /* DSCACHE_DTYPE_*                                                     */
+  int32_t device;           /* CUDA device ordinal the handle lives on                             */
+  int32_t attn_impl;        /* DSCACHE_IMPL_*                                                      */
+} dscache_config;
+
+typedef struct {
+  int64_t frames_seen;         /* frames appended to this layer (sink excluded)                    */
+  int64_t last_evicted_frame;  /* frame dropped from U at the latest append (Eq. 6), -1 if none    */
+  int32_t sink_filled;         /* 1 once the A sink tokens are stored                              */
+  int32_t past_tokens;         /* P_t = |U_t| in tokens                                            */
+  int32_t instant_tokens;      /* C_t = |B_t| in tokens                                            */
+  int32_t ring_slots;          /* R = W + C + tpf (one slack frame)                                */
+  int32_t tail_slot;           /* ring slot of the oldest token of U (or of B when U is empty)     */
+  int32_t instant_slot;        /* ring slot of the oldest instant token                            */
+  int32_t max_key_id;          /* largest context key id of attend: A + P_t + C_t - 1              */
+  int32_t max_query_id;        /* largest query id of attend with n_q = q_max                      */
+} dscache_state;
+
+/* Create a handle: validates the configuration, allocates the ring
+ * [S][N][Hkv][R][d] for K and V (raw, un-rotated), the sink slabs [S][N][Hkv][A][d],
+ * and the fp32 RoPE (cos, sin) table built in fp64 for ids 0 .. A+W+C+q_max-1.
+ * The ring is zero-initialised (finite).  Synchronises the device.
+ * Errors: E_ARG (null), E_CONFIG (d not in {64,128}, Hq % Hkv, budgets < 0, tpf < 1,
+ * bf16 tcgen05 forced on an ineligible shape), E_POS_OVERFLOW, E_OOM, E_CUDA. */
+dscache_status dscache_create(const dscache_config* cfg, dscache_t* out);
+
+/* Release all device memory of the handle.  Synchronises the device. */
+dscache_status dscache_destroy(dscache_t h);
+
+/* Append one frame's raw K/V (or, on the first call of a layer when A > 0, the A
+ * sink tokens) for layers [layer_begin, layer_begin+layer_count) of all S streams.
+ *   k, v : [S][layer_count][n_tokens][Hkv][d]
+ *   n_tokens: A on the first call of a layer with A > 0 (fills C_a, frozen afterwards,
+ *             PAPER.md:113), tokens_per_frame afterwards; anything else -> E_ARG.
+ * Frame f's token j goes to ring slot (f*tpf + j) mod R (contracted layout).  The
+ * append realises Eq. 3 (push into the buffer window), Eq. 5 (the frame leaving
+ * the buffer becomes past: a boundary move, no copy) and Eq. 6 (FIFO eviction of
+ * frame t - l_I - l_U: a pointer move, zero bytes).  All layers of the range must
+ * be at the same step (E_STATE otherwise). */
+dscache_status dscache_append_frame(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                                    const void* k, const void* v, int32_t n_tokens, void* stream);
+
+/* Build the instant cache outputs (Eq. 7, I = phi(B, C_a)): every instant token i
+ * (i < C_t, oldest first) attends to the sink and to instant tokens 0..i, never
+ * to U (decoupled), with ids sink j -> j, instant i -> A + i
+ * (PAPER.md:236); causal.  GQA flash attention with RoPE applied on load.
+ *   q_inst : [S][layer_count][C_t][Hq][d]   (C_t from dscache_get_state)
+ *   o_inst : [S][layer_count][C_t][Hq][d]   output, softmax(QK^T/sqrt(d)) V
+ * C_t == 0 (l_I = 0) is a no-op.  E_STATE before the sink / first frame. */
+dscache_status dscache_build_instant(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                                     const void* q_inst, void* o_inst, void* stream);
+
+/* Attention of an n_q-token query chunk over [C_a | U | I | self] (Eq. 8 plus the
+ * chunk's own K/V, which are used and then discarded: PAPER.md:212/699).  Ids:
+ * sink 0..A-1, past+instant A..A+P_t+C_t-1 (oldest first), query/self token i at
+ * A+P_t+C_t+i (Eq. 2's l_A+l_W once the window is full); causal inside the chunk.
+ *   q      : [S][layer_count][n_q][Hq][d]
+ *   k_self : [S][layer_count][n_q][Hkv][d]   raw (un-rotated) K of the chunk
+ *   v_self : [S][layer_count][n_q][Hkv][d]
+ *   o      : [S][layer_count][n_q][Hq][d]    output
+ * 1 <= n_q <= max_query_tokens, else E_ARG.  E_STATE before the first frame. */
+dscache_status dscache_attend(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                              const void* q, const void* k_self, const void* v_self, int32_t n_q,
+                              void* o, void* stream);
+
+/* Host counters of `layer` (closed form of Eq. 3/5/6 at the latest append). */
+dscache_status dscache_get_state(dscache_t h, int32_t layer, dscache_state* out);
+
+/* Test/checkpoint: synchronous copy of the ring of (stream, layer) to HOST memory,
+ * slot-exact, each [Hkv][R][d] in the config dtype. */
+dscache_status dscache_copy_ring(dscache_t h, int32_t stream_idx, int32_t layer,
+                                 void* k_host, void* v_host);
+
+/* Test/checkpoint: synchronous copy of the sink slab of (stream, layer), [Hkv][A][d]. */
+dscache_status dscache_copy_sink(dscache_t h, int32_t stream_idx, int32_t layer,
+                                 void* k_host, void* v_host);
+
+/* Debug exports (K7).  build_pos / attend_pos: NULL = off, else DEVICE int32
+ * buffers of dscache_debug_len(h) entries which the attention kernels fill, for
+ * (stream 0, first layer of the call, kv head 0), with the position ids they
+ * actually applied: [0,A) sink keys, [A,A+R) ring slot -> id (untouched if the
+ * slot is not in the window), [A+R, A+R+M) self keys, [A+R+M, A+R+2M) queries,
+ * M = max(C, q_max).  poison != 0: after each append the slots of the frame just
+ * evicted are overwritten with a large finite sentinel (finite, not NaN). */
+dscache_status dscache_set_debug(dscache_t h, int32_t* build_pos, int32_t* attend_pos, int32_t poison);
+int32_t        dscache_debug_len(dscache_t h);
+
+/* Profiling: when enabled, every attention/combine kernel launch is bracketed by
+ * CUDA events on the caller's stream; read accumulates the device time (ms) and
+ * launch counts since the last reset, per kind (0 = build_instant, 1 = attend).
+ * kernel_launches counts every kernel this handle launched (append, attention,
+ * combine).  read synchronises the events it consumes. */
+dscache_status dscache_profile(dscache_t h, int32_t enable);
+dscache_status dscache_profile_read(dscache_t h, double* ms_build, double* ms_attend,
+                                    int64_t* n_build, int64_t* n_attend, int64_t* kernel_launches,
+                                    int32_t reset);
+
+/* Which attention kernel serves build_instant (which=0) / attend (which=1) on this
+ * handle: DSCACHE_IMPL_TC or DSCACHE_IMPL_SIMT. */
+int32_t dscache_attn_impl(dscache_t h, int32_t which);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* dscache_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSCACHE_H_ */

@@ -1,0 +1,463 @@
+// Host side of the C ABI (include/dscache.h): validation, the closed-form
+// eviction / position-id bookkeeping, and kernel launches.
+//
+// Per layer r the host keeps one int64 counter (frames appended).  At step t
+// (frame t appended) with l_I = instant_frames, l_U = past_frames:
+//   instant frames  [max(0, t-l_I+1), t]          C_t = min(t+1, l_I) * tpf      (Eq. 3)
+//   past frames     [max(0, t-l_I-l_U+1), t-l_I]  P_t = min(max(t+1-l_I,0), l_U) * tpf (Eq. 5-6)
+//   evicted at t    frame t - l_I - l_U (if >= 0)                               (Eq. 6)
+//   ring slot of token j of frame f = (f*tpf + j) mod R,  R = (l_U + l_I + 1) * tpf
+// Ids are contiguous from 0 over [sink | past | instant | query].
+// No device bytes move on eviction.
+#include "../../include/dscache.h"
+#include "dscache_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+dscache_status fail(dscache_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define DSC_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(DSCACHE_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct Schedule {
+  int64_t t;          // newest frame index (frames_seen - 1)
+  int C_t, P_t;
+  int ring_start;     // slot of the oldest window token (past, or instant if no past)
+  int inst_start;     // slot of the oldest instant token
+  int64_t evicted;    // frame dropped at this step, -1 if none
+};
+
+}  // namespace
+
+struct dscache_s {
+  dscache_config cfg;
+  int W, C, R, elem, npos;
+  void* ring_k = nullptr;
+  void* ring_v = nullptr;
+  void* sink_k = nullptr;
+  void* sink_v = nullptr;
+  float2* rope = nullptr;
+  float* ws = nullptr;       // split-KV workspace (grown on demand)
+  size_t ws_bytes = 0;
+  std::vector<int64_t> frames;
+  std::vector<int> sink_filled;
+  std::vector<int64_t> last_evicted;
+  int* dbg_build = nullptr;
+  int* dbg_attend = nullptr;
+  int poison = 0;
+  int impl_build = DSCACHE_IMPL_SIMT, impl_attend = DSCACHE_IMPL_SIMT;
+  int num_sms = 148;
+  // profiling
+  int prof = 0;
+  struct Ev { cudaEvent_t a, b; int kind; };
+  std::vector<Ev> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[2] = {0, 0};
+  int64_t n[2] = {0, 0};
+  int64_t launches = 0;
+
+  Schedule schedule(int layer) const {
+    Schedule s{};
+    const int tpf = cfg.tokens_per_frame, lI = cfg.instant_frames, lU = cfg.past_frames;
+    s.t = frames[layer] - 1;
+    const int64_t t = s.t;
+    s.C_t = (int)(std::min<int64_t>(t + 1, lI) * tpf);
+    s.P_t = (int)(std::min<int64_t>(std::max<int64_t>(t + 1 - lI, 0), lU) * tpf);
+    const int64_t f0 = std::max<int64_t>(0, t - lI - lU + 1);
+    const int64_t fi = std::max<int64_t>(0, t - lI + 1);
+    s.ring_start = (int)((f0 * tpf) % R);
+    s.inst_start = (int)((fi * tpf) % R);
+    s.evicted = (t - lI - lU >= 0) ? t - lI - lU : -1;
+    return s;
+  }
+
+  cudaEvent_t take_event() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e; cudaEventCreate(&e); return e;
+  }
+};
+
+namespace {
+
+dscache_status check_layers(dscache_t h, int lb, int lc) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  if (lc < 1 || lb < 0 || lb + lc > h->cfg.num_layers)
+    return fail(DSCACHE_E_ARG, "layer range [" + std::to_string(lb) + ", +" + std::to_string(lc) +
+                                   ") outside [0, " + std::to_string(h->cfg.num_layers) + ")");
+  for (int l = lb + 1; l < lb + lc; ++l)
+    if (h->frames[l] != h->frames[lb] || h->sink_filled[l] != h->sink_filled[lb])
+      return fail(DSCACHE_E_STATE, "layers of the range are not at the same step");
+  return DSCACHE_OK;
+}
+
+bool tc_eligible(const dscache_config& c, int n_self_max) {
+  return c.dtype == DSCACHE_DTYPE_BF16 && c.head_dim == 128 && c.rope_style == DSCACHE_ROPE_SPLIT_HALF &&
+         c.tokens_per_frame >= dsc::kTileN && c.sink_tokens + n_self_max <= dsc::kTileN;
+}
+
+void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
+  const dscache_config& c = h->cfg;
+  p.S = c.num_streams; p.layer_count = lc; p.layer_begin = lb; p.N_total = c.num_layers;
+  p.P = c.num_streams * lc;
+  p.Hq = c.num_q_heads; p.Hkv = c.num_kv_heads; p.grp = c.num_q_heads / c.num_kv_heads; p.d = c.head_dim;
+  p.sink_k = h->sink_k; p.sink_v = h->sink_v; p.A = c.sink_tokens;
+  p.ring_k = h->ring_k; p.ring_v = h->ring_v; p.R = h->R;
+  p.rope = h->rope; p.rope_style = c.rope_style;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c.head_dim));
+  p.dtype = c.dtype;
+  p.dbg_M = std::max(h->C, c.max_query_tokens);
+  p.n_splits = 1; p.tiles_per_split = 1 << 30;
+}
+
+dscache_status grow_ws(dscache_t h, size_t bytes) {
+  if (bytes <= h->ws_bytes) return DSCACHE_OK;
+  if (h->ws) cudaFree(h->ws);
+  h->ws = nullptr; h->ws_bytes = 0;
+  if (cudaMalloc(&h->ws, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(DSCACHE_E_OOM, "split-KV workspace allocation failed");
+  }
+  h->ws_bytes = bytes;
+  return DSCACHE_OK;
+}
+
+dscache_status run_attention(dscache_t h, dsc::AttnParams& p, int impl, int kind, cudaStream_t st) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->prof) { e0 = h->take_event(); e1 = h->take_event(); cudaEventRecord(e0, st); }
+  cudaError_t e;
+  if (impl == DSCACHE_IMPL_TC) e = dsc::launch_attn_tc(p, st);
+  else e = dsc::launch_attn_simt(p, st);
+  h->launches++;
+  if (e == cudaSuccess && p.n_splits > 1) { e = dsc::launch_combine(p, st); h->launches++; }
+  if (h->prof) {
+    cudaEventRecord(e1, st);
+    h->pending.push_back({e0, e1, kind});
+  }
+  if (e != cudaSuccess) return fail(DSCACHE_E_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
+  return DSCACHE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dscache_last_error(void) { return g_err.c_str(); }
+
+dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
+  if (!cfg || !out) return fail(DSCACHE_E_ARG, "null config or output pointer");
+  *out = nullptr;
+  const dscache_config& c = *cfg;
+  if (c.num_streams < 1 || c.num_layers < 1 || c.num_q_heads < 1 || c.num_kv_heads < 1)
+    return fail(DSCACHE_E_CONFIG, "S, N, Hq, Hkv must be >= 1");
+  if (c.num_q_heads % c.num_kv_heads) return fail(DSCACHE_E_CONFIG, "Hq must be a multiple of Hkv");
+  if (c.head_dim != 64 && c.head_dim != 128) return fail(DSCACHE_E_CONFIG, "head_dim must be 64 or 128");
+  if (c.tokens_per_frame < 1 || c.sink_tokens < 0 || c.past_frames < 0 || c.instant_frames < 0 ||
+      c.max_query_tokens < 1 || c.max_position < 1)
+    return fail(DSCACHE_E_CONFIG, "tpf >= 1, A/l_U/l_I >= 0, q_max >= 1, max_position >= 1 required");
+  if (c.past_frames + c.instant_frames < 1)
+    return fail(DSCACHE_E_CONFIG, "l_U + l_I must be >= 1 (the newest frame must be held)");
+  if (c.dtype != DSCACHE_DTYPE_BF16 && c.dtype != DSCACHE_DTYPE_FP32) return fail(DSCACHE_E_CONFIG, "dtype");
+  if (c.rope_style != DSCACHE_ROPE_SPLIT_HALF && c.rope_style != DSCACHE_ROPE_ADJACENT)
+    return fail(DSCACHE_E_CONFIG, "rope_style");
+  if (!(c.rope_theta > 1.0)) return fail(DSCACHE_E_CONFIG, "rope_theta must be > 1");
+  const int64_t W = (int64_t)c.past_frames * c.tokens_per_frame, C = (int64_t)c.instant_frames * c.tokens_per_frame;
+  const int64_t span = c.sink_tokens + W + C + c.max_query_tokens;
+  if (span > c.max_position)
+    return fail(DSCACHE_E_POS_OVERFLOW, "A+W+C+q_max = " + std::to_string(span) + " exceeds max_position " +
+                                            std::to_string(c.max_position));
+  if (c.attn_impl == DSCACHE_IMPL_TC && !tc_eligible(c, c.max_query_tokens))
+    return fail(DSCACHE_E_CONFIG, "tcgen05 kernel needs bf16, d=128, split-half RoPE, tpf>=128, A+q_max<=128");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || c.device < 0 || c.device >= ndev) {
+    cudaGetLastError();
+    return fail(DSCACHE_E_CUDA, "no CUDA device " + std::to_string(c.device));
+  }
+  DeviceGuard dg(c.device);
+
+  dscache_s* h = new dscache_s();
+  h->cfg = c;
+  h->W = (int)W; h->C = (int)C;
+  h->R = (int)(W + C + c.tokens_per_frame);
+  h->elem = c.dtype == DSCACHE_DTYPE_BF16 ? 2 : 4;
+  h->npos = (int)span;
+  h->frames.assign(c.num_layers, 0);
+  h->sink_filled.assign(c.num_layers, c.sink_tokens == 0 ? 1 : 0);
+  h->last_evicted.assign(c.num_layers, -1);
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, c.device);
+  if (c.attn_impl == DSCACHE_IMPL_SIMT) {
+    h->impl_build = h->impl_attend = DSCACHE_IMPL_SIMT;
+  } else {
+    h->impl_build = tc_eligible(c, 0) ? DSCACHE_IMPL_TC : DSCACHE_IMPL_SIMT;
+    h->impl_attend = tc_eligible(c, c.max_query_tokens) ? DSCACHE_IMPL_TC : DSCACHE_IMPL_SIMT;
+  }
+
+  const size_t heads = (size_t)c.num_streams * c.num_layers * c.num_kv_heads;
+  const size_t ring_bytes = heads * h->R * c.head_dim * h->elem;
+  const size_t sink_bytes = heads * std::max(c.sink_tokens, 1) * c.head_dim * h->elem;
+  const size_t rope_bytes = (size_t)h->npos * (c.head_dim / 2) * sizeof(float2);
+  auto oom = [&](const char* what) {
+    cudaGetLastError();
+    dscache_destroy(h);
+    return fail(DSCACHE_E_OOM, std::string("cudaMalloc failed for ") + what);
+  };
+  if (cudaMalloc(&h->ring_k, ring_bytes) != cudaSuccess) return oom("ring K");
+  if (cudaMalloc(&h->ring_v, ring_bytes) != cudaSuccess) return oom("ring V");
+  if (cudaMalloc(&h->sink_k, sink_bytes) != cudaSuccess) return oom("sink K");
+  if (cudaMalloc(&h->sink_v, sink_bytes) != cudaSuccess) return oom("sink V");
+  if (cudaMalloc(&h->rope, rope_bytes) != cudaSuccess) return oom("rope table");
+  cudaError_t e = cudaMemset(h->ring_k, 0, ring_bytes);
+  if (e == cudaSuccess) e = cudaMemset(h->ring_v, 0, ring_bytes);
+  if (e == cudaSuccess) e = cudaMemset(h->sink_k, 0, sink_bytes);
+  if (e == cudaSuccess) e = cudaMemset(h->sink_v, 0, sink_bytes);
+  if (e == cudaSuccess) e = dsc::launch_rope_table(h->rope, h->npos, c.head_dim, c.rope_theta, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    std::string m = cudaGetErrorString(e);
+    dscache_destroy(h);
+    return fail(DSCACHE_E_CUDA, "create: " + m);
+  }
+  *out = h;
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_destroy(dscache_t h) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  DeviceGuard dg(h->cfg.device);
+  cudaDeviceSynchronize();
+  for (auto& ev : h->pending) { cudaEventDestroy(ev.a); cudaEventDestroy(ev.b); }
+  for (auto e : h->pool) cudaEventDestroy(e);
+  cudaFree(h->ring_k); cudaFree(h->ring_v); cudaFree(h->sink_k); cudaFree(h->sink_v);
+  cudaFree(h->rope); cudaFree(h->ws);
+  delete h;
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_append_frame(dscache_t h, int32_t lb, int32_t lc, const void* k, const void* v,
+                                    int32_t n_tokens, void* stream) {
+  dscache_status s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  if (!k || !v) return fail(DSCACHE_E_ARG, "null k/v");
+  const dscache_config& c = h->cfg;
+  DeviceGuard dg(c.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  dsc::AppendParams p{};
+  p.k = k; p.v = v;
+  p.S = c.num_streams; p.layer_count = lc; p.layer_begin = lb; p.N_total = c.num_layers; p.Hkv = c.num_kv_heads;
+  p.row_bytes = c.head_dim * h->elem; p.elem_bytes = h->elem; p.n = n_tokens; p.poison_slot0 = -1;
+  if (!h->sink_filled[lb]) {
+    if (n_tokens != c.sink_tokens)
+      return fail(DSCACHE_E_ARG, "first append of a layer must carry the " + std::to_string(c.sink_tokens) +
+                                     " sink tokens, got " + std::to_string(n_tokens));
+    p.dst_k = h->sink_k; p.dst_v = h->sink_v; p.rows_dst = c.sink_tokens; p.slot0 = 0;
+    DSC_CUDA(dsc::launch_append(p, st));
+    h->launches++;
+    for (int l = lb; l < lb + lc; ++l) h->sink_filled[l] = 1;
+    return DSCACHE_OK;
+  }
+  if (n_tokens != c.tokens_per_frame)
+    return fail(DSCACHE_E_ARG, "frame append must carry tokens_per_frame = " + std::to_string(c.tokens_per_frame) +
+                                   " tokens, got " + std::to_string(n_tokens));
+  const int64_t f = h->frames[lb];
+  p.dst_k = h->ring_k; p.dst_v = h->ring_v; p.rows_dst = h->R;
+  p.slot0 = (int)((f * c.tokens_per_frame) % h->R);
+  const int64_t ev = f - c.instant_frames - c.past_frames;
+  if (h->poison && ev >= 0) p.poison_slot0 = (int)((ev * c.tokens_per_frame) % h->R);
+  DSC_CUDA(dsc::launch_append(p, st));
+  h->launches++;
+  for (int l = lb; l < lb + lc; ++l) { h->frames[l] = f + 1; h->last_evicted[l] = ev >= 0 ? ev : -1; }
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_build_instant(dscache_t h, int32_t lb, int32_t lc, const void* q_inst, void* o_inst,
+                                     void* stream) {
+  dscache_status s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  if (!h->sink_filled[lb] || h->frames[lb] < 1)
+    return fail(DSCACHE_E_STATE, "build_instant before the sink and the first frame were appended");
+  const Schedule sc = h->schedule(lb);
+  if (sc.C_t == 0) return DSCACHE_OK;   // l_I = 0: the instant cache is empty (uniform reduction)
+  if (!q_inst || !o_inst) return fail(DSCACHE_E_ARG, "null q_inst/o_inst");
+  DeviceGuard dg(h->cfg.device);
+  dsc::AttnParams p{};
+  fill_common(h, p, lb, lc);
+  p.q = q_inst; p.o = o_inst; p.n_q = sc.C_t; p.q_pos0 = h->cfg.sink_tokens;
+  p.ring_start = sc.inst_start; p.ring_count = sc.C_t;
+  p.self_k = p.self_v = nullptr; p.n_self = 0;
+  p.dbg_pos = h->dbg_build;
+  p.n_mblocks = (p.n_q * p.grp + 2 * dsc::kTileM - 1) / (2 * dsc::kTileM);
+  return run_attention(h, p, h->impl_build, 0, (cudaStream_t)stream);
+}
+
+dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                              const void* v_self, int32_t n_q, void* o, void* stream) {
+  dscache_status s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  if (!h->sink_filled[lb] || h->frames[lb] < 1)
+    return fail(DSCACHE_E_STATE, "attend before the sink and the first frame were appended");
+  if (n_q < 1 || n_q > h->cfg.max_query_tokens)
+    return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
+  if (!q || !k_self || !v_self || !o) return fail(DSCACHE_E_ARG, "null q/k_self/v_self/o");
+  DeviceGuard dg(h->cfg.device);
+  const Schedule sc = h->schedule(lb);
+  dsc::AttnParams p{};
+  fill_common(h, p, lb, lc);
+  p.q = q; p.o = o; p.n_q = n_q;
+  p.ring_start = sc.ring_start; p.ring_count = sc.P_t + sc.C_t;
+  p.q_pos0 = h->cfg.sink_tokens + p.ring_count;
+  p.self_k = k_self; p.self_v = v_self; p.n_self = n_q;
+  p.dbg_pos = h->dbg_attend;
+  p.n_mblocks = (p.n_q * p.grp + 2 * dsc::kTileM - 1) / (2 * dsc::kTileM);
+  const int impl = h->impl_attend;
+  if (impl == DSCACHE_IMPL_TC) {
+    // split the key range when (problem, kv head, m-block) work items cannot fill the SMs
+    const int R = h->R, BN = dsc::kTileN;
+    const int nT = (R + BN - 1) / BN;
+    int ring_tiles = 0;
+    if (p.ring_count > 0) {
+      const int k0 = p.ring_start / BN;
+      const int end = p.ring_start + p.ring_count;
+      ring_tiles = end <= R ? (end + BN - 1) / BN - k0 : (nT - k0) + (end - R + BN - 1) / BN;
+      ring_tiles = std::min(ring_tiles, nT);
+    }
+    const int tiles = 1 + ring_tiles;
+    const int items = p.P * p.Hkv * p.n_mblocks;
+    int splits = 1;
+    if (items < h->num_sms) {
+      splits = std::min((h->num_sms + items - 1) / items, std::max(1, tiles / 4));
+    }
+    if (splits > 1) {
+      p.tiles_per_split = (tiles + splits - 1) / splits;
+      splits = (tiles + p.tiles_per_split - 1) / p.tiles_per_split;
+    }
+    p.n_splits = splits;
+    if (splits > 1) {
+      const size_t rows = (size_t)p.P * n_q * p.Hq;
+      dscache_status gs = grow_ws(h, (size_t)splits * rows * (p.d + 1) * sizeof(float));
+      if (gs != DSCACHE_OK) return gs;
+      p.ws_o = h->ws;
+      p.ws_lse = h->ws + (size_t)splits * rows * p.d;
+    }
+  }
+  return run_attention(h, p, impl, 1, (cudaStream_t)stream);
+}
+
+dscache_status dscache_get_state(dscache_t h, int32_t layer, dscache_state* out) {
+  if (!h || !out) return fail(DSCACHE_E_ARG, "null handle/output");
+  if (layer < 0 || layer >= h->cfg.num_layers) return fail(DSCACHE_E_ARG, "layer out of range");
+  dscache_state st{};
+  st.frames_seen = h->frames[layer];
+  st.sink_filled = h->sink_filled[layer];
+  st.ring_slots = h->R;
+  st.last_evicted_frame = h->last_evicted[layer];
+  if (h->frames[layer] > 0) {
+    Schedule sc = h->schedule(layer);
+    st.past_tokens = sc.P_t; st.instant_tokens = sc.C_t;
+    st.tail_slot = sc.ring_start; st.instant_slot = sc.inst_start;
+  }
+  st.max_key_id = h->cfg.sink_tokens + st.past_tokens + st.instant_tokens - 1;
+  st.max_query_id = st.max_key_id + h->cfg.max_query_tokens;
+  *out = st;
+  return DSCACHE_OK;
+}
+
+static dscache_status copy_rows(dscache_t h, int s_idx, int layer, const void* dk, const void* dv, int rows,
+                                void* kh, void* vh) {
+  if (!h || !kh || !vh) return fail(DSCACHE_E_ARG, "null argument");
+  const dscache_config& c = h->cfg;
+  if (s_idx < 0 || s_idx >= c.num_streams || layer < 0 || layer >= c.num_layers)
+    return fail(DSCACHE_E_ARG, "stream/layer out of range");
+  DeviceGuard dg(c.device);
+  const size_t per = (size_t)c.num_kv_heads * rows * c.head_dim * h->elem;
+  const size_t off = ((size_t)s_idx * c.num_layers + layer) * per;
+  DSC_CUDA(cudaDeviceSynchronize());
+  DSC_CUDA(cudaMemcpy(kh, (const char*)dk + off, per, cudaMemcpyDeviceToHost));
+  DSC_CUDA(cudaMemcpy(vh, (const char*)dv + off, per, cudaMemcpyDeviceToHost));
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_copy_ring(dscache_t h, int32_t s_idx, int32_t layer, void* kh, void* vh) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  return copy_rows(h, s_idx, layer, h->ring_k, h->ring_v, h->R, kh, vh);
+}
+
+dscache_status dscache_copy_sink(dscache_t h, int32_t s_idx, int32_t layer, void* kh, void* vh) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  if (h->cfg.sink_tokens == 0) return DSCACHE_OK;
+  return copy_rows(h, s_idx, layer, h->sink_k, h->sink_v, h->cfg.sink_tokens, kh, vh);
+}
+
+int32_t dscache_debug_len(dscache_t h) {
+  if (!h) return 0;
+  return h->cfg.sink_tokens + h->R + 2 * std::max(h->C, h->cfg.max_query_tokens);
+}
+
+dscache_status dscache_set_debug(dscache_t h, int32_t* build_pos, int32_t* attend_pos, int32_t poison) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  h->dbg_build = build_pos; h->dbg_attend = attend_pos; h->poison = poison;
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_profile(dscache_t h, int32_t enable) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  h->prof = enable;
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_profile_read(dscache_t h, double* ms_build, double* ms_attend, int64_t* n_build,
+                                    int64_t* n_attend, int64_t* kernel_launches, int32_t reset) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  DeviceGuard dg(h->cfg.device);
+  for (auto& ev : h->pending) {
+    DSC_CUDA(cudaEventSynchronize(ev.b));
+    float ms = 0.f;
+    DSC_CUDA(cudaEventElapsedTime(&ms, ev.a, ev.b));
+    h->ms[ev.kind] += ms;
+    h->n[ev.kind] += 1;
+    h->pool.push_back(ev.a); h->pool.push_back(ev.b);
+  }
+  h->pending.clear();
+  if (ms_build) *ms_build = h->ms[0];
+  if (ms_attend) *ms_attend = h->ms[1];
+  if (n_build) *n_build = h->n[0];
+  if (n_attend) *n_attend = h->n[1];
+  if (kernel_launches) *kernel_launches = h->launches;
+  if (reset) { h->ms[0] = h->ms[1] = 0; h->n[0] = h->n[1] = 0; h->launches = 0; }
+  return DSCACHE_OK;
+}
+
+int32_t dscache_attn_impl(dscache_t h, int32_t which) {
+  if (!h) return -1;
+  return which == 0 ? h->impl_build : h->impl_attend;
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+// Internal launch parameters shared by the host bookkeeping (dscache_api.cu) and
+// the sm_100a kernels.  Product code only; nothing here is visible through the ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dsc {
+
+constexpr int kTileN = 128;   // keys per attention tile (tcgen05 N of QK^T, K of PV)
+constexpr int kTileM = 128;   // query rows per Q tile (tcgen05 M)
+
+// One attention launch (build_instant or attend) over P = S * layer_count problems.
+// Keys of problem p, kv head g, in logical order L = 0, 1, ...:
+//   [0, A)                  sink rows           (position L)
+//   [A, A + ring_count)     ring slots (ring_start + L - A) mod R   (position L)
+//   [A+ring_count, +n_self) self rows            (position L)
+// Query row i (i < n_q) of q head h sits at position q_pos0 + i and sees key L iff
+// L <= q_pos0 + i.  Ids are contiguous from 0.
+struct AttnParams {
+  // problems
+  int P, S, layer_count, layer_begin, N_total;
+  int Hq, Hkv, grp, d;
+  // queries / outputs: [P][n_q][Hq][d]
+  const void* q;
+  void* o;
+  int n_q;
+  int q_pos0;
+  // keys
+  const void* sink_k; const void* sink_v;   // [S][N][Hkv][A][d]
+  int A;
+  const void* ring_k; const void* ring_v;   // [S][N][Hkv][R][d]
+  int R;
+  int ring_start, ring_count;
+  const void* self_k; const void* self_v;   // [P][n_self][Hkv][d]
+  int n_self;
+  // rope
+  const float2* rope;                        // [npos][d/2] (cos, sin)
+  int rope_style;
+  float scale_log2;                          // log2(e) / sqrt(d)
+  // split-KV (attend): partial (O/l, log2-sum-exp) per split
+  int n_splits, tiles_per_split;
+  float* ws_o;                               // [n_splits][P][n_q][Hq][d]
+  float* ws_lse;                             // [n_splits][P][n_q][Hq]
+  // tcgen05 kernel work decomposition
+  int n_mblocks;                             // ceil(n_q * grp / (2 * kTileM))
+  // debug export (K7); null = off
+  int* dbg_pos; int dbg_M;
+  int dtype;                                 // 0 bf16, 1 fp32
+};
+
+struct AppendParams {
+  const void* k; const void* v;              // [S][lc][n][Hkv][d]
+  void* dst_k; void* dst_v;                  // ring [S][N][Hkv][R][d] or sink [S][N][Hkv][A][d]
+  int S, layer_count, layer_begin, N_total, Hkv, n, rows_dst;  // rows_dst = R or A
+  int slot0;                                 // destination row of token 0
+  int row_bytes;                             // d * elem
+  // eviction poison (debug): slots [poison_slot0, +n) of every head, -1 = off
+  int poison_slot0;
+  int elem_bytes;
+};
+
+// kernels (launchers return cudaGetLastError())
+cudaError_t launch_rope_table(float2* table, int npos, int d, double theta, cudaStream_t st);
+cudaError_t launch_append(const AppendParams& p, cudaStream_t st);
+cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t st);
+cudaError_t launch_attn_tc(const AttnParams& p, cudaStream_t st);
+cudaError_t launch_combine(const AttnParams& p, cudaStream_t st);
+int attn_tc_smem_bytes();
+
+}  // namespace dsc

@@ -1,0 +1,277 @@
+// sm_100a kernels of the DSCache hot path other than the tcgen05 attention:
+//   K1 append/evict  -- 16-byte vector copy of a frame's raw K/V into ring slots
+//                       (f*tpf + j) mod R; eviction is a host pointer move, the
+//                       optional debug poison overwrites the evicted frame's slots
+//   K2 rope table    -- (cos, sin)(p * theta_i) in fp64, rounded to fp32, indexed by id
+//   K6 SIMT attention-- fp32 FFMA flash attention (online softmax, warp shuffles) with
+//                       RoPE on load; serves the fp32 configs and ineligible shapes
+//   K5 combine       -- merges split-KV partials (O_s / l_s, log2-sum-exp) into O
+#include "dscache_internal.h"
+
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <algorithm>
+
+namespace dsc {
+
+// ------------------------------------------------------------------ K2 RoPE table
+// theta_i = base^(-2i/d) (reading Q7); the angle p*theta_i is formed in
+// fp64 so the table is exact to fp32 rounding at every id (< 3e-8 abs).
+__global__ void rope_table_kernel(float2* __restrict__ t, int npos, int d, double theta) {
+  const int half = d / 2;
+  const long long total = (long long)npos * half;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int f = (int)(idx % half);
+    const long long pos = idx / half;
+    const double inv = pow(theta, -2.0 * (double)f / (double)d);
+    double s, c;
+    sincos((double)pos * inv, &s, &c);
+    t[idx] = make_float2((float)c, (float)s);
+  }
+}
+
+cudaError_t launch_rope_table(float2* table, int npos, int d, double theta, cudaStream_t st) {
+  const long long total = (long long)npos * (d / 2);
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+  rope_table_kernel<<<blocks, 256, 0, st>>>(table, npos, d, theta);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K1 append / evict
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+// blockIdx.y: 0 = K, 1 = V.  Each thread moves 4 independent 16-byte chunks per
+// iteration (4 loads in flight before the stores).  Source [S][lc][n][Hkv][d] is
+// read fully coalesced; destination rows are 256-byte contiguous per (head, slot).
+__global__ void __launch_bounds__(256) append_kernel(AppendParams p) {
+  const int cpr = p.row_bytes >> 4;
+  const long long total = (long long)p.S * p.layer_count * p.n * p.Hkv * cpr;
+  const uint4* __restrict__ src = reinterpret_cast<const uint4*>(blockIdx.y ? p.v : p.k);
+  uint4* __restrict__ dst = reinterpret_cast<uint4*>(blockIdx.y ? p.dst_v : p.dst_k);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  auto dst_index = [&](long long idx) -> long long {
+    const int c = (int)(idx % cpr);
+    long long r = idx / cpr;
+    const int g = (int)(r % p.Hkv); r /= p.Hkv;
+    const int j = (int)(r % p.n); r /= p.n;
+    const int l = (int)(r % p.layer_count);
+    const long long s = r / p.layer_count;
+    const long long row = ((s * p.N_total + p.layer_begin + l) * p.Hkv + g) * p.rows_dst + p.slot0 + j;
+    return row * cpr + c;
+  };
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; idx + 3 * stride < total; idx += 4 * stride) {
+    uint4 a = ld_stream(src + idx), b = ld_stream(src + idx + stride);
+    uint4 c = ld_stream(src + idx + 2 * stride), d = ld_stream(src + idx + 3 * stride);
+    dst[dst_index(idx)] = a;
+    dst[dst_index(idx + stride)] = b;
+    dst[dst_index(idx + 2 * stride)] = c;
+    dst[dst_index(idx + 3 * stride)] = d;
+  }
+  for (; idx < total; idx += stride) dst[dst_index(idx)] = ld_stream(src + idx);
+
+  if (p.poison_slot0 >= 0) {
+    // sentinel = 1e30 (finite): bf16 0x714A, fp32 0x7149F2CA
+    const uint32_t w = p.elem_bytes == 2 ? 0x714A714Au : 0x7149F2CAu;
+    const uint4 pv = make_uint4(w, w, w, w);
+    for (long long i2 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i2 < total; i2 += stride) {
+      const int c = (int)(i2 % cpr);
+      long long r = i2 / cpr;
+      const int g = (int)(r % p.Hkv); r /= p.Hkv;
+      const int j = (int)(r % p.n); r /= p.n;
+      const int l = (int)(r % p.layer_count);
+      const long long s = r / p.layer_count;
+      const long long row = ((s * p.N_total + p.layer_begin + l) * p.Hkv + g) * p.rows_dst + p.poison_slot0 + j;
+      dst[row * cpr + c] = pv;
+    }
+  }
+}
+
+cudaError_t launch_append(const AppendParams& p, cudaStream_t st) {
+  const long long total = (long long)p.S * p.layer_count * p.n * p.Hkv * (p.row_bytes >> 4);
+  int blocks = (int)std::min<long long>((total + 1023) / 1024, 148 * 8);
+  if (blocks < 1) blocks = 1;
+  append_kernel<<<dim3(blocks, 2), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K6 SIMT attention
+template <typename T> __device__ __forceinline__ float to_f(T x);
+template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+
+// Lane `lane` holds E = D/32 elements.  Split-half: element e_k = lane + 32k, pairs
+// (k, k+E/2) with frequency lane + 32k.  Adjacent: element 2(lane+32m)+b for k = 2m+b,
+// pairs (2m, 2m+1) with frequency lane + 32m.  Either way both members of a pair are
+// in the same lane, so the rotation needs no shuffles.
+template <int D>
+__device__ __forceinline__ int elem_of(int lane, int k, int style) {
+  return style == 0 ? lane + 32 * k : 2 * (lane + 32 * (k >> 1)) + (k & 1);
+}
+
+template <int D>
+__device__ __forceinline__ void rotate(float (&x)[D / 32], const float2* __restrict__ rope, int pos, int lane,
+                                       int style) {
+  constexpr int E = D / 32;
+  const float2* row = rope + (long long)pos * (D / 2);
+  if (style == 0) {
+#pragma unroll
+    for (int k = 0; k < E / 2; ++k) {
+      const float2 cs = row[lane + 32 * k];
+      const float a = x[k], b = x[k + E / 2];
+      x[k] = a * cs.x - b * cs.y;
+      x[k + E / 2] = a * cs.y + b * cs.x;
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+      const float2 cs = row[lane + 32 * m];
+      const float a = x[2 * m], b = x[2 * m + 1];
+      x[2 * m] = a * cs.x - b * cs.y;
+      x[2 * m + 1] = a * cs.y + b * cs.x;
+    }
+  }
+}
+
+// One warp per (problem, query row i, q head h).  Keys in logical order L, id L;
+// visible iff L <= q_pos0 + i (AttnParams).  Online softmax in fp32 with expf.
+template <typename T, int D>
+__global__ void __launch_bounds__(128) attn_simt_kernel(AttnParams p) {
+  constexpr int E = D / 32;
+  const int lane = threadIdx.x & 31;
+  const long long wg = blockIdx.x * 4ll + (threadIdx.x >> 5);
+  const long long total = (long long)p.P * p.n_q * p.Hq;
+  if (wg >= total) return;
+  const int h = (int)(wg % p.Hq);
+  const int i = (int)((wg / p.Hq) % p.n_q);
+  const int pp = (int)(wg / ((long long)p.Hq * p.n_q));
+  const int s = pp / p.layer_count, l = pp % p.layer_count;
+  const int g = h / p.grp;
+  const long long head_row = ((long long)s * p.N_total + p.layer_begin + l) * p.Hkv + g;
+  const T* __restrict__ Q = reinterpret_cast<const T*>(p.q);
+  const T* __restrict__ SK = reinterpret_cast<const T*>(p.sink_k);
+  const T* __restrict__ SV = reinterpret_cast<const T*>(p.sink_v);
+  const T* __restrict__ RK = reinterpret_cast<const T*>(p.ring_k);
+  const T* __restrict__ RV = reinterpret_cast<const T*>(p.ring_v);
+  const T* __restrict__ XK = reinterpret_cast<const T*>(p.self_k);
+  const T* __restrict__ XV = reinterpret_cast<const T*>(p.self_v);
+
+  const int qpos = p.q_pos0 + i;
+  float q[E];
+  const T* qrow = Q + (((long long)pp * p.n_q + i) * p.Hq + h) * D;
+#pragma unroll
+  for (int k = 0; k < E; ++k) q[k] = to_f(qrow[elem_of<D>(lane, k, p.rope_style)]);
+  rotate<D>(q, p.rope, qpos, lane, p.rope_style);
+  const float scale = rsqrtf((float)D);
+
+  const bool dbg = p.dbg_pos && pp == 0 && g == 0 && h == 0;
+  if (dbg && lane == 0) p.dbg_pos[p.A + p.R + p.dbg_M + i] = qpos;
+  const bool dbg_keys = dbg && i == p.n_q - 1;
+
+  const int n_keys = p.A + p.ring_count + p.n_self;
+  const int last = min(qpos, n_keys - 1);
+  float m = -INFINITY, lsum = 0.f, acc[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = 0.f;
+  for (int L = 0; L <= last; ++L) {
+    const T *kr, *vr;
+    if (L < p.A) {
+      kr = SK + (head_row * p.A + L) * D; vr = SV + (head_row * p.A + L) * D;
+      if (dbg_keys && lane == 0) p.dbg_pos[L] = L;
+    } else if (L < p.A + p.ring_count) {
+      int slot = p.ring_start + (L - p.A);
+      if (slot >= p.R) slot -= p.R;
+      kr = RK + (head_row * p.R + slot) * D; vr = RV + (head_row * p.R + slot) * D;
+      if (dbg_keys && lane == 0) p.dbg_pos[p.A + slot] = L;
+    } else {
+      const int j = L - p.A - p.ring_count;
+      kr = XK + (((long long)pp * p.n_self + j) * p.Hkv + g) * D;
+      vr = XV + (((long long)pp * p.n_self + j) * p.Hkv + g) * D;
+      if (dbg_keys && lane == 0) p.dbg_pos[p.A + p.R + j] = L;
+    }
+    float kx[E], vx[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int e = elem_of<D>(lane, k, p.rope_style);
+      kx[k] = to_f(kr[e]);
+      vx[k] = to_f(vr[e]);
+    }
+    rotate<D>(kx, p.rope, L, lane, p.rope_style);
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < E; ++k) dot = fmaf(q[k], kx[k], dot);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    const float sc = dot * scale;
+    const float mn = fmaxf(m, sc);
+    const float corr = expf(m - mn);
+    const float pw = expf(sc - mn);
+    lsum = lsum * corr + pw;
+#pragma unroll
+    for (int k = 0; k < E; ++k) acc[k] = fmaf(acc[k], corr, pw * vx[k]);
+    m = mn;
+  }
+  const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+  T* orow = reinterpret_cast<T*>(p.o) + (((long long)pp * p.n_q + i) * p.Hq + h) * D;
+#pragma unroll
+  for (int k = 0; k < E; ++k) orow[elem_of<D>(lane, k, p.rope_style)] = from_f<T>(acc[k] * inv);
+}
+
+cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t st) {
+  const long long warps = (long long)p.P * p.n_q * p.Hq;
+  const int blocks = (int)((warps + 3) / 4);
+  if (p.dtype == 1) {
+    if (p.d == 64) attn_simt_kernel<float, 64><<<blocks, 128, 0, st>>>(p);
+    else attn_simt_kernel<float, 128><<<blocks, 128, 0, st>>>(p);
+  } else {
+    if (p.d == 64) attn_simt_kernel<__nv_bfloat16, 64><<<blocks, 128, 0, st>>>(p);
+    else attn_simt_kernel<__nv_bfloat16, 128><<<blocks, 128, 0, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K5 split-KV combine
+// O = sum_s 2^(lse_s - M) O_s / sum_s 2^(lse_s - M), M = max_s lse_s (log2 domain).
+// One warp per output row; lanes own 4 consecutive features (d = 128).
+__global__ void __launch_bounds__(128) combine_kernel(AttnParams p) {
+  const int lane = threadIdx.x & 31;
+  const long long row = blockIdx.x * 4ll + (threadIdx.x >> 5);
+  const long long rows = (long long)p.P * p.n_q * p.Hq;
+  if (row >= rows) return;
+  float M = -INFINITY;
+  for (int s = 0; s < p.n_splits; ++s) M = fmaxf(M, p.ws_lse[s * rows + row]);
+  float den = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < p.n_splits; ++s) {
+    const float lse = p.ws_lse[s * rows + row];
+    const float w = (lse == -INFINITY) ? 0.f : exp2f(lse - M);
+    den += w;
+    const float4 o = reinterpret_cast<const float4*>(p.ws_o + (s * rows + row) * p.d)[lane];
+    acc.x = fmaf(w, o.x, acc.x); acc.y = fmaf(w, o.y, acc.y);
+    acc.z = fmaf(w, o.z, acc.z); acc.w = fmaf(w, o.w, acc.w);
+  }
+  const float inv = den > 0.f ? 1.f / den : 0.f;
+  __nv_bfloat162 a = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+  __nv_bfloat162 b = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+  uint2 out;
+  out.x = *reinterpret_cast<uint32_t*>(&a);
+  out.y = *reinterpret_cast<uint32_t*>(&b);
+  reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.o) + row * p.d)[lane] = out;
+}
+
+cudaError_t launch_combine(const AttnParams& p, cudaStream_t st) {
+  const long long rows = (long long)p.P * p.n_q * p.Hq;
+  combine_kernel<<<(int)((rows + 3) / 4), 128, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace dsc

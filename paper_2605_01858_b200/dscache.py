@@ -1,0 +1,268 @@
+"""Thin ctypes binding of libdscache.so (include/dscache.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+sm_100a kernels.  There is no CPU or PyTorch fallback -- if the library is
+missing, :func:`load_library` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdscache.so")
+
+OK, E_ARG, E_CONFIG, E_POS_OVERFLOW, E_STATE, E_CUDA, E_OOM = 0, -1, -2, -3, -4, -5, -6
+STATUS_NAMES = {0: "OK", -1: "E_ARG", -2: "E_CONFIG", -3: "E_POS_OVERFLOW", -4: "E_STATE", -5: "E_CUDA",
+                -6: "E_OOM"}
+DTYPE_BF16, DTYPE_FP32 = 0, 1
+ROPE_SPLIT_HALF, ROPE_ADJACENT = 0, 1
+IMPL_AUTO, IMPL_TC, IMPL_SIMT = 0, 1, 2
+
+
+class DSCacheError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("num_streams", ctypes.c_int32), ("num_layers", ctypes.c_int32),
+                ("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("kv_head_offset", ctypes.c_int32),
+                ("tokens_per_frame", ctypes.c_int32), ("sink_tokens", ctypes.c_int32),
+                ("past_frames", ctypes.c_int32), ("instant_frames", ctypes.c_int32),
+                ("max_query_tokens", ctypes.c_int32), ("max_position", ctypes.c_int32),
+                ("rope_theta", ctypes.c_double), ("rope_style", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("device", ctypes.c_int32), ("attn_impl", ctypes.c_int32)]
+
+
+class State(ctypes.Structure):
+    _fields_ = [("frames_seen", ctypes.c_int64), ("last_evicted_frame", ctypes.c_int64),
+                ("sink_filled", ctypes.c_int32), ("past_tokens", ctypes.c_int32),
+                ("instant_tokens", ctypes.c_int32), ("ring_slots", ctypes.c_int32),
+                ("tail_slot", ctypes.c_int32), ("instant_slot", ctypes.c_int32),
+                ("max_key_id", ctypes.c_int32), ("max_query_id", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
+           "dscache_attend", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
+           "dscache_set_debug", "dscache_debug_len", "dscache_profile", "dscache_profile_read",
+           "dscache_attn_impl", "dscache_last_error"]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libdscache.so (once).  Raises if it is missing: no fallback exists."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing; build it with `python -m paper_2605_01858_b200._build` "
+                           "(or __graft_entry__.build()).  There is no CPU fallback.")
+    lib = ctypes.CDLL(path)
+    P, I32, I64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    sig = {
+        "dscache_create": ([ctypes.POINTER(Config), ctypes.POINTER(P)], I32),
+        "dscache_destroy": ([P], I32),
+        "dscache_append_frame": ([P, I32, I32, P, P, I32, P], I32),
+        "dscache_build_instant": ([P, I32, I32, P, P, P], I32),
+        "dscache_attend": ([P, I32, I32, P, P, P, I32, P, P], I32),
+        "dscache_get_state": ([P, I32, ctypes.POINTER(State)], I32),
+        "dscache_copy_ring": ([P, I32, I32, P, P], I32),
+        "dscache_copy_sink": ([P, I32, I32, P, P], I32),
+        "dscache_set_debug": ([P, P, P, I32], I32),
+        "dscache_debug_len": ([P], I32),
+        "dscache_profile": ([P, I32], I32),
+        "dscache_profile_read": ([P, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(I64),
+                                  ctypes.POINTER(I64), ctypes.POINTER(I64), I32], I32),
+        "dscache_attn_impl": ([P, I32], I32),
+        "dscache_last_error": ([], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != OK:
+        raise DSCacheError(status, _lib.dscache_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class DSCache:
+    """One handle = S streams x N layers x Hkv KV heads of DSCache state on one GPU."""
+
+    def __init__(self, *, num_streams: int, num_layers: int, num_q_heads: int, num_kv_heads: int,
+                 head_dim: int, tokens_per_frame: int, sink_tokens: int, past_frames: int,
+                 instant_frames: int, max_query_tokens: int, rope_theta: float,
+                 max_position: int = 32768, dtype: str = "bf16", rope_style: int = ROPE_SPLIT_HALF,
+                 device: int = 0, kv_head_offset: int = 0, attn_impl: int = IMPL_AUTO):
+        lib = load_library()
+        self.torch_dtype = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.cfg = Config(num_streams, num_layers, num_q_heads, num_kv_heads, head_dim, kv_head_offset,
+                          tokens_per_frame, sink_tokens, past_frames, instant_frames, max_query_tokens,
+                          max_position, float(rope_theta), rope_style,
+                          DTYPE_BF16 if dtype == "bf16" else DTYPE_FP32, device, attn_impl)
+        self.device = torch.device("cuda", device)
+        h = ctypes.c_void_p()
+        _check(lib.dscache_create(ctypes.byref(self.cfg), ctypes.byref(h)))
+        self._h = h
+        self.R = (past_frames + instant_frames + 1) * tokens_per_frame
+
+    @classmethod
+    def from_config(cls, cfg, device: int = 0, **kw):
+        """From a dscache_synth.StreamConfig-like object (attribute names as in the ABI)."""
+        args = dict(num_streams=cfg.num_streams, num_layers=cfg.num_layers, num_q_heads=cfg.num_q_heads,
+                    num_kv_heads=cfg.num_kv_heads, head_dim=cfg.head_dim,
+                    tokens_per_frame=cfg.tokens_per_frame, sink_tokens=cfg.sink_tokens,
+                    past_frames=cfg.past_frames, instant_frames=cfg.instant_frames,
+                    max_query_tokens=cfg.query_tokens, rope_theta=cfg.rope_theta,
+                    max_position=cfg.max_position, dtype=cfg.dtype, device=device)
+        args.update(kw)
+        return cls(**args)
+
+    # ------------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(_lib.dscache_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ------------------------------------------------------------------ checks
+    def _t(self, t: torch.Tensor, name: str, shape=None) -> torch.Tensor:
+        if not isinstance(t, torch.Tensor) or t.device != self.device:
+            raise ValueError(f"{name} must be a CUDA tensor on {self.device}")
+        if t.dtype != self.torch_dtype:
+            raise ValueError(f"{name} must be {self.torch_dtype}, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if shape is not None and tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+        return t
+
+    def _layers(self, layer_begin, layer_count):
+        return layer_begin, (self.cfg.num_layers - layer_begin if layer_count is None else layer_count)
+
+    # ------------------------------------------------------------------ hot path
+    def append_frame(self, k: torch.Tensor, v: torch.Tensor, layer_begin: int = 0,
+                     layer_count: Optional[int] = None, stream=None):
+        """k, v: [S][layer_count][n][Hkv][d] (n = A for the sink, tpf for frames)."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        self._t(k, "k"); self._t(v, "v", k.shape)
+        if k.dim() != 5 or k.shape[0] != c.num_streams or k.shape[1] != lc or k.shape[3] != c.num_kv_heads \
+                or k.shape[4] != c.head_dim:
+            raise ValueError(f"k has shape {tuple(k.shape)}, expected [S, {lc}, n, Hkv, d]")
+        _check(_lib.dscache_append_frame(self._h, lb, lc, _ptr(k), _ptr(v), int(k.shape[2]),
+                                         _stream_ptr(stream)))
+
+    def build_instant(self, q_inst: torch.Tensor, o_inst: Optional[torch.Tensor] = None, layer_begin: int = 0,
+                      layer_count: Optional[int] = None, stream=None) -> torch.Tensor:
+        """q_inst: [S][layer_count][C_t][Hq][d] -> O_inst (same shape)."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        C_t = self.state(lb)["instant_tokens"]
+        shape = (c.num_streams, lc, C_t, c.num_q_heads, c.head_dim)
+        self._t(q_inst, "q_inst", shape)
+        if o_inst is None:
+            o_inst = torch.empty(shape, dtype=self.torch_dtype, device=self.device)
+        self._t(o_inst, "o_inst", shape)
+        _check(_lib.dscache_build_instant(self._h, lb, lc, _ptr(q_inst), _ptr(o_inst), _stream_ptr(stream)))
+        return o_inst
+
+    def attend(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor,
+               o: Optional[torch.Tensor] = None, layer_begin: int = 0, layer_count: Optional[int] = None,
+               stream=None) -> torch.Tensor:
+        """q: [S][lc][n_q][Hq][d], k_self/v_self: [S][lc][n_q][Hkv][d] -> O [S][lc][n_q][Hq][d]."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        n_q = int(q.shape[2])
+        self._t(q, "q", (c.num_streams, lc, n_q, c.num_q_heads, c.head_dim))
+        self._t(k_self, "k_self", (c.num_streams, lc, n_q, c.num_kv_heads, c.head_dim))
+        self._t(v_self, "v_self", k_self.shape)
+        if o is None:
+            o = torch.empty(q.shape, dtype=self.torch_dtype, device=self.device)
+        self._t(o, "o", q.shape)
+        _check(_lib.dscache_attend(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, _ptr(o),
+                                   _stream_ptr(stream)))
+        return o
+
+    # ------------------------------------------------------------------ introspection
+    def state(self, layer: int = 0) -> dict:
+        st = State()
+        _check(_lib.dscache_get_state(self._h, layer, ctypes.byref(st)))
+        return st.as_dict()
+
+    def copy_ring(self, stream_idx: int, layer: int):
+        c = self.cfg
+        shape = (c.num_kv_heads, self.R, c.head_dim)
+        k = torch.empty(shape, dtype=self.torch_dtype)
+        v = torch.empty(shape, dtype=self.torch_dtype)
+        _check(_lib.dscache_copy_ring(self._h, stream_idx, layer, _ptr(k), _ptr(v)))
+        return k, v
+
+    def copy_sink(self, stream_idx: int, layer: int):
+        c = self.cfg
+        shape = (c.num_kv_heads, c.sink_tokens, c.head_dim)
+        k = torch.empty(shape, dtype=self.torch_dtype)
+        v = torch.empty(shape, dtype=self.torch_dtype)
+        _check(_lib.dscache_copy_sink(self._h, stream_idx, layer, _ptr(k), _ptr(v)))
+        return k, v
+
+    def debug_len(self) -> int:
+        return int(_lib.dscache_debug_len(self._h))
+
+    def set_debug(self, build_pos: Optional[torch.Tensor] = None, attend_pos: Optional[torch.Tensor] = None,
+                  poison: bool = False):
+        for t in (build_pos, attend_pos):
+            if t is not None and (t.dtype != torch.int32 or t.device != self.device or t.numel() < self.debug_len()):
+                raise ValueError("debug buffers must be int32 CUDA tensors of debug_len() entries")
+        self._dbg = (build_pos, attend_pos)   # keep alive
+        _check(_lib.dscache_set_debug(self._h, _ptr(build_pos), _ptr(attend_pos), int(bool(poison))))
+
+    def profile(self, enable: bool = True):
+        _check(_lib.dscache_profile(self._h, int(enable)))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        mb, ma = ctypes.c_double(), ctypes.c_double()
+        nb, na, nl = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.dscache_profile_read(self._h, ctypes.byref(mb), ctypes.byref(ma), ctypes.byref(nb),
+                                         ctypes.byref(na), ctypes.byref(nl), int(reset)))
+        return {"ms_build": mb.value, "ms_attend": ma.value, "n_build": nb.value, "n_attend": na.value,
+                "kernel_launches": nl.value}
+
+    def attn_impl(self) -> dict:
+        names = {IMPL_TC: "tcgen05", IMPL_SIMT: "simt"}
+        return {"build_instant": names.get(_lib.dscache_attn_impl(self._h, 0)),
+                "attend": names.get(_lib.dscache_attn_impl(self._h, 1))}

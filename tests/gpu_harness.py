@@ -1,0 +1,109 @@
+"""Drive the CUDA path over a seeded stream and capture outputs for parity tests.
+
+Streams/layers listed in `exact` get the exact seeded inputs of dscache_synth
+(so the oracle can recompute them); all other (stream, layer) slots get cheap
+device-side random data of the same distribution -- they still run through
+every kernel (full launch configuration) and double as an isolation check.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import dscache_synth as synth
+from paper_2605_01858_b200 import dscache as D
+
+
+def _batch(cfg, shape_tail, exact, fill, dev, gen):
+    """[S][N][*shape_tail] on device: random everywhere, exact slices from fill(s, l)."""
+    t = (torch.randn((cfg.num_streams, cfg.num_layers) + tuple(shape_tail), device=dev, generator=gen)
+         * cfg.scale).to(cfg.torch_dtype)
+    for (s, l) in exact:
+        t[s, l] = fill(s, l).to(dev)
+    return t
+
+
+def run_stream(cfg, capture_steps, exact, impl=D.IMPL_AUTO, debug=False, poison=False, ring_capture=(),
+               layer_by_layer=False, n_q=None, past_override=None):
+    """Returns {t: {(s,l): (o_inst cpu, o cpu)}, "ring": {(t,s,l): (k,v)}, "dbg": {t: (b,a)}, "state": {t: st}}.
+
+    past_override(s, l, f) -> (k, v) or None lets a test replace past frames (decoupling test)."""
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + cfg.cfg_id)
+    n_q = cfg.query_tokens if n_q is None else n_q
+    dsc = D.DSCache.from_config(cfg, attn_impl=impl)
+    out = {"ring": {}, "dbg": {}, "state": {}, "impl": dsc.attn_impl()}
+    dbg_b = dbg_a = None
+    if debug or poison:
+        if debug:
+            dbg_b = torch.full((dsc.debug_len(),), -1, dtype=torch.int32, device=dev)
+            dbg_a = torch.full((dsc.debug_len(),), -1, dtype=torch.int32, device=dev)
+        dsc.set_debug(dbg_b, dbg_a, poison)
+    A, tpf, Hkv, Hq, d = cfg.sink_tokens, cfg.tokens_per_frame, cfg.num_kv_heads, cfg.num_q_heads, cfg.head_dim
+    if A > 0:
+        skv = {sl: synth.sink_kv(cfg, sl[0], sl[1]) for sl in exact}
+        sk = _batch(cfg, (A, Hkv, d), exact, lambda s, l: skv[(s, l)][0], dev, gen)
+        sv = _batch(cfg, (A, Hkv, d), exact, lambda s, l: skv[(s, l)][1], dev, gen)
+        dsc.append_frame(sk, sv)
+    last = max(capture_steps)
+    for t in range(last + 1):
+        kv = {}
+        for (s, l) in exact:
+            r = past_override(s, l, t) if past_override is not None else None
+            kv[(s, l)] = r if r is not None else synth.frame_kv(cfg, s, l, t)
+        k = _batch(cfg, (tpf, Hkv, d), exact, lambda s, l: kv[(s, l)][0], dev, gen)
+        v = _batch(cfg, (tpf, Hkv, d), exact, lambda s, l: kv[(s, l)][1], dev, gen)
+        if layer_by_layer:
+            for l in range(cfg.num_layers):
+                dsc.append_frame(k[:, l:l + 1].contiguous(), v[:, l:l + 1].contiguous(), layer_begin=l, layer_count=1)
+        else:
+            dsc.append_frame(k, v)
+        if t not in capture_steps:
+            continue
+        st = dsc.state(0)
+        out["state"][t] = st
+        C_t = st["instant_tokens"]
+        caps = {}
+        o_inst = None
+        if C_t > 0:
+            qi = _batch(cfg, (C_t, Hq, d), exact, lambda s, l: synth.instant_q(cfg, s, l, t, C_t), dev, gen)
+            if debug:
+                dbg_b.fill_(-1)
+            o_inst = dsc.build_instant(qi)
+        qkv = {sl: synth.query_qkv(cfg, sl[0], sl[1], t, n_q) for sl in exact}
+        q = _batch(cfg, (n_q, Hq, d), exact, lambda s, l: qkv[(s, l)][0], dev, gen)
+        ks = _batch(cfg, (n_q, Hkv, d), exact, lambda s, l: qkv[(s, l)][1], dev, gen)
+        vs = _batch(cfg, (n_q, Hkv, d), exact, lambda s, l: qkv[(s, l)][2], dev, gen)
+        if debug:
+            dbg_a.fill_(-1)
+        o = dsc.attend(q, ks, vs)
+        torch.cuda.synchronize()
+        for (s, l) in exact:
+            caps[(s, l)] = (None if o_inst is None else o_inst[s, l].float().cpu(), o[s, l].float().cpu())
+        out[t] = caps
+        if debug:
+            out["dbg"][t] = (dbg_b.cpu().numpy().copy(), dbg_a.cpu().numpy().copy())
+        for (s, l) in ring_capture:
+            out["ring"][(t, s, l)] = dsc.copy_ring(s, l)
+    out["sink"] = {(s, l): dsc.copy_sink(s, l) for (s, l) in ring_capture}
+    dsc.close()
+    return out
+
+
+def errors(gpu: torch.Tensor, ref: np.ndarray):
+    g = gpu.double().numpy()
+    diff = g - ref
+    max_abs = float(np.abs(diff).max()) if diff.size else 0.0
+    den = float(np.linalg.norm(ref))
+    rel_l2 = float(np.linalg.norm(diff) / den) if den > 0 else float(np.linalg.norm(diff))
+    return max_abs, rel_l2
+
+
+def assert_close(gpu, ref, dtype: str, what: str):
+    max_abs, rel_l2 = errors(gpu, ref)
+    if dtype == "fp32":
+        assert max_abs <= 1e-4, f"{what}: max abs {max_abs:.3e} > 1e-4"
+    else:
+        assert max_abs <= 2e-2 and rel_l2 <= 5e-3, f"{what}: max abs {max_abs:.3e}, rel L2 {rel_l2:.3e}"
+    return max_abs, rel_l2

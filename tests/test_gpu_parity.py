@@ -1,0 +1,256 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bar (BASELINE.json north_star): ring slots, eviction order and position ids
+bit-exact; fp32 configs max abs <= 1e-4; bf16 configs max abs <= 2e-2 AND
+relative L2 <= 5e-3 (the binding check, SURVEY §8(c) "Tolerances"), per
+(step, stream, layer, output kind).
+"""
+import numpy as np
+import pytest
+import torch
+
+import dscache_synth as synth
+from oracle import dscache_oracle as O
+from oracle.workload import StreamInputs, expected_ring, oracle_step, step_schedule
+from tests.gpu_harness import assert_close, errors, run_stream
+from paper_2605_01858_b200 import dscache as D
+
+pytestmark = pytest.mark.gpu
+
+REPORT = []
+
+
+def _check_steps(cfg, res, steps, exact, style=O.SPLIT_HALF, tag=""):
+    for t in steps:
+        for (s, l) in exact:
+            sch, o_inst, o = oracle_step(cfg, s, l, t, style=style)
+            g_inst, g_o = res[t][(s, l)]
+            if sch.C_t > 0:
+                ma, rl = assert_close(g_inst, o_inst, cfg.dtype, f"{tag} O_inst t={t} s={s} l={l}")
+                REPORT.append((cfg.name + tag, "O_inst", t, s, l, ma, rl))
+            ma, rl = assert_close(g_o, o, cfg.dtype, f"{tag} O t={t} s={s} l={l}")
+            REPORT.append((cfg.name + tag, "O", t, s, l, ma, rl))
+
+
+def test_c1_fp32_all_steps(lib):
+    cfg = synth.CONFIGS["c1"]
+    steps = list(range(cfg.num_frames))
+    res = run_stream(cfg, steps, [(0, 0)])
+    assert res["impl"] == {"build_instant": "simt", "attend": "simt"}
+    _check_steps(cfg, res, steps, [(0, 0)])
+
+
+def test_c1_adjacent_rope_style(lib):
+    cfg = synth.CONFIGS["c1"]
+    steps = [0, 5, 19]
+    dev_cfg = cfg
+    res = run_stream_style(dev_cfg, steps, D.ROPE_ADJACENT)
+    _check_steps(cfg, res, steps, [(0, 0)], style=O.ADJACENT, tag="-adj")
+
+
+def run_stream_style(cfg, steps, style):
+    # same as run_stream, through a handle created with the adjacent-pair RoPE flag
+    orig = D.DSCache.from_config
+
+    def patched(c, device=0, **kw):
+        kw["rope_style"] = style
+        return orig(c, device, **kw)
+    D.DSCache.from_config = patched
+    try:
+        return run_stream(cfg, steps, [(0, 0)])
+    finally:
+        D.DSCache.from_config = orig
+
+
+def test_c2_bf16_tcgen05(lib):
+    cfg = synth.CONFIGS["c2"]
+    steps = [0, 1, 3, 4, 35, 36, 37, 63]
+    res = run_stream(cfg, steps, [(0, 0)])
+    assert res["impl"] == {"build_instant": "tcgen05", "attend": "tcgen05"}
+    _check_steps(cfg, res, steps, [(0, 0)])
+
+
+def test_c2_bf16_simt_crosscheck(lib):
+    cfg = synth.CONFIGS["c2"]
+    steps = [3, 40]
+    res = run_stream(cfg, steps, [(0, 0)], impl=D.IMPL_SIMT)
+    assert res["impl"] == {"build_instant": "simt", "attend": "simt"}
+    _check_steps(cfg, res, steps, [(0, 0)], tag="-simt")
+
+
+def test_zero_output_negative_control(lib):
+    # an all-zero output must FAIL the bf16 bar (rel L2 = 1): the tolerance is not vacuous
+    cfg = synth.CONFIGS["c2"]
+    sch, o_inst, o = oracle_step(cfg, 0, 0, 40)
+    with pytest.raises(AssertionError):
+        assert_close(torch.zeros(o.shape), o, "bf16", "zero control")
+    # and off-by-one positions / a dropped sink in the reference must be detected too
+    res = run_stream(cfg, [40], [(0, 0)])
+    g_inst, g_o = res[40][(0, 0)]
+    inp = StreamInputs(cfg, 0, 0)
+    q, ks, vs = inp.query(40)
+    sink = inp.sink()
+    shifted = O.attend_output(sch, sink, inp.frame_kv, q, ks, vs, cfg.rope_theta)   # correct
+    assert errors(g_o, shifted)[1] < 5e-3
+    # reference with every id + 1 for the keys only (relative distances broken by one)
+    frames = sch.past_frames + sch.instant_frames
+    kk = np.concatenate([sink[0]] + [inp.frame_kv(f)[0] for f in frames] + [ks])
+    vv = np.concatenate([sink[1]] + [inp.frame_kv(f)[1] for f in frames] + [vs])
+    pk = np.arange(len(kk))
+    bad = O.gqa_attention(q, pk[-len(q):], kk, vv, pk + 1, cfg.rope_theta)
+    assert errors(g_o, bad)[1] > 5e-3
+    nosink = O.gqa_attention(q, pk[-len(q):] - cfg.sink_tokens, kk[cfg.sink_tokens:], vv[cfg.sink_tokens:],
+                             pk[cfg.sink_tokens:] - cfg.sink_tokens, cfg.rope_theta)
+    assert errors(g_o, nosink)[1] > 5e-3
+
+
+def test_ring_slots_sink_and_eviction_bit_exact(lib):
+    for name, steps in (("c1", [0, 4, 5, 13, 19]), ("c2", [0, 36, 37, 50])):
+        cfg = synth.CONFIGS[name]
+        res = run_stream(cfg, steps, [(0, 0)], ring_capture=[(0, 0)])
+        inp = StreamInputs(cfg, 0, 0)
+        for t in steps:
+            k, v = res["ring"][(t, 0, 0)]
+            sch = step_schedule(cfg, t)
+            exp = expected_ring(cfg, sch, inp)
+            st = res["state"][t]
+            assert st["past_tokens"] == sch.P_t and st["instant_tokens"] == sch.C_t
+            assert st["last_evicted_frame"] == (sch.evicted[0] if sch.evicted else -1)
+            for slot, (ek, ev) in exp.items():
+                assert torch.equal(k[:, slot].double(), torch.from_numpy(ek)), (name, t, slot)
+                assert torch.equal(v[:, slot].double(), torch.from_numpy(ev)), (name, t, slot)
+        sk, sv = res["sink"][(0, 0)]
+        ek, ev = inp.sink()
+        assert torch.equal(sk.double(), torch.from_numpy(ek).permute(1, 0, 2))
+        assert torch.equal(sv.double(), torch.from_numpy(ev).permute(1, 0, 2))
+
+
+def test_poison_evicted_slots_and_outputs_unchanged(lib):
+    cfg = synth.CONFIGS["c2"]
+    steps = [40, 41]
+    clean = run_stream(cfg, steps, [(0, 0)])
+    pois = run_stream(cfg, steps, [(0, 0)], poison=True, ring_capture=[(0, 0)])
+    for t in steps:
+        assert torch.equal(clean[t][(0, 0)][1], pois[t][(0, 0)][1])
+        assert torch.equal(clean[t][(0, 0)][0], pois[t][(0, 0)][0])
+        sch = step_schedule(cfg, t)
+        ev = sch.evicted[0]
+        slots = O.ring_slots(ev, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames)
+        k, _ = pois["ring"][(t, 0, 0)]
+        assert torch.all(k[:, slots].float() > 1e29)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_debug_position_ids_bit_exact(lib, name):
+    cfg = synth.CONFIGS[name]
+    steps = [0, 3, 37] if name == "c2" else [0, 3, 7, 19]
+    res = run_stream(cfg, steps, [(0, 0)], debug=True)
+    R = (cfg.past_frames + cfg.instant_frames + 1) * cfg.tokens_per_frame
+    A = cfg.sink_tokens
+    M = max(cfg.C, cfg.query_tokens)
+    for t in steps:
+        sch = step_schedule(cfg, t)
+        bk, bq, ak, aq = O.position_ids(sch, cfg.query_tokens)
+        dbg_b, dbg_a = res["dbg"][t]
+        # attend: sink ids, ring slot -> id, self ids, query ids
+        assert np.array_equal(dbg_a[:A], ak[:A])
+        frames = sch.past_frames + sch.instant_frames
+        slots = np.concatenate([O.ring_slots(f, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames)
+                                for f in frames])
+        assert np.array_equal(dbg_a[A + slots], ak[A:A + len(slots)])
+        in_window = np.zeros(R, bool); in_window[slots] = True
+        assert np.all(dbg_a[A:A + R][~in_window] == -1)
+        nq = cfg.query_tokens
+        assert np.array_equal(dbg_a[A + R:A + R + nq], ak[A + len(slots):])
+        assert np.array_equal(dbg_a[A + R + M:A + R + M + nq], aq)
+        # build: sink ids, instant slots -> A + i, query ids A + i
+        islots = np.concatenate([O.ring_slots(f, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames)
+                                 for f in sch.instant_frames])
+        assert np.array_equal(dbg_b[:A], bk[:A])
+        assert np.array_equal(dbg_b[A + islots], bk[A:])
+        assert np.array_equal(dbg_b[A + R + M:A + R + M + sch.C_t], bq)
+
+
+def test_decoupling_instant_independent_of_past(lib):
+    # Eq. 7: O_inst bitwise unchanged when every past frame holds other data
+    cfg = synth.CONFIGS["c2"]
+    t = 45
+    sch = step_schedule(cfg, t)
+    gen = torch.Generator().manual_seed(7)
+
+    def override(s, l, f):
+        if f in sch.instant_frames:
+            return None
+        shp = (cfg.tokens_per_frame, cfg.num_kv_heads, cfg.head_dim)
+        return ((torch.randn(shp, generator=gen) * 3).to(torch.bfloat16),
+                (torch.randn(shp, generator=gen) * 3).to(torch.bfloat16))
+    a = run_stream(cfg, [t], [(0, 0)])
+    b = run_stream(cfg, [t], [(0, 0)], past_override=override)
+    assert torch.equal(a[t][(0, 0)][0], b[t][(0, 0)][0])
+    assert not torch.equal(a[t][(0, 0)][1], b[t][(0, 0)][1])
+
+
+@pytest.mark.parametrize("variant", ["no_sink", "lI0_uniform", "lU0_window", "layerwise"])
+def test_edge_configs_tcgen05(lib, variant):
+    base = synth.CONFIGS["c2"].replace(tokens_per_frame=128, past_frames=6, instant_frames=3, num_frames=16,
+                                       query_tokens=37, num_layers=2)
+    if variant == "no_sink":
+        cfg = base.replace(sink_tokens=0)
+    elif variant == "lI0_uniform":
+        cfg = base.replace(instant_frames=0)
+    elif variant == "lU0_window":
+        cfg = base.replace(past_frames=0)
+    else:
+        cfg = base
+    steps = [0, 2, 9, 10, 15]
+    res = run_stream(cfg, steps, [(0, 0), (0, 1)], layer_by_layer=(variant == "layerwise"))
+    assert res["impl"]["attend"] == "tcgen05"
+    _check_steps(cfg, res, steps, [(0, 0), (0, 1)], tag="-" + variant)
+
+
+def test_c3_28_layers_sampled(lib):
+    cfg = synth.CONFIGS["c3"]
+    steps = [0, 7, 8, 71, 72, 100]
+    exact = [(0, 0), (0, 13), (0, 27)]
+    res = run_stream(cfg, steps, exact)
+    _check_steps(cfg, res, steps, exact)
+
+
+def test_c4_long_stream_sampled(lib):
+    cfg = synth.CONFIGS["c4"]
+    steps = [0, 8, 136, 272, 1000, 2047, 4095]
+    res = run_stream(cfg, steps, [(0, 0)], debug=True)
+    _check_steps(cfg, res, steps, [(0, 0)])
+    dbg_b, dbg_a = res["dbg"][4095]
+    assert dbg_a.max() == 26723 and dbg_a.max() < cfg.max_position
+
+
+def test_c5_multistream_sampled(lib):
+    cfg = synth.CONFIGS["c5"]
+    steps = [0, 35, 36, 127]
+    exact = [(0, 0), (7, 3), (63, 0), (63, 3)]
+    res = run_stream(cfg, steps, exact)
+    _check_steps(cfg, res, steps, exact)
+
+
+def test_errors_through_the_abi(lib):
+    cfg = synth.CONFIGS["c2"]
+    with pytest.raises(D.DSCacheError) as e:
+        D.DSCache.from_config(cfg, max_position=7000)
+    assert e.value.status == D.E_POS_OVERFLOW
+    h = D.DSCache.from_config(cfg)
+    q = torch.zeros(1, 1, 64, 28, 128, dtype=torch.bfloat16, device="cuda")
+    kv = torch.zeros(1, 1, 64, 4, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(D.DSCacheError) as e:
+        h.attend(q, kv, kv)
+    assert e.value.status == D.E_STATE
+    bad = torch.zeros(1, 1, 5, 4, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(D.DSCacheError) as e:
+        h.append_frame(bad, bad)
+    assert e.value.status == D.E_ARG
+    h.close()
+
+
+def test_zz_print_report(lib):
+    for r in REPORT:
+        print("PARITY %-16s %-6s t=%-5d s=%-3d l=%-3d max_abs=%.3e rel_l2=%.3e" % r)

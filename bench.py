@@ -1,0 +1,418 @@
+#!/usr/bin/env python3
+"""DSCache streaming hot-path benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+
+A *step* is one pass of the whole hot path for every (stream, layer) a rank
+holds: append the new frame's raw K/V (ring append + FIFO eviction), build the
+instant cache (Eq. 7), and attend the query chunk over [sink|past|instant|self]
+(Eq. 8), all through the C ABI on one CUDA stream.  Default workload is c5
+(BASELINE.json configs[4]: 64 independent streams x 4 layers of the 7B
+attention shape), the configuration the metric is quoted on "at 1/2/4/8 GPUs";
+for N > 1 its 64 streams are partitioned across ranks (rank r holds streams
+[r*64/N, (r+1)*64/N)), with no collective on the data path.  Timed steps are
+steady state (the window is full: l_I + l_U frames appended before timing).
+
+value = frames processed by all ranks / max-over-ranks device time (frames/s,
+one frame per stream per step).  The ring (3.8 GB for c5) is far larger than
+L2, so no L2 flush is needed; for configs whose working set fits in L2 the
+bench flushes L2 between steps and times each step separately.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import dscache_synth as synth  # noqa: E402
+
+METRIC = "frames/s per stream and attention TFLOP/s (% B200 bf16 peak) at 1/2/4/8 GPUs"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"bf16_tflops": d["bf16_tflops"], "bf16_tflops_sustained": d.get("bf16_tflops_sustained"),
+                "hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+# ----------------------------------------------------------------------------- workload arithmetic
+def steady_counts(cfg, n_q=None):
+    """Steady-state token counts per (stream, layer): A, P = W, C, q."""
+    n_q = cfg.query_tokens if n_q is None else n_q
+    return cfg.sink_tokens, cfg.W, cfg.C, n_q
+
+
+def flops_per_unit(cfg):
+    """Algorithmic FLOPs of one (stream, layer) step: 4 * d * Hq * visible (query, key) pairs.
+    build: instant token i sees A + i + 1 keys; attend: query i sees A + P + C + i + 1 keys."""
+    A, P, C, q = steady_counts(cfg)
+    k = 4 * cfg.head_dim * cfg.num_q_heads
+    build = k * (C * A + C * (C + 1) // 2)
+    attend = k * (q * (A + P + C) + q * (q + 1) // 2)
+    return build, attend
+
+
+def bytes_per_unit(cfg):
+    """Algorithmic HBM bytes of one (stream, layer) step (each context K/V row read once,
+    Q read, O written, append read + written; eviction moves nothing)."""
+    A, P, C, q = steady_counts(cfg)
+    e = 2 if cfg.dtype == "bf16" else 4
+    row_kv = cfg.num_kv_heads * cfg.head_dim * e
+    row_q = cfg.num_q_heads * cfg.head_dim * e
+    build = (A + C) * 2 * row_kv + 2 * C * row_q
+    attend = (A + P + C) * 2 * row_kv + 2 * q * row_kv + 2 * q * row_q
+    append = 2 * 2 * cfg.tokens_per_frame * row_kv
+    return build, attend, append
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, device_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device_index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        loaded = [x for x in sm if x > 500] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def stream_range(S: int, world: int, rank: int):
+    from paper_2605_01858_b200.dist import stream_partition
+    return stream_partition(S, world, rank)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, cfg, world, rank, local):
+    from paper_2605_01858_b200 import dscache as D
+    dev = torch.device("cuda", local)
+    lo, hi = stream_range(cfg.num_streams, world, rank)
+    S = hi - lo
+    lcfg = cfg.replace(num_streams=S)
+    dsc = D.DSCache.from_config(lcfg, device=local)
+    A, P, C, q = steady_counts(cfg)
+    N, Hq, Hkv, d, tpf = cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.tokens_per_frame
+    dt = cfg.torch_dtype
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+
+    def rnd(*shape):
+        return (torch.randn(shape, device=dev, generator=g) * cfg.scale).to(dt)
+
+    # device-resident synthetic input pool (values cycle; positions / slots never repeat)
+    POOL = 4
+    frames = [(rnd(S, N, tpf, Hkv, d), rnd(S, N, tpf, Hkv, d)) for _ in range(POOL)]
+    q_inst = [rnd(S, N, C, Hq, d) for _ in range(2)]
+    qry = [(rnd(S, N, q, Hq, d), rnd(S, N, q, Hkv, d), rnd(S, N, q, Hkv, d)) for _ in range(2)]
+    o_inst = torch.empty(S, N, C, Hq, d, dtype=dt, device=dev)
+    o = torch.empty(S, N, q, Hq, d, dtype=dt, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    if A > 0:
+        dsc.append_frame(rnd(S, N, A, Hkv, d), rnd(S, N, A, Hkv, d))
+    fill = cfg.instant_frames + cfg.past_frames - 1
+    for t in range(fill):
+        dsc.append_frame(*frames[t % POOL])
+    tcount = [fill]
+
+    def step(i):
+        t = tcount[0]
+        dsc.append_frame(*frames[t % POOL])
+        dsc.build_instant(q_inst[i & 1], o_inst)
+        qq = qry[i & 1]
+        dsc.attend(qq[0], qq[1], qq[2], o)
+        tcount[0] += 1
+
+    ring_bytes = 2 * S * N * Hkv * dsc.R * d * (2 if cfg.dtype == "bf16" else 4)
+    flush = ring_bytes < 2 * L2_BYTES
+    scratch = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if flush else None
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    assert dsc.state(0)["past_tokens"] == P and dsc.state(0)["instant_tokens"] == C
+
+    dsc.profile(True)
+    dsc.profile_read(reset=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local) if rank == 0 else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if flush:
+        total_ms = 0.0
+        for i in range(args.steps):
+            scratch.zero_()
+            ev[i][0].record(stream)
+            step(i)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    else:
+        ev[0][0].record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev[0][1].record(stream)
+        torch.cuda.synchronize()
+        total_ms = ev[0][0].elapsed_time(ev[0][1])
+    barrier(world)
+    torch.cuda.synchronize()
+    clk = clocks.stop() if clocks else None
+    prof = dsc.profile_read(reset=True)
+    dsc.profile(False)
+    t_max = max_over_ranks(total_ms, world)
+
+    # e2e: the same step through the public API with pinned host buffers, H2D of every
+    # input of the step and D2H of the query answer O inside the timed region
+    e2e = run_e2e(args, cfg, dsc, S, dev, stream, world)
+    impl = dsc.attn_impl()
+    dsc.close()
+
+    fb, fa = flops_per_unit(cfg)
+    units = S * N
+    frames_total = cfg.num_streams * args.steps
+    value = frames_total / (t_max / 1e3)
+    attn_flops_step_local = units * (fb + fa)
+    attn_ms = prof["ms_build"] + prof["ms_attend"]
+    n_launch = prof["n_build"] + prof["n_attend"]
+    pk = peaks()
+    achieved = (attn_flops_step_local * args.steps) / (attn_ms / 1e3) / 1e12 if attn_ms > 0 else None
+    step_tflops = attn_flops_step_local * args.steps / (total_ms / 1e3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(cfg.name, {}).get("attn_tc_kernel_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "strong",
+        "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.num_streams} streams x {cfg.num_layers} layers, Hq={Hq} Hkv={Hkv} "
+                               f"d={d}, tpf={tpf}, A={A}, W={cfg.past_frames}f, C={cfg.instant_frames}f, q={q}",
+                   "config_id": cfg.name, "streams": cfg.num_streams, "layers": N, "query_tokens": q,
+                   "parallelism": f"stream partition x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed between steps" if flush else "inputs larger than L2 (ring %.2f GB)" % (ring_bytes / 1e9),
+                   "steady_state": True, "input_pool": f"{POOL} distinct frames cycled (positions never repeat)"},
+        "frames_per_s_per_stream": round(value / cfg.num_streams, 3),
+        "attention_tflops_per_gpu_step": round(step_tflops, 2),
+        "attention_pct_peak_step": round(100 * step_tflops / pk["bf16_tflops"], 2),
+        "roofline": {"bound": "tensor", "kernel": "attn_tc_kernel (tcgen05 rotate-on-load flash attention)",
+                     "achieved": round(achieved, 2) if achieved else None, "peak": pk["bf16_tflops"],
+                     "peak_source": pk["source"] + " bf16 burst", "unit": "TFLOP/s",
+                     "frac": round(achieved / pk["bf16_tflops"], 4) if achieved else None,
+                     "traffic": traffic, "launches": n_launch,
+                     "algorithmic_flops_per_launch": (attn_flops_step_local * args.steps) / max(n_launch, 1)},
+        "gpu_launches": prof["kernel_launches"],
+        "attn_impl": impl,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    return line
+
+
+def run_e2e(args, cfg, dsc, S, dev, stream, world):
+    N, Hq, Hkv, d, tpf = cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.tokens_per_frame
+    A, P, C, q = steady_counts(cfg)
+    dt = cfg.torch_dtype
+    steps = max(3, min(args.steps, 10))
+
+    def host(*shape):
+        return (torch.randn(shape) * cfg.scale).to(dt).pin_memory()
+    hk, hv = host(S, N, tpf, Hkv, d), host(S, N, tpf, Hkv, d)
+    hqi = host(S, N, C, Hq, d)
+    hq, hks, hvs = host(S, N, q, Hq, d), host(S, N, q, Hkv, d), host(S, N, q, Hkv, d)
+    ho = torch.empty(S, N, q, Hq, d, dtype=dt).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in (hk, hv, hqi, hq, hks, hvs))
+    d2h = ho.numel() * ho.element_size()
+
+    def one():
+        k = hk.to(dev, non_blocking=True); v = hv.to(dev, non_blocking=True)
+        dsc.append_frame(k, v)
+        oi = dsc.build_instant(hqi.to(dev, non_blocking=True))
+        o = dsc.attend(hq.to(dev, non_blocking=True), hks.to(dev, non_blocking=True), hvs.to(dev, non_blocking=True))
+        ho.copy_(o, non_blocking=True)
+        del oi
+    one()
+    torch.cuda.synchronize()
+    barrier(world)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        one()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(a.elapsed_time(b), world)
+    return {"value": round(cfg.num_streams * steps / (ms / 1e3), 2), "unit": "frames/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "note": "pinned host inputs (frame K/V, Q_inst, Q, K_self, V_self) copied H2D and the query "
+                    "answer O copied D2H every step, through DSCache.append_frame/build_instant/attend"}
+
+
+# ----------------------------------------------------------------------------- oracle (cpu baseline / reference arm)
+def oracle_sample(cfg, budget_s: float):
+    """Time the fp64 oracle on (stream, layer) units of the steady-state workload."""
+    from oracle.workload import StreamInputs, oracle_step
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    t_steady = cfg.instant_frames + cfg.past_frames
+    units, t0 = 0, time.perf_counter()
+    times = []
+    while True:
+        s, l = units % cfg.num_streams, (units // cfg.num_streams) % cfg.num_layers
+        inp = StreamInputs(cfg, s, l)
+        a = time.perf_counter()
+        oracle_step(cfg, s, l, t_steady + units % 4, inputs=inp)
+        times.append(time.perf_counter() - a)
+        units += 1
+        if time.perf_counter() - t0 > budget_s or units >= 64:
+            break
+    per_unit = float(np.mean(times))
+    step_s = per_unit * cfg.num_streams * cfg.num_layers
+    return {"value": round(cfg.num_streams / step_s, 6), "unit": "frames/s", "cores": threads,
+            "kind": "oracle",
+            "sample": f"{units} steady-state (stream, layer) units of {cfg.name} (build_instant + attend, fp64 "
+                      f"numpy), {per_unit:.3f} s/unit, extrapolated to {cfg.num_streams * cfg.num_layers} "
+                      f"units per step",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args, cfg):
+    per_step = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        r = oracle_sample(cfg, budget_s=max(2.0, 60.0 / (args.warmup + args.steps)))
+        if i >= args.warmup:
+            per_step.append(r)
+        cb = r
+    value = float(np.mean([r["value"] for r in per_step]))
+    fb, fa = flops_per_unit(cfg)
+    return {"metric": METRIC, "value": round(value, 6), "unit": "frames/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * cfg.num_streams / value, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg.name, "config_id": cfg.name, "streams": cfg.num_streams,
+                       "layers": cfg.num_layers, "note": "fp64 CPU oracle (oracle/), the tier's reference arm"},
+            "cpu_baseline": {"value": round(value, 6), "unit": "frames/s", "cores": cb["cores"], "kind": "oracle",
+                             "sample": cb["sample"], "cpu": cb["cpu"]},
+            "e2e": {"value": round(value, 6), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return 0
+        print(json.dumps(run_reference(args, cfg)), flush=True)
+        return 0
+    world, rank, local = dist_setup(args.gpus)
+    line = run_ours(args, cfg, world, rank, local)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = oracle_sample(cfg, args.cpu_budget)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,62 @@
+"""Multi-GPU plumbing of the hot path (one process per GPU, torch.distributed).
+
+Two partitions, both from the north_star:
+
+* P1 -- independent streams: rank r holds streams [r*S/G, (r+1)*S/G) in its own
+  DSCache handle.  Streams share nothing, so the data path has no collective.
+* P2 -- KV-head groups of one stream: rank r holds KV heads
+  [r*Hkv/G, (r+1)*Hkv/G) and their Hq/Hkv query heads each.  Attention is
+  independent per KV head; the only exchange is an all-gather of the attend
+  output O, gathered head-major so no permute is needed on the wire.
+
+The collective backend is whatever the process group was created with: NCCL
+over NVLink on the GPU box, gloo on CPU for the multi-process tests.
+"""
+from __future__ import annotations
+
+from typing import Tuple
+
+import torch
+
+
+def stream_partition(num_streams: int, world: int, rank: int) -> Tuple[int, int]:
+    """[lo, hi) streams of `rank` -- contiguous, sizes differ by at most one."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    lo = rank * num_streams // world
+    hi = (rank + 1) * num_streams // world
+    return lo, hi
+
+
+def kv_head_partition(num_q_heads: int, num_kv_heads: int, world: int, rank: int):
+    """(kv_lo, kv_count, q_lo, q_count) of `rank`.  Needs Hkv % world == 0 (the
+    GQA group of a KV head never straddles ranks)."""
+    if num_kv_heads % world:
+        raise ValueError(f"Hkv={num_kv_heads} is not divisible by world={world}")
+    grp = num_q_heads // num_kv_heads
+    kv_count = num_kv_heads // world
+    kv_lo = rank * kv_count
+    return kv_lo, kv_count, kv_lo * grp, kv_count * grp
+
+
+def head_major(o: torch.Tensor) -> torch.Tensor:
+    """[S][N][n_q][Hq_local][d] -> contiguous [Hq_local][S][N][n_q][d] (one local copy
+    on the sender so the gathered buffer is contiguous per rank's head block)."""
+    return o.permute(3, 0, 1, 2, 4).contiguous()
+
+
+def gather_heads(o_local: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather the head-sharded attend outputs of every rank (P2).
+
+    o_local: [S][N][n_q][Hq_local][d] on this rank.  Returns [S][N][n_q][Hq][d]
+    with rank r's heads at [r*Hq_local, (r+1)*Hq_local), i.e. global head order."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    hm = head_major(o_local)                                   # [Hl][S][N][q][d]
+    out = torch.empty((world,) + tuple(hm.shape), dtype=hm.dtype, device=hm.device)
+    if hasattr(dist, "all_gather_into_tensor") and dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, hm, group=group)
+    else:
+        dist.all_gather(list(out.unbind(0)), hm, group=group)
+    full = out.reshape((world * hm.shape[0],) + tuple(hm.shape[1:]))   # [Hq][S][N][q][d]
+    return full.permute(1, 2, 3, 0, 4)

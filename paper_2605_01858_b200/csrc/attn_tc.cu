@@ -9,12 +9,14 @@
 // query rows (2 x 128-row Q tiles) that share it.  Softmax a_ij =
 // softmax(Q_i K_j / sqrt(d)) in the exp2 domain with lazy rescale.
 //
-// CTA = 13 warps:
+// CTA = 14 warps:
 //   warps 0-3  softmax of Q tile 0 (thread = query row = TMEM lane)
 //   warps 4-7  softmax of Q tile 1
-//   warps 8-11 loader: Q (rotate) once; per key tile K (LDG -> rotate -> STS,
-//              SW128 K-major) and V (cp.async 16B, zero-fill, SW128)
-//   warp 12    TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 8-11 rotation: Q (LDG -> rotate -> STS) once; then every raw K tile
+//              in place in shared memory (LDS -> rotate -> STS), R(p+1) = R(p)R(1)
+//   warp 12    copy: raw K and V tiles -> SW128 smem; TMA (2 x 64x128 boxes) for
+//              ring tiles, cp.async for the sink/self tile
+//   warp 13    TMEM allocator + single-thread tcgen05.mma issuer
 // TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512);
 // P_qt (bf16x2) overwrites S_qt cols [0,64) and feeds O_qt += P V as the TMEM A operand.
 // MMA issue order S0_0 S1_0 | PV0_j S0_{j+1} PV1_j S1_{j+1} | ... so each softmax
@@ -28,16 +30,17 @@ namespace dsc {
 namespace tc {
 
 constexpr int kNQT = 2;                       // Q tiles per CTA
-constexpr int kWarps = 13;
+constexpr int kWarps = 14;
 constexpr int kThreads = kWarps * 32;
 constexpr int kTileBytes = 128 * 128 * 2;     // one 128 x 128 bf16 tile
-constexpr int kStages = 2;
+constexpr int KST = 3;                        // K stages (raw -> rotated in place)
+constexpr int VST = 2;                        // V stages
 constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + kNQT * kTileBytes;
-constexpr int OFF_V = OFF_K + kStages * kTileBytes;
-constexpr int OFF_BAR = OFF_V + kStages * kTileBytes;
-// barriers (8 B each)
-constexpr int B_Q = 0, B_KF = 1, B_KE = 3, B_VF = 5, B_VE = 7, B_S = 9, B_P = 11, B_O = 13, B_N = 15;
+constexpr int OFF_V = OFF_K + KST * kTileBytes;
+constexpr int OFF_BAR = OFF_V + VST * kTileBytes;
+// barriers (8 B each): Q | K raw landed | K rotated | K free | V landed | V free | S | P | O
+constexpr int B_Q = 0, B_KR = 1, B_KF = 4, B_KE = 7, B_VF = 10, B_VE = 12, B_S = 14, B_P = 16, B_O = 18, B_N = 20;
 constexpr int kSmemBytes = OFF_BAR + B_N * 8 + 16 + 1024;   // + tmem slot + alignment slack
 constexpr float kRescaleThreshold = 8.0f;     // log2 units (factor 256)
 
@@ -196,6 +199,23 @@ __device__ __forceinline__ void ring_tile_info(int k, int R, int start, int cnt,
   c_b = rem > 0 ? min(width, c_a + rem) : c_a;
 }
 
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 r;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(addr) : "memory");
+  return r;
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 struct Work {
   int pp, g, mb, sp;
   long long head_row;
@@ -233,6 +253,38 @@ __device__ __forceinline__ Work decode_work(const AttnParams& p) {
   return w;
 }
 
+// Key rows of tile u as (at most) two segments; key row r of segment s has id
+// pos0_s + r.  Tile 0 = sink rows [0, A) + self rows [A, A+n_self); tile u > 0 =
+// physical ring tile (k0 + u - 1) mod nT, valid rows [c_a, c_b).
+struct TileSeg {
+  int lo0, hi0, pos0_0;
+  int lo1, hi1, pos0_1;
+  int phys;           // physical ring tile (u > 0), -1 for tile 0
+};
+
+__device__ __forceinline__ TileSeg tile_segments(const AttnParams& p, const Work& w, int u) {
+  TileSeg t;
+  if (u == 0) {
+    t.lo0 = 0; t.hi0 = p.A; t.pos0_0 = 0;
+    t.lo1 = p.A; t.hi1 = p.A + p.n_self; t.pos0_1 = p.ring_count;
+    t.phys = -1;
+  } else {
+    int k = w.k0 + u - 1;
+    if (k >= w.nT) k -= w.nT;
+    int c_a, c_b, rel_a;
+    ring_tile_info(k, p.R, p.ring_start, w.cnt, c_a, c_b, rel_a);
+    t.lo0 = c_a; t.hi0 = c_b; t.pos0_0 = p.A + rel_a - c_a;
+    t.lo1 = 0; t.hi1 = 0; t.pos0_1 = 0;
+    t.phys = k;
+  }
+  return t;
+}
+__device__ __forceinline__ int seg_pos(const TileSeg& t, int r) {
+  if (r >= t.lo0 && r < t.hi0) return t.pos0_0 + r;
+  if (r >= t.lo1 && r < t.hi1) return t.pos0_1 + r;
+  return -1;
+}
+
 // ------------------------------------------------------------------ kernel
 __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -247,11 +299,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
 
   if (threadIdx.x == 0) {
     mbar_init(bar(B_Q), 128);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < KST; ++i) {
+      mbar_init(bar(B_KR + i), 1);
       mbar_init(bar(B_KF + i), 128);
       mbar_init(bar(B_KE + i), 1);
-      mbar_init(bar(B_VF + i), 128);
+    }
+    for (int i = 0; i < VST; ++i) {
+      mbar_init(bar(B_VF + i), 1);
       mbar_init(bar(B_VE + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(bar(B_S + i), 1);
       mbar_init(bar(B_P + i), 128);
       mbar_init(bar(B_O + i), 1);
@@ -259,10 +316,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
   }
-  if (warp == 12) {
+  if (warp == 13) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (warp == 12 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_k)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_v)) : "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -283,7 +344,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     const uint32_t tS = tmem + lane_off + (uint32_t)(qt * 128);
     const uint32_t tO = tmem + lane_off + (uint32_t)(256 + qt * 128);
     const float sl2 = p.scale_log2;
-    float m = -INFINITY, lsum = 0.f;
+    const float2 scale2 = make_float2(sl2, sl2);
+    float m = -INFINITY;
+    float2 lsum2 = make_float2(0.f, 0.f);
     for (int jj = 0; jj < n; ++jj) {
       const int u = w.t_begin + jj;
       int c_lo, c_hi;
@@ -293,10 +356,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         c_lo = 0;
         c_hi = min(A + p.n_self, max(A, lim - p.ring_count + 1));
       } else {
-        int c_a, c_b, rel_a;
-        ring_tile_info((w.k0 + u - 1) % w.nT, p.R, p.ring_start, w.cnt, c_a, c_b, rel_a);
-        c_lo = c_a;
-        c_hi = max(c_lo, min(c_b, c_a + (lim - A - rel_a) + 1));
+        const TileSeg t = tile_segments(p, w, u);
+        c_lo = t.lo0;
+        // key at column c has id pos0 + c; visible iff id <= lim
+        c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));
       }
       const bool full = (c_lo == 0) && (c_hi == 128);
       mbar_wait(bar(B_S + qt), jj & 1);
@@ -310,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         tmem_wait_ld();
         if (full) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) mx = fmaxf(mx, __uint_as_float(r[c]));
+          for (int c = 0; c < 32; c += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(r[c]), __uint_as_float(r[c + 1])));
         } else {
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
@@ -326,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       const bool need_o = upd && (m != -INFINITY);
       const float f = need_o ? ex2(m - m_tile) : 1.f;
       if (upd) {
-        lsum *= f;
+        lsum2.x *= f; lsum2.y *= f;
         m = m_tile;
       }
       if (__any_sync(0xffffffffu, need_o)) {
@@ -345,6 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         tmem_wait_st();
       }
       const float m_use = (m == -INFINITY) ? 0.f : m;
+      const float2 negm2 = make_float2(-m_use, -m_use);
       // pass 2: P = 2^(s*scale - m) -> bf16x2 into S cols [0,64)
 #pragma unroll 1
       for (int ch = 0; ch < 4; ++ch) {
@@ -354,14 +418,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         uint32_t pk[16];
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
-          const int col = ch * 32 + c;
-          float p0 = ex2(fmaf(__uint_as_float(r[c]), sl2, -m_use));
-          float p1 = ex2(fmaf(__uint_as_float(r[c + 1]), sl2, -m_use));
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+          float p0 = ex2(x.x), p1 = ex2(x.y);
           if (!full) {
+            const int col = ch * 32 + c;
             p0 = (col >= c_lo && col < c_hi) ? p0 : 0.f;
             p1 = (col + 1 >= c_lo && col + 1 < c_hi) ? p1 : 0.f;
           }
-          lsum += p0 + p1;
+          lsum2 = __fadd2_rn(lsum2, make_float2(p0, p1));
           pk[c >> 1] = pack_bf16(p0, p1);
         }
         tmem_st16(tS + ch * 16, pk);
@@ -371,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       mbar_arrive(bar(B_P + qt));
     }
     // epilogue
+    const float lsum = lsum2.x + lsum2.y;
     mbar_wait(bar(B_O + qt), (n - 1) & 1);
     tc_fence_after();
     const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
@@ -405,14 +470,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       }
     }
   } else if (warp < 12) {
-    // ================================================================ loader
+    // ================================================================ rotation (Q once, then K tiles)
     const int lt = threadIdx.x - 256;
-    const int c = lt & 15;             // K/Q: frequency chunk (freqs 4c..4c+3); V: 16-byte chunk
+    const int c = lt & 15;             // frequency chunk: freqs 4c..4c+3 (elements 4c.. and 64+4c..)
     const int rgrp = lt >> 4;          // 0..7
     const __nv_bfloat16* __restrict__ Qg = reinterpret_cast<const __nv_bfloat16*>(p.q);
     const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
     const float4* __restrict__ rope4 = reinterpret_cast<const float4*>(p.rope);   // [pos][32] float4
-    // ---- Q: 256 rows, thread rows rgrp*32 .. +31, rotated at the query id
+    // ---- Q: 256 rows, thread rows rgrp*32 .. +31, rotated at the query id (table values)
 #pragma unroll 1
     for (int rb = 0; rb < 32; rb += 8) {
       uint2 lo[8], hi[8];
@@ -455,132 +520,129 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     fence_proxy_async();
     mbar_arrive(bar(B_Q));
 
-    // per-thread rotation step R(theta_f) for f = 4c..4c+3 (table row of id 1)
+    // per-thread rotation step R(theta_f), f = 4c..4c+3 (table row of id 1), packed by freq pairs
     const float4 st0 = rope4[32 + 2 * c], st1 = rope4[32 + 2 * c + 1];
-    const __nv_bfloat16* __restrict__ SK = reinterpret_cast<const __nv_bfloat16*>(p.sink_k);
-    const __nv_bfloat16* __restrict__ SV = reinterpret_cast<const __nv_bfloat16*>(p.sink_v);
-    const __nv_bfloat16* __restrict__ RK = reinterpret_cast<const __nv_bfloat16*>(p.ring_k);
-    const __nv_bfloat16* __restrict__ RV = reinterpret_cast<const __nv_bfloat16*>(p.ring_v);
-    const __nv_bfloat16* __restrict__ XK = reinterpret_cast<const __nv_bfloat16*>(p.self_k);
-    const __nv_bfloat16* __restrict__ XV = reinterpret_cast<const __nv_bfloat16*>(p.self_v);
-
-    // source row + id of key row r of tile u (nullptr = no key: zero-fill)
-    auto key_row = [&](int u, int r, bool want_v, int& pos, int& dbg_idx) -> const __nv_bfloat16* {
-      pos = -1; dbg_idx = -1;
-      if (u == 0) {
-        if (r < A) {
-          pos = r; dbg_idx = r;
-          return (want_v ? SV : SK) + (w.head_row * A + r) * 128;
-        }
-        if (r < A + p.n_self) {
-          const int j = r - A;
-          pos = A + p.ring_count + j; dbg_idx = A + p.R + j;
-          return (want_v ? XV : XK) + (((long long)w.pp * p.n_self + j) * p.Hkv + w.g) * 128;
-        }
-        return nullptr;
-      }
-      const int k = (w.k0 + u - 1) % w.nT;
-      int c_a, c_b, rel_a;
-      ring_tile_info(k, p.R, p.ring_start, w.cnt, c_a, c_b, rel_a);
-      if (r < c_a || r >= c_b) return nullptr;
-      const int slot = k * 128 + r;
-      pos = A + rel_a + (r - c_a); dbg_idx = A + slot;
-      return (want_v ? RV : RK) + (w.head_row * p.R + slot) * 128;
-    };
-
-    auto issue_v = [&](int jj) {
-      const int u = w.t_begin + jj, stg = jj & 1;
-      const uint32_t vb = sbase + OFF_V + stg * kTileBytes;
-      const int blk = c >> 3, chk = c & 7;
-#pragma unroll 4
-      for (int k = 0; k < 16; ++k) {
-        const int r = rgrp + 8 * k;
-        int pos, di;
-        const __nv_bfloat16* src = key_row(u, r, true, pos, di);
-        const uint32_t dst = vb + blk * 16384 + r * 128 + ((chk ^ (r & 7)) << 4);
-        cp_async16(dst, src ? (const void*)(src + 8 * c) : (const void*)RV, src ? 16u : 0u);
-      }
-    };
-
+    const float2 cth01 = make_float2(st0.x, st0.z), sth01 = make_float2(st0.y, st0.w);
+    const float2 cth23 = make_float2(st1.x, st1.z), sth23 = make_float2(st1.y, st1.w);
 #pragma unroll 1
     for (int jj = 0; jj < n; ++jj) {
-      const int u = w.t_begin + jj, stg = jj & 1;
-      // K rows rgrp*16 .. +15: issue all loads first
-      uint2 lo[16], hi[16];
-      int pos[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int r = rgrp * 16 + k;
-        int di;
-        const __nv_bfloat16* src = key_row(u, r, false, pos[k], di);
-        if (src) {
-          lo[k] = ldg64(src + 4 * c);
-          hi[k] = ldg64(src + 64 + 4 * c);
-          if (dbg && c == 0) p.dbg_pos[di] = pos[k];
-        } else {
-          lo[k] = make_uint2(0, 0); hi[k] = make_uint2(0, 0);
-        }
-      }
-      if (jj > 0) {   // V of the previous tile has landed -> publish it
-        cp_async_wait_all();
-        fence_proxy_async();
-        mbar_arrive(bar(B_VF + ((jj - 1) & 1)));
-      }
-      if (jj >= 2) mbar_wait(bar(B_KE + stg), ((jj - 2) >> 1) & 1);
-      const uint32_t kb = sbase + OFF_K + stg * kTileBytes;
-      float c0 = 1.f, s0 = 0.f, c1 = 1.f, s1 = 0.f, c2 = 1.f, s2 = 0.f, c3 = 1.f, s3 = 0.f;
+      const int u = w.t_begin + jj, ks = jj % KST;
+      const TileSeg t = tile_segments(p, w, u);
+      const uint32_t kb = sbase + OFF_K + ks * kTileBytes;
+      mbar_wait(bar(B_KR + ks), (jj / KST) & 1);
+      float2 c01 = make_float2(1.f, 1.f), s01 = make_float2(0.f, 0.f);
+      float2 c23 = c01, s23 = s01;
       int prev = -2;
-#pragma unroll
+#pragma unroll 4
       for (int k = 0; k < 16; ++k) {
         const int r = rgrp * 16 + k;
-        uint32_t olo0 = 0, olo1 = 0, ohi0 = 0, ohi1 = 0;
-        if (pos[k] >= 0) {
-          if (pos[k] == prev + 1) {   // R((p+1) theta) = R(p theta) R(theta)
-            float t;
-            t = c0 * st0.x - s0 * st0.y; s0 = s0 * st0.x + c0 * st0.y; c0 = t;
-            t = c1 * st0.z - s1 * st0.w; s1 = s1 * st0.z + c1 * st0.w; c1 = t;
-            t = c2 * st1.x - s2 * st1.y; s2 = s2 * st1.x + c2 * st1.y; c2 = t;
-            t = c3 * st1.z - s3 * st1.w; s3 = s3 * st1.z + c3 * st1.w; c3 = t;
-          } else {                    // exact table value (fp64-built) at a segment start
-            const float4 a = rope4[(long long)pos[k] * 32 + 2 * c];
-            const float4 b = rope4[(long long)pos[k] * 32 + 2 * c + 1];
-            c0 = a.x; s0 = a.y; c1 = a.z; s1 = a.w; c2 = b.x; s2 = b.y; c3 = b.z; s3 = b.w;
-          }
-          prev = pos[k];
-          const float a0 = bf_lo(lo[k].x), a1 = bf_hi(lo[k].x), a2 = bf_lo(lo[k].y), a3 = bf_hi(lo[k].y);
-          const float b0 = bf_lo(hi[k].x), b1 = bf_hi(hi[k].x), b2 = bf_lo(hi[k].y), b3 = bf_hi(hi[k].y);
-          olo0 = pack_bf16(a0 * c0 - b0 * s0, a1 * c1 - b1 * s1);
-          olo1 = pack_bf16(a2 * c2 - b2 * s2, a3 * c3 - b3 * s3);
-          ohi0 = pack_bf16(a0 * s0 + b0 * c0, a1 * s1 + b1 * c1);
-          ohi1 = pack_bf16(a2 * s2 + b2 * c2, a3 * s3 + b3 * c3);
-        } else {
+        const int pos = seg_pos(t, r);
+        const uint32_t alo = kb + sw128(r, 4 * c), ahi = kb + sw128(r, 64 + 4 * c);
+        if (pos < 0) {       // no key in this row: clear whatever the copy left there
+          sts64(alo, 0, 0);
+          sts64(ahi, 0, 0);
           prev = -2;
+          continue;
         }
-        sts64(kb + sw128(r, 4 * c), olo0, olo1);
-        sts64(kb + sw128(r, 64 + 4 * c), ohi0, ohi1);
+        if (dbg && c == 0) {
+          const int di = (u == 0) ? (r < A ? r : A + p.R + (r - A)) : A + t.phys * 128 + r;
+          p.dbg_pos[di] = pos;
+        }
+        if (pos == prev + 1) {   // R((p+1) theta) = R(p theta) R(theta)
+          const float2 nc01 = __ffma2_rn(c01, cth01, __fmul2_rn(make_float2(-s01.x, -s01.y), sth01));
+          const float2 ns01 = __ffma2_rn(s01, cth01, __fmul2_rn(c01, sth01));
+          const float2 nc23 = __ffma2_rn(c23, cth23, __fmul2_rn(make_float2(-s23.x, -s23.y), sth23));
+          const float2 ns23 = __ffma2_rn(s23, cth23, __fmul2_rn(c23, sth23));
+          c01 = nc01; s01 = ns01; c23 = nc23; s23 = ns23;
+        } else {                 // exact table value (fp64-built) at a segment start
+          const float4 a = rope4[(long long)pos * 32 + 2 * c];
+          const float4 b = rope4[(long long)pos * 32 + 2 * c + 1];
+          c01 = make_float2(a.x, a.z); s01 = make_float2(a.y, a.w);
+          c23 = make_float2(b.x, b.z); s23 = make_float2(b.y, b.w);
+        }
+        prev = pos;
+        const uint2 lo = lds64(alo), hi = lds64(ahi);
+        const float2 a01 = make_float2(bf_lo(lo.x), bf_hi(lo.x)), a23 = make_float2(bf_lo(lo.y), bf_hi(lo.y));
+        const float2 b01 = make_float2(bf_lo(hi.x), bf_hi(hi.x)), b23 = make_float2(bf_lo(hi.y), bf_hi(hi.y));
+        // y_lo = a cos - b sin ; y_hi = a sin + b cos
+        const float2 ylo01 = __ffma2_rn(a01, c01, __fmul2_rn(make_float2(-b01.x, -b01.y), s01));
+        const float2 ylo23 = __ffma2_rn(a23, c23, __fmul2_rn(make_float2(-b23.x, -b23.y), s23));
+        const float2 yhi01 = __ffma2_rn(a01, s01, __fmul2_rn(b01, c01));
+        const float2 yhi23 = __ffma2_rn(a23, s23, __fmul2_rn(b23, c23));
+        sts64(alo, pack_bf16(ylo01.x, ylo01.y), pack_bf16(ylo23.x, ylo23.y));
+        sts64(ahi, pack_bf16(yhi01.x, yhi01.y), pack_bf16(yhi23.x, yhi23.y));
       }
       fence_proxy_async();
-      mbar_arrive(bar(B_KF + stg));
-      if (jj >= 2) mbar_wait(bar(B_VE + stg), ((jj - 2) >> 1) & 1);
-      issue_v(jj);
+      mbar_arrive(bar(B_KF + ks));
     }
-    cp_async_wait_all();
-    fence_proxy_async();
-    mbar_arrive(bar(B_VF + ((n - 1) & 1)));
+  } else if (warp == 12) {
+    // ================================================================ copy warp
+    const __nv_bfloat16* __restrict__ SK = reinterpret_cast<const __nv_bfloat16*>(p.sink_k);
+    const __nv_bfloat16* __restrict__ SV = reinterpret_cast<const __nv_bfloat16*>(p.sink_v);
+    const __nv_bfloat16* __restrict__ XK = reinterpret_cast<const __nv_bfloat16*>(p.self_k);
+    const __nv_bfloat16* __restrict__ XV = reinterpret_cast<const __nv_bfloat16*>(p.self_v);
+    // tile 0 (sink rows [0,A) + self rows [A, A+n_self), zeros elsewhere) with cp.async
+    auto copy_extra = [&](uint32_t dst, const __nv_bfloat16* sink, const __nv_bfloat16* self) {
+#pragma unroll 4
+      for (int it = 0; it < 64; ++it) {
+        const int idx = it * 32 + lane;          // 2048 16-byte chunks
+        const int r = idx >> 4, ch = idx & 15;
+        const __nv_bfloat16* src = nullptr;
+        if (r < A) src = sink + (w.head_row * A + r) * 128;
+        else if (r < A + p.n_self) src = self + (((long long)w.pp * p.n_self + (r - A)) * p.Hkv + w.g) * 128;
+        const uint32_t d = dst + (ch >> 3) * 16384 + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
+        cp_async16(d, src ? (const void*)(src + 8 * ch) : (const void*)sink, src ? 16u : 0u);
+      }
+      cp_async_wait_all();
+      fence_proxy_async();
+      __syncwarp();
+    };
+#pragma unroll 1
+    for (int jj = 0; jj < n; ++jj) {
+      const int u = w.t_begin + jj;
+      int phys = -1;
+      if (u > 0) {
+        phys = w.k0 + u - 1;
+        if (phys >= w.nT) phys -= w.nT;
+      }
+      const int row = (int)(w.head_row * p.R) + phys * 128;
+      const int ks = jj % KST, vs = jj % VST;
+      if (jj >= KST) mbar_wait(bar(B_KE + ks), ((jj - KST) / KST) & 1);
+      const uint32_t kdst = sbase + OFF_K + ks * kTileBytes;
+      if (u == 0) {
+        copy_extra(kdst, SK, XK);
+        if (lane == 0) mbar_arrive(bar(B_KR + ks));
+      } else if (lane == 0) {
+        mbar_arrive_tx(bar(B_KR + ks), kTileBytes);
+        tma_load_2d(kdst, &p.tmap_k, 0, row, bar(B_KR + ks));
+        tma_load_2d(kdst + 16384, &p.tmap_k, 64, row, bar(B_KR + ks));
+      }
+      if (jj >= VST) mbar_wait(bar(B_VE + vs), ((jj - VST) / VST) & 1);
+      const uint32_t vdst = sbase + OFF_V + vs * kTileBytes;
+      if (u == 0) {
+        copy_extra(vdst, SV, XV);
+        if (lane == 0) mbar_arrive(bar(B_VF + vs));
+      } else if (lane == 0) {
+        mbar_arrive_tx(bar(B_VF + vs), kTileBytes);
+        tma_load_2d(vdst, &p.tmap_v, 0, row, bar(B_VF + vs));
+        tma_load_2d(vdst + 16384, &p.tmap_v, 64, row, bar(B_VF + vs));
+      }
+      __syncwarp();
+    }
   } else if (lane == 0) {
-    // ================================================================ MMA issuer
+    // ================================================================ MMA issuer (warp 13)
     constexpr uint32_t IQK = idesc_bf16(128, 128, 0, 0);   // S = Q K^T, both K-major
     constexpr uint32_t IPV = idesc_bf16(128, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
-    auto issue_qk = [&](int qt, int stg) {
-      const uint32_t qa = sbase + OFF_Q + qt * kTileBytes, kb = sbase + OFF_K + stg * kTileBytes;
+    auto issue_qk = [&](int qt, int ks) {
+      const uint32_t qa = sbase + OFF_Q + qt * kTileBytes, kb = sbase + OFF_K + ks * kTileBytes;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
         mma_ss(tmem + qt * 128, sdesc(qa + off, 16, 1024), sdesc(kb + off, 16, 1024), IQK, kk > 0);
       }
     };
-    auto issue_pv = [&](int qt, int stg, bool acc) {
-      const uint32_t vb = sbase + OFF_V + stg * kTileBytes;
+    auto issue_pv = [&](int qt, int vs, bool acc) {
+      const uint32_t vb = sbase + OFF_V + vs * kTileBytes;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)
         mma_ts(tmem + 256 + qt * 128, tmem + qt * 128 + kk * 8, sdesc(vb + kk * 2048, 16384, 1024), IPV,
@@ -593,34 +655,34 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     issue_qk(1, 0); mma_commit(bar(B_S + 1));
     mma_commit(bar(B_KE + 0));
     for (int jj = 0; jj < n; ++jj) {
-      const int stg = jj & 1;
-      mbar_wait(bar(B_VF + stg), (jj >> 1) & 1);
+      const int vs = jj % VST;
+      mbar_wait(bar(B_VF + vs), (jj / VST) & 1);
       for (int qt = 0; qt < 2; ++qt) {
         mbar_wait(bar(B_P + qt), jj & 1);
         tc_fence_after();
-        issue_pv(qt, stg, jj > 0);
+        issue_pv(qt, vs, jj > 0);
         mma_commit(bar(B_O + qt));
-        if (qt == 1) mma_commit(bar(B_VE + stg));
+        if (qt == 1) mma_commit(bar(B_VE + vs));
         if (jj + 1 < n) {
-          const int s2 = (jj + 1) & 1;
+          const int ks = (jj + 1) % KST;
           if (qt == 0) {
-            mbar_wait(bar(B_KF + s2), ((jj + 1) >> 1) & 1);
+            mbar_wait(bar(B_KF + ks), ((jj + 1) / KST) & 1);
             tc_fence_after();
           }
-          issue_qk(qt, s2);
+          issue_qk(qt, ks);
           mma_commit(bar(B_S + qt));
-          if (qt == 1) mma_commit(bar(B_KE + s2));
+          if (qt == 1) mma_commit(bar(B_KE + ks));
         }
       }
     }
-    // drain: the last V-empty commit tracks every MMA of this CTA
-    mbar_wait(bar(B_VE + ((n - 1) & 1)), ((n - 1) >> 1) & 1);
+    // drain: the last V-free commit tracks every MMA of this CTA
+    mbar_wait(bar(B_VE + (n - 1) % VST), ((n - 1) / VST) & 1);
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 12) {
+  if (warp == 13) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
@@ -628,6 +690,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
 }  // namespace tc
 
 int attn_tc_smem_bytes() { return tc::kSmemBytes; }
+
+cudaError_t make_ring_tmap(CUtensorMap* map, void* base, unsigned long long rows) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || fn == nullptr) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    encode = reinterpret_cast<Encode>(fn);
+  }
+  const cuuint64_t dims[2] = {128, rows};
+  const cuuint64_t strides[1] = {128 * 2};
+  const cuuint32_t box[2] = {64, 128};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
 
 cudaError_t launch_attn_tc(const AttnParams& p, cudaStream_t st) {
   static bool configured = false;

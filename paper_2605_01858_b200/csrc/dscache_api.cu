@@ -77,6 +77,7 @@ struct dscache_s {
   int poison = 0;
   int impl_build = DSCACHE_IMPL_SIMT, impl_attend = DSCACHE_IMPL_SIMT;
   int num_sms = 148;
+  CUtensorMap tmap_k{}, tmap_v{};
   // profiling
   int prof = 0;
   struct Ev { cudaEvent_t a, b; int kind; };
@@ -136,6 +137,7 @@ void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c.head_dim));
   p.dtype = c.dtype;
   p.dbg_M = std::max(h->C, c.max_query_tokens);
+  p.tmap_k = h->tmap_k; p.tmap_v = h->tmap_v;
   p.n_splits = 1; p.tiles_per_split = 1 << 30;
 }
 
@@ -240,6 +242,11 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   if (e == cudaSuccess) e = cudaMemset(h->sink_k, 0, sink_bytes);
   if (e == cudaSuccess) e = cudaMemset(h->sink_v, 0, sink_bytes);
   if (e == cudaSuccess) e = dsc::launch_rope_table(h->rope, h->npos, c.head_dim, c.rope_theta, 0);
+  if (e == cudaSuccess && (h->impl_build == DSCACHE_IMPL_TC || h->impl_attend == DSCACHE_IMPL_TC)) {
+    const unsigned long long rows = (unsigned long long)heads * h->R;
+    e = dsc::make_ring_tmap(&h->tmap_k, h->ring_k, rows);
+    if (e == cudaSuccess) e = dsc::make_ring_tmap(&h->tmap_v, h->ring_v, rows);
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     std::string m = cudaGetErrorString(e);

@@ -2,6 +2,7 @@
 // the sm_100a kernels.  Product code only; nothing here is visible through the ABI.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace dsc {
@@ -46,6 +47,9 @@ struct AttnParams {
   // debug export (K7); null = off
   int* dbg_pos; int dbg_M;
   int dtype;                                 // 0 bf16, 1 fp32
+  // TMA descriptors of the K / V rings viewed as [S*N*Hkv*R rows][128] bf16, box 64 x 128, SW128
+  CUtensorMap tmap_k;
+  CUtensorMap tmap_v;
 };
 
 struct AppendParams {
@@ -66,5 +70,7 @@ cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t st);
 cudaError_t launch_attn_tc(const AttnParams& p, cudaStream_t st);
 cudaError_t launch_combine(const AttnParams& p, cudaStream_t st);
 int attn_tc_smem_bytes();
+// encode the 2-D ring tensor map (bf16, d = 128) used by the tcgen05 kernel
+cudaError_t make_ring_tmap(CUtensorMap* map, void* base, unsigned long long rows);
 
 }  // namespace dsc

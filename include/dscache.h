@@ -169,6 +169,14 @@ dscache_status dscache_copy_sink(dscache_t h, int32_t stream_idx, int32_t layer,
 dscache_status dscache_set_debug(dscache_t h, int32_t* build_pos, int32_t* attend_pos, int32_t poison);
 int32_t        dscache_debug_len(dscache_t h);
 
+/* Per-CTA event timeline of the tcgen05 attention kernel (profiling aid).  buf: DEVICE
+ * int64 buffer of ntrace_cta * 16 * 64 entries (NULL = off): for the first ntrace_cta
+ * CTAs of each launch, clock64() at [cta][event][tile] for events 0 K tile issued,
+ * 1 V tile issued, 2 raw K landed, 3 rotated K seen by the MMA issuer, 4/5 S0/S1 seen
+ * by softmax, 6/7 P0/P1 written, 8/9 PV0/PV1 issued, 10 Q ready, 11 CTA start,
+ * 12 CTA end (tile index 0 for 10-12); tiles >= 64 are not recorded. */
+dscache_status dscache_set_trace(dscache_t h, int64_t* buf, int32_t ntrace_cta);
+
 /* Profiling: when enabled, every attention/combine kernel launch is bracketed by
  * CUDA events on the caller's stream; read accumulates the device time (ms) and
  * launch counts since the last reset, per kind (0 = build_instant, 1 = attend).

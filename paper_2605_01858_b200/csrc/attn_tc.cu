@@ -9,14 +9,23 @@
 // query rows (2 x 128-row Q tiles) that share it.  Softmax a_ij =
 // softmax(Q_i K_j / sqrt(d)) in the exp2 domain with lazy rescale.
 //
-// CTA = 14 warps:
+// Persistent CTAs (grid <= #SMs) walk a longest-first list of work items
+// (problem, kv head, 256-row m-block, key split); every pipeline phase runs on a
+// CTA-global tile counter, Q and O are recycled across items by barriers.
+//
+// CTA = 16 warps:
 //   warps 0-3  softmax of Q tile 0 (thread = query row = TMEM lane)
 //   warps 4-7  softmax of Q tile 1
-//   warps 8-11 rotation: Q (LDG -> rotate -> STS) once; then every raw K tile
-//              in place in shared memory (LDS -> rotate -> STS), R(p+1) = R(p)R(1)
-//   warp 12    copy: raw K and V tiles -> SW128 smem; TMA (2 x 64x128 boxes) for
-//              ring tiles, cp.async for the sink/self tile
-//   warp 13    TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 8-11 rotation: per item Q (cp.async raw -> rotate in place), then every
+//              raw K tile in place in shared memory (LDS -> rotate -> STS), with
+//              R(p+1) = R(p) R(1) between consecutive ids
+//   warp 12    K copy: raw K tiles -> SW128 smem; TMA (2 x 64x128 boxes) for ring
+//              tiles, cp.async for the sink/self tile
+//   warp 13    V copy: same for V (K and V stage recycling is independent)
+//   warp 14    TMEM allocator + single-thread tcgen05.mma issuer
+//   warp 15    idle
+// Softmax reads each S row from TMEM in two 64-column halves (max pass, then
+// exp pass); registers (setmaxnreg): softmax 144, rotation 136, copy/MMA 88.
 // TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512);
 // P_qt (bf16x2) overwrites S_qt cols [0,64) and feeds O_qt += P V as the TMEM A operand.
 // MMA issue order S0_0 S1_0 | PV0_j S0_{j+1} PV1_j S1_{j+1} | ... so each softmax
@@ -30,7 +39,7 @@ namespace dsc {
 namespace tc {
 
 constexpr int kNQT = 2;                       // Q tiles per CTA
-constexpr int kWarps = 14;
+constexpr int kWarps = 16;
 constexpr int kThreads = kWarps * 32;
 constexpr int kTileBytes = 128 * 128 * 2;     // one 128 x 128 bf16 tile
 constexpr int KST = 3;                        // K stages (raw -> rotated in place)
@@ -39,8 +48,13 @@ constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + kNQT * kTileBytes;
 constexpr int OFF_V = OFF_K + KST * kTileBytes;
 constexpr int OFF_BAR = OFF_V + VST * kTileBytes;
-// barriers (8 B each): Q | K raw landed | K rotated | K free | V landed | V free | S | P | O
-constexpr int B_Q = 0, B_KR = 1, B_KF = 4, B_KE = 7, B_VF = 10, B_VE = 12, B_S = 14, B_P = 16, B_O = 18, B_N = 20;
+// barriers (8 B each): Q ready | Q free | K raw landed | K rotated | K free | V landed | V free |
+// S ready | P ready | O done | O read (epilogue done)
+constexpr int B_Q = 0, B_QE = 1, B_KR = 2, B_KF = 5, B_KE = 8, B_VF = 11, B_VE = 13, B_S = 15, B_P = 17, B_O = 19,
+              B_OF = 21, B_N = 23;
+// setmaxnreg budget per warpgroup: 2*144 (softmax) + 136 (rotation) + 88 (copy/MMA) = 512 x 128 threads
+constexpr int kRegSoftmax = 144, kRegRotate = 136, kRegCopy = 88;
+static_assert(2 * kRegSoftmax + kRegRotate + kRegCopy <= 512, "setmaxnreg budget exceeds the 64K register file");
 constexpr int kSmemBytes = OFF_BAR + B_N * 8 + 16 + 1024;   // + tmem slot + alignment slack
 constexpr float kRescaleThreshold = 8.0f;     // log2 units (factor 256)
 
@@ -216,7 +230,15 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
 }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-struct Work {
+// timeline events (TRACE): clock64 per (event, tile) for the first ntrace_cta CTAs
+enum { EV_K_ISSUE = 0, EV_V_ISSUE, EV_KR, EV_KF, EV_S0, EV_S1, EV_P0, EV_P1, EV_PV0, EV_PV1, EV_Q, EV_START, EV_END };
+#define TRACE(ev, tile)                                                                                  \
+  do {                                                                                                   \
+    if (p.trace && blockIdx.x < (unsigned)p.ntrace_cta && (tile) < kTraceTiles)                          \
+      p.trace[((long long)blockIdx.x * kTraceEvents + (ev)) * kTraceTiles + (tile)] = clock64();          \
+  } while (0)
+
+struct Item {
   int pp, g, mb, sp;
   long long head_row;
   int m0, rows_total;
@@ -225,13 +247,16 @@ struct Work {
   int t_begin, n_tiles;
 };
 
-__device__ __forceinline__ Work decode_work(const AttnParams& p) {
-  Work w;
-  int x = blockIdx.x;
-  w.sp = x % p.n_splits; x /= p.n_splits;
-  w.mb = p.n_mblocks - 1 - (x % p.n_mblocks); x /= p.n_mblocks;   // longest (causal) m-blocks first
-  w.g = x % p.Hkv;
-  w.pp = x / p.Hkv;
+// work item idx -> (split fastest, then problem x kv head, then m-block descending):
+// all (problem, head) pairs of the longest causal m-block come first.
+__device__ __forceinline__ Item decode_item(const AttnParams& p, int idx) {
+  Item w;
+  w.sp = idx % p.n_splits;
+  const int rest = idx / p.n_splits;
+  const int ph = rest % (p.P * p.Hkv);
+  w.mb = p.n_mblocks - 1 - rest / (p.P * p.Hkv);
+  w.g = ph % p.Hkv;
+  w.pp = ph / p.Hkv;
   const int s = w.pp / p.layer_count, l = w.pp % p.layer_count;
   w.head_row = ((long long)s * p.N_total + p.layer_begin + l) * p.Hkv + w.g;
   w.rows_total = p.n_q * p.grp;
@@ -262,7 +287,7 @@ struct TileSeg {
   int phys;           // physical ring tile (u > 0), -1 for tile 0
 };
 
-__device__ __forceinline__ TileSeg tile_segments(const AttnParams& p, const Work& w, int u) {
+__device__ __forceinline__ TileSeg tile_segments(const AttnParams& p, const Item& w, int u) {
   TileSeg t;
   if (u == 0) {
     t.lo0 = 0; t.hi0 = p.A; t.pos0_0 = 0;
@@ -285,6 +310,80 @@ __device__ __forceinline__ int seg_pos(const TileSeg& t, int r) {
   return -1;
 }
 
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr) : "memory");
+  return r;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ float2 bf2(uint32_t w) { return make_float2(bf_lo(w), bf_hi(w)); }
+__device__ __forceinline__ uint32_t get_w(const uint4& v, int j) { return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w; }
+
+// In-place RoPE of 8 rows x 8 frequencies (f = 8*c8 .. 8*c8+7: 16-byte chunk c8 of the
+// low and of the high 64-column block) of a SW128 bf16 tile in smem.  Row k gets
+// id pos[k] (-1 = clear the row).  All 16 chunks are loaded first (ILP); between
+// consecutive ids the (cos, sin) advance by R(theta) (id + 1) or stay (same id),
+// any other jump reloads the fp64-built pair table rp[id][32].
+__device__ __forceinline__ void rotate8(uint32_t tile, int r0, int c8, const float4* __restrict__ rp,
+                                        const float2 (&cth)[4], const float2 (&sth)[4], const int (&pos)[8]) {
+  float2 cs[4], sn[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) { cs[j] = make_float2(1.f, 1.f); sn[j] = make_float2(0.f, 0.f); }
+  int prev = -2;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint4 lo[4], hi[4];
+    uint32_t addr[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = r0 + half * 4 + k;
+      addr[k] = tile + r * 128 + ((c8 ^ (r & 7)) << 4);
+      lo[k] = lds128(addr[k]);
+      hi[k] = lds128(addr[k] + 16384);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int pk = pos[half * 4 + k];
+      uint4 ylo = make_uint4(0, 0, 0, 0), yhi = make_uint4(0, 0, 0, 0);
+      if (pk >= 0) {
+        if (pk == prev + 1) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 nc = __ffma2_rn(cs[j], cth[j], __fmul2_rn(make_float2(-sn[j].x, -sn[j].y), sth[j]));
+            sn[j] = __ffma2_rn(sn[j], cth[j], __fmul2_rn(cs[j], sth[j]));
+            cs[j] = nc;
+          }
+        } else if (pk != prev) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 t = rp[(long long)pk * 32 + 4 * c8 + j];
+            cs[j] = make_float2(t.x, t.y);
+            sn[j] = make_float2(t.z, t.w);
+          }
+        }
+        prev = pk;
+        uint32_t ol[4], oh[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 av = bf2(get_w(lo[k], j)), bv = bf2(get_w(hi[k], j));
+          const float2 yl = __ffma2_rn(av, cs[j], __fmul2_rn(make_float2(-bv.x, -bv.y), sn[j]));   // a cos - b sin
+          const float2 yh = __ffma2_rn(av, sn[j], __fmul2_rn(bv, cs[j]));                        // a sin + b cos
+          ol[j] = pack_bf16(yl.x, yl.y);
+          oh[j] = pack_bf16(yh.x, yh.y);
+        }
+        ylo = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+        yhi = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+      } else {
+        prev = -2;
+      }
+      sts128(addr[k], ylo);
+      sts128(addr[k] + 16384, yhi);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -295,10 +394,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + B_N * 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Work w = decode_work(p);
+  const int n_items = p.n_mblocks * p.P * p.Hkv * p.n_splits;
 
   if (threadIdx.x == 0) {
     mbar_init(bar(B_Q), 128);
+    mbar_init(bar(B_QE), 1);
     for (int i = 0; i < KST; ++i) {
       mbar_init(bar(B_KR + i), 1);
       mbar_init(bar(B_KF + i), 128);
@@ -312,16 +412,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       mbar_init(bar(B_S + i), 1);
       mbar_init(bar(B_P + i), 128);
       mbar_init(bar(B_O + i), 1);
+      mbar_init(bar(B_OF + i), 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
   }
-  if (warp == 13) {
+  if (warp == 14) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (warp == 12 && lane == 0) {
+    TRACE(EV_START, 0);
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_k)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_v)) : "memory");
   }
@@ -329,360 +431,359 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int n = w.n_tiles;
   const int A = p.A;
 
   if (warp < 8) {
     // ================================================================ softmax
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
     const int qt = warp >> 2, quarter = warp & 3;
     const int rloc = quarter * 32 + lane;
-    const int rglob = w.m0 + qt * 128 + rloc;
-    const bool valid_row = rglob < w.rows_total;
-    const int qi = valid_row ? rglob / p.grp : 0;
-    const int lim = valid_row ? p.q_pos0 + qi : -1;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const uint32_t tS = tmem + lane_off + (uint32_t)(qt * 128);
     const uint32_t tO = tmem + lane_off + (uint32_t)(256 + qt * 128);
     const float sl2 = p.scale_log2;
     const float2 scale2 = make_float2(sl2, sl2);
-    float m = -INFINITY;
-    float2 lsum2 = make_float2(0.f, 0.f);
-    for (int jj = 0; jj < n; ++jj) {
-      const int u = w.t_begin + jj;
-      int c_lo, c_hi;
-      if (!valid_row) {
-        c_lo = 0; c_hi = 0;
-      } else if (u == 0) {
-        c_lo = 0;
-        c_hi = min(A + p.n_self, max(A, lim - p.ring_count + 1));
-      } else {
-        const TileSeg t = tile_segments(p, w, u);
-        c_lo = t.lo0;
-        // key at column c has id pos0 + c; visible iff id <= lim
-        c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));
-      }
-      const bool full = (c_lo == 0) && (c_hi == 128);
-      mbar_wait(bar(B_S + qt), jj & 1);
-      tc_fence_after();
-      // pass 1: row max over the visible columns
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t r[32];
-        tmem_ld32(tS + ch * 32, r);
-        tmem_wait_ld();
-        if (full) {
-#pragma unroll
-          for (int c = 0; c < 32; c += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(r[c]), __uint_as_float(r[c + 1])));
+    int gt = 0, kk = 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
+      const Item w = decode_item(p, idx);
+      const int n = w.n_tiles;
+      const int rglob = w.m0 + qt * 128 + rloc;
+      const bool valid_row = rglob < w.rows_total;
+      const int qi = valid_row ? rglob / p.grp : 0;
+      const int lim = valid_row ? p.q_pos0 + qi : -1;
+      float m = -INFINITY;
+      float2 lsum2 = make_float2(0.f, 0.f);
+      for (int jj = 0; jj < n; ++jj) {
+        const int g = gt + jj;
+        const int u = w.t_begin + jj;
+        int c_lo, c_hi;
+        if (!valid_row) {
+          c_lo = 0; c_hi = 0;
+        } else if (u == 0) {
+          c_lo = 0;
+          c_hi = min(A + p.n_self, max(A, lim - p.ring_count + 1));
         } else {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int col = ch * 32 + c;
-            if (col >= c_lo && col < c_hi) mx = fmaxf(mx, __uint_as_float(r[c]));
-          }
+          const TileSeg t = tile_segments(p, w, u);
+          c_lo = t.lo0;
+          c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));   // id pos0 + c <= lim
         }
-      }
-      const float m_tile = mx * sl2;
-      // lazy rescale: move the running max only when it grew by > 2^8; the TMEM
-      // load/store of O is warp-collective, so the decision is made per warp.
-      const bool upd = m_tile > m + kRescaleThreshold;
-      const bool need_o = upd && (m != -INFINITY);
-      const float f = need_o ? ex2(m - m_tile) : 1.f;
-      if (upd) {
-        lsum2.x *= f; lsum2.y *= f;
-        m = m_tile;
-      }
-      if (__any_sync(0xffffffffu, need_o)) {
-        // O_qt holds PV up to tile jj-1: wait for it, rescale in TMEM
-        mbar_wait(bar(B_O + qt), (jj - 1) & 1);
+        const bool full = (c_lo == 0) && (c_hi == 128);
+        mbar_wait(bar(B_S + qt), g & 1);
+        if (rloc == 0) TRACE(EV_S0 + qt, g);
         tc_fence_after();
+        // pass 1: row max over the visible columns, two 64-column halves
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t r[32];
-          tmem_ld32(tO + ch * 32, r);
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t r[64];
+          tmem_ld32(tS + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
           tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < 32; ++c) r[c] = __float_as_uint(__uint_as_float(r[c]) * f);
-          tmem_st32(tO + ch * 32, r);
-        }
-        tmem_wait_st();
-      }
-      const float m_use = (m == -INFINITY) ? 0.f : m;
-      const float2 negm2 = make_float2(-m_use, -m_use);
-      // pass 2: P = 2^(s*scale - m) -> bf16x2 into S cols [0,64)
-#pragma unroll 1
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t r[32];
-        tmem_ld32(tS + ch * 32, r);
-        tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
-          float p0 = ex2(x.x), p1 = ex2(x.y);
           if (!full) {
-            const int col = ch * 32 + c;
-            p0 = (col >= c_lo && col < c_hi) ? p0 : 0.f;
-            p1 = (col + 1 >= c_lo && col + 1 < c_hi) ? p1 : 0.f;
+#pragma unroll
+            for (int c = 0; c < 64; ++c)
+              if (64 * hf + c < c_lo || 64 * hf + c >= c_hi) r[c] = 0xFF800000u;   // -inf
           }
-          lsum2 = __fadd2_rn(lsum2, make_float2(p0, p1));
-          pk[c >> 1] = pack_bf16(p0, p1);
+#pragma unroll
+          for (int c = 0; c < 64; c += 4) {
+            mx0 = fmaxf(mx0, __uint_as_float(r[c]));
+            mx1 = fmaxf(mx1, __uint_as_float(r[c + 1]));
+            mx2 = fmaxf(mx2, __uint_as_float(r[c + 2]));
+            mx3 = fmaxf(mx3, __uint_as_float(r[c + 3]));
+          }
         }
-        tmem_st16(tS + ch * 16, pk);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(bar(B_P + qt));
-    }
-    // epilogue
-    const float lsum = lsum2.x + lsum2.y;
-    mbar_wait(bar(B_O + qt), (n - 1) & 1);
-    tc_fence_after();
-    const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
-    const int h = valid_row ? w.g * p.grp + rglob % p.grp : 0;
-    const long long orow = ((long long)w.pp * p.n_q + qi) * p.Hq + h;
+        const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+        // lazy rescale: move the running max only when it grew by > 2^8; the TMEM
+        // load/store of O is warp-collective, so the decision is made per warp.
+        const bool upd = m_tile > m + kRescaleThreshold;
+        const bool need_o = upd && (m != -INFINITY);
+        const float f = need_o ? ex2(m - m_tile) : 1.f;
+        if (upd) {
+          lsum2.x *= f; lsum2.y *= f;
+          m = m_tile;
+        }
+        if (__any_sync(0xffffffffu, need_o)) {
+          // O_qt holds PV up to the previous tile: wait for it, rescale in TMEM
+          mbar_wait(bar(B_O + qt), (g - 1) & 1);
+          tc_fence_after();
 #pragma unroll 1
-    for (int ch = 0; ch < 4; ++ch) {
-      uint32_t r[32];
-      tmem_ld32(tO + ch * 32, r);
-      tmem_wait_ld();
-      if (!valid_row) continue;
-      if (p.n_splits == 1) {
-        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) + orow * 128 + ch * 32);
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t o[32];
+            tmem_ld32(tO + ch * 32, o);
+            tmem_wait_ld();
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 o;
-          o.x = pack_bf16(__uint_as_float(r[8 * v + 0]) * inv, __uint_as_float(r[8 * v + 1]) * inv);
-          o.y = pack_bf16(__uint_as_float(r[8 * v + 2]) * inv, __uint_as_float(r[8 * v + 3]) * inv);
-          o.z = pack_bf16(__uint_as_float(r[8 * v + 4]) * inv, __uint_as_float(r[8 * v + 5]) * inv);
-          o.w = pack_bf16(__uint_as_float(r[8 * v + 6]) * inv, __uint_as_float(r[8 * v + 7]) * inv);
-          dst[v] = o;
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+            tmem_st32(tO + ch * 32, o);
+          }
+          tmem_wait_st();
         }
-      } else {
-        const long long rows = (long long)p.P * p.n_q * p.Hq;
-        float4* dst = reinterpret_cast<float4*>(p.ws_o + ((long long)w.sp * rows + orow) * 128 + ch * 32);
+        const float m_use = (m == -INFINITY) ? 0.f : m;
+        const float2 negm2 = make_float2(-m_use, -m_use);
+        // pass 2: P = 2^(s*scale - m) (masked -> 2^-inf = 0), packed bf16x2; half hf of S
+        // (cols 64hf..64hf+63) becomes P cols 32hf..32hf+31 (already consumed S columns)
+        float2 l0 = make_float2(0.f, 0.f), l1 = l0;
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t r[64];
+          tmem_ld32(tS + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          tmem_wait_ld();
+          if (!full) {
 #pragma unroll
-        for (int v = 0; v < 8; ++v)
-          dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv, __uint_as_float(r[4 * v + 1]) * inv,
-                               __uint_as_float(r[4 * v + 2]) * inv, __uint_as_float(r[4 * v + 3]) * inv);
-        if (ch == 0)
-          p.ws_lse[(long long)w.sp * rows + orow] = lsum > 0.f ? m + __log2f(lsum) : -INFINITY;
+            for (int c = 0; c < 64; ++c)
+              if (64 * hf + c < c_lo || 64 * hf + c >= c_hi) r[c] = 0xFF800000u;
+          }
+#pragma unroll
+          for (int c = 0; c < 64; c += 4) {
+            const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+            const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
+            const float2 p0 = make_float2(ex2(x0.x), ex2(x0.y));
+            const float2 p1 = make_float2(ex2(x1.x), ex2(x1.y));
+            l0 = __fadd2_rn(l0, p0);
+            l1 = __fadd2_rn(l1, p1);
+            r[c >> 1] = pack_bf16(p0.x, p0.y);
+            r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
+          }
+          tmem_st32(tS + 32 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        }
+        lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bar(B_P + qt));
+        if (rloc == 0) TRACE(EV_P0 + qt, g);
+      }
+      gt += n;
+      // epilogue of the item
+      const float lsum = lsum2.x + lsum2.y;
+      mbar_wait(bar(B_O + qt), (gt - 1) & 1);
+      tc_fence_after();
+      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+      const int h = valid_row ? w.g * p.grp + rglob % p.grp : 0;
+      const long long orow = ((long long)w.pp * p.n_q + qi) * p.Hq + h;
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t o[64];
+        tmem_ld32(tO + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+        tmem_ld32(tO + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+        tmem_wait_ld();
+        if (hf == 1) {
+          tc_fence_before();
+          mbar_arrive(bar(B_OF + qt));      // O_qt may be overwritten by the next item
+        }
+        if (!valid_row) continue;
+        if (p.n_splits == 1) {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) + orow * 128 + 64 * hf);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            uint4 q;
+            q.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
+            q.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
+            q.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
+            q.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
+            dst[v] = q;
+          }
+        } else {
+          const long long rows = (long long)p.P * p.n_q * p.Hq;
+          float4* dst = reinterpret_cast<float4*>(p.ws_o + ((long long)w.sp * rows + orow) * 128 + 64 * hf);
+#pragma unroll
+          for (int v = 0; v < 16; ++v)
+            dst[v] = make_float4(__uint_as_float(o[4 * v]) * inv, __uint_as_float(o[4 * v + 1]) * inv,
+                                 __uint_as_float(o[4 * v + 2]) * inv, __uint_as_float(o[4 * v + 3]) * inv);
+          if (hf == 0) p.ws_lse[(long long)w.sp * rows + orow] = lsum > 0.f ? m + __log2f(lsum) : -INFINITY;
+        }
       }
     }
   } else if (warp < 12) {
-    // ================================================================ rotation (Q once, then K tiles)
+    // ================================================================ rotation (Q per item, then K tiles)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegRotate));   // 136 > 128 at launch
     const int lt = threadIdx.x - 256;
-    const int c = lt & 15;             // frequency chunk: freqs 4c..4c+3 (elements 4c.. and 64+4c..)
-    const int rgrp = lt >> 4;          // 0..7
+    const int c8 = lt & 7;             // frequencies 8*c8 .. 8*c8+7
+    const int rg8 = lt >> 3;           // rows rg8*8 .. +7 of a 128-row tile
     const __nv_bfloat16* __restrict__ Qg = reinterpret_cast<const __nv_bfloat16*>(p.q);
-    const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
-    const float4* __restrict__ rope4 = reinterpret_cast<const float4*>(p.rope);   // [pos][32] float4
-    // ---- Q: 256 rows, thread rows rgrp*32 .. +31, rotated at the query id (table values)
-#pragma unroll 1
-    for (int rb = 0; rb < 32; rb += 8) {
-      uint2 lo[8], hi[8];
-      int pos[8];
+    const float4* __restrict__ rp = p.rope_pairs;
+    float2 cth[4], sth[4];             // R(theta_f) = table entry of id 1
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int r = rgrp * 32 + rb + k;
-        const int rg = w.m0 + r;
-        pos[k] = -1;
-        lo[k] = make_uint2(0, 0); hi[k] = make_uint2(0, 0);
-        if (rg < w.rows_total) {
-          const int i = rg / p.grp, h = w.g * p.grp + rg % p.grp;
-          const __nv_bfloat16* src = Qg + (((long long)w.pp * p.n_q + i) * p.Hq + h) * 128;
-          lo[k] = ldg64(src + 4 * c);
-          hi[k] = ldg64(src + 64 + 4 * c);
-          pos[k] = p.q_pos0 + i;
-          if (dbg && c == 0 && (rg % p.grp) == 0) p.dbg_pos[A + p.R + p.dbg_M + i] = pos[k];
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int r = rgrp * 32 + rb + k;
-        const int qt = r >> 7, rl = r & 127;
-        uint32_t olo0 = 0, olo1 = 0, ohi0 = 0, ohi1 = 0;
-        if (pos[k] >= 0) {
-          const float4 cs0 = rope4[(long long)pos[k] * 32 + 2 * c];
-          const float4 cs1 = rope4[(long long)pos[k] * 32 + 2 * c + 1];
-          const float a0 = bf_lo(lo[k].x), a1 = bf_hi(lo[k].x), a2 = bf_lo(lo[k].y), a3 = bf_hi(lo[k].y);
-          const float b0 = bf_lo(hi[k].x), b1 = bf_hi(hi[k].x), b2 = bf_lo(hi[k].y), b3 = bf_hi(hi[k].y);
-          olo0 = pack_bf16(a0 * cs0.x - b0 * cs0.y, a1 * cs0.z - b1 * cs0.w);
-          olo1 = pack_bf16(a2 * cs1.x - b2 * cs1.y, a3 * cs1.z - b3 * cs1.w);
-          ohi0 = pack_bf16(a0 * cs0.y + b0 * cs0.x, a1 * cs0.w + b1 * cs0.z);
-          ohi1 = pack_bf16(a2 * cs1.y + b2 * cs1.x, a3 * cs1.w + b3 * cs1.z);
-        }
-        const uint32_t qb = sbase + OFF_Q + qt * kTileBytes;
-        sts64(qb + sw128(rl, 4 * c), olo0, olo1);
-        sts64(qb + sw128(rl, 64 + 4 * c), ohi0, ohi1);
-      }
+    for (int j = 0; j < 4; ++j) {
+      const float4 t = rp[32 + 4 * c8 + j];
+      cth[j] = make_float2(t.x, t.y);
+      sth[j] = make_float2(t.z, t.w);
     }
-    fence_proxy_async();
-    mbar_arrive(bar(B_Q));
-
-    // per-thread rotation step R(theta_f), f = 4c..4c+3 (table row of id 1), packed by freq pairs
-    const float4 st0 = rope4[32 + 2 * c], st1 = rope4[32 + 2 * c + 1];
-    const float2 cth01 = make_float2(st0.x, st0.z), sth01 = make_float2(st0.y, st0.w);
-    const float2 cth23 = make_float2(st1.x, st1.z), sth23 = make_float2(st1.y, st1.w);
-#pragma unroll 1
-    for (int jj = 0; jj < n; ++jj) {
-      const int u = w.t_begin + jj, ks = jj % KST;
-      const TileSeg t = tile_segments(p, w, u);
-      const uint32_t kb = sbase + OFF_K + ks * kTileBytes;
-      mbar_wait(bar(B_KR + ks), (jj / KST) & 1);
-      float2 c01 = make_float2(1.f, 1.f), s01 = make_float2(0.f, 0.f);
-      float2 c23 = c01, s23 = s01;
-      int prev = -2;
+    int gt = 0, kk = 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
+      const Item w = decode_item(p, idx);
+      const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
+      // ---- Q of this item: raw rows via cp.async into the Q tiles, then rotate in place
+      if (kk > 0) mbar_wait(bar(B_QE), (kk - 1) & 1);
 #pragma unroll 4
-      for (int k = 0; k < 16; ++k) {
-        const int r = rgrp * 16 + k;
-        const int pos = seg_pos(t, r);
-        const uint32_t alo = kb + sw128(r, 4 * c), ahi = kb + sw128(r, 64 + 4 * c);
-        if (pos < 0) {       // no key in this row: clear whatever the copy left there
-          sts64(alo, 0, 0);
-          sts64(ahi, 0, 0);
-          prev = -2;
-          continue;
-        }
-        if (dbg && c == 0) {
-          const int di = (u == 0) ? (r < A ? r : A + p.R + (r - A)) : A + t.phys * 128 + r;
-          p.dbg_pos[di] = pos;
-        }
-        if (pos == prev + 1) {   // R((p+1) theta) = R(p theta) R(theta)
-          const float2 nc01 = __ffma2_rn(c01, cth01, __fmul2_rn(make_float2(-s01.x, -s01.y), sth01));
-          const float2 ns01 = __ffma2_rn(s01, cth01, __fmul2_rn(c01, sth01));
-          const float2 nc23 = __ffma2_rn(c23, cth23, __fmul2_rn(make_float2(-s23.x, -s23.y), sth23));
-          const float2 ns23 = __ffma2_rn(s23, cth23, __fmul2_rn(c23, sth23));
-          c01 = nc01; s01 = ns01; c23 = nc23; s23 = ns23;
-        } else {                 // exact table value (fp64-built) at a segment start
-          const float4 a = rope4[(long long)pos * 32 + 2 * c];
-          const float4 b = rope4[(long long)pos * 32 + 2 * c + 1];
-          c01 = make_float2(a.x, a.z); s01 = make_float2(a.y, a.w);
-          c23 = make_float2(b.x, b.z); s23 = make_float2(b.y, b.w);
-        }
-        prev = pos;
-        const uint2 lo = lds64(alo), hi = lds64(ahi);
-        const float2 a01 = make_float2(bf_lo(lo.x), bf_hi(lo.x)), a23 = make_float2(bf_lo(lo.y), bf_hi(lo.y));
-        const float2 b01 = make_float2(bf_lo(hi.x), bf_hi(hi.x)), b23 = make_float2(bf_lo(hi.y), bf_hi(hi.y));
-        // y_lo = a cos - b sin ; y_hi = a sin + b cos
-        const float2 ylo01 = __ffma2_rn(a01, c01, __fmul2_rn(make_float2(-b01.x, -b01.y), s01));
-        const float2 ylo23 = __ffma2_rn(a23, c23, __fmul2_rn(make_float2(-b23.x, -b23.y), s23));
-        const float2 yhi01 = __ffma2_rn(a01, s01, __fmul2_rn(b01, c01));
-        const float2 yhi23 = __ffma2_rn(a23, s23, __fmul2_rn(b23, c23));
-        sts64(alo, pack_bf16(ylo01.x, ylo01.y), pack_bf16(ylo23.x, ylo23.y));
-        sts64(ahi, pack_bf16(yhi01.x, yhi01.y), pack_bf16(yhi23.x, yhi23.y));
-      }
-      fence_proxy_async();
-      mbar_arrive(bar(B_KF + ks));
-    }
-  } else if (warp == 12) {
-    // ================================================================ copy warp
-    const __nv_bfloat16* __restrict__ SK = reinterpret_cast<const __nv_bfloat16*>(p.sink_k);
-    const __nv_bfloat16* __restrict__ SV = reinterpret_cast<const __nv_bfloat16*>(p.sink_v);
-    const __nv_bfloat16* __restrict__ XK = reinterpret_cast<const __nv_bfloat16*>(p.self_k);
-    const __nv_bfloat16* __restrict__ XV = reinterpret_cast<const __nv_bfloat16*>(p.self_v);
-    // tile 0 (sink rows [0,A) + self rows [A, A+n_self), zeros elsewhere) with cp.async
-    auto copy_extra = [&](uint32_t dst, const __nv_bfloat16* sink, const __nv_bfloat16* self) {
-#pragma unroll 4
-      for (int it = 0; it < 64; ++it) {
-        const int idx = it * 32 + lane;          // 2048 16-byte chunks
-        const int r = idx >> 4, ch = idx & 15;
+      for (int it = 0; it < 32; ++it) {
+        const int id = it * 128 + lt;          // 4096 16-byte chunks of 256 rows
+        const int r = id >> 4, ch = id & 15;
+        const int rgl = w.m0 + r;
         const __nv_bfloat16* src = nullptr;
-        if (r < A) src = sink + (w.head_row * A + r) * 128;
-        else if (r < A + p.n_self) src = self + (((long long)w.pp * p.n_self + (r - A)) * p.Hkv + w.g) * 128;
-        const uint32_t d = dst + (ch >> 3) * 16384 + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
-        cp_async16(d, src ? (const void*)(src + 8 * ch) : (const void*)sink, src ? 16u : 0u);
+        if (rgl < w.rows_total)
+          src = Qg + (((long long)w.pp * p.n_q + rgl / p.grp) * p.Hq + w.g * p.grp + rgl % p.grp) * 128;
+        const uint32_t d = sbase + OFF_Q + (r >> 7) * kTileBytes + (ch >> 3) * 16384 + (r & 127) * 128 +
+                           (((ch & 7) ^ (r & 7)) << 4);
+        cp_async16(d, src ? (const void*)(src + 8 * ch) : (const void*)Qg, src ? 16u : 0u);
       }
       cp_async_wait_all();
-      fence_proxy_async();
-      __syncwarp();
-    };
+      named_bar(1, 128);
 #pragma unroll 1
-    for (int jj = 0; jj < n; ++jj) {
-      const int u = w.t_begin + jj;
-      int phys = -1;
-      if (u > 0) {
-        phys = w.k0 + u - 1;
-        if (phys >= w.nT) phys -= w.nT;
-      }
-      const int row = (int)(w.head_row * p.R) + phys * 128;
-      const int ks = jj % KST, vs = jj % VST;
-      if (jj >= KST) mbar_wait(bar(B_KE + ks), ((jj - KST) / KST) & 1);
-      const uint32_t kdst = sbase + OFF_K + ks * kTileBytes;
-      if (u == 0) {
-        copy_extra(kdst, SK, XK);
-        if (lane == 0) mbar_arrive(bar(B_KR + ks));
-      } else if (lane == 0) {
-        mbar_arrive_tx(bar(B_KR + ks), kTileBytes);
-        tma_load_2d(kdst, &p.tmap_k, 0, row, bar(B_KR + ks));
-        tma_load_2d(kdst + 16384, &p.tmap_k, 64, row, bar(B_KR + ks));
-      }
-      if (jj >= VST) mbar_wait(bar(B_VE + vs), ((jj - VST) / VST) & 1);
-      const uint32_t vdst = sbase + OFF_V + vs * kTileBytes;
-      if (u == 0) {
-        copy_extra(vdst, SV, XV);
-        if (lane == 0) mbar_arrive(bar(B_VF + vs));
-      } else if (lane == 0) {
-        mbar_arrive_tx(bar(B_VF + vs), kTileBytes);
-        tma_load_2d(vdst, &p.tmap_v, 0, row, bar(B_VF + vs));
-        tma_load_2d(vdst + 16384, &p.tmap_v, 64, row, bar(B_VF + vs));
-      }
-      __syncwarp();
-    }
-  } else if (lane == 0) {
-    // ================================================================ MMA issuer (warp 13)
-    constexpr uint32_t IQK = idesc_bf16(128, 128, 0, 0);   // S = Q K^T, both K-major
-    constexpr uint32_t IPV = idesc_bf16(128, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
-    auto issue_qk = [&](int qt, int ks) {
-      const uint32_t qa = sbase + OFF_Q + qt * kTileBytes, kb = sbase + OFF_K + ks * kTileBytes;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-        mma_ss(tmem + qt * 128, sdesc(qa + off, 16, 1024), sdesc(kb + off, 16, 1024), IQK, kk > 0);
-      }
-    };
-    auto issue_pv = [&](int qt, int vs, bool acc) {
-      const uint32_t vb = sbase + OFF_V + vs * kTileBytes;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        mma_ts(tmem + 256 + qt * 128, tmem + qt * 128 + kk * 8, sdesc(vb + kk * 2048, 16384, 1024), IPV,
-               (acc || kk > 0) ? 1u : 0u);
-    };
-    mbar_wait(bar(B_Q), 0);
-    mbar_wait(bar(B_KF + 0), 0);
-    tc_fence_after();
-    issue_qk(0, 0); mma_commit(bar(B_S + 0));
-    issue_qk(1, 0); mma_commit(bar(B_S + 1));
-    mma_commit(bar(B_KE + 0));
-    for (int jj = 0; jj < n; ++jj) {
-      const int vs = jj % VST;
-      mbar_wait(bar(B_VF + vs), (jj / VST) & 1);
       for (int qt = 0; qt < 2; ++qt) {
-        mbar_wait(bar(B_P + qt), jj & 1);
-        tc_fence_after();
-        issue_pv(qt, vs, jj > 0);
-        mma_commit(bar(B_O + qt));
-        if (qt == 1) mma_commit(bar(B_VE + vs));
-        if (jj + 1 < n) {
-          const int ks = (jj + 1) % KST;
-          if (qt == 0) {
-            mbar_wait(bar(B_KF + ks), ((jj + 1) / KST) & 1);
-            tc_fence_after();
+        const int row0 = w.m0 + qt * 128 + rg8 * 8;       // global row of the first of the 8 rows
+        int i = row0 / p.grp, hh = row0 % p.grp;
+        int pos[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          pos[k] = (row0 + k < w.rows_total) ? p.q_pos0 + i : -1;
+          if (dbg && c8 == 0 && hh == 0 && pos[k] >= 0) p.dbg_pos[A + p.R + p.dbg_M + i] = pos[k];
+          if (++hh == p.grp) { hh = 0; ++i; }
+        }
+        rotate8(sbase + OFF_Q + qt * kTileBytes, rg8 * 8, c8, rp, cth, sth, pos);
+      }
+      fence_proxy_async();
+      mbar_arrive(bar(B_Q));
+      // ---- K tiles of this item
+      for (int jj = 0; jj < w.n_tiles; ++jj) {
+        const int g = gt + jj, u = w.t_begin + jj, ks = g % KST;
+        const TileSeg t = tile_segments(p, w, u);
+        int pos[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pos[k] = seg_pos(t, rg8 * 8 + k);
+        mbar_wait(bar(B_KR + ks), (g / KST) & 1);
+        if (lt == 0) TRACE(EV_KR, g);
+        rotate8(sbase + OFF_K + ks * kTileBytes, rg8 * 8, c8, rp, cth, sth, pos);
+        fence_proxy_async();
+        mbar_arrive(bar(B_KF + ks));
+        if (dbg && c8 == 0) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int r = rg8 * 8 + k;
+            if (pos[k] >= 0) p.dbg_pos[(u == 0) ? (r < A ? r : A + p.R + (r - A)) : A + t.phys * 128 + r] = pos[k];
           }
-          issue_qk(qt, ks);
-          mma_commit(bar(B_S + qt));
-          if (qt == 1) mma_commit(bar(B_KE + ks));
         }
       }
+      gt += w.n_tiles;
     }
-    // drain: the last V-free commit tracks every MMA of this CTA
-    mbar_wait(bar(B_VE + (n - 1) % VST), ((n - 1) / VST) & 1);
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCopy));
+    if (warp == 12 || warp == 13) {
+      // ============================================================== copy warps (12: K, 13: V)
+      const bool isk = warp == 12;
+      const __nv_bfloat16* __restrict__ SX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.sink_k : p.sink_v);
+      const __nv_bfloat16* __restrict__ XX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.self_k : p.self_v);
+      const CUtensorMap* tmap = isk ? &p.tmap_k : &p.tmap_v;
+      const int nst = isk ? KST : VST;
+      const int off = isk ? OFF_K : OFF_V;
+      const int b_full = isk ? B_KR : B_VF, b_free = isk ? B_KE : B_VE;
+      int gt = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const Item w = decode_item(p, idx);
+#pragma unroll 1
+        for (int jj = 0; jj < w.n_tiles; ++jj) {
+          const int g = gt + jj, u = w.t_begin + jj, st = g % nst;
+          if (g >= nst) mbar_wait(bar(b_free + st), ((g - nst) / nst) & 1);
+          const uint32_t dst = sbase + off + st * kTileBytes;
+          if (u == 0) {
+            // sink rows [0,A) + self rows [A, A+n_self), zeros elsewhere, with cp.async
+#pragma unroll 4
+            for (int it = 0; it < 64; ++it) {
+              const int id = it * 32 + lane;          // 2048 16-byte chunks
+              const int r = id >> 4, ch = id & 15;
+              const __nv_bfloat16* src = nullptr;
+              if (r < A) src = SX + (w.head_row * A + r) * 128;
+              else if (r < A + p.n_self) src = XX + (((long long)w.pp * p.n_self + (r - A)) * p.Hkv + w.g) * 128;
+              const uint32_t d = dst + (ch >> 3) * 16384 + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
+              cp_async16(d, src ? (const void*)(src + 8 * ch) : (const void*)SX, src ? 16u : 0u);
+            }
+            cp_async_wait_all();
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(b_full + st));
+          } else if (lane == 0) {
+            int phys = w.k0 + u - 1;
+            if (phys >= w.nT) phys -= w.nT;
+            const int row = (int)(w.head_row * p.R) + phys * 128;
+            mbar_arrive_tx(bar(b_full + st), kTileBytes);
+            tma_load_2d(dst, tmap, 0, row, bar(b_full + st));
+            tma_load_2d(dst + 16384, tmap, 64, row, bar(b_full + st));
+          }
+          if (lane == 0) TRACE(isk ? EV_K_ISSUE : EV_V_ISSUE, g);
+          __syncwarp();
+        }
+        gt += w.n_tiles;
+      }
+    } else if (warp == 14 && lane == 0) {
+      // ============================================================== MMA issuer
+      constexpr uint32_t IQK = idesc_bf16(128, 128, 0, 0);   // S = Q K^T, both K-major
+      constexpr uint32_t IPV = idesc_bf16(128, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
+      auto issue_qk = [&](int qt, int ks) {
+        const uint32_t qa = sbase + OFF_Q + qt * kTileBytes, kb = sbase + OFF_K + ks * kTileBytes;
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) {
+          const uint32_t off = (k8 >> 2) * 16384 + (k8 & 3) * 32;
+          mma_ss(tmem + qt * 128, sdesc(qa + off, 16, 1024), sdesc(kb + off, 16, 1024), IQK, k8 > 0);
+        }
+      };
+      auto issue_pv = [&](int qt, int vs, bool acc) {
+        const uint32_t vb = sbase + OFF_V + vs * kTileBytes;
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8)
+          mma_ts(tmem + 256 + qt * 128, tmem + qt * 128 + k8 * 8, sdesc(vb + k8 * 2048, 16384, 1024), IPV,
+                 (acc || k8 > 0) ? 1u : 0u);
+      };
+      int gt = 0, kk = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
+        const Item w = decode_item(p, idx);
+        const int n = w.n_tiles;
+        mbar_wait(bar(B_Q), kk & 1);
+        if (kk == 0) TRACE(EV_Q, 0);
+        mbar_wait(bar(B_KF + gt % KST), (gt / KST) & 1);
+        TRACE(EV_KF, gt);
+        tc_fence_after();
+        issue_qk(0, gt % KST); mma_commit(bar(B_S + 0));
+        issue_qk(1, gt % KST); mma_commit(bar(B_S + 1));
+        mma_commit(bar(B_KE + gt % KST));
+        if (n == 1) mma_commit(bar(B_QE));
+        for (int jj = 0; jj < n; ++jj) {
+          const int g = gt + jj, vs = g % VST;
+          mbar_wait(bar(B_VF + vs), (g / VST) & 1);
+          for (int qt = 0; qt < 2; ++qt) {
+            mbar_wait(bar(B_P + qt), g & 1);
+            if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
+            TRACE(EV_PV0 + qt, g);
+            tc_fence_after();
+            issue_pv(qt, vs, jj > 0);
+            mma_commit(bar(B_O + qt));
+            if (qt == 1) mma_commit(bar(B_VE + vs));
+            if (jj + 1 < n) {
+              const int ks = (g + 1) % KST;
+              if (qt == 0) {
+                mbar_wait(bar(B_KF + ks), ((g + 1) / KST) & 1);
+                TRACE(EV_KF, g + 1);
+                tc_fence_after();
+              }
+              issue_qk(qt, ks);
+              mma_commit(bar(B_S + qt));
+              if (qt == 1) {
+                mma_commit(bar(B_KE + ks));
+                if (jj + 2 == n) mma_commit(bar(B_QE));   // last QK of the item issued: Q may be reloaded
+              }
+            }
+          }
+        }
+        gt += n;
+      }
+      // drain: the last V-free commit tracks every MMA of this CTA
+      if (gt > 0) mbar_wait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1);
+      TRACE(EV_END, 0);
+    }
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 13) {
+  if (warp == 14) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
@@ -721,8 +822,15 @@ cudaError_t launch_attn_tc(const AttnParams& p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const long long blocks = (long long)p.P * p.Hkv * p.n_mblocks * p.n_splits;
-  tc::attn_tc_kernel<<<(unsigned)blocks, tc::kThreads, tc::kSmemBytes, st>>>(p);
+  const long long items = (long long)p.P * p.Hkv * p.n_mblocks * p.n_splits;
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const unsigned grid = (unsigned)(items < num_sms ? items : num_sms);
+  tc::attn_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, st>>>(p);
   return cudaGetLastError();
 }
 

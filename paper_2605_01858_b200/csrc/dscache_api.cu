@@ -75,6 +75,8 @@ struct dscache_s {
   int* dbg_build = nullptr;
   int* dbg_attend = nullptr;
   int poison = 0;
+  long long* trace = nullptr;
+  int ntrace = 0;
   int impl_build = DSCACHE_IMPL_SIMT, impl_attend = DSCACHE_IMPL_SIMT;
   int num_sms = 148;
   CUtensorMap tmap_k{}, tmap_v{};
@@ -134,10 +136,12 @@ void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
   p.sink_k = h->sink_k; p.sink_v = h->sink_v; p.A = c.sink_tokens;
   p.ring_k = h->ring_k; p.ring_v = h->ring_v; p.R = h->R;
   p.rope = h->rope; p.rope_style = c.rope_style;
+  p.rope_pairs = reinterpret_cast<const float4*>(h->rope + (size_t)h->npos * (c.head_dim / 2));
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c.head_dim));
   p.dtype = c.dtype;
   p.dbg_M = std::max(h->C, c.max_query_tokens);
   p.tmap_k = h->tmap_k; p.tmap_v = h->tmap_v;
+  p.trace = h->trace; p.ntrace_cta = h->ntrace;
   p.n_splits = 1; p.tiles_per_split = 1 << 30;
 }
 
@@ -226,7 +230,7 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   const size_t heads = (size_t)c.num_streams * c.num_layers * c.num_kv_heads;
   const size_t ring_bytes = heads * h->R * c.head_dim * h->elem;
   const size_t sink_bytes = heads * std::max(c.sink_tokens, 1) * c.head_dim * h->elem;
-  const size_t rope_bytes = (size_t)h->npos * (c.head_dim / 2) * sizeof(float2);
+  const size_t rope_bytes = 2 * (size_t)h->npos * (c.head_dim / 2) * sizeof(float2);   // float2 + pair-packed copy
   auto oom = [&](const char* what) {
     cudaGetLastError();
     dscache_destroy(h);
@@ -431,6 +435,14 @@ int32_t dscache_debug_len(dscache_t h) {
 dscache_status dscache_set_debug(dscache_t h, int32_t* build_pos, int32_t* attend_pos, int32_t poison) {
   if (!h) return fail(DSCACHE_E_ARG, "null handle");
   h->dbg_build = build_pos; h->dbg_attend = attend_pos; h->poison = poison;
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_set_trace(dscache_t h, int64_t* buf, int32_t ntrace_cta) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  if (buf && ntrace_cta < 1) return fail(DSCACHE_E_ARG, "ntrace_cta must be >= 1");
+  h->trace = reinterpret_cast<long long*>(buf);
+  h->ntrace = buf ? ntrace_cta : 0;
   return DSCACHE_OK;
 }
 

@@ -9,6 +9,7 @@ namespace dsc {
 
 constexpr int kTileN = 128;   // keys per attention tile (tcgen05 N of QK^T, K of PV)
 constexpr int kTileM = 128;   // query rows per Q tile (tcgen05 M)
+constexpr int kTraceEvents = 16, kTraceTiles = 64;
 
 // One attention launch (build_instant or attend) over P = S * layer_count problems.
 // Keys of problem p, kv head g, in logical order L = 0, 1, ...:
@@ -36,6 +37,7 @@ struct AttnParams {
   int n_self;
   // rope
   const float2* rope;                        // [npos][d/2] (cos, sin)
+  const float4* rope_pairs;                  // [npos][d/4] (cos f, cos f+1, sin f, sin f+1), f = 2j
   int rope_style;
   float scale_log2;                          // log2(e) / sqrt(d)
   // split-KV (attend): partial (O/l, log2-sum-exp) per split
@@ -46,6 +48,8 @@ struct AttnParams {
   int n_mblocks;                             // ceil(n_q * grp / (2 * kTileM))
   // debug export (K7); null = off
   int* dbg_pos; int dbg_M;
+  // per-CTA event timeline (profiling); null = off.  [ntrace_cta][kTraceEvents][kTraceTiles] clock64
+  long long* trace; int ntrace_cta;
   int dtype;                                 // 0 bf16, 1 fp32
   // TMA descriptors of the K / V rings viewed as [S*N*Hkv*R rows][128] bf16, box 64 x 128, SW128
   CUtensorMap tmap_k;

@@ -31,10 +31,28 @@ __global__ void rope_table_kernel(float2* __restrict__ t, int npos, int d, doubl
   }
 }
 
+// Same angles, pair-packed for f32x2 math: entry (pos, j) = (cos f, cos f+1, sin f, sin f+1)
+// with f = 2j, so a float4 load yields the cos and sin of two adjacent frequencies.
+__global__ void rope_table_pairs_kernel(float4* __restrict__ t, int npos, int d, double theta) {
+  const int pairs = d / 4;
+  const long long total = (long long)npos * pairs;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx % pairs);
+    const long long pos = idx / pairs;
+    double s0, c0, s1, c1;
+    sincos((double)pos * pow(theta, -2.0 * (double)(2 * j) / (double)d), &s0, &c0);
+    sincos((double)pos * pow(theta, -2.0 * (double)(2 * j + 1) / (double)d), &s1, &c1);
+    t[idx] = make_float4((float)c0, (float)c1, (float)s0, (float)s1);
+  }
+}
+
 cudaError_t launch_rope_table(float2* table, int npos, int d, double theta, cudaStream_t st) {
   const long long total = (long long)npos * (d / 2);
   int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
   rope_table_kernel<<<blocks, 256, 0, st>>>(table, npos, d, theta);
+  // the pair-packed copy lives right after the float2 table (same byte size)
+  rope_table_pairs_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<float4*>(table + total), npos, d, theta);
   return cudaGetLastError();
 }
 

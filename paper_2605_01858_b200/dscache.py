@@ -53,7 +53,7 @@ class State(ctypes.Structure):
 
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
            "dscache_attend", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
-           "dscache_set_debug", "dscache_debug_len", "dscache_profile", "dscache_profile_read",
+           "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
            "dscache_attn_impl", "dscache_last_error"]
 
 _lib = None
@@ -80,6 +80,7 @@ def load_library(path: str = LIB_PATH):
         "dscache_copy_sink": ([P, I32, I32, P, P], I32),
         "dscache_set_debug": ([P, P, P, I32], I32),
         "dscache_debug_len": ([P], I32),
+        "dscache_set_trace": ([P, P, I32], I32),
         "dscache_profile": ([P, I32], I32),
         "dscache_profile_read": ([P, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(I64),
                                   ctypes.POINTER(I64), ctypes.POINTER(I64), I32], I32),
@@ -250,6 +251,13 @@ class DSCache:
                 raise ValueError("debug buffers must be int32 CUDA tensors of debug_len() entries")
         self._dbg = (build_pos, attend_pos)   # keep alive
         _check(_lib.dscache_set_debug(self._h, _ptr(build_pos), _ptr(attend_pos), int(bool(poison))))
+
+    def set_trace(self, buf: Optional[torch.Tensor], ntrace_cta: int = 1):
+        """buf: int64 CUDA tensor of ntrace_cta*16*64 entries (None = off)."""
+        if buf is not None and (buf.dtype != torch.int64 or buf.numel() < ntrace_cta * 16 * 64):
+            raise ValueError("trace buffer must be int64 with ntrace_cta*16*64 entries")
+        self._trace = buf
+        _check(_lib.dscache_set_trace(self._h, _ptr(buf), int(ntrace_cta)))
 
     def profile(self, enable: bool = True):
         _check(_lib.dscache_profile(self._h, int(enable)))

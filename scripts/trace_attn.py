@@ -1,0 +1,64 @@
+"""Per-CTA event timeline of the tcgen05 attention kernel (build_instant and attend)
+on a steady-state c5-shaped workload.  Prints, per tile, the cycle at which each
+pipeline event happened relative to the CTA start.
+
+    python scripts/trace_attn.py [--streams 8] [--ctas 2]
+"""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import dscache_synth as synth  # noqa: E402
+from paper_2605_01858_b200 import dscache as D  # noqa: E402
+
+EV = ["K_issue", "V_issue", "KR", "KF(mma)", "S0", "S1", "P0", "P1", "PV0", "PV1", "Q", "start", "end"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--streams", type=int, default=8)
+    ap.add_argument("--ctas", type=int, default=2)
+    ap.add_argument("--config", default="c5")
+    args = ap.parse_args()
+    cfg = synth.CONFIGS[args.config].replace(num_streams=args.streams)
+    dev = torch.device("cuda", 0)
+    h = D.DSCache.from_config(cfg)
+    S, N, A, tpf, Hkv, Hq, d = cfg.num_streams, cfg.num_layers, cfg.sink_tokens, cfg.tokens_per_frame, \
+        cfg.num_kv_heads, cfg.num_q_heads, cfg.head_dim
+
+    def r(*s):
+        return (torch.randn(s, device=dev) * cfg.scale).to(torch.bfloat16)
+    h.append_frame(r(S, N, A, Hkv, d), r(S, N, A, Hkv, d))
+    for t in range(cfg.instant_frames + cfg.past_frames):
+        h.append_frame(r(S, N, tpf, Hkv, d), r(S, N, tpf, Hkv, d))
+    C, q = cfg.C, cfg.query_tokens
+    qi, qq, kk, vv = r(S, N, C, Hq, d), r(S, N, q, Hq, d), r(S, N, q, Hkv, d), r(S, N, q, Hkv, d)
+    h.build_instant(qi); h.attend(qq, kk, vv)      # warm
+    torch.cuda.synchronize()
+    for name in ("build_instant", "attend"):
+        buf = torch.zeros(args.ctas * 16 * 64, dtype=torch.int64, device=dev)
+        h.set_trace(buf, args.ctas)
+        if name == "build_instant":
+            h.build_instant(qi)
+        else:
+            h.attend(qq, kk, vv)
+        torch.cuda.synchronize()
+        h.set_trace(None)
+        tr = buf.view(args.ctas, 16, 64).cpu()
+        for c in range(args.ctas):
+            t0 = int(tr[c, 11, 0])
+            end = int(tr[c, 12, 0]) - t0
+            ntiles = int((tr[c, 8] != 0).sum())
+            print(f"== {name} CTA {c}: tiles {ntiles}, total {end} cycles, Q ready at {int(tr[c, 10, 0]) - t0}")
+            print("tile " + " ".join(f"{e:>8}" for e in EV[:10]))
+            for j in range(min(ntiles, 64)):
+                row = [int(tr[c, e, j]) - t0 if int(tr[c, e, j]) else -1 for e in range(10)]
+                print(f"{j:4d} " + " ".join(f"{x:8d}" for x in row))
+    h.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -170,11 +170,13 @@ dscache_status dscache_set_debug(dscache_t h, int32_t* build_pos, int32_t* atten
 int32_t        dscache_debug_len(dscache_t h);
 
 /* Per-CTA event timeline of the tcgen05 attention kernel (profiling aid).  buf: DEVICE
- * int64 buffer of ntrace_cta * 16 * 64 entries (NULL = off): for the first ntrace_cta
+ * int64 buffer of ntrace_cta * 32 * 64 entries (NULL = off): for the first ntrace_cta
  * CTAs of each launch, clock64() at [cta][event][tile] for events 0 K tile issued,
  * 1 V tile issued, 2 raw K landed, 3 rotated K seen by the MMA issuer, 4/5 S0/S1 seen
  * by softmax, 6/7 P0/P1 written, 8/9 PV0/PV1 issued, 10 Q ready, 11 CTA start,
- * 12 CTA end (tile index 0 for 10-12); tiles >= 64 are not recorded. */
+ * 12 CTA end (tile index 0 for 10-12), 13 V seen by the MMA issuer, 14..21 P written
+ * by softmax warp 0..7, 22..27 softmax warp 0 internal steps (S half 0/1 loaded for the
+ * max, rescale decided, S half 0/1 reloaded, P packed); tiles >= 64 are not recorded. */
 dscache_status dscache_set_trace(dscache_t h, int64_t* buf, int32_t ntrace_cta);
 
 /* Profiling: when enabled, every attention/combine kernel launch is bracketed by

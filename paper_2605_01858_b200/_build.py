@@ -35,35 +35,47 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    if not force and not needs_build():
+def build(verbose: bool = False, force: bool = False, defines=(), out: str = LIB) -> str:
+    """Compile the library.  `defines` (e.g. ["DSC_POLY=2"]) build a tuning variant into `out`."""
+    if not force and not defines and not needs_build():
         return LIB
     objs = []
-    tmp = os.path.join(PKG, "build")
+    tag = "_".join(d.replace("=", "") for d in defines)
+    tmp = os.path.join(PKG, "build", tag) if tag else os.path.join(PKG, "build")
     os.makedirs(tmp, exist_ok=True)
     procs = []
     for src in SOURCES:
         obj = os.path.join(tmp, src.replace(".cu", ".o"))
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd += [f"-D{d}" for d in defines]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
     for cmd, p in procs:
-        out, _ = p.communicate()
+        log, _ = p.communicate()
         if verbose or p.returncode:
-            sys.stderr.write(out)
+            sys.stderr.write(log)
         if p.returncode:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    link = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static"]
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    link = [nvcc(), *ARCH, "-shared", "-o", out, *objs, "-lcudart_static"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    return LIB
+    return out
+
+
+def build_variant(name: str, defines) -> str:
+    return build(force=True, defines=list(defines), out=os.path.join(PKG, "variants", f"libdscache_{name}.so"))
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, force=True)
-    print(LIB)
+    if "--variant" in sys.argv:      # --variant NAME DEF1 DEF2 ...
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+    else:
+        build(verbose="--verbose" in sys.argv, force=True)
+        print(LIB)

@@ -165,6 +165,28 @@ __device__ __forceinline__ float ex2(float x) {
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA/ALU pipes (keeps the MUFU free): x = j + f with j = round(x) via the
+// 1.5*2^23 trick, 2^f on [-1/2, 1/2] by a degree-3 fit (max rel. error 1.4e-4 incl.
+// rounding, far below bf16's 2^-9), 2^j added into the exponent bits.  x >= -126.
+constexpr float kP0 = 0.99992829561233520f, kP1 = 0.69326096773147580f, kP2 = 0.24260866641998290f,
+                kP3 = 0.05517056211829185f;
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 y = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+  const float2 j = __fadd2_rn(y, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
+  float2 q = __ffma2_rn(make_float2(kP3, kP3), f, make_float2(kP2, kP2));
+  q = __ffma2_rn(q, f, make_float2(kP1, kP1));
+  q = __ffma2_rn(q, f, make_float2(kP0, kP0));
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(y.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(y.y) << 23)));
+}
+#ifndef DSC_POLY
+#define DSC_POLY 0
+#endif
+constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, this many use exp2_poly2
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -231,7 +253,9 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // timeline events (TRACE): clock64 per (event, tile) for the first ntrace_cta CTAs
-enum { EV_K_ISSUE = 0, EV_V_ISSUE, EV_KR, EV_KF, EV_S0, EV_S1, EV_P0, EV_P1, EV_PV0, EV_PV1, EV_Q, EV_START, EV_END };
+enum { EV_K_ISSUE = 0, EV_V_ISSUE, EV_KR, EV_KF, EV_S0, EV_S1, EV_P0, EV_P1, EV_PV0, EV_PV1, EV_Q, EV_START, EV_END,
+       EV_VF, EV_PW0 /* 14..21: P arrival of softmax warps 0..7 */, EV_L = 22 /* 22..27: warp-0 softmax steps */,
+       EV_KDONE = 28, EV_QDONE = 29, EV_QLOADED = 30, EV_QSTART = 31 };
 #define TRACE(ev, tile)                                                                                  \
   do {                                                                                                   \
     if (p.trace && blockIdx.x < (unsigned)p.ntrace_cta && (tile) < kTraceTiles)                          \
@@ -327,11 +351,13 @@ __device__ __forceinline__ uint32_t get_w(const uint4& v, int j) { return j == 0
 // consecutive ids the (cos, sin) advance by R(theta) (id + 1) or stay (same id),
 // any other jump reloads the fp64-built pair table rp[id][32].
 __device__ __forceinline__ void rotate8(uint32_t tile, int r0, int c8, const float4* __restrict__ rp,
-                                        const float2 (&cth)[4], const float2 (&sth)[4], const int (&pos)[8]) {
+                                        const float2 (&cth)[4], const float2 (&sth)[4], const int (&pos)[8],
+                                        const float4 (&pre)[4], int pre_pos) {
+  // (cs, sn) start at the prefetched table entry of id pre_pos (the first valid row)
   float2 cs[4], sn[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) { cs[j] = make_float2(1.f, 1.f); sn[j] = make_float2(0.f, 0.f); }
-  int prev = -2;
+  for (int j = 0; j < 4; ++j) { cs[j] = make_float2(pre[j].x, pre[j].y); sn[j] = make_float2(pre[j].z, pre[j].w); }
+  int prev = pre_pos;
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     uint4 lo[4], hi[4];
@@ -348,14 +374,15 @@ __device__ __forceinline__ void rotate8(uint32_t tile, int r0, int c8, const flo
       const int pk = pos[half * 4 + k];
       uint4 ylo = make_uint4(0, 0, 0, 0), yhi = make_uint4(0, 0, 0, 0);
       if (pk >= 0) {
-        if (pk == prev + 1) {
+        if (pk == prev) {
+        } else if (pk == prev + 1) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const float2 nc = __ffma2_rn(cs[j], cth[j], __fmul2_rn(make_float2(-sn[j].x, -sn[j].y), sth[j]));
             sn[j] = __ffma2_rn(sn[j], cth[j], __fmul2_rn(cs[j], sth[j]));
             cs[j] = nc;
           }
-        } else if (pk != prev) {
+        } else {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const float4 t = rp[(long long)pk * 32 + 4 * c8 + j];
@@ -376,7 +403,7 @@ __device__ __forceinline__ void rotate8(uint32_t tile, int r0, int c8, const flo
         ylo = make_uint4(ol[0], ol[1], ol[2], ol[3]);
         yhi = make_uint4(oh[0], oh[1], oh[2], oh[3]);
       } else {
-        prev = -2;
+        prev = -3;
       }
       sts128(addr[k], ylo);
       sts128(addr[k] + 16384, yhi);
@@ -451,6 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       const bool valid_row = rglob < w.rows_total;
       const int qi = valid_row ? rglob / p.grp : 0;
       const int lim = valid_row ? p.q_pos0 + qi : -1;
+      const bool warp_dead = __all_sync(0xffffffffu, !valid_row);
       float m = -INFINITY;
       float2 lsum2 = make_float2(0.f, 0.f);
       for (int jj = 0; jj < n; ++jj) {
@@ -470,8 +498,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         const bool full = (c_lo == 0) && (c_hi == 128);
         mbar_wait(bar(B_S + qt), g & 1);
         if (rloc == 0) TRACE(EV_S0 + qt, g);
+        if (warp_dead) {                      // all 32 rows are padding: their P / O are never used
+          mbar_arrive(bar(B_P + qt));
+          continue;
+        }
         tc_fence_after();
-        // pass 1: row max over the visible columns, two 64-column halves
+        // pass 1: row max over the visible columns, two 64-column halves.  In a partial
+        // tile the invisible columns are set to -inf and written back to TMEM, so the
+        // exp pass needs no mask (2^-inf = 0).
+        const bool any_partial = __any_sync(0xffffffffu, !full);
+        const unsigned span = (unsigned)max(c_hi - c_lo, 0);
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll 1
         for (int hf = 0; hf < 2; ++hf) {
@@ -479,10 +515,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           tmem_ld32(tS + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
           tmem_ld32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
           tmem_wait_ld();
-          if (!full) {
+          if (warp == 0 && lane == 0) TRACE(EV_L + hf, g);
+          if (any_partial) {
 #pragma unroll
-            for (int c = 0; c < 64; ++c)
-              if (64 * hf + c < c_lo || 64 * hf + c >= c_hi) r[c] = 0xFF800000u;   // -inf
+            for (int c = 0; c < 64; ++c) r[c] = ((unsigned)(64 * hf + c - c_lo) < span) ? r[c] : 0xFF800000u;
+            tmem_st32(tS + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+            tmem_st32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
           }
 #pragma unroll
           for (int c = 0; c < 64; c += 4) {
@@ -492,6 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
             mx3 = fmaxf(mx3, __uint_as_float(r[c + 3]));
           }
         }
+        if (any_partial) tmem_wait_st();
         const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
         // lazy rescale: move the running max only when it grew by > 2^8; the TMEM
         // load/store of O is warp-collective, so the decision is made per warp.
@@ -517,6 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           }
           tmem_wait_st();
         }
+        if (warp == 0 && lane == 0) TRACE(EV_L + 5, g);
         const float m_use = (m == -INFINITY) ? 0.f : m;
         const float2 negm2 = make_float2(-m_use, -m_use);
         // pass 2: P = 2^(s*scale - m) (masked -> 2^-inf = 0), packed bf16x2; half hf of S
@@ -528,17 +568,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           tmem_ld32(tS + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
           tmem_ld32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
           tmem_wait_ld();
-          if (!full) {
-#pragma unroll
-            for (int c = 0; c < 64; ++c)
-              if (64 * hf + c < c_lo || 64 * hf + c >= c_hi) r[c] = 0xFF800000u;
-          }
+          if (warp == 0 && lane == 0) TRACE(EV_L + 2 + hf, g);
 #pragma unroll
           for (int c = 0; c < 64; c += 4) {
             const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
             const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
-            const float2 p0 = make_float2(ex2(x0.x), ex2(x0.y));
-            const float2 p1 = make_float2(ex2(x1.x), ex2(x1.y));
+            float2 p0, p1;
+            constexpr bool poly0_any = kPolyPerGroup > 0;
+            const bool poly0 = poly0_any && ((c % 8) + 2 > 8 - kPolyPerGroup);
+            const bool poly1 = poly0_any && ((c % 8) + 4 > 8 - kPolyPerGroup);
+            if (poly0 && !any_partial) p0 = exp2_poly2(x0); else p0 = make_float2(ex2(x0.x), ex2(x0.y));
+            if (poly1 && !any_partial) p1 = exp2_poly2(x1); else p1 = make_float2(ex2(x1.x), ex2(x1.y));
             l0 = __fadd2_rn(l0, p0);
             l1 = __fadd2_rn(l1, p1);
             r[c >> 1] = pack_bf16(p0.x, p0.y);
@@ -547,10 +587,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           tmem_st32(tS + 32 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
         }
         lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
+        if (warp == 0 && lane == 0) TRACE(EV_L + 4, g);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(bar(B_P + qt));
         if (rloc == 0) TRACE(EV_P0 + qt, g);
+        if (lane == 0) TRACE(EV_PW0 + warp, g);
       }
       gt += n;
       // epilogue of the item
@@ -614,52 +656,99 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
       // ---- Q of this item: raw rows via cp.async into the Q tiles, then rotate in place
       if (kk > 0) mbar_wait(bar(B_QE), (kk - 1) & 1);
+      if (lt == 0) TRACE(EV_QSTART, gt);
+      {
+        // thread lt copies 16-byte chunk (lt & 15) of rows (lt >> 4) + 8*it, it = 0..31; the
+        // (query, head) of a row advances incrementally (8 rows per step), no divisions
+        const int ch = lt & 15;
+        int rgl = w.m0 + (lt >> 4);
+        int qi = rgl / p.grp, hh = rgl % p.grp;
+        const int step_i = 8 / p.grp, step_h = 8 % p.grp;
+        const __nv_bfloat16* qbase = Qg + ((long long)w.pp * p.n_q) * p.Hq * 128 + (long long)w.g * p.grp * 128 + 8 * ch;
+        const uint32_t dbase = sbase + OFF_Q + (ch >> 3) * 16384;
 #pragma unroll 4
-      for (int it = 0; it < 32; ++it) {
-        const int id = it * 128 + lt;          // 4096 16-byte chunks of 256 rows
-        const int r = id >> 4, ch = id & 15;
-        const int rgl = w.m0 + r;
-        const __nv_bfloat16* src = nullptr;
-        if (rgl < w.rows_total)
-          src = Qg + (((long long)w.pp * p.n_q + rgl / p.grp) * p.Hq + w.g * p.grp + rgl % p.grp) * 128;
-        const uint32_t d = sbase + OFF_Q + (r >> 7) * kTileBytes + (ch >> 3) * 16384 + (r & 127) * 128 +
-                           (((ch & 7) ^ (r & 7)) << 4);
-        cp_async16(d, src ? (const void*)(src + 8 * ch) : (const void*)Qg, src ? 16u : 0u);
-      }
-      cp_async_wait_all();
-      named_bar(1, 128);
-#pragma unroll 1
-      for (int qt = 0; qt < 2; ++qt) {
-        const int row0 = w.m0 + qt * 128 + rg8 * 8;       // global row of the first of the 8 rows
-        int i = row0 / p.grp, hh = row0 % p.grp;
-        int pos[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          pos[k] = (row0 + k < w.rows_total) ? p.q_pos0 + i : -1;
-          if (dbg && c8 == 0 && hh == 0 && pos[k] >= 0) p.dbg_pos[A + p.R + p.dbg_M + i] = pos[k];
-          if (++hh == p.grp) { hh = 0; ++i; }
+        for (int it = 0; it < 32; ++it) {
+          const int r = it * 8 + (lt >> 4);
+          const bool ok = rgl < w.rows_total;
+          const __nv_bfloat16* src = qbase + ((long long)qi * p.Hq + hh) * 128;
+          const uint32_t d = dbase + (r >> 7) * kTileBytes + (r & 127) * 128 + (((ch & 7) ^ (r & 7)) << 4);
+          cp_async16(d, ok ? (const void*)src : (const void*)Qg, ok ? 16u : 0u);
+          rgl += 8;
+          qi += step_i;
+          hh += step_h;
+          if (hh >= p.grp) { hh -= p.grp; ++qi; }
         }
-        rotate8(sbase + OFF_Q + qt * kTileBytes, rg8 * 8, c8, rp, cth, sth, pos);
+      }
+      {
+        int qpos[2][8];
+        float4 qpre[2][4];
+#pragma unroll
+        for (int qt = 0; qt < 2; ++qt) {
+          const int row0 = w.m0 + qt * 128 + rg8 * 8;       // global row of the first of the 8 rows
+          int i = row0 / p.grp, hh = row0 % p.grp;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            qpos[qt][k] = (row0 + k < w.rows_total) ? p.q_pos0 + i : -1;
+            if (dbg && c8 == 0 && hh == 0 && qpos[qt][k] >= 0) p.dbg_pos[A + p.R + p.dbg_M + i] = qpos[qt][k];
+            if (++hh == p.grp) { hh = 0; ++i; }
+          }
+          const int p0 = max(qpos[qt][0], 0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) qpre[qt][j] = rp[(long long)p0 * 32 + 4 * c8 + j];
+        }
+        cp_async_wait_all();
+        named_bar(1, 128);
+        if (lt == 0) TRACE(EV_QLOADED, gt);
+#pragma unroll
+        for (int qt = 0; qt < 2; ++qt)
+          rotate8(sbase + OFF_Q + qt * kTileBytes, rg8 * 8, c8, rp, cth, sth, qpos[qt], qpre[qt],
+                  max(qpos[qt][0], 0));
       }
       fence_proxy_async();
       mbar_arrive(bar(B_Q));
-      // ---- K tiles of this item
+      if (lt == 0) TRACE(EV_QDONE, gt);
+      // ---- K tiles of this item; the table entry of each tile's first row is fetched
+      // one tile ahead so the L2 latency is off the rotation's critical path
+      int kpos[8];
+      float4 kpre[4];
+      auto first_pos = [&](int u) {
+        const TileSeg t = tile_segments(p, w, u);
+        int q = -1;
+#pragma unroll
+        for (int k = 7; k >= 0; --k) {
+          const int pk = seg_pos(t, rg8 * 8 + k);
+          if (pk >= 0) q = pk;
+        }
+        return q;
+      };
+      int pre_pos = w.n_tiles > 0 ? first_pos(w.t_begin) : -1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) kpre[j] = rp[(long long)max(pre_pos, 0) * 32 + 4 * c8 + j];
       for (int jj = 0; jj < w.n_tiles; ++jj) {
         const int g = gt + jj, u = w.t_begin + jj, ks = g % KST;
         const TileSeg t = tile_segments(p, w, u);
-        int pos[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) pos[k] = seg_pos(t, rg8 * 8 + k);
+        for (int k = 0; k < 8; ++k) kpos[k] = seg_pos(t, rg8 * 8 + k);
+        float4 cur[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cur[j] = kpre[j];
+        const int cur_pos = pre_pos;
+        if (jj + 1 < w.n_tiles) {          // prefetch for the next tile
+          pre_pos = first_pos(u + 1);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) kpre[j] = rp[(long long)max(pre_pos, 0) * 32 + 4 * c8 + j];
+        }
         mbar_wait(bar(B_KR + ks), (g / KST) & 1);
         if (lt == 0) TRACE(EV_KR, g);
-        rotate8(sbase + OFF_K + ks * kTileBytes, rg8 * 8, c8, rp, cth, sth, pos);
+        rotate8(sbase + OFF_K + ks * kTileBytes, rg8 * 8, c8, rp, cth, sth, kpos, cur, max(cur_pos, 0));
         fence_proxy_async();
         mbar_arrive(bar(B_KF + ks));
+        if (lt == 0) TRACE(EV_KDONE, g);
         if (dbg && c8 == 0) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const int r = rg8 * 8 + k;
-            if (pos[k] >= 0) p.dbg_pos[(u == 0) ? (r < A ? r : A + p.R + (r - A)) : A + t.phys * 128 + r] = pos[k];
+            if (kpos[k] >= 0) p.dbg_pos[(u == 0) ? (r < A ? r : A + p.R + (r - A)) : A + t.phys * 128 + r] = kpos[k];
           }
         }
       }
@@ -748,6 +837,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         for (int jj = 0; jj < n; ++jj) {
           const int g = gt + jj, vs = g % VST;
           mbar_wait(bar(B_VF + vs), (g / VST) & 1);
+          TRACE(EV_VF, g);
           for (int qt = 0; qt < 2; ++qt) {
             mbar_wait(bar(B_P + qt), g & 1);
             if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read

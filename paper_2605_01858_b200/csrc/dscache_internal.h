@@ -9,7 +9,7 @@ namespace dsc {
 
 constexpr int kTileN = 128;   // keys per attention tile (tcgen05 N of QK^T, K of PV)
 constexpr int kTileM = 128;   // query rows per Q tile (tcgen05 M)
-constexpr int kTraceEvents = 16, kTraceTiles = 64;
+constexpr int kTraceEvents = 32, kTraceTiles = 64;
 
 // One attention launch (build_instant or attend) over P = S * layer_count problems.
 // Keys of problem p, kv head g, in logical order L = 0, 1, ...:

@@ -13,7 +13,8 @@ from typing import Optional
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libdscache.so")
+# DSCACHE_LIB selects a tuning variant built by _build.build_variant (same ABI)
+LIB_PATH = os.environ.get("DSCACHE_LIB") or os.path.join(_PKG, "libdscache.so")
 
 OK, E_ARG, E_CONFIG, E_POS_OVERFLOW, E_STATE, E_CUDA, E_OOM = 0, -1, -2, -3, -4, -5, -6
 STATUS_NAMES = {0: "OK", -1: "E_ARG", -2: "E_CONFIG", -3: "E_POS_OVERFLOW", -4: "E_STATE", -5: "E_CUDA",
@@ -253,9 +254,9 @@ class DSCache:
         _check(_lib.dscache_set_debug(self._h, _ptr(build_pos), _ptr(attend_pos), int(bool(poison))))
 
     def set_trace(self, buf: Optional[torch.Tensor], ntrace_cta: int = 1):
-        """buf: int64 CUDA tensor of ntrace_cta*16*64 entries (None = off)."""
-        if buf is not None and (buf.dtype != torch.int64 or buf.numel() < ntrace_cta * 16 * 64):
-            raise ValueError("trace buffer must be int64 with ntrace_cta*16*64 entries")
+        """buf: int64 CUDA tensor of ntrace_cta*32*64 entries (None = off)."""
+        if buf is not None and (buf.dtype != torch.int64 or buf.numel() < ntrace_cta * 32 * 64):
+            raise ValueError("trace buffer must be int64 with ntrace_cta*32*64 entries")
         self._trace = buf
         _check(_lib.dscache_set_trace(self._h, _ptr(buf), int(ntrace_cta)))
 

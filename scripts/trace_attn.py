@@ -14,7 +14,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import dscache_synth as synth  # noqa: E402
 from paper_2605_01858_b200 import dscache as D  # noqa: E402
 
-EV = ["K_issue", "V_issue", "KR", "KF(mma)", "S0", "S1", "P0", "P1", "PV0", "PV1", "Q", "start", "end"]
+EV = ["K_issue", "V_issue", "KR", "KF(mma)", "S0", "S1", "P0", "P1", "PV0", "PV1", "Q", "start", "end", "VF(mma)"] + [f"Pw{i}" for i in range(8)] + ["max_h0", "max_h1", "exp_h0", "exp_h1", "packed", "resc", "Kdone", "Qdone", "Qloaded", "Qstart"]
+NE = 32
 
 
 def main():
@@ -39,7 +40,7 @@ def main():
     h.build_instant(qi); h.attend(qq, kk, vv)      # warm
     torch.cuda.synchronize()
     for name in ("build_instant", "attend"):
-        buf = torch.zeros(args.ctas * 16 * 64, dtype=torch.int64, device=dev)
+        buf = torch.zeros(args.ctas * NE * 64, dtype=torch.int64, device=dev)
         h.set_trace(buf, args.ctas)
         if name == "build_instant":
             h.build_instant(qi)
@@ -47,15 +48,16 @@ def main():
             h.attend(qq, kk, vv)
         torch.cuda.synchronize()
         h.set_trace(None)
-        tr = buf.view(args.ctas, 16, 64).cpu()
+        tr = buf.view(args.ctas, NE, 64).cpu()
         for c in range(args.ctas):
             t0 = int(tr[c, 11, 0])
             end = int(tr[c, 12, 0]) - t0
             ntiles = int((tr[c, 8] != 0).sum())
             print(f"== {name} CTA {c}: tiles {ntiles}, total {end} cycles, Q ready at {int(tr[c, 10, 0]) - t0}")
-            print("tile " + " ".join(f"{e:>8}" for e in EV[:10]))
+            cols = [31, 30, 29, 2, 28, 3, 4, 6, 8, 5, 7, 9] + [22, 23, 27, 24, 25, 26]
+            print("tile " + " ".join(f"{EV[e]:>8}" for e in cols))
             for j in range(min(ntiles, 64)):
-                row = [int(tr[c, e, j]) - t0 if int(tr[c, e, j]) else -1 for e in range(10)]
+                row = [int(tr[c, e, j]) - t0 if int(tr[c, e, j]) else -1 for e in cols]
                 print(f"{j:4d} " + " ".join(f"{x:8d}" for x in row))
     h.close()
 

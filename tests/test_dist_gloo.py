@@ -1,0 +1,138 @@
+"""Multi-process (world_size 2, gloo on CPU) checks of the multi-GPU host logic.
+
+The GPU box has one GPU, so the N>1 paths are covered here: each rank stands in
+for one GPU and computes its shard with the fp64 oracle (the CUDA backend's
+stand-in on CPU); the tests check the partitions (P1 streams, P2 KV-head groups)
+and the head-major all-gather of paper_2605_01858_b200.dist against the
+unsharded oracle.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import dscache_synth as synth
+from paper_2605_01858_b200.dist import gather_heads, kv_head_partition, stream_partition
+
+
+def test_stream_partition_covers_every_stream_once():
+    for S in (1, 5, 8, 64):
+        for world in (1, 2, 3, 4, 8):
+            got = []
+            for r in range(world):
+                lo, hi = stream_partition(S, world, r)
+                assert 0 <= lo <= hi <= S
+                got += list(range(lo, hi))
+            assert got == list(range(S))
+            sizes = [stream_partition(S, world, r)[1] - stream_partition(S, world, r)[0] for r in range(world)]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_kv_head_partition_keeps_gqa_groups_together():
+    for world in (1, 2, 4):
+        qs, ks = [], []
+        for r in range(world):
+            kv_lo, kv_n, q_lo, q_n = kv_head_partition(28, 4, world, r)
+            ks += list(range(kv_lo, kv_lo + kv_n))
+            qs += list(range(q_lo, q_lo + q_n))
+            for h in range(q_lo, q_lo + q_n):          # every local q head reads a local kv head
+                assert kv_lo <= h // 7 < kv_lo + kv_n
+        assert ks == list(range(4)) and qs == list(range(28))
+    with pytest.raises(ValueError):
+        kv_head_partition(28, 4, 8, 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _oracle_attend(cfg, s, t, heads=None):
+    """Oracle O [q, Hq(_local), d] of stream s at step t, optionally on a KV-head shard."""
+    from oracle.workload import StreamInputs, step_schedule
+    from oracle import dscache_oracle as O
+    inp = StreamInputs(cfg, s, 0)
+    sch = step_schedule(cfg, t)
+    sk, sv = inp.sink()
+    q, ks, vs = inp.query(t)
+    frame = inp.frame_kv
+    if heads is not None:
+        kv_lo, kv_n, q_lo, q_n = heads
+        sk, sv = sk[:, kv_lo:kv_lo + kv_n], sv[:, kv_lo:kv_lo + kv_n]
+        q = q[:, q_lo:q_lo + q_n]
+        ks, vs = ks[:, kv_lo:kv_lo + kv_n], vs[:, kv_lo:kv_lo + kv_n]
+        frame = lambda f: tuple(x[:, kv_lo:kv_lo + kv_n] for x in inp.frame_kv(f))   # noqa: E731
+    return O.attend_output(sch, (sk, sv), frame, q, ks, vs, cfg.rope_theta)
+
+
+def _small_cfg():
+    # c2's head layout (28 q / 4 kv heads, GQA 7) on a short, small-frame stream
+    return synth.CONFIGS["c2"].replace(num_streams=4, tokens_per_frame=8, past_frames=3, instant_frames=2,
+                                       query_tokens=5, num_frames=8, head_dim=32)
+
+
+def _worker_kv_split(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = _small_cfg()
+    heads = kv_head_partition(cfg.num_q_heads, cfg.num_kv_heads, world, rank)
+    t = 6
+    local = torch.from_numpy(_oracle_attend(cfg, 0, t, heads))       # [q, Hq/G, d]
+    full = gather_heads(local[None, None])                          # [1, 1, q, Hq, d]
+    if rank == 0:
+        out_q.put(full[0, 0].numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _worker_streams(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = _small_cfg()
+    lo, hi = stream_partition(cfg.num_streams, world, rank)
+    t = 7
+    digests = torch.zeros(cfg.num_streams, dtype=torch.float64)
+    for s in range(lo, hi):                      # this rank's streams only; no data-path collective
+        digests[s] = float(np.abs(_oracle_attend(cfg, s, t)).sum())
+    dist.all_reduce(digests)                     # end-of-run digest gather (not on the hot path)
+    if rank == 0:
+        out_q.put(digests.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(worker, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def test_kv_head_split_allgather_matches_unsharded_oracle():
+    full = _run(_worker_kv_split)
+    ref = _oracle_attend(_small_cfg(), 0, 6)
+    assert full.shape == ref.shape
+    assert np.abs(full - ref).max() < 1e-12
+
+
+def test_stream_partition_two_ranks_matches_single_process():
+    digests = _run(_worker_streams)
+    cfg = _small_cfg()
+    ref = np.array([np.abs(_oracle_attend(cfg, s, 7)).sum() for s in range(cfg.num_streams)])
+    assert np.allclose(digests, ref, rtol=0, atol=1e-12)

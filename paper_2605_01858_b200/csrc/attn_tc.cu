@@ -271,14 +271,16 @@ struct Item {
   int t_begin, n_tiles;
 };
 
-// work item idx -> (split fastest, then problem x kv head, then m-block descending):
-// all (problem, head) pairs of the longest causal m-block come first.
+// work item idx -> (split fastest, then m-block descending, then problem x kv head):
+// the m-blocks of one (problem, head) are adjacent, so the CTAs working on them at
+// the same time share its K/V tiles in L2 (the causal build re-reads the instant
+// window once per m-block); longest m-block first within the group.
 __device__ __forceinline__ Item decode_item(const AttnParams& p, int idx) {
   Item w;
   w.sp = idx % p.n_splits;
   const int rest = idx / p.n_splits;
-  const int ph = rest % (p.P * p.Hkv);
-  w.mb = p.n_mblocks - 1 - rest / (p.P * p.Hkv);
+  w.mb = p.n_mblocks - 1 - rest % p.n_mblocks;
+  const int ph = rest / p.n_mblocks;
   w.g = ph % p.Hkv;
   w.pp = ph / p.Hkv;
   const int s = w.pp / p.layer_count, l = w.pp % p.layer_count;

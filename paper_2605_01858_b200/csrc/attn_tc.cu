@@ -16,9 +16,10 @@
 // CTA = 16 warps:
 //   warps 0-3  softmax of Q tile 0 (thread = query row = TMEM lane)
 //   warps 4-7  softmax of Q tile 1
-//   warps 8-11 rotation: per item Q (cp.async raw -> rotate in place), then every
-//              raw K tile in place in shared memory (LDS -> rotate -> STS), with
-//              R(p+1) = R(p) R(1) between consecutive ids
+//   warps 8-11 rotation: every raw K tile in place in shared memory
+//              (LDS -> rotate -> STS), with R(p+1) = R(p) R(1) between consecutive ids
+//   (each softmax warpgroup loads + rotates the Q tile of its next item itself, as soon
+//    as it has consumed S of its last tile, overlapped with its epilogue)
 //   warp 12    K copy: raw K tiles -> SW128 smem; TMA (2 x 64x128 boxes) for ring
 //              tiles, cp.async for the sink/self tile
 //   warp 13    V copy: same for V (K and V stage recycling is independent)
@@ -50,7 +51,7 @@ constexpr int OFF_V = OFF_K + KST * kTileBytes;
 constexpr int OFF_BAR = OFF_V + VST * kTileBytes;
 // barriers (8 B each): Q ready | Q free | K raw landed | K rotated | K free | V landed | V free |
 // S ready | P ready | O done | O read (epilogue done)
-constexpr int B_Q = 0, B_QE = 1, B_KR = 2, B_KF = 5, B_KE = 8, B_VF = 11, B_VE = 13, B_S = 15, B_P = 17, B_O = 19,
+constexpr int B_Q = 0 /* +qt */, B_KR = 2, B_KF = 5, B_KE = 8, B_VF = 11, B_VE = 13, B_S = 15, B_P = 17, B_O = 19,
               B_OF = 21, B_N = 23;
 // setmaxnreg budget per warpgroup: 2*144 (softmax) + 136 (rotation) + 88 (copy/MMA) = 512 x 128 threads
 constexpr int kRegSoftmax = 144, kRegRotate = 136, kRegCopy = 88;
@@ -262,6 +263,9 @@ enum { EV_K_ISSUE = 0, EV_V_ISSUE, EV_KR, EV_KF, EV_S0, EV_S1, EV_P0, EV_P1, EV_
       p.trace[((long long)blockIdx.x * kTraceEvents + (ev)) * kTraceTiles + (tile)] = clock64();          \
   } while (0)
 
+#ifndef DSC_ORDER
+#define DSC_ORDER 1
+#endif
 struct Item {
   int pp, g, mb, sp;
   long long head_row;
@@ -271,16 +275,21 @@ struct Item {
   int t_begin, n_tiles;
 };
 
-// work item idx -> (split fastest, then m-block descending, then problem x kv head):
-// the m-blocks of one (problem, head) are adjacent, so the CTAs working on them at
-// the same time share its K/V tiles in L2 (the causal build re-reads the instant
-// window once per m-block); longest m-block first within the group.
+// work item idx -> split fastest, then (DSC_ORDER 1, default) problem x kv head, then
+// m-block descending: all (problem, head) pairs of the longest causal m-block first
+// (LPT-like balance of the persistent CTAs).  DSC_ORDER 0 groups the m-blocks of one
+// (problem, head) for L2 reuse of its K/V; measured slower on c5 (9.8K vs 12.4K frames/s).
 __device__ __forceinline__ Item decode_item(const AttnParams& p, int idx) {
   Item w;
   w.sp = idx % p.n_splits;
   const int rest = idx / p.n_splits;
+#if DSC_ORDER == 1   // longest-first across all (problem, head) pairs
+  const int ph = rest % (p.P * p.Hkv);
+  w.mb = p.n_mblocks - 1 - rest / (p.P * p.Hkv);
+#else
   w.mb = p.n_mblocks - 1 - rest % p.n_mblocks;
   const int ph = rest / p.n_mblocks;
+#endif
   w.g = ph % p.Hkv;
   w.pp = ph / p.Hkv;
   const int s = w.pp / p.layer_count, l = w.pp % p.layer_count;
@@ -413,6 +422,59 @@ __device__ __forceinline__ void rotate8(uint32_t tile, int r0, int c8, const flo
   }
 }
 
+// Raw Q rows [m0 + 128*qt, +128) of an item -> SW128 tile in smem by cp.async (16 chunks
+// per thread, (query, head) advanced incrementally), then rotated in place at the query
+// id (8 rows x 8 frequencies per thread).  Executed by one 128-thread warpgroup.
+__device__ __forceinline__ void issue_q_tile(const AttnParams& p, const Item& w, int qt, int lt, uint32_t qtile) {
+  const __nv_bfloat16* __restrict__ Qg = reinterpret_cast<const __nv_bfloat16*>(p.q);
+  const int ch = lt & 15;
+  int rgl = w.m0 + qt * 128 + (lt >> 4);
+  int qi = rgl / p.grp, hh = rgl % p.grp;
+  const int step_i = 8 / p.grp, step_h = 8 % p.grp;
+  const __nv_bfloat16* qbase = Qg + ((long long)w.pp * p.n_q) * p.Hq * 128 + (long long)w.g * p.grp * 128 + 8 * ch;
+  const uint32_t dbase = qtile + (ch >> 3) * 16384;
+#pragma unroll 4
+  for (int it = 0; it < 16; ++it) {
+    const int r = it * 8 + (lt >> 4);
+    const bool ok = rgl < w.rows_total;
+    const __nv_bfloat16* src = qbase + ((long long)qi * p.Hq + hh) * 128;
+    cp_async16(dbase + r * 128 + (((ch & 7) ^ (r & 7)) << 4), ok ? (const void*)src : (const void*)Qg, ok ? 16u : 0u);
+    rgl += 8;
+    qi += step_i;
+    hh += step_h;
+    if (hh >= p.grp) { hh -= p.grp; ++qi; }
+  }
+}
+__device__ __forceinline__ void rotate_q_tile(const AttnParams& p, const Item& w, int qt, int lt, uint32_t qtile,
+                                              int bar_id) {
+  const float4* __restrict__ rp = p.rope_pairs;
+  const int c8 = lt & 7, rg8 = lt >> 3;
+  float2 cth[4], sth[4];
+  float4 pre[4];
+  int pos[8];
+  const int row0 = w.m0 + qt * 128 + rg8 * 8;
+  int i = row0 / p.grp, hh = row0 % p.grp;
+  const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    pos[k] = (row0 + k < w.rows_total) ? p.q_pos0 + i : -1;
+    if (dbg && c8 == 0 && hh == 0 && pos[k] >= 0) p.dbg_pos[p.A + p.R + p.dbg_M + i] = pos[k];
+    if (++hh == p.grp) { hh = 0; ++i; }
+  }
+  const int p0 = max(pos[0], 0);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float4 t = rp[32 + 4 * c8 + j];
+    cth[j] = make_float2(t.x, t.y);
+    sth[j] = make_float2(t.z, t.w);
+    pre[j] = rp[(long long)p0 * 32 + 4 * c8 + j];
+  }
+  cp_async_wait_all();
+  named_bar(bar_id, 128);
+  rotate8(qtile, rg8 * 8, c8, rp, cth, sth, pos, pre, p0);
+  fence_proxy_async();
+}
+
 // ------------------------------------------------------------------ kernel
 __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -426,8 +488,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   const int n_items = p.n_mblocks * p.P * p.Hkv * p.n_splits;
 
   if (threadIdx.x == 0) {
-    mbar_init(bar(B_Q), 128);
-    mbar_init(bar(B_QE), 1);
+    mbar_init(bar(B_Q + 0), 128);
+    mbar_init(bar(B_Q + 1), 128);
     for (int i = 0; i < KST; ++i) {
       mbar_init(bar(B_KR + i), 1);
       mbar_init(bar(B_KF + i), 128);
@@ -472,6 +534,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     const uint32_t tO = tmem + lane_off + (uint32_t)(256 + qt * 128);
     const float sl2 = p.scale_log2;
     const float2 scale2 = make_float2(sl2, sl2);
+    const int lt = threadIdx.x - qt * 128;          // 0..127 within the warpgroup
+    const uint32_t qtile = sbase + OFF_Q + qt * kTileBytes;
+    if (blockIdx.x < (unsigned)n_items) {            // Q tile of the first item
+      const Item w0 = decode_item(p, blockIdx.x);
+      issue_q_tile(p, w0, qt, lt, qtile);
+      rotate_q_tile(p, w0, qt, lt, qtile, 2 + qt);
+      mbar_arrive(bar(B_Q + qt));
+    }
     int gt = 0, kk = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
       const Item w = decode_item(p, idx);
@@ -597,6 +667,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         if (lane == 0) TRACE(EV_PW0 + warp, g);
       }
       gt += n;
+      // S_qt of the last tile has been read: the MMA is done with Q tile qt, so the next
+      // item's Q tile is fetched now (overlapping this item's epilogue)
+      const int nidx = idx + gridDim.x;
+      Item wn;
+      if (nidx < n_items) {
+        wn = decode_item(p, nidx);
+        issue_q_tile(p, wn, qt, lt, qtile);
+      }
       // epilogue of the item
       const float lsum = lsum2.x + lsum2.y;
       mbar_wait(bar(B_O + qt), (gt - 1) & 1);
@@ -636,6 +714,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           if (hf == 0) p.ws_lse[(long long)w.sp * rows + orow] = lsum > 0.f ? m + __log2f(lsum) : -INFINITY;
         }
       }
+      if (nidx < n_items) {
+        rotate_q_tile(p, wn, qt, lt, qtile, 2 + qt);
+        mbar_arrive(bar(B_Q + qt));
+        if (rloc == 0) TRACE(EV_QDONE, gt);
+      }
     }
   } else if (warp < 12) {
     // ================================================================ rotation (Q per item, then K tiles)
@@ -643,7 +726,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     const int lt = threadIdx.x - 256;
     const int c8 = lt & 7;             // frequencies 8*c8 .. 8*c8+7
     const int rg8 = lt >> 3;           // rows rg8*8 .. +7 of a 128-row tile
-    const __nv_bfloat16* __restrict__ Qg = reinterpret_cast<const __nv_bfloat16*>(p.q);
     const float4* __restrict__ rp = p.rope_pairs;
     float2 cth[4], sth[4];             // R(theta_f) = table entry of id 1
 #pragma unroll
@@ -656,59 +738,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
       const Item w = decode_item(p, idx);
       const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
-      // ---- Q of this item: raw rows via cp.async into the Q tiles, then rotate in place
-      if (kk > 0) mbar_wait(bar(B_QE), (kk - 1) & 1);
-      if (lt == 0) TRACE(EV_QSTART, gt);
-      {
-        // thread lt copies 16-byte chunk (lt & 15) of rows (lt >> 4) + 8*it, it = 0..31; the
-        // (query, head) of a row advances incrementally (8 rows per step), no divisions
-        const int ch = lt & 15;
-        int rgl = w.m0 + (lt >> 4);
-        int qi = rgl / p.grp, hh = rgl % p.grp;
-        const int step_i = 8 / p.grp, step_h = 8 % p.grp;
-        const __nv_bfloat16* qbase = Qg + ((long long)w.pp * p.n_q) * p.Hq * 128 + (long long)w.g * p.grp * 128 + 8 * ch;
-        const uint32_t dbase = sbase + OFF_Q + (ch >> 3) * 16384;
-#pragma unroll 4
-        for (int it = 0; it < 32; ++it) {
-          const int r = it * 8 + (lt >> 4);
-          const bool ok = rgl < w.rows_total;
-          const __nv_bfloat16* src = qbase + ((long long)qi * p.Hq + hh) * 128;
-          const uint32_t d = dbase + (r >> 7) * kTileBytes + (r & 127) * 128 + (((ch & 7) ^ (r & 7)) << 4);
-          cp_async16(d, ok ? (const void*)src : (const void*)Qg, ok ? 16u : 0u);
-          rgl += 8;
-          qi += step_i;
-          hh += step_h;
-          if (hh >= p.grp) { hh -= p.grp; ++qi; }
-        }
-      }
-      {
-        int qpos[2][8];
-        float4 qpre[2][4];
-#pragma unroll
-        for (int qt = 0; qt < 2; ++qt) {
-          const int row0 = w.m0 + qt * 128 + rg8 * 8;       // global row of the first of the 8 rows
-          int i = row0 / p.grp, hh = row0 % p.grp;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            qpos[qt][k] = (row0 + k < w.rows_total) ? p.q_pos0 + i : -1;
-            if (dbg && c8 == 0 && hh == 0 && qpos[qt][k] >= 0) p.dbg_pos[A + p.R + p.dbg_M + i] = qpos[qt][k];
-            if (++hh == p.grp) { hh = 0; ++i; }
-          }
-          const int p0 = max(qpos[qt][0], 0);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) qpre[qt][j] = rp[(long long)p0 * 32 + 4 * c8 + j];
-        }
-        cp_async_wait_all();
-        named_bar(1, 128);
-        if (lt == 0) TRACE(EV_QLOADED, gt);
-#pragma unroll
-        for (int qt = 0; qt < 2; ++qt)
-          rotate8(sbase + OFF_Q + qt * kTileBytes, rg8 * 8, c8, rp, cth, sth, qpos[qt], qpre[qt],
-                  max(qpos[qt][0], 0));
-      }
-      fence_proxy_async();
-      mbar_arrive(bar(B_Q));
-      if (lt == 0) TRACE(EV_QDONE, gt);
       // ---- K tiles of this item; the table entry of each tile's first row is fetched
       // one tile ahead so the L2 latency is off the rotation's critical path
       int kpos[8];
@@ -827,15 +856,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
         const Item w = decode_item(p, idx);
         const int n = w.n_tiles;
-        mbar_wait(bar(B_Q), kk & 1);
-        if (kk == 0) TRACE(EV_Q, 0);
         mbar_wait(bar(B_KF + gt % KST), (gt / KST) & 1);
         TRACE(EV_KF, gt);
+        mbar_wait(bar(B_Q + 0), kk & 1);
+        if (kk == 0) TRACE(EV_Q, 0);
         tc_fence_after();
         issue_qk(0, gt % KST); mma_commit(bar(B_S + 0));
+        mbar_wait(bar(B_Q + 1), kk & 1);
+        tc_fence_after();
         issue_qk(1, gt % KST); mma_commit(bar(B_S + 1));
         mma_commit(bar(B_KE + gt % KST));
-        if (n == 1) mma_commit(bar(B_QE));
         for (int jj = 0; jj < n; ++jj) {
           const int g = gt + jj, vs = g % VST;
           mbar_wait(bar(B_VF + vs), (g / VST) & 1);
@@ -857,10 +887,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
               }
               issue_qk(qt, ks);
               mma_commit(bar(B_S + qt));
-              if (qt == 1) {
-                mma_commit(bar(B_KE + ks));
-                if (jj + 2 == n) mma_commit(bar(B_QE));   // last QK of the item issued: Q may be reloaded
-              }
+              if (qt == 1) mma_commit(bar(B_KE + ks));
             }
           }
         }

@@ -53,9 +53,18 @@ constexpr int OFF_BAR = OFF_V + VST * kTileBytes;
 // S ready | P ready | O done | O read (epilogue done)
 constexpr int B_Q = 0 /* +qt */, B_KR = 2, B_KF = 5, B_KE = 8, B_VF = 11, B_VE = 13, B_S = 15, B_P = 17, B_O = 19,
               B_OF = 21, B_N = 23;
-// setmaxnreg budget per warpgroup: 2*144 (softmax) + 136 (rotation) + 88 (copy/MMA) = 512 x 128 threads
+// setmaxnreg budget per warpgroup: 2*softmax + rotation + copy/MMA <= 512 (x 128 threads)
+#ifndef DSC_SM1
+#define DSC_SM1 0
+#endif
+#if DSC_SM1
+constexpr int kRegSoftmax = 184, kRegRotate = 104, kRegCopy = 40;
+#else
 constexpr int kRegSoftmax = 144, kRegRotate = 136, kRegCopy = 88;
+#endif
 static_assert(2 * kRegSoftmax + kRegRotate + kRegCopy <= 512, "setmaxnreg budget exceeds the 64K register file");
+constexpr int kThreadRegs = 65536 / kThreads;   // allocation at launch (128); inc above it, dec below it
+static_assert(kRegSoftmax > kThreadRegs && kRegCopy < kThreadRegs, "softmax must grow, copy/MMA must shrink");
 constexpr int kSmemBytes = OFF_BAR + B_N * 8 + 16 + 1024;   // + tmem slot + alignment slack
 constexpr float kRescaleThreshold = 8.0f;     // log2 units (factor 256)
 
@@ -575,6 +584,69 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           continue;
         }
         tc_fence_after();
+#if DSC_SM1
+        // single TMEM read of the whole S row (128 registers), mask in registers
+        uint32_t r[128];
+        tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
+        tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
+        tmem_wait_ld();
+        if (warp == 0 && lane == 0) TRACE(EV_L + 0, g);
+        const bool any_partial = __any_sync(0xffffffffu, !full);
+        if (any_partial) {
+          const unsigned span = (unsigned)max(c_hi - c_lo, 0);
+#pragma unroll
+          for (int c = 0; c < 128; ++c) r[c] = ((unsigned)(c - c_lo) < span) ? r[c] : 0xFF800000u;
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 128; c += 8) {
+          mx0 = fmaxf(mx0, fmaxf(__uint_as_float(r[c]), __uint_as_float(r[c + 1])));
+          mx1 = fmaxf(mx1, fmaxf(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])));
+          mx2 = fmaxf(mx2, fmaxf(__uint_as_float(r[c + 4]), __uint_as_float(r[c + 5])));
+          mx3 = fmaxf(mx3, fmaxf(__uint_as_float(r[c + 6]), __uint_as_float(r[c + 7])));
+        }
+        const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+        const bool upd = m_tile > m + kRescaleThreshold;
+        const bool need_o = upd && (m != -INFINITY);
+        const float f = need_o ? ex2(m - m_tile) : 1.f;
+        if (upd) {
+          lsum2.x *= f; lsum2.y *= f;
+          m = m_tile;
+        }
+        if (__any_sync(0xffffffffu, need_o)) {
+          mbar_wait(bar(B_O + qt), (g - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t o[32];
+            tmem_ld32(tO + ch * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+            tmem_st32(tO + ch * 32, o);
+          }
+          tmem_wait_st();
+        }
+        if (warp == 0 && lane == 0) TRACE(EV_L + 5, g);
+        const float m_use = (m == -INFINITY) ? 0.f : m;
+        const float2 negm2 = make_float2(-m_use, -m_use);
+        float2 l0 = make_float2(0.f, 0.f), l1 = l0;
+#pragma unroll
+        for (int c = 0; c < 128; c += 4) {
+          const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+          const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
+          const float2 p0 = make_float2(ex2(x0.x), ex2(x0.y));
+          const float2 p1 = make_float2(ex2(x1.x), ex2(x1.y));
+          l0 = __fadd2_rn(l0, p0);
+          l1 = __fadd2_rn(l1, p1);
+          r[c >> 1] = pack_bf16(p0.x, p0.y);
+          r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
+        }
+        tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+#else
         // pass 1: row max over the visible columns, two 64-column halves.  In a partial
         // tile the invisible columns are set to -inf and written back to TMEM, so the
         // exp pass needs no mask (2^-inf = 0).
@@ -658,6 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           }
           tmem_st32(tS + 32 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
         }
+#endif
         lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
         if (warp == 0 && lane == 0) TRACE(EV_L + 4, g);
         tmem_wait_st();
@@ -722,7 +795,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     }
   } else if (warp < 12) {
     // ================================================================ rotation (Q per item, then K tiles)
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegRotate));   // 136 > 128 at launch
+    if constexpr (kRegRotate > kThreadRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegRotate));
+    else if constexpr (kRegRotate < kThreadRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegRotate));
     const int lt = threadIdx.x - 256;
     const int c8 = lt & 7;             // frequencies 8*c8 .. 8*c8+7
     const int rg8 = lt >> 3;           // rows rg8*8 .. +7 of a 128-row tile
@@ -806,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           const uint32_t dst = sbase + off + st * kTileBytes;
           if (u == 0) {
             // sink rows [0,A) + self rows [A, A+n_self), zeros elsewhere, with cp.async
-#pragma unroll 4
+#pragma unroll 1
             for (int it = 0; it < 64; ++it) {
               const int id = it * 32 + lane;          // 2048 16-byte chunks
               const int r = id >> 4, ch = id & 15;
@@ -837,19 +911,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       // ============================================================== MMA issuer
       constexpr uint32_t IQK = idesc_bf16(128, 128, 0, 0);   // S = Q K^T, both K-major
       constexpr uint32_t IPV = idesc_bf16(128, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
+      // descriptors advance in the 14-bit start-address field: +32 B (2) per 16-element
+      // K step inside a 128 B swizzle row, +16 KB (1024) to the second 64-column block
       auto issue_qk = [&](int qt, int ks) {
-        const uint32_t qa = sbase + OFF_Q + qt * kTileBytes, kb = sbase + OFF_K + ks * kTileBytes;
-#pragma unroll
+        const uint64_t da = sdesc(sbase + OFF_Q + qt * kTileBytes, 16, 1024);
+        const uint64_t db = sdesc(sbase + OFF_K + ks * kTileBytes, 16, 1024);
+#pragma unroll 1
         for (int k8 = 0; k8 < 8; ++k8) {
-          const uint32_t off = (k8 >> 2) * 16384 + (k8 & 3) * 32;
-          mma_ss(tmem + qt * 128, sdesc(qa + off, 16, 1024), sdesc(kb + off, 16, 1024), IQK, k8 > 0);
+          const uint64_t off = (uint64_t)((k8 >> 2) * 1024 + (k8 & 3) * 2);
+          mma_ss(tmem + qt * 128, da + off, db + off, IQK, k8 > 0);
         }
       };
       auto issue_pv = [&](int qt, int vs, bool acc) {
-        const uint32_t vb = sbase + OFF_V + vs * kTileBytes;
-#pragma unroll
+        const uint64_t dv = sdesc(sbase + OFF_V + vs * kTileBytes, 16384, 1024);
+#pragma unroll 1
         for (int k8 = 0; k8 < 8; ++k8)
-          mma_ts(tmem + 256 + qt * 128, tmem + qt * 128 + k8 * 8, sdesc(vb + k8 * 2048, 16384, 1024), IPV,
+          mma_ts(tmem + 256 + qt * 128, tmem + qt * 128 + k8 * 8, dv + (uint64_t)(k8 * 128), IPV,
                  (acc || k8 > 0) ? 1u : 0u);
       };
       int gt = 0, kk = 0;

@@ -275,6 +275,9 @@ enum { EV_K_ISSUE = 0, EV_V_ISSUE, EV_KR, EV_KF, EV_S0, EV_S1, EV_P0, EV_P1, EV_
 #ifndef DSC_ORDER
 #define DSC_ORDER 1
 #endif
+#ifndef DSC_QFIRST
+#define DSC_QFIRST 0
+#endif
 struct Item {
   int pp, g, mb, sp;
   long long head_row;
@@ -748,6 +751,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         wn = decode_item(p, nidx);
         issue_q_tile(p, wn, qt, lt, qtile);
       }
+      // publish the next item's Q before this item's epilogue, so the tensor core can start
+      // the next item's first S MMAs while O is read out (the MMA waits for B_OF before it
+      // overwrites O with the next item's first PV)
+#if DSC_QFIRST
+      if (nidx < n_items) {
+        rotate_q_tile(p, wn, qt, lt, qtile, 2 + qt);
+        mbar_arrive(bar(B_Q + qt));
+        if (rloc == 0) TRACE(EV_QDONE, gt);
+      }
+#endif
       // epilogue of the item
       const float lsum = lsum2.x + lsum2.y;
       mbar_wait(bar(B_O + qt), (gt - 1) & 1);
@@ -787,11 +800,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           if (hf == 0) p.ws_lse[(long long)w.sp * rows + orow] = lsum > 0.f ? m + __log2f(lsum) : -INFINITY;
         }
       }
+#if !DSC_QFIRST
       if (nidx < n_items) {
         rotate_q_tile(p, wn, qt, lt, qtile, 2 + qt);
         mbar_arrive(bar(B_Q + qt));
         if (rloc == 0) TRACE(EV_QDONE, gt);
       }
+#endif
     }
   } else if (warp < 12) {
     // ================================================================ rotation (Q per item, then K tiles)

@@ -27,9 +27,10 @@ SINK_K, SINK_V = 0, 1          # the A sink tokens (first append)            [A]
 FRM_K, FRM_V = 2, 3            # raw K/V of frame f                           [tpf][Hkv][d]
 INST_Q = 4                     # instant-build queries at step t              [C_t][Hq][d]
 QRY_Q, QRY_K, QRY_V = 5, 6, 7  # query chunk at step t (K/V transient)        [q][Hq|Hkv][d]
+UPD_Q = 8                      # queries of the frame leaving the buffer at t [tpf][Hq][d]
 
 KIND_NAMES = {SINK_K: "SINK_K", SINK_V: "SINK_V", FRM_K: "FRM_K", FRM_V: "FRM_V",
-              INST_Q: "INST_Q", QRY_Q: "QRY_Q", QRY_K: "QRY_K", QRY_V: "QRY_V"}
+              INST_Q: "INST_Q", QRY_Q: "QRY_Q", QRY_K: "QRY_K", QRY_V: "QRY_V", UPD_Q: "UPD_Q"}
 
 
 @dataclasses.dataclass(frozen=True)
@@ -103,6 +104,10 @@ def frame_kv(cfg: StreamConfig, stream: int, layer: int, frame: int):
 
 def instant_q(cfg: StreamConfig, stream: int, layer: int, step: int, n_inst: int):
     return draw(cfg, stream, layer, INST_Q, step, (n_inst, cfg.num_q_heads, cfg.head_dim))
+
+
+def update_q(cfg: StreamConfig, stream: int, layer: int, step: int):
+    return draw(cfg, stream, layer, UPD_Q, step, (cfg.tokens_per_frame, cfg.num_q_heads, cfg.head_dim))
 
 
 def query_qkv(cfg: StreamConfig, stream: int, layer: int, step: int, n_q: int | None = None):

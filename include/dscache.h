@@ -51,8 +51,8 @@ typedef enum {
   DSCACHE_OK = 0,
   DSCACHE_E_ARG = -1,           /* bad argument (null pointer, size, layer range, n_tokens)        */
   DSCACHE_E_CONFIG = -2,        /* invalid configuration at create                                  */
-  DSCACHE_E_POS_OVERFLOW = -3,  /* A+W+C+q_max > max_position (SPEC.md:112's overflow error, raised
-                                   at create: re-based ids never exceed this bound afterwards)      */
+  DSCACHE_E_POS_OVERFLOW = -3,  /* A+W+max(C+q_max, tpf) > max_position (SPEC.md:112's overflow
+                                   error, raised at create: re-based ids never exceed it afterwards) */
   DSCACHE_E_STATE = -4,         /* call out of order (attend before the sink, layers not in step)  */
   DSCACHE_E_CUDA = -5,          /* CUDA runtime error (launch / memcpy)                             */
   DSCACHE_E_OOM = -6            /* device allocation failed                                         */
@@ -79,7 +79,8 @@ typedef struct {
   int32_t instant_frames;   /* l_I: feature-buffer / instant window in frames (C = l_I*tpf)        */
   int32_t max_query_tokens; /* q_max: largest n_q passed to attend                                 */
   int32_t max_position;     /* training length; create fails with E_POS_OVERFLOW if
-                               A + W + C + q_max > max_position                                   */
+                               A + W + max(C + q_max, tpf) > max_position (the largest id of the
+                               attend and of the Eq. 5 update attention)                          */
   double  rope_theta;       /* RoPE base; theta_i = base^(-2i/d)                                   */
   int32_t rope_style;       /* DSCACHE_ROPE_*                                                      */
   int32_t dtype;            /* DSCACHE_DTYPE_*                                                     */
@@ -102,7 +103,7 @@ typedef struct {
 
 /* Create a handle: validates the configuration, allocates the ring
  * [S][N][Hkv][R][d] for K and V (raw, un-rotated), the sink slabs [S][N][Hkv][A][d],
- * and the fp32 RoPE (cos, sin) table built in fp64 for ids 0 .. A+W+C+q_max-1.
+ * and the fp32 RoPE (cos, sin) table built in fp64 for ids 0 .. A+W+max(C+q_max,tpf)-1.
  * The ring is zero-initialised (finite).  Synchronises the device.
  * Errors: E_ARG (null), E_CONFIG (d not in {64,128}, Hq % Hkv, budgets < 0, tpf < 1,
  * bf16 tcgen05 forced on an ineligible shape), E_POS_OVERFLOW, E_OOM, E_CUDA. */
@@ -146,6 +147,21 @@ dscache_status dscache_build_instant(dscache_t h, int32_t layer_begin, int32_t l
 dscache_status dscache_attend(dscache_t h, int32_t layer_begin, int32_t layer_count,
                               const void* q, const void* k_self, const void* v_self, int32_t n_q,
                               void* o, void* stream);
+
+/* Cumulative-update attention of Eq. 5: at step t
+ * the input X_{t-l_I} that just left the buffer is encoded as phi(X_{t-l_I},
+ * [C_a, zeta(U_{t-1})]); this call runs its attention: each of the tpf tokens of frame
+ * e = t - l_I attends to the sink, to zeta(U_{t-1}) = the newest active_frames frames
+ * of the cumulative cache before the update (l_L <= l_U; active_frames
+ * is clamped to the frames U_{t-1} holds), and to the tokens of frame e up to itself.
+ * Ids are consecutive from 0 over that active cache.  The keys are the
+ * raw K/V already in the ring: frames e-l_L .. e are contiguous there (the one slack
+ * frame of the ring keeps the frame Eq. 6 evicts at step t readable during step t).
+ *   q_upd : [S][layer_count][tpf][Hq][d]   queries of frame e's tokens
+ *   o_upd : [S][layer_count][tpf][Hq][d]   output
+ * E_STATE before step l_I (nothing has left the buffer), E_ARG if active_frames < 0. */
+dscache_status dscache_update_attend(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                                     const void* q_upd, void* o_upd, int32_t active_frames, void* stream);
 
 /* Host counters of `layer` (closed form of Eq. 3/5/6 at the latest append). */
 dscache_status dscache_get_state(dscache_t h, int32_t layer, dscache_state* out);

@@ -17,6 +17,9 @@ What it computes (per stream s, per layer r; everything in float64):
 * the final attention over [C_a, U, I] (Eq. 8) plus the query
   chunk itself, again with consecutive position ids from 0 (PAPER.md:236,
   Eq. 2 PAPER.md:141-146);
+* the cumulative-update attention inside phi(X_{t-l_I}, [C_a, zeta(U_{t-1})]) of
+  Eq. 5: the input leaving the buffer attends to the sink, the
+  newest l_L frames of U_{t-1} and itself (SURVEY NEXT-1);
 * position-agnostic encoding (Def. 4.1): keys are kept raw and
   RoPE f(., m) (PAPER.md:124) is applied at use time;
 * softmax attention a_ij = softmax(Q_i K_j / sqrt(D)), with D read
@@ -224,6 +227,33 @@ def attend_output(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], fram
     pos_k = np.arange(ks.shape[0])
     pos_q = L_ctx + np.arange(q.shape[0])
     return gqa_attention(np.asarray(q, np.float64), pos_q, ks, vs, pos_k, theta, style)
+
+
+def cumulative_update_output(t: int, instant_frames: int, past_frames: int, active_frames: int,
+                             sink: Tuple[np.ndarray, np.ndarray], frame_kv: FrameFn, q_upd: np.ndarray,
+                             theta: float, tokens_per_frame: int, style: int = SPLIT_HALF) -> np.ndarray:
+    """The attention inside phi(X_{t-l_I}, [C_a, zeta(U_{t-1})]) of Eq. 5.
+
+    At step t the input X_{t-l_I} leaves the buffer (Eq. 3) and its tokens attend to the
+    sink C_a, to zeta(U_{t-1}) -- "the most recent l_L KV caches" of the cumulative cache
+    before this update (l_L = active_frames frames) -- and to themselves,
+    causally.  Ids are consecutive from 0 over that active cache: sink
+    0..A-1, zeta(U) from A, the frame's token i at A + |zeta(U)| + i.  Requires t >= l_I.
+    q_upd [tpf, Hq, d] -> [tpf, Hq, d].
+    """
+    if t < instant_frames:
+        raise ValueError("no input has left the buffer before step l_I")
+    prev = schedule_fifo(t - 1, instant_frames, past_frames, tokens_per_frame, sink[0].shape[0]) if t >= 1 else None
+    U_prev = list(prev.past_frames) if prev is not None else []
+    zeta = U_prev[len(U_prev) - min(active_frames, len(U_prev)):] if active_frames > 0 else []
+    e = t - instant_frames
+    sk, sv = sink
+    hkv, d = sk.shape[1], sk.shape[2]
+    ks = _cat([sk] + [frame_kv(f)[0] for f in zeta] + [frame_kv(e)[0]], hkv, d)
+    vs = _cat([sv] + [frame_kv(f)[1] for f in zeta] + [frame_kv(e)[1]], hkv, d)
+    pos_k = np.arange(ks.shape[0])
+    pos_q = ks.shape[0] - tokens_per_frame + np.arange(tokens_per_frame)
+    return gqa_attention(np.asarray(q_upd, np.float64), pos_q, ks, vs, pos_k, theta, style)
 
 
 def position_ids(sched: StepSchedule, n_query: int):

@@ -197,9 +197,10 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
     return fail(DSCACHE_E_CONFIG, "rope_style");
   if (!(c.rope_theta > 1.0)) return fail(DSCACHE_E_CONFIG, "rope_theta must be > 1");
   const int64_t W = (int64_t)c.past_frames * c.tokens_per_frame, C = (int64_t)c.instant_frames * c.tokens_per_frame;
-  const int64_t span = c.sink_tokens + W + C + c.max_query_tokens;
+  // largest id any attention applies: attend A+W+C+q_max-1, update attention (Eq. 5) A+W+tpf-1
+  const int64_t span = c.sink_tokens + W + std::max<int64_t>(C + c.max_query_tokens, c.tokens_per_frame);
   if (span > c.max_position)
-    return fail(DSCACHE_E_POS_OVERFLOW, "A+W+C+q_max = " + std::to_string(span) + " exceeds max_position " +
+    return fail(DSCACHE_E_POS_OVERFLOW, "A+W+max(C+q_max,tpf) = " + std::to_string(span) + " exceeds max_position " +
                                             std::to_string(c.max_position));
   if (c.attn_impl == DSCACHE_IMPL_TC && !tc_eligible(c, c.max_query_tokens))
     return fail(DSCACHE_E_CONFIG, "tcgen05 kernel needs bf16, d=128, split-half RoPE, tpf>=128, A+q_max<=128");
@@ -380,6 +381,36 @@ dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q
     }
   }
   return run_attention(h, p, impl, 1, (cudaStream_t)stream);
+}
+
+dscache_status dscache_update_attend(dscache_t h, int32_t lb, int32_t lc, const void* q_upd, void* o_upd,
+                                     int32_t active_frames, void* stream) {
+  dscache_status s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  const dscache_config& c = h->cfg;
+  if (!h->sink_filled[lb] || h->frames[lb] < 1)
+    return fail(DSCACHE_E_STATE, "update_attend before the sink and the first frame were appended");
+  if (active_frames < 0) return fail(DSCACHE_E_ARG, "active_frames must be >= 0");
+  const int64_t t = h->frames[lb] - 1;
+  const int64_t e = t - c.instant_frames;               // the input leaving the buffer at step t
+  if (e < 0) return fail(DSCACHE_E_STATE, "no input has left the buffer yet (step < l_I)");
+  if (!q_upd || !o_upd) return fail(DSCACHE_E_ARG, "null q_upd/o_upd");
+  DeviceGuard dg(c.device);
+  // U_{t-1} holds min(e, l_U) frames (e - min(e,l_U) .. e-1); zeta = the newest nz of them
+  const int64_t nz = std::min<int64_t>({(int64_t)active_frames, (int64_t)c.past_frames, e});
+  dsc::AttnParams p{};
+  fill_common(h, p, lb, lc);
+  p.q = q_upd; p.o = o_upd; p.n_q = c.tokens_per_frame;
+  p.ring_start = (int)(((e - nz) * c.tokens_per_frame) % h->R);
+  p.ring_count = (int)((nz + 1) * c.tokens_per_frame);
+  p.q_pos0 = c.sink_tokens + (int)(nz * c.tokens_per_frame);
+  p.self_k = p.self_v = nullptr; p.n_self = 0;
+  p.dbg_pos = nullptr;
+  p.n_mblocks = (p.n_q * p.grp + 2 * dsc::kTileM - 1) / (2 * dsc::kTileM);
+  // the tcgen05 kernel needs a gap of >= one tile between the window's ends in the ring
+  const int impl = (h->impl_build == DSCACHE_IMPL_TC && h->R - p.ring_count >= dsc::kTileN) ? DSCACHE_IMPL_TC
+                                                                                            : DSCACHE_IMPL_SIMT;
+  return run_attention(h, p, impl, 0, (cudaStream_t)stream);
 }
 
 dscache_status dscache_get_state(dscache_t h, int32_t layer, dscache_state* out) {

@@ -53,7 +53,7 @@ class State(ctypes.Structure):
 
 
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
-           "dscache_attend", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
+           "dscache_attend", "dscache_update_attend", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
            "dscache_attn_impl", "dscache_last_error"]
 
@@ -76,6 +76,7 @@ def load_library(path: str = LIB_PATH):
         "dscache_append_frame": ([P, I32, I32, P, P, I32, P], I32),
         "dscache_build_instant": ([P, I32, I32, P, P, P], I32),
         "dscache_attend": ([P, I32, I32, P, P, P, I32, P, P], I32),
+        "dscache_update_attend": ([P, I32, I32, P, P, I32, P], I32),
         "dscache_get_state": ([P, I32, ctypes.POINTER(State)], I32),
         "dscache_copy_ring": ([P, I32, I32, P, P], I32),
         "dscache_copy_sink": ([P, I32, I32, P, P], I32),
@@ -219,6 +220,22 @@ class DSCache:
         _check(_lib.dscache_attend(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, _ptr(o),
                                    _stream_ptr(stream)))
         return o
+
+    def update_attend(self, q_upd: torch.Tensor, o_upd: Optional[torch.Tensor] = None,
+                      active_frames: Optional[int] = None, layer_begin: int = 0,
+                      layer_count: Optional[int] = None, stream=None) -> torch.Tensor:
+        """Eq. 5 cumulative-update attention of the frame leaving the buffer.
+        q_upd: [S][lc][tpf][Hq][d]; active_frames = l_L (default l_U)."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        shape = (c.num_streams, lc, c.tokens_per_frame, c.num_q_heads, c.head_dim)
+        self._t(q_upd, "q_upd", shape)
+        if o_upd is None:
+            o_upd = torch.empty(shape, dtype=self.torch_dtype, device=self.device)
+        self._t(o_upd, "o_upd", shape)
+        l_L = c.past_frames if active_frames is None else int(active_frames)
+        _check(_lib.dscache_update_attend(self._h, lb, lc, _ptr(q_upd), _ptr(o_upd), l_L, _stream_ptr(stream)))
+        return o_upd
 
     # ------------------------------------------------------------------ introspection
     def state(self, layer: int = 0) -> dict:

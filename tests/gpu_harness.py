@@ -24,7 +24,7 @@ def _batch(cfg, shape_tail, exact, fill, dev, gen):
 
 
 def run_stream(cfg, capture_steps, exact, impl=D.IMPL_AUTO, debug=False, poison=False, ring_capture=(),
-               layer_by_layer=False, n_q=None, past_override=None):
+               layer_by_layer=False, n_q=None, past_override=None, update_lL=None):
     """Returns {t: {(s,l): (o_inst cpu, o cpu)}, "ring": {(t,s,l): (k,v)}, "dbg": {t: (b,a)}, "state": {t: st}}.
 
     past_override(s, l, f) -> (k, v) or None lets a test replace past frames (decoupling test)."""
@@ -82,6 +82,11 @@ def run_stream(cfg, capture_steps, exact, impl=D.IMPL_AUTO, debug=False, poison=
         for (s, l) in exact:
             caps[(s, l)] = (None if o_inst is None else o_inst[s, l].float().cpu(), o[s, l].float().cpu())
         out[t] = caps
+        if update_lL is not None and t >= cfg.instant_frames:
+            qu = _batch(cfg, (tpf, Hq, d), exact, lambda s, l: synth.update_q(cfg, s, l, t), dev, gen)
+            ou = dsc.update_attend(qu, active_frames=update_lL)
+            torch.cuda.synchronize()
+            out.setdefault("upd", {})[t] = {(s, l): ou[s, l].float().cpu() for (s, l) in exact}
         if debug:
             out["dbg"][t] = (dbg_b.cpu().numpy().copy(), dbg_a.cpu().numpy().copy())
         for (s, l) in ring_capture:

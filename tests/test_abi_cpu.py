@@ -60,6 +60,8 @@ def _cfg(dscache, **kw):
 
 @pytest.mark.parametrize("kw,status", [
     (dict(max_position=7000), -3),            # A+W+C+q_max = 7124 > 7000: E_POS_OVERFLOW
+    # l_I = 0: the Eq. 5 update attention reaches id A+W+tpf-1 = 6471 > A+W+C+q_max-1 = 6283
+    (dict(instant_frames=0, max_query_tokens=8, max_position=6300), -3),
     (dict(head_dim=96), -2),                  # E_CONFIG
     (dict(num_q_heads=30), -2),               # Hq % Hkv
     (dict(past_frames=0, instant_frames=0), -2),

@@ -251,6 +251,40 @@ def test_errors_through_the_abi(lib):
     h.close()
 
 
+
+
+@pytest.mark.parametrize("name,l_L,steps", [("c2", 32, [4, 5, 20, 36, 37, 50]), ("c2", 8, [4, 12, 40]),
+                                           ("c5", 32, [4, 35, 36, 127])])
+def test_update_attend_eq5_parity(lib, name, l_L, steps):
+    # NEXT-1: attention inside phi(X_{t-l_I}, [C_a, zeta(U_{t-1})]) (Eq. 5), through the ABI
+    cfg = synth.CONFIGS[name]
+    exact = [(0, 0)] if name == "c2" else [(0, 0), (63, 3)]
+    res = run_stream(cfg, steps, exact, update_lL=l_L)
+    for t in steps:
+        for (s, l) in exact:
+            inp = StreamInputs(cfg, s, l)
+            qu = synth.update_q(cfg, s, l, t).double().numpy()
+            ref = O.cumulative_update_output(t, cfg.instant_frames, cfg.past_frames, l_L, inp.sink(), inp.frame_kv,
+                                             qu, cfg.rope_theta, cfg.tokens_per_frame)
+            ma, rl = assert_close(res["upd"][t][(s, l)], ref, cfg.dtype, f"upd t={t} s={s} l={l} lL={l_L}")
+            REPORT.append((cfg.name + "-upd", "O_upd", t, s, l, ma, rl))
+
+
+def test_update_attend_simt_paths(lib):
+    # fp32 config (SIMT kernel) and l_I = 0 (window may fill the ring: SIMT kernel)
+    for cfg, l_L in ((synth.CONFIGS["c1"], 3), (synth.CONFIGS["c2"].replace(instant_frames=0, tokens_per_frame=128,
+                                                                              past_frames=6, num_frames=12), 6)):
+        steps = [2, 7, 11]
+        res = run_stream(cfg, steps, [(0, 0)], update_lL=l_L)
+        for t in steps:
+            inp = StreamInputs(cfg, 0, 0)
+            qu = synth.update_q(cfg, 0, 0, t).double().numpy()
+            ref = O.cumulative_update_output(t, cfg.instant_frames, cfg.past_frames, l_L, inp.sink(), inp.frame_kv,
+                                             qu, cfg.rope_theta, cfg.tokens_per_frame)
+            ma, rl = assert_close(res["upd"][t][(0, 0)], ref, cfg.dtype, f"upd {cfg.name} t={t}")
+            REPORT.append((cfg.name + "-upd", "O_upd", t, 0, 0, ma, rl))
+
+
 def test_zz_print_report(lib):
     for r in REPORT:
         print("PARITY %-16s %-6s t=%-5d s=%-3d l=%-3d max_abs=%.3e rel_l2=%.3e" % r)

@@ -469,3 +469,62 @@ def test_instant_cache_decoupled_from_past():
     sch2, o_inst2, o2 = oracle_step(cfg, 0, 0, t, inputs=g)
     assert np.array_equal(o_inst, o_inst2)
     assert np.abs(o - o2).max() > 1e-3
+
+
+# --------------------------------------------------------------------------- Eq. 5 update attention (NEXT-1)
+def _upd_cfg():
+    return synth.StreamConfig("upd", 98, 1, 1, 4, 2, 8, 1e4, 3, 2, 4, 2, 3, 12, "fp32", 1.0)
+
+
+@pytest.mark.parametrize("l_L", [0, 2, 4, 9])
+def test_update_attention_brute_force_full_history(l_L):
+    """Eq. 5: phi(X_{t-l_I}, [C_a, zeta(U_{t-1})]); zeta = the newest l_L frames of U_{t-1}
+    (PAPER.md:202).  Reference from the full history: U_{t-1} holds the last min(e, l_U)
+    frames before e = t - l_I, so zeta = frames [e - min(l_L, l_U, e), e); pure-Python loops."""
+    cfg = _upd_cfg()
+    inp = StreamInputs(cfg, 0, 0)
+    sk, sv = inp.sink()
+    A, tpf, lI, lU = cfg.sink_tokens, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames
+    grp = cfg.num_q_heads // cfg.num_kv_heads
+    for t in range(lI, cfg.num_frames):
+        e = t - lI
+        nz = min(l_L, lU, e)
+        frames = list(range(e - nz, e + 1))
+        qu = f64_of(synth.update_q(cfg, 0, 0, t))
+        o = O.cumulative_update_output(t, lI, lU, l_L, (sk, sv), inp.frame_kv, qu, cfg.rope_theta, tpf)
+        for h in range(cfg.num_q_heads):
+            g = h // grp
+            keys = [(j, list(sk[j, g]), list(sv[j, g])) for j in range(A)]
+            n = A
+            for f in frames:
+                fk, fv = inp.frame_kv(f)
+                for j in range(tpf):
+                    keys.append((n, list(fk[j, g]), list(fv[j, g])))
+                    n += 1
+            for i in range(tpf):
+                ref = _brute_attend(list(qu[i, h]), A + nz * tpf + i, keys, cfg.rope_theta)
+                assert np.abs(np.array(ref) - o[i, h]).max() < 1e-12
+
+
+def test_update_attention_zero_query_mean():
+    # Q = 0: token i of the leaving frame sees A + |zeta| + i + 1 keys -> O = their mean V
+    cfg = synth.CONFIGS["c1"]
+    inp = StreamInputs(cfg, 0, 0)
+    sk, sv = inp.sink()
+    tpf, lI, lU = cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames
+    for t, l_L in ((1, 4), (7, 2), (19, 4), (19, 0)):
+        e = t - lI
+        nz = min(l_L, lU, e)
+        vals = np.concatenate([sv] + [inp.frame_kv(f)[1] for f in range(e - nz, e + 1)])
+        o = O.cumulative_update_output(t, lI, lU, l_L, (sk, sv), inp.frame_kv,
+                                       np.zeros((tpf, cfg.num_q_heads, cfg.head_dim)), cfg.rope_theta, tpf)
+        L0 = cfg.sink_tokens + nz * tpf
+        for i in (0, tpf - 1):
+            assert np.abs(o[i, 0] - vals[: L0 + i + 1, 0].mean(0)).max() < 1e-12
+    with pytest.raises(ValueError):
+        O.cumulative_update_output(0, 1, lU, 4, (sk, sv), inp.frame_kv,
+                                   np.zeros((tpf, cfg.num_q_heads, cfg.head_dim)), cfg.rope_theta, tpf)
+
+
+def f64_of(x):
+    return x.double().numpy()

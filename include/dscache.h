@@ -62,7 +62,7 @@ enum { DSCACHE_DTYPE_BF16 = 0, DSCACHE_DTYPE_FP32 = 1 };
 enum { DSCACHE_ROPE_SPLIT_HALF = 0,   /* pairs (i, i+d/2): Qwen2 / LLaVA-OV-7B (reading Q7, default) */
        DSCACHE_ROPE_ADJACENT = 1 };   /* pairs (2i, 2i+1)                                            */
 enum { DSCACHE_IMPL_AUTO = 0,         /* tcgen05 kernel when eligible, else the SIMT kernel          */
-       DSCACHE_IMPL_TC = 1,           /* force tcgen05 (E_CONFIG if the shape is not eligible)       */
+       DSCACHE_IMPL_TC = 1,           /* force tcgen05 (E_CONFIG unless bf16, d=128, split-half, tpf>=128) */
        DSCACHE_IMPL_SIMT = 2 };       /* force the fp32 CUDA-core kernel                             */
 
 typedef struct {
@@ -103,7 +103,7 @@ typedef struct {
 
 /* Create a handle: validates the configuration, allocates the ring
  * [S][N][Hkv][R][d] for K and V (raw, un-rotated), the sink slabs [S][N][Hkv][A][d],
- * and the fp32 RoPE (cos, sin) table built in fp64 for ids 0 .. A+W+max(C+q_max,tpf)-1.
+ * and the fp32 RoPE (cos, sin) table built in fp64 for ids 0 .. max_position-1.
  * The ring is zero-initialised (finite).  Synchronises the device.
  * Errors: E_ARG (null), E_CONFIG (d not in {64,128}, Hq % Hkv, budgets < 0, tpf < 1,
  * bf16 tcgen05 forced on an ineligible shape), E_POS_OVERFLOW, E_OOM, E_CUDA. */
@@ -147,6 +147,20 @@ dscache_status dscache_build_instant(dscache_t h, int32_t layer_begin, int32_t l
 dscache_status dscache_attend(dscache_t h, int32_t layer_begin, int32_t layer_count,
                               const void* q, const void* k_self, const void* v_self, int32_t n_q,
                               void* o, void* stream);
+
+/* Decoding: "autoregressive decoding is performed using
+ * the KV cache C_{t+1}".  The last n_q tokens of a transient self segment of n_self >= n_q
+ * tokens (the query chunk followed by the tokens generated so far; their K/V are used and
+ * discarded) attend over [sink | past | instant | self], causal inside
+ * self; self token j has id A + P_t + C_t + j.  n_q = 1 is one decode step.
+ *   q      : [S][layer_count][n_q][Hq][d]       queries of the last n_q self tokens
+ *   k_self : [S][layer_count][n_self][Hkv][d]   raw K of the self segment
+ *   v_self : [S][layer_count][n_self][Hkv][d]
+ *   o      : [S][layer_count][n_q][Hq][d]
+ * E_ARG unless 1 <= n_q <= n_self; E_POS_OVERFLOW if A + P_t + C_t + n_self > max_position. */
+dscache_status dscache_decode(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                              const void* q, const void* k_self, const void* v_self, int32_t n_self,
+                              int32_t n_q, void* o, void* stream);
 
 /* Cumulative-update attention of Eq. 5: at step t
  * the input X_{t-l_I} that just left the buffer is encoded as phi(X_{t-l_I},

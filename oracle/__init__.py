@@ -7,4 +7,4 @@ from .dscache_oracle import *  # noqa: F401,F403
 from .dscache_oracle import (SPLIT_HALF, ADJACENT, StepSchedule, rope, rope_frequencies,  # noqa: F401
                              softmax_attention, gqa_attention, schedule_fifo, ring_slots,
                              instant_cache_output, attend_output, position_ids,
-                             cumulative_update_output)
+                             cumulative_update_output, decode_output)

@@ -17,6 +17,8 @@ What it computes (per stream s, per layer r; everything in float64):
 * the final attention over [C_a, U, I] (Eq. 8) plus the query
   chunk itself, again with consecutive position ids from 0 (PAPER.md:236,
   Eq. 2 PAPER.md:141-146);
+* decoding over C_{t+1}: the last tokens of [query chunk | generated
+  tokens] attend over [C_a, U, I, self] (SURVEY NEXT-2);
 * the cumulative-update attention inside phi(X_{t-l_I}, [C_a, zeta(U_{t-1})]) of
   Eq. 5: the input leaving the buffer attends to the sink, the
   newest l_L frames of U_{t-1} and itself (SURVEY NEXT-1);
@@ -227,6 +229,23 @@ def attend_output(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], fram
     pos_k = np.arange(ks.shape[0])
     pos_q = L_ctx + np.arange(q.shape[0])
     return gqa_attention(np.asarray(q, np.float64), pos_q, ks, vs, pos_k, theta, style)
+
+
+def decode_output(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], frame_kv: FrameFn,
+                  q_last: np.ndarray, k_self: np.ndarray, v_self: np.ndarray, theta: float,
+                  style: int = SPLIT_HALF) -> np.ndarray:
+    """Decoding over C_{t+1}: the self segment (query chunk followed by the
+    tokens generated so far; n_self tokens, used then discarded PAPER.md:212) extends the
+    context [sink | past | instant] with consecutive ids; q_last are the
+    queries of its last n_q tokens, causal.  q_last [n_q, Hq, d] -> [n_q, Hq, d]."""
+    sk, sv = sink
+    hkv, d = sk.shape[1], sk.shape[2]
+    frames = list(sched.past_frames) + list(sched.instant_frames)
+    ks = _cat([sk] + [frame_kv(f)[0] for f in frames] + [k_self], hkv, d)
+    vs = _cat([sv] + [frame_kv(f)[1] for f in frames] + [v_self], hkv, d)
+    pos_k = np.arange(ks.shape[0])
+    pos_q = ks.shape[0] - q_last.shape[0] + np.arange(q_last.shape[0])
+    return gqa_attention(np.asarray(q_last, np.float64), pos_q, ks, vs, pos_k, theta, style)
 
 
 def cumulative_update_output(t: int, instant_frames: int, past_frames: int, active_frames: int,

@@ -284,6 +284,7 @@ struct Item {
   int m0, rows_total;
   int cnt;            // ring keys needed by this m-block (causal cut)
   int k0, nT;         // first physical ring tile, number of physical tiles
+  int n_extra;        // leading tiles holding sink + self rows (>= 1)
   int t_begin, n_tiles;
 };
 
@@ -319,15 +320,17 @@ __device__ __forceinline__ Item decode_item(const AttnParams& p, int idx) {
     rt = end <= p.R ? (end + 127) / 128 - w.k0 : (w.nT - w.k0) + (end - p.R + 127) / 128;
     rt = min(rt, w.nT);
   }
-  const int total = 1 + rt;
+  w.n_extra = max(1, (p.A + p.n_self + 127) / 128);
+  const int total = w.n_extra + rt;
   w.t_begin = min(w.sp * p.tiles_per_split, total);
   w.n_tiles = min(total, w.t_begin + p.tiles_per_split) - w.t_begin;
   return w;
 }
 
 // Key rows of tile u as (at most) two segments; key row r of segment s has id
-// pos0_s + r.  Tile 0 = sink rows [0, A) + self rows [A, A+n_self); tile u > 0 =
-// physical ring tile (k0 + u - 1) mod nT, valid rows [c_a, c_b).
+// pos0_s + r.  Tiles u < n_extra hold the sink rows (extra index x = 128u + r < A, id x)
+// and then the self rows (A <= x < A + n_self, id ring_count + x); tile u >= n_extra =
+// physical ring tile (k0 + u - n_extra) mod nT, valid rows [c_a, c_b).
 struct TileSeg {
   int lo0, hi0, pos0_0;
   int lo1, hi1, pos0_1;
@@ -336,12 +339,13 @@ struct TileSeg {
 
 __device__ __forceinline__ TileSeg tile_segments(const AttnParams& p, const Item& w, int u) {
   TileSeg t;
-  if (u == 0) {
-    t.lo0 = 0; t.hi0 = p.A; t.pos0_0 = 0;
-    t.lo1 = p.A; t.hi1 = p.A + p.n_self; t.pos0_1 = p.ring_count;
+  if (u < w.n_extra) {
+    const int x0 = 128 * u;
+    t.lo0 = 0; t.hi0 = min(max(p.A - x0, 0), 128); t.pos0_0 = x0;
+    t.lo1 = t.hi0; t.hi1 = min(max(p.A + p.n_self - x0, 0), 128); t.pos0_1 = p.ring_count + x0;
     t.phys = -1;
   } else {
-    int k = w.k0 + u - 1;
+    int k = w.k0 + u - w.n_extra;
     if (k >= w.nT) k -= w.nT;
     int c_a, c_b, rel_a;
     ring_tile_info(k, p.R, p.ring_start, w.cnt, c_a, c_b, rel_a);
@@ -571,9 +575,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         int c_lo, c_hi;
         if (!valid_row) {
           c_lo = 0; c_hi = 0;
-        } else if (u == 0) {
+        } else if (u < w.n_extra) {       // sink always visible, self row j iff its id <= lim
           c_lo = 0;
-          c_hi = min(A + p.n_self, max(A, lim - p.ring_count + 1));
+          c_hi = min(max(min(A + p.n_self, max(A, lim - p.ring_count + 1)) - 128 * u, 0), 128);
         } else {
           const TileSeg t = tile_segments(p, w, u);
           c_lo = t.lo0;
@@ -868,7 +872,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const int r = rg8 * 8 + k;
-            if (kpos[k] >= 0) p.dbg_pos[(u == 0) ? (r < A ? r : A + p.R + (r - A)) : A + t.phys * 128 + r] = kpos[k];
+            const int x = 128 * u + r;
+            if (kpos[k] >= 0) p.dbg_pos[(u < w.n_extra) ? (x < A ? x : A + p.R + (x - A)) : A + t.phys * 128 + r] = kpos[k];
           }
         }
       }
@@ -893,15 +898,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           const int g = gt + jj, u = w.t_begin + jj, st = g % nst;
           if (g >= nst) mbar_wait(bar(b_free + st), ((g - nst) / nst) & 1);
           const uint32_t dst = sbase + off + st * kTileBytes;
-          if (u == 0) {
-            // sink rows [0,A) + self rows [A, A+n_self), zeros elsewhere, with cp.async
+          if (u < w.n_extra) {
+            // sink rows (x < A) + self rows (A <= x < A + n_self), zeros elsewhere, with cp.async
 #pragma unroll 1
             for (int it = 0; it < 64; ++it) {
               const int id = it * 32 + lane;          // 2048 16-byte chunks
               const int r = id >> 4, ch = id & 15;
+              const int x = 128 * u + r;
               const __nv_bfloat16* src = nullptr;
-              if (r < A) src = SX + (w.head_row * A + r) * 128;
-              else if (r < A + p.n_self) src = XX + (((long long)w.pp * p.n_self + (r - A)) * p.Hkv + w.g) * 128;
+              if (x < A) src = SX + (w.head_row * A + x) * 128;
+              else if (x < A + p.n_self) src = XX + (((long long)w.pp * p.n_self + (x - A)) * p.Hkv + w.g) * 128;
               const uint32_t d = dst + (ch >> 3) * 16384 + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
               cp_async16(d, src ? (const void*)(src + 8 * ch) : (const void*)SX, src ? 16u : 0u);
             }
@@ -910,7 +916,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(b_full + st));
           } else if (lane == 0) {
-            int phys = w.k0 + u - 1;
+            int phys = w.k0 + u - w.n_extra;
             if (phys >= w.nT) phys -= w.nT;
             const int row = (int)(w.head_row * p.R) + phys * 128;
             mbar_arrive_tx(bar(b_full + st), kTileBytes);

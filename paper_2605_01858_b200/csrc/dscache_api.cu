@@ -123,9 +123,9 @@ dscache_status check_layers(dscache_t h, int lb, int lc) {
   return DSCACHE_OK;
 }
 
-bool tc_eligible(const dscache_config& c, int n_self_max) {
+bool tc_eligible(const dscache_config& c) {
   return c.dtype == DSCACHE_DTYPE_BF16 && c.head_dim == 128 && c.rope_style == DSCACHE_ROPE_SPLIT_HALF &&
-         c.tokens_per_frame >= dsc::kTileN && c.sink_tokens + n_self_max <= dsc::kTileN;
+         c.tokens_per_frame >= dsc::kTileN;
 }
 
 void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
@@ -202,8 +202,8 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   if (span > c.max_position)
     return fail(DSCACHE_E_POS_OVERFLOW, "A+W+max(C+q_max,tpf) = " + std::to_string(span) + " exceeds max_position " +
                                             std::to_string(c.max_position));
-  if (c.attn_impl == DSCACHE_IMPL_TC && !tc_eligible(c, c.max_query_tokens))
-    return fail(DSCACHE_E_CONFIG, "tcgen05 kernel needs bf16, d=128, split-half RoPE, tpf>=128, A+q_max<=128");
+  if (c.attn_impl == DSCACHE_IMPL_TC && !tc_eligible(c))
+    return fail(DSCACHE_E_CONFIG, "tcgen05 kernel needs bf16, d=128, split-half RoPE, tpf>=128");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || c.device < 0 || c.device >= ndev) {
     cudaGetLastError();
@@ -216,7 +216,7 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   h->W = (int)W; h->C = (int)C;
   h->R = (int)(W + C + c.tokens_per_frame);
   h->elem = c.dtype == DSCACHE_DTYPE_BF16 ? 2 : 4;
-  h->npos = (int)span;
+  h->npos = c.max_position;   // RoPE table covers every id < max_position (decode ids grow per token)
   h->frames.assign(c.num_layers, 0);
   h->sink_filled.assign(c.num_layers, c.sink_tokens == 0 ? 1 : 0);
   h->last_evicted.assign(c.num_layers, -1);
@@ -224,8 +224,8 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   if (c.attn_impl == DSCACHE_IMPL_SIMT) {
     h->impl_build = h->impl_attend = DSCACHE_IMPL_SIMT;
   } else {
-    h->impl_build = tc_eligible(c, 0) ? DSCACHE_IMPL_TC : DSCACHE_IMPL_SIMT;
-    h->impl_attend = tc_eligible(c, c.max_query_tokens) ? DSCACHE_IMPL_TC : DSCACHE_IMPL_SIMT;
+    h->impl_build = tc_eligible(c) ? DSCACHE_IMPL_TC : DSCACHE_IMPL_SIMT;
+    h->impl_attend = h->impl_build;
   }
 
   const size_t heads = (size_t)c.num_streams * c.num_layers * c.num_kv_heads;
@@ -330,24 +330,29 @@ dscache_status dscache_build_instant(dscache_t h, int32_t lb, int32_t lc, const 
   return run_attention(h, p, h->impl_build, 0, (cudaStream_t)stream);
 }
 
-dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
-                              const void* v_self, int32_t n_q, void* o, void* stream) {
+namespace {
+// Attention of n_q query rows over [sink | past | instant | self], where the self segment
+// holds n_self >= n_q transient tokens (the query chunk, and during decode the tokens
+// generated so far) and the queries are its last n_q tokens.
+dscache_status attend_common(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                             const void* v_self, int32_t n_self, int32_t n_q, void* o, void* stream, bool dbg) {
   dscache_status s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
   if (!h->sink_filled[lb] || h->frames[lb] < 1)
     return fail(DSCACHE_E_STATE, "attend before the sink and the first frame were appended");
-  if (n_q < 1 || n_q > h->cfg.max_query_tokens)
-    return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
+  if (n_q < 1 || n_q > n_self) return fail(DSCACHE_E_ARG, "need 1 <= n_q <= n_self");
   if (!q || !k_self || !v_self || !o) return fail(DSCACHE_E_ARG, "null q/k_self/v_self/o");
   DeviceGuard dg(h->cfg.device);
   const Schedule sc = h->schedule(lb);
+  if ((int64_t)h->cfg.sink_tokens + sc.P_t + sc.C_t + n_self > h->cfg.max_position)
+    return fail(DSCACHE_E_POS_OVERFLOW, "A + P_t + C_t + n_self exceeds max_position");
   dsc::AttnParams p{};
   fill_common(h, p, lb, lc);
   p.q = q; p.o = o; p.n_q = n_q;
   p.ring_start = sc.ring_start; p.ring_count = sc.P_t + sc.C_t;
-  p.q_pos0 = h->cfg.sink_tokens + p.ring_count;
-  p.self_k = k_self; p.self_v = v_self; p.n_self = n_q;
-  p.dbg_pos = h->dbg_attend;
+  p.q_pos0 = h->cfg.sink_tokens + p.ring_count + (n_self - n_q);
+  p.self_k = k_self; p.self_v = v_self; p.n_self = n_self;
+  p.dbg_pos = dbg ? h->dbg_attend : nullptr;
   p.n_mblocks = (p.n_q * p.grp + 2 * dsc::kTileM - 1) / (2 * dsc::kTileM);
   const int impl = h->impl_attend;
   if (impl == DSCACHE_IMPL_TC) {
@@ -361,7 +366,7 @@ dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q
       ring_tiles = end <= R ? (end + BN - 1) / BN - k0 : (nT - k0) + (end - R + BN - 1) / BN;
       ring_tiles = std::min(ring_tiles, nT);
     }
-    const int tiles = 1 + ring_tiles;
+    const int tiles = std::max(1, (p.A + n_self + BN - 1) / BN) + ring_tiles;
     const int items = p.P * p.Hkv * p.n_mblocks;
     int splits = 1;
     if (items < h->num_sms) {
@@ -381,6 +386,19 @@ dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q
     }
   }
   return run_attention(h, p, impl, 1, (cudaStream_t)stream);
+}
+}  // namespace
+
+dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                              const void* v_self, int32_t n_q, void* o, void* stream) {
+  if (h && (n_q < 1 || n_q > h->cfg.max_query_tokens))
+    return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
+  return attend_common(h, lb, lc, q, k_self, v_self, n_q, n_q, o, stream, true);
+}
+
+dscache_status dscache_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                              const void* v_self, int32_t n_self, int32_t n_q, void* o, void* stream) {
+  return attend_common(h, lb, lc, q, k_self, v_self, n_self, n_q, o, stream, false);
 }
 
 dscache_status dscache_update_attend(dscache_t h, int32_t lb, int32_t lc, const void* q_upd, void* o_upd,

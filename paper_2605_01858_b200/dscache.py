@@ -53,7 +53,7 @@ class State(ctypes.Structure):
 
 
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
-           "dscache_attend", "dscache_update_attend", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
+           "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
            "dscache_attn_impl", "dscache_last_error"]
 
@@ -77,6 +77,7 @@ def load_library(path: str = LIB_PATH):
         "dscache_build_instant": ([P, I32, I32, P, P, P], I32),
         "dscache_attend": ([P, I32, I32, P, P, P, I32, P, P], I32),
         "dscache_update_attend": ([P, I32, I32, P, P, I32, P], I32),
+        "dscache_decode": ([P, I32, I32, P, P, P, I32, I32, P, P], I32),
         "dscache_get_state": ([P, I32, ctypes.POINTER(State)], I32),
         "dscache_copy_ring": ([P, I32, I32, P, P], I32),
         "dscache_copy_sink": ([P, I32, I32, P, P], I32),
@@ -218,6 +219,23 @@ class DSCache:
             o = torch.empty(q.shape, dtype=self.torch_dtype, device=self.device)
         self._t(o, "o", q.shape)
         _check(_lib.dscache_attend(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, _ptr(o),
+                                   _stream_ptr(stream)))
+        return o
+
+    def decode(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, o: Optional[torch.Tensor] = None,
+               layer_begin: int = 0, layer_count: Optional[int] = None, stream=None) -> torch.Tensor:
+        """Decode (NEXT-2): q [S][lc][n_q][Hq][d] = the last n_q tokens of the self segment
+        k_self/v_self [S][lc][n_self][Hkv][d] (query chunk + generated tokens)."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        n_q, n_self = int(q.shape[2]), int(k_self.shape[2])
+        self._t(q, "q", (c.num_streams, lc, n_q, c.num_q_heads, c.head_dim))
+        self._t(k_self, "k_self", (c.num_streams, lc, n_self, c.num_kv_heads, c.head_dim))
+        self._t(v_self, "v_self", k_self.shape)
+        if o is None:
+            o = torch.empty(q.shape, dtype=self.torch_dtype, device=self.device)
+        self._t(o, "o", q.shape)
+        _check(_lib.dscache_decode(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_self, n_q, _ptr(o),
                                    _stream_ptr(stream)))
         return o
 

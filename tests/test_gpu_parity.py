@@ -285,6 +285,35 @@ def test_update_attend_simt_paths(lib):
             REPORT.append((cfg.name + "-upd", "O_upd", t, 0, 0, ma, rl))
 
 
+
+
+@pytest.mark.parametrize("n_self,n_q", [(64 + 1, 1), (64 + 40, 1), (300, 5), (64, 64)])
+def test_decode_parity(lib, n_self, n_q):
+    # NEXT-2: the last n_q tokens of [query chunk | generated] over [sink|past|instant|self]
+    import torch as _t
+    cfg = synth.CONFIGS["c2"].replace(num_frames=40)
+    t = 39
+    dev = _t.device("cuda", 0)
+    h = D.DSCache.from_config(cfg)
+    sk, sv = synth.sink_kv(cfg, 0, 0)
+    h.append_frame(sk[None, None].to(dev), sv[None, None].to(dev))
+    for f in range(t + 1):
+        k, v = synth.frame_kv(cfg, 0, 0, f)
+        h.append_frame(k[None, None].to(dev), v[None, None].to(dev))
+    g = _t.Generator().manual_seed(n_self)
+    ks = (_t.randn(n_self, 4, 128, generator=g) * 0.5).to(_t.bfloat16)
+    vs = (_t.randn(n_self, 4, 128, generator=g) * 0.5).to(_t.bfloat16)
+    q = (_t.randn(n_q, 28, 128, generator=g) * 0.5).to(_t.bfloat16)
+    o = h.decode(q[None, None].to(dev), ks[None, None].to(dev), vs[None, None].to(dev))
+    _t.cuda.synchronize()
+    inp = StreamInputs(cfg, 0, 0)
+    ref = O.decode_output(step_schedule(cfg, t), inp.sink(), inp.frame_kv, q.double().numpy(), ks.double().numpy(),
+                          vs.double().numpy(), cfg.rope_theta)
+    ma, rl = assert_close(o[0, 0].float().cpu(), ref, "bf16", f"decode n_self={n_self} n_q={n_q}")
+    REPORT.append(("c2-decode", "O_dec", t, n_self, n_q, ma, rl))
+    h.close()
+
+
 def test_zz_print_report(lib):
     for r in REPORT:
         print("PARITY %-16s %-6s t=%-5d s=%-3d l=%-3d max_abs=%.3e rel_l2=%.3e" % r)

@@ -528,3 +528,47 @@ def test_update_attention_zero_query_mean():
 
 def f64_of(x):
     return x.double().numpy()
+
+
+# --------------------------------------------------------------------------- decode (NEXT-2)
+def test_decode_equals_attend_when_self_is_the_query_chunk():
+    # n_q = n_self: decode_output is the Eq. 8 attend itself
+    cfg = synth.CONFIGS["c1"]
+    inp = StreamInputs(cfg, 0, 0)
+    sch = step_schedule(cfg, 9)
+    q, ks, vs = inp.query(9)
+    a = O.attend_output(sch, inp.sink(), inp.frame_kv, q, ks, vs, cfg.rope_theta)
+    b = O.decode_output(sch, inp.sink(), inp.frame_kv, q, ks, vs, cfg.rope_theta)
+    assert np.array_equal(a, b)
+
+
+def test_decode_token_by_token_matches_brute_force():
+    """A decode step (n_q = 1) after g generated tokens == pure-Python attention of that
+    token over sink + window + query chunk + generated tokens, ids consecutive."""
+    cfg = _upd_cfg()
+    inp = StreamInputs(cfg, 0, 0)
+    t = 10
+    sch = step_schedule(cfg, t)
+    sk, sv = inp.sink()
+    q, kq, vq = inp.query(t)
+    gen = np.random.default_rng(3)
+    kg = gen.standard_normal((4, cfg.num_kv_heads, cfg.head_dim))
+    vg = gen.standard_normal((4, cfg.num_kv_heads, cfg.head_dim))
+    qg = gen.standard_normal((4, cfg.num_q_heads, cfg.head_dim))
+    grp = cfg.num_q_heads // cfg.num_kv_heads
+    frames = sch.past_frames + sch.instant_frames
+    for g in range(4):
+        k_self = np.concatenate([kq, kg[: g + 1]]); v_self = np.concatenate([vq, vg[: g + 1]])
+        o = O.decode_output(sch, (sk, sv), inp.frame_kv, qg[g:g + 1], k_self, v_self, cfg.rope_theta)
+        for h in range(cfg.num_q_heads):
+            gh = h // grp
+            keys = [(j, list(sk[j, gh]), list(sv[j, gh])) for j in range(cfg.sink_tokens)]
+            n = cfg.sink_tokens
+            for f in frames:
+                fk, fv = inp.frame_kv(f)
+                for j in range(cfg.tokens_per_frame):
+                    keys.append((n, list(fk[j, gh]), list(fv[j, gh]))); n += 1
+            for j in range(len(k_self)):
+                keys.append((n, list(k_self[j, gh]), list(v_self[j, gh]))); n += 1
+            ref = _brute_attend(list(qg[g, h]), n - 1, keys, cfg.rope_theta)
+            assert np.abs(np.array(ref) - o[0, h]).max() < 1e-12

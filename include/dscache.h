@@ -135,6 +135,16 @@ dscache_status dscache_append_frame(dscache_t h, int32_t layer_begin, int32_t la
 dscache_status dscache_build_instant(dscache_t h, int32_t layer_begin, int32_t layer_count,
                                      const void* q_inst, void* o_inst, void* stream);
 
+/* Approximate instant cache: between the periodic full
+ * rebuilds (dscache_build_instant, the "refresh"), only the newest frame's instant rows are
+ * computed and the older rows are reused, so the per-step build costs O(C*tpf) instead of
+ * O(C^2).  The rows are exactly the last tpf rows of dscache_build_instant at this step:
+ * token j of frame t attends to the sink and to the instant window up to itself.
+ *   q_new : [S][layer_count][tpf][Hq][d] ; o_new : [S][layer_count][tpf][Hq][d]
+ * E_STATE before the sink and the first frame; E_CONFIG when l_I = 0. */
+dscache_status dscache_build_instant_newest(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                                            const void* q_new, void* o_new, void* stream);
+
 /* Attention of an n_q-token query chunk over [C_a | U | I | self] (Eq. 8 plus the
  * chunk's own K/V, which are used and then discarded: PAPER.md:212/699).  Ids:
  * sink 0..A-1, past+instant A..A+P_t+C_t-1 (oldest first), query/self token i at

@@ -330,6 +330,28 @@ dscache_status dscache_build_instant(dscache_t h, int32_t lb, int32_t lc, const 
   return run_attention(h, p, h->impl_build, 0, (cudaStream_t)stream);
 }
 
+dscache_status dscache_build_instant_newest(dscache_t h, int32_t lb, int32_t lc, const void* q_new, void* o_new,
+                                            void* stream) {
+  dscache_status s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  if (!h->sink_filled[lb] || h->frames[lb] < 1)
+    return fail(DSCACHE_E_STATE, "build_instant_newest before the sink and the first frame were appended");
+  if (h->cfg.instant_frames < 1) return fail(DSCACHE_E_CONFIG, "l_I = 0: there is no instant cache");
+  if (!q_new || !o_new) return fail(DSCACHE_E_ARG, "null q_new/o_new");
+  DeviceGuard dg(h->cfg.device);
+  const Schedule sc = h->schedule(lb);
+  const int tpf = h->cfg.tokens_per_frame;
+  dsc::AttnParams p{};
+  fill_common(h, p, lb, lc);
+  p.q = q_new; p.o = o_new; p.n_q = tpf;
+  p.q_pos0 = h->cfg.sink_tokens + sc.C_t - tpf;   // the newest frame's tokens are the last tpf instant ids
+  p.ring_start = sc.inst_start; p.ring_count = sc.C_t;
+  p.self_k = p.self_v = nullptr; p.n_self = 0;
+  p.dbg_pos = nullptr;
+  p.n_mblocks = (p.n_q * p.grp + 2 * dsc::kTileM - 1) / (2 * dsc::kTileM);
+  return run_attention(h, p, h->impl_build, 0, (cudaStream_t)stream);
+}
+
 namespace {
 // Attention of n_q query rows over [sink | past | instant | self], where the self segment
 // holds n_self >= n_q transient tokens (the query chunk, and during decode the tokens

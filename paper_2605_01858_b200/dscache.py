@@ -53,7 +53,7 @@ class State(ctypes.Structure):
 
 
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
-           "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
+           "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
            "dscache_attn_impl", "dscache_last_error"]
 
@@ -78,6 +78,7 @@ def load_library(path: str = LIB_PATH):
         "dscache_attend": ([P, I32, I32, P, P, P, I32, P, P], I32),
         "dscache_update_attend": ([P, I32, I32, P, P, I32, P], I32),
         "dscache_decode": ([P, I32, I32, P, P, P, I32, I32, P, P], I32),
+        "dscache_build_instant_newest": ([P, I32, I32, P, P, P], I32),
         "dscache_get_state": ([P, I32, ctypes.POINTER(State)], I32),
         "dscache_copy_ring": ([P, I32, I32, P, P], I32),
         "dscache_copy_sink": ([P, I32, I32, P, P], I32),
@@ -221,6 +222,19 @@ class DSCache:
         _check(_lib.dscache_attend(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, _ptr(o),
                                    _stream_ptr(stream)))
         return o
+
+    def build_instant_newest(self, q_new: torch.Tensor, o_new: Optional[torch.Tensor] = None,
+                             layer_begin: int = 0, layer_count: Optional[int] = None, stream=None) -> torch.Tensor:
+        """Approximate instant cache (NEXT-3): only the newest frame's instant rows."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        shape = (c.num_streams, lc, c.tokens_per_frame, c.num_q_heads, c.head_dim)
+        self._t(q_new, "q_new", shape)
+        if o_new is None:
+            o_new = torch.empty(shape, dtype=self.torch_dtype, device=self.device)
+        self._t(o_new, "o_new", shape)
+        _check(_lib.dscache_build_instant_newest(self._h, lb, lc, _ptr(q_new), _ptr(o_new), _stream_ptr(stream)))
+        return o_new
 
     def decode(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, o: Optional[torch.Tensor] = None,
                layer_begin: int = 0, layer_count: Optional[int] = None, stream=None) -> torch.Tensor:

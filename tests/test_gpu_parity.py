@@ -314,6 +314,43 @@ def test_decode_parity(lib, n_self, n_q):
     h.close()
 
 
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c5"])
+def test_build_instant_newest_parity(lib, name):
+    # NEXT-3: the incremental instant rows == the last tpf rows of the exact Eq. 7 build
+    import torch as _t
+    cfg = synth.CONFIGS[name]
+    steps = [0, 2, 3, 10, cfg.num_frames - 1]
+    dev = _t.device("cuda", 0)
+    exact = [(0, 0)] if cfg.num_streams == 1 else [(0, 0), (63, 3)]
+    h = D.DSCache.from_config(cfg)
+    S, N, tpf = cfg.num_streams, cfg.num_layers, cfg.tokens_per_frame
+    def batch(fn, shape):
+        t_ = (_t.randn((S, N) + shape, device=dev) * cfg.scale).to(cfg.torch_dtype)
+        for (s_, l_) in exact:
+            t_[s_, l_] = fn(s_, l_).to(dev)
+        return t_
+    shp = (cfg.sink_tokens, cfg.num_kv_heads, cfg.head_dim)
+    h.append_frame(batch(lambda s_, l_: synth.sink_kv(cfg, s_, l_)[0], shp),
+                   batch(lambda s_, l_: synth.sink_kv(cfg, s_, l_)[1], shp))
+    for t in range(max(steps) + 1):
+        fshp = (tpf, cfg.num_kv_heads, cfg.head_dim)
+        kv = {sl: synth.frame_kv(cfg, sl[0], sl[1], t) for sl in exact}
+        h.append_frame(batch(lambda s_, l_: kv[(s_, l_)][0], fshp), batch(lambda s_, l_: kv[(s_, l_)][1], fshp))
+        if t not in steps:
+            continue
+        C_t = h.state(0)["instant_tokens"]
+        qn = batch(lambda s_, l_: synth.instant_q(cfg, s_, l_, t, C_t)[C_t - tpf:], (tpf, cfg.num_q_heads, cfg.head_dim))
+        o = h.build_instant_newest(qn)
+        _t.cuda.synchronize()
+        for (s_, l_) in exact:
+            sch, o_inst, _ = oracle_step(cfg, s_, l_, t)
+            ma, rl = assert_close(o[s_, l_].float().cpu(), o_inst[sch.C_t - tpf:], cfg.dtype, f"newest t={t}")
+            REPORT.append((name + "-newest", "O_new", t, s_, l_, ma, rl))
+    h.close()
+
+
 def test_zz_print_report(lib):
     for r in REPORT:
         print("PARITY %-16s %-6s t=%-5d s=%-3d l=%-3d max_abs=%.3e rel_l2=%.3e" % r)

@@ -159,12 +159,22 @@ def stream_range(S: int, world: int, rank: int):
 def run_ours(args, cfg, world, rank, local):
     from paper_2605_01858_b200 import dscache as D
     dev = torch.device("cuda", local)
-    lo, hi = stream_range(cfg.num_streams, world, rank)
-    S = hi - lo
-    lcfg = cfg.replace(num_streams=S)
-    dsc = D.DSCache.from_config(lcfg, device=local)
+    kvsplit = args.mode == "kvsplit"
+    if kvsplit:
+        # P2: one stream, rank r holds KV heads [r*Hkv/G, (r+1)*Hkv/G) and their q heads
+        from paper_2605_01858_b200.dist import kv_head_partition
+        kv_lo, kv_n, q_lo, q_n = kv_head_partition(cfg.num_q_heads, cfg.num_kv_heads, world, rank)
+        cfg = cfg.replace(num_streams=1)
+        lcfg = cfg.replace(num_q_heads=q_n, num_kv_heads=kv_n)
+        S = 1
+        dsc = D.DSCache.from_config(lcfg, device=local, kv_head_offset=kv_lo)
+    else:
+        lo, hi = stream_range(cfg.num_streams, world, rank)
+        S = hi - lo
+        lcfg = cfg.replace(num_streams=S)
+        dsc = D.DSCache.from_config(lcfg, device=local)
     A, P, C, q = steady_counts(cfg)
-    N, Hq, Hkv, d, tpf = cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.tokens_per_frame
+    N, Hq, Hkv, d, tpf = cfg.num_layers, lcfg.num_q_heads, lcfg.num_kv_heads, cfg.head_dim, cfg.tokens_per_frame
     dt = cfg.torch_dtype
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
@@ -187,12 +197,17 @@ def run_ours(args, cfg, world, rank, local):
         dsc.append_frame(*frames[t % POOL])
     tcount = [fill]
 
+    gathered = [None]
+
     def step(i):
         t = tcount[0]
         dsc.append_frame(*frames[t % POOL])
         dsc.build_instant(q_inst[i & 1], o_inst)
         qq = qry[i & 1]
         dsc.attend(qq[0], qq[1], qq[2], o)
+        if kvsplit and world > 1:           # the only exchange of P2: head-major all-gather of O
+            from paper_2605_01858_b200.dist import gather_heads
+            gathered[0] = gather_heads(o)
         tcount[0] += 1
 
     ring_bytes = 2 * S * N * Hkv * dsc.R * d * (2 if cfg.dtype == "bf16" else 4)
@@ -238,7 +253,7 @@ def run_ours(args, cfg, world, rank, local):
     impl = dsc.attn_impl()
     dsc.close()
 
-    fb, fa = flops_per_unit(cfg)
+    fb, fa = flops_per_unit(lcfg)
     units = S * N
     frames_total = cfg.num_streams * args.steps
     value = frames_total / (t_max / 1e3)
@@ -263,7 +278,9 @@ def run_ours(args, cfg, world, rank, local):
         "config": {"workload": f"{cfg.name}: {cfg.num_streams} streams x {cfg.num_layers} layers, Hq={Hq} Hkv={Hkv} "
                                f"d={d}, tpf={tpf}, A={A}, W={cfg.past_frames}f, C={cfg.instant_frames}f, q={q}",
                    "config_id": cfg.name, "streams": cfg.num_streams, "layers": N, "query_tokens": q,
-                   "parallelism": f"stream partition x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"KV-head split x{world} (NCCL all-gather of O)" if kvsplit else
+                                   f"stream partition x{world}") if world > 1 else "single GPU",
+                   "mode": args.mode,
                    "l2": "flushed between steps" if flush else "inputs larger than L2 (ring %.2f GB)" % (ring_bytes / 1e9),
                    "steady_state": True, "input_pool": f"{POOL} distinct frames cycled (positions never repeat)"},
         "frames_per_s_per_stream": round(value / cfg.num_streams, 3),
@@ -390,6 +407,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="streams", choices=["streams", "kvsplit"],
+                    help="streams: P1 stream partition (default); kvsplit: P2 KV-head split of one stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()

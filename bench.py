@@ -199,12 +199,17 @@ def run_ours(args, cfg, world, rank, local):
 
     gathered = [None]
 
+    fused = args.api == "fused"
+
     def step(i):
         t = tcount[0]
-        dsc.append_frame(*frames[t % POOL])
-        dsc.build_instant(q_inst[i & 1], o_inst)
         qq = qry[i & 1]
-        dsc.attend(qq[0], qq[1], qq[2], o)
+        if fused:       # dscache_step: append + build_instant + attend, one attention launch
+            dsc.step(*frames[t % POOL], q_inst[i & 1], qq[0], qq[1], qq[2], o_inst=o_inst, o=o)
+        else:
+            dsc.append_frame(*frames[t % POOL])
+            dsc.build_instant(q_inst[i & 1], o_inst)
+            dsc.attend(qq[0], qq[1], qq[2], o)
         if kvsplit and world > 1:           # the only exchange of P2: head-major all-gather of O
             from paper_2605_01858_b200.dist import gather_heads
             gathered[0] = gather_heads(o)
@@ -249,7 +254,7 @@ def run_ours(args, cfg, world, rank, local):
 
     # e2e: the same step through the public API with pinned host buffers, H2D of every
     # input of the step and D2H of the query answer O inside the timed region
-    e2e = run_e2e(args, cfg, dsc, S, dev, stream, world)
+    e2e = run_e2e(args, cfg, lcfg, dsc, S, dev, stream, world, kvsplit)
     impl = dsc.attn_impl()
     dsc.close()
 
@@ -280,7 +285,7 @@ def run_ours(args, cfg, world, rank, local):
                    "config_id": cfg.name, "streams": cfg.num_streams, "layers": N, "query_tokens": q,
                    "parallelism": (f"KV-head split x{world} (NCCL all-gather of O)" if kvsplit else
                                    f"stream partition x{world}") if world > 1 else "single GPU",
-                   "mode": args.mode,
+                   "mode": args.mode, "api": args.api,
                    "l2": "flushed between steps" if flush else "inputs larger than L2 (ring %.2f GB)" % (ring_bytes / 1e9),
                    "steady_state": True, "input_pool": f"{POOL} distinct frames cycled (positions never repeat)"},
         "frames_per_s_per_stream": round(value / cfg.num_streams, 3),
@@ -300,8 +305,8 @@ def run_ours(args, cfg, world, rank, local):
     return line
 
 
-def run_e2e(args, cfg, dsc, S, dev, stream, world):
-    N, Hq, Hkv, d, tpf = cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.tokens_per_frame
+def run_e2e(args, cfg, lcfg, dsc, S, dev, stream, world, kvsplit):
+    N, Hq, Hkv, d, tpf = cfg.num_layers, lcfg.num_q_heads, lcfg.num_kv_heads, cfg.head_dim, cfg.tokens_per_frame
     A, P, C, q = steady_counts(cfg)
     dt = cfg.torch_dtype
     steps = max(3, min(args.steps, 10))
@@ -311,15 +316,25 @@ def run_e2e(args, cfg, dsc, S, dev, stream, world):
     hk, hv = host(S, N, tpf, Hkv, d), host(S, N, tpf, Hkv, d)
     hqi = host(S, N, C, Hq, d)
     hq, hks, hvs = host(S, N, q, Hq, d), host(S, N, q, Hkv, d), host(S, N, q, Hkv, d)
-    ho = torch.empty(S, N, q, Hq, d, dtype=dt).pin_memory()
+    ho = torch.empty(S, N, q, Hq * (world if kvsplit else 1), d, dtype=dt).pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in (hk, hv, hqi, hq, hks, hvs))
     d2h = ho.numel() * ho.element_size()
+    fused = args.api == "fused"
 
     def one():
         k = hk.to(dev, non_blocking=True); v = hv.to(dev, non_blocking=True)
-        dsc.append_frame(k, v)
-        oi = dsc.build_instant(hqi.to(dev, non_blocking=True))
-        o = dsc.attend(hq.to(dev, non_blocking=True), hks.to(dev, non_blocking=True), hvs.to(dev, non_blocking=True))
+        qi = hqi.to(dev, non_blocking=True)
+        qq, ks, vs = (hq.to(dev, non_blocking=True), hks.to(dev, non_blocking=True),
+                      hvs.to(dev, non_blocking=True))
+        if fused:
+            oi, o = dsc.step(k, v, qi, qq, ks, vs)
+        else:
+            dsc.append_frame(k, v)
+            oi = dsc.build_instant(qi)
+            o = dsc.attend(qq, ks, vs)
+        if kvsplit and world > 1:
+            from paper_2605_01858_b200.dist import gather_heads
+            o = gather_heads(o)
         ho.copy_(o, non_blocking=True)
         del oi
     one()
@@ -335,7 +350,8 @@ def run_e2e(args, cfg, dsc, S, dev, stream, world):
     return {"value": round(cfg.num_streams * steps / (ms / 1e3), 2), "unit": "frames/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
             "note": "pinned host inputs (frame K/V, Q_inst, Q, K_self, V_self) copied H2D and the query "
-                    "answer O copied D2H every step, through DSCache.append_frame/build_instant/attend"}
+                    "answer O copied D2H every step, through DSCache.step (or append_frame/build_instant/attend "
+                    "with --api split)"}
 
 
 # ----------------------------------------------------------------------------- oracle (cpu baseline / reference arm)
@@ -409,6 +425,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="streams", choices=["streams", "kvsplit"],
                     help="streams: P1 stream partition (default); kvsplit: P2 KV-head split of one stream")
+    ap.add_argument("--api", default="fused", choices=["fused", "split"],
+                    help="fused: DSCache.step (one attention launch per step); split: three calls")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()

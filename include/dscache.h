@@ -187,6 +187,19 @@ dscache_status dscache_decode(dscache_t h, int32_t layer_begin, int32_t layer_co
 dscache_status dscache_update_attend(dscache_t h, int32_t layer_begin, int32_t layer_count,
                                      const void* q_upd, void* o_upd, int32_t active_frames, void* stream);
 
+/* One streaming step of the hot path for a layer range:
+ * exactly dscache_append_frame(k_frame, v_frame, tpf) + dscache_build_instant(q_inst,
+ * o_inst) + dscache_attend(q, k_self, v_self, n_q, o), with identical results.  When both
+ * attention calls take the tcgen05 kernel (and no debug capture is set) the build and the
+ * attend run as ONE persistent launch: attend items first (longest), build items after,
+ * so the SMs the attend leaves idle at its tail run the build (Eq. 3 + Eq. 7 + Eq. 8).
+ * Arguments and layouts as in the three calls; all device pointers, stream-ordered.
+ * Errors as the three calls; E_STATE before the sink was appended. */
+dscache_status dscache_step(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                            const void* k_frame, const void* v_frame, const void* q_inst, void* o_inst,
+                            const void* q, const void* k_self, const void* v_self, int32_t n_q, void* o,
+                            void* stream);
+
 /* Host counters of `layer` (closed form of Eq. 3/5/6 at the latest append). */
 dscache_status dscache_get_state(dscache_t h, int32_t layer, dscache_state* out);
 

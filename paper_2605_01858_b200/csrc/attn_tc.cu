@@ -492,7 +492,11 @@ __device__ __forceinline__ void rotate_q_tile(const AttnParams& p, const Item& w
 }
 
 // ------------------------------------------------------------------ kernel
-__global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_constant__ AttnParams p) {
+// Two attention problems can share one persistent launch (the fused step: attend items
+// first, then build_instant items); items [0, na) use pa, [na, na + nb) use pb.
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_tc_kernel(const __grid_constant__ AttnParams pa, const __grid_constant__ AttnParams pb, int na, int nb) {
+  const AttnParams& p = pa;   // launch-wide fields (rope table, tensor maps, trace) are shared
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = su32(smem);
@@ -501,7 +505,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + B_N * 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_items = p.n_mblocks * p.P * p.Hkv * p.n_splits;
+  const int n_items = na + nb;
+#define ITEM_PARAMS(I) ((I) < na ? pa : pb)
+#define ITEM_LOCAL(I) ((I) < na ? (I) : (I) - na)
 
   if (threadIdx.x == 0) {
     mbar_init(bar(B_Q + 0), 128);
@@ -538,7 +544,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int A = p.A;
 
   if (warp < 8) {
     // ================================================================ softmax
@@ -553,14 +558,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     const int lt = threadIdx.x - qt * 128;          // 0..127 within the warpgroup
     const uint32_t qtile = sbase + OFF_Q + qt * kTileBytes;
     if (blockIdx.x < (unsigned)n_items) {            // Q tile of the first item
-      const Item w0 = decode_item(p, blockIdx.x);
-      issue_q_tile(p, w0, qt, lt, qtile);
-      rotate_q_tile(p, w0, qt, lt, qtile, 2 + qt);
+      const AttnParams& p0 = ITEM_PARAMS((int)blockIdx.x);
+      const Item w0 = decode_item(p0, ITEM_LOCAL((int)blockIdx.x));
+      issue_q_tile(p0, w0, qt, lt, qtile);
+      rotate_q_tile(p0, w0, qt, lt, qtile, 2 + qt);
       mbar_arrive(bar(B_Q + qt));
     }
     int gt = 0, kk = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
-      const Item w = decode_item(p, idx);
+      const AttnParams& p = ITEM_PARAMS(idx);
+      const Item w = decode_item(p, ITEM_LOCAL(idx));
+      const int A = p.A;
       const int n = w.n_tiles;
       const int rglob = w.m0 + qt * 128 + rloc;
       const bool valid_row = rglob < w.rows_total;
@@ -752,15 +760,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       const int nidx = idx + gridDim.x;
       Item wn;
       if (nidx < n_items) {
-        wn = decode_item(p, nidx);
-        issue_q_tile(p, wn, qt, lt, qtile);
+        wn = decode_item(ITEM_PARAMS(nidx), ITEM_LOCAL(nidx));
+        issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile);
       }
       // publish the next item's Q before this item's epilogue, so the tensor core can start
       // the next item's first S MMAs while O is read out (the MMA waits for B_OF before it
       // overwrites O with the next item's first PV)
 #if DSC_QFIRST
       if (nidx < n_items) {
-        rotate_q_tile(p, wn, qt, lt, qtile, 2 + qt);
+        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile, 2 + qt);
         mbar_arrive(bar(B_Q + qt));
         if (rloc == 0) TRACE(EV_QDONE, gt);
       }
@@ -806,7 +814,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       }
 #if !DSC_QFIRST
       if (nidx < n_items) {
-        rotate_q_tile(p, wn, qt, lt, qtile, 2 + qt);
+        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile, 2 + qt);
         mbar_arrive(bar(B_Q + qt));
         if (rloc == 0) TRACE(EV_QDONE, gt);
       }
@@ -829,7 +837,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     }
     int gt = 0, kk = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
-      const Item w = decode_item(p, idx);
+      const AttnParams& p = ITEM_PARAMS(idx);
+      const Item w = decode_item(p, ITEM_LOCAL(idx));
+      const int A = p.A;
       const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
       // ---- K tiles of this item; the table entry of each tile's first row is fetched
       // one tile ahead so the L2 latency is off the rotation's critical path
@@ -884,15 +894,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     if (warp == 12 || warp == 13) {
       // ============================================================== copy warps (12: K, 13: V)
       const bool isk = warp == 12;
-      const __nv_bfloat16* __restrict__ SX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.sink_k : p.sink_v);
-      const __nv_bfloat16* __restrict__ XX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.self_k : p.self_v);
       const CUtensorMap* tmap = isk ? &p.tmap_k : &p.tmap_v;
       const int nst = isk ? KST : VST;
       const int off = isk ? OFF_K : OFF_V;
       const int b_full = isk ? B_KR : B_VF, b_free = isk ? B_KE : B_VE;
       int gt = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
-        const Item w = decode_item(p, idx);
+        const AttnParams& p = ITEM_PARAMS(idx);
+        const Item w = decode_item(p, ITEM_LOCAL(idx));
+        const int A = p.A;
+        const __nv_bfloat16* __restrict__ SX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.sink_k : p.sink_v);
+        const __nv_bfloat16* __restrict__ XX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.self_k : p.self_v);
 #pragma unroll 1
         for (int jj = 0; jj < w.n_tiles; ++jj) {
           const int g = gt + jj, u = w.t_begin + jj, st = g % nst;
@@ -952,7 +964,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       };
       int gt = 0, kk = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
-        const Item w = decode_item(p, idx);
+        const AttnParams& p = ITEM_PARAMS(idx);
+        const Item w = decode_item(p, ITEM_LOCAL(idx));
         const int n = w.n_tiles;
         mbar_wait(bar(B_KF + gt % KST), (gt / KST) & 1);
         TRACE(EV_KF, gt);
@@ -1031,7 +1044,9 @@ cudaError_t make_ring_tmap(CUtensorMap* map, void* base, unsigned long long rows
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-cudaError_t launch_attn_tc(const AttnParams& p, cudaStream_t st) {
+static long long tc_items(const AttnParams& p) { return (long long)p.P * p.Hkv * p.n_mblocks * p.n_splits; }
+
+cudaError_t launch_attn_tc2(const AttnParams& pa, const AttnParams* pb, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1039,16 +1054,19 @@ cudaError_t launch_attn_tc(const AttnParams& p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const long long items = (long long)p.P * p.Hkv * p.n_mblocks * p.n_splits;
   static int num_sms = 0;
   if (num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  const long long na = tc_items(pa), nb = pb ? tc_items(*pb) : 0;
+  const long long items = na + nb;
   const unsigned grid = (unsigned)(items < num_sms ? items : num_sms);
-  tc::attn_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, st>>>(p);
+  tc::attn_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, st>>>(pa, pb ? *pb : pa, (int)na, (int)nb);
   return cudaGetLastError();
 }
+
+cudaError_t launch_attn_tc(const AttnParams& p, cudaStream_t st) { return launch_attn_tc2(p, nullptr, st); }
 
 }  // namespace dsc

@@ -310,23 +310,37 @@ dscache_status dscache_append_frame(dscache_t h, int32_t lb, int32_t lc, const v
   return DSCACHE_OK;
 }
 
-dscache_status dscache_build_instant(dscache_t h, int32_t lb, int32_t lc, const void* q_inst, void* o_inst,
-                                     void* stream) {
+namespace {
+// Parameters of build_instant (Eq. 7): the C_t instant tokens attend causally over
+// [sink | instant window].  *empty is set when l_I = 0 (nothing to build).
+dscache_status prep_build(dscache_t h, int32_t lb, int32_t lc, const void* q_inst, void* o_inst, dsc::AttnParams& p,
+                          bool* empty) {
+  *empty = false;
   dscache_status s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
   if (!h->sink_filled[lb] || h->frames[lb] < 1)
     return fail(DSCACHE_E_STATE, "build_instant before the sink and the first frame were appended");
   const Schedule sc = h->schedule(lb);
-  if (sc.C_t == 0) return DSCACHE_OK;   // l_I = 0: the instant cache is empty (uniform reduction)
+  if (sc.C_t == 0) { *empty = true; return DSCACHE_OK; }   // l_I = 0: the instant cache is empty
   if (!q_inst || !o_inst) return fail(DSCACHE_E_ARG, "null q_inst/o_inst");
-  DeviceGuard dg(h->cfg.device);
-  dsc::AttnParams p{};
+  p = dsc::AttnParams{};
   fill_common(h, p, lb, lc);
   p.q = q_inst; p.o = o_inst; p.n_q = sc.C_t; p.q_pos0 = h->cfg.sink_tokens;
   p.ring_start = sc.inst_start; p.ring_count = sc.C_t;
   p.self_k = p.self_v = nullptr; p.n_self = 0;
   p.dbg_pos = h->dbg_build;
   p.n_mblocks = (p.n_q * p.grp + 2 * dsc::kTileM - 1) / (2 * dsc::kTileM);
+  return DSCACHE_OK;
+}
+}  // namespace
+
+dscache_status dscache_build_instant(dscache_t h, int32_t lb, int32_t lc, const void* q_inst, void* o_inst,
+                                     void* stream) {
+  dsc::AttnParams p{};
+  bool empty = false;
+  dscache_status s = prep_build(h, lb, lc, q_inst, o_inst, p, &empty);
+  if (s != DSCACHE_OK || empty) return s;
+  DeviceGuard dg(h->cfg.device);
   return run_attention(h, p, h->impl_build, 0, (cudaStream_t)stream);
 }
 
@@ -356,19 +370,18 @@ namespace {
 // Attention of n_q query rows over [sink | past | instant | self], where the self segment
 // holds n_self >= n_q transient tokens (the query chunk, and during decode the tokens
 // generated so far) and the queries are its last n_q tokens.
-dscache_status attend_common(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
-                             const void* v_self, int32_t n_self, int32_t n_q, void* o, void* stream, bool dbg) {
+dscache_status prep_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                           const void* v_self, int32_t n_self, int32_t n_q, void* o, bool dbg, dsc::AttnParams& p) {
   dscache_status s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
   if (!h->sink_filled[lb] || h->frames[lb] < 1)
     return fail(DSCACHE_E_STATE, "attend before the sink and the first frame were appended");
   if (n_q < 1 || n_q > n_self) return fail(DSCACHE_E_ARG, "need 1 <= n_q <= n_self");
   if (!q || !k_self || !v_self || !o) return fail(DSCACHE_E_ARG, "null q/k_self/v_self/o");
-  DeviceGuard dg(h->cfg.device);
   const Schedule sc = h->schedule(lb);
   if ((int64_t)h->cfg.sink_tokens + sc.P_t + sc.C_t + n_self > h->cfg.max_position)
     return fail(DSCACHE_E_POS_OVERFLOW, "A + P_t + C_t + n_self exceeds max_position");
-  dsc::AttnParams p{};
+  p = dsc::AttnParams{};
   fill_common(h, p, lb, lc);
   p.q = q; p.o = o; p.n_q = n_q;
   p.ring_start = sc.ring_start; p.ring_count = sc.P_t + sc.C_t;
@@ -407,7 +420,16 @@ dscache_status attend_common(dscache_t h, int32_t lb, int32_t lc, const void* q,
       p.ws_lse = h->ws + (size_t)splits * rows * p.d;
     }
   }
-  return run_attention(h, p, impl, 1, (cudaStream_t)stream);
+  return DSCACHE_OK;
+}
+
+dscache_status attend_common(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                             const void* v_self, int32_t n_self, int32_t n_q, void* o, void* stream, bool dbg) {
+  dsc::AttnParams p{};
+  dscache_status s = prep_attend(h, lb, lc, q, k_self, v_self, n_self, n_q, o, dbg, p);
+  if (s != DSCACHE_OK) return s;
+  DeviceGuard dg(h->cfg.device);
+  return run_attention(h, p, h->impl_attend, 1, (cudaStream_t)stream);
 }
 }  // namespace
 
@@ -421,6 +443,46 @@ dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q
 dscache_status dscache_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                               const void* v_self, int32_t n_self, int32_t n_q, void* o, void* stream) {
   return attend_common(h, lb, lc, q, k_self, v_self, n_self, n_q, o, stream, false);
+}
+
+dscache_status dscache_step(dscache_t h, int32_t lb, int32_t lc, const void* k_frame, const void* v_frame,
+                            const void* q_inst, void* o_inst, const void* q, const void* k_self, const void* v_self,
+                            int32_t n_q, void* o, void* stream) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
+  dscache_status cs = check_layers(h, lb, lc);
+  if (cs != DSCACHE_OK) return cs;
+  if (!h->sink_filled[lb]) return fail(DSCACHE_E_STATE, "step before the sink was appended");
+  dscache_status s = dscache_append_frame(h, lb, lc, k_frame, v_frame, h->cfg.tokens_per_frame, stream);
+  if (s != DSCACHE_OK) return s;
+  dsc::AttnParams pb{}, pa{};
+  bool empty = false;
+  s = prep_build(h, lb, lc, q_inst, o_inst, pb, &empty);
+  if (s != DSCACHE_OK) return s;
+  s = prep_attend(h, lb, lc, q, k_self, v_self, n_q, n_q, o, true, pa);
+  if (s != DSCACHE_OK) return s;
+  DeviceGuard dg(h->cfg.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool debug = h->dbg_build || h->dbg_attend;
+  if (empty || debug || h->impl_build != DSCACHE_IMPL_TC || h->impl_attend != DSCACHE_IMPL_TC) {
+    if (!empty) {
+      s = run_attention(h, pb, h->impl_build, 0, st);
+      if (s != DSCACHE_OK) return s;
+    }
+    return run_attention(h, pa, h->impl_attend, 1, st);
+  }
+  // one persistent tcgen05 launch: the attend items (longest) first, then the build items
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->prof) { e0 = h->take_event(); e1 = h->take_event(); cudaEventRecord(e0, st); }
+  cudaError_t e = dsc::launch_attn_tc2(pa, &pb, st);
+  h->launches++;
+  if (e == cudaSuccess && pa.n_splits > 1) { e = dsc::launch_combine(pa, st); h->launches++; }
+  if (h->prof) {
+    cudaEventRecord(e1, st);
+    h->pending.push_back({e0, e1, 1});
+  }
+  if (e != cudaSuccess) return fail(DSCACHE_E_CUDA, std::string("fused step launch: ") + cudaGetErrorString(e));
+  return DSCACHE_OK;
 }
 
 dscache_status dscache_update_attend(dscache_t h, int32_t lb, int32_t lc, const void* q_upd, void* o_upd,

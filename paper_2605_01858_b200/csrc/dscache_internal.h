@@ -72,6 +72,8 @@ cudaError_t launch_rope_table(float2* table, int npos, int d, double theta, cuda
 cudaError_t launch_append(const AppendParams& p, cudaStream_t st);
 cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t st);
 cudaError_t launch_attn_tc(const AttnParams& p, cudaStream_t st);
+// one persistent launch over the items of pa (first) and then those of *pb (same handle)
+cudaError_t launch_attn_tc2(const AttnParams& pa, const AttnParams* pb, cudaStream_t st);
 cudaError_t launch_combine(const AttnParams& p, cudaStream_t st);
 int attn_tc_smem_bytes();
 // encode the 2-D ring tensor map (bf16, d = 128) used by the tcgen05 kernel

@@ -53,7 +53,7 @@ class State(ctypes.Structure):
 
 
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
-           "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
+           "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
            "dscache_attn_impl", "dscache_last_error"]
 
@@ -79,6 +79,7 @@ def load_library(path: str = LIB_PATH):
         "dscache_update_attend": ([P, I32, I32, P, P, I32, P], I32),
         "dscache_decode": ([P, I32, I32, P, P, P, I32, I32, P, P], I32),
         "dscache_build_instant_newest": ([P, I32, I32, P, P, P], I32),
+        "dscache_step": ([P, I32, I32, P, P, P, P, P, P, P, I32, P, P], I32),
         "dscache_get_state": ([P, I32, ctypes.POINTER(State)], I32),
         "dscache_copy_ring": ([P, I32, I32, P, P], I32),
         "dscache_copy_sink": ([P, I32, I32, P, P], I32),
@@ -222,6 +223,32 @@ class DSCache:
         _check(_lib.dscache_attend(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, _ptr(o),
                                    _stream_ptr(stream)))
         return o
+
+    def step(self, k: torch.Tensor, v: torch.Tensor, q_inst: torch.Tensor, q: torch.Tensor, k_self: torch.Tensor,
+             v_self: torch.Tensor, o_inst: Optional[torch.Tensor] = None, o: Optional[torch.Tensor] = None,
+             layer_begin: int = 0, layer_count: Optional[int] = None, stream=None):
+        """append_frame(k, v) + build_instant(q_inst) + attend(q, k_self, v_self) in one call
+        (one fused tcgen05 launch for the two attentions).  Returns (O_inst, O)."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        fshape = (c.num_streams, lc, c.tokens_per_frame, c.num_kv_heads, c.head_dim)
+        self._t(k, "k", fshape); self._t(v, "v", fshape)
+        C_t = min(self.state(lb)["frames_seen"] + 1, c.instant_frames) * c.tokens_per_frame
+        ishape = (c.num_streams, lc, C_t, c.num_q_heads, c.head_dim)
+        self._t(q_inst, "q_inst", ishape)
+        if o_inst is None:
+            o_inst = torch.empty(ishape, dtype=self.torch_dtype, device=self.device)
+        self._t(o_inst, "o_inst", ishape)
+        n_q = int(q.shape[2])
+        self._t(q, "q", (c.num_streams, lc, n_q, c.num_q_heads, c.head_dim))
+        self._t(k_self, "k_self", (c.num_streams, lc, n_q, c.num_kv_heads, c.head_dim))
+        self._t(v_self, "v_self", k_self.shape)
+        if o is None:
+            o = torch.empty(q.shape, dtype=self.torch_dtype, device=self.device)
+        self._t(o, "o", q.shape)
+        _check(_lib.dscache_step(self._h, lb, lc, _ptr(k), _ptr(v), _ptr(q_inst), _ptr(o_inst), _ptr(q),
+                                 _ptr(k_self), _ptr(v_self), n_q, _ptr(o), _stream_ptr(stream)))
+        return o_inst, o
 
     def build_instant_newest(self, q_new: torch.Tensor, o_new: Optional[torch.Tensor] = None,
                              layer_begin: int = 0, layer_count: Optional[int] = None, stream=None) -> torch.Tensor:

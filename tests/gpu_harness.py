@@ -24,10 +24,11 @@ def _batch(cfg, shape_tail, exact, fill, dev, gen):
 
 
 def run_stream(cfg, capture_steps, exact, impl=D.IMPL_AUTO, debug=False, poison=False, ring_capture=(),
-               layer_by_layer=False, n_q=None, past_override=None, update_lL=None):
+               layer_by_layer=False, n_q=None, past_override=None, update_lL=None, fused=False):
     """Returns {t: {(s,l): (o_inst cpu, o cpu)}, "ring": {(t,s,l): (k,v)}, "dbg": {t: (b,a)}, "state": {t: st}}.
 
-    past_override(s, l, f) -> (k, v) or None lets a test replace past frames (decoupling test)."""
+    past_override(s, l, f) -> (k, v) or None lets a test replace past frames (decoupling test).
+    fused=True runs captured steps through DSCache.step (append + build + attend in one call)."""
     dev = torch.device("cuda", 0)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + cfg.cfg_id)
@@ -54,30 +55,43 @@ def run_stream(cfg, capture_steps, exact, impl=D.IMPL_AUTO, debug=False, poison=
             kv[(s, l)] = r if r is not None else synth.frame_kv(cfg, s, l, t)
         k = _batch(cfg, (tpf, Hkv, d), exact, lambda s, l: kv[(s, l)][0], dev, gen)
         v = _batch(cfg, (tpf, Hkv, d), exact, lambda s, l: kv[(s, l)][1], dev, gen)
-        if layer_by_layer:
+        do_fused = fused and t in capture_steps
+        if do_fused:
+            pass
+        elif layer_by_layer:
             for l in range(cfg.num_layers):
                 dsc.append_frame(k[:, l:l + 1].contiguous(), v[:, l:l + 1].contiguous(), layer_begin=l, layer_count=1)
         else:
             dsc.append_frame(k, v)
         if t not in capture_steps:
             continue
-        st = dsc.state(0)
-        out["state"][t] = st
-        C_t = st["instant_tokens"]
+        C_t = min(t + 1, cfg.instant_frames) * tpf
         caps = {}
         o_inst = None
+        qi = None
         if C_t > 0:
             qi = _batch(cfg, (C_t, Hq, d), exact, lambda s, l: synth.instant_q(cfg, s, l, t, C_t), dev, gen)
             if debug:
                 dbg_b.fill_(-1)
-            o_inst = dsc.build_instant(qi)
+            if not do_fused:
+                o_inst = dsc.build_instant(qi)
         qkv = {sl: synth.query_qkv(cfg, sl[0], sl[1], t, n_q) for sl in exact}
         q = _batch(cfg, (n_q, Hq, d), exact, lambda s, l: qkv[(s, l)][0], dev, gen)
         ks = _batch(cfg, (n_q, Hkv, d), exact, lambda s, l: qkv[(s, l)][1], dev, gen)
         vs = _batch(cfg, (n_q, Hkv, d), exact, lambda s, l: qkv[(s, l)][2], dev, gen)
         if debug:
             dbg_a.fill_(-1)
-        o = dsc.attend(q, ks, vs)
+        if do_fused:
+            if qi is None:
+                qi = torch.empty((cfg.num_streams, cfg.num_layers, 0, Hq, d), dtype=dsc.torch_dtype, device=dev)
+            o_inst, o = dsc.step(k, v, qi, q, ks, vs)
+            if C_t == 0:
+                o_inst = None
+        else:
+            o = dsc.attend(q, ks, vs)
+        st = dsc.state(0)
+        out["state"][t] = st
+        assert st["instant_tokens"] == C_t
         torch.cuda.synchronize()
         for (s, l) in exact:
             caps[(s, l)] = (None if o_inst is None else o_inst[s, l].float().cpu(), o[s, l].float().cpu())

@@ -233,6 +233,37 @@ def test_c5_multistream_sampled(lib):
     _check_steps(cfg, res, steps, exact)
 
 
+@pytest.mark.parametrize("name,steps,exact", [
+    ("c2", [0, 3, 4, 36, 37, 63], [(0, 0)]),
+    ("c5", [0, 36, 127], [(0, 0), (63, 3)]),
+])
+def test_fused_step_parity_and_bitwise_equal_to_three_calls(lib, name, steps, exact):
+    # dscache_step = append + build_instant + attend in one persistent tcgen05 launch:
+    # within the bar against the oracle AND bitwise equal to the three separate calls
+    cfg = synth.CONFIGS[name]
+    fused = run_stream(cfg, steps, exact, fused=True)
+    _check_steps(cfg, fused, steps, exact, tag="-fused")
+    sep = run_stream(cfg, steps, exact)
+    for t in steps:
+        for sl in exact:
+            a, b = fused[t][sl], sep[t][sl]
+            assert torch.equal(a[1], b[1]), (t, sl)
+            assert (a[0] is None) == (b[0] is None) and (a[0] is None or torch.equal(a[0], b[0])), (t, sl)
+
+
+@pytest.mark.parametrize("variant", ["no_sink", "lI0_uniform", "lU0_window", "small_multi"])
+def test_fused_step_edge_configs(lib, variant):
+    base = synth.CONFIGS["c2"].replace(tokens_per_frame=128, past_frames=6, instant_frames=3, num_frames=16,
+                                       query_tokens=37, num_layers=2)
+    cfg = {"no_sink": base.replace(sink_tokens=0), "lI0_uniform": base.replace(instant_frames=0),
+           "lU0_window": base.replace(past_frames=0),
+           "small_multi": base.replace(num_streams=3, query_tokens=1)}[variant]
+    exact = [(0, 0), (cfg.num_streams - 1, 1)]
+    steps = [0, 2, 9, 10, 15]
+    res = run_stream(cfg, steps, exact, fused=True)
+    _check_steps(cfg, res, steps, exact, tag="-fused-" + variant)
+
+
 def test_errors_through_the_abi(lib):
     cfg = synth.CONFIGS["c2"]
     with pytest.raises(D.DSCacheError) as e:

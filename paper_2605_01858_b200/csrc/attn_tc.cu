@@ -31,13 +31,11 @@
 // P_qt (bf16x2) overwrites S_qt cols [0,64) and feeds O_qt += P V as the TMEM A operand.
 // MMA issue order S0_0 S1_0 | PV0_j S0_{j+1} PV1_j S1_{j+1} | ... so each softmax
 // warpgroup overlaps the other Q tile's MMAs.
-#include "dscache_internal.h"
-
-#include <cuda_bf16.h>
-#include <cstdint>
+#include "tc_common.cuh"
 
 namespace dsc {
 namespace tc {
+using namespace tcc;
 
 constexpr int kNQT = 2;                       // Q tiles per CTA
 constexpr int kWarps = 16;
@@ -67,429 +65,22 @@ constexpr int kThreadRegs = 65536 / kThreads;   // allocation at launch (128); i
 static_assert(kRegSoftmax > kThreadRegs && kRegCopy < kThreadRegs, "softmax must grow, copy/MMA must shrink");
 constexpr int kSmemBytes = OFF_BAR + B_N * 8 + 16 + 1024;   // + tmem slot + alignment slack
 constexpr float kRescaleThreshold = 8.0f;     // log2 units (factor 256)
-
-// ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n.reg .pred P1;\n"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, P1;\n}\n"
-      : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
-  return ok != 0;
-}
-// Watchdog: a pipeline bug must not hang the GPU -- trap after ~2^31 cycles (~1 s).
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  if (mbar_try(bar, parity)) return;
-  const long long t0 = clock64();
-  while (!mbar_try(bar, parity)) {
-    if (clock64() - t0 > (1ll << 31)) __trap();
-  }
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start>>4 [0,14),
-// LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48), base offset 0, swizzle
-// mode 2 = 128B [61,64).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
-// instruction descriptor, kind::f16: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
-// A major [15], B major [16] (1 = MN-major), N>>3 [17,23), M>>4 [24,29).
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
-}
-
-// 32 lanes x 32 consecutive 32-bit columns (thread = lane = row)
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
-      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
-      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
-      : "memory");
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-          taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-      : "memory");
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// 2^x on the FMA/ALU pipes (keeps the MUFU free): x = j + f with j = round(x) via the
-// 1.5*2^23 trick, 2^f on [-1/2, 1/2] by a degree-3 fit (max rel. error 1.4e-4 incl.
-// rounding, far below bf16's 2^-9), 2^j added into the exponent bits.  x >= -126.
-constexpr float kP0 = 0.99992829561233520f, kP1 = 0.69326096773147580f, kP2 = 0.24260866641998290f,
-                kP3 = 0.05517056211829185f;
-__device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const float2 y = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
-  const float2 j = __fadd2_rn(y, make_float2(-12582912.f, -12582912.f));
-  const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
-  float2 q = __ffma2_rn(make_float2(kP3, kP3), f, make_float2(kP2, kP2));
-  q = __ffma2_rn(q, f, make_float2(kP1, kP1));
-  q = __ffma2_rn(q, f, make_float2(kP0, kP0));
-  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(y.x) << 23)),
-                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(y.y) << 23)));
-}
+static_assert(kNQT * 128 == kMBlockRows, "work items are 256-row m-blocks");
 #ifndef DSC_POLY
 #define DSC_POLY 0
 #endif
-constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, this many use exp2_poly2
-
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
-__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
-
-__device__ __forceinline__ uint2 ldg64(const void* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
-  asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
-}
-
-// byte offset of element (row, col) in a 128 x 128 bf16 tile stored as two
-// 64-column SW128 blocks (16 KB each): the canonical K-major SWIZZLE_128B layout
-// (8 rows x 128 B atoms, 16-byte chunk index XOR row%8).
-__device__ __forceinline__ uint32_t sw128(int row, int col) {
-  const int blk = col >> 6;
-  const int byte = (col & 63) * 2;
-  return (uint32_t)(blk * 16384 + row * 128 + ((((byte >> 4) ^ (row & 7))) << 4) + (byte & 15));
-}
-
-// Ring tile k covers slots [k*128, min(k*128+128, R)).  Valid keys of the window
-// [start, start+cnt) (mod R) form one column interval [c_a, c_b) with logical ring
-// index rel_a at c_a (needs R - cnt >= 128, guaranteed by tpf >= 128).
-__device__ __forceinline__ void ring_tile_info(int k, int R, int start, int cnt, int& c_a, int& c_b, int& rel_a) {
-  const int base = k * 128;
-  const int width = min(128, R - base);
-  if (start > base && start < base + width) {
-    c_a = start - base;
-    rel_a = 0;
-  } else {
-    c_a = 0;
-    rel_a = base - start;
-    if (rel_a < 0) rel_a += R;
-  }
-  const int rem = cnt - rel_a;
-  c_b = rem > 0 ? min(width, c_a + rem) : c_a;
-}
-
-__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ uint2 lds64(uint32_t addr) {
-  uint2 r;
-  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(addr) : "memory");
-  return r;
-}
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-// timeline events (TRACE): clock64 per (event, tile) for the first ntrace_cta CTAs
-enum { EV_K_ISSUE = 0, EV_V_ISSUE, EV_KR, EV_KF, EV_S0, EV_S1, EV_P0, EV_P1, EV_PV0, EV_PV1, EV_Q, EV_START, EV_END,
-       EV_VF, EV_PW0 /* 14..21: P arrival of softmax warps 0..7 */, EV_L = 22 /* 22..27: warp-0 softmax steps */,
-       EV_KDONE = 28, EV_QDONE = 29, EV_QLOADED = 30, EV_QSTART = 31 };
-#define TRACE(ev, tile)                                                                                  \
-  do {                                                                                                   \
-    if (p.trace && blockIdx.x < (unsigned)p.ntrace_cta && (tile) < kTraceTiles)                          \
-      p.trace[((long long)blockIdx.x * kTraceEvents + (ev)) * kTraceTiles + (tile)] = clock64();          \
-  } while (0)
-
-#ifndef DSC_ORDER
-#define DSC_ORDER 1
+// ablation knobs (timing experiments only; results are wrong when set):
+// DSC_ABL_SOFTMAX skips the softmax body, DSC_ABL_ROT skips the K rotation
+#ifndef DSC_ABL_SOFTMAX
+#define DSC_ABL_SOFTMAX 0
 #endif
+#ifndef DSC_ABL_ROT
+#define DSC_ABL_ROT 0
+#endif
+constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, this many use exp2_poly2
 #ifndef DSC_QFIRST
 #define DSC_QFIRST 0
 #endif
-struct Item {
-  int pp, g, mb, sp;
-  long long head_row;
-  int m0, rows_total;
-  int cnt;            // ring keys needed by this m-block (causal cut)
-  int k0, nT;         // first physical ring tile, number of physical tiles
-  int n_extra;        // leading tiles holding sink + self rows (>= 1)
-  int t_begin, n_tiles;
-};
-
-// work item idx -> split fastest, then (DSC_ORDER 1, default) problem x kv head, then
-// m-block descending: all (problem, head) pairs of the longest causal m-block first
-// (LPT-like balance of the persistent CTAs).  DSC_ORDER 0 groups the m-blocks of one
-// (problem, head) for L2 reuse of its K/V; measured slower on c5 (9.8K vs 12.4K frames/s).
-__device__ __forceinline__ Item decode_item(const AttnParams& p, int idx) {
-  Item w;
-  w.sp = idx % p.n_splits;
-  const int rest = idx / p.n_splits;
-#if DSC_ORDER == 1   // longest-first across all (problem, head) pairs
-  const int ph = rest % (p.P * p.Hkv);
-  w.mb = p.n_mblocks - 1 - rest / (p.P * p.Hkv);
-#else
-  w.mb = p.n_mblocks - 1 - rest % p.n_mblocks;
-  const int ph = rest / p.n_mblocks;
-#endif
-  w.g = ph % p.Hkv;
-  w.pp = ph / p.Hkv;
-  const int s = w.pp / p.layer_count, l = w.pp % p.layer_count;
-  w.head_row = ((long long)s * p.N_total + p.layer_begin + l) * p.Hkv + w.g;
-  w.rows_total = p.n_q * p.grp;
-  w.m0 = w.mb * (kNQT * 128);
-  const int last_row = min(w.m0 + kNQT * 128, w.rows_total) - 1;
-  const int lim_max = p.q_pos0 + last_row / p.grp;
-  w.cnt = min(max(lim_max - p.A + 1, 0), p.ring_count);
-  w.nT = (p.R + 127) / 128;
-  w.k0 = p.ring_start / 128;
-  int rt = 0;
-  if (w.cnt > 0) {
-    const int end = p.ring_start + w.cnt;
-    rt = end <= p.R ? (end + 127) / 128 - w.k0 : (w.nT - w.k0) + (end - p.R + 127) / 128;
-    rt = min(rt, w.nT);
-  }
-  w.n_extra = max(1, (p.A + p.n_self + 127) / 128);
-  const int total = w.n_extra + rt;
-  w.t_begin = min(w.sp * p.tiles_per_split, total);
-  w.n_tiles = min(total, w.t_begin + p.tiles_per_split) - w.t_begin;
-  return w;
-}
-
-// Key rows of tile u as (at most) two segments; key row r of segment s has id
-// pos0_s + r.  Tiles u < n_extra hold the sink rows (extra index x = 128u + r < A, id x)
-// and then the self rows (A <= x < A + n_self, id ring_count + x); tile u >= n_extra =
-// physical ring tile (k0 + u - n_extra) mod nT, valid rows [c_a, c_b).
-struct TileSeg {
-  int lo0, hi0, pos0_0;
-  int lo1, hi1, pos0_1;
-  int phys;           // physical ring tile (u > 0), -1 for tile 0
-};
-
-__device__ __forceinline__ TileSeg tile_segments(const AttnParams& p, const Item& w, int u) {
-  TileSeg t;
-  if (u < w.n_extra) {
-    const int x0 = 128 * u;
-    t.lo0 = 0; t.hi0 = min(max(p.A - x0, 0), 128); t.pos0_0 = x0;
-    t.lo1 = t.hi0; t.hi1 = min(max(p.A + p.n_self - x0, 0), 128); t.pos0_1 = p.ring_count + x0;
-    t.phys = -1;
-  } else {
-    int k = w.k0 + u - w.n_extra;
-    if (k >= w.nT) k -= w.nT;
-    int c_a, c_b, rel_a;
-    ring_tile_info(k, p.R, p.ring_start, w.cnt, c_a, c_b, rel_a);
-    t.lo0 = c_a; t.hi0 = c_b; t.pos0_0 = p.A + rel_a - c_a;
-    t.lo1 = 0; t.hi1 = 0; t.pos0_1 = 0;
-    t.phys = k;
-  }
-  return t;
-}
-__device__ __forceinline__ int seg_pos(const TileSeg& t, int r) {
-  if (r >= t.lo0 && r < t.hi0) return t.pos0_0 + r;
-  if (r >= t.lo1 && r < t.hi1) return t.pos0_1 + r;
-  return -1;
-}
-
-__device__ __forceinline__ uint4 lds128(uint32_t addr) {
-  uint4 r;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr) : "memory");
-  return r;
-}
-__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
-  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-}
-__device__ __forceinline__ float2 bf2(uint32_t w) { return make_float2(bf_lo(w), bf_hi(w)); }
-__device__ __forceinline__ uint32_t get_w(const uint4& v, int j) { return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w; }
-
-// In-place RoPE of 8 rows x 8 frequencies (f = 8*c8 .. 8*c8+7: 16-byte chunk c8 of the
-// low and of the high 64-column block) of a SW128 bf16 tile in smem.  Row k gets
-// id pos[k] (-1 = clear the row).  All 16 chunks are loaded first (ILP); between
-// consecutive ids the (cos, sin) advance by R(theta) (id + 1) or stay (same id),
-// any other jump reloads the fp64-built pair table rp[id][32].
-__device__ __forceinline__ void rotate8(uint32_t tile, int r0, int c8, const float4* __restrict__ rp,
-                                        const float2 (&cth)[4], const float2 (&sth)[4], const int (&pos)[8],
-                                        const float4 (&pre)[4], int pre_pos) {
-  // (cs, sn) start at the prefetched table entry of id pre_pos (the first valid row)
-  float2 cs[4], sn[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) { cs[j] = make_float2(pre[j].x, pre[j].y); sn[j] = make_float2(pre[j].z, pre[j].w); }
-  int prev = pre_pos;
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    uint4 lo[4], hi[4];
-    uint32_t addr[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int r = r0 + half * 4 + k;
-      addr[k] = tile + r * 128 + ((c8 ^ (r & 7)) << 4);
-      lo[k] = lds128(addr[k]);
-      hi[k] = lds128(addr[k] + 16384);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int pk = pos[half * 4 + k];
-      uint4 ylo = make_uint4(0, 0, 0, 0), yhi = make_uint4(0, 0, 0, 0);
-      if (pk >= 0) {
-        if (pk == prev) {
-        } else if (pk == prev + 1) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float2 nc = __ffma2_rn(cs[j], cth[j], __fmul2_rn(make_float2(-sn[j].x, -sn[j].y), sth[j]));
-            sn[j] = __ffma2_rn(sn[j], cth[j], __fmul2_rn(cs[j], sth[j]));
-            cs[j] = nc;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 t = rp[(long long)pk * 32 + 4 * c8 + j];
-            cs[j] = make_float2(t.x, t.y);
-            sn[j] = make_float2(t.z, t.w);
-          }
-        }
-        prev = pk;
-        uint32_t ol[4], oh[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 av = bf2(get_w(lo[k], j)), bv = bf2(get_w(hi[k], j));
-          const float2 yl = __ffma2_rn(av, cs[j], __fmul2_rn(make_float2(-bv.x, -bv.y), sn[j]));   // a cos - b sin
-          const float2 yh = __ffma2_rn(av, sn[j], __fmul2_rn(bv, cs[j]));                        // a sin + b cos
-          ol[j] = pack_bf16(yl.x, yl.y);
-          oh[j] = pack_bf16(yh.x, yh.y);
-        }
-        ylo = make_uint4(ol[0], ol[1], ol[2], ol[3]);
-        yhi = make_uint4(oh[0], oh[1], oh[2], oh[3]);
-      } else {
-        prev = -3;
-      }
-      sts128(addr[k], ylo);
-      sts128(addr[k] + 16384, yhi);
-    }
-  }
-}
-
-// Raw Q rows [m0 + 128*qt, +128) of an item -> SW128 tile in smem by cp.async (16 chunks
-// per thread, (query, head) advanced incrementally), then rotated in place at the query
-// id (8 rows x 8 frequencies per thread).  Executed by one 128-thread warpgroup.
-__device__ __forceinline__ void issue_q_tile(const AttnParams& p, const Item& w, int qt, int lt, uint32_t qtile) {
-  const __nv_bfloat16* __restrict__ Qg = reinterpret_cast<const __nv_bfloat16*>(p.q);
-  const int ch = lt & 15;
-  int rgl = w.m0 + qt * 128 + (lt >> 4);
-  int qi = rgl / p.grp, hh = rgl % p.grp;
-  const int step_i = 8 / p.grp, step_h = 8 % p.grp;
-  const __nv_bfloat16* qbase = Qg + ((long long)w.pp * p.n_q) * p.Hq * 128 + (long long)w.g * p.grp * 128 + 8 * ch;
-  const uint32_t dbase = qtile + (ch >> 3) * 16384;
-#pragma unroll 4
-  for (int it = 0; it < 16; ++it) {
-    const int r = it * 8 + (lt >> 4);
-    const bool ok = rgl < w.rows_total;
-    const __nv_bfloat16* src = qbase + ((long long)qi * p.Hq + hh) * 128;
-    cp_async16(dbase + r * 128 + (((ch & 7) ^ (r & 7)) << 4), ok ? (const void*)src : (const void*)Qg, ok ? 16u : 0u);
-    rgl += 8;
-    qi += step_i;
-    hh += step_h;
-    if (hh >= p.grp) { hh -= p.grp; ++qi; }
-  }
-}
-__device__ __forceinline__ void rotate_q_tile(const AttnParams& p, const Item& w, int qt, int lt, uint32_t qtile,
-                                              int bar_id) {
-  const float4* __restrict__ rp = p.rope_pairs;
-  const int c8 = lt & 7, rg8 = lt >> 3;
-  float2 cth[4], sth[4];
-  float4 pre[4];
-  int pos[8];
-  const int row0 = w.m0 + qt * 128 + rg8 * 8;
-  int i = row0 / p.grp, hh = row0 % p.grp;
-  const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    pos[k] = (row0 + k < w.rows_total) ? p.q_pos0 + i : -1;
-    if (dbg && c8 == 0 && hh == 0 && pos[k] >= 0) p.dbg_pos[p.A + p.R + p.dbg_M + i] = pos[k];
-    if (++hh == p.grp) { hh = 0; ++i; }
-  }
-  const int p0 = max(pos[0], 0);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float4 t = rp[32 + 4 * c8 + j];
-    cth[j] = make_float2(t.x, t.y);
-    sth[j] = make_float2(t.z, t.w);
-    pre[j] = rp[(long long)p0 * 32 + 4 * c8 + j];
-  }
-  cp_async_wait_all();
-  named_bar(bar_id, 128);
-  rotate8(qtile, rg8 * 8, c8, rp, cth, sth, pos, pre, p0);
-  fence_proxy_async();
-}
 
 // ------------------------------------------------------------------ kernel
 // Two attention problems can share one persistent launch (the fused step: attend items
@@ -594,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool full = (c_lo == 0) && (c_hi == 128);
         mbar_wait(bar(B_S + qt), g & 1);
         if (rloc == 0) TRACE(EV_S0 + qt, g);
-        if (warp_dead) {                      // all 32 rows are padding: their P / O are never used
+        if (warp_dead || DSC_ABL_SOFTMAX) {   // all 32 rows are padding: their P / O are never used
           mbar_arrive(bar(B_P + qt));
           continue;
         }
@@ -874,7 +465,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(bar(B_KR + ks), (g / KST) & 1);
         if (lt == 0) TRACE(EV_KR, g);
-        rotate8(sbase + OFF_K + ks * kTileBytes, rg8 * 8, c8, rp, cth, sth, kpos, cur, max(cur_pos, 0));
+        if (!DSC_ABL_ROT)
+          rotate8(sbase + OFF_K + ks * kTileBytes, rg8 * 8, c8, rp, cth, sth, kpos, cur, max(cur_pos, 0));
         fence_proxy_async();
         mbar_arrive(bar(B_KF + ks));
         if (lt == 0) TRACE(EV_KDONE, g);

@@ -62,7 +62,7 @@ enum { DSCACHE_DTYPE_BF16 = 0, DSCACHE_DTYPE_FP32 = 1 };
 enum { DSCACHE_ROPE_SPLIT_HALF = 0,   /* pairs (i, i+d/2): Qwen2 / LLaVA-OV-7B (reading Q7, default) */
        DSCACHE_ROPE_ADJACENT = 1 };   /* pairs (2i, 2i+1)                                            */
 enum { DSCACHE_IMPL_AUTO = 0,         /* tcgen05 kernel when eligible, else the SIMT kernel          */
-       DSCACHE_IMPL_TC = 1,           /* force tcgen05 (E_CONFIG unless bf16, d=128, split-half, tpf>=128) */
+       DSCACHE_IMPL_TC = 1,           /* force tcgen05 (E_CONFIG unless bf16, d=128, split-half RoPE)    */
        DSCACHE_IMPL_SIMT = 2 };       /* force the fp32 CUDA-core kernel                             */
 
 typedef struct {
@@ -102,7 +102,8 @@ typedef struct {
 } dscache_state;
 
 /* Create a handle: validates the configuration, allocates the ring
- * [S][N][Hkv][R][d] for K and V (raw, un-rotated), the sink slabs [S][N][Hkv][A][d],
+ * [S][N][Hkv][R + 128][d] for K and V (raw, un-rotated; rows R..R+127 mirror slots
+ * 0..127 so that any 128 consecutive slots are one contiguous box), the sink slabs [S][N][Hkv][A][d],
  * and the fp32 RoPE (cos, sin) table built in fp64 for ids 0 .. max_position-1.
  * The ring is zero-initialised (finite).  Synchronises the device.
  * Errors: E_ARG (null), E_CONFIG (d not in {64,128}, Hq % Hkv, budgets < 0, tpf < 1,

@@ -52,14 +52,7 @@ constexpr int OFF_BAR = OFF_V + VST * kTileBytes;
 constexpr int B_Q = 0 /* +qt */, B_KR = 2, B_KF = 5, B_KE = 8, B_VF = 11, B_VE = 13, B_S = 15, B_P = 17, B_O = 19,
               B_OF = 21, B_N = 23;
 // setmaxnreg budget per warpgroup: 2*softmax + rotation + copy/MMA <= 512 (x 128 threads)
-#ifndef DSC_SM1
-#define DSC_SM1 0
-#endif
-#if DSC_SM1
-constexpr int kRegSoftmax = 184, kRegRotate = 104, kRegCopy = 40;
-#else
 constexpr int kRegSoftmax = 144, kRegRotate = 136, kRegCopy = 88;
-#endif
 static_assert(2 * kRegSoftmax + kRegRotate + kRegCopy <= 512, "setmaxnreg budget exceeds the 64K register file");
 constexpr int kThreadRegs = 65536 / kThreads;   // allocation at launch (128); inc above it, dec below it
 static_assert(kRegSoftmax > kThreadRegs && kRegCopy < kThreadRegs, "softmax must grow, copy/MMA must shrink");
@@ -77,7 +70,25 @@ static_assert(kNQT * 128 == kMBlockRows, "work items are 256-row m-blocks");
 #ifndef DSC_ABL_ROT
 #define DSC_ABL_ROT 0
 #endif
+// DSC_ABL_EX2 replaces ex2 by a copy (MUFU-free softmax), DSC_ABL_PST skips the P store to TMEM
+#ifndef DSC_ABL_EX2
+#define DSC_ABL_EX2 0
+#endif
+#ifndef DSC_ABL_PST
+#define DSC_ABL_PST 0
+#endif
 constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, this many use exp2_poly2
+// DSC_PINGPONG: the exp passes of the two softmax warpgroups alternate (a token passed
+// through two named barriers), so each runs with the MUFU to itself while the tensor core
+// works on the other Q tile; the max passes still overlap
+#ifndef DSC_PINGPONG
+#define DSC_PINGPONG 1
+#endif
+constexpr int kBarTok0 = 4, kBarTok1 = 5;     // named barriers: exp-pass token of WG0 / WG1
+// DSC_INTERLEAVE: the fused step interleaves attend and build items per (problem, kv head)
+#ifndef DSC_INTERLEAVE
+#define DSC_INTERLEAVE 0
+#endif
 #ifndef DSC_QFIRST
 #define DSC_QFIRST 0
 #endif
@@ -86,7 +97,8 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 // Two attention problems can share one persistent launch (the fused step: attend items
 // first, then build_instant items); items [0, na) use pa, [na, na + nb) use pb.
 __global__ void __launch_bounds__(kThreads, 1)
-    attn_tc_kernel(const __grid_constant__ AttnParams pa, const __grid_constant__ AttnParams pb, int na, int nb) {
+    attn_tc_kernel(const __grid_constant__ AttnParams pa, const __grid_constant__ AttnParams pb, int na, int nb, int ka,
+                   int kb) {
   const AttnParams& p = pa;   // launch-wide fields (rope table, tensor maps, trace) are shared
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -97,8 +109,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = na + nb;
-#define ITEM_PARAMS(I) ((I) < na ? pa : pb)
-#define ITEM_LOCAL(I) ((I) < na ? (I) : (I) - na)
+  // kb > 0: the items of pa and pb are interleaved in groups of ka (pa) + kb (pb) items
+  // (one group per (problem, kv head) when both use the head-major item order)
+#define ITEM_B(I) (kb > 0 ? ((I) % (ka + kb)) >= ka : (I) >= na)
+#define ITEM_PARAMS(I) (ITEM_B(I) ? pb : pa)
+#define ITEM_LOCAL(I)                                                                                  \
+  (kb > 0 ? (ITEM_B(I) ? ((I) / (ka + kb)) * kb + ((I) % (ka + kb)) - ka : ((I) / (ka + kb)) * ka + ((I) % (ka + kb))) \
+          : (ITEM_B(I) ? (I) - na : (I)))
 
   if (threadIdx.x == 0) {
     mbar_init(bar(B_Q + 0), 128);
@@ -155,6 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       rotate_q_tile(p0, w0, qt, lt, qtile, 2 + qt);
       mbar_arrive(bar(B_Q + qt));
     }
+    const int tok_mine = qt == 0 ? kBarTok0 : kBarTok1, tok_other = qt == 0 ? kBarTok1 : kBarTok0;
+    if (DSC_PINGPONG && qt == 1) named_bar_arrive(kBarTok0, 256);   // WG0 takes the first exp pass
     int gt = 0, kk = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
       const AttnParams& p = ITEM_PARAMS(idx);
@@ -172,13 +191,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int g = gt + jj;
         const int u = w.t_begin + jj;
         int c_lo, c_hi;
+        const TileSeg t = tile_segments(p, w, u);
+        const int nu = t.width;                // S columns [0, nu) hold this tile's scores
         if (!valid_row) {
           c_lo = 0; c_hi = 0;
         } else if (u < w.n_extra) {       // sink always visible, self row j iff its id <= lim
           c_lo = 0;
           c_hi = min(max(min(A + p.n_self, max(A, lim - p.ring_count + 1)) - 128 * u, 0), 128);
         } else {
-          const TileSeg t = tile_segments(p, w, u);
           c_lo = t.lo0;
           c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));   // id pos0 + c <= lim
         }
@@ -186,81 +206,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(bar(B_S + qt), g & 1);
         if (rloc == 0) TRACE(EV_S0 + qt, g);
         if (warp_dead || DSC_ABL_SOFTMAX) {   // all 32 rows are padding: their P / O are never used
+          if (DSC_PINGPONG) { named_bar_sync(tok_mine, 256); named_bar_arrive(tok_other, 256); }
           mbar_arrive(bar(B_P + qt));
           continue;
         }
         tc_fence_after();
-#if DSC_SM1
-        // single TMEM read of the whole S row (128 registers), mask in registers
-        uint32_t r[128];
-        tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-        tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-        tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
-        tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
-        tmem_wait_ld();
-        if (warp == 0 && lane == 0) TRACE(EV_L + 0, g);
-        const bool any_partial = __any_sync(0xffffffffu, !full);
-        if (any_partial) {
-          const unsigned span = (unsigned)max(c_hi - c_lo, 0);
-#pragma unroll
-          for (int c = 0; c < 128; ++c) r[c] = ((unsigned)(c - c_lo) < span) ? r[c] : 0xFF800000u;
-        }
-        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 128; c += 8) {
-          mx0 = fmaxf(mx0, fmaxf(__uint_as_float(r[c]), __uint_as_float(r[c + 1])));
-          mx1 = fmaxf(mx1, fmaxf(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])));
-          mx2 = fmaxf(mx2, fmaxf(__uint_as_float(r[c + 4]), __uint_as_float(r[c + 5])));
-          mx3 = fmaxf(mx3, fmaxf(__uint_as_float(r[c + 6]), __uint_as_float(r[c + 7])));
-        }
-        const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
-        const bool upd = m_tile > m + kRescaleThreshold;
-        const bool need_o = upd && (m != -INFINITY);
-        const float f = need_o ? ex2(m - m_tile) : 1.f;
-        if (upd) {
-          lsum2.x *= f; lsum2.y *= f;
-          m = m_tile;
-        }
-        if (__any_sync(0xffffffffu, need_o)) {
-          mbar_wait(bar(B_O + qt), (g - 1) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int ch = 0; ch < 4; ++ch) {
-            uint32_t o[32];
-            tmem_ld32(tO + ch * 32, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
-            tmem_st32(tO + ch * 32, o);
-          }
-          tmem_wait_st();
-        }
-        if (warp == 0 && lane == 0) TRACE(EV_L + 5, g);
-        const float m_use = (m == -INFINITY) ? 0.f : m;
-        const float2 negm2 = make_float2(-m_use, -m_use);
-        float2 l0 = make_float2(0.f, 0.f), l1 = l0;
-#pragma unroll
-        for (int c = 0; c < 128; c += 4) {
-          const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
-          const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
-          const float2 p0 = make_float2(ex2(x0.x), ex2(x0.y));
-          const float2 p1 = make_float2(ex2(x1.x), ex2(x1.y));
-          l0 = __fadd2_rn(l0, p0);
-          l1 = __fadd2_rn(l1, p1);
-          r[c >> 1] = pack_bf16(p0.x, p0.y);
-          r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
-        }
-        tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-#else
-        // pass 1: row max over the visible columns, two 64-column halves.  In a partial
-        // tile the invisible columns are set to -inf and written back to TMEM, so the
-        // exp pass needs no mask (2^-inf = 0).
+        // pass 1: row max over the visible columns, in 64-column halves.  In a partial
+        // tile the invisible columns are set to -inf and written back to TMEM, so the exp
+        // pass needs no mask (2^-inf = 0).  A tile narrower than 128 is always partial
+        // (columns past its width are stale and get masked).
         const bool any_partial = __any_sync(0xffffffffu, !full);
         const unsigned span = (unsigned)max(c_hi - c_lo, 0);
+        const int nh = (nu + 63) >> 6;
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll 1
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int hf = 0; hf < nh; ++hf) {
           uint32_t r[64];
           tmem_ld32(tS + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
           tmem_ld32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
@@ -273,11 +233,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
           }
 #pragma unroll
-          for (int c = 0; c < 64; c += 4) {
-            mx0 = fmaxf(mx0, __uint_as_float(r[c]));
-            mx1 = fmaxf(mx1, __uint_as_float(r[c + 1]));
-            mx2 = fmaxf(mx2, __uint_as_float(r[c + 2]));
-            mx3 = fmaxf(mx3, __uint_as_float(r[c + 3]));
+          for (int c = 0; c < 64; c += 8) {     // 3-input max (FMNMX3): 2 columns per instruction
+            mx0 = fmax3f(mx0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+            mx1 = fmax3f(mx1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+            mx2 = fmax3f(mx2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
+            mx3 = fmax3f(mx3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
           }
         }
         if (any_partial) tmem_wait_st();
@@ -310,33 +270,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float m_use = (m == -INFINITY) ? 0.f : m;
         const float2 negm2 = make_float2(-m_use, -m_use);
         // pass 2: P = 2^(s*scale - m) (masked -> 2^-inf = 0), packed bf16x2; half hf of S
-        // (cols 64hf..64hf+63) becomes P cols 32hf..32hf+31 (already consumed S columns)
+        // (cols 64hf..64hf+63) becomes P cols 32hf..32hf+31 (already consumed S columns);
+        // a 32-column chunk past the tile width is skipped
         float2 l0 = make_float2(0.f, 0.f), l1 = l0;
+        if (DSC_PINGPONG) named_bar_sync(tok_mine, 256);
 #pragma unroll 1
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int hf = 0; hf < nh; ++hf) {
+          const bool two = 64 * hf + 32 < nu;
           uint32_t r[64];
           tmem_ld32(tS + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-          tmem_ld32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          if (two) tmem_ld32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
           tmem_wait_ld();
           if (warp == 0 && lane == 0) TRACE(EV_L + 2 + hf, g);
+          auto exp_chunk = [&](const int cb) {   // columns cb .. cb+31 -> P words cb/2 .. cb/2+15
 #pragma unroll
-          for (int c = 0; c < 64; c += 4) {
-            const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
-            const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
-            float2 p0, p1;
-            constexpr bool poly0_any = kPolyPerGroup > 0;
-            const bool poly0 = poly0_any && ((c % 8) + 2 > 8 - kPolyPerGroup);
-            const bool poly1 = poly0_any && ((c % 8) + 4 > 8 - kPolyPerGroup);
-            if (poly0 && !any_partial) p0 = exp2_poly2(x0); else p0 = make_float2(ex2(x0.x), ex2(x0.y));
-            if (poly1 && !any_partial) p1 = exp2_poly2(x1); else p1 = make_float2(ex2(x1.x), ex2(x1.y));
-            l0 = __fadd2_rn(l0, p0);
-            l1 = __fadd2_rn(l1, p1);
-            r[c >> 1] = pack_bf16(p0.x, p0.y);
-            r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
-          }
-          tmem_st32(tS + 32 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+            for (int c = cb; c < cb + 32; c += 4) {
+              const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+              const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
+              float2 p0, p1;
+              constexpr bool poly0_any = kPolyPerGroup > 0;
+              const bool poly0 = poly0_any && ((c % 8) + 2 > 8 - kPolyPerGroup);
+              const bool poly1 = poly0_any && ((c % 8) + 4 > 8 - kPolyPerGroup);
+              if (DSC_ABL_EX2) { p0 = x0; p1 = x1; } else {
+              if (poly0 && !any_partial) p0 = exp2_poly2(x0); else p0 = make_float2(ex2(x0.x), ex2(x0.y));
+              if (poly1 && !any_partial) p1 = exp2_poly2(x1); else p1 = make_float2(ex2(x1.x), ex2(x1.y));
+              }
+              l0 = __fadd2_rn(l0, p0);
+              l1 = __fadd2_rn(l1, p1);
+              r[c >> 1] = pack_bf16(p0.x, p0.y);
+              r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
+            }
+          };
+          exp_chunk(0);
+          if (two) exp_chunk(32);
+          if (DSC_ABL_PST && r[0] != 0x12345u) continue;
+          if (two) tmem_st32(tS + 32 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          else tmem_st16(tS + 32 * hf, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
         }
-#endif
+        if (DSC_PINGPONG) named_bar_arrive(tok_other, 256);
         lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
         if (warp == 0 && lane == 0) TRACE(EV_L + 4, g);
         tmem_wait_st();
@@ -411,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 #endif
     }
+    if (DSC_PINGPONG && qt == 0) named_bar_sync(kBarTok0, 256);   // WG1's last token
   } else if (warp < 12) {
     // ================================================================ rotation (Q per item, then K tiles)
     if constexpr (kRegRotate > kThreadRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegRotate));
@@ -465,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(bar(B_KR + ks), (g / KST) & 1);
         if (lt == 0) TRACE(EV_KR, g);
-        if (!DSC_ABL_ROT)
+        if (!DSC_ABL_ROT && rg8 * 8 < t.width)   // rows >= width are never read by the MMA
           rotate8(sbase + OFF_K + ks * kTileBytes, rg8 * 8, c8, rp, cth, sth, kpos, cur, max(cur_pos, 0));
         fence_proxy_async();
         mbar_arrive(bar(B_KF + ks));
@@ -475,7 +447,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < 8; ++k) {
             const int r = rg8 * 8 + k;
             const int x = 128 * u + r;
-            if (kpos[k] >= 0) p.dbg_pos[(u < w.n_extra) ? (x < A ? x : A + p.R + (x - A)) : A + t.phys * 128 + r] = kpos[k];
+            int slot = t.slot0 + r;
+            if (slot >= p.R) slot -= p.R;
+            if (kpos[k] >= 0) p.dbg_pos[(u < w.n_extra) ? (x < A ? x : A + p.R + (x - A)) : A + slot] = kpos[k];
           }
         }
       }
@@ -502,10 +476,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int g = gt + jj, u = w.t_begin + jj, st = g % nst;
           if (g >= nst) mbar_wait(bar(b_free + st), ((g - nst) / nst) & 1);
           const uint32_t dst = sbase + off + st * kTileBytes;
+          const TileSeg t = tile_segments(p, w, u);
           if (u < w.n_extra) {
-            // sink rows (x < A) + self rows (A <= x < A + n_self), zeros elsewhere, with cp.async
+            // sink rows (x < A) + self rows (A <= x < A + n_self), zeros up to the tile
+            // width, with cp.async
+            const int nit = t.width >> 1;
 #pragma unroll 1
-            for (int it = 0; it < 64; ++it) {
+            for (int it = 0; it < nit; ++it) {
               const int id = it * 32 + lane;          // 2048 16-byte chunks
               const int r = id >> 4, ch = id & 15;
               const int x = 128 * u + r;
@@ -520,9 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(b_full + st));
           } else if (lane == 0) {
-            int phys = w.k0 + u - w.n_extra;
-            if (phys >= w.nT) phys -= w.nT;
-            const int row = (int)(w.head_row * p.R) + phys * 128;
+            const int row = (int)(w.head_row * p.Rp) + t.slot0;   // logical window tile (mirror: no wrap)
             mbar_arrive_tx(bar(b_full + st), kTileBytes);
             tma_load_2d(dst, tmap, 0, row, bar(b_full + st));
             tma_load_2d(dst + 16384, tmap, 64, row, bar(b_full + st));
@@ -534,23 +509,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else if (warp == 14 && lane == 0) {
       // ============================================================== MMA issuer
-      constexpr uint32_t IQK = idesc_bf16(128, 128, 0, 0);   // S = Q K^T, both K-major
+      constexpr uint32_t IQK0 = idesc_bf16(128, 0, 0, 0);    // S = Q K^T, both K-major; N = tile width
       constexpr uint32_t IPV = idesc_bf16(128, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
       // descriptors advance in the 14-bit start-address field: +32 B (2) per 16-element
       // K step inside a 128 B swizzle row, +16 KB (1024) to the second 64-column block
-      auto issue_qk = [&](int qt, int ks) {
+      auto issue_qk = [&](int qt, int ks, int nu) {
         const uint64_t da = sdesc(sbase + OFF_Q + qt * kTileBytes, 16, 1024);
         const uint64_t db = sdesc(sbase + OFF_K + ks * kTileBytes, 16, 1024);
+        const uint32_t iqk = IQK0 | ((uint32_t)(nu >> 3) << 17);
 #pragma unroll 1
         for (int k8 = 0; k8 < 8; ++k8) {
           const uint64_t off = (uint64_t)((k8 >> 2) * 1024 + (k8 & 3) * 2);
-          mma_ss(tmem + qt * 128, da + off, db + off, IQK, k8 > 0);
+          mma_ss(tmem + qt * 128, da + off, db + off, iqk, k8 > 0);
         }
       };
-      auto issue_pv = [&](int qt, int vs, bool acc) {
+      // K of the PV product = tile width (keys), 16 per MMA
+      auto issue_pv = [&](int qt, int vs, bool acc, int nu) {
         const uint64_t dv = sdesc(sbase + OFF_V + vs * kTileBytes, 16384, 1024);
 #pragma unroll 1
-        for (int k8 = 0; k8 < 8; ++k8)
+        for (int k8 = 0; k8 < (nu >> 4); ++k8)
           mma_ts(tmem + 256 + qt * 128, tmem + qt * 128 + k8 * 8, dv + (uint64_t)(k8 * 128), IPV,
                  (acc || k8 > 0) ? 1u : 0u);
       };
@@ -564,13 +541,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(bar(B_Q + 0), kk & 1);
         if (kk == 0) TRACE(EV_Q, 0);
         tc_fence_after();
-        issue_qk(0, gt % KST); mma_commit(bar(B_S + 0));
+        int nu = tile_segments(p, w, w.t_begin).width;
+        issue_qk(0, gt % KST, nu); mma_commit(bar(B_S + 0));
         mbar_wait(bar(B_Q + 1), kk & 1);
         tc_fence_after();
-        issue_qk(1, gt % KST); mma_commit(bar(B_S + 1));
+        issue_qk(1, gt % KST, nu); mma_commit(bar(B_S + 1));
         mma_commit(bar(B_KE + gt % KST));
         for (int jj = 0; jj < n; ++jj) {
           const int g = gt + jj, vs = g % VST;
+          const int nu_next = jj + 1 < n ? tile_segments(p, w, w.t_begin + jj + 1).width : 0;
           mbar_wait(bar(B_VF + vs), (g / VST) & 1);
           TRACE(EV_VF, g);
           for (int qt = 0; qt < 2; ++qt) {
@@ -578,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
             TRACE(EV_PV0 + qt, g);
             tc_fence_after();
-            issue_pv(qt, vs, jj > 0);
+            issue_pv(qt, vs, jj > 0, nu);
             mma_commit(bar(B_O + qt));
             if (qt == 1) mma_commit(bar(B_VE + vs));
             if (jj + 1 < n) {
@@ -588,11 +567,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 TRACE(EV_KF, g + 1);
                 tc_fence_after();
               }
-              issue_qk(qt, ks);
+              issue_qk(qt, ks, nu_next);
               mma_commit(bar(B_S + qt));
               if (qt == 1) mma_commit(bar(B_KE + ks));
             }
           }
+          nu = nu_next;
         }
         gt += n;
       }
@@ -626,7 +606,7 @@ cudaError_t make_ring_tmap(CUtensorMap* map, void* base, unsigned long long rows
     if (e != cudaSuccess || fn == nullptr) return e != cudaSuccess ? e : cudaErrorNotSupported;
     encode = reinterpret_cast<Encode>(fn);
   }
-  const cuuint64_t dims[2] = {128, rows};
+  const cuuint64_t dims[2] = {128, rows};   // rows = heads * (R + 128): ring + mirror
   const cuuint64_t strides[1] = {128 * 2};
   const cuuint32_t box[2] = {64, 128};
   const cuuint32_t estr[2] = {1, 1};
@@ -655,7 +635,15 @@ cudaError_t launch_attn_tc2(const AttnParams& pa, const AttnParams* pb, cudaStre
   const long long na = tc_items(pa), nb = pb ? tc_items(*pb) : 0;
   const long long items = na + nb;
   const unsigned grid = (unsigned)(items < num_sms ? items : num_sms);
-  tc::attn_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, st>>>(pa, pb ? *pb : pa, (int)na, (int)nb);
+  int ka = 0, kb = 0;
+#if DSC_INTERLEAVE
+  const long long G = (long long)pa.P * pa.Hkv;
+  if (pb && nb > 0 && G == (long long)pb->P * pb->Hkv && na % G == 0 && nb % G == 0) {
+    ka = (int)(na / G);
+    kb = (int)(nb / G);
+  }
+#endif
+  tc::attn_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, st>>>(pa, pb ? *pb : pa, (int)na, (int)nb, ka, kb);
   return cudaGetLastError();
 }
 

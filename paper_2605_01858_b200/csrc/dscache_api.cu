@@ -61,7 +61,7 @@ struct Schedule {
 
 struct dscache_s {
   dscache_config cfg;
-  int W, C, R, elem, npos;
+  int W, C, R, Rp, elem, npos;   // Rp = R + kMirror rows per head
   void* ring_k = nullptr;
   void* ring_v = nullptr;
   void* sink_k = nullptr;
@@ -124,8 +124,7 @@ dscache_status check_layers(dscache_t h, int lb, int lc) {
 }
 
 bool tc_eligible(const dscache_config& c) {
-  return c.dtype == DSCACHE_DTYPE_BF16 && c.head_dim == 128 && c.rope_style == DSCACHE_ROPE_SPLIT_HALF &&
-         c.tokens_per_frame >= dsc::kTileN;
+  return c.dtype == DSCACHE_DTYPE_BF16 && c.head_dim == 128 && c.rope_style == DSCACHE_ROPE_SPLIT_HALF;
 }
 
 void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
@@ -134,7 +133,7 @@ void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
   p.P = c.num_streams * lc;
   p.Hq = c.num_q_heads; p.Hkv = c.num_kv_heads; p.grp = c.num_q_heads / c.num_kv_heads; p.d = c.head_dim;
   p.sink_k = h->sink_k; p.sink_v = h->sink_v; p.A = c.sink_tokens;
-  p.ring_k = h->ring_k; p.ring_v = h->ring_v; p.R = h->R;
+  p.ring_k = h->ring_k; p.ring_v = h->ring_v; p.R = h->R; p.Rp = h->Rp;
   p.rope = h->rope; p.rope_style = c.rope_style;
   p.rope_pairs = reinterpret_cast<const float4*>(h->rope + (size_t)h->npos * (c.head_dim / 2));
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c.head_dim));
@@ -203,7 +202,7 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
     return fail(DSCACHE_E_POS_OVERFLOW, "A+W+max(C+q_max,tpf) = " + std::to_string(span) + " exceeds max_position " +
                                             std::to_string(c.max_position));
   if (c.attn_impl == DSCACHE_IMPL_TC && !tc_eligible(c))
-    return fail(DSCACHE_E_CONFIG, "tcgen05 kernel needs bf16, d=128, split-half RoPE, tpf>=128");
+    return fail(DSCACHE_E_CONFIG, "tcgen05 kernel needs bf16, d=128, split-half RoPE");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || c.device < 0 || c.device >= ndev) {
     cudaGetLastError();
@@ -215,6 +214,7 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   h->cfg = c;
   h->W = (int)W; h->C = (int)C;
   h->R = (int)(W + C + c.tokens_per_frame);
+  h->Rp = h->R + dsc::kMirror;
   h->elem = c.dtype == DSCACHE_DTYPE_BF16 ? 2 : 4;
   h->npos = c.max_position;   // RoPE table covers every id < max_position (decode ids grow per token)
   h->frames.assign(c.num_layers, 0);
@@ -229,7 +229,7 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   }
 
   const size_t heads = (size_t)c.num_streams * c.num_layers * c.num_kv_heads;
-  const size_t ring_bytes = heads * h->R * c.head_dim * h->elem;
+  const size_t ring_bytes = heads * h->Rp * c.head_dim * h->elem;
   const size_t sink_bytes = heads * std::max(c.sink_tokens, 1) * c.head_dim * h->elem;
   const size_t rope_bytes = 2 * (size_t)h->npos * (c.head_dim / 2) * sizeof(float2);   // float2 + pair-packed copy
   auto oom = [&](const char* what) {
@@ -248,7 +248,7 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   if (e == cudaSuccess) e = cudaMemset(h->sink_v, 0, sink_bytes);
   if (e == cudaSuccess) e = dsc::launch_rope_table(h->rope, h->npos, c.head_dim, c.rope_theta, 0);
   if (e == cudaSuccess && (h->impl_build == DSCACHE_IMPL_TC || h->impl_attend == DSCACHE_IMPL_TC)) {
-    const unsigned long long rows = (unsigned long long)heads * h->R;
+    const unsigned long long rows = (unsigned long long)heads * h->Rp;
     e = dsc::make_ring_tmap(&h->tmap_k, h->ring_k, rows);
     if (e == cudaSuccess) e = dsc::make_ring_tmap(&h->tmap_v, h->ring_v, rows);
   }
@@ -286,6 +286,7 @@ dscache_status dscache_append_frame(dscache_t h, int32_t lb, int32_t lc, const v
   p.k = k; p.v = v;
   p.S = c.num_streams; p.layer_count = lc; p.layer_begin = lb; p.N_total = c.num_layers; p.Hkv = c.num_kv_heads;
   p.row_bytes = c.head_dim * h->elem; p.elem_bytes = h->elem; p.n = n_tokens; p.poison_slot0 = -1;
+  p.mirror_R = 0;
   if (!h->sink_filled[lb]) {
     if (n_tokens != c.sink_tokens)
       return fail(DSCACHE_E_ARG, "first append of a layer must carry the " + std::to_string(c.sink_tokens) +
@@ -300,7 +301,7 @@ dscache_status dscache_append_frame(dscache_t h, int32_t lb, int32_t lc, const v
     return fail(DSCACHE_E_ARG, "frame append must carry tokens_per_frame = " + std::to_string(c.tokens_per_frame) +
                                    " tokens, got " + std::to_string(n_tokens));
   const int64_t f = h->frames[lb];
-  p.dst_k = h->ring_k; p.dst_v = h->ring_v; p.rows_dst = h->R;
+  p.dst_k = h->ring_k; p.dst_v = h->ring_v; p.rows_dst = h->Rp; p.mirror_R = h->R;
   p.slot0 = (int)((f * c.tokens_per_frame) % h->R);
   const int64_t ev = f - c.instant_frames - c.past_frames;
   if (h->poison && ev >= 0) p.poison_slot0 = (int)((ev * c.tokens_per_frame) % h->R);
@@ -392,16 +393,9 @@ dscache_status prep_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, c
   const int impl = h->impl_attend;
   if (impl == DSCACHE_IMPL_TC) {
     // split the key range when (problem, kv head, m-block) work items cannot fill the SMs
-    const int R = h->R, BN = dsc::kTileN;
-    const int nT = (R + BN - 1) / BN;
-    int ring_tiles = 0;
-    if (p.ring_count > 0) {
-      const int k0 = p.ring_start / BN;
-      const int end = p.ring_start + p.ring_count;
-      ring_tiles = end <= R ? (end + BN - 1) / BN - k0 : (nT - k0) + (end - R + BN - 1) / BN;
-      ring_tiles = std::min(ring_tiles, nT);
-    }
-    const int tiles = std::max(1, (p.A + n_self + BN - 1) / BN) + ring_tiles;
+    // sink/self tiles + logical window tiles (see tc_common.cuh tile_segments)
+    const int BN = dsc::kTileN;
+    const int tiles = std::max(1, (p.A + n_self + BN - 1) / BN + (p.ring_count + BN - 1) / BN);
     const int items = p.P * p.Hkv * p.n_mblocks;
     int splits = 1;
     if (items < h->num_sms) {
@@ -509,10 +503,7 @@ dscache_status dscache_update_attend(dscache_t h, int32_t lb, int32_t lc, const 
   p.self_k = p.self_v = nullptr; p.n_self = 0;
   p.dbg_pos = nullptr;
   p.n_mblocks = (p.n_q * p.grp + 2 * dsc::kTileM - 1) / (2 * dsc::kTileM);
-  // the tcgen05 kernel needs a gap of >= one tile between the window's ends in the ring
-  const int impl = (h->impl_build == DSCACHE_IMPL_TC && h->R - p.ring_count >= dsc::kTileN) ? DSCACHE_IMPL_TC
-                                                                                            : DSCACHE_IMPL_SIMT;
-  return run_attention(h, p, impl, 0, (cudaStream_t)stream);
+  return run_attention(h, p, h->impl_build, 0, (cudaStream_t)stream);
 }
 
 dscache_status dscache_get_state(dscache_t h, int32_t layer, dscache_state* out) {
@@ -534,30 +525,33 @@ dscache_status dscache_get_state(dscache_t h, int32_t layer, dscache_state* out)
   return DSCACHE_OK;
 }
 
+// rows per head [rows] copied out of a device layout with `pitch_rows` rows per head
 static dscache_status copy_rows(dscache_t h, int s_idx, int layer, const void* dk, const void* dv, int rows,
-                                void* kh, void* vh) {
+                                int pitch_rows, void* kh, void* vh) {
   if (!h || !kh || !vh) return fail(DSCACHE_E_ARG, "null argument");
   const dscache_config& c = h->cfg;
   if (s_idx < 0 || s_idx >= c.num_streams || layer < 0 || layer >= c.num_layers)
     return fail(DSCACHE_E_ARG, "stream/layer out of range");
   DeviceGuard dg(c.device);
-  const size_t per = (size_t)c.num_kv_heads * rows * c.head_dim * h->elem;
-  const size_t off = ((size_t)s_idx * c.num_layers + layer) * per;
+  const size_t row_bytes = (size_t)c.head_dim * h->elem;
+  const size_t off = ((size_t)s_idx * c.num_layers + layer) * c.num_kv_heads * pitch_rows * row_bytes;
   DSC_CUDA(cudaDeviceSynchronize());
-  DSC_CUDA(cudaMemcpy(kh, (const char*)dk + off, per, cudaMemcpyDeviceToHost));
-  DSC_CUDA(cudaMemcpy(vh, (const char*)dv + off, per, cudaMemcpyDeviceToHost));
+  DSC_CUDA(cudaMemcpy2D(kh, rows * row_bytes, (const char*)dk + off, pitch_rows * row_bytes, rows * row_bytes,
+                        c.num_kv_heads, cudaMemcpyDeviceToHost));
+  DSC_CUDA(cudaMemcpy2D(vh, rows * row_bytes, (const char*)dv + off, pitch_rows * row_bytes, rows * row_bytes,
+                        c.num_kv_heads, cudaMemcpyDeviceToHost));
   return DSCACHE_OK;
 }
 
 dscache_status dscache_copy_ring(dscache_t h, int32_t s_idx, int32_t layer, void* kh, void* vh) {
   if (!h) return fail(DSCACHE_E_ARG, "null handle");
-  return copy_rows(h, s_idx, layer, h->ring_k, h->ring_v, h->R, kh, vh);
+  return copy_rows(h, s_idx, layer, h->ring_k, h->ring_v, h->R, h->Rp, kh, vh);
 }
 
 dscache_status dscache_copy_sink(dscache_t h, int32_t s_idx, int32_t layer, void* kh, void* vh) {
   if (!h) return fail(DSCACHE_E_ARG, "null handle");
   if (h->cfg.sink_tokens == 0) return DSCACHE_OK;
-  return copy_rows(h, s_idx, layer, h->sink_k, h->sink_v, h->cfg.sink_tokens, kh, vh);
+  return copy_rows(h, s_idx, layer, h->sink_k, h->sink_v, h->cfg.sink_tokens, h->cfg.sink_tokens, kh, vh);
 }
 
 int32_t dscache_debug_len(dscache_t h) {

@@ -9,6 +9,7 @@ namespace dsc {
 
 constexpr int kTileN = 128;   // keys per attention tile (tcgen05 N of QK^T, K of PV)
 constexpr int kTileM = 128;   // query rows per Q tile (tcgen05 M)
+constexpr int kMirror = 128;  // ring rows after slot R-1 mirroring slots [0, 128): a 128-row tile never wraps
 constexpr int kTraceEvents = 32, kTraceTiles = 64;
 
 // One attention launch (build_instant or attend) over P = S * layer_count problems.
@@ -30,8 +31,8 @@ struct AttnParams {
   // keys
   const void* sink_k; const void* sink_v;   // [S][N][Hkv][A][d]
   int A;
-  const void* ring_k; const void* ring_v;   // [S][N][Hkv][R][d]
-  int R;
+  const void* ring_k; const void* ring_v;   // [S][N][Hkv][Rp][d]: slots [0, R) + mirror of slots [0, 128)
+  int R, Rp;                                 // ring slots, rows per head (R + kMirror)
   int ring_start, ring_count;
   const void* self_k; const void* self_v;   // [P][n_self][Hkv][d]
   int n_self;
@@ -58,8 +59,9 @@ struct AttnParams {
 
 struct AppendParams {
   const void* k; const void* v;              // [S][lc][n][Hkv][d]
-  void* dst_k; void* dst_v;                  // ring [S][N][Hkv][R][d] or sink [S][N][Hkv][A][d]
-  int S, layer_count, layer_begin, N_total, Hkv, n, rows_dst;  // rows_dst = R or A
+  void* dst_k; void* dst_v;                  // ring [S][N][Hkv][Rp][d] or sink [S][N][Hkv][A][d]
+  int S, layer_count, layer_begin, N_total, Hkv, n, rows_dst;  // rows_dst = Rp or A
+  int mirror_R;                              // ring: slot s < kMirror is also written to row R + s; 0 = sink
   int slot0;                                 // destination row of token 0
   int row_bytes;                             // d * elem
   // eviction poison (debug): slots [poison_slot0, +n) of every head, -1 = off

@@ -73,26 +73,35 @@ __global__ void __launch_bounds__(256) append_kernel(AppendParams p) {
   const uint4* __restrict__ src = reinterpret_cast<const uint4*>(blockIdx.y ? p.v : p.k);
   uint4* __restrict__ dst = reinterpret_cast<uint4*>(blockIdx.y ? p.dst_v : p.dst_k);
   const long long stride = (long long)gridDim.x * blockDim.x;
-  auto dst_index = [&](long long idx) -> long long {
+  // destination chunk of source chunk idx; *mirror = the chunk's mirror copy (ring slot
+  // s < kMirror is also stored at row R + s), -1 if none
+  auto dst_index = [&](long long idx, long long* mirror) -> long long {
     const int c = (int)(idx % cpr);
     long long r = idx / cpr;
     const int g = (int)(r % p.Hkv); r /= p.Hkv;
     const int j = (int)(r % p.n); r /= p.n;
     const int l = (int)(r % p.layer_count);
     const long long s = r / p.layer_count;
-    const long long row = ((s * p.N_total + p.layer_begin + l) * p.Hkv + g) * p.rows_dst + p.slot0 + j;
-    return row * cpr + c;
+    const long long head = ((s * p.N_total + p.layer_begin + l) * p.Hkv + g) * p.rows_dst;
+    const int slot = p.slot0 + j;
+    *mirror = (p.mirror_R > 0 && slot < kMirror) ? (head + p.mirror_R + slot) * cpr + c : -1;
+    return (head + slot) * cpr + c;
+  };
+  auto put = [&](long long idx, uint4 v) {
+    long long mi;
+    dst[dst_index(idx, &mi)] = v;
+    if (mi >= 0) dst[mi] = v;
   };
   long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   for (; idx + 3 * stride < total; idx += 4 * stride) {
     uint4 a = ld_stream(src + idx), b = ld_stream(src + idx + stride);
     uint4 c = ld_stream(src + idx + 2 * stride), d = ld_stream(src + idx + 3 * stride);
-    dst[dst_index(idx)] = a;
-    dst[dst_index(idx + stride)] = b;
-    dst[dst_index(idx + 2 * stride)] = c;
-    dst[dst_index(idx + 3 * stride)] = d;
+    put(idx, a);
+    put(idx + stride, b);
+    put(idx + 2 * stride, c);
+    put(idx + 3 * stride, d);
   }
-  for (; idx < total; idx += stride) dst[dst_index(idx)] = ld_stream(src + idx);
+  for (; idx < total; idx += stride) put(idx, ld_stream(src + idx));
 
   if (p.poison_slot0 >= 0) {
     // sentinel = 1e30 (finite): bf16 0x714A, fp32 0x7149F2CA
@@ -105,8 +114,10 @@ __global__ void __launch_bounds__(256) append_kernel(AppendParams p) {
       const int j = (int)(r % p.n); r /= p.n;
       const int l = (int)(r % p.layer_count);
       const long long s = r / p.layer_count;
-      const long long row = ((s * p.N_total + p.layer_begin + l) * p.Hkv + g) * p.rows_dst + p.poison_slot0 + j;
-      dst[row * cpr + c] = pv;
+      const long long head = ((s * p.N_total + p.layer_begin + l) * p.Hkv + g) * p.rows_dst;
+      const int slot = p.poison_slot0 + j;
+      dst[(head + slot) * cpr + c] = pv;
+      if (p.mirror_R > 0 && slot < kMirror) dst[(head + p.mirror_R + slot) * cpr + c] = pv;
     }
   }
 }
@@ -208,7 +219,7 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnParams p) {
     } else if (L < p.A + p.ring_count) {
       int slot = p.ring_start + (L - p.A);
       if (slot >= p.R) slot -= p.R;
-      kr = RK + (head_row * p.R + slot) * D; vr = RV + (head_row * p.R + slot) * D;
+      kr = RK + (head_row * p.Rp + slot) * D; vr = RV + (head_row * p.Rp + slot) * D;
       if (dbg_keys && lane == 0) p.dbg_pos[p.A + slot] = L;
     } else {
       const int j = L - p.A - p.ring_count;

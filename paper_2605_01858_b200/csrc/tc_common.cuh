@@ -115,6 +115,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float m;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(m) : "f"(a), "f"(b), "f"(c));
+  return m;
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -168,24 +173,6 @@ __device__ __forceinline__ uint32_t sw128(int row, int col) {
   return (uint32_t)(blk * 16384 + row * 128 + ((((byte >> 4) ^ (row & 7))) << 4) + (byte & 15));
 }
 
-// Ring tile k covers slots [k*128, min(k*128+128, R)).  Valid keys of the window
-// [start, start+cnt) (mod R) form one column interval [c_a, c_b) with logical ring
-// index rel_a at c_a (needs R - cnt >= 128, guaranteed by tpf >= 128).
-__device__ __forceinline__ void ring_tile_info(int k, int R, int start, int cnt, int& c_a, int& c_b, int& rel_a) {
-  const int base = k * 128;
-  const int width = min(128, R - base);
-  if (start > base && start < base + width) {
-    c_a = start - base;
-    rel_a = 0;
-  } else {
-    c_a = 0;
-    rel_a = base - start;
-    if (rel_a < 0) rel_a += R;
-  }
-  const int rem = cnt - rel_a;
-  c_b = rem > 0 ? min(width, c_a + rem) : c_a;
-}
-
 __device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -202,6 +189,10 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   return r;
 }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_bar_sync(int id, int n) { named_bar(id, n); }
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 // timeline events (TRACE): clock64 per (event, tile) for the first ntrace_cta CTAs
 enum { EV_K_ISSUE = 0, EV_V_ISSUE, EV_KR, EV_KF, EV_S0, EV_S1, EV_P0, EV_P1, EV_PV0, EV_PV1, EV_Q, EV_START, EV_END,
@@ -220,9 +211,8 @@ struct Item {
   int pp, g, mb, sp;
   long long head_row;
   int m0, rows_total;
-  int cnt;            // ring keys needed by this m-block (causal cut)
-  int k0, nT;         // first physical ring tile, number of physical tiles
-  int n_extra;        // leading tiles holding sink + self rows (>= 1)
+  int cnt;            // window keys needed by this m-block (causal cut)
+  int n_extra;        // leading tiles holding sink + self rows (0 when A + n_self = 0)
   int t_begin, n_tiles;
 };
 
@@ -250,16 +240,8 @@ __device__ __forceinline__ Item decode_item(const AttnParams& p, int idx) {
   const int last_row = min(w.m0 + kMBlockRows, w.rows_total) - 1;
   const int lim_max = p.q_pos0 + last_row / p.grp;
   w.cnt = min(max(lim_max - p.A + 1, 0), p.ring_count);
-  w.nT = (p.R + 127) / 128;
-  w.k0 = p.ring_start / 128;
-  int rt = 0;
-  if (w.cnt > 0) {
-    const int end = p.ring_start + w.cnt;
-    rt = end <= p.R ? (end + 127) / 128 - w.k0 : (w.nT - w.k0) + (end - p.R + 127) / 128;
-    rt = min(rt, w.nT);
-  }
-  w.n_extra = max(1, (p.A + p.n_self + 127) / 128);
-  const int total = w.n_extra + rt;
+  w.n_extra = (p.A + p.n_self + 127) / 128;
+  const int total = w.n_extra + (w.cnt + 127) / 128;
   w.t_begin = min(w.sp * p.tiles_per_split, total);
   w.n_tiles = min(total, w.t_begin + p.tiles_per_split) - w.t_begin;
   return w;
@@ -267,30 +249,38 @@ __device__ __forceinline__ Item decode_item(const AttnParams& p, int idx) {
 
 // Key rows of tile u as (at most) two segments; key row r of segment s has id
 // pos0_s + r.  Tiles u < n_extra hold the sink rows (extra index x = 128u + r < A, id x)
-// and then the self rows (A <= x < A + n_self, id ring_count + x); tile u >= n_extra =
-// physical ring tile (k0 + u - n_extra) mod nT, valid rows [c_a, c_b).
+// and then the self rows (A <= x < A + n_self, id ring_count + x).  Tile u >= n_extra is
+// the LOGICAL window tile b = u - n_extra: window keys [128b, 128b + 128), i.e. the ring
+// slots (ring_start + 128b + r) mod R, read as one 128-row box from slot0 = (ring_start +
+// 128b) mod R -- the ring keeps a mirror of slots [0, 128) after slot R - 1, so the box
+// never wraps.  Row r is valid iff 128b + r < cnt, with id A + 128b + r.
+// `width` = valid rows rounded up to 16: the N of the QK^T MMA and the K of the PV MMA.
 struct TileSeg {
   int lo0, hi0, pos0_0;
   int lo1, hi1, pos0_1;
-  int phys;           // physical ring tile (u > 0), -1 for tile 0
+  int slot0;          // first ring slot of a window tile, -1 for sink/self tiles
+  int width;
 };
 
 __device__ __forceinline__ TileSeg tile_segments(const AttnParams& p, const Item& w, int u) {
   TileSeg t;
+  int valid;
   if (u < w.n_extra) {
     const int x0 = 128 * u;
     t.lo0 = 0; t.hi0 = min(max(p.A - x0, 0), 128); t.pos0_0 = x0;
     t.lo1 = t.hi0; t.hi1 = min(max(p.A + p.n_self - x0, 0), 128); t.pos0_1 = p.ring_count + x0;
-    t.phys = -1;
+    t.slot0 = -1;
+    valid = t.hi1;
   } else {
-    int k = w.k0 + u - w.n_extra;
-    if (k >= w.nT) k -= w.nT;
-    int c_a, c_b, rel_a;
-    ring_tile_info(k, p.R, p.ring_start, w.cnt, c_a, c_b, rel_a);
-    t.lo0 = c_a; t.hi0 = c_b; t.pos0_0 = p.A + rel_a - c_a;
+    const int base = 128 * (u - w.n_extra);
+    valid = min(w.cnt - base, 128);
+    t.lo0 = 0; t.hi0 = valid; t.pos0_0 = p.A + base;
     t.lo1 = 0; t.hi1 = 0; t.pos0_1 = 0;
-    t.phys = k;
+    int s0 = p.ring_start + base;
+    if (s0 >= p.R) s0 -= p.R;
+    t.slot0 = s0;
   }
+  t.width = (valid + 15) & ~15;
   return t;
 }
 __device__ __forceinline__ int seg_pos(const TileSeg& t, int r) {

@@ -54,8 +54,33 @@ def main():
             end = int(tr[c, 12, 0]) - t0
             ntiles = int((tr[c, 8] != 0).sum())
             print(f"== {name} CTA {c}: tiles {ntiles}, total {end} cycles, Q ready at {int(tr[c, 10, 0]) - t0}")
-            cols = [31, 30, 29, 2, 28, 3, 4, 6, 8, 5, 7, 9] + [22, 23, 27, 24, 25, 26]
+            cols = [0, 1, 2, 28, 3, 13, 4, 6, 8, 5, 7, 9] + [22, 23, 27, 24, 25, 26]
             print("tile " + " ".join(f"{EV[e]:>8}" for e in cols))
+            # steady-state summary over tiles 2..ntiles-2 (cycles): tile period at the S0 wait,
+            # softmax time per Q tile (S ready -> P arrived), P -> next S latency (PV + QK MMAs)
+            def ev(e, j):
+                return int(tr[c, e, j]) - t0 if int(tr[c, e, j]) else None
+            per, sm0, sm1, lat0, rot, klat, vlat = [], [], [], [], [], [], []
+            for j in range(2, min(ntiles, 64) - 1):
+                a, b = ev(4, j), ev(4, j + 1)
+                if a is not None and b is not None and b > a:
+                    per.append(b - a)
+                if ev(4, j) is not None and ev(6, j) is not None:
+                    sm0.append(ev(6, j) - ev(4, j))
+                if ev(5, j) is not None and ev(7, j) is not None:
+                    sm1.append(ev(7, j) - ev(5, j))
+                if ev(6, j) is not None and ev(4, j + 1) is not None:
+                    lat0.append(ev(4, j + 1) - ev(6, j))
+                if ev(2, j) is not None and ev(28, j) is not None:
+                    rot.append(ev(28, j) - ev(2, j))
+                if ev(0, j) is not None and ev(2, j) is not None:
+                    klat.append(ev(2, j) - ev(0, j))
+                if ev(1, j) is not None and ev(13, j) is not None:
+                    vlat.append(ev(13, j) - ev(1, j))
+            med = lambda v: sorted(v)[len(v) // 2] if v else -1
+            print(f"   summary: median tile period {med(per)}, softmax0 {med(sm0)}, softmax1 {med(sm1)}, "
+                  f"P0->S0next {med(lat0)}, K rotate {med(rot)}, K issue->landed {med(klat)}, "
+                  f"V issue->MMA {med(vlat)}")
             for j in range(min(ntiles, 64)):
                 row = [int(tr[c, e, j]) - t0 if int(tr[c, e, j]) else -1 for e in cols]
                 print(f"{j:4d} " + " ".join(f"{x:8d}" for x in row))

@@ -66,7 +66,7 @@ def _cfg(dscache, **kw):
     (dict(num_q_heads=30), -2),               # Hq % Hkv
     (dict(past_frames=0, instant_frames=0), -2),
     (dict(rope_theta=1.0), -2),
-    (dict(attn_impl=1, tokens_per_frame=16), -2),   # tcgen05 forced on an ineligible shape (tpf < 128)
+    (dict(attn_impl=1, head_dim=64), -2),     # tcgen05 forced on an ineligible shape (d = 64)
 ])
 def test_create_validation_without_gpu(kw, status):
     lib, dscache = _lib()

@@ -507,29 +507,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         gt += w.n_tiles;
       }
-    } else if (warp == 14 && lane == 0) {
-      // ============================================================== MMA issuer
+    } else if (warp == 14) {
+      // ============================================================== MMA issuer (whole warp, elected lane issues)
       constexpr uint32_t IQK0 = idesc_bf16(128, 0, 0, 0);    // S = Q K^T, both K-major; N = tile width
       constexpr uint32_t IPV = idesc_bf16(128, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
       // descriptors advance in the 14-bit start-address field: +32 B (2) per 16-element
       // K step inside a 128 B swizzle row, +16 KB (1024) to the second 64-column block
+      // fully unrolled: the descriptors are formed once per call and advanced by
+      // immediates, so each tcgen05.mma costs a handful of uniform-datapath instructions
+      // (a rolled loop re-materialised them per MMA and capped the issue rate well below
+      // the tensor pipe's 64 cycles per M128 N128 K16 MMA)
       auto issue_qk = [&](int qt, int ks, int nu) {
         const uint64_t da = sdesc(sbase + OFF_Q + qt * kTileBytes, 16, 1024);
         const uint64_t db = sdesc(sbase + OFF_K + ks * kTileBytes, 16, 1024);
         const uint32_t iqk = IQK0 | ((uint32_t)(nu >> 3) << 17);
-#pragma unroll 1
+        const uint32_t d = tmem + qt * 128;
+#pragma unroll
         for (int k8 = 0; k8 < 8; ++k8) {
           const uint64_t off = (uint64_t)((k8 >> 2) * 1024 + (k8 & 3) * 2);
-          mma_ss(tmem + qt * 128, da + off, db + off, iqk, k8 > 0);
+          mma_ss_w(d, da + off, db + off, iqk, k8 > 0);
         }
       };
       // K of the PV product = tile width (keys), 16 per MMA
       auto issue_pv = [&](int qt, int vs, bool acc, int nu) {
         const uint64_t dv = sdesc(sbase + OFF_V + vs * kTileBytes, 16384, 1024);
-#pragma unroll 1
-        for (int k8 = 0; k8 < (nu >> 4); ++k8)
-          mma_ts(tmem + 256 + qt * 128, tmem + qt * 128 + k8 * 8, dv + (uint64_t)(k8 * 128), IPV,
-                 (acc || k8 > 0) ? 1u : 0u);
+        const uint32_t d = tmem + 256 + qt * 128, a = tmem + qt * 128;
+        const int nk = nu >> 4;
+        mma_ts_w(d, a, dv, IPV, acc ? 1u : 0u);
+#pragma unroll
+        for (int k8 = 1; k8 < 8; ++k8)
+          if (k8 < nk) mma_ts_w(d, a + k8 * 8, dv + (uint64_t)(k8 * 128), IPV, 1u);
       };
       int gt = 0, kk = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
@@ -537,39 +544,39 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Item w = decode_item(p, ITEM_LOCAL(idx));
         const int n = w.n_tiles;
         mbar_wait(bar(B_KF + gt % KST), (gt / KST) & 1);
-        TRACE(EV_KF, gt);
+        if (lane == 0) TRACE(EV_KF, gt);
         mbar_wait(bar(B_Q + 0), kk & 1);
-        if (kk == 0) TRACE(EV_Q, 0);
+        if (kk == 0 && lane == 0) TRACE(EV_Q, 0);
         tc_fence_after();
         int nu = tile_segments(p, w, w.t_begin).width;
-        issue_qk(0, gt % KST, nu); mma_commit(bar(B_S + 0));
+        issue_qk(0, gt % KST, nu); mma_commit_w(bar(B_S + 0));
         mbar_wait(bar(B_Q + 1), kk & 1);
         tc_fence_after();
-        issue_qk(1, gt % KST, nu); mma_commit(bar(B_S + 1));
-        mma_commit(bar(B_KE + gt % KST));
+        issue_qk(1, gt % KST, nu); mma_commit_w(bar(B_S + 1));
+        mma_commit_w(bar(B_KE + gt % KST));
         for (int jj = 0; jj < n; ++jj) {
           const int g = gt + jj, vs = g % VST;
           const int nu_next = jj + 1 < n ? tile_segments(p, w, w.t_begin + jj + 1).width : 0;
           mbar_wait(bar(B_VF + vs), (g / VST) & 1);
-          TRACE(EV_VF, g);
+          if (lane == 0) TRACE(EV_VF, g);
           for (int qt = 0; qt < 2; ++qt) {
             mbar_wait(bar(B_P + qt), g & 1);
             if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
-            TRACE(EV_PV0 + qt, g);
+            if (lane == 0) TRACE(EV_PV0 + qt, g);
             tc_fence_after();
             issue_pv(qt, vs, jj > 0, nu);
-            mma_commit(bar(B_O + qt));
-            if (qt == 1) mma_commit(bar(B_VE + vs));
+            mma_commit_w(bar(B_O + qt));
+            if (qt == 1) mma_commit_w(bar(B_VE + vs));
             if (jj + 1 < n) {
               const int ks = (g + 1) % KST;
               if (qt == 0) {
                 mbar_wait(bar(B_KF + ks), ((g + 1) / KST) & 1);
-                TRACE(EV_KF, g + 1);
+                if (lane == 0) TRACE(EV_KF, g + 1);
                 tc_fence_after();
               }
               issue_qk(qt, ks, nu_next);
-              mma_commit(bar(B_S + qt));
-              if (qt == 1) mma_commit(bar(B_KE + ks));
+              mma_commit_w(bar(B_S + qt));
+              if (qt == 1) mma_commit_w(bar(B_KE + ks));
             }
           }
           nu = nu_next;
@@ -578,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // drain: the last V-free commit tracks every MMA of this CTA
       if (gt > 0) mbar_wait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1);
-      TRACE(EV_END, 0);
+      if (lane == 0) TRACE(EV_END, 0);
     }
   }
 

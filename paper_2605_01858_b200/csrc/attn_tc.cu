@@ -5,32 +5,37 @@
 //
 // Position-agnostic encoding (Def. 4.1): the ring holds raw
 // K; each K tile is rotated in registers by its use-time id (consecutive from 0,
-// PAPER.md:236) while it is moved global -> shared, once per CTA for the 256
-// query rows (2 x 128-row Q tiles) that share it.  Softmax a_ij =
-// softmax(Q_i K_j / sqrt(d)) in the exp2 domain with lazy rescale.
+// PAPER.md:236) while it sits in shared memory, once per CTA for the 256 query rows
+// (2 x 128-row Q tiles) that share it.  Softmax a_ij = softmax(Q_i K_j / sqrt(d))
+// in the exp2 domain with lazy rescale.
 //
-// Persistent CTAs (grid <= #SMs) walk a longest-first list of work items
-// (problem, kv head, 256-row m-block, key split); every pipeline phase runs on a
-// CTA-global tile counter, Q and O are recycled across items by barriers.
+// Persistent CTAs (grid <= #SMs) walk a list of work items (problem, kv head,
+// 256-row m-block, key split); every pipeline phase runs on a CTA-global tile counter
+// g, Q and O are recycled across items by barriers.
+//
+// Key tiles are 64 keys wide, so S of each Q tile is DOUBLE-BUFFERED in TMEM: the MMA
+// computes S(g+1) (and issues S(g+2) right after PV(g)) while the softmax works on
+// S(g), and a softmax warpgroup moves to its next tile without waiting for the tensor
+// core.  TMEM (512 columns):
+//   S[qt][b] = cols qt*128 + b*64 (b = g & 1)   O[qt] = cols 256 + qt*128
+// P(g) (bf16x2, 32 columns) overwrites the first half of S[qt][g&1] and feeds
+// O[qt] += P V as the TMEM A operand.  MMA issue order per tile g (after the item's
+// prologue S(g0), S(g0+1)): PV0(g) S0(g+2) PV1(g) S1(g+2).
 //
 // CTA = 16 warps:
-//   warps 0-3  softmax of Q tile 0 (thread = query row = TMEM lane)
+//   warps 0-3  softmax of Q tile 0 (thread = query row = TMEM lane); one TMEM read per
+//              tile (64 columns), row max, exps, P store
 //   warps 4-7  softmax of Q tile 1
 //   warps 8-11 rotation: every raw K tile in place in shared memory
 //              (LDS -> rotate -> STS), with R(p+1) = R(p) R(1) between consecutive ids
 //   (each softmax warpgroup loads + rotates the Q tile of its next item itself, as soon
-//    as it has consumed S of its last tile, overlapped with its epilogue)
-//   warp 12    K copy: raw K tiles -> SW128 smem; TMA (2 x 64x128 boxes) for ring
-//              tiles, cp.async for the sink/self tile
+//    as it has consumed S of its last tile, before its epilogue)
+//   warp 12    K copy: raw K tiles -> SW128 smem; TMA (2 x 64x64 boxes) for window
+//              tiles, cp.async for sink/self tiles
 //   warp 13    V copy: same for V (K and V stage recycling is independent)
-//   warp 14    TMEM allocator + single-thread tcgen05.mma issuer
-//   warp 15    idle
-// Softmax reads each S row from TMEM in two 64-column halves (max pass, then
-// exp pass); registers (setmaxnreg): softmax 144, rotation 136, copy/MMA 88.
-// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512);
-// P_qt (bf16x2) overwrites S_qt cols [0,64) and feeds O_qt += P V as the TMEM A operand.
-// MMA issue order S0_0 S1_0 | PV0_j S0_{j+1} PV1_j S1_{j+1} | ... so each softmax
-// warpgroup overlaps the other Q tile's MMAs.
+//   warp 14    TMEM allocator + MMA issuer (whole warp, elected lane issues)
+//   warp 15    idle (second MMA issuer with DSC_MMA2)
+// Registers (setmaxnreg): softmax 144, rotation 136, copy/MMA 88.
 #include "tc_common.cuh"
 
 namespace dsc {
@@ -40,57 +45,73 @@ using namespace tcc;
 constexpr int kNQT = 2;                       // Q tiles per CTA
 constexpr int kWarps = 16;
 constexpr int kThreads = kWarps * 32;
-constexpr int kTileBytes = 128 * 128 * 2;     // one 128 x 128 bf16 tile
-constexpr int KST = 3;                        // K stages (raw -> rotated in place)
-constexpr int VST = 2;                        // V stages
+constexpr int kQBytes = 128 * 128 * 2;        // one 128-row Q tile (2 x 64-column SW128 blocks)
+constexpr int kKT = kTileN;                   // keys per K/V tile
+constexpr int kKVHalf = kKT * 128;            // bytes of one 64-column SW128 block of a K/V tile
+constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
+constexpr int KST = 5;                        // K stages (raw -> rotated in place)
+constexpr int VST = 5;                        // V stages
 constexpr int OFF_Q = 0;
-constexpr int OFF_K = OFF_Q + kNQT * kTileBytes;
-constexpr int OFF_V = OFF_K + KST * kTileBytes;
-constexpr int OFF_BAR = OFF_V + VST * kTileBytes;
-// barriers (8 B each): Q ready | Q free | K raw landed | K rotated | K free | V landed | V free |
-// S ready | P ready | O done | O read (epilogue done)
-constexpr int B_Q = 0 /* +qt */, B_KR = 2, B_KF = 5, B_KE = 8, B_VF = 11, B_VE = 13, B_S = 15, B_P = 17, B_O = 19,
-              B_OF = 21, B_N = 23;
+constexpr int OFF_K = OFF_Q + kNQT * kQBytes;
+constexpr int OFF_V = OFF_K + KST * kKVBytes;
+constexpr int OFF_BAR = OFF_V + VST * kKVBytes;
+// barriers (8 B each): Q ready [qt] | K raw landed | K rotated | K free | V landed | V free |
+// S ready [qt][buf] | P ready [qt][buf] | PV done [qt][buf] | O read (epilogue done) [qt].
+// Every barrier a waiter may lag is per buffer parity, so no waiter is ever two phases
+// behind (the parity test of mbarrier.try_wait cannot tell phase k from phase k+2): with S
+// prefetched two tiles ahead, PV(g-1) may still be pending when the softmax finishes tile g.
+constexpr int B_Q = 0, B_KR = 2, B_KF = B_KR + KST, B_KE = B_KF + KST, B_VF = B_KE + KST, B_VE = B_VF + VST,
+              B_S = B_VE + VST, B_P = B_S + 4, B_O = B_P + 4, B_OF = B_O + 4, B_N = B_OF + 2;
 // setmaxnreg budget per warpgroup: 2*softmax + rotation + copy/MMA <= 512 (x 128 threads)
 constexpr int kRegSoftmax = 144, kRegRotate = 136, kRegCopy = 88;
 static_assert(2 * kRegSoftmax + kRegRotate + kRegCopy <= 512, "setmaxnreg budget exceeds the 64K register file");
 constexpr int kThreadRegs = 65536 / kThreads;   // allocation at launch (128); inc above it, dec below it
 static_assert(kRegSoftmax > kThreadRegs && kRegCopy < kThreadRegs, "softmax must grow, copy/MMA must shrink");
 constexpr int kSmemBytes = OFF_BAR + B_N * 8 + 16 + 1024;   // + tmem slot + alignment slack
+static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+static_assert(kKT == 64, "the S double buffer assumes 64-key tiles");
 constexpr float kRescaleThreshold = 8.0f;     // log2 units (factor 256)
 static_assert(kNQT * 128 == kMBlockRows, "work items are 256-row m-blocks");
 #ifndef DSC_POLY
 #define DSC_POLY 0
 #endif
 // ablation knobs (timing experiments only; results are wrong when set):
-// DSC_ABL_SOFTMAX skips the softmax body, DSC_ABL_ROT skips the K rotation
+// DSC_ABL_SOFTMAX skips the softmax body, DSC_ABL_ROT skips the K rotation,
+// DSC_ABL_EX2 replaces ex2 by a copy (MUFU-free softmax)
 #ifndef DSC_ABL_SOFTMAX
 #define DSC_ABL_SOFTMAX 0
 #endif
 #ifndef DSC_ABL_ROT
 #define DSC_ABL_ROT 0
 #endif
-// DSC_ABL_EX2 replaces ex2 by a copy (MUFU-free softmax), DSC_ABL_PST skips the P store to TMEM
 #ifndef DSC_ABL_EX2
 #define DSC_ABL_EX2 0
 #endif
-#ifndef DSC_ABL_PST
-#define DSC_ABL_PST 0
-#endif
 constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, this many use exp2_poly2
-// DSC_PINGPONG: the exp passes of the two softmax warpgroups alternate (a token passed
-// through two named barriers), so each runs with the MUFU to itself while the tensor core
-// works on the other Q tile; the max passes still overlap
-#ifndef DSC_PINGPONG
-#define DSC_PINGPONG 1
+// DSC_MMA2 1: two MMA-issuing warps (14: Q tile 0, 15: Q tile 1).  Faster steady tiles,
+// but warp 15 then competes for issue slots with the softmax/rotation warps of SMSP 3 and
+// the item switches got slower: measured 11.1K vs 13.3K frames/s (c5), so off by default.
+#ifndef DSC_MMA2
+#define DSC_MMA2 0
 #endif
-constexpr int kBarTok0 = 4, kBarTok1 = 5;     // named barriers: exp-pass token of WG0 / WG1
+// DSC_QPREF: L2 prefetch of the next item's Q rows at item start; DSC_QREG: Q rows loaded and
+// rotated in registers (else cp.async + in-smem rotation).  Both measured slower on c5
+// (QREG 11.3K vs 12.8K frames/s: the inlined row path raises the softmax warps' register
+// pressure), so both are off.
+#ifndef DSC_QPREF
+#define DSC_QPREF 0
+#endif
+#ifndef DSC_QREG
+#define DSC_QREG 0
+#endif
 // DSC_INTERLEAVE: the fused step interleaves attend and build items per (problem, kv head)
 #ifndef DSC_INTERLEAVE
 #define DSC_INTERLEAVE 0
 #endif
+// DSC_QFIRST 1: the next item's Q tile is published before the epilogue, so its first S
+// MMAs run while O is read out
 #ifndef DSC_QFIRST
-#define DSC_QFIRST 0
+#define DSC_QFIRST 1
 #endif
 
 // ------------------------------------------------------------------ kernel
@@ -123,18 +144,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < KST; ++i) {
       mbar_init(bar(B_KR + i), 1);
       mbar_init(bar(B_KF + i), 128);
-      mbar_init(bar(B_KE + i), 1);
+      mbar_init(bar(B_KE + i), DSC_MMA2 ? 2 : 1);   // one commit per MMA warp
     }
     for (int i = 0; i < VST; ++i) {
       mbar_init(bar(B_VF + i), 1);
-      mbar_init(bar(B_VE + i), 1);
+      mbar_init(bar(B_VE + i), DSC_MMA2 ? 2 : 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(bar(B_S + i), 1);
       mbar_init(bar(B_P + i), 128);
       mbar_init(bar(B_O + i), 1);
-      mbar_init(bar(B_OF + i), 128);
     }
+    for (int i = 0; i < 2; ++i) mbar_init(bar(B_OF + i), 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
   }
@@ -159,21 +180,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int qt = warp >> 2, quarter = warp & 3;
     const int rloc = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t tS = tmem + lane_off + (uint32_t)(qt * 128);
+    const uint32_t tS0 = tmem + lane_off + (uint32_t)(qt * 128);
     const uint32_t tO = tmem + lane_off + (uint32_t)(256 + qt * 128);
     const float sl2 = p.scale_log2;
     const float2 scale2 = make_float2(sl2, sl2);
-    const int lt = threadIdx.x - qt * 128;          // 0..127 within the warpgroup
-    const uint32_t qtile = sbase + OFF_Q + qt * kTileBytes;
+
+    const uint32_t qtile = sbase + OFF_Q + qt * kQBytes;
     if (blockIdx.x < (unsigned)n_items) {            // Q tile of the first item
       const AttnParams& p0 = ITEM_PARAMS((int)blockIdx.x);
       const Item w0 = decode_item(p0, ITEM_LOCAL((int)blockIdx.x));
-      issue_q_tile(p0, w0, qt, lt, qtile);
-      rotate_q_tile(p0, w0, qt, lt, qtile, 2 + qt);
+#if DSC_QREG
+      load_q_row_rotated(p0, w0, qt, rloc, qtile);
+      fence_proxy_async();
+#else
+      issue_q_tile(p0, w0, qt, threadIdx.x - qt * 128, qtile);
+      rotate_q_tile(p0, w0, qt, threadIdx.x - qt * 128, qtile, 2 + qt);
+#endif
       mbar_arrive(bar(B_Q + qt));
     }
-    const int tok_mine = qt == 0 ? kBarTok0 : kBarTok1, tok_other = qt == 0 ? kBarTok1 : kBarTok0;
-    if (DSC_PINGPONG && qt == 1) named_bar_arrive(kBarTok0, 256);   // WG0 takes the first exp pass
     int gt = 0, kk = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
       const AttnParams& p = ITEM_PARAMS(idx);
@@ -185,62 +209,81 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int qi = valid_row ? rglob / p.grp : 0;
       const int lim = valid_row ? p.q_pos0 + qi : -1;
       const bool warp_dead = __all_sync(0xffffffffu, !valid_row);
+      if (DSC_QPREF) {   // warm L2 with this thread's Q row of the NEXT item (fetched at the item switch)
+        const int nidx = idx + gridDim.x;
+        if (nidx < n_items) {
+          const AttnParams& pn = ITEM_PARAMS(nidx);
+          const Item wn = decode_item(pn, ITEM_LOCAL(nidx));
+          const int rn = wn.m0 + qt * 128 + rloc;
+          if (rn < wn.rows_total) {
+            const char* row = reinterpret_cast<const char*>(pn.q) +
+                              ((((long long)wn.pp * pn.n_q + rn / pn.grp) * pn.Hq + wn.g * pn.grp + rn % pn.grp) * 256);
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(row));
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(row + 128));
+          }
+        }
+      }
       float m = -INFINITY;
       float2 lsum2 = make_float2(0.f, 0.f);
       for (int jj = 0; jj < n; ++jj) {
         const int g = gt + jj;
         const int u = w.t_begin + jj;
+        const int sb = qt * 2 + (g & 1);           // S/P buffer of this tile
+        const uint32_t tS = tS0 + (uint32_t)((g & 1) * 64);
         int c_lo, c_hi;
         const TileSeg t = tile_segments(p, w, u);
-        const int nu = t.width;                // S columns [0, nu) hold this tile's scores
+        const int nu = t.width;                    // S columns [0, nu) hold this tile's scores
         if (!valid_row) {
           c_lo = 0; c_hi = 0;
-        } else if (u < w.n_extra) {       // sink always visible, self row j iff its id <= lim
+        } else if (u < w.n_extra) {                // sink always visible, self row j iff its id <= lim
           c_lo = 0;
-          c_hi = min(max(min(A + p.n_self, max(A, lim - p.ring_count + 1)) - 128 * u, 0), 128);
+          c_hi = min(max(min(A + p.n_self, max(A, lim - p.ring_count + 1)) - kKT * u, 0), kKT);
         } else {
           c_lo = t.lo0;
           c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));   // id pos0 + c <= lim
         }
-        const bool full = (c_lo == 0) && (c_hi == 128);
-        mbar_wait(bar(B_S + qt), g & 1);
+        const bool full = (c_lo == 0) && (c_hi == kKT);
+        mbar_wait(bar(B_S + sb), (g >> 1) & 1);
         if (rloc == 0) TRACE(EV_S0 + qt, g);
         if (warp_dead || DSC_ABL_SOFTMAX) {   // all 32 rows are padding: their P / O are never used
-          if (DSC_PINGPONG) { named_bar_sync(tok_mine, 256); named_bar_arrive(tok_other, 256); }
-          mbar_arrive(bar(B_P + qt));
+          mbar_arrive(bar(B_P + sb));
           continue;
         }
         tc_fence_after();
-        // pass 1: row max over the visible columns, in 64-column halves.  In a partial
-        // tile the invisible columns are set to -inf and written back to TMEM, so the exp
-        // pass needs no mask (2^-inf = 0).  A tile narrower than 128 is always partial
-        // (columns past its width are stale and get masked).
+        // one TMEM read of the tile's (up to) 64 scores; invisible columns -> -inf
+#ifdef DSC_DBG_TWO
+        const bool two = true;
+#else
+        const bool two = nu > 32;
+#endif
+        uint32_t r[64];
+        tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        if (two) tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        tmem_wait_ld();
+        if (warp == 0 && lane == 0) TRACE(EV_L + 0, g);
         const bool any_partial = __any_sync(0xffffffffu, !full);
-        const unsigned span = (unsigned)max(c_hi - c_lo, 0);
-        const int nh = (nu + 63) >> 6;
+        if (any_partial) {
+          const unsigned span = (unsigned)max(c_hi - c_lo, 0);
+#pragma unroll
+          for (int c = 0; c < 64; ++c) r[c] = ((unsigned)(c - c_lo) < span) ? r[c] : 0xFF800000u;
+        }
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll 1
-        for (int hf = 0; hf < nh; ++hf) {
-          uint32_t r[64];
-          tmem_ld32(tS + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-          tmem_ld32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-          tmem_wait_ld();
-          if (warp == 0 && lane == 0) TRACE(EV_L + hf, g);
-          if (any_partial) {
 #pragma unroll
-            for (int c = 0; c < 64; ++c) r[c] = ((unsigned)(64 * hf + c - c_lo) < span) ? r[c] : 0xFF800000u;
-            tmem_st32(tS + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-            tmem_st32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-          }
+        for (int c = 0; c < 32; c += 8) {     // 3-input max (FMNMX3): 2 columns per instruction
+          mx0 = fmax3f(mx0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+          mx1 = fmax3f(mx1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+          mx2 = fmax3f(mx2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
+          mx3 = fmax3f(mx3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
+        }
+        if (two) {
 #pragma unroll
-          for (int c = 0; c < 64; c += 8) {     // 3-input max (FMNMX3): 2 columns per instruction
+          for (int c = 32; c < 64; c += 8) {
             mx0 = fmax3f(mx0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
             mx1 = fmax3f(mx1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
             mx2 = fmax3f(mx2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
             mx3 = fmax3f(mx3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
           }
         }
-        if (any_partial) tmem_wait_st();
         const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
         // lazy rescale: move the running max only when it grew by > 2^8; the TMEM
         // load/store of O is warp-collective, so the decision is made per warp.
@@ -252,8 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           m = m_tile;
         }
         if (__any_sync(0xffffffffu, need_o)) {
-          // O_qt holds PV up to the previous tile: wait for it, rescale in TMEM
-          mbar_wait(bar(B_O + qt), (g - 1) & 1);
+          // O_qt holds P V up to tile g-1: wait for that PV, rescale in TMEM
+          mbar_wait(bar(B_O + qt * 2 + ((g - 1) & 1)), ((g - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int ch = 0; ch < 4; ++ch) {
@@ -266,53 +309,41 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tmem_wait_st();
         }
-        if (warp == 0 && lane == 0) TRACE(EV_L + 5, g);
         const float m_use = (m == -INFINITY) ? 0.f : m;
         const float2 negm2 = make_float2(-m_use, -m_use);
-        // pass 2: P = 2^(s*scale - m) (masked -> 2^-inf = 0), packed bf16x2; half hf of S
-        // (cols 64hf..64hf+63) becomes P cols 32hf..32hf+31 (already consumed S columns);
-        // a 32-column chunk past the tile width is skipped
+        // P = 2^(s*scale - m) (masked -> 2^-inf = 0) packed bf16x2 into words 0..31
         float2 l0 = make_float2(0.f, 0.f), l1 = l0;
-        if (DSC_PINGPONG) named_bar_sync(tok_mine, 256);
-#pragma unroll 1
-        for (int hf = 0; hf < nh; ++hf) {
-          const bool two = 64 * hf + 32 < nu;
-          uint32_t r[64];
-          tmem_ld32(tS + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-          if (two) tmem_ld32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-          tmem_wait_ld();
-          if (warp == 0 && lane == 0) TRACE(EV_L + 2 + hf, g);
-          auto exp_chunk = [&](const int cb) {   // columns cb .. cb+31 -> P words cb/2 .. cb/2+15
+        auto exp_chunk = [&](const int cb) {   // columns cb .. cb+31 -> P words cb/2 .. cb/2+15
 #pragma unroll
-            for (int c = cb; c < cb + 32; c += 4) {
-              const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
-              const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
-              float2 p0, p1;
-              constexpr bool poly0_any = kPolyPerGroup > 0;
-              const bool poly0 = poly0_any && ((c % 8) + 2 > 8 - kPolyPerGroup);
-              const bool poly1 = poly0_any && ((c % 8) + 4 > 8 - kPolyPerGroup);
-              if (DSC_ABL_EX2) { p0 = x0; p1 = x1; } else {
+          for (int c = cb; c < cb + 32; c += 4) {
+            const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+            const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
+            float2 p0, p1;
+            constexpr bool poly_any = kPolyPerGroup > 0;
+            const bool poly0 = poly_any && ((c % 8) + 2 > 8 - kPolyPerGroup);
+            const bool poly1 = poly_any && ((c % 8) + 4 > 8 - kPolyPerGroup);
+            if (DSC_ABL_EX2) { p0 = x0; p1 = x1; } else {
               if (poly0 && !any_partial) p0 = exp2_poly2(x0); else p0 = make_float2(ex2(x0.x), ex2(x0.y));
               if (poly1 && !any_partial) p1 = exp2_poly2(x1); else p1 = make_float2(ex2(x1.x), ex2(x1.y));
-              }
-              l0 = __fadd2_rn(l0, p0);
-              l1 = __fadd2_rn(l1, p1);
-              r[c >> 1] = pack_bf16(p0.x, p0.y);
-              r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
             }
-          };
-          exp_chunk(0);
-          if (two) exp_chunk(32);
-          if (DSC_ABL_PST && r[0] != 0x12345u) continue;
-          if (two) tmem_st32(tS + 32 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-          else tmem_st16(tS + 32 * hf, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+            l0 = __fadd2_rn(l0, p0);
+            l1 = __fadd2_rn(l1, p1);
+            r[c >> 1] = pack_bf16(p0.x, p0.y);
+            r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
+          }
+        };
+        exp_chunk(0);
+        if (two) {
+          exp_chunk(32);
+          tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        } else {
+          tmem_st16(tS, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
         }
-        if (DSC_PINGPONG) named_bar_arrive(tok_other, 256);
         lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
         if (warp == 0 && lane == 0) TRACE(EV_L + 4, g);
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(bar(B_P + qt));
+        mbar_arrive(bar(B_P + sb));
         if (rloc == 0) TRACE(EV_P0 + qt, g);
         if (lane == 0) TRACE(EV_PW0 + warp, g);
       }
@@ -321,23 +352,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       // item's Q tile is fetched now (overlapping this item's epilogue)
       const int nidx = idx + gridDim.x;
       Item wn;
-      if (nidx < n_items) {
-        wn = decode_item(ITEM_PARAMS(nidx), ITEM_LOCAL(nidx));
-        issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile);
-      }
-      // publish the next item's Q before this item's epilogue, so the tensor core can start
-      // the next item's first S MMAs while O is read out (the MMA waits for B_OF before it
-      // overwrites O with the next item's first PV)
+      if (nidx < n_items) wn = decode_item(ITEM_PARAMS(nidx), ITEM_LOCAL(nidx));
 #if DSC_QFIRST
       if (nidx < n_items) {
-        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile, 2 + qt);
+        if (rloc == 0) TRACE(EV_QSTART, gt);
+#if DSC_QREG
+        load_q_row_rotated(ITEM_PARAMS(nidx), wn, qt, rloc, qtile);
+        fence_proxy_async();
+#else
+        issue_q_tile(ITEM_PARAMS(nidx), wn, qt, threadIdx.x - qt * 128, qtile);
+        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, threadIdx.x - qt * 128, qtile, 2 + qt);
+#endif
+        if (rloc == 0) TRACE(EV_QLOADED, gt);
         mbar_arrive(bar(B_Q + qt));
         if (rloc == 0) TRACE(EV_QDONE, gt);
       }
 #endif
-      // epilogue of the item
+      // epilogue of the item: O / l once the last PV is done
       const float lsum = lsum2.x + lsum2.y;
-      mbar_wait(bar(B_O + qt), (gt - 1) & 1);
+      mbar_wait(bar(B_O + qt * 2 + ((gt - 1) & 1)), ((gt - 1) >> 1) & 1);
+      if (rloc == 0) TRACE(EV_EPI0, gt);
       tc_fence_after();
       const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
       const int h = valid_row ? w.g * p.grp + rglob % p.grp : 0;
@@ -374,22 +408,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (hf == 0) p.ws_lse[(long long)w.sp * rows + orow] = lsum > 0.f ? m + __log2f(lsum) : -INFINITY;
         }
       }
+      if (rloc == 0) TRACE(EV_EPI1, gt);
 #if !DSC_QFIRST
       if (nidx < n_items) {
-        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile, 2 + qt);
+        issue_q_tile(ITEM_PARAMS(nidx), wn, qt, threadIdx.x - qt * 128, qtile);
+        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, threadIdx.x - qt * 128, qtile, 2 + qt);
         mbar_arrive(bar(B_Q + qt));
         if (rloc == 0) TRACE(EV_QDONE, gt);
       }
 #endif
     }
-    if (DSC_PINGPONG && qt == 0) named_bar_sync(kBarTok0, 256);   // WG1's last token
   } else if (warp < 12) {
-    // ================================================================ rotation (Q per item, then K tiles)
+    // ================================================================ rotation (K tiles)
     if constexpr (kRegRotate > kThreadRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegRotate));
     else if constexpr (kRegRotate < kThreadRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegRotate));
     const int lt = threadIdx.x - 256;
     const int c8 = lt & 7;             // frequencies 8*c8 .. 8*c8+7
-    const int rg8 = lt >> 3;           // rows rg8*8 .. +7 of a 128-row tile
+    const int rg = lt >> 3;            // rows rg*4 .. rg*4+3 of a 64-row tile
     const float4* __restrict__ rp = p.rope_pairs;
     float2 cth[4], sth[4];             // R(theta_f) = table entry of id 1
 #pragma unroll
@@ -406,14 +441,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
       // ---- K tiles of this item; the table entry of each tile's first row is fetched
       // one tile ahead so the L2 latency is off the rotation's critical path
-      int kpos[8];
+      int kpos[4];
       float4 kpre[4];
       auto first_pos = [&](int u) {
         const TileSeg t = tile_segments(p, w, u);
         int q = -1;
 #pragma unroll
-        for (int k = 7; k >= 0; --k) {
-          const int pk = seg_pos(t, rg8 * 8 + k);
+        for (int k = 3; k >= 0; --k) {
+          const int pk = seg_pos(t, rg * 4 + k);
           if (pk >= 0) q = pk;
         }
         return q;
@@ -425,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int g = gt + jj, u = w.t_begin + jj, ks = g % KST;
         const TileSeg t = tile_segments(p, w, u);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) kpos[k] = seg_pos(t, rg8 * 8 + k);
+        for (int k = 0; k < 4; ++k) kpos[k] = seg_pos(t, rg * 4 + k);
         float4 cur[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) cur[j] = kpre[j];
@@ -437,16 +472,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(bar(B_KR + ks), (g / KST) & 1);
         if (lt == 0) TRACE(EV_KR, g);
-        if (!DSC_ABL_ROT && rg8 * 8 < t.width)   // rows >= width are never read by the MMA
-          rotate8(sbase + OFF_K + ks * kTileBytes, rg8 * 8, c8, rp, cth, sth, kpos, cur, max(cur_pos, 0));
+#ifdef DSC_DBG_ROTFULL
+        if (!DSC_ABL_ROT)
+#else
+        if (!DSC_ABL_ROT && rg * 4 < t.width)   // rows >= width are never read by the MMA
+#endif
+          rotate_rows<1, kKVHalf>(sbase + OFF_K + ks * kKVBytes, rg * 4, c8, rp, cth, sth, kpos, cur,
+                                  max(cur_pos, 0));
         fence_proxy_async();
         mbar_arrive(bar(B_KF + ks));
         if (lt == 0) TRACE(EV_KDONE, g);
         if (dbg && c8 == 0) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int r = rg8 * 8 + k;
-            const int x = 128 * u + r;
+          for (int k = 0; k < 4; ++k) {
+            const int r = rg * 4 + k;
+            const int x = kKT * u + r;
             int slot = t.slot0 + r;
             if (slot >= p.R) slot -= p.R;
             if (kpos[k] >= 0) p.dbg_pos[(u < w.n_extra) ? (x < A ? x : A + p.R + (x - A)) : A + slot] = kpos[k];
@@ -475,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int jj = 0; jj < w.n_tiles; ++jj) {
           const int g = gt + jj, u = w.t_begin + jj, st = g % nst;
           if (g >= nst) mbar_wait(bar(b_free + st), ((g - nst) / nst) & 1);
-          const uint32_t dst = sbase + off + st * kTileBytes;
+          const uint32_t dst = sbase + off + st * kKVBytes;
           const TileSeg t = tile_segments(p, w, u);
           if (u < w.n_extra) {
             // sink rows (x < A) + self rows (A <= x < A + n_self), zeros up to the tile
@@ -483,13 +523,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int nit = t.width >> 1;
 #pragma unroll 1
             for (int it = 0; it < nit; ++it) {
-              const int id = it * 32 + lane;          // 2048 16-byte chunks
+              const int id = it * 32 + lane;          // 16-byte chunks
               const int r = id >> 4, ch = id & 15;
-              const int x = 128 * u + r;
+              const int x = kKT * u + r;
               const __nv_bfloat16* src = nullptr;
               if (x < A) src = SX + (w.head_row * A + x) * 128;
               else if (x < A + p.n_self) src = XX + (((long long)w.pp * p.n_self + (x - A)) * p.Hkv + w.g) * 128;
-              const uint32_t d = dst + (ch >> 3) * 16384 + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
+              const uint32_t d = dst + (ch >> 3) * kKVHalf + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
               cp_async16(d, src ? (const void*)(src + 8 * ch) : (const void*)SX, src ? 16u : 0u);
             }
             cp_async_wait_all();
@@ -498,94 +538,109 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) mbar_arrive(bar(b_full + st));
           } else if (lane == 0) {
             const int row = (int)(w.head_row * p.Rp) + t.slot0;   // logical window tile (mirror: no wrap)
-            mbar_arrive_tx(bar(b_full + st), kTileBytes);
+            mbar_arrive_tx(bar(b_full + st), kKVBytes);
             tma_load_2d(dst, tmap, 0, row, bar(b_full + st));
-            tma_load_2d(dst + 16384, tmap, 64, row, bar(b_full + st));
+            tma_load_2d(dst + kKVHalf, tmap, 64, row, bar(b_full + st));
           }
           if (lane == 0) TRACE(isk ? EV_K_ISSUE : EV_V_ISSUE, g);
           __syncwarp();
         }
         gt += w.n_tiles;
       }
-    } else if (warp == 14) {
-      // ============================================================== MMA issuer (whole warp, elected lane issues)
+    } else {
+      // ============================================================== MMA issuers: warp 14 for Q tile 0,
+      // warp 15 for Q tile 1 (whole warp runs the loop, an elected lane issues); two issuers
+      // halve the per-warp tcgen05 issue work, which otherwise bounds the tile rate
+      // DSC_MMA2 = 0: warp 14 issues for both Q tiles (warp 15 idles)
+      const int q_lo = DSC_MMA2 ? warp - 14 : 0, q_hi = DSC_MMA2 ? warp - 13 : 2;
+      if (!DSC_MMA2 && warp == 15) goto mma_done;
+      {
       constexpr uint32_t IQK0 = idesc_bf16(128, 0, 0, 0);    // S = Q K^T, both K-major; N = tile width
       constexpr uint32_t IPV = idesc_bf16(128, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
-      // descriptors advance in the 14-bit start-address field: +32 B (2) per 16-element
-      // K step inside a 128 B swizzle row, +16 KB (1024) to the second 64-column block
       // fully unrolled: the descriptors are formed once per call and advanced by
-      // immediates, so each tcgen05.mma costs a handful of uniform-datapath instructions
-      // (a rolled loop re-materialised them per MMA and capped the issue rate well below
-      // the tensor pipe's 64 cycles per M128 N128 K16 MMA)
-      auto issue_qk = [&](int qt, int ks, int nu) {
-        const uint64_t da = sdesc(sbase + OFF_Q + qt * kTileBytes, 16, 1024);
-        const uint64_t db = sdesc(sbase + OFF_K + ks * kTileBytes, 16, 1024);
+      // immediates (16-element K steps: +32 B inside a 128 B swizzle row, then the next
+      // 64-column block), so each tcgen05.mma costs a few uniform-datapath instructions
+      auto issue_qk = [&](int qt, int ks, int nu, int buf) {
+        const uint64_t da = sdesc(sbase + OFF_Q + qt * kQBytes, 16, 1024);
+        const uint64_t db = sdesc(sbase + OFF_K + ks * kKVBytes, 16, 1024);
+#ifdef DSC_DBG_QKFULL
+        const uint32_t iqk = IQK0 | ((uint32_t)(64 >> 3) << 17);
+#else
         const uint32_t iqk = IQK0 | ((uint32_t)(nu >> 3) << 17);
-        const uint32_t d = tmem + qt * 128;
+#endif
+        const uint32_t d = tmem + qt * 128 + buf * 64;
+        static_assert(kQBytes / 2 / 16 == 1024 && kKVHalf / 16 == 512, "mma_qk8_w block offsets");
+        mma_qk8_w(d, da, db, iqk);
+      };
+      // K of the PV product = tile width (keys), 16 per MMA; V rows advance 16 x 128 B
+      auto issue_pv = [&](int qt, int vs, bool acc, int nu, int buf) {
+        const uint64_t dv = sdesc(sbase + OFF_V + vs * kKVBytes, kKVHalf, 1024);
+        const uint32_t d = tmem + 256 + qt * 128, a = tmem + qt * 128 + buf * 64;
+#ifdef DSC_DBG_PVFULL
+        const int nk = 4;
+#else
+        const int nk = nu >> 4;
+#endif
+        if (nk == 4) {
+          mma_pv4_w(d, a, dv, IPV, acc ? 1u : 0u);
+        } else {
+          mma_ts_w(d, a, dv, IPV, acc ? 1u : 0u);
 #pragma unroll
-        for (int k8 = 0; k8 < 8; ++k8) {
-          const uint64_t off = (uint64_t)((k8 >> 2) * 1024 + (k8 & 3) * 2);
-          mma_ss_w(d, da + off, db + off, iqk, k8 > 0);
+          for (int k8 = 1; k8 < kKT / 16; ++k8)
+            if (k8 < nk) mma_ts_w(d, a + k8 * 8, dv + (uint64_t)(k8 * 128), IPV, 1u);
         }
       };
-      // K of the PV product = tile width (keys), 16 per MMA
-      auto issue_pv = [&](int qt, int vs, bool acc, int nu) {
-        const uint64_t dv = sdesc(sbase + OFF_V + vs * kTileBytes, 16384, 1024);
-        const uint32_t d = tmem + 256 + qt * 128, a = tmem + qt * 128;
-        const int nk = nu >> 4;
-        mma_ts_w(d, a, dv, IPV, acc ? 1u : 0u);
-#pragma unroll
-        for (int k8 = 1; k8 < 8; ++k8)
-          if (k8 < nk) mma_ts_w(d, a + k8 * 8, dv + (uint64_t)(k8 * 128), IPV, 1u);
+      // S of tile g for Q tile qt into buffer g & 1; K stage g % KST is free when both MMA
+      // warps' QK^T of the tile are done (K-free barrier counts 2 commits)
+      auto issue_s = [&](const AttnParams& p, const Item& w, int g, int u) {
+        const int ks = g % KST, buf = g & 1;
+        const int nu = tile_segments(p, w, u).width;
+        mbar_wait(bar(B_KF + ks), (g / KST) & 1);
+        if (lane == 0 && q_lo == 0) TRACE(EV_KF, g);
+        tc_fence_after();
+#pragma unroll 1
+        for (int qt = q_lo; qt < q_hi; ++qt) {
+          issue_qk(qt, ks, nu, buf);
+          mma_commit_w(bar(B_S + qt * 2 + buf));
+        }
+        mma_commit_w(bar(B_KE + ks));
+        if (lane == 0 && q_lo == 0) TRACE(EV_QKI, g);
       };
       int gt = 0, kk = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
         const AttnParams& p = ITEM_PARAMS(idx);
         const Item w = decode_item(p, ITEM_LOCAL(idx));
         const int n = w.n_tiles;
-        mbar_wait(bar(B_KF + gt % KST), (gt / KST) & 1);
-        if (lane == 0) TRACE(EV_KF, gt);
-        mbar_wait(bar(B_Q + 0), kk & 1);
-        if (kk == 0 && lane == 0) TRACE(EV_Q, 0);
-        tc_fence_after();
-        int nu = tile_segments(p, w, w.t_begin).width;
-        issue_qk(0, gt % KST, nu); mma_commit_w(bar(B_S + 0));
-        mbar_wait(bar(B_Q + 1), kk & 1);
-        tc_fence_after();
-        issue_qk(1, gt % KST, nu); mma_commit_w(bar(B_S + 1));
-        mma_commit_w(bar(B_KE + gt % KST));
+        for (int qt = q_lo; qt < q_hi; ++qt) mbar_wait(bar(B_Q + qt), kk & 1);
+        if (kk == 0 && lane == 0 && q_lo == 0) TRACE(EV_Q, 0);
+        if (n > 0) issue_s(p, w, gt, w.t_begin);
+        if (n > 1) issue_s(p, w, gt + 1, w.t_begin + 1);
         for (int jj = 0; jj < n; ++jj) {
-          const int g = gt + jj, vs = g % VST;
-          const int nu_next = jj + 1 < n ? tile_segments(p, w, w.t_begin + jj + 1).width : 0;
+          const int g = gt + jj, vs = g % VST, buf = g & 1;
+          const int nu = tile_segments(p, w, w.t_begin + jj).width;
           mbar_wait(bar(B_VF + vs), (g / VST) & 1);
-          if (lane == 0) TRACE(EV_VF, g);
-          for (int qt = 0; qt < 2; ++qt) {
-            mbar_wait(bar(B_P + qt), g & 1);
+          if (lane == 0 && q_lo == 0) TRACE(EV_VF, g);
+#pragma unroll 1
+          for (int qt = q_lo; qt < q_hi; ++qt) {
+            mbar_wait(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
             if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
             if (lane == 0) TRACE(EV_PV0 + qt, g);
             tc_fence_after();
-            issue_pv(qt, vs, jj > 0, nu);
-            mma_commit_w(bar(B_O + qt));
-            if (qt == 1) mma_commit_w(bar(B_VE + vs));
-            if (jj + 1 < n) {
-              const int ks = (g + 1) % KST;
-              if (qt == 0) {
-                mbar_wait(bar(B_KF + ks), ((g + 1) / KST) & 1);
-                if (lane == 0) TRACE(EV_KF, g + 1);
-                tc_fence_after();
-              }
-              issue_qk(qt, ks, nu_next);
-              mma_commit_w(bar(B_S + qt));
-              if (qt == 1) mma_commit_w(bar(B_KE + ks));
-            }
+            issue_pv(qt, vs, jj > 0, nu, buf);
+            mma_commit_w(bar(B_O + qt * 2 + buf));
+            if (lane == 0) TRACE(EV_PVI + qt, g);
           }
-          nu = nu_next;
+          mma_commit_w(bar(B_VE + vs));
+          // S(g+2) reuses buffer g & 1: issued after PV(g) has consumed P(g)
+          if (jj + 2 < n) issue_s(p, w, g + 2, w.t_begin + jj + 2);
         }
         gt += n;
       }
       // drain: the last V-free commit tracks every MMA of this CTA
       if (gt > 0) mbar_wait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1);
       if (lane == 0) TRACE(EV_END, 0);
+      }
+    mma_done:;
     }
   }
 
@@ -615,7 +670,7 @@ cudaError_t make_ring_tmap(CUtensorMap* map, void* base, unsigned long long rows
   }
   const cuuint64_t dims[2] = {128, rows};   // rows = heads * (R + 128): ring + mirror
   const cuuint64_t strides[1] = {128 * 2};
-  const cuuint32_t box[2] = {64, 128};
+  const cuuint32_t box[2] = {64, (cuuint32_t)kTileN};   // 64 columns x one key tile
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -7,10 +7,10 @@
 
 namespace dsc {
 
-constexpr int kTileN = 128;   // keys per attention tile (tcgen05 N of QK^T, K of PV)
+constexpr int kTileN = 64;    // keys per attention tile (tcgen05 N of QK^T, K of PV)
 constexpr int kTileM = 128;   // query rows per Q tile (tcgen05 M)
 constexpr int kMirror = 128;  // ring rows after slot R-1 mirroring slots [0, 128): a 128-row tile never wraps
-constexpr int kTraceEvents = 32, kTraceTiles = 64;
+constexpr int kTraceEvents = 40, kTraceTiles = 64;
 
 // One attention launch (build_instant or attend) over P = S * layer_count problems.
 // Keys of problem p, kv head g, in logical order L = 0, 1, ...:

@@ -94,6 +94,46 @@ __device__ __forceinline__ void mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint6
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// Batched warp-converged issue: ONE elect for a whole K sweep (the per-MMA elect of
+// mma_ss_w costs a WARPSYNC/ELECT sequence and operand moves per instruction, which
+// capped the issue rate of the single MMA warp below the tensor pipe's).
+// S = Q K^T over K = 128 (8 x K16): A (Q, 128 rows) and B (K tile, 64 rows) SW128
+// K-major; the second 64-column block of A is +16 KB (1024 in 16-B units), of B +8 KB (512).
+__device__ __forceinline__ void mma_qk8_w(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred e;\n.reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n"
+      "add.s64 a1, %1, 2; add.s64 a2, %1, 4; add.s64 a3, %1, 6;\n"
+      "add.s64 a4, %1, 1024; add.s64 a5, %1, 1026; add.s64 a6, %1, 1028; add.s64 a7, %1, 1030;\n"
+      "add.s64 b1, %2, 2; add.s64 b2, %2, 4; add.s64 b3, %2, 6;\n"
+      "add.s64 b4, %2, 512; add.s64 b5, %2, 514; add.s64 b6, %2, 516; add.s64 b7, %2, 518;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, 1;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc)
+      : "memory");
+}
+// O += P V over one 64-key tile (4 x K16): A (P) in TMEM, 8 columns per K16 step; B (V)
+// MN-major SW128, 16 keys = 2048 B (128 in 16-B units) per step.  acc = 0 overwrites O.
+__device__ __forceinline__ void mma_pv4_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred e, p;\n.reg .b64 b1, b2, b3;\n.reg .b32 t1, t2, t3;\n"
+      "add.s64 b1, %2, 128; add.s64 b2, %2, 256; add.s64 b3, %2, 384;\n"
+      "add.u32 t1, %1, 8; add.u32 t2, %1, 16; add.u32 t3, %1, 24;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t1], b1, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t2], b2, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t3], b3, %3, 1;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit_w(uint32_t bar) {
   asm volatile(
       "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
@@ -219,7 +259,9 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
 // timeline events (TRACE): clock64 per (event, tile) for the first ntrace_cta CTAs
 enum { EV_K_ISSUE = 0, EV_V_ISSUE, EV_KR, EV_KF, EV_S0, EV_S1, EV_P0, EV_P1, EV_PV0, EV_PV1, EV_Q, EV_START, EV_END,
        EV_VF, EV_PW0 /* 14..21: P arrival of softmax warps 0..7 */, EV_L = 22 /* 22..27: warp-0 softmax steps */,
-       EV_KDONE = 28, EV_QDONE = 29, EV_QLOADED = 30, EV_QSTART = 31 };
+       EV_KDONE = 28, EV_QDONE = 29, EV_QLOADED = 30, EV_QSTART = 31,
+       EV_QKI = 32 /* MMA warp: S(g) issued */, EV_PVI = 33 /* PV0(g) issued */, EV_PV1I = 34 /* PV1(g) issued */,
+       EV_EPI0 = 35 /* epilogue: last PV done */, EV_EPI1 = 36 /* epilogue stores issued */ };
 #define TRACE(ev, tile)                                                                                  \
   do {                                                                                                   \
     if (p.trace && blockIdx.x < (unsigned)p.ntrace_cta && (tile) < kTraceTiles)                          \
@@ -262,20 +304,20 @@ __device__ __forceinline__ Item decode_item(const AttnParams& p, int idx) {
   const int last_row = min(w.m0 + kMBlockRows, w.rows_total) - 1;
   const int lim_max = p.q_pos0 + last_row / p.grp;
   w.cnt = min(max(lim_max - p.A + 1, 0), p.ring_count);
-  w.n_extra = (p.A + p.n_self + 127) / 128;
-  const int total = w.n_extra + (w.cnt + 127) / 128;
+  w.n_extra = (p.A + p.n_self + kTileN - 1) / kTileN;
+  const int total = w.n_extra + (w.cnt + kTileN - 1) / kTileN;
   w.t_begin = min(w.sp * p.tiles_per_split, total);
   w.n_tiles = min(total, w.t_begin + p.tiles_per_split) - w.t_begin;
   return w;
 }
 
-// Key rows of tile u as (at most) two segments; key row r of segment s has id
-// pos0_s + r.  Tiles u < n_extra hold the sink rows (extra index x = 128u + r < A, id x)
-// and then the self rows (A <= x < A + n_self, id ring_count + x).  Tile u >= n_extra is
-// the LOGICAL window tile b = u - n_extra: window keys [128b, 128b + 128), i.e. the ring
-// slots (ring_start + 128b + r) mod R, read as one 128-row box from slot0 = (ring_start +
-// 128b) mod R -- the ring keeps a mirror of slots [0, 128) after slot R - 1, so the box
-// never wraps.  Row r is valid iff 128b + r < cnt, with id A + 128b + r.
+// Key rows of tile u (kTileN = 64 keys) as (at most) two segments; key row r of segment s
+// has id pos0_s + r.  Tiles u < n_extra hold the sink rows (extra index x = 64u + r < A,
+// id x) and then the self rows (A <= x < A + n_self, id ring_count + x).  Tile u >= n_extra
+// is the LOGICAL window tile b = u - n_extra: window keys [64b, 64b + 64), i.e. the ring
+// slots (ring_start + 64b + r) mod R, read as one 64-row box from slot0 = (ring_start +
+// 64b) mod R -- the ring keeps a mirror of slots [0, kMirror) after slot R - 1, so the box
+// never wraps.  Row r is valid iff 64b + r < cnt, with id A + 64b + r.
 // `width` = valid rows rounded up to 16: the N of the QK^T MMA and the K of the PV MMA.
 struct TileSeg {
   int lo0, hi0, pos0_0;
@@ -288,21 +330,25 @@ __device__ __forceinline__ TileSeg tile_segments(const AttnParams& p, const Item
   TileSeg t;
   int valid;
   if (u < w.n_extra) {
-    const int x0 = 128 * u;
-    t.lo0 = 0; t.hi0 = min(max(p.A - x0, 0), 128); t.pos0_0 = x0;
-    t.lo1 = t.hi0; t.hi1 = min(max(p.A + p.n_self - x0, 0), 128); t.pos0_1 = p.ring_count + x0;
+    const int x0 = kTileN * u;
+    t.lo0 = 0; t.hi0 = min(max(p.A - x0, 0), kTileN); t.pos0_0 = x0;
+    t.lo1 = t.hi0; t.hi1 = min(max(p.A + p.n_self - x0, 0), kTileN); t.pos0_1 = p.ring_count + x0;
     t.slot0 = -1;
     valid = t.hi1;
   } else {
-    const int base = 128 * (u - w.n_extra);
-    valid = min(w.cnt - base, 128);
+    const int base = kTileN * (u - w.n_extra);
+    valid = min(w.cnt - base, kTileN);
     t.lo0 = 0; t.hi0 = valid; t.pos0_0 = p.A + base;
     t.lo1 = 0; t.hi1 = 0; t.pos0_1 = 0;
     int s0 = p.ring_start + base;
     if (s0 >= p.R) s0 -= p.R;
     t.slot0 = s0;
   }
+#ifdef DSC_FULLW
+  t.width = kTileN;
+#else
   t.width = (valid + 15) & ~15;
+#endif
   return t;
 }
 __device__ __forceinline__ int seg_pos(const TileSeg& t, int r) {
@@ -448,6 +494,52 @@ __device__ __forceinline__ void rotate_q_tile(const AttnParams& p, const Item& w
   fence_proxy_async();
 }
 
+// Q row rloc of Q tile qt of an item, rotated at its query id in registers and stored to the
+// SW128 smem tile (one thread per row: split-half pairs (f, f+64) live in the same thread).
+// Replaces the cp.async + in-smem rotation at item switches (no named barrier, one pass).
+// The caller fences (proxy.async) and arrives on the Q barrier.
+__device__ __forceinline__ void load_q_row_rotated(const AttnParams& p, const Item& w, int qt, int rloc,
+                                                   uint32_t qtile) {
+  const int rglob = w.m0 + qt * 128 + rloc;
+  const bool ok = rglob < w.rows_total;
+  const int qi = ok ? rglob / p.grp : 0, hh = ok ? rglob % p.grp : 0;
+  const int pos = p.q_pos0 + qi;
+  const uint4* __restrict__ src = reinterpret_cast<const uint4*>(
+      reinterpret_cast<const __nv_bfloat16*>(p.q) + (((long long)w.pp * p.n_q + qi) * p.Hq + w.g * p.grp + hh) * 128);
+  const float4* __restrict__ tab = p.rope_pairs + (long long)pos * 32;
+  if (ok && p.dbg_pos != nullptr && w.pp == 0 && w.g == 0 && hh == 0) p.dbg_pos[p.A + p.R + p.dbg_M + qi] = pos;
+  const uint32_t rowb = qtile + (uint32_t)rloc * 128;
+#pragma unroll
+  for (int c = 0; c < 8; c += 2) {          // 16-byte chunks c, c+1 (cols 8c..) and their partners c+8, c+9
+    uint4 lo[2], hi[2];
+    float4 t[8];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      lo[k] = ok ? src[c + k] : make_uint4(0, 0, 0, 0);
+      hi[k] = ok ? src[c + k + 8] : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = tab[4 * c + j];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      uint32_t ol[4], oh[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 tt = t[4 * k + j];
+        const float2 cs = make_float2(tt.x, tt.y), sn = make_float2(tt.z, tt.w);
+        const float2 av = bf2(get_w(lo[k], j)), bv = bf2(get_w(hi[k], j));
+        const float2 yl = __ffma2_rn(av, cs, __fmul2_rn(make_float2(-bv.x, -bv.y), sn));   // a cos - b sin
+        const float2 yh = __ffma2_rn(av, sn, __fmul2_rn(bv, cs));                        // a sin + b cos
+        ol[j] = pack_bf16(yl.x, yl.y);
+        oh[j] = pack_bf16(yh.x, yh.y);
+      }
+      const int ch = c + k;
+      const uint32_t sw = (uint32_t)(((ch ^ (rloc & 7)) & 7) << 4);
+      sts128(rowb + sw, make_uint4(ol[0], ol[1], ol[2], ol[3]));
+      sts128(rowb + 16384 + sw, make_uint4(oh[0], oh[1], oh[2], oh[3]));
+    }
+  }
+}
 
 }  // namespace tcc
 }  // namespace dsc

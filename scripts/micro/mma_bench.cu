@@ -50,6 +50,9 @@ __global__ void __launch_bounds__(512, 1) k(long long* cyc, int rounds) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t barx[6];
+  uint32_t bar_b[6];
+  for (int i = 0; i < 6; ++i) bar_b[i] = (uint32_t)__cvta_generic_to_shared(&barx[i]);
   const int warp = threadIdx.x >> 5;
   const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(sm) + 1023) & ~1023u;
   const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
@@ -59,6 +62,7 @@ __global__ void __launch_bounds__(512, 1) k(long long* cyc, int rounds) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
+  if (threadIdx.x == 0) for (int i = 0; i < 6; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_b[i]));
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -99,6 +103,32 @@ __global__ void __launch_bounds__(512, 1) k(long long* cyc, int rounds) {
         if (MODE == 1) mma_ts(tmem + 256, tmem + k8 * 8, db + off, idesc_bf16(128, 128, 0, 0), k8 > 0);
         if (MODE == 2) mma_ss(tmem, da + off, db + off, idesc_bf16(128, 256, 0, 0), k8 > 0);
         if (MODE == 3) mma_ss(tmem + (r & 3) * 128, da + off, db + off, idesc_bf16(128, 128, 0, 0), k8 > 0);
+        if (MODE == 5) mma_ss(tmem, da + off, db + off, idesc_bf16(128, 64, 0, 0), k8 > 0);
+        if (MODE == 6) mma_ss(tmem, da + off, db + off, idesc_bf16(128, 16, 0, 0), k8 > 0);
+        if (MODE == 7) mma_ss(tmem, da + off, db + off, idesc_bf16(128, 256, 0, 0), k8 > 0);
+        if (MODE == 8) {   // one 64-key tile of the v5 attention: QK0 QK1 (SS N64) + PV0 PV1 (TS K=64 -> 4 MMAs each)
+          const uint64_t offb = (uint64_t)((k8 >> 2) * 512 + (k8 & 3) * 2);
+          mma_ss(tmem + (r & 1) * 64, da + off, db + offb, idesc_bf16(128, 64, 0, 0), k8 > 0);
+          mma_ss(tmem + 128 + (r & 1) * 64, da + off, db + offb, idesc_bf16(128, 64, 0, 0), k8 > 0);
+          if (k8 < 4) {
+            mma_ts(tmem + 256, tmem + (r & 1) * 64 + k8 * 8, db + (uint64_t)(k8 * 128), idesc_bf16(128, 128, 0, 1), 1);
+            mma_ts(tmem + 384, tmem + 128 + (r & 1) * 64 + k8 * 8, db + (uint64_t)(k8 * 128), idesc_bf16(128, 128, 0, 1), 1);
+          }
+        }
+        if (MODE == 9 || MODE == 10) {   // v5 tile with the kernel's commits (MODE 10: 1 commit per tile)
+          const uint64_t offb = (uint64_t)((k8 >> 2) * 512 + (k8 & 3) * 2);
+          mma_ss(tmem + (r & 1) * 64, da + off, db + offb, idesc_bf16(128, 64, 0, 0), k8 > 0);
+          if (MODE == 9 && k8 == 7) commit(bar_b[0]);
+          mma_ss(tmem + 128 + (r & 1) * 64, da + off, db + offb, idesc_bf16(128, 64, 0, 0), k8 > 0);
+          if (MODE == 9 && k8 == 7) { commit(bar_b[1]); commit(bar_b[2]); }
+          if (k8 < 4) {
+            mma_ts(tmem + 256, tmem + (r & 1) * 64 + k8 * 8, db + (uint64_t)(k8 * 128), idesc_bf16(128, 128, 0, 1), 1);
+            if (MODE == 9 && k8 == 3) commit(bar_b[3]);
+            mma_ts(tmem + 384, tmem + 128 + (r & 1) * 64 + k8 * 8, db + (uint64_t)(k8 * 128), idesc_bf16(128, 128, 0, 1), 1);
+            if (MODE == 9 && k8 == 3) { commit(bar_b[4]); commit(bar_b[5]); }
+          }
+          if (MODE == 10 && k8 == 7) commit(bar_b[0]);
+        }
         if (MODE == 4) {
           if (r & 1) mma_ts(tmem + 256 + (r & 2) * 64, tmem + (r & 2) * 64 + k8 * 8, db + (uint64_t)(k8 * 128),
                             idesc_bf16(128, 128, 0, 1), 1);
@@ -136,6 +166,13 @@ int main() {
   run<0, 2>("SS M128 N128 K16", c, smem); run<0, 3>("SS M128 N128 K16", c, smem);
   run<1, 0>("TS M128 N128 K16", c, smem); run<1, 1>("TS M128 N128 K16", c, smem);
   run<1, 2>("TS M128 N128 K16", c, smem); run<1, 3>("TS M128 N128 K16", c, smem);
+  run<5, 0>("SS M128 N64 K16 (flop as N128)", c, smem);
+  run<6, 0>("SS M128 N16 K16 (flop as N128)", c, smem);
+
+  run<8, 0>("v5 tile (per 3 MMAs)", c, smem);
+  run<8, 1>("v5 tile (per 3 MMAs)", c, smem);
+  run<9, 0>("v5 tile + 6 commits", c, smem);
+  run<10, 0>("v5 tile + 1 commit", c, smem);
   run<4, 0>("QK+PV mix", c, smem); run<4, 1>("QK+PV mix", c, smem);
   run<4, 2>("QK+PV mix", c, smem); run<4, 3>("QK+PV mix", c, smem);
   return 0;

@@ -14,8 +14,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import dscache_synth as synth  # noqa: E402
 from paper_2605_01858_b200 import dscache as D  # noqa: E402
 
-EV = ["K_issue", "V_issue", "KR", "KF(mma)", "S0", "S1", "P0", "P1", "PV0", "PV1", "Q", "start", "end", "VF(mma)"] + [f"Pw{i}" for i in range(8)] + ["max_h0", "max_h1", "exp_h0", "exp_h1", "packed", "resc", "Kdone", "Qdone", "Qloaded", "Qstart"]
-NE = 32
+EV = ["K_issue", "V_issue", "KR", "KF(mma)", "S0", "S1", "P0", "P1", "PV0", "PV1", "Q", "start", "end", "VF(mma)"] + [f"Pw{i}" for i in range(8)] + ["max_h0", "max_h1", "exp_h0", "exp_h1", "packed", "resc", "Kdone", "Qdone", "Qloaded", "Qstart", "QKiss", "PV0iss", "PV1iss", "epi0", "epi1"]
+NE = 40
 
 
 def main():
@@ -54,7 +54,7 @@ def main():
             end = int(tr[c, 12, 0]) - t0
             ntiles = int((tr[c, 8] != 0).sum())
             print(f"== {name} CTA {c}: tiles {ntiles}, total {end} cycles, Q ready at {int(tr[c, 10, 0]) - t0}")
-            cols = [0, 1, 2, 28, 3, 13, 4, 6, 8, 5, 7, 9] + [22, 23, 27, 24, 25, 26]
+            cols = [0, 1, 2, 28, 3, 32, 13, 4, 6, 8, 33, 5, 7, 9, 34] + [22, 26]
             print("tile " + " ".join(f"{EV[e]:>8}" for e in cols))
             # steady-state summary over tiles 2..ntiles-2 (cycles): tile period at the S0 wait,
             # softmax time per Q tile (S ready -> P arrived), P -> next S latency (PV + QK MMAs)
@@ -81,6 +81,16 @@ def main():
             print(f"   summary: median tile period {med(per)}, softmax0 {med(sm0)}, softmax1 {med(sm1)}, "
                   f"P0->S0next {med(lat0)}, K rotate {med(rot)}, K issue->landed {med(klat)}, "
                   f"V issue->MMA {med(vlat)}")
+            # item switches of softmax WG0 (indexed by the next item's first tile)
+            sw = []
+            for j in range(1, 64):
+                qs, ql, qd, e0, e1 = (ev(31, j), ev(30, j), ev(29, j), ev(35, j), ev(36, j))
+                if qs is not None and e1 is not None:
+                    sw.append((j, qs, ql - qs if ql else -1, qd - ql if (qd and ql) else -1, e0 - qd if (e0 and qd) else -1,
+                               e1 - e0 if (e1 and e0) else -1))
+            for t in sw[:6]:
+                print(f"   switch @tile {t[0]}: start {t[1]}, Q cp.async issue {t[2]}, Q wait+rotate {t[3]}, "
+                      f"wait last PV {t[4]}, O read+store {t[5]}")
             for j in range(min(ntiles, 64)):
                 row = [int(tr[c, e, j]) - t0 if int(tr[c, e, j]) else -1 for e in cols]
                 print(f"{j:4d} " + " ".join(f"{x:8d}" for x in row))

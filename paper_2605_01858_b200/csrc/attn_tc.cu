@@ -49,8 +49,14 @@ constexpr int kQBytes = 128 * 128 * 2;        // one 128-row Q tile (2 x 64-colu
 constexpr int kKT = kTileN;                   // keys per K/V tile
 constexpr int kKVHalf = kKT * 128;            // bytes of one 64-column SW128 block of a K/V tile
 constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
-constexpr int KST = 5;                        // K stages (raw -> rotated in place)
-constexpr int VST = 5;                        // V stages
+#ifndef DSC_KST
+#define DSC_KST 6
+#endif
+#ifndef DSC_VST
+#define DSC_VST 4
+#endif
+constexpr int KST = DSC_KST;                  // K stages (raw -> rotated in place)
+constexpr int VST = DSC_VST;                  // V stages
 constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + kNQT * kQBytes;
 constexpr int OFF_V = OFF_K + KST * kKVBytes;
@@ -121,6 +127,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ AttnParams pa, const __grid_constant__ AttnParams pb, int na, int nb, int ka,
                    int kb) {
   const AttnParams& p = pa;   // launch-wide fields (rope table, tensor maps, trace) are shared
+#if DSC_TRACE
+  long long* const trace_cta =
+      (pa.trace && blockIdx.x < (unsigned)pa.ntrace_cta) ? pa.trace + (long long)blockIdx.x * kTraceEvents * kTraceTiles
+                                                         : nullptr;
+#endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = su32(smem);
@@ -202,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
       const AttnParams& p = ITEM_PARAMS(idx);
       const Item w = decode_item(p, ITEM_LOCAL(idx));
-      const int A = p.A;
+      const int A = w.A;
       const int n = w.n_tiles;
       const int rglob = w.m0 + qt * 128 + rloc;
       const bool valid_row = rglob < w.rows_total;
@@ -237,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           c_lo = 0; c_hi = 0;
         } else if (u < w.n_extra) {                // sink always visible, self row j iff its id <= lim
           c_lo = 0;
-          c_hi = min(max(min(A + p.n_self, max(A, lim - p.ring_count + 1)) - kKT * u, 0), kKT);
+          c_hi = min(max(min(A + w.n_self, max(A, lim - w.ring_count + 1)) - kKT * u, 0), kKT);
         } else {
           c_lo = t.lo0;
           c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));   // id pos0 + c <= lim
@@ -528,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int x = kKT * u + r;
               const __nv_bfloat16* src = nullptr;
               if (x < A) src = SX + (w.head_row * A + x) * 128;
-              else if (x < A + p.n_self) src = XX + (((long long)w.pp * p.n_self + (x - A)) * p.Hkv + w.g) * 128;
+              else if (x < A + w.n_self) src = XX + (((long long)w.pp * w.n_self + (x - A)) * p.Hkv + w.g) * 128;
               const uint32_t d = dst + (ch >> 3) * kKVHalf + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
               cp_async16(d, src ? (const void*)(src + 8 * ch) : (const void*)SX, src ? 16u : 0u);
             }
@@ -537,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(b_full + st));
           } else if (lane == 0) {
-            const int row = (int)(w.head_row * p.Rp) + t.slot0;   // logical window tile (mirror: no wrap)
+            const int row = (int)(w.head_row * (w.R + kMirror)) + t.slot0;   // logical window tile (mirror: no wrap)
             mbar_arrive_tx(bar(b_full + st), kKVBytes);
             tma_load_2d(dst, tmap, 0, row, bar(b_full + st));
             tma_load_2d(dst + kKVHalf, tmap, 64, row, bar(b_full + st));

@@ -262,11 +262,20 @@ enum { EV_K_ISSUE = 0, EV_V_ISSUE, EV_KR, EV_KF, EV_S0, EV_S1, EV_P0, EV_P1, EV_
        EV_KDONE = 28, EV_QDONE = 29, EV_QLOADED = 30, EV_QSTART = 31,
        EV_QKI = 32 /* MMA warp: S(g) issued */, EV_PVI = 33 /* PV0(g) issued */, EV_PV1I = 34 /* PV1(g) issued */,
        EV_EPI0 = 35 /* epilogue: last PV done */, EV_EPI1 = 36 /* epilogue stores issued */ };
+// `trace_cta` = the launch-wide trace row of this CTA (nullptr = off), hoisted at kernel start.
+// Compiled in only with -DDSC_TRACE=1 (the profiling variant built by scripts/trace_attn.py):
+// even disabled, the checks cost registers and a reload per event in the softmax loop.
+#ifndef DSC_TRACE
+#define DSC_TRACE 0
+#endif
+#if DSC_TRACE
 #define TRACE(ev, tile)                                                                                  \
   do {                                                                                                   \
-    if (p.trace && blockIdx.x < (unsigned)p.ntrace_cta && (tile) < kTraceTiles)                          \
-      p.trace[((long long)blockIdx.x * kTraceEvents + (ev)) * kTraceTiles + (tile)] = clock64();          \
+    if (trace_cta && (tile) < kTraceTiles) trace_cta[(ev) * kTraceTiles + (tile)] = clock64();           \
   } while (0)
+#else
+#define TRACE(ev, tile) do { } while (0)
+#endif
 
 #ifndef DSC_ORDER
 #define DSC_ORDER 1
@@ -278,6 +287,9 @@ struct Item {
   int cnt;            // window keys needed by this m-block (causal cut)
   int n_extra;        // leading tiles holding sink + self rows (0 when A + n_self = 0)
   int t_begin, n_tiles;
+  // per-launch geometry copied to registers once per item: the tile map below reads no
+  // kernel parameters (parameters of a pa/pb-selected launch are indexed constant loads)
+  int A, n_self, ring_count, ring_start, R;
 };
 
 // work item idx -> split fastest, then (DSC_ORDER 1, default) problem x kv head, then
@@ -304,6 +316,7 @@ __device__ __forceinline__ Item decode_item(const AttnParams& p, int idx) {
   const int last_row = min(w.m0 + kMBlockRows, w.rows_total) - 1;
   const int lim_max = p.q_pos0 + last_row / p.grp;
   w.cnt = min(max(lim_max - p.A + 1, 0), p.ring_count);
+  w.A = p.A; w.n_self = p.n_self; w.ring_count = p.ring_count; w.ring_start = p.ring_start; w.R = p.R;
   w.n_extra = (p.A + p.n_self + kTileN - 1) / kTileN;
   const int total = w.n_extra + (w.cnt + kTileN - 1) / kTileN;
   w.t_begin = min(w.sp * p.tiles_per_split, total);
@@ -326,22 +339,22 @@ struct TileSeg {
   int width;
 };
 
-__device__ __forceinline__ TileSeg tile_segments(const AttnParams& p, const Item& w, int u) {
+__device__ __forceinline__ TileSeg tile_segments(const AttnParams&, const Item& w, int u) {
   TileSeg t;
   int valid;
   if (u < w.n_extra) {
     const int x0 = kTileN * u;
-    t.lo0 = 0; t.hi0 = min(max(p.A - x0, 0), kTileN); t.pos0_0 = x0;
-    t.lo1 = t.hi0; t.hi1 = min(max(p.A + p.n_self - x0, 0), kTileN); t.pos0_1 = p.ring_count + x0;
+    t.lo0 = 0; t.hi0 = min(max(w.A - x0, 0), kTileN); t.pos0_0 = x0;
+    t.lo1 = t.hi0; t.hi1 = min(max(w.A + w.n_self - x0, 0), kTileN); t.pos0_1 = w.ring_count + x0;
     t.slot0 = -1;
     valid = t.hi1;
   } else {
     const int base = kTileN * (u - w.n_extra);
     valid = min(w.cnt - base, kTileN);
-    t.lo0 = 0; t.hi0 = valid; t.pos0_0 = p.A + base;
+    t.lo0 = 0; t.hi0 = valid; t.pos0_0 = w.A + base;
     t.lo1 = 0; t.hi1 = 0; t.pos0_1 = 0;
-    int s0 = p.ring_start + base;
-    if (s0 >= p.R) s0 -= p.R;
+    int s0 = w.ring_start + base;
+    if (s0 >= w.R) s0 -= w.R;
     t.slot0 = s0;
   }
 #ifdef DSC_FULLW

@@ -11,6 +11,7 @@ for lib in paper_2605_01858_b200/libdscache.so paper_2605_01858_b200/variants/*.
   v=$(DSCACHE_LIB=$PWD/$lib timeout -s KILL 300 python bench.py --no-cpu-baseline --steps 30 --api $api 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['roofline']['achieved'], d['roofline'].get('traffic'))")
   echo "$(basename $lib) $api | $v" | tee -a $OUT
   done
-  DSCACHE_LIB=$PWD/$lib timeout -s KILL 300 python scripts/trace_attn.py --ctas 2 --streams 64 > gpurun_out/trace_${TAG}_$(basename $lib .so).txt 2>&1
-  grep -E "==|summary" gpurun_out/trace_${TAG}_$(basename $lib .so).txt | tee -a $OUT
 done
+# event timeline of the default build (trace variant compiled by the script)
+timeout -s KILL 300 python scripts/trace_attn.py --ctas 2 --streams 64 > gpurun_out/trace_${TAG}.txt 2>&1
+grep -E "==|summary|switch" gpurun_out/trace_${TAG}.txt | tee -a $OUT

@@ -63,6 +63,12 @@ __global__ void __launch_bounds__(512, 1) k(long long* cyc, int rounds) {
   }
   if (threadIdx.x == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
   if (threadIdx.x == 0) for (int i = 0; i < 6; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_b[i]));
+  __shared__ __align__(8) uint64_t bard;
+  const uint32_t bar_done = (uint32_t)__cvta_generic_to_shared(&bard);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_done));
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_done) : "memory");
+  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -115,7 +121,7 @@ __global__ void __launch_bounds__(512, 1) k(long long* cyc, int rounds) {
             mma_ts(tmem + 384, tmem + 128 + (r & 1) * 64 + k8 * 8, db + (uint64_t)(k8 * 128), idesc_bf16(128, 128, 0, 1), 1);
           }
         }
-        if (MODE == 9 || MODE == 10) {   // v5 tile with the kernel's commits (MODE 10: 1 commit per tile)
+        if (MODE == 9 || MODE == 10 || MODE == 11) {   // v5 tile with the kernel's commits (MODE 10: 1 commit per tile)
           const uint64_t offb = (uint64_t)((k8 >> 2) * 512 + (k8 & 3) * 2);
           mma_ss(tmem + (r & 1) * 64, da + off, db + offb, idesc_bf16(128, 64, 0, 0), k8 > 0);
           if (MODE == 9 && k8 == 7) commit(bar_b[0]);
@@ -128,6 +134,9 @@ __global__ void __launch_bounds__(512, 1) k(long long* cyc, int rounds) {
             if (MODE == 9 && k8 == 3) { commit(bar_b[4]); commit(bar_b[5]); }
           }
           if (MODE == 10 && k8 == 7) commit(bar_b[0]);
+          if (MODE == 11 && (k8 == 3 || k8 == 7)) {   // satisfied mbarrier waits between MMA groups (4 per tile)
+            wait(bar_done, 0); wait(bar_done, 0);
+          }
         }
         if (MODE == 4) {
           if (r & 1) mma_ts(tmem + 256 + (r & 2) * 64, tmem + (r & 2) * 64 + k8 * 8, db + (uint64_t)(k8 * 128),
@@ -173,6 +182,7 @@ int main() {
   run<8, 1>("v5 tile (per 3 MMAs)", c, smem);
   run<9, 0>("v5 tile + 6 commits", c, smem);
   run<10, 0>("v5 tile + 1 commit", c, smem);
+  run<11, 0>("v5 tile + 4 waits", c, smem);
   run<4, 0>("QK+PV mix", c, smem); run<4, 1>("QK+PV mix", c, smem);
   run<4, 2>("QK+PV mix", c, smem); run<4, 3>("QK+PV mix", c, smem);
   return 0;

@@ -10,6 +10,14 @@ import sys
 
 import torch
 
+# the event timeline is compiled only into the DSC_TRACE=1 variant of the library
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_01858_b200 import _build as _B  # noqa: E402
+from paper_2605_01858_b200 import dscache as _D  # noqa: E402
+if "DSCACHE_LIB" not in os.environ:
+    _defs = [d for d in os.environ.get("DSC_TRACE_DEFS", "").split() if d]
+    _D.load_library(_B.build_variant("trace" + "_".join(d.replace("=", "") for d in _defs), ["DSC_TRACE=1"] + _defs))
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import dscache_synth as synth  # noqa: E402
 from paper_2605_01858_b200 import dscache as D  # noqa: E402

@@ -110,6 +110,10 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 #ifndef DSC_QREG
 #define DSC_QREG 0
 #endif
+// DSC_SORDER 1: MMA order PV0(g) S0(g+2) PV1(g) S1(g+2) (else PV0 PV1 S0 S1)
+#ifndef DSC_SORDER
+#define DSC_SORDER 1
+#endif
 // DSC_INTERLEAVE: the fused step interleaves attend and build items per (problem, kv head)
 #ifndef DSC_INTERLEAVE
 #define DSC_INTERLEAVE 0
@@ -631,6 +635,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nu = tile_segments(p, w, w.t_begin + jj).width;
           mbar_wait(bar(B_VF + vs), (g / VST) & 1);
           if (lane == 0 && q_lo == 0) TRACE(EV_VF, g);
+#if DSC_SORDER
+          // per Q tile: PV(g) then S(g+2) into the buffer PV(g) just consumed, so Q tile 0's
+          // next scores do not wait for Q tile 1's P(g)
+          const bool more = jj + 2 < n;
+          const int ks2 = (g + 2) % KST;
+          const int nu2 = more ? tile_segments(p, w, w.t_begin + jj + 2).width : 0;
+#pragma unroll 1
+          for (int qt = q_lo; qt < q_hi; ++qt) {
+            mbar_wait(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
+            if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
+            if (lane == 0) TRACE(EV_PV0 + qt, g);
+            tc_fence_after();
+            issue_pv(qt, vs, jj > 0, nu, buf);
+            mma_commit_w(bar(B_O + qt * 2 + buf));
+            if (lane == 0) TRACE(EV_PVI + qt, g);
+            if (more) {
+              if (qt == q_lo) {
+                mbar_wait(bar(B_KF + ks2), ((g + 2) / KST) & 1);
+                tc_fence_after();
+              }
+              issue_qk(qt, ks2, nu2, buf);
+              mma_commit_w(bar(B_S + qt * 2 + buf));
+            }
+          }
+          mma_commit_w(bar(B_VE + vs));
+          if (more) mma_commit_w(bar(B_KE + ks2));
+#else
 #pragma unroll 1
           for (int qt = q_lo; qt < q_hi; ++qt) {
             mbar_wait(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
@@ -644,6 +675,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit_w(bar(B_VE + vs));
           // S(g+2) reuses buffer g & 1: issued after PV(g) has consumed P(g)
           if (jj + 2 < n) issue_s(p, w, g + 2, w.t_begin + jj + 2);
+#endif
         }
         gt += n;
       }

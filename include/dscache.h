@@ -223,14 +223,18 @@ dscache_status dscache_copy_sink(dscache_t h, int32_t stream_idx, int32_t layer,
 dscache_status dscache_set_debug(dscache_t h, int32_t* build_pos, int32_t* attend_pos, int32_t poison);
 int32_t        dscache_debug_len(dscache_t h);
 
-/* Per-CTA event timeline of the tcgen05 attention kernel (profiling aid).  buf: DEVICE
- * int64 buffer of ntrace_cta * 32 * 64 entries (NULL = off): for the first ntrace_cta
- * CTAs of each launch, clock64() at [cta][event][tile] for events 0 K tile issued,
- * 1 V tile issued, 2 raw K landed, 3 rotated K seen by the MMA issuer, 4/5 S0/S1 seen
- * by softmax, 6/7 P0/P1 written, 8/9 PV0/PV1 issued, 10 Q ready, 11 CTA start,
- * 12 CTA end (tile index 0 for 10-12), 13 V seen by the MMA issuer, 14..21 P written
- * by softmax warp 0..7, 22..27 softmax warp 0 internal steps (S half 0/1 loaded for the
- * max, rescale decided, S half 0/1 reloaded, P packed); tiles >= 64 are not recorded. */
+/* Per-CTA event timeline of the tcgen05 attention kernel (profiling aid).  Recorded only
+ * by a library built with -DDSC_TRACE=1 (scripts/trace_attn.py builds that variant); the
+ * production library accepts the call and records nothing.  buf: DEVICE int64 buffer of
+ * ntrace_cta * 40 * 64 entries (NULL = off): for the first ntrace_cta CTAs of each launch,
+ * clock64() at [cta][event][tile] for events 0 K tile issued, 1 V tile issued, 2 raw K
+ * landed, 3 rotated K seen by the MMA issuer, 4/5 S0/S1 seen by softmax, 6/7 P0/P1
+ * written, 8/9 PV0/PV1 about to be issued, 10 Q ready, 11 CTA start, 12 CTA end (tile
+ * index 0 for 10-12), 13 V seen by the MMA issuer, 14..21 P written by softmax warp 0..7,
+ * 22 softmax warp 0 scores loaded, 26 P packed, 28 K rotated, 29..31 item switch (Q
+ * published / loaded / started, indexed by the next item's first tile), 32 S issued,
+ * 33/34 PV0/PV1 issued, 35/36 epilogue start / stores issued; tiles (64 keys each)
+ * >= 64 are not recorded. */
 dscache_status dscache_set_trace(dscache_t h, int64_t* buf, int32_t ntrace_cta);
 
 /* Profiling: when enabled, every attention/combine kernel launch is bracketed by

@@ -331,7 +331,7 @@ class DSCache:
 
     def set_trace(self, buf: Optional[torch.Tensor], ntrace_cta: int = 1):
         """buf: int64 CUDA tensor of ntrace_cta*32*64 entries (None = off)."""
-        if buf is not None and (buf.dtype != torch.int64 or buf.numel() < ntrace_cta * 32 * 64):
+        if buf is not None and (buf.dtype != torch.int64 or buf.numel() < ntrace_cta * 40 * 64):
             raise ValueError("trace buffer must be int64 with ntrace_cta*32*64 entries")
         self._trace = buf
         _check(_lib.dscache_set_trace(self._h, _ptr(buf), int(ntrace_cta)))

@@ -78,26 +78,37 @@ def main():
         "(fill, warm-up, timed steps, e2e).  Per-launch times are cold-cache and serialised: "
         "compare shares, not absolutes.\n\n" + table + "\n")
     recs = ncu_raw(tag)
-    lines = [f"# ncu --set full of attn_tc_kernel ({tag}, {cfg})\n",
-             "`ncu --set full --clock-control none --import-source on -k regex:attn_tc -s 4 -c 2` on the "
-             "bench command; launch 1 = build_instant, launch 2 = attend (one c5 step each).\n",
-             "| metric | " + " | ".join(f"launch {i + 1}" for i in range(len(recs))) + " |",
-             "|---|" + "---|" * len(recs)]
-    for k, name in KEYS:
-        vals = [r.get(k, "") for r in recs]
-        lines.append(f"| {name} (`{k}`) | " + " | ".join(vals) + " |")
-    stalls = []
-    for r in recs:
-        items = []
-        for k, v in r.items():
-            if k.startswith("smsp__pcsamp_warps_issue_stalled") and not k.endswith("not_issued"):
-                try:
-                    items.append((float(v.replace(",", "")), k[33:]))
-                except ValueError:
-                    pass
-        tot = sum(v for v, _ in items) or 1.0
-        stalls.append(", ".join(f"{n} {100 * v / tot:.0f}%" for v, n in sorted(items, reverse=True)[:6]))
-    lines.append("\nTop warp-stall reasons (pc sampling): " + " / ".join(stalls) + "\n")
+    lines = [f"# ncu --set full of attn_tc_kernel ({tag}, {cfg})\n"]
+
+    def section(recs, title, labels):
+        lines.append(f"## {title}\n")
+        lines.append("| metric | " + " | ".join(labels[:len(recs)]) + " |")
+        lines.append("|---|" + "---|" * len(recs))
+        for k, name in KEYS:
+            vals = [r.get(k, "") for r in recs]
+            lines.append(f"| {name} (`{k}`) | " + " | ".join(vals) + " |")
+        stalls = []
+        for r in recs:
+            items = []
+            for k, v in r.items():
+                if k.startswith("smsp__pcsamp_warps_issue_stalled") and not k.endswith("not_issued"):
+                    try:
+                        items.append((float(v.replace(",", "")), k[33:]))
+                    except ValueError:
+                        pass
+            tot = sum(v for v, _ in items) or 1.0
+            stalls.append(", ".join(f"{n} {100 * v / tot:.0f}%" for v, n in sorted(items, reverse=True)[:6]))
+        lines.append("\nTop warp-stall reasons (pc sampling): " + " / ".join(stalls) + "\n")
+
+    section(recs, "Fused step launch (the bench's dominant kernel): `-k regex:attn_tc -s 4 -c 1`, "
+            "one c5 step = build_instant + attend items in one persistent launch", ["fused step"])
+    split_rep = os.path.join(G, f"prof_split_{tag}.ncu-rep")
+    if os.path.exists(split_rep):
+        txt = subprocess.run(["ncu", "-i", split_rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(txt)))
+        srecs = [dict(zip(rows[0], r)) for r in rows[2:]]
+        section(srecs, "Split API (`--api split`, `-s 8 -c 2`): launch 1 = build_instant, launch 2 = attend",
+                ["build_instant", "attend"])
     open(os.path.join(P, f"{tag}_ncu_full.md"), "w").write("\n".join(lines) + "\n")
     # DRAM traffic per launch for bench.py's roofline.traffic (units from the raw page: MB or GB)
     units = {}

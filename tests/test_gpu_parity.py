@@ -208,6 +208,24 @@ def test_edge_configs_tcgen05(lib, variant):
     _check_steps(cfg, res, steps, [(0, 0), (0, 1)], tag="-" + variant)
 
 
+@pytest.mark.parametrize("variant", ["odd_tpf_wrap", "big_sink_multi_extra", "tiny_frames"])
+def test_logical_tiles_mirror_and_narrow_widths(lib, variant):
+    """64-key logical window tiles read through the ring's mirror rows (windows that wrap
+    around slot R-1), tile widths that are not multiples of 64 (narrow QK^T N / PV K),
+    several sink+self tiles, and the tcgen05 path for tpf < 64 (any tpf is eligible)."""
+    base = synth.CONFIGS["c2"].replace(num_frames=17, num_layers=1)
+    if variant == "odd_tpf_wrap":        # R = 8 * 40 = 320 slots: the window wraps every few steps
+        cfg = base.replace(tokens_per_frame=40, sink_tokens=3, past_frames=5, instant_frames=2, query_tokens=21)
+    elif variant == "big_sink_multi_extra":   # A + q = 134 > 2 tiles of sink/self keys
+        cfg = base.replace(tokens_per_frame=100, sink_tokens=70, past_frames=3, instant_frames=2, query_tokens=64)
+    else:                                 # 24-token frames: every tile narrow or partial
+        cfg = base.replace(tokens_per_frame=24, sink_tokens=5, past_frames=4, instant_frames=3, query_tokens=9)
+    steps = list(range(0, cfg.num_frames, 2)) + [cfg.num_frames - 1]
+    res = run_stream(cfg, steps, [(0, 0)])
+    assert res["impl"] == {"build_instant": "tcgen05", "attend": "tcgen05"}
+    _check_steps(cfg, res, steps, [(0, 0)], tag="-" + variant)
+
+
 def test_c3_28_layers_sampled(lib):
     cfg = synth.CONFIGS["c3"]
     steps = [0, 7, 8, 71, 72, 100]

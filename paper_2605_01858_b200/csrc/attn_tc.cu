@@ -138,7 +138,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sbase = su32(smem);
+  // shared-window base computed from the dynamic-smem symbol itself (not via a generic
+  // pointer) so the compiler keeps it, and every descriptor derived from it, uniform
+  const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(smem_raw) + 1023u) & ~1023u;
   const uint32_t bar0 = sbase + OFF_BAR;
   auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + B_N * 8);
@@ -187,7 +189,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // one CTA per SM allocates all 512 columns, so the allocation is column 0 of lane 0;
+  // the MMA descriptors use that constant (uniform registers, no per-MMA moves)
+  const uint32_t tmem_alloc = *tmem_slot;
+  if (tmem_alloc != 0u) __trap();
+  constexpr uint32_t tmem = 0u;
 
   if (warp < 8) {
     // ================================================================ softmax
@@ -691,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 14) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_alloc) : "memory");
   }
 }
 

@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       // S of tile g for Q tile qt into buffer g & 1; K stage g % KST is free when both MMA
       // warps' QK^T of the tile are done (K-free barrier counts 2 commits)
-      auto issue_s = [&](const AttnParams& p, const Item& w, int g, int u) {
+      auto issue_s = [&](const ItemGeo& p, const Item& w, int g, int u) {
         const int ks = g % KST, buf = g & 1;
         const int nu = tile_segments(p, w, u).width;
         mbar_wait(bar(B_KF + ks), (g / KST) & 1);
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       int gt = 0, kk = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
-        const AttnParams& p = ITEM_PARAMS(idx);
+        const ItemGeo p = item_geo(pa, pb, ITEM_B(idx));
         const Item w = decode_item(p, ITEM_LOCAL(idx));
         const int n = w.n_tiles;
         for (int qt = q_lo; qt < q_hi; ++qt) mbar_wait(bar(B_Q + qt), kk & 1);

@@ -296,7 +296,24 @@ struct Item {
 // m-block descending: all (problem, head) pairs of the longest causal m-block first
 // (LPT-like balance of the persistent CTAs).  DSC_ORDER 0 groups the m-blocks of one
 // (problem, head) for L2 reuse of its K/V; measured slower on c5 (9.8K vs 12.4K frames/s).
-__device__ __forceinline__ Item decode_item(const AttnParams& p, int idx) {
+// The integer fields decode_item needs, selected per item from the two launch parameter
+// blocks with constant-offset loads (a reference chosen at run time turns every field read
+// into an indexed constant load whose result the compiler cannot keep uniform).
+struct ItemGeo {
+  int n_splits, P, Hkv, n_mblocks, layer_count, N_total, layer_begin, n_q, grp, q_pos0, A, ring_count, n_self,
+      ring_start, R, tiles_per_split;
+};
+__device__ __forceinline__ ItemGeo item_geo(const AttnParams& pa, const AttnParams& pb, bool isb) {
+  ItemGeo q;
+#define DSC_SEL(f) q.f = isb ? pb.f : pa.f
+  DSC_SEL(n_splits); DSC_SEL(P); DSC_SEL(Hkv); DSC_SEL(n_mblocks); DSC_SEL(layer_count); DSC_SEL(N_total);
+  DSC_SEL(layer_begin); DSC_SEL(n_q); DSC_SEL(grp); DSC_SEL(q_pos0); DSC_SEL(A); DSC_SEL(ring_count);
+  DSC_SEL(n_self); DSC_SEL(ring_start); DSC_SEL(R); DSC_SEL(tiles_per_split);
+#undef DSC_SEL
+  return q;
+}
+template <class PT>
+__device__ __forceinline__ Item decode_item(const PT& p, int idx) {
   Item w;
   w.sp = idx % p.n_splits;
   const int rest = idx / p.n_splits;
@@ -339,7 +356,8 @@ struct TileSeg {
   int width;
 };
 
-__device__ __forceinline__ TileSeg tile_segments(const AttnParams&, const Item& w, int u) {
+template <class PT>
+__device__ __forceinline__ TileSeg tile_segments(const PT&, const Item& w, int u) {
   TileSeg t;
   int valid;
   if (u < w.n_extra) {

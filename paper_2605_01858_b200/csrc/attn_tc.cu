@@ -82,8 +82,14 @@ static_assert(kNQT * 128 == kMBlockRows, "work items are 256-row m-blocks");
 #define DSC_POLY 0
 #endif
 // ablation knobs (timing experiments only; results are wrong when set):
+// DSC_ABL_MMAONLY: only the MMA warp runs, issuing every MMA and commit without waiting
+// (measures the issue loop alone),
 // DSC_ABL_SOFTMAX skips the softmax body, DSC_ABL_ROT skips the K rotation,
 // DSC_ABL_EX2 replaces ex2 by a copy (MUFU-free softmax)
+#ifndef DSC_ABL_MMAONLY
+#define DSC_ABL_MMAONLY 0
+#endif
+#define MWAIT(b, ph) do { if (!DSC_ABL_MMAONLY) mbar_wait((b), (ph)); } while (0)
 #ifndef DSC_ABL_SOFTMAX
 #define DSC_ABL_SOFTMAX 0
 #endif
@@ -195,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tmem_alloc != 0u) __trap();
   constexpr uint32_t tmem = 0u;
 
+  const int n_role_items = (DSC_ABL_MMAONLY && warp < 14) ? 0 : n_items;   // ablation: only the MMA issuer works
   if (warp < 8) {
     // ================================================================ softmax
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float2 scale2 = make_float2(sl2, sl2);
 
     const uint32_t qtile = sbase + OFF_Q + qt * kQBytes;
-    if (blockIdx.x < (unsigned)n_items) {            // Q tile of the first item
+    if (blockIdx.x < (unsigned)n_role_items) {       // Q tile of the first item
       const AttnParams& p0 = ITEM_PARAMS((int)blockIdx.x);
       const Item w0 = decode_item(p0, ITEM_LOCAL((int)blockIdx.x));
 #if DSC_QREG
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(bar(B_Q + qt));
     }
     int gt = 0, kk = 0;
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
+    for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x, ++kk) {
       const AttnParams& p = ITEM_PARAMS(idx);
       const Item w = decode_item(p, ITEM_LOCAL(idx));
       const int A = w.A;
@@ -455,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       sth[j] = make_float2(t.z, t.w);
     }
     int gt = 0, kk = 0;
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
+    for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x, ++kk) {
       const AttnParams& p = ITEM_PARAMS(idx);
       const Item w = decode_item(p, ITEM_LOCAL(idx));
       const int A = p.A;
@@ -526,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int off = isk ? OFF_K : OFF_V;
       const int b_full = isk ? B_KR : B_VF, b_free = isk ? B_KE : B_VE;
       int gt = 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x) {
         const AttnParams& p = ITEM_PARAMS(idx);
         const Item w = decode_item(p, ITEM_LOCAL(idx));
         const int A = p.A;
@@ -616,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_s = [&](const ItemGeo& p, const Item& w, int g, int u) {
         const int ks = g % KST, buf = g & 1;
         const int nu = tile_segments(p, w, u).width;
-        mbar_wait(bar(B_KF + ks), (g / KST) & 1);
+        MWAIT(bar(B_KF + ks), (g / KST) & 1);
         if (lane == 0 && q_lo == 0) TRACE(EV_KF, g);
         tc_fence_after();
 #pragma unroll 1
@@ -632,16 +639,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         const ItemGeo p = item_geo(pa, pb, ITEM_B(idx));
         const Item w = decode_item(p, ITEM_LOCAL(idx));
         const int n = w.n_tiles;
-        for (int qt = q_lo; qt < q_hi; ++qt) mbar_wait(bar(B_Q + qt), kk & 1);
+        for (int qt = q_lo; qt < q_hi; ++qt) MWAIT(bar(B_Q + qt), kk & 1);
         if (kk == 0 && lane == 0 && q_lo == 0) TRACE(EV_Q, 0);
         if (n > 0) issue_s(p, w, gt, w.t_begin);
         if (n > 1) issue_s(p, w, gt + 1, w.t_begin + 1);
         for (int jj = 0; jj < n; ++jj) {
           const int g = gt + jj, vs = g % VST, buf = g & 1;
           const int nu = tile_segments(p, w, w.t_begin + jj).width;
-          mbar_wait(bar(B_VF + vs), (g / VST) & 1);
+          MWAIT(bar(B_VF + vs), (g / VST) & 1);
           if (lane == 0 && q_lo == 0) TRACE(EV_VF, g);
-#if DSC_SORDER
+#if DSC_SORDER == 2
+          // one burst per tile: every wait first (V(g), P0(g), P1(g), K(g+2) rotated), then
+          // PV0 PV1 S0(g+2) S1(g+2) back to back and the commits.  The tensor pipe queues
+          // only a couple of MMAs, so every wait/commit between MMA groups left it idle.
+          const bool more = jj + 2 < n;
+          const int ks2 = (g + 2) % KST;
+          const int nu2 = more ? tile_segments(p, w, w.t_begin + jj + 2).width : 0;
+          for (int qt = q_lo; qt < q_hi; ++qt) {
+            MWAIT(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
+            if (jj == 0 && kk > 0) MWAIT(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
+          }
+          if (more) MWAIT(bar(B_KF + ks2), ((g + 2) / KST) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int qt = q_lo; qt < q_hi; ++qt) issue_pv(qt, vs, jj > 0, nu, buf);
+          if (more) {
+#pragma unroll 1
+            for (int qt = q_lo; qt < q_hi; ++qt) issue_qk(qt, ks2, nu2, buf);
+          }
+#pragma unroll 1
+          for (int qt = q_lo; qt < q_hi; ++qt) mma_commit_w(bar(B_O + qt * 2 + buf));
+          mma_commit_w(bar(B_VE + vs));
+          if (more) {
+#pragma unroll 1
+            for (int qt = q_lo; qt < q_hi; ++qt) mma_commit_w(bar(B_S + qt * 2 + buf));
+            mma_commit_w(bar(B_KE + ks2));
+          }
+#elif DSC_SORDER
           // per Q tile: PV(g) then S(g+2) into the buffer PV(g) just consumed, so Q tile 0's
           // next scores do not wait for Q tile 1's P(g)
           const bool more = jj + 2 < n;
@@ -649,8 +683,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nu2 = more ? tile_segments(p, w, w.t_begin + jj + 2).width : 0;
 #pragma unroll 1
           for (int qt = q_lo; qt < q_hi; ++qt) {
-            mbar_wait(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
-            if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
+            MWAIT(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
+            if (jj == 0 && kk > 0) MWAIT(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
             if (lane == 0) TRACE(EV_PV0 + qt, g);
             tc_fence_after();
             issue_pv(qt, vs, jj > 0, nu, buf);
@@ -658,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) TRACE(EV_PVI + qt, g);
             if (more) {
               if (qt == q_lo) {
-                mbar_wait(bar(B_KF + ks2), ((g + 2) / KST) & 1);
+                MWAIT(bar(B_KF + ks2), ((g + 2) / KST) & 1);
                 tc_fence_after();
               }
               issue_qk(qt, ks2, nu2, buf);
@@ -670,8 +704,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #else
 #pragma unroll 1
           for (int qt = q_lo; qt < q_hi; ++qt) {
-            mbar_wait(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
-            if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
+            MWAIT(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
+            if (jj == 0 && kk > 0) MWAIT(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
             if (lane == 0) TRACE(EV_PV0 + qt, g);
             tc_fence_after();
             issue_pv(qt, vs, jj > 0, nu, buf);
@@ -686,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         gt += n;
       }
       // drain: the last V-free commit tracks every MMA of this CTA
-      if (gt > 0) mbar_wait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1);
+      if (gt > 0) mbar_wait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1);   // drain (kept in every variant)
       if (lane == 0) TRACE(EV_END, 0);
       }
     mma_done:;

@@ -191,6 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     TRACE(EV_START, 0);
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_k)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_v)) : "memory");
+    if (nb > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pb.tmap_k)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pb.tmap_v)) : "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -503,7 +507,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef DSC_DBG_ROTFULL
         if (!DSC_ABL_ROT)
 #else
-        if (!DSC_ABL_ROT && rg * 4 < t.width)   // rows >= width are never read by the MMA
+        if (!DSC_ABL_ROT && !w.staged && rg * 4 < t.width)   // rows >= width are never read by the MMA;
+                                                             // staged K arrives rotated
 #endif
           rotate_rows<1, kKVHalf>(sbase + OFF_K + ks * kKVBytes, rg * 4, c8, rp, cth, sth, kpos, cur,
                                   max(cur_pos, 0));
@@ -528,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 12 || warp == 13) {
       // ============================================================== copy warps (12: K, 13: V)
       const bool isk = warp == 12;
-      const CUtensorMap* tmap = isk ? &p.tmap_k : &p.tmap_v;
+
       const int nst = isk ? KST : VST;
       const int off = isk ? OFF_K : OFF_V;
       const int b_full = isk ? B_KR : B_VF, b_free = isk ? B_KE : B_VE;
@@ -565,7 +570,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(b_full + st));
           } else if (lane == 0) {
-            const int row = (int)(w.head_row * (w.R + kMirror)) + t.slot0;   // logical window tile (mirror: no wrap)
+            // logical window tile: one box (the ring's mirror rows, or the staging rows)
+            const AttnParams& pi = ITEM_PARAMS(idx);
+            const CUtensorMap* tmap = isk ? &pi.tmap_k : &pi.tmap_v;
+            const int row = (int)(w.head_row * w.Rp) + t.slot0;
             mbar_arrive_tx(bar(b_full + st), kKVBytes);
             tma_load_2d(dst, tmap, 0, row, bar(b_full + st));
             tma_load_2d(dst + kKVHalf, tmap, 64, row, bar(b_full + st));
@@ -759,6 +767,10 @@ cudaError_t make_ring_tmap(CUtensorMap* map, void* base, unsigned long long rows
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t make_stage_tmap(CUtensorMap* map, void* base, unsigned long long rows) {
+  return make_ring_tmap(map, base, rows);   // same geometry: [rows][128] bf16, box 64 x kTileN, SW128
 }
 
 static long long tc_items(const AttnParams& p) { return (long long)p.P * p.Hkv * p.n_mblocks * p.n_splits; }

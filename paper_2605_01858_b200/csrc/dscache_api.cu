@@ -80,6 +80,11 @@ struct dscache_s {
   int impl_build = DSCACHE_IMPL_SIMT, impl_attend = DSCACHE_IMPL_SIMT;
   int num_sms = 148;
   CUtensorMap tmap_k{}, tmap_v{};
+  // staged build (tcgen05): per-step copy of sink ++ instant window, K pre-rotated
+  void* stage_k = nullptr;
+  void* stage_v = nullptr;
+  int stage_rows = 0;          // A + C
+  CUtensorMap tmap_sk{}, tmap_sv{};
   // profiling
   int prof = 0;
   struct Ev { cudaEvent_t a, b; int kind; };
@@ -140,6 +145,7 @@ void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
   p.dtype = c.dtype;
   p.dbg_M = std::max(h->C, c.max_query_tokens);
   p.tmap_k = h->tmap_k; p.tmap_v = h->tmap_v;
+  p.staged = 0;
   p.trace = h->trace; p.ntrace_cta = h->ntrace;
   p.n_splits = 1; p.tiles_per_split = 1 << 30;
 }
@@ -252,6 +258,15 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
     e = dsc::make_ring_tmap(&h->tmap_k, h->ring_k, rows);
     if (e == cudaSuccess) e = dsc::make_ring_tmap(&h->tmap_v, h->ring_v, rows);
   }
+  if (e == cudaSuccess && h->impl_build == DSCACHE_IMPL_TC && h->C > 0) {
+    h->stage_rows = c.sink_tokens + h->C;
+    const size_t sb = heads * h->stage_rows * c.head_dim * h->elem;
+    if (cudaMalloc(&h->stage_k, sb) != cudaSuccess || cudaMalloc(&h->stage_v, sb) != cudaSuccess) return oom("staging");
+    e = cudaMemset(h->stage_k, 0, sb);
+    if (e == cudaSuccess) e = cudaMemset(h->stage_v, 0, sb);
+    if (e == cudaSuccess) e = dsc::make_stage_tmap(&h->tmap_sk, h->stage_k, (unsigned long long)heads * h->stage_rows);
+    if (e == cudaSuccess) e = dsc::make_stage_tmap(&h->tmap_sv, h->stage_v, (unsigned long long)heads * h->stage_rows);
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     std::string m = cudaGetErrorString(e);
@@ -270,6 +285,7 @@ dscache_status dscache_destroy(dscache_t h) {
   for (auto e : h->pool) cudaEventDestroy(e);
   cudaFree(h->ring_k); cudaFree(h->ring_v); cudaFree(h->sink_k); cudaFree(h->sink_v);
   cudaFree(h->rope); cudaFree(h->ws);
+  cudaFree(h->stage_k); cudaFree(h->stage_v);
   delete h;
   return DSCACHE_OK;
 }
@@ -315,7 +331,7 @@ namespace {
 // Parameters of build_instant (Eq. 7): the C_t instant tokens attend causally over
 // [sink | instant window].  *empty is set when l_I = 0 (nothing to build).
 dscache_status prep_build(dscache_t h, int32_t lb, int32_t lc, const void* q_inst, void* o_inst, dsc::AttnParams& p,
-                          bool* empty) {
+                          bool* empty, dsc::StageParams* stage) {
   *empty = false;
   dscache_status s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
@@ -331,6 +347,22 @@ dscache_status prep_build(dscache_t h, int32_t lb, int32_t lc, const void* q_ins
   p.self_k = p.self_v = nullptr; p.n_self = 0;
   p.dbg_pos = h->dbg_build;
   p.n_mblocks = (p.n_q * p.grp + 2 * dsc::kTileM - 1) / (2 * dsc::kTileM);
+  // tcgen05 build: stage sink ++ instant window once per (stream, layer, head) with K
+  // rotated at the build ids 0.. (the window is re-read by every m-block; rotating it once
+  // instead of per m-block removes the RoPE work from the build items).  The debug id
+  // export records ids where the kernel rotates, so debug runs keep the ring path.
+  if (h->impl_build == DSCACHE_IMPL_TC && h->stage_k && !h->dbg_build) {
+    dsc::StageParams sp{};
+    sp.sink_k = h->sink_k; sp.sink_v = h->sink_v; sp.ring_k = h->ring_k; sp.ring_v = h->ring_v;
+    sp.stage_k = h->stage_k; sp.stage_v = h->stage_v; sp.rope_pairs = p.rope_pairs;
+    sp.S = p.S; sp.layer_count = lc; sp.layer_begin = lb; sp.N_total = p.N_total; sp.Hkv = p.Hkv;
+    sp.A = p.A; sp.R = h->R; sp.Rp_ring = h->Rp; sp.inst_start = sc.inst_start;
+    sp.rows = p.A + sc.C_t; sp.rows_stage = h->stage_rows;
+    *stage = sp;
+    p.staged = 1;
+    p.A = 0; p.ring_start = 0; p.ring_count = sp.rows; p.R = h->stage_rows; p.Rp = h->stage_rows;
+    p.tmap_k = h->tmap_sk; p.tmap_v = h->tmap_sv;
+  }
   return DSCACHE_OK;
 }
 }  // namespace
@@ -338,10 +370,15 @@ dscache_status prep_build(dscache_t h, int32_t lb, int32_t lc, const void* q_ins
 dscache_status dscache_build_instant(dscache_t h, int32_t lb, int32_t lc, const void* q_inst, void* o_inst,
                                      void* stream) {
   dsc::AttnParams p{};
+  dsc::StageParams sp{};
   bool empty = false;
-  dscache_status s = prep_build(h, lb, lc, q_inst, o_inst, p, &empty);
+  dscache_status s = prep_build(h, lb, lc, q_inst, o_inst, p, &empty, &sp);
   if (s != DSCACHE_OK || empty) return s;
   DeviceGuard dg(h->cfg.device);
+  if (p.staged) {
+    DSC_CUDA(dsc::launch_stage_instant(sp, (cudaStream_t)stream));
+    h->launches++;
+  }
   return run_attention(h, p, h->impl_build, 0, (cudaStream_t)stream);
 }
 
@@ -450,13 +487,18 @@ dscache_status dscache_step(dscache_t h, int32_t lb, int32_t lc, const void* k_f
   dscache_status s = dscache_append_frame(h, lb, lc, k_frame, v_frame, h->cfg.tokens_per_frame, stream);
   if (s != DSCACHE_OK) return s;
   dsc::AttnParams pb{}, pa{};
+  dsc::StageParams sp{};
   bool empty = false;
-  s = prep_build(h, lb, lc, q_inst, o_inst, pb, &empty);
+  s = prep_build(h, lb, lc, q_inst, o_inst, pb, &empty, &sp);
   if (s != DSCACHE_OK) return s;
   s = prep_attend(h, lb, lc, q, k_self, v_self, n_q, n_q, o, true, pa);
   if (s != DSCACHE_OK) return s;
   DeviceGuard dg(h->cfg.device);
   cudaStream_t st = (cudaStream_t)stream;
+  if (!empty && pb.staged) {
+    DSC_CUDA(dsc::launch_stage_instant(sp, st));
+    h->launches++;
+  }
   const bool debug = h->dbg_build || h->dbg_attend;
   if (empty || debug || h->impl_build != DSCACHE_IMPL_TC || h->impl_attend != DSCACHE_IMPL_TC) {
     if (!empty) {

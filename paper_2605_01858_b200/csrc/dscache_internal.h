@@ -52,6 +52,10 @@ struct AttnParams {
   // per-CTA event timeline (profiling); null = off.  [ntrace_cta][kTraceEvents][kTraceTiles] clock64
   long long* trace; int ntrace_cta;
   int dtype;                                 // 0 bf16, 1 fp32
+  // staged build (tcgen05 path): the keys are rows [0, ring_count) of the per-step staging
+  // buffers [S*N*Hkv][Rp][d] holding sink ++ instant window with K ALREADY rotated at ids
+  // 0..ring_count-1 (stage_instant_kernel); A = 0, ring_start = 0, no K rotation in-kernel
+  int staged;
   // TMA descriptors of the K / V rings viewed as [S*N*Hkv*R rows][128] bf16, box 64 x 128, SW128
   CUtensorMap tmap_k;
   CUtensorMap tmap_v;
@@ -69,7 +73,19 @@ struct AppendParams {
   int elem_bytes;
 };
 
+// One step's instant-cache keys, staged once per (stream, layer, kv head) instead of once
+// per m-block: row i < A is sink row i, row i >= A is ring slot (inst_start + i - A) mod R;
+// K rows are rotated at id i (split-half RoPE, pair table), V rows copied.
+struct StageParams {
+  const void* sink_k; const void* sink_v;    // [S][N][Hkv][A][d]
+  const void* ring_k; const void* ring_v;    // [S][N][Hkv][Rp_ring][d]
+  void* stage_k; void* stage_v;              // [S][N][Hkv][rows_stage][d]
+  const float4* rope_pairs;
+  int S, layer_count, layer_begin, N_total, Hkv, A, R, Rp_ring, inst_start, rows, rows_stage;
+};
+
 // kernels (launchers return cudaGetLastError())
+cudaError_t launch_stage_instant(const StageParams& p, cudaStream_t st);
 cudaError_t launch_rope_table(float2* table, int npos, int d, double theta, cudaStream_t st);
 cudaError_t launch_append(const AppendParams& p, cudaStream_t st);
 cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t st);
@@ -80,5 +96,6 @@ cudaError_t launch_combine(const AttnParams& p, cudaStream_t st);
 int attn_tc_smem_bytes();
 // encode the 2-D ring tensor map (bf16, d = 128) used by the tcgen05 kernel
 cudaError_t make_ring_tmap(CUtensorMap* map, void* base, unsigned long long rows);
+cudaError_t make_stage_tmap(CUtensorMap* map, void* base, unsigned long long rows);
 
 }  // namespace dsc

@@ -130,6 +130,68 @@ cudaError_t launch_append(const AppendParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ K8 instant-window staging
+// One thread per (head, staged row, 8-frequency chunk c8): K chunk c8 (cols 8c8..8c8+7) and
+// its split-half partner (cols 64+8c8..) rotated at id = row with the fp64-built pair table
+// (y_f = x_f cos - x_{f+64} sin, y_{f+64} = x_f sin + x_{f+64} cos, Def. 4.1
+// applied at the build's ids), rounded to bf16; the V row's two 16-byte chunks
+// are copied alongside.
+__device__ __forceinline__ float2 bfp(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+__device__ __forceinline__ uint32_t pk_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__global__ void __launch_bounds__(256) stage_instant_kernel(StageParams p) {
+  const long long total = (long long)p.S * p.layer_count * p.Hkv * p.rows * 8;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int c8 = (int)(idx & 7);
+    long long r = idx >> 3;
+    const int row = (int)(r % p.rows); r /= p.rows;
+    const int g = (int)(r % p.Hkv); r /= p.Hkv;
+    const int l = (int)(r % p.layer_count);
+    const long long s = r / p.layer_count;
+    const long long head = (s * p.N_total + p.layer_begin + l) * p.Hkv + g;
+    const uint4 *sk, *sv;
+    if (row < p.A) {
+      sk = reinterpret_cast<const uint4*>(p.sink_k) + (head * p.A + row) * 16;
+      sv = reinterpret_cast<const uint4*>(p.sink_v) + (head * p.A + row) * 16;
+    } else {
+      int slot = p.inst_start + row - p.A;
+      if (slot >= p.R) slot -= p.R;
+      sk = reinterpret_cast<const uint4*>(p.ring_k) + (head * p.Rp_ring + slot) * 16;
+      sv = reinterpret_cast<const uint4*>(p.ring_v) + (head * p.Rp_ring + slot) * 16;
+    }
+    uint4* dk = reinterpret_cast<uint4*>(p.stage_k) + (head * p.rows_stage + row) * 16;
+    uint4* dv = reinterpret_cast<uint4*>(p.stage_v) + (head * p.rows_stage + row) * 16;
+    const uint4 lo = sk[c8], hi = sk[c8 + 8];
+    const float4* t = p.rope_pairs + (long long)row * 32 + 4 * c8;
+    const uint32_t lw[4] = {lo.x, lo.y, lo.z, lo.w}, hw[4] = {hi.x, hi.y, hi.z, hi.w};
+    uint32_t ol[4], oh[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 cs = t[j];   // (cos f, cos f+1, sin f, sin f+1), f = 8c8 + 2j
+      const float2 a = bfp(lw[j]), b = bfp(hw[j]);
+      ol[j] = pk_bf16(a.x * cs.x - b.x * cs.z, a.y * cs.y - b.y * cs.w);
+      oh[j] = pk_bf16(a.x * cs.z + b.x * cs.x, a.y * cs.w + b.y * cs.y);
+    }
+    dk[c8] = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+    dk[c8 + 8] = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+    dv[c8] = sv[c8];
+    dv[c8 + 8] = sv[c8 + 8];
+  }
+}
+
+cudaError_t launch_stage_instant(const StageParams& p, cudaStream_t st) {
+  const long long total = (long long)p.S * p.layer_count * p.Hkv * p.rows * 8;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+  stage_instant_kernel<<<std::max(blocks, 1), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ K6 SIMT attention
 template <typename T> __device__ __forceinline__ float to_f(T x);
 template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }

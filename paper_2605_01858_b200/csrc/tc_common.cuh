@@ -290,6 +290,7 @@ struct Item {
   // per-launch geometry copied to registers once per item: the tile map below reads no
   // kernel parameters (parameters of a pa/pb-selected launch are indexed constant loads)
   int A, n_self, ring_count, ring_start, R;
+  int Rp, staged;     // ring rows per head (R + mirror, or the staging rows); staged build
 };
 
 // work item idx -> split fastest, then (DSC_ORDER 1, default) problem x kv head, then
@@ -301,14 +302,14 @@ struct Item {
 // into an indexed constant load whose result the compiler cannot keep uniform).
 struct ItemGeo {
   int n_splits, P, Hkv, n_mblocks, layer_count, N_total, layer_begin, n_q, grp, q_pos0, A, ring_count, n_self,
-      ring_start, R, tiles_per_split;
+      ring_start, R, tiles_per_split, Rp, staged;
 };
 __device__ __forceinline__ ItemGeo item_geo(const AttnParams& pa, const AttnParams& pb, bool isb) {
   ItemGeo q;
 #define DSC_SEL(f) q.f = isb ? pb.f : pa.f
   DSC_SEL(n_splits); DSC_SEL(P); DSC_SEL(Hkv); DSC_SEL(n_mblocks); DSC_SEL(layer_count); DSC_SEL(N_total);
   DSC_SEL(layer_begin); DSC_SEL(n_q); DSC_SEL(grp); DSC_SEL(q_pos0); DSC_SEL(A); DSC_SEL(ring_count);
-  DSC_SEL(n_self); DSC_SEL(ring_start); DSC_SEL(R); DSC_SEL(tiles_per_split);
+  DSC_SEL(n_self); DSC_SEL(ring_start); DSC_SEL(R); DSC_SEL(tiles_per_split); DSC_SEL(Rp); DSC_SEL(staged);
 #undef DSC_SEL
   return q;
 }
@@ -334,6 +335,7 @@ __device__ __forceinline__ Item decode_item(const PT& p, int idx) {
   const int lim_max = p.q_pos0 + last_row / p.grp;
   w.cnt = min(max(lim_max - p.A + 1, 0), p.ring_count);
   w.A = p.A; w.n_self = p.n_self; w.ring_count = p.ring_count; w.ring_start = p.ring_start; w.R = p.R;
+  w.Rp = p.Rp; w.staged = p.staged;
   w.n_extra = (p.A + p.n_self + kTileN - 1) / kTileN;
   const int total = w.n_extra + (w.cnt + kTileN - 1) / kTileN;
   w.t_begin = min(w.sp * p.tiles_per_split, total);

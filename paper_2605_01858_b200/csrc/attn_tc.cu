@@ -120,6 +120,11 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 #ifndef DSC_SORDER
 #define DSC_SORDER 1
 #endif
+// DSC_QEARLY 1: the next item's Q cp.async are issued at the last tile's S wait (else
+// after the last tile)
+#ifndef DSC_QEARLY
+#define DSC_QEARLY 1
+#endif
 // DSC_INTERLEAVE: the fused step interleaves attend and build items per (problem, kv head)
 #ifndef DSC_INTERLEAVE
 #define DSC_INTERLEAVE 0
@@ -277,6 +282,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool full = (c_lo == 0) && (c_hi == kKT);
         mbar_wait(bar(B_S + sb), (g >> 1) & 1);
         if (rloc == 0) TRACE(EV_S0 + qt, g);
+#if DSC_QEARLY
+        // S(last) is in: the MMA is done reading this Q tile, so the next item's Q rows are
+        // fetched now and land while the last tile's softmax runs
+        if (jj == n - 1 && idx + (int)gridDim.x < n_role_items) {
+          const int nidx = idx + gridDim.x;
+          issue_q_tile(ITEM_PARAMS(nidx), decode_item(ITEM_PARAMS(nidx), ITEM_LOCAL(nidx)), qt, threadIdx.x - qt * 128,
+                       qtile);
+        }
+#endif
         if (warp_dead || DSC_ABL_SOFTMAX) {   // all 32 rows are padding: their P / O are never used
           mbar_arrive(bar(B_P + sb));
           continue;
@@ -392,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         load_q_row_rotated(ITEM_PARAMS(nidx), wn, qt, rloc, qtile);
         fence_proxy_async();
 #else
-        issue_q_tile(ITEM_PARAMS(nidx), wn, qt, threadIdx.x - qt * 128, qtile);
+        if (!DSC_QEARLY || n == 0) issue_q_tile(ITEM_PARAMS(nidx), wn, qt, threadIdx.x - qt * 128, qtile);
         rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, threadIdx.x - qt * 128, qtile, 2 + qt);
 #endif
         if (rloc == 0) TRACE(EV_QLOADED, gt);

@@ -99,6 +99,12 @@ static_assert(kNQT * 128 == kMBlockRows, "work items are 256-row m-blocks");
 #ifndef DSC_ABL_EX2
 #define DSC_ABL_EX2 0
 #endif
+#ifndef DSC_ABL_TMEM
+#define DSC_ABL_TMEM 0
+#endif
+#ifndef DSC_ABL_SMSP2   // ablation: the softmax warps sharing the MMA warp's sub-partition idle
+#define DSC_ABL_SMSP2 0
+#endif
 constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, this many use exp2_poly2
 // DSC_MMA2 1: two MMA-issuing warps (14: Q tile 0, 15: Q tile 1).  Faster steady tiles,
 // but warp 15 then competes for issue slots with the softmax/rotation warps of SMSP 3 and
@@ -291,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        qtile);
         }
 #endif
-        if (warp_dead || DSC_ABL_SOFTMAX) {   // all 32 rows are padding: their P / O are never used
+        if (warp_dead || DSC_ABL_SOFTMAX || (DSC_ABL_SMSP2 && (warp & 3) == 2)) {   // all 32 rows are padding: their P / O are never used
           mbar_arrive(bar(B_P + sb));
           continue;
         }
@@ -303,9 +309,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool two = nu > 32;
 #endif
         uint32_t r[64];
+#if DSC_ABL_TMEM   // ablation: no TMEM traffic from the softmax (scores fabricated)
+#pragma unroll
+        for (int c = 0; c < 64; ++c) r[c] = __float_as_uint((float)((c * 7 + rloc) & 15) * 0.01f);
+#else
         tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
         if (two) tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
         tmem_wait_ld();
+#endif
         if (warp == 0 && lane == 0) TRACE(EV_L + 0, g);
         const bool any_partial = __any_sync(0xffffffffu, !full);
         if (any_partial) {
@@ -381,9 +392,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         exp_chunk(0);
         if (two) {
           exp_chunk(32);
-          tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          if (!DSC_ABL_TMEM) tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
         } else {
-          tmem_st16(tS, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+          if (!DSC_ABL_TMEM) tmem_st16(tS, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
         }
         lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
         if (warp == 0 && lane == 0) TRACE(EV_L + 4, g);

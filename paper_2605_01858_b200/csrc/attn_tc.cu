@@ -303,11 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_after();
         // one TMEM read of the tile's (up to) 64 scores; invisible columns -> -inf
-#ifdef DSC_DBG_TWO
-        const bool two = true;
-#else
         const bool two = nu > 32;
-#endif
         uint32_t r[64];
 #if DSC_ABL_TMEM   // ablation: no TMEM traffic from the softmax (scores fabricated)
 #pragma unroll
@@ -529,12 +525,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(bar(B_KR + ks), (g / KST) & 1);
         if (lt == 0) TRACE(EV_KR, g);
-#ifdef DSC_DBG_ROTFULL
-        if (!DSC_ABL_ROT)
-#else
         if (!DSC_ABL_ROT && !w.staged && rg * 4 < t.width)   // rows >= width are never read by the MMA;
                                                              // staged K arrives rotated
-#endif
           rotate_rows<1, kKVHalf>(sbase + OFF_K + ks * kKVBytes, rg * 4, c8, rp, cth, sth, kpos, cur,
                                   max(cur_pos, 0));
         fence_proxy_async();
@@ -624,11 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_qk = [&](int qt, int ks, int nu, int buf) {
         const uint64_t da = sdesc(sbase + OFF_Q + qt * kQBytes, 16, 1024);
         const uint64_t db = sdesc(sbase + OFF_K + ks * kKVBytes, 16, 1024);
-#ifdef DSC_DBG_QKFULL
-        const uint32_t iqk = IQK0 | ((uint32_t)(64 >> 3) << 17);
-#else
         const uint32_t iqk = IQK0 | ((uint32_t)(nu >> 3) << 17);
-#endif
         const uint32_t d = tmem + qt * 128 + buf * 64;
         static_assert(kQBytes / 2 / 16 == 1024 && kKVHalf / 16 == 512, "mma_qk8_w block offsets");
         mma_qk8_w(d, da, db, iqk);
@@ -637,11 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_pv = [&](int qt, int vs, bool acc, int nu, int buf) {
         const uint64_t dv = sdesc(sbase + OFF_V + vs * kKVBytes, kKVHalf, 1024);
         const uint32_t d = tmem + 256 + qt * 128, a = tmem + qt * 128 + buf * 64;
-#ifdef DSC_DBG_PVFULL
-        const int nk = 4;
-#else
         const int nk = nu >> 4;
-#endif
         if (nk == 4) {
           mma_pv4_w(d, a, dv, IPV, acc ? 1u : 0u);
         } else {

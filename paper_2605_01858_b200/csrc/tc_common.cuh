@@ -377,11 +377,7 @@ __device__ __forceinline__ TileSeg tile_segments(const PT&, const Item& w, int u
     if (s0 >= w.R) s0 -= w.R;
     t.slot0 = s0;
   }
-#ifdef DSC_FULLW
-  t.width = kTileN;
-#else
   t.width = (valid + 15) & ~15;
-#endif
   return t;
 }
 __device__ __forceinline__ int seg_pos(const TileSeg& t, int r) {

@@ -49,16 +49,20 @@ constexpr int kQBytes = 128 * 128 * 2;        // one 128-row Q tile (2 x 64-colu
 constexpr int kKT = kTileN;                   // keys per K/V tile
 constexpr int kKVHalf = kKT * 128;            // bytes of one 64-column SW128 block of a K/V tile
 constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
+#ifndef DSC_QDB   // double-buffered Q tiles (next item's Q loaded + rotated during the current item)
+#define DSC_QDB 0
+#endif
 #ifndef DSC_KST
-#define DSC_KST 6
+#define DSC_KST (DSC_QDB ? 3 : 6)
 #endif
 #ifndef DSC_VST
-#define DSC_VST 4
+#define DSC_VST (DSC_QDB ? 3 : 4)
 #endif
 constexpr int KST = DSC_KST;                  // K stages (raw -> rotated in place)
 constexpr int VST = DSC_VST;                  // V stages
+constexpr int kQBufs = DSC_QDB ? 2 : 1;       // Q tile sets (double-buffered: next item's Q prepared early)
 constexpr int OFF_Q = 0;
-constexpr int OFF_K = OFF_Q + kNQT * kQBytes;
+constexpr int OFF_K = OFF_Q + kQBufs * kNQT * kQBytes;
 constexpr int OFF_V = OFF_K + KST * kKVBytes;
 constexpr int OFF_BAR = OFF_V + VST * kKVBytes;
 // barriers (8 B each): Q ready [qt] | K raw landed | K rotated | K free | V landed | V free |
@@ -66,7 +70,7 @@ constexpr int OFF_BAR = OFF_V + VST * kKVBytes;
 // Every barrier a waiter may lag is per buffer parity, so no waiter is ever two phases
 // behind (the parity test of mbarrier.try_wait cannot tell phase k from phase k+2): with S
 // prefetched two tiles ahead, PV(g-1) may still be pending when the softmax finishes tile g.
-constexpr int B_Q = 0, B_KR = 2, B_KF = B_KR + KST, B_KE = B_KF + KST, B_VF = B_KE + KST, B_VE = B_VF + VST,
+constexpr int B_Q = 0, B_KR = 2 * kQBufs, B_KF = B_KR + KST, B_KE = B_KF + KST, B_VF = B_KE + KST, B_VE = B_VF + VST,
               B_S = B_VE + VST, B_P = B_S + 4, B_O = B_P + 4, B_OF = B_O + 4, B_N = B_OF + 2;
 // setmaxnreg budget per warpgroup: 2*softmax + rotation + copy/MMA <= 512 (x 128 threads)
 constexpr int kRegSoftmax = 144, kRegRotate = 136, kRegCopy = 88;
@@ -112,15 +116,9 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 #ifndef DSC_MMA2
 #define DSC_MMA2 0
 #endif
-// DSC_QPREF: L2 prefetch of the next item's Q rows at item start; DSC_QREG: Q rows loaded and
-// rotated in registers (else cp.async + in-smem rotation).  Both measured slower on c5
-// (QREG 11.3K vs 12.8K frames/s: the inlined row path raises the softmax warps' register
-// pressure), so both are off.
+// DSC_QPREF: L2 prefetch of the next item's Q rows at item start (measured slower, off)
 #ifndef DSC_QPREF
 #define DSC_QPREF 0
-#endif
-#ifndef DSC_QREG
-#define DSC_QREG 0
 #endif
 // DSC_SORDER 1: MMA order PV0(g) S0(g+2) PV1(g) S1(g+2) (else PV0 PV1 S0 S1)
 #ifndef DSC_SORDER
@@ -173,8 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           : (ITEM_B(I) ? (I) - na : (I)))
 
   if (threadIdx.x == 0) {
-    mbar_init(bar(B_Q + 0), 128);
-    mbar_init(bar(B_Q + 1), 128);
+    for (int i = 0; i < 2 * kQBufs; ++i) mbar_init(bar(B_Q + i), 128);
     for (int i = 0; i < KST; ++i) {
       mbar_init(bar(B_KR + i), 1);
       mbar_init(bar(B_KF + i), 128);
@@ -228,18 +225,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sl2 = p.scale_log2;
     const float2 scale2 = make_float2(sl2, sl2);
 
-    const uint32_t qtile = sbase + OFF_Q + qt * kQBytes;
+    const int lt = threadIdx.x - qt * 128;           // 0..127 within the warpgroup
+    auto qtile_of = [&](int kk) { return sbase + OFF_Q + (uint32_t)(((DSC_QDB ? (kk & 1) : 0) * 2 + qt) * kQBytes); };
+    auto qbar_of = [&](int kk) { return bar(B_Q + (DSC_QDB ? (kk & 1) : 0) * 2 + qt); };
     if (blockIdx.x < (unsigned)n_role_items) {       // Q tile of the first item
       const AttnParams& p0 = ITEM_PARAMS((int)blockIdx.x);
       const Item w0 = decode_item(p0, ITEM_LOCAL((int)blockIdx.x));
-#if DSC_QREG
-      load_q_row_rotated(p0, w0, qt, rloc, qtile);
-      fence_proxy_async();
-#else
-      issue_q_tile(p0, w0, qt, threadIdx.x - qt * 128, qtile);
-      rotate_q_tile(p0, w0, qt, threadIdx.x - qt * 128, qtile, 2 + qt);
-#endif
-      mbar_arrive(bar(B_Q + qt));
+      issue_q_tile(p0, w0, qt, lt, qtile_of(0));
+      rotate_q_tile(p0, w0, qt, lt, qtile_of(0), 2 + qt);
+      mbar_arrive(qbar_of(0));
     }
     int gt = 0, kk = 0;
     for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x, ++kk) {
@@ -247,6 +241,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Item w = decode_item(p, ITEM_LOCAL(idx));
       const int A = w.A;
       const int n = w.n_tiles;
+      const int nidx = idx + gridDim.x;
+      const bool has_next = nidx < n_role_items;
+      Item wn;
+      if (has_next) wn = decode_item(ITEM_PARAMS(nidx), ITEM_LOCAL(nidx));
+#if DSC_QDB
+      // the other Q buffer held item kk-1's Q, whose last S we have consumed: the next
+      // item's Q rows are fetched now and rotated after this item's first tile
+      if (has_next) issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1));
+#endif
       const int rglob = w.m0 + qt * 128 + rloc;
       const bool valid_row = rglob < w.rows_total;
       const int qi = valid_row ? rglob / p.grp : 0;
@@ -288,14 +291,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool full = (c_lo == 0) && (c_hi == kKT);
         mbar_wait(bar(B_S + sb), (g >> 1) & 1);
         if (rloc == 0) TRACE(EV_S0 + qt, g);
-#if DSC_QEARLY
+#if DSC_QDB
+        if (jj == 1 && has_next) {   // next item's Q: rotate in place and publish (every warp takes part)
+          rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1), 2 + qt);
+          mbar_arrive(qbar_of(kk + 1));
+        }
+#elif DSC_QEARLY
         // S(last) is in: the MMA is done reading this Q tile, so the next item's Q rows are
         // fetched now and land while the last tile's softmax runs
-        if (jj == n - 1 && idx + (int)gridDim.x < n_role_items) {
-          const int nidx = idx + gridDim.x;
-          issue_q_tile(ITEM_PARAMS(nidx), decode_item(ITEM_PARAMS(nidx), ITEM_LOCAL(nidx)), qt, threadIdx.x - qt * 128,
-                       qtile);
-        }
+        if (jj == n - 1 && has_next) issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1));
 #endif
         if (warp_dead || DSC_ABL_SOFTMAX || (DSC_ABL_SMSP2 && (warp & 3) == 2)) {   // all 32 rows are padding: their P / O are never used
           mbar_arrive(bar(B_P + sb));
@@ -401,23 +405,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) TRACE(EV_PW0 + warp, g);
       }
       gt += n;
+#if DSC_QDB
+      if (has_next && n < 2) {     // a one-tile item never reached the in-loop rotation point
+        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1), 2 + qt);
+        mbar_arrive(qbar_of(kk + 1));
+      }
+#elif DSC_QFIRST
       // S_qt of the last tile has been read: the MMA is done with Q tile qt, so the next
-      // item's Q tile is fetched now (overlapping this item's epilogue)
-      const int nidx = idx + gridDim.x;
-      Item wn;
-      if (nidx < n_items) wn = decode_item(ITEM_PARAMS(nidx), ITEM_LOCAL(nidx));
-#if DSC_QFIRST
-      if (nidx < n_items) {
+      // item's Q tile is fetched (unless already issued) and published before the epilogue
+      if (has_next) {
         if (rloc == 0) TRACE(EV_QSTART, gt);
-#if DSC_QREG
-        load_q_row_rotated(ITEM_PARAMS(nidx), wn, qt, rloc, qtile);
-        fence_proxy_async();
-#else
-        if (!DSC_QEARLY || n == 0) issue_q_tile(ITEM_PARAMS(nidx), wn, qt, threadIdx.x - qt * 128, qtile);
-        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, threadIdx.x - qt * 128, qtile, 2 + qt);
-#endif
+        if (!DSC_QEARLY || n == 0) issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1));
+        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1), 2 + qt);
         if (rloc == 0) TRACE(EV_QLOADED, gt);
-        mbar_arrive(bar(B_Q + qt));
+        mbar_arrive(qbar_of(kk + 1));
         if (rloc == 0) TRACE(EV_QDONE, gt);
       }
 #endif
@@ -462,11 +463,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (rloc == 0) TRACE(EV_EPI1, gt);
-#if !DSC_QFIRST
-      if (nidx < n_items) {
-        issue_q_tile(ITEM_PARAMS(nidx), wn, qt, threadIdx.x - qt * 128, qtile);
-        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, threadIdx.x - qt * 128, qtile, 2 + qt);
-        mbar_arrive(bar(B_Q + qt));
+#if !DSC_QDB && !DSC_QFIRST
+      if (has_next) {
+        issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1));
+        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1), 2 + qt);
+        mbar_arrive(qbar_of(kk + 1));
         if (rloc == 0) TRACE(EV_QDONE, gt);
       }
 #endif
@@ -608,13 +609,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int q_lo = DSC_MMA2 ? warp - 14 : 0, q_hi = DSC_MMA2 ? warp - 13 : 2;
       if (!DSC_MMA2 && warp == 15) goto mma_done;
       {
+      int qbuf = 0;                                          // Q tile set of the current item
       constexpr uint32_t IQK0 = idesc_bf16(128, 0, 0, 0);    // S = Q K^T, both K-major; N = tile width
       constexpr uint32_t IPV = idesc_bf16(128, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
       // fully unrolled: the descriptors are formed once per call and advanced by
       // immediates (16-element K steps: +32 B inside a 128 B swizzle row, then the next
       // 64-column block), so each tcgen05.mma costs a few uniform-datapath instructions
       auto issue_qk = [&](int qt, int ks, int nu, int buf) {
-        const uint64_t da = sdesc(sbase + OFF_Q + qt * kQBytes, 16, 1024);
+        const uint64_t da = sdesc(sbase + OFF_Q + (qbuf * 2 + qt) * kQBytes, 16, 1024);
         const uint64_t db = sdesc(sbase + OFF_K + ks * kKVBytes, 16, 1024);
         const uint32_t iqk = IQK0 | ((uint32_t)(nu >> 3) << 17);
         const uint32_t d = tmem + qt * 128 + buf * 64;
@@ -656,7 +658,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const ItemGeo p = item_geo(pa, pb, ITEM_B(idx));
         const Item w = decode_item(p, ITEM_LOCAL(idx));
         const int n = w.n_tiles;
-        for (int qt = q_lo; qt < q_hi; ++qt) MWAIT(bar(B_Q + qt), kk & 1);
+        qbuf = DSC_QDB ? (kk & 1) : 0;
+        for (int qt = q_lo; qt < q_hi; ++qt) MWAIT(bar(B_Q + qbuf * 2 + qt), DSC_QDB ? ((kk >> 1) & 1) : (kk & 1));
         if (kk == 0 && lane == 0 && q_lo == 0) TRACE(EV_Q, 0);
         if (n > 0) issue_s(p, w, gt, w.t_begin);
         if (n > 1) issue_s(p, w, gt + 1, w.t_begin + 1);

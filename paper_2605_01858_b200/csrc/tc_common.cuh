@@ -523,52 +523,5 @@ __device__ __forceinline__ void rotate_q_tile(const AttnParams& p, const Item& w
   fence_proxy_async();
 }
 
-// Q row rloc of Q tile qt of an item, rotated at its query id in registers and stored to the
-// SW128 smem tile (one thread per row: split-half pairs (f, f+64) live in the same thread).
-// Replaces the cp.async + in-smem rotation at item switches (no named barrier, one pass).
-// The caller fences (proxy.async) and arrives on the Q barrier.
-__device__ __forceinline__ void load_q_row_rotated(const AttnParams& p, const Item& w, int qt, int rloc,
-                                                   uint32_t qtile) {
-  const int rglob = w.m0 + qt * 128 + rloc;
-  const bool ok = rglob < w.rows_total;
-  const int qi = ok ? rglob / p.grp : 0, hh = ok ? rglob % p.grp : 0;
-  const int pos = p.q_pos0 + qi;
-  const uint4* __restrict__ src = reinterpret_cast<const uint4*>(
-      reinterpret_cast<const __nv_bfloat16*>(p.q) + (((long long)w.pp * p.n_q + qi) * p.Hq + w.g * p.grp + hh) * 128);
-  const float4* __restrict__ tab = p.rope_pairs + (long long)pos * 32;
-  if (ok && p.dbg_pos != nullptr && w.pp == 0 && w.g == 0 && hh == 0) p.dbg_pos[p.A + p.R + p.dbg_M + qi] = pos;
-  const uint32_t rowb = qtile + (uint32_t)rloc * 128;
-#pragma unroll
-  for (int c = 0; c < 8; c += 2) {          // 16-byte chunks c, c+1 (cols 8c..) and their partners c+8, c+9
-    uint4 lo[2], hi[2];
-    float4 t[8];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      lo[k] = ok ? src[c + k] : make_uint4(0, 0, 0, 0);
-      hi[k] = ok ? src[c + k + 8] : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) t[j] = tab[4 * c + j];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      uint32_t ol[4], oh[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float4 tt = t[4 * k + j];
-        const float2 cs = make_float2(tt.x, tt.y), sn = make_float2(tt.z, tt.w);
-        const float2 av = bf2(get_w(lo[k], j)), bv = bf2(get_w(hi[k], j));
-        const float2 yl = __ffma2_rn(av, cs, __fmul2_rn(make_float2(-bv.x, -bv.y), sn));   // a cos - b sin
-        const float2 yh = __ffma2_rn(av, sn, __fmul2_rn(bv, cs));                        // a sin + b cos
-        ol[j] = pack_bf16(yl.x, yl.y);
-        oh[j] = pack_bf16(yh.x, yh.y);
-      }
-      const int ch = c + k;
-      const uint32_t sw = (uint32_t)(((ch ^ (rloc & 7)) & 7) << 4);
-      sts128(rowb + sw, make_uint4(ol[0], ol[1], ol[2], ol[3]));
-      sts128(rowb + 16384 + sw, make_uint4(oh[0], oh[1], oh[2], oh[3]));
-    }
-  }
-}
-
 }  // namespace tcc
 }  // namespace dsc

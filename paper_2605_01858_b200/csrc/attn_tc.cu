@@ -106,6 +106,9 @@ static_assert(kNQT * 128 == kMBlockRows, "work items are 256-row m-blocks");
 #ifndef DSC_ABL_TMEM
 #define DSC_ABL_TMEM 0
 #endif
+#ifndef DSC_ABL_SWITCH   // ablation: item switches without the Q load/rotation (bit 0) / the O epilogue (bit 1)
+#define DSC_ABL_SWITCH 0
+#endif
 #ifndef DSC_ABL_SMSP2   // ablation: the softmax warps sharing the MMA warp's sub-partition idle
 #define DSC_ABL_SMSP2 0
 #endif
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #elif DSC_QEARLY
         // S(last) is in: the MMA is done reading this Q tile, so the next item's Q rows are
         // fetched now and land while the last tile's softmax runs
-        if (jj == n - 1 && has_next) issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1));
+        if (jj == n - 1 && has_next && !(DSC_ABL_SWITCH & 1)) issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1));
 #endif
         if (warp_dead || DSC_ABL_SOFTMAX || (DSC_ABL_SMSP2 && (warp & 3) == 2)) {   // all 32 rows are padding: their P / O are never used
           mbar_arrive(bar(B_P + sb));
@@ -415,8 +418,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // item's Q tile is fetched (unless already issued) and published before the epilogue
       if (has_next) {
         if (rloc == 0) TRACE(EV_QSTART, gt);
-        if (!DSC_QEARLY || n == 0) issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1));
-        rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1), 2 + qt);
+        if (!(DSC_ABL_SWITCH & 1)) {
+          if (!DSC_QEARLY || n == 0) issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1));
+          rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1), 2 + qt);
+        }
         if (rloc == 0) TRACE(EV_QLOADED, gt);
         mbar_arrive(qbar_of(kk + 1));
         if (rloc == 0) TRACE(EV_QDONE, gt);
@@ -432,6 +437,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long orow = ((long long)w.pp * p.n_q + qi) * p.Hq + h;
 #pragma unroll 1
       for (int hf = 0; hf < 2; ++hf) {
+        if (DSC_ABL_SWITCH & 2) {   // ablation: no O read-out / stores
+          if (hf == 1) { tc_fence_before(); mbar_arrive(bar(B_OF + qt)); }
+          continue;
+        }
         uint32_t o[64];
         tmem_ld32(tO + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
         tmem_ld32(tO + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
@@ -442,15 +451,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!valid_row) continue;
         if (p.n_splits == 1) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) + orow * 128 + 64 * hf);
+          // 32-byte stores (STG.256): each one fills a whole L2 sector of this thread's row
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) + orow * 128 + 64 * hf;
 #pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            uint4 q;
-            q.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
-            q.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
-            q.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
-            q.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
-            dst[v] = q;
+          for (int v = 0; v < 4; ++v) {
+            uint32_t q[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              q[j] = pack_bf16(__uint_as_float(o[16 * v + 2 * j]) * inv, __uint_as_float(o[16 * v + 2 * j + 1]) * inv);
+            stg256(dst + 16 * v, q);
           }
         } else {
           const long long rows = (long long)p.P * p.n_q * p.Hq;

@@ -49,9 +49,17 @@ constexpr int kQBytes = 128 * 128 * 2;        // one 128-row Q tile (2 x 64-colu
 constexpr int kKT = kTileN;                   // keys per K/V tile
 constexpr int kKVHalf = kKT * 128;            // bytes of one 64-column SW128 block of a K/V tile
 constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
-#ifndef DSC_QDB   // double-buffered Q tiles (next item's Q loaded + rotated during the current item)
-#define DSC_QDB 0
+// DSC_QROT: the rotation warpgroup loads + rotates every item's Q tiles (into the second Q
+// buffer, a whole item ahead), so item switches cost the softmax warpgroups only their
+// epilogue; staged build items need no K rotation, so their K tiles go straight from the
+// copy warp to the MMA (the rotation warpgroup is free for Q during builds)
+#ifndef DSC_QROT
+#define DSC_QROT 1
 #endif
+#ifndef DSC_QDB   // double-buffered Q tiles (next item's Q loaded + rotated during the current item)
+#define DSC_QDB DSC_QROT
+#endif
+static_assert(!DSC_QROT || DSC_QDB, "DSC_QROT needs the Q double buffer");
 #ifndef DSC_KST
 #define DSC_KST (DSC_QDB ? 3 : 6)
 #endif
@@ -71,7 +79,7 @@ constexpr int OFF_BAR = OFF_V + VST * kKVBytes;
 // behind (the parity test of mbarrier.try_wait cannot tell phase k from phase k+2): with S
 // prefetched two tiles ahead, PV(g-1) may still be pending when the softmax finishes tile g.
 constexpr int B_Q = 0, B_KR = 2 * kQBufs, B_KF = B_KR + KST, B_KE = B_KF + KST, B_VF = B_KE + KST, B_VE = B_VF + VST,
-              B_S = B_VE + VST, B_P = B_S + 4, B_O = B_P + 4, B_OF = B_O + 4, B_N = B_OF + 2;
+              B_S = B_VE + VST, B_P = B_S + 4, B_O = B_P + 4, B_OF = B_O + 4, B_QE = B_OF + 2, B_N = B_QE + 2;
 // setmaxnreg budget per warpgroup: 2*softmax + rotation + copy/MMA <= 512 (x 128 threads)
 constexpr int kRegSoftmax = 144, kRegRotate = 136, kRegCopy = 88;
 static_assert(2 * kRegSoftmax + kRegRotate + kRegCopy <= 512, "setmaxnreg budget exceeds the 64K register file");
@@ -190,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(B_O + i), 1);
     }
     for (int i = 0; i < 2; ++i) mbar_init(bar(B_OF + i), 128);
+    for (int i = 0; i < 2; ++i) mbar_init(bar(B_QE + i), 1);   // Q buffer i free (MMA commit after an item)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
   }
@@ -231,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lt = threadIdx.x - qt * 128;           // 0..127 within the warpgroup
     auto qtile_of = [&](int kk) { return sbase + OFF_Q + (uint32_t)(((DSC_QDB ? (kk & 1) : 0) * 2 + qt) * kQBytes); };
     auto qbar_of = [&](int kk) { return bar(B_Q + (DSC_QDB ? (kk & 1) : 0) * 2 + qt); };
-    if (blockIdx.x < (unsigned)n_role_items) {       // Q tile of the first item
+    if (!DSC_QROT && blockIdx.x < (unsigned)n_role_items) {       // Q tile of the first item
       const AttnParams& p0 = ITEM_PARAMS((int)blockIdx.x);
       const Item w0 = decode_item(p0, ITEM_LOCAL((int)blockIdx.x));
       issue_q_tile(p0, w0, qt, lt, qtile_of(0));
@@ -248,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool has_next = nidx < n_role_items;
       Item wn;
       if (has_next) wn = decode_item(ITEM_PARAMS(nidx), ITEM_LOCAL(nidx));
-#if DSC_QDB
+#if DSC_QDB && !DSC_QROT
       // the other Q buffer held item kk-1's Q, whose last S we have consumed: the next
       // item's Q rows are fetched now and rotated after this item's first tile
       if (has_next) issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1));
@@ -294,7 +303,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool full = (c_lo == 0) && (c_hi == kKT);
         mbar_wait(bar(B_S + sb), (g >> 1) & 1);
         if (rloc == 0) TRACE(EV_S0 + qt, g);
-#if DSC_QDB
+#if DSC_QROT
+#elif DSC_QDB
         if (jj == 1 && has_next) {   // next item's Q: rotate in place and publish (every warp takes part)
           rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1), 2 + qt);
           mbar_arrive(qbar_of(kk + 1));
@@ -408,7 +418,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) TRACE(EV_PW0 + warp, g);
       }
       gt += n;
-#if DSC_QDB
+#if DSC_QROT
+#elif DSC_QDB
       if (has_next && n < 2) {     // a one-tile item never reached the in-loop rotation point
         rotate_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1), 2 + qt);
         mbar_arrive(qbar_of(kk + 1));
@@ -496,12 +507,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       cth[j] = make_float2(t.x, t.y);
       sth[j] = make_float2(t.z, t.w);
     }
+#if DSC_QROT
+    // Q tiles (both) of item k into Q buffer k & 1; the buffer's previous item (k - 2) must be
+    // done with it (its last QK^T MMA committed to B_QE)
+    auto prep_q = [&](int k, int qidx) {
+      const uint32_t qb = (uint32_t)(k & 1);
+      if (k >= 2) mbar_wait(bar(B_QE + qb), ((k - 2) >> 1) & 1);
+      const AttnParams& pq = ITEM_PARAMS(qidx);
+      const Item wq = decode_item(pq, ITEM_LOCAL(qidx));
+#pragma unroll 1
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t qtile = sbase + OFF_Q + (qb * 2 + q) * kQBytes;
+        issue_q_tile(pq, wq, q, lt, qtile);
+        rotate_q_tile(pq, wq, q, lt, qtile, 6);
+        mbar_arrive(bar(B_Q + qb * 2 + q));
+      }
+    };
+    if (blockIdx.x < (unsigned)n_role_items) prep_q(0, blockIdx.x);
+#endif
     int gt = 0, kk = 0;
     for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x, ++kk) {
       const AttnParams& p = ITEM_PARAMS(idx);
       const Item w = decode_item(p, ITEM_LOCAL(idx));
       const int A = p.A;
       const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
+#if DSC_QROT
+      const int nidx_q = idx + gridDim.x;
+      const bool q_next = nidx_q < n_role_items;
+      if (w.staged) {   // no K to rotate: the MMA waits on the copy barrier; prepare the next Q
+        if (q_next) prep_q(kk + 1, nidx_q);
+        gt += w.n_tiles;
+        continue;
+      }
+#endif
       // ---- K tiles of this item; the table entry of each tile's first row is fetched
       // one tile ahead so the L2 latency is off the rotation's critical path
       int kpos[4];
@@ -542,6 +580,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async();
         mbar_arrive(bar(B_KF + ks));
         if (lt == 0) TRACE(EV_KDONE, g);
+#if DSC_QROT
+        if (jj == min(1, w.n_tiles - 1) && q_next) prep_q(kk + 1, nidx_q);   // after the item's first K tiles
+#endif
         if (dbg && c8 == 0) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -553,6 +594,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+#if DSC_QROT
+      if (w.n_tiles == 0 && q_next) prep_q(kk + 1, nidx_q);
+#endif
       gt += w.n_tiles;
     }
   } else {
@@ -651,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_s = [&](const ItemGeo& p, const Item& w, int g, int u) {
         const int ks = g % KST, buf = g & 1;
         const int nu = tile_segments(p, w, u).width;
-        MWAIT(bar(B_KF + ks), (g / KST) & 1);
+        MWAIT(bar((DSC_QROT && w.staged ? B_KR : B_KF) + ks), (g / KST) & 1);
         if (lane == 0 && q_lo == 0) TRACE(EV_KF, g);
         tc_fence_after();
 #pragma unroll 1
@@ -688,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             MWAIT(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
             if (jj == 0 && kk > 0) MWAIT(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
           }
-          if (more) MWAIT(bar(B_KF + ks2), ((g + 2) / KST) & 1);
+          if (more) MWAIT(bar((DSC_QROT && w.staged ? B_KR : B_KF) + ks2), ((g + 2) / KST) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int qt = q_lo; qt < q_hi; ++qt) issue_pv(qt, vs, jj > 0, nu, buf);
@@ -721,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) TRACE(EV_PVI + qt, g);
             if (more) {
               if (qt == q_lo) {
-                MWAIT(bar(B_KF + ks2), ((g + 2) / KST) & 1);
+                MWAIT(bar((DSC_QROT && w.staged ? B_KR : B_KF) + ks2), ((g + 2) / KST) & 1);
                 tc_fence_after();
               }
               issue_qk(qt, ks2, nu2, buf);
@@ -746,6 +790,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (jj + 2 < n) issue_s(p, w, g + 2, w.t_begin + jj + 2);
 #endif
         }
+        if (DSC_QROT) mma_commit_w(bar(B_QE + qbuf));   // Q buffer of this item free once its MMAs are done
         gt += n;
       }
       // drain: the last V-free commit tracks every MMA of this CTA

@@ -351,7 +351,10 @@ dscache_status prep_build(dscache_t h, int32_t lb, int32_t lc, const void* q_ins
   // rotated at the build ids 0.. (the window is re-read by every m-block; rotating it once
   // instead of per m-block removes the RoPE work from the build items).  The debug id
   // export records ids where the kernel rotates, so debug runs keep the ring path.
-  if (h->impl_build == DSCACHE_IMPL_TC && h->stage_k && !h->dbg_build) {
+  // Small launches (fewer build items than two waves of SMs, e.g. one stream x one layer)
+  // are latency-bound: the extra staging launch costs more than the RoPE it saves there.
+  const long long build_items = (long long)p.P * p.Hkv * p.n_mblocks;
+  if (h->impl_build == DSCACHE_IMPL_TC && h->stage_k && !h->dbg_build && build_items >= 2LL * h->num_sms) {
     dsc::StageParams sp{};
     sp.sink_k = h->sink_k; sp.sink_v = h->sink_v; sp.ring_k = h->ring_k; sp.ring_v = h->ring_v;
     sp.stage_k = h->stage_k; sp.stage_v = h->stage_v; sp.rope_pairs = p.rope_pairs;

@@ -201,6 +201,27 @@ dscache_status dscache_step(dscache_t h, int32_t layer_begin, int32_t layer_coun
                             const void* q, const void* k_self, const void* v_self, int32_t n_q, void* o,
                             void* stream);
 
+/* Context-parallel building blocks: the attend of dscache_attend split
+ * over its keys.  The keys of every (stream, layer, kv head, m-block) work item -- sink and
+ * self rows, then the [past | instant] window in 64-key tiles, all with their full-context
+ * ids -- are cut into n_parts contiguous tile ranges; this call computes
+ * range `part` only and writes the partial softmax attention over it:
+ *   o_part   : DEVICE fp32 [S][layer_count][n_q][Hq][d], O_part = sum_j p_j v_j / sum_j p_j
+ *   lse_part : DEVICE fp32 [S][layer_count][n_q][Hq], log2 of sum_j 2^(s_j log2e / sqrt(d))
+ * Softmax attention is invariant to how the key set is split, so combining the n_parts
+ * partials (dscache_combine_partials, on any rank after an all-gather) equals
+ * dscache_attend up to rounding.  tcgen05 path only (E_CONFIG otherwise); E_ARG if a part
+ * would get no keys or n_q is out of range. */
+dscache_status dscache_attend_partial(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                                      const void* q, const void* k_self, const void* v_self, int32_t n_q,
+                                      int32_t part, int32_t n_parts, float* o_part, float* lse_part,
+                                      void* stream);
+/* O = sum_r 2^(lse_r - M) O_r / sum_r 2^(lse_r - M), M = max_r lse_r (partials with
+ * lse = -inf weigh 0).  o_parts: DEVICE fp32 [n_parts][rows][d], lse_parts: [n_parts][rows],
+ * o: DEVICE bf16 [rows][d] (rows = S*layer_count*n_q*Hq for attend partials). */
+dscache_status dscache_combine_partials(dscache_t h, int32_t n_parts, int64_t rows, const float* o_parts,
+                                        const float* lse_parts, void* o, void* stream);
+
 /* Host counters of `layer` (closed form of Eq. 3/5/6 at the latest append). */
 dscache_status dscache_get_state(dscache_t h, int32_t layer, dscache_state* out);
 

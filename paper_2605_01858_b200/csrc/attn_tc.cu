@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(bar(B_OF + qt));      // O_qt may be overwritten by the next item
         }
         if (!valid_row) continue;
-        if (p.n_splits == 1) {
+        if (p.n_splits == 1 && p.split_only < 0) {
           // 32-byte stores (STG.256): each one fills a whole L2 sector of this thread's row
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) + orow * 128 + 64 * hf;
 #pragma unroll
@@ -474,12 +474,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
           const long long rows = (long long)p.P * p.n_q * p.Hq;
-          float4* dst = reinterpret_cast<float4*>(p.ws_o + ((long long)w.sp * rows + orow) * 128 + 64 * hf);
+          const long long slot = p.split_only >= 0 ? 0 : w.sp;
+          float4* dst = reinterpret_cast<float4*>(p.ws_o + (slot * rows + orow) * 128 + 64 * hf);
 #pragma unroll
           for (int v = 0; v < 16; ++v)
             dst[v] = make_float4(__uint_as_float(o[4 * v]) * inv, __uint_as_float(o[4 * v + 1]) * inv,
                                  __uint_as_float(o[4 * v + 2]) * inv, __uint_as_float(o[4 * v + 3]) * inv);
-          if (hf == 0) p.ws_lse[(long long)w.sp * rows + orow] = lsum > 0.f ? m + __log2f(lsum) : -INFINITY;
+          if (hf == 0) p.ws_lse[slot * rows + orow] = lsum > 0.f ? m + __log2f(lsum) : -INFINITY;
         }
       }
       if (rloc == 0) TRACE(EV_EPI1, gt);
@@ -839,7 +840,9 @@ cudaError_t make_stage_tmap(CUtensorMap* map, void* base, unsigned long long row
   return make_ring_tmap(map, base, rows);   // same geometry: [rows][128] bf16, box 64 x kTileN, SW128
 }
 
-static long long tc_items(const AttnParams& p) { return (long long)p.P * p.Hkv * p.n_mblocks * p.n_splits; }
+static long long tc_items(const AttnParams& p) {
+  return (long long)p.P * p.Hkv * p.n_mblocks * (p.split_only >= 0 ? 1 : p.n_splits);
+}
 
 cudaError_t launch_attn_tc2(const AttnParams& pa, const AttnParams* pb, cudaStream_t st) {
   static bool configured = false;

@@ -147,7 +147,7 @@ void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
   p.tmap_k = h->tmap_k; p.tmap_v = h->tmap_v;
   p.staged = 0;
   p.trace = h->trace; p.ntrace_cta = h->ntrace;
-  p.n_splits = 1; p.tiles_per_split = 1 << 30;
+  p.n_splits = 1; p.tiles_per_split = 1 << 30; p.split_only = -1;
 }
 
 dscache_status grow_ws(dscache_t h, size_t bytes) {
@@ -169,7 +169,7 @@ dscache_status run_attention(dscache_t h, dsc::AttnParams& p, int impl, int kind
   if (impl == DSCACHE_IMPL_TC) e = dsc::launch_attn_tc(p, st);
   else e = dsc::launch_attn_simt(p, st);
   h->launches++;
-  if (e == cudaSuccess && p.n_splits > 1) { e = dsc::launch_combine(p, st); h->launches++; }
+  if (e == cudaSuccess && p.n_splits > 1 && p.split_only < 0) { e = dsc::launch_combine(p, st); h->launches++; }
   if (h->prof) {
     cudaEventRecord(e1, st);
     h->pending.push_back({e0, e1, kind});
@@ -477,6 +477,44 @@ dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q
 dscache_status dscache_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                               const void* v_self, int32_t n_self, int32_t n_q, void* o, void* stream) {
   return attend_common(h, lb, lc, q, k_self, v_self, n_self, n_q, o, stream, false);
+}
+
+dscache_status dscache_attend_partial(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                                      const void* v_self, int32_t n_q, int32_t part, int32_t n_parts, float* o_part,
+                                      float* lse_part, void* stream) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
+  if (n_parts < 1 || part < 0 || part >= n_parts) return fail(DSCACHE_E_ARG, "need 0 <= part < n_parts");
+  if (!o_part || !lse_part) return fail(DSCACHE_E_ARG, "null o_part/lse_part");
+  if (h->impl_attend != DSCACHE_IMPL_TC)
+    return fail(DSCACHE_E_CONFIG, "attend_partial runs on the tcgen05 path (bf16, d=128, split-half RoPE)");
+  dsc::AttnParams p{};
+  dscache_status s = prep_attend(h, lb, lc, q, k_self, v_self, n_q, n_q, /*o*/ o_part, false, p);
+  if (s != DSCACHE_OK) return s;
+  // the key tiles of every item (sink/self tiles, then logical window tiles), cut into n_parts
+  // contiguous ranges; part `part` is computed here
+  const int BN = dsc::kTileN;
+  const int tiles = (p.A + n_q + BN - 1) / BN + (p.ring_count + BN - 1) / BN;
+  const int tps = (tiles + n_parts - 1) / n_parts;
+  if ((long long)(n_parts - 1) * tps >= tiles)
+    return fail(DSCACHE_E_ARG, "n_parts = " + std::to_string(n_parts) + " leaves a part without keys (" +
+                                   std::to_string(tiles) + " key tiles)");
+  p.n_splits = n_parts; p.tiles_per_split = tps; p.split_only = part;
+  p.ws_o = o_part; p.ws_lse = lse_part;
+  DeviceGuard dg(h->cfg.device);
+  return run_attention(h, p, h->impl_attend, 1, (cudaStream_t)stream);
+}
+
+dscache_status dscache_combine_partials(dscache_t h, int32_t n_parts, int64_t rows, const float* o_parts,
+                                        const float* lse_parts, void* o, void* stream) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  if (n_parts < 1 || rows < 1 || !o_parts || !lse_parts || !o) return fail(DSCACHE_E_ARG, "bad combine arguments");
+  if (h->cfg.dtype != DSCACHE_DTYPE_BF16 || h->cfg.head_dim != 128)
+    return fail(DSCACHE_E_CONFIG, "combine_partials writes bf16 rows of d = 128");
+  DeviceGuard dg(h->cfg.device);
+  DSC_CUDA(dsc::launch_combine_partials(n_parts, rows, h->cfg.head_dim, o_parts, lse_parts, o, (cudaStream_t)stream));
+  h->launches++;
+  return DSCACHE_OK;
 }
 
 dscache_status dscache_step(dscache_t h, int32_t lb, int32_t lc, const void* k_frame, const void* v_frame,

@@ -43,6 +43,7 @@ struct AttnParams {
   float scale_log2;                          // log2(e) / sqrt(d)
   // split-KV (attend): partial (O/l, log2-sum-exp) per split
   int n_splits, tiles_per_split;
+  int split_only;                            // >= 0: compute only this split; its partial goes to ws_o/ws_lse slot 0
   float* ws_o;                               // [n_splits][P][n_q][Hq][d]
   float* ws_lse;                             // [n_splits][P][n_q][Hq]
   // tcgen05 kernel work decomposition
@@ -93,6 +94,9 @@ cudaError_t launch_attn_tc(const AttnParams& p, cudaStream_t st);
 // one persistent launch over the items of pa (first) and then those of *pb (same handle)
 cudaError_t launch_attn_tc2(const AttnParams& pa, const AttnParams* pb, cudaStream_t st);
 cudaError_t launch_combine(const AttnParams& p, cudaStream_t st);
+// O (bf16 [rows][d]) = merge of n fp32 partials o_parts [n][rows][d] with log2-sum-exps lse [n][rows]
+cudaError_t launch_combine_partials(int n, long long rows, int d, const float* o_parts, const float* lse, void* o,
+                                    cudaStream_t st);
 int attn_tc_smem_bytes();
 // encode the 2-D ring tensor map (bf16, d = 128) used by the tcgen05 kernel
 cudaError_t make_ring_tmap(CUtensorMap* map, void* base, unsigned long long rows);

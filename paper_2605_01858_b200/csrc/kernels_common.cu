@@ -359,6 +359,14 @@ __global__ void __launch_bounds__(128) combine_kernel(AttnParams p) {
   reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.o) + row * p.d)[lane] = out;
 }
 
+cudaError_t launch_combine_partials(int n, long long rows, int d, const float* o_parts, const float* lse, void* o,
+                                    cudaStream_t st) {
+  AttnParams p{};
+  p.P = 1; p.n_q = (int)rows; p.Hq = 1; p.d = d; p.n_splits = n;
+  p.ws_o = const_cast<float*>(o_parts); p.ws_lse = const_cast<float*>(lse); p.o = o;
+  return launch_combine(p, st);
+}
+
 cudaError_t launch_combine(const AttnParams& p, cudaStream_t st) {
   const long long rows = (long long)p.P * p.n_q * p.Hq;
   combine_kernel<<<(int)((rows + 3) / 4), 128, 0, st>>>(p);

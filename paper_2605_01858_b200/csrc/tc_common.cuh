@@ -307,22 +307,23 @@ struct Item {
 // into an indexed constant load whose result the compiler cannot keep uniform).
 struct ItemGeo {
   int n_splits, P, Hkv, n_mblocks, layer_count, N_total, layer_begin, n_q, grp, q_pos0, A, ring_count, n_self,
-      ring_start, R, tiles_per_split, Rp, staged;
+      ring_start, R, tiles_per_split, Rp, staged, split_only;
 };
 __device__ __forceinline__ ItemGeo item_geo(const AttnParams& pa, const AttnParams& pb, bool isb) {
   ItemGeo q;
 #define DSC_SEL(f) q.f = isb ? pb.f : pa.f
   DSC_SEL(n_splits); DSC_SEL(P); DSC_SEL(Hkv); DSC_SEL(n_mblocks); DSC_SEL(layer_count); DSC_SEL(N_total);
   DSC_SEL(layer_begin); DSC_SEL(n_q); DSC_SEL(grp); DSC_SEL(q_pos0); DSC_SEL(A); DSC_SEL(ring_count);
-  DSC_SEL(n_self); DSC_SEL(ring_start); DSC_SEL(R); DSC_SEL(tiles_per_split); DSC_SEL(Rp); DSC_SEL(staged);
+  DSC_SEL(n_self); DSC_SEL(ring_start); DSC_SEL(R); DSC_SEL(tiles_per_split); DSC_SEL(Rp); DSC_SEL(staged); DSC_SEL(split_only);
 #undef DSC_SEL
   return q;
 }
 template <class PT>
 __device__ __forceinline__ Item decode_item(const PT& p, int idx) {
   Item w;
-  w.sp = idx % p.n_splits;
-  const int rest = idx / p.n_splits;
+  const bool one = p.split_only >= 0;          // context-parallel partial: one split per launch
+  w.sp = one ? p.split_only : idx % p.n_splits;
+  const int rest = one ? idx : idx / p.n_splits;
 #if DSC_ORDER == 1   // longest-first across all (problem, head) pairs
   const int ph = rest % (p.P * p.Hkv);
   w.mb = p.n_mblocks - 1 - rest / (p.P * p.Hkv);

@@ -8,6 +8,11 @@ Two partitions, both from the north_star:
   [r*Hkv/G, (r+1)*Hkv/G) and their Hq/Hkv query heads each.  Attention is
   independent per KV head; the only exchange is an all-gather of the attend
   output O, gathered head-major so no permute is needed on the wire.
+* P3 -- context parallelism of one stream: every rank holds the
+  stream's cache and computes the attend over 1/G of its keys (dscache_attend_partial);
+  the partials (O_r, lse_r) are all-gathered and merged (dscache_combine_partials).
+  Softmax attention is invariant to how its key set is split, so the merge is exact up
+  to rounding; G = 8 works for Hkv = 4, where P2 cannot.
 
 The collective backend is whatever the process group was created with: NCCL
 over NVLink on the GPU box, gloo on CPU for the multi-process tests.
@@ -60,3 +65,38 @@ def gather_heads(o_local: torch.Tensor, group=None) -> torch.Tensor:
         dist.all_gather(list(out.unbind(0)), hm, group=group)
     full = out.reshape((world * hm.shape[0],) + tuple(hm.shape[1:]))   # [Hq][S][N][q][d]
     return full.permute(1, 2, 3, 0, 4)
+
+
+def merge_partials(o_parts: torch.Tensor, lse_parts: torch.Tensor) -> torch.Tensor:
+    """Reference merge of key-split partials (any backend, any dtype): o_parts [n][..., d],
+    lse_parts [n][...] (log2-sum-exp) -> sum_r 2^(lse_r - M) O_r / sum_r 2^(lse_r - M)."""
+    m = lse_parts.max(dim=0).values
+    w = torch.exp2(lse_parts - m)
+    w = torch.where(torch.isfinite(lse_parts), w, torch.zeros_like(w))
+    return (w.unsqueeze(-1) * o_parts).sum(0) / w.sum(0).unsqueeze(-1)
+
+
+def gather_partials(o_part: torch.Tensor, lse_part: torch.Tensor, group=None):
+    """All-gather every rank's (O_part, lse_part) -> ([G][...], [G][...]) in rank order."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    o_all = torch.empty((world,) + tuple(o_part.shape), dtype=o_part.dtype, device=o_part.device)
+    l_all = torch.empty((world,) + tuple(lse_part.shape), dtype=lse_part.dtype, device=lse_part.device)
+    if hasattr(dist, "all_gather_into_tensor") and dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(o_all, o_part.contiguous(), group=group)
+        dist.all_gather_into_tensor(l_all, lse_part.contiguous(), group=group)
+    else:
+        dist.all_gather(list(o_all.unbind(0)), o_part.contiguous(), group=group)
+        dist.all_gather(list(l_all.unbind(0)), lse_part.contiguous(), group=group)
+    return o_all, l_all
+
+
+def context_parallel_attend(dsc, q, k_self, v_self, group=None, **kw) -> torch.Tensor:
+    """P3: rank r attends over key range r of G (DSCache.attend_partial), the partials are
+    all-gathered over `group` (NCCL on the GPU box) and merged on every rank with the
+    library's combine kernel.  Returns O like DSCache.attend."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    o_part, lse = dsc.attend_partial(q, k_self, v_self, rank, world, **kw)
+    o_all, l_all = gather_partials(o_part, lse, group)
+    return dsc.combine_partials(o_all, l_all)

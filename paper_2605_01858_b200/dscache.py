@@ -55,7 +55,7 @@ class State(ctypes.Structure):
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
            "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
-           "dscache_attn_impl", "dscache_last_error"]
+           "dscache_attn_impl", "dscache_last_error", "dscache_attend_partial", "dscache_combine_partials"]
 
 _lib = None
 
@@ -90,6 +90,8 @@ def load_library(path: str = LIB_PATH):
         "dscache_profile_read": ([P, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(I64),
                                   ctypes.POINTER(I64), ctypes.POINTER(I64), I32], I32),
         "dscache_attn_impl": ([P, I32], I32),
+        "dscache_attend_partial": ([P, I32, I32, P, P, P, I32, I32, I32, P, P, P], I32),
+        "dscache_combine_partials": ([P, I32, I64, P, P, P, P], I32),
         "dscache_last_error": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -222,6 +224,37 @@ class DSCache:
         self._t(o, "o", q.shape)
         _check(_lib.dscache_attend(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, _ptr(o),
                                    _stream_ptr(stream)))
+        return o
+
+    def attend_partial(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, part: int, n_parts: int,
+                       layer_begin: int = 0, layer_count: Optional[int] = None, stream=None):
+        """Part `part` of `n_parts` of the attend's keys (context parallelism):
+        returns (O_part fp32 [S][lc][n_q][Hq][d], lse_part fp32 [S][lc][n_q][Hq])."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        n_q = int(q.shape[2])
+        self._t(q, "q", (c.num_streams, lc, n_q, c.num_q_heads, c.head_dim))
+        self._t(k_self, "k_self", (c.num_streams, lc, n_q, c.num_kv_heads, c.head_dim))
+        self._t(v_self, "v_self", k_self.shape)
+        o_part = torch.empty(q.shape, dtype=torch.float32, device=self.device)
+        lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=self.device)
+        _check(_lib.dscache_attend_partial(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, part, n_parts,
+                                           _ptr(o_part), _ptr(lse), _stream_ptr(stream)))
+        return o_part, lse
+
+    def combine_partials(self, o_parts: torch.Tensor, lse_parts: torch.Tensor, stream=None) -> torch.Tensor:
+        """o_parts [n][..., d] fp32, lse_parts [n][...] fp32 -> merged O (bf16, shape o_parts[0])."""
+        if o_parts.dtype != torch.float32 or lse_parts.dtype != torch.float32:
+            raise TypeError("partials must be fp32")
+        if not (o_parts.is_contiguous() and lse_parts.is_contiguous()):
+            raise ValueError("partials must be contiguous")
+        n = int(o_parts.shape[0])
+        rows = lse_parts[0].numel()
+        if o_parts[0].numel() != rows * self.cfg.head_dim:
+            raise ValueError("o_parts / lse_parts shapes disagree")
+        o = torch.empty(o_parts.shape[1:], dtype=torch.bfloat16, device=self.device)
+        _check(_lib.dscache_combine_partials(self._h, n, rows, _ptr(o_parts), _ptr(lse_parts), _ptr(o),
+                                             _stream_ptr(stream)))
         return o
 
     def step(self, k: torch.Tensor, v: torch.Tensor, q_inst: torch.Tensor, q: torch.Tensor, k_self: torch.Tensor,

@@ -2,9 +2,9 @@
 
 The GPU box has one GPU, so the N>1 paths are covered here: each rank stands in
 for one GPU and computes its shard with the fp64 oracle (the CUDA backend's
-stand-in on CPU); the tests check the partitions (P1 streams, P2 KV-head groups)
-and the head-major all-gather of paper_2605_01858_b200.dist against the
-unsharded oracle.
+stand-in on CPU); the tests check the partitions (P1 streams, P2 KV-head groups,
+P3 context split), the head-major all-gather and the partial gather + merge of
+paper_2605_01858_b200.dist against the unsharded oracle.
 """
 import os
 import socket
@@ -16,7 +16,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import dscache_synth as synth
-from paper_2605_01858_b200.dist import gather_heads, kv_head_partition, stream_partition
+from paper_2605_01858_b200.dist import (gather_heads, gather_partials, kv_head_partition, merge_partials,
+                                        stream_partition)
 
 
 def test_stream_partition_covers_every_stream_once():
@@ -136,3 +137,73 @@ def test_stream_partition_two_ranks_matches_single_process():
     cfg = _small_cfg()
     ref = np.array([np.abs(_oracle_attend(cfg, s, 7)).sum() for s in range(cfg.num_streams)])
     assert np.allclose(digests, ref, rtol=0, atol=1e-12)
+
+
+def _partial_attend(cfg, s, t, part, n_parts):
+    """fp64 partial of the attend over the n_parts-way contiguous split of its context
+    keys (plain softmax over the subset, built from the oracle's key assembly and RoPE):
+    (O_part [q, Hq, d], lse_part [q, Hq] in log2 units)."""
+    from oracle.workload import StreamInputs, step_schedule
+    from oracle import dscache_oracle as O
+    inp = StreamInputs(cfg, s, 0)
+    sch = step_schedule(cfg, t)
+    sk, sv = inp.sink()
+    q, ks, vs = inp.query(t)
+    frames = list(sch.past_frames) + list(sch.instant_frames)
+    hkv, d = sk.shape[1], sk.shape[2]
+    K = O._cat([sk] + [inp.frame_kv(f)[0] for f in frames] + [ks], hkv, d)
+    V = O._cat([sv] + [inp.frame_kv(f)[1] for f in frames] + [vs], hkv, d)
+    nk, nq = K.shape[0], q.shape[0]
+    pos_k = np.arange(nk)
+    pos_q = (nk - nq) + np.arange(nq)
+    qr = O.rope(np.asarray(q, np.float64), pos_q, cfg.rope_theta)
+    kr = O.rope(K, pos_k, cfg.rope_theta)
+    grp = q.shape[1] // hkv
+    lo, hi = part * nk // n_parts, (part + 1) * nk // n_parts
+    o = np.zeros(q.shape, np.float64)
+    lse = np.full(q.shape[:2], -np.inf)
+    for h in range(q.shape[1]):
+        g = h // grp
+        sc = qr[:, h, :] @ kr[lo:hi, g, :].T / np.sqrt(d)                  # [nq, hi-lo]
+        sc = np.where(pos_k[None, lo:hi] <= pos_q[:, None], sc, -np.inf)
+        m = sc.max(axis=1, keepdims=True)
+        ok = np.isfinite(m[:, 0])
+        pr = np.where(ok[:, None], np.exp(sc - np.where(ok[:, None], m, 0.0)), 0.0)
+        l = pr.sum(axis=1)
+        o[ok, h, :] = (pr @ V[lo:hi, g, :])[ok] / l[ok, None]
+        lse[ok, h] = (m[ok, 0] + np.log(l[ok])) / np.log(2.0)
+    return o, lse
+
+
+def _worker_context(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = _small_cfg()
+    t = 6
+    o, lse = _partial_attend(cfg, 1, t, rank, world)          # this rank's key range only
+    o_all, l_all = gather_partials(torch.from_numpy(o), torch.from_numpy(lse))
+    merged = merge_partials(o_all, l_all)
+    if rank == 0:
+        out_q.put(merged.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_context_split_partials_merge_to_unsharded_oracle():
+    """P3 (SURVEY NEXT-4): each rank attends over its contiguous range of the context keys;
+    the all-gathered (O_r, lse_r) merge to the full attention (PAPER.md:637 softmax is
+    invariant to how its key set is partitioned)."""
+    merged = _run(_worker_context)
+    ref = _oracle_attend(_small_cfg(), 1, 6)
+    assert merged.shape == ref.shape
+    assert np.abs(merged - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("n_parts", [1, 3, 5])
+def test_partial_merge_single_process(n_parts):
+    cfg = _small_cfg()
+    parts = [_partial_attend(cfg, 2, 7, r, n_parts) for r in range(n_parts)]
+    merged = merge_partials(torch.from_numpy(np.stack([p[0] for p in parts])),
+                            torch.from_numpy(np.stack([p[1] for p in parts])))
+    assert np.abs(merged.numpy() - _oracle_attend(cfg, 2, 7)).max() < 1e-12

@@ -365,6 +365,42 @@ def test_decode_parity(lib, n_self, n_q):
 
 
 
+@pytest.mark.parametrize("n_parts", [2, 3, 8])
+def test_context_parallel_partials_combine(lib, n_parts):
+    """NEXT-4 building blocks: the attend split into n_parts key ranges (dscache_attend_partial),
+    merged by dscache_combine_partials == the oracle attend; also == dscache_attend up to
+    rounding.  8 parts = the 8-GPU context split of one stream (P3)."""
+    import torch as _t
+    cfg = synth.CONFIGS["c5"].replace(num_streams=2, num_layers=2, num_frames=40)
+    t = 39
+    dev = _t.device("cuda", 0)
+    h = D.DSCache.from_config(cfg)
+    S, N = cfg.num_streams, cfg.num_layers
+    sink = [[synth.sink_kv(cfg, s, l) for l in range(N)] for s in range(S)]
+    h.append_frame(_t.stack([_t.stack([sink[s][l][0] for l in range(N)]) for s in range(S)]).to(dev),
+                   _t.stack([_t.stack([sink[s][l][1] for l in range(N)]) for s in range(S)]).to(dev))
+    for f in range(t + 1):
+        kv = [[synth.frame_kv(cfg, s, l, f) for l in range(N)] for s in range(S)]
+        h.append_frame(_t.stack([_t.stack([kv[s][l][0] for l in range(N)]) for s in range(S)]).to(dev),
+                       _t.stack([_t.stack([kv[s][l][1] for l in range(N)]) for s in range(S)]).to(dev))
+    qkv = [[synth.query_qkv(cfg, s, l, t) for l in range(N)] for s in range(S)]
+    q, ks, vs = (_t.stack([_t.stack([qkv[s][l][i] for l in range(N)]) for s in range(S)]).to(dev) for i in range(3))
+    parts = [h.attend_partial(q, ks, vs, r, n_parts) for r in range(n_parts)]
+    o = h.combine_partials(_t.stack([p[0] for p in parts]), _t.stack([p[1] for p in parts]))
+    o_full = h.attend(q, ks, vs)
+    _t.cuda.synchronize()
+    for s in range(S):
+        for l in range(N):
+            _, _, ref = oracle_step(cfg, s, l, t)
+            ma, rl = assert_close(o[s, l].float().cpu(), ref, "bf16", f"context-parallel {n_parts} parts s={s} l={l}")
+            REPORT.append((f"c5-cp{n_parts}", "O", t, s, l, ma, rl))
+    diff = (o.float() - o_full.float()).norm() / o_full.float().norm()
+    assert diff.item() < 5e-3, diff.item()
+    with pytest.raises(D.DSCacheError):
+        h.attend_partial(q, ks, vs, 0, 10_000)          # parts without keys are refused
+    h.close()
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "c5"])
 def test_build_instant_newest_parity(lib, name):
     # NEXT-3: the incremental instant rows == the last tpf rows of the exact Eq. 7 build

@@ -117,6 +117,9 @@ static_assert(kNQT * 128 == kMBlockRows, "work items are 256-row m-blocks");
 #ifndef DSC_ABL_SWITCH   // ablation: item switches without the Q load/rotation (bit 0) / the O epilogue (bit 1)
 #define DSC_ABL_SWITCH 0
 #endif
+#ifndef DSC_ABL_LOADS   // ablation: window K/V tiles are not loaded
+#define DSC_ABL_LOADS 0
+#endif
 #ifndef DSC_ABL_SMSP2   // ablation: the softmax warps sharing the MMA warp's sub-partition idle
 #define DSC_ABL_SMSP2 0
 #endif
@@ -646,9 +649,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const AttnParams& pi = ITEM_PARAMS(idx);
             const CUtensorMap* tmap = isk ? &pi.tmap_k : &pi.tmap_v;
             const int row = (int)(w.head_row * w.Rp) + t.slot0;
-            mbar_arrive_tx(bar(b_full + st), kKVBytes);
-            tma_load_2d(dst, tmap, 0, row, bar(b_full + st));
-            tma_load_2d(dst + kKVHalf, tmap, 64, row, bar(b_full + st));
+            if (DSC_ABL_LOADS) {   // ablation: no K/V bytes move (tiles keep stale data)
+              mbar_arrive(bar(b_full + st));
+            } else {
+              mbar_arrive_tx(bar(b_full + st), kKVBytes);
+              tma_load_2d(dst, tmap, 0, row, bar(b_full + st));
+              tma_load_2d(dst + kKVHalf, tmap, 64, row, bar(b_full + st));
+            }
           }
           if (lane == 0) TRACE(isk ? EV_K_ISSUE : EV_V_ISSUE, g);
           __syncwarp();

@@ -851,7 +851,14 @@ static long long tc_items(const AttnParams& p) {
   return (long long)p.P * p.Hkv * p.n_mblocks * (p.split_only >= 0 ? 1 : p.n_splits);
 }
 
+cudaError_t launch_attn_tc6(const AttnParams& pa, const AttnParams* pb, cudaStream_t st);
+// DSC_V6 1: kernel v6 (attn_tc6.cu: Q in TMEM, TS QK^T, 7 + 7 K/V stages)
+#ifndef DSC_V6
+#define DSC_V6 0
+#endif
+
 cudaError_t launch_attn_tc2(const AttnParams& pa, const AttnParams* pb, cudaStream_t st) {
+  if (DSC_V6) return launch_attn_tc6(pa, pb, st);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

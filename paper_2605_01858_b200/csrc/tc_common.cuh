@@ -118,6 +118,28 @@ __device__ __forceinline__ void mma_qk8_w(uint32_t d_tmem, uint64_t a, uint64_t 
       "l"(a), "l"(b), "r"(idesc)
       : "memory");
 }
+// S = Q K^T over K = 128 with Q in TMEM (TS form): A step k8 = TMEM columns a + 8k8 (16 bf16
+// of the head dim per lane), B = the K tile (64 rows, K-major SW128; second 64-column block
+// +8 KB = 512 in 16-B units).  Only B is read from shared memory.
+__device__ __forceinline__ void mma_qk8_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7;\n.reg .b32 t1, t2, t3, t4, t5, t6, t7;\n"
+      "add.s64 b1, %2, 2; add.s64 b2, %2, 4; add.s64 b3, %2, 6;\n"
+      "add.s64 b4, %2, 512; add.s64 b5, %2, 514; add.s64 b6, %2, 516; add.s64 b7, %2, 518;\n"
+      "add.u32 t1, %1, 8; add.u32 t2, %1, 16; add.u32 t3, %1, 24; add.u32 t4, %1, 32;\n"
+      "add.u32 t5, %1, 40; add.u32 t6, %1, 48; add.u32 t7, %1, 56;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t1], b1, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t2], b2, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t3], b3, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t4], b4, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t5], b5, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t6], b6, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t7], b7, %3, 1;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc)
+      : "memory");
+}
 // O += P V over one 64-key tile (4 x K16): A (P) in TMEM, 8 columns per K16 step; B (V)
 // MN-major SW128, 16 keys = 2048 B (128 in 16-B units) per step.  acc = 0 overwrites O.
 __device__ __forceinline__ void mma_pv4_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {

@@ -305,7 +305,7 @@ enum { EV_K_ISSUE = 0, EV_V_ISSUE, EV_KR, EV_KF, EV_S0, EV_S1, EV_P0, EV_P1, EV_
 #endif
 
 #ifndef DSC_ORDER
-#define DSC_ORDER 1
+#define DSC_ORDER 2
 #endif
 struct Item {
   int pp, g, mb, sp;
@@ -349,6 +349,17 @@ __device__ __forceinline__ Item decode_item(const PT& p, int idx) {
 #if DSC_ORDER == 1   // longest-first across all (problem, head) pairs
   const int ph = rest % (p.P * p.Hkv);
   w.mb = p.n_mblocks - 1 - rest / (p.P * p.Hkv);
+#elif DSC_ORDER == 2   // longest-first inside groups of kOrderGroup (problem, head) pairs (L2 reuse)
+#ifndef DSC_OGRP
+#define DSC_OGRP 148
+#endif
+  constexpr int kOrderGroup = DSC_OGRP;
+  const int nph = p.P * p.Hkv;
+  const int grp0 = rest / (kOrderGroup * p.n_mblocks) * kOrderGroup;   // first pair of this group
+  const int gsz = min(kOrderGroup, nph - grp0);
+  const int r2 = rest - grp0 * p.n_mblocks;
+  const int ph = grp0 + r2 % gsz;
+  w.mb = p.n_mblocks - 1 - r2 / gsz;
 #else
   w.mb = p.n_mblocks - 1 - rest % p.n_mblocks;
   const int ph = rest / p.n_mblocks;

@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tO = tmem + lane_off + (uint32_t)(256 + qt * 128);
     const float sl2 = p.scale_log2;
     const float2 scale2 = make_float2(sl2, sl2);
-
+    const uint32_t barS = bar(B_S + qt * 2), barP = bar(B_P + qt * 2);   // + 8 * buffer
     const int lt = threadIdx.x - qt * 128;           // 0..127 within the warpgroup
     auto qtile_of = [&](int kk) { return sbase + OFF_Q + (uint32_t)(((DSC_QDB ? (kk & 1) : 0) * 2 + qt) * kQBytes); };
     auto qbar_of = [&](int kk) { return bar(B_Q + (DSC_QDB ? (kk & 1) : 0) * 2 + qt); };
@@ -258,8 +258,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n = w.n_tiles;
       const int nidx = idx + gridDim.x;
       const bool has_next = nidx < n_role_items;
+#if !DSC_QROT   // (with DSC_QROT the rotation warpgroup prepares the next item's Q)
       Item wn;
       if (has_next) wn = decode_item(ITEM_PARAMS(nidx), ITEM_LOCAL(nidx));
+#endif
 #if DSC_QDB && !DSC_QROT
       // the other Q buffer held item kk-1's Q, whose last S we have consumed: the next
       // item's Q rows are fetched now and rotated after this item's first tile
@@ -289,7 +291,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int jj = 0; jj < n; ++jj) {
         const int g = gt + jj;
         const int u = w.t_begin + jj;
-        const int sb = qt * 2 + (g & 1);           // S/P buffer of this tile
         const uint32_t tS = tS0 + (uint32_t)((g & 1) * 64);
         int c_lo, c_hi;
         const TileSeg t = tile_segments(p, w, u);
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));   // id pos0 + c <= lim
         }
         const bool full = (c_lo == 0) && (c_hi == kKT);
-        mbar_wait(bar(B_S + sb), (g >> 1) & 1);
+        mbar_wait(barS + 8u * (uint32_t)(g & 1), (g >> 1) & 1);
         if (rloc == 0) TRACE(EV_S0 + qt, g);
 #if DSC_QROT
 #elif DSC_QDB
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (jj == n - 1 && has_next && !(DSC_ABL_SWITCH & 1)) issue_q_tile(ITEM_PARAMS(nidx), wn, qt, lt, qtile_of(kk + 1));
 #endif
         if (warp_dead || DSC_ABL_SOFTMAX || (DSC_ABL_SMSP2 && (warp & 3) == 2)) {   // all 32 rows are padding: their P / O are never used
-          mbar_arrive(bar(B_P + sb));
+          mbar_arrive(barP + 8u * (uint32_t)(g & 1));
           continue;
         }
         tc_fence_after();
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (warp == 0 && lane == 0) TRACE(EV_L + 4, g);
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(bar(B_P + sb));
+        mbar_arrive(barP + 8u * (uint32_t)(g & 1));
         if (rloc == 0) TRACE(EV_P0 + qt, g);
         if (lane == 0) TRACE(EV_PW0 + warp, g);
       }

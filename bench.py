@@ -58,10 +58,13 @@ def steady_counts(cfg, n_q=None):
     return cfg.sink_tokens, cfg.W, cfg.C, n_q
 
 
-def flops_per_unit(cfg):
+def flops_per_unit(cfg, n_boost=0):
     """Algorithmic FLOPs of one (stream, layer) step: 4 * d * Hq * visible (query, key) pairs.
-    build: instant token i sees A + i + 1 keys; attend: query i sees A + P + C + i + 1 keys."""
+    build: instant token i sees A + i + 1 keys; attend: query i sees A + P + C + i + 1 keys.
+    With a boosted newest frame (n_boost tokens) the instant segment holds C - tpf + n_boost."""
     A, P, C, q = steady_counts(cfg)
+    if n_boost:
+        C = C - cfg.tokens_per_frame + n_boost
     k = 4 * cfg.head_dim * cfg.num_q_heads
     build = k * (C * A + C * (C + 1) // 2)
     attend = k * (q * (A + P + C) + q * (q + 1) // 2)
@@ -185,9 +188,12 @@ def run_ours(args, cfg, world, rank, local):
     # device-resident synthetic input pool (values cycle; positions / slots never repeat)
     POOL = 4
     frames = [(rnd(S, N, tpf, Hkv, d), rnd(S, N, tpf, Hkv, d)) for _ in range(POOL)]
-    q_inst = [rnd(S, N, C, Hq, d) for _ in range(2)]
+    n_boost = int(round(args.boost * tpf)) if args.boost > 0 else 0
+    Cq = C - tpf + n_boost if n_boost else C          # instant rows built per step
+    q_inst = [rnd(S, N, Cq, Hq, d) for _ in range(2)]
+    boost_kv = [(rnd(S, N, n_boost, Hkv, d), rnd(S, N, n_boost, Hkv, d)) for _ in range(2)] if n_boost else None
     qry = [(rnd(S, N, q, Hq, d), rnd(S, N, q, Hkv, d), rnd(S, N, q, Hkv, d)) for _ in range(2)]
-    o_inst = torch.empty(S, N, C, Hq, d, dtype=dt, device=dev)
+    o_inst = torch.empty(S, N, Cq, Hq, d, dtype=dt, device=dev)
     o = torch.empty(S, N, q, Hq, d, dtype=dt, device=dev)
     stream = torch.cuda.current_stream(dev)
     if A > 0:
@@ -204,7 +210,11 @@ def run_ours(args, cfg, world, rank, local):
     def step(i):
         t = tcount[0]
         qq = qry[i & 1]
-        if fused:       # dscache_step: append + build_instant + attend, one attention launch
+        if n_boost:     # NEXT-4 resolution boost: the newest frame re-encoded (n_boost tokens)
+            dsc.append_frame(*frames[t % POOL])
+            dsc.build_instant_boost(q_inst[i & 1], *boost_kv[i & 1], o_inst=o_inst)
+            dsc.attend_boost(qq[0], qq[1], qq[2], *boost_kv[i & 1], o=o)
+        elif fused:     # dscache_step: append + build_instant + attend, one attention launch
             dsc.step(*frames[t % POOL], q_inst[i & 1], qq[0], qq[1], qq[2], o_inst=o_inst, o=o)
         else:
             dsc.append_frame(*frames[t % POOL])
@@ -254,11 +264,12 @@ def run_ours(args, cfg, world, rank, local):
 
     # e2e: the same step through the public API with pinned host buffers, H2D of every
     # input of the step and D2H of the query answer O inside the timed region
-    e2e = run_e2e(args, cfg, lcfg, dsc, S, dev, stream, world, kvsplit)
+    e2e = (run_e2e(args, cfg, lcfg, dsc, S, dev, stream, world, kvsplit) if not n_boost else
+           {"skipped": "boost mode times the device-resident path only"})
     impl = dsc.attn_impl()
     dsc.close()
 
-    fb, fa = flops_per_unit(lcfg)
+    fb, fa = flops_per_unit(lcfg, n_boost)
     units = S * N
     frames_total = cfg.num_streams * args.steps
     value = frames_total / (t_max / 1e3)
@@ -285,7 +296,8 @@ def run_ours(args, cfg, world, rank, local):
                    "config_id": cfg.name, "streams": cfg.num_streams, "layers": N, "query_tokens": q,
                    "parallelism": (f"KV-head split x{world} (NCCL all-gather of O)" if kvsplit else
                                    f"stream partition x{world}") if world > 1 else "single GPU",
-                   "mode": args.mode, "api": args.api,
+                   "mode": args.mode, "api": "boost (split calls)" if n_boost else args.api,
+                   "n_boost": n_boost,
                    "l2": "flushed between steps" if flush else "inputs larger than L2 (ring %.2f GB)" % (ring_bytes / 1e9),
                    "steady_state": True, "input_pool": f"{POOL} distinct frames cycled (positions never repeat)"},
         "frames_per_s_per_stream": round(value / cfg.num_streams, 3),
@@ -427,6 +439,8 @@ def main():
                     help="streams: P1 stream partition (default); kvsplit: P2 KV-head split of one stream")
     ap.add_argument("--api", default="fused", choices=["fused", "split"],
                     help="fused: DSCache.step (one attention launch per step); split: three calls")
+    ap.add_argument("--boost", type=float, default=0.0,
+                    help="> 0: resolution-boosted newest frame with boost*tpf tokens (SURVEY NEXT-4), split calls")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()

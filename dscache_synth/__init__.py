@@ -28,9 +28,11 @@ FRM_K, FRM_V = 2, 3            # raw K/V of frame f                           [t
 INST_Q = 4                     # instant-build queries at step t              [C_t][Hq][d]
 QRY_Q, QRY_K, QRY_V = 5, 6, 7  # query chunk at step t (K/V transient)        [q][Hq|Hkv][d]
 UPD_Q = 8                      # queries of the frame leaving the buffer at t [tpf][Hq][d]
+BST_K, BST_V = 9, 10           # re-encoded (boosted) newest frame at step t  [n_boost][Hkv][d]
 
 KIND_NAMES = {SINK_K: "SINK_K", SINK_V: "SINK_V", FRM_K: "FRM_K", FRM_V: "FRM_V",
-              INST_Q: "INST_Q", QRY_Q: "QRY_Q", QRY_K: "QRY_K", QRY_V: "QRY_V", UPD_Q: "UPD_Q"}
+              INST_Q: "INST_Q", QRY_Q: "QRY_Q", QRY_K: "QRY_K", QRY_V: "QRY_V", UPD_Q: "UPD_Q",
+              BST_K: "BST_K", BST_V: "BST_V"}
 
 
 @dataclasses.dataclass(frozen=True)
@@ -108,6 +110,26 @@ def instant_q(cfg: StreamConfig, stream: int, layer: int, step: int, n_inst: int
 
 def update_q(cfg: StreamConfig, stream: int, layer: int, step: int):
     return draw(cfg, stream, layer, UPD_Q, step, (cfg.tokens_per_frame, cfg.num_q_heads, cfg.head_dim))
+
+
+def boost_kv(cfg: StreamConfig, stream: int, layer: int, step: int, n_boost: int):
+    """Raw K/V of the newest frame re-encoded at a higher resolution (n_boost tokens)."""
+    shp = (n_boost, cfg.num_kv_heads, cfg.head_dim)
+    return draw(cfg, stream, layer, BST_K, step, shp), draw(cfg, stream, layer, BST_V, step, shp)
+
+
+def batch_boost_kv(cfg: StreamConfig, step: int, n_boost: int, streams=None, layers=None):
+    """[S][N][n_boost][Hkv][d] stacked boosted K and V."""
+    streams = range(cfg.num_streams) if streams is None else streams
+    layers = range(cfg.num_layers) if layers is None else layers
+    ks, vs = [], []
+    for s in streams:
+        kl, vl = [], []
+        for l in layers:
+            k, v = boost_kv(cfg, s, l, step, n_boost)
+            kl.append(k); vl.append(v)
+        ks.append(torch.stack(kl)); vs.append(torch.stack(vl))
+    return torch.stack(ks), torch.stack(vs)
 
 
 def query_qkv(cfg: StreamConfig, stream: int, layer: int, step: int, n_q: int | None = None):

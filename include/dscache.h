@@ -146,6 +146,38 @@ dscache_status dscache_build_instant(dscache_t h, int32_t layer_begin, int32_t l
 dscache_status dscache_build_instant_newest(dscache_t h, int32_t layer_begin, int32_t layer_count,
                                             const void* q_new, void* o_new, void* stream);
 
+/* Resolution-boosted newest frame ("the buffer inputs may be temporarily
+ * re-encoded, e.g. using a higher-resolution version of X_{t+1}, without modifying the
+ * buffer itself"; PAPER.md:695 / Table "spa" PAPER.md:719-749).  The
+ * instant cache is built from the buffer with its newest frame replaced by a caller-supplied
+ * re-encoding of n_boost tokens (n_boost >= 1, any count: x1.5 / x2 spatial resolution gives
+ * more tokens than tpf); the ring keeps the normal frame, so the cumulative update and every
+ * later step are unchanged (reading Q22).  Keys [sink | older instant frames |
+ * boosted frame], ids 0.. contiguous; query i at id A + i, causal.
+ *   q_inst  : [S][layer_count][C_t - tpf + n_boost][Hq][d]  older instant tokens, then the
+ *             boosted frame's tokens
+ *   k_boost : [S][layer_count][n_boost][Hkv][d]   raw (un-rotated) K of the boosted frame
+ *   v_boost : [S][layer_count][n_boost][Hkv][d]
+ *   o_inst  : [S][layer_count][C_t - tpf + n_boost][Hq][d]
+ * E_STATE before the sink and the first frame; E_CONFIG when l_I = 0; E_ARG for null
+ * pointers or n_boost < 1; E_POS_OVERFLOW if A + C_t - tpf + n_boost > max_position. */
+dscache_status dscache_build_instant_boost(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                                           const void* q_inst, const void* k_boost, const void* v_boost,
+                                           int32_t n_boost, void* o_inst, void* stream);
+
+/* Attention of the query chunk over the final cache whose instant segment carries the
+ * boosted newest frame: keys [sink | past | older instant frames | boosted frame (n_boost)
+ * | self (n_q)], ids contiguous from 0, query i at
+ * A + P_t + C_t - tpf + n_boost + i, causal inside the chunk (Eq. 8 with I built by
+ * dscache_build_instant_boost).  Layouts as dscache_attend plus k_boost / v_boost as in
+ * dscache_build_instant_boost.  The [boost | self] keys are gathered into a library-owned
+ * scratch slab (device copies, stream-ordered) before the attention launch.
+ * Errors as dscache_attend; E_ARG for n_boost < 1; E_CONFIG when l_I = 0. */
+dscache_status dscache_attend_boost(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                                    const void* q, const void* k_self, const void* v_self, int32_t n_q,
+                                    const void* k_boost, const void* v_boost, int32_t n_boost, void* o,
+                                    void* stream);
+
 /* Attention of an n_q-token query chunk over [C_a | U | I | self] (Eq. 8 plus the
  * chunk's own K/V, which are used and then discarded: PAPER.md:212/699).  Ids:
  * sink 0..A-1, past+instant A..A+P_t+C_t-1 (oldest first), query/self token i at

@@ -17,6 +17,8 @@ What it computes (per stream s, per layer r; everything in float64):
 * the final attention over [C_a, U, I] (Eq. 8) plus the query
   chunk itself, again with consecutive position ids from 0 (PAPER.md:236,
   Eq. 2 PAPER.md:141-146);
+* the resolution-boosted newest frame: the instant cache
+  and the final attention with the buffer's newest input re-encoded (SURVEY NEXT-4);
 * decoding over C_{t+1}: the last tokens of [query chunk | generated
   tokens] attend over [C_a, U, I, self] (SURVEY NEXT-2);
 * the cumulative-update attention inside phi(X_{t-l_I}, [C_a, zeta(U_{t-1})]) of
@@ -225,6 +227,44 @@ def attend_output(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], fram
     frames = list(sched.past_frames) + list(sched.instant_frames)
     ks = _cat([sk] + [frame_kv(f)[0] for f in frames] + [k_self], hkv, d)
     vs = _cat([sv] + [frame_kv(f)[1] for f in frames] + [v_self], hkv, d)
+    L_ctx = ks.shape[0] - q.shape[0]
+    pos_k = np.arange(ks.shape[0])
+    pos_q = L_ctx + np.arange(q.shape[0])
+    return gqa_attention(np.asarray(q, np.float64), pos_q, ks, vs, pos_k, theta, style)
+
+
+def instant_cache_output_boosted(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], frame_kv: FrameFn,
+                                 q_inst: np.ndarray, k_boost: np.ndarray, v_boost: np.ndarray, theta: float,
+                                 style: int = SPLIT_HALF) -> np.ndarray:
+    """I_t = phi(B_t, C_a) with the newest buffer input temporarily re-encoded at a higher
+    resolution, "without modifying the buffer itself" (PAPER.md:221; PAPER.md:695, Table
+    "spa" PAPER.md:719-749).  The context is [C_a | B_t minus its newest
+    frame | re-encoded newest frame (n_boost tokens)] with consecutive ids 0.. (PAPER.md:236);
+    query i sits at id A + i and sees ids <= A + i (Eq. 7 otherwise unchanged).
+    q_inst [C_t - tpf + n_boost, Hq, d], k_boost/v_boost [n_boost, Hkv, d] -> same rows as q_inst."""
+    sk, sv = sink
+    hkv, d = sk.shape[1], sk.shape[2]
+    older = list(sched.instant_frames)[:-1]
+    ks = _cat([sk] + [frame_kv(f)[0] for f in older] + [k_boost], hkv, d)
+    vs = _cat([sv] + [frame_kv(f)[1] for f in older] + [v_boost], hkv, d)
+    A = sk.shape[0]
+    pos_k = np.arange(ks.shape[0])
+    pos_q = A + np.arange(q_inst.shape[0])
+    return gqa_attention(np.asarray(q_inst, np.float64), pos_q, ks, vs, pos_k, theta, style)
+
+
+def attend_output_boosted(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], frame_kv: FrameFn,
+                          q: np.ndarray, k_self: np.ndarray, v_self: np.ndarray, k_boost: np.ndarray,
+                          v_boost: np.ndarray, theta: float, style: int = SPLIT_HALF) -> np.ndarray:
+    """Eq. 8 over [C_a, U_t, I_t] where I_t was built from the re-encoded
+    newest frame (instant_cache_output_boosted): the instant segment holds the older instant
+    frames and then the n_boost re-encoded tokens (reading Q22), followed by the
+    query chunk; ids consecutive from 0, causal inside the chunk."""
+    sk, sv = sink
+    hkv, d = sk.shape[1], sk.shape[2]
+    frames = list(sched.past_frames) + list(sched.instant_frames)[:-1]
+    ks = _cat([sk] + [frame_kv(f)[0] for f in frames] + [k_boost, k_self], hkv, d)
+    vs = _cat([sv] + [frame_kv(f)[1] for f in frames] + [v_boost, v_self], hkv, d)
     L_ctx = ks.shape[0] - q.shape[0]
     pos_k = np.arange(ks.shape[0])
     pos_q = L_ctx + np.arange(q.shape[0])

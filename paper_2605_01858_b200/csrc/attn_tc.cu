@@ -79,7 +79,7 @@ constexpr int OFF_BAR = OFF_V + VST * kKVBytes;
 // behind (the parity test of mbarrier.try_wait cannot tell phase k from phase k+2): with S
 // prefetched two tiles ahead, PV(g-1) may still be pending when the softmax finishes tile g.
 constexpr int B_Q = 0, B_KR = 2 * kQBufs, B_KF = B_KR + KST, B_KE = B_KF + KST, B_VF = B_KE + KST, B_VE = B_VF + VST,
-              B_S = B_VE + VST, B_P = B_S + 4, B_O = B_P + 4, B_OF = B_O + 4, B_QE = B_OF + 2, B_N = B_QE + 2;
+              B_S = B_VE + VST, B_P = B_S + 4, B_O = B_P + 4, B_OF = B_O + 4, B_QE = B_OF + 2, B_EP = B_QE + 2, B_N = B_EP + 2;
 // setmaxnreg budget per warpgroup: 2*softmax + rotation + copy/MMA <= 512 (x 128 threads)
 constexpr int kRegSoftmax = 144, kRegRotate = 136, kRegCopy = 88;
 static_assert(2 * kRegSoftmax + kRegRotate + kRegCopy <= 512, "setmaxnreg budget exceeds the 64K register file");
@@ -147,6 +147,19 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 #ifndef DSC_INTERLEAVE
 #define DSC_INTERLEAVE 0
 #endif
+// DSC_EPIROT 1 (measured neutral on c5/c4/c2, off): the O epilogue of staged (build) items
+// runs on the rotation warpgroup (idle
+// there: staged K arrives rotated), so the softmax warpgroups go straight to the next item.
+// The softmax hands l over through the item's consumed Q tile (B_EP), the rotation
+// warpgroup reads O out of TMEM and releases it (B_OF) as the softmax would.
+#ifndef DSC_L2PF   // window K/V tiles prefetched into L2 this many tiles ahead of their TMA load
+                   // (0 = off: 2/4/8 measured 1-3% slower on c5 / c3)
+#define DSC_L2PF 0
+#endif
+#ifndef DSC_EPIROT
+#define DSC_EPIROT 0
+#endif
+static_assert(!DSC_EPIROT || DSC_QROT, "DSC_EPIROT hands the epilogue to the rotation warpgroup of DSC_QROT");
 // DSC_QFIRST 1: the next item's Q tile is published before the epilogue, so its first S
 // MMAs run while O is read out
 #ifndef DSC_QFIRST
@@ -202,6 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) mbar_init(bar(B_OF + i), 128);
     for (int i = 0; i < 2; ++i) mbar_init(bar(B_QE + i), 1);   // Q buffer i free (MMA commit after an item)
+    for (int i = 0; i < 2; ++i) mbar_init(bar(B_EP + i), 128); // l of a staged item handed to the rotation WG
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
   }
@@ -442,6 +456,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (rloc == 0) TRACE(EV_QDONE, gt);
       }
 #endif
+#if DSC_EPIROT
+      if (w.staged && p.n_splits == 1 && p.split_only < 0) {
+        // the rotation warpgroup writes O out.  l goes into Q tile qt of this item's buffer
+        // (its last QK^T has completed; the buffer is refilled by the rotation warpgroup
+        // itself, after this epilogue).  Waiting for the previous item's O release keeps the
+        // slot and B_EP at most one phase ahead of the reader.
+        if (kk > 0) mbar_wait(bar(B_OF + qt), (kk - 1) & 1);
+        reinterpret_cast<float*>(smem + OFF_Q + (uint32_t)(((kk & 1) * 2 + qt) * kQBytes))[rloc] = lsum2.x + lsum2.y;
+        mbar_arrive(bar(B_EP + qt));
+        continue;
+      }
+#endif
       // epilogue of the item: O / l once the last PV is done
       const float lsum = lsum2.x + lsum2.y;
       mbar_wait(bar(B_O + qt * 2 + ((gt - 1) & 1)), ((gt - 1) >> 1) & 1);
@@ -530,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     if (blockIdx.x < (unsigned)n_role_items) prep_q(0, blockIdx.x);
 #endif
-    int gt = 0, kk = 0;
+    int gt = 0, kk = 0, ne = 0;   // ne: staged items whose epilogue this warpgroup ran (B_EP phase)
     for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x, ++kk) {
       const AttnParams& p = ITEM_PARAMS(idx);
       const Item w = decode_item(p, ITEM_LOCAL(idx));
@@ -542,6 +568,45 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (w.staged) {   // no K to rotate: the MMA waits on the copy barrier; prepare the next Q
         if (q_next) prep_q(kk + 1, nidx_q);
         gt += w.n_tiles;
+#if DSC_EPIROT
+        if (p.n_splits == 1 && p.split_only < 0) {   // O epilogue of both Q tiles (see DSC_EPIROT)
+          const uint32_t tq = tmem + ((uint32_t)((lt >> 5) * 32) << 16);
+#pragma unroll 1
+          for (int qt = 0; qt < 2; ++qt) {
+            mbar_wait(bar(B_EP + qt), ne & 1);
+            const float lsum = reinterpret_cast<const float*>(smem + OFF_Q + (uint32_t)(((kk & 1) * 2 + qt) * kQBytes))[lt];
+            mbar_wait(bar(B_O + qt * 2 + ((gt - 1) & 1)), ((gt - 1) >> 1) & 1);
+            tc_fence_after();
+            const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+            const int rglob = w.m0 + qt * 128 + lt;
+            const bool valid_row = rglob < w.rows_total;
+            const int qi = valid_row ? rglob / p.grp : 0;
+            const int h = valid_row ? w.g * p.grp + rglob % p.grp : 0;
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) + (((long long)w.pp * p.n_q + qi) * p.Hq + h) * 128;
+#pragma unroll 1
+            for (int hf = 0; hf < 2; ++hf) {
+              uint32_t o[64];
+              tmem_ld32(tq + 256 + qt * 128 + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+              tmem_ld32(tq + 256 + qt * 128 + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+              tmem_wait_ld();
+              if (hf == 1) {
+                tc_fence_before();
+                mbar_arrive(bar(B_OF + qt));
+              }
+              if (!valid_row) continue;
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                uint32_t q[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  q[j] = pack_bf16(__uint_as_float(o[16 * v + 2 * j]) * inv, __uint_as_float(o[16 * v + 2 * j + 1]) * inv);
+                stg256(dst + 64 * hf + 16 * v, q);
+              }
+            }
+          }
+          ++ne;
+        }
+#endif
         continue;
       }
 #endif
@@ -614,6 +679,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int off = isk ? OFF_K : OFF_V;
       const int b_full = isk ? B_KR : B_VF, b_free = isk ? B_KE : B_VE;
       int gt = 0;
+#if DSC_L2PF
+      // L2 prefetch cursor, DSC_L2PF window tiles ahead of the loads (across items): a TMA
+      // load issued when its stage frees then hits L2 instead of waiting ~5K clk on HBM
+      int pf_idx = blockIdx.x, pf_jj = -1;
+      Item pf_w;
+      auto pf_next = [&]() {
+        if (pf_idx >= n_role_items) return;
+        ++pf_jj;
+        while (true) {
+          if (pf_jj == 0) pf_w = decode_item(ITEM_PARAMS(pf_idx), ITEM_LOCAL(pf_idx));
+          if (pf_jj < pf_w.n_tiles) break;
+          pf_idx += gridDim.x;
+          pf_jj = 0;
+          if (pf_idx >= n_role_items) return;
+        }
+        const AttnParams& pq = ITEM_PARAMS(pf_idx);
+        const int u = pf_w.t_begin + pf_jj;
+        if (u < pf_w.n_extra || lane != 0) return;
+        const TileSeg t = tile_segments(pq, pf_w, u);
+        const CUtensorMap* tmap = isk ? &pq.tmap_k : &pq.tmap_v;
+        const int row = (int)(pf_w.head_row * pf_w.Rp) + t.slot0;
+        tma_prefetch_2d(tmap, 0, row);
+        tma_prefetch_2d(tmap, 64, row);
+      };
+      for (int i = 0; i < DSC_L2PF; ++i) pf_next();
+#endif
       for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x) {
         const AttnParams& p = ITEM_PARAMS(idx);
         const Item w = decode_item(p, ITEM_LOCAL(idx));
@@ -659,6 +750,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (lane == 0) TRACE(isk ? EV_K_ISSUE : EV_V_ISSUE, g);
+#if DSC_L2PF
+          pf_next();
+#endif
           __syncwarp();
         }
         gt += w.n_tiles;

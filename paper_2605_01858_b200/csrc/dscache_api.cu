@@ -69,6 +69,13 @@ struct dscache_s {
   float2* rope = nullptr;
   float* ws = nullptr;       // split-KV workspace (grown on demand)
   size_t ws_bytes = 0;
+  void* bstage_k = nullptr;  // staged boosted build: sink ++ older instant ++ boosted frame (grown on demand)
+  void* bstage_v = nullptr;
+  int bstage_rows = 0;
+  CUtensorMap tmap_bk{}, tmap_bv{};
+  void* boost_k = nullptr;   // [boost | self] key gather of dscache_attend_boost (grown on demand)
+  void* boost_v = nullptr;
+  size_t boost_bytes = 0;
   std::vector<int64_t> frames;
   std::vector<int> sink_filled;
   std::vector<int64_t> last_evicted;
@@ -286,6 +293,8 @@ dscache_status dscache_destroy(dscache_t h) {
   cudaFree(h->ring_k); cudaFree(h->ring_v); cudaFree(h->sink_k); cudaFree(h->sink_v);
   cudaFree(h->rope); cudaFree(h->ws);
   cudaFree(h->stage_k); cudaFree(h->stage_v);
+  cudaFree(h->boost_k); cudaFree(h->boost_v);
+  cudaFree(h->bstage_k); cudaFree(h->bstage_v);
   delete h;
   return DSCACHE_OK;
 }
@@ -411,8 +420,11 @@ namespace {
 // Attention of n_q query rows over [sink | past | instant | self], where the self segment
 // holds n_self >= n_q transient tokens (the query chunk, and during decode the tokens
 // generated so far) and the queries are its last n_q tokens.
+// ring_drop: tokens left out at the newest end of the window (the boosted newest frame's
+// ring slots, whose keys the caller supplies re-encoded inside the self segment instead)
 dscache_status prep_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
-                           const void* v_self, int32_t n_self, int32_t n_q, void* o, bool dbg, dsc::AttnParams& p) {
+                           const void* v_self, int32_t n_self, int32_t n_q, void* o, bool dbg, dsc::AttnParams& p,
+                           int ring_drop = 0) {
   dscache_status s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
   if (!h->sink_filled[lb] || h->frames[lb] < 1)
@@ -420,12 +432,12 @@ dscache_status prep_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, c
   if (n_q < 1 || n_q > n_self) return fail(DSCACHE_E_ARG, "need 1 <= n_q <= n_self");
   if (!q || !k_self || !v_self || !o) return fail(DSCACHE_E_ARG, "null q/k_self/v_self/o");
   const Schedule sc = h->schedule(lb);
-  if ((int64_t)h->cfg.sink_tokens + sc.P_t + sc.C_t + n_self > h->cfg.max_position)
+  if ((int64_t)h->cfg.sink_tokens + sc.P_t + sc.C_t - ring_drop + n_self > h->cfg.max_position)
     return fail(DSCACHE_E_POS_OVERFLOW, "A + P_t + C_t + n_self exceeds max_position");
   p = dsc::AttnParams{};
   fill_common(h, p, lb, lc);
   p.q = q; p.o = o; p.n_q = n_q;
-  p.ring_start = sc.ring_start; p.ring_count = sc.P_t + sc.C_t;
+  p.ring_start = sc.ring_start; p.ring_count = sc.P_t + sc.C_t - ring_drop;
   p.q_pos0 = h->cfg.sink_tokens + p.ring_count + (n_self - n_q);
   p.self_k = k_self; p.self_v = v_self; p.n_self = n_self;
   p.dbg_pos = dbg ? h->dbg_attend : nullptr;
@@ -477,6 +489,106 @@ dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q
 dscache_status dscache_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                               const void* v_self, int32_t n_self, int32_t n_q, void* o, void* stream) {
   return attend_common(h, lb, lc, q, k_self, v_self, n_self, n_q, o, stream, false);
+}
+
+dscache_status dscache_build_instant_boost(dscache_t h, int32_t lb, int32_t lc, const void* q_inst,
+                                           const void* k_boost, const void* v_boost, int32_t n_boost, void* o_inst,
+                                           void* stream) {
+  dscache_status s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  if (!h->sink_filled[lb] || h->frames[lb] < 1)
+    return fail(DSCACHE_E_STATE, "build_instant_boost before the sink and the first frame were appended");
+  if (h->cfg.instant_frames < 1) return fail(DSCACHE_E_CONFIG, "l_I = 0: there is no instant cache");
+  if (!q_inst || !k_boost || !v_boost || !o_inst) return fail(DSCACHE_E_ARG, "null q_inst/k_boost/v_boost/o_inst");
+  if (n_boost < 1) return fail(DSCACHE_E_ARG, "n_boost must be >= 1");
+  const Schedule sc = h->schedule(lb);
+  const int older = sc.C_t - h->cfg.tokens_per_frame;   // instant tokens before the newest frame
+  if ((int64_t)h->cfg.sink_tokens + older + n_boost > h->cfg.max_position)
+    return fail(DSCACHE_E_POS_OVERFLOW, "A + C_t - tpf + n_boost exceeds max_position");
+  DeviceGuard dg(h->cfg.device);
+  // keys: sink | ring window of the older instant frames | boosted frame as the self
+  // segment (ids A + older + j); queries: ids A + i over [older | boosted]
+  dsc::AttnParams p{};
+  fill_common(h, p, lb, lc);
+  p.q = q_inst; p.o = o_inst; p.n_q = older + n_boost; p.q_pos0 = h->cfg.sink_tokens;
+  p.ring_start = sc.inst_start; p.ring_count = older;
+  p.self_k = k_boost; p.self_v = v_boost; p.n_self = n_boost;
+  p.dbg_pos = nullptr;
+  p.n_mblocks = (p.n_q * p.grp + 2 * dsc::kTileM - 1) / (2 * dsc::kTileM);
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long build_items = (long long)p.P * p.Hkv * p.n_mblocks;
+  if (h->impl_build == DSCACHE_IMPL_TC && build_items >= 2LL * h->num_sms) {
+    // staged as the plain build: [sink | older instant | boosted frame] once per (stream,
+    // layer, kv head), K rotated at ids 0.., read by TMA (the boosted frame otherwise goes
+    // through the per-item sink/self loads)
+    const int rows = h->cfg.sink_tokens + older + n_boost;
+    if (rows > h->bstage_rows) {
+      cudaFree(h->bstage_k); cudaFree(h->bstage_v);
+      h->bstage_k = h->bstage_v = nullptr; h->bstage_rows = 0;
+      const size_t heads = (size_t)h->cfg.num_streams * h->cfg.num_layers * h->cfg.num_kv_heads;
+      const size_t sb = heads * rows * h->cfg.head_dim * h->elem;
+      if (cudaMalloc(&h->bstage_k, sb) != cudaSuccess || cudaMalloc(&h->bstage_v, sb) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DSCACHE_E_OOM, "boost staging allocation failed");
+      }
+      DSC_CUDA(dsc::make_stage_tmap(&h->tmap_bk, h->bstage_k, (unsigned long long)heads * rows));
+      DSC_CUDA(dsc::make_stage_tmap(&h->tmap_bv, h->bstage_v, (unsigned long long)heads * rows));
+      h->bstage_rows = rows;
+    }
+    dsc::StageParams sp{};
+    sp.sink_k = h->sink_k; sp.sink_v = h->sink_v; sp.ring_k = h->ring_k; sp.ring_v = h->ring_v;
+    sp.stage_k = h->bstage_k; sp.stage_v = h->bstage_v; sp.rope_pairs = p.rope_pairs;
+    sp.S = p.S; sp.layer_count = lc; sp.layer_begin = lb; sp.N_total = p.N_total; sp.Hkv = p.Hkv;
+    sp.A = p.A; sp.R = h->R; sp.Rp_ring = h->Rp; sp.inst_start = sc.inst_start;
+    sp.rows = rows; sp.rows_stage = h->bstage_rows;
+    sp.boost_k = k_boost; sp.boost_v = v_boost; sp.n_older = older;
+    DSC_CUDA(dsc::launch_stage_instant(sp, st));
+    h->launches++;
+    p.staged = 1;
+    p.A = 0; p.ring_start = 0; p.ring_count = rows; p.R = h->bstage_rows; p.Rp = h->bstage_rows;
+    p.self_k = p.self_v = nullptr; p.n_self = 0;
+    p.tmap_k = h->tmap_bk; p.tmap_v = h->tmap_bv;
+  }
+  return run_attention(h, p, h->impl_build, 0, st);
+}
+
+dscache_status dscache_attend_boost(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                                    const void* v_self, int32_t n_q, const void* k_boost, const void* v_boost,
+                                    int32_t n_boost, void* o, void* stream) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
+  if (h->cfg.instant_frames < 1) return fail(DSCACHE_E_CONFIG, "l_I = 0: there is no instant frame to boost");
+  if (!k_boost || !v_boost || !k_self || !v_self) return fail(DSCACHE_E_ARG, "null k/v pointers");
+  if (n_boost < 1) return fail(DSCACHE_E_ARG, "n_boost must be >= 1");
+  dscache_status s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  const dscache_config& c = h->cfg;
+  const size_t row = (size_t)c.num_kv_heads * c.head_dim * h->elem;      // one token of one problem
+  const size_t P = (size_t)c.num_streams * lc;
+  const size_t need = P * (size_t)(n_boost + n_q) * row;
+  DeviceGuard dg(c.device);
+  if (need > h->boost_bytes) {
+    cudaFree(h->boost_k); cudaFree(h->boost_v);
+    h->boost_k = h->boost_v = nullptr; h->boost_bytes = 0;
+    if (cudaMalloc(&h->boost_k, need) != cudaSuccess || cudaMalloc(&h->boost_v, need) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DSCACHE_E_OOM, "boost scratch allocation failed");
+    }
+    h->boost_bytes = need;
+  }
+  dsc::AttnParams p{};
+  s = prep_attend(h, lb, lc, q, h->boost_k, h->boost_v, n_boost + n_q, n_q, o, false, p, c.tokens_per_frame);
+  if (s != DSCACHE_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  // self segment [boosted frame | query chunk] per problem: [P][n_boost + n_q][Hkv][d]
+  const size_t pitch = (size_t)(n_boost + n_q) * row;
+  DSC_CUDA(cudaMemcpy2DAsync(h->boost_k, pitch, k_boost, n_boost * row, n_boost * row, P, cudaMemcpyDeviceToDevice, st));
+  DSC_CUDA(cudaMemcpy2DAsync(h->boost_v, pitch, v_boost, n_boost * row, n_boost * row, P, cudaMemcpyDeviceToDevice, st));
+  DSC_CUDA(cudaMemcpy2DAsync((char*)h->boost_k + n_boost * row, pitch, k_self, n_q * row, n_q * row, P,
+                             cudaMemcpyDeviceToDevice, st));
+  DSC_CUDA(cudaMemcpy2DAsync((char*)h->boost_v + n_boost * row, pitch, v_self, n_q * row, n_q * row, P,
+                             cudaMemcpyDeviceToDevice, st));
+  return run_attention(h, p, h->impl_attend, 1, st);
 }
 
 dscache_status dscache_attend_partial(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,

@@ -83,6 +83,10 @@ struct StageParams {
   void* stage_k; void* stage_v;              // [S][N][Hkv][rows_stage][d]
   const float4* rope_pairs;
   int S, layer_count, layer_begin, N_total, Hkv, A, R, Rp_ring, inst_start, rows, rows_stage;
+  // resolution boost (NEXT-4): rows >= A + n_older come from the caller's re-encoded newest
+  // frame boost_k/v [S][layer_count][rows - A - n_older][Hkv][d] instead of the ring; null = off
+  const void* boost_k; const void* boost_v;
+  int n_older;
 };
 
 // kernels (launchers return cudaGetLastError())

@@ -159,6 +159,11 @@ __global__ void __launch_bounds__(256) stage_instant_kernel(StageParams p) {
     if (row < p.A) {
       sk = reinterpret_cast<const uint4*>(p.sink_k) + (head * p.A + row) * 16;
       sv = reinterpret_cast<const uint4*>(p.sink_v) + (head * p.A + row) * 16;
+    } else if (p.boost_k != nullptr && row >= p.A + p.n_older) {
+      const int nb = p.rows - p.A - p.n_older;
+      const long long br = ((s * p.layer_count + l) * nb + (row - p.A - p.n_older)) * p.Hkv + g;
+      sk = reinterpret_cast<const uint4*>(p.boost_k) + br * 16;
+      sv = reinterpret_cast<const uint4*>(p.boost_v) + br * 16;
     } else {
       int slot = p.inst_start + row - p.A;
       if (slot >= p.R) slot -= p.R;

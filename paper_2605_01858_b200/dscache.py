@@ -55,7 +55,8 @@ class State(ctypes.Structure):
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
            "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
-           "dscache_attn_impl", "dscache_last_error", "dscache_attend_partial", "dscache_combine_partials"]
+           "dscache_attn_impl", "dscache_last_error", "dscache_attend_partial", "dscache_combine_partials",
+           "dscache_build_instant_boost", "dscache_attend_boost"]
 
 _lib = None
 
@@ -92,6 +93,8 @@ def load_library(path: str = LIB_PATH):
         "dscache_attn_impl": ([P, I32], I32),
         "dscache_attend_partial": ([P, I32, I32, P, P, P, I32, I32, I32, P, P, P], I32),
         "dscache_combine_partials": ([P, I32, I64, P, P, P, P], I32),
+        "dscache_build_instant_boost": ([P, I32, I32, P, P, P, I32, P, P], I32),
+        "dscache_attend_boost": ([P, I32, I32, P, P, P, I32, P, P, I32, P, P], I32),
         "dscache_last_error": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -224,6 +227,46 @@ class DSCache:
         self._t(o, "o", q.shape)
         _check(_lib.dscache_attend(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, _ptr(o),
                                    _stream_ptr(stream)))
+        return o
+
+    def build_instant_boost(self, q_inst: torch.Tensor, k_boost: torch.Tensor, v_boost: torch.Tensor,
+                            o_inst: Optional[torch.Tensor] = None, layer_begin: int = 0,
+                            layer_count: Optional[int] = None, stream=None) -> torch.Tensor:
+        """Instant cache with the newest frame re-encoded:
+        k_boost/v_boost [S][lc][n_boost][Hkv][d] replace the newest frame's ring K/V;
+        q_inst [S][lc][C_t - tpf + n_boost][Hq][d] -> O_inst (same shape)."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        n_boost = int(k_boost.shape[2])
+        self._t(k_boost, "k_boost", (c.num_streams, lc, n_boost, c.num_kv_heads, c.head_dim))
+        self._t(v_boost, "v_boost", k_boost.shape)
+        C_t = self.state(lb)["instant_tokens"]
+        shape = (c.num_streams, lc, C_t - c.tokens_per_frame + n_boost, c.num_q_heads, c.head_dim)
+        self._t(q_inst, "q_inst", shape)
+        if o_inst is None:
+            o_inst = torch.empty(shape, dtype=self.torch_dtype, device=self.device)
+        self._t(o_inst, "o_inst", shape)
+        _check(_lib.dscache_build_instant_boost(self._h, lb, lc, _ptr(q_inst), _ptr(k_boost), _ptr(v_boost), n_boost,
+                                                _ptr(o_inst), _stream_ptr(stream)))
+        return o_inst
+
+    def attend_boost(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, k_boost: torch.Tensor,
+                     v_boost: torch.Tensor, o: Optional[torch.Tensor] = None, layer_begin: int = 0,
+                     layer_count: Optional[int] = None, stream=None) -> torch.Tensor:
+        """attend() over a final cache whose newest instant frame is the boosted re-encoding."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        n_q, n_boost = int(q.shape[2]), int(k_boost.shape[2])
+        self._t(q, "q", (c.num_streams, lc, n_q, c.num_q_heads, c.head_dim))
+        self._t(k_self, "k_self", (c.num_streams, lc, n_q, c.num_kv_heads, c.head_dim))
+        self._t(v_self, "v_self", k_self.shape)
+        self._t(k_boost, "k_boost", (c.num_streams, lc, n_boost, c.num_kv_heads, c.head_dim))
+        self._t(v_boost, "v_boost", k_boost.shape)
+        if o is None:
+            o = torch.empty(q.shape, dtype=self.torch_dtype, device=self.device)
+        self._t(o, "o", q.shape)
+        _check(_lib.dscache_attend_boost(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, _ptr(k_boost),
+                                         _ptr(v_boost), n_boost, _ptr(o), _stream_ptr(stream)))
         return o
 
     def attend_partial(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, part: int, n_parts: int,

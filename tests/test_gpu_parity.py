@@ -436,6 +436,103 @@ def test_build_instant_newest_parity(lib, name):
     h.close()
 
 
+@pytest.mark.parametrize("name,boost", [("c1", 1.0), ("c1", 2.25), ("c2", 1.0), ("c2", 2.25), ("c2", 4.0),
+                                        ("c5", 4.0)])
+def test_boosted_newest_frame_parity(lib, name, boost):
+    """NEXT-4 resolution boost: build_instant_boost / attend_boost vs the fp64 oracle, with
+    n_boost = boost * tpf re-encoded tokens (x1.5 / x2 spatial -> 2.25x / 4x tokens); t = 0
+    has no older instant frame (window of the build empty), and boost = 1 with the ring's own
+    frame must reproduce the plain build / attend."""
+    import torch as _t
+    cfg = synth.CONFIGS[name]
+    steps = [0, 2, 3, 10, cfg.num_frames - 1]
+    dev = _t.device("cuda", 0)
+    exact = [(0, 0)] if cfg.num_streams == 1 else [(0, 0), (37, 2)]
+    h = D.DSCache.from_config(cfg)
+    S, N, tpf = cfg.num_streams, cfg.num_layers, cfg.tokens_per_frame
+    nb = int(round(boost * tpf))
+    def batch(fn, shape):
+        t_ = (_t.randn((S, N) + shape, device=dev) * cfg.scale).to(cfg.torch_dtype)
+        for (s_, l_) in exact:
+            t_[s_, l_] = fn(s_, l_).to(dev)
+        return t_
+    shp = (cfg.sink_tokens, cfg.num_kv_heads, cfg.head_dim)
+    h.append_frame(batch(lambda s_, l_: synth.sink_kv(cfg, s_, l_)[0], shp),
+                   batch(lambda s_, l_: synth.sink_kv(cfg, s_, l_)[1], shp))
+    bshp = (nb, cfg.num_kv_heads, cfg.head_dim)
+    for t in range(max(steps) + 1):
+        fshp = (tpf, cfg.num_kv_heads, cfg.head_dim)
+        kv = {sl: synth.frame_kv(cfg, sl[0], sl[1], t) for sl in exact}
+        k_f = batch(lambda s_, l_: kv[(s_, l_)][0], fshp)
+        v_f = batch(lambda s_, l_: kv[(s_, l_)][1], fshp)
+        h.append_frame(k_f, v_f)
+        if t not in steps:
+            continue
+        C_t = h.state(0)["instant_tokens"]
+        n_inst = C_t - tpf + nb
+        if boost == 1.0:      # the newest frame "re-encoded" as itself
+            bkv = {sl: kv[sl] for sl in exact}
+            kb, vb = k_f.clone(), v_f.clone()
+        else:
+            bkv = {sl: synth.boost_kv(cfg, sl[0], sl[1], t, nb) for sl in exact}
+            kb = batch(lambda s_, l_: bkv[(s_, l_)][0], bshp)
+            vb = batch(lambda s_, l_: bkv[(s_, l_)][1], bshp)
+        qi = batch(lambda s_, l_: synth.instant_q(cfg, s_, l_, t, n_inst), (n_inst, cfg.num_q_heads, cfg.head_dim))
+        qkv = {sl: synth.query_qkv(cfg, sl[0], sl[1], t) for sl in exact}
+        qshp = (cfg.query_tokens, cfg.num_q_heads, cfg.head_dim)
+        kshp = (cfg.query_tokens, cfg.num_kv_heads, cfg.head_dim)
+        q = batch(lambda s_, l_: qkv[(s_, l_)][0], qshp)
+        kq = batch(lambda s_, l_: qkv[(s_, l_)][1], kshp)
+        vq = batch(lambda s_, l_: qkv[(s_, l_)][2], kshp)
+        oi = h.build_instant_boost(qi, kb, vb)
+        o = h.attend_boost(q, kq, vq, kb, vb)
+        if boost == 1.0:
+            oi_plain = h.build_instant(qi)
+            o_plain = h.attend(q, kq, vq)
+        _t.cuda.synchronize()
+        for (s_, l_) in exact:
+            inp = StreamInputs(cfg, s_, l_)
+            sch = step_schedule(cfg, t)
+            f64 = lambda x: x.double().numpy()
+            kb64, vb64 = f64(bkv[(s_, l_)][0]), f64(bkv[(s_, l_)][1])
+            ref_i = O.instant_cache_output_boosted(sch, inp.sink(), inp.frame_kv, f64(synth.instant_q(cfg, s_, l_, t, n_inst)),
+                                                   kb64, vb64, cfg.rope_theta)
+            qq, kk, vv = (f64(x) for x in qkv[(s_, l_)])
+            ref = O.attend_output_boosted(sch, inp.sink(), inp.frame_kv, qq, kk, vv, kb64, vb64, cfg.rope_theta)
+            ma, rl = assert_close(oi[s_, l_].float().cpu(), ref_i, cfg.dtype, f"boost build t={t}")
+            REPORT.append((f"{name}-boost{boost}", "O_inst", t, s_, l_, ma, rl))
+            ma, rl = assert_close(o[s_, l_].float().cpu(), ref, cfg.dtype, f"boost attend t={t}")
+            REPORT.append((f"{name}-boost{boost}", "O", t, s_, l_, ma, rl))
+        if boost == 1.0:     # same keys, same ids: the plain calls agree to rounding
+            assert (oi.float() - oi_plain.float()).abs().max().item() <= (1e-5 if cfg.dtype == "fp32" else 2e-2)
+            assert (o.float() - o_plain.float()).abs().max().item() <= (1e-5 if cfg.dtype == "fp32" else 2e-2)
+    h.close()
+
+
+def test_boost_abi_errors(lib):
+    import ctypes
+    cfg = synth.CONFIGS["c2"]
+    dev = torch.device("cuda", 0)
+    h = D.DSCache.from_config(cfg)
+    buf = torch.zeros(1 << 22, dtype=cfg.torch_dtype, device=dev)
+    p = ctypes.c_void_p(buf.data_ptr())
+    L = D._lib
+    assert L.dscache_build_instant_boost(h._h, 0, 1, p, p, p, 5, p, None) == D.E_STATE   # no frame yet
+    A = cfg.sink_tokens
+    sk = torch.zeros((1, 1, A, cfg.num_kv_heads, cfg.head_dim), dtype=cfg.torch_dtype, device=dev)
+    fk = torch.zeros((1, 1, cfg.tokens_per_frame, cfg.num_kv_heads, cfg.head_dim), dtype=cfg.torch_dtype, device=dev)
+    h.append_frame(sk, sk)
+    h.append_frame(fk, fk)
+    assert L.dscache_build_instant_boost(h._h, 0, 1, p, p, p, 0, p, None) == D.E_ARG      # n_boost < 1
+    assert L.dscache_build_instant_boost(h._h, 0, 1, None, p, p, 5, p, None) == D.E_ARG   # null q
+    assert L.dscache_attend_boost(h._h, 0, 1, p, p, p, 0, p, p, 5, p, None) == D.E_ARG    # n_q < 1
+    assert L.dscache_attend_boost(h._h, 0, 1, p, p, p, 4, p, p, 0, p, None) == D.E_ARG    # n_boost < 1
+    big = cfg.max_position
+    assert L.dscache_build_instant_boost(h._h, 0, 1, p, p, p, big, p, None) == D.E_POS_OVERFLOW
+    torch.cuda.synchronize()
+    h.close()
+
+
 def test_zz_print_report(lib):
     for r in REPORT:
         print("PARITY %-16s %-6s t=%-5d s=%-3d l=%-3d max_abs=%.3e rel_l2=%.3e" % r)

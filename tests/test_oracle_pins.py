@@ -572,3 +572,83 @@ def test_decode_token_by_token_matches_brute_force():
                 keys.append((n, list(k_self[j, gh]), list(v_self[j, gh]))); n += 1
             ref = _brute_attend(list(qg[g, h]), n - 1, keys, cfg.rope_theta)
             assert np.abs(np.array(ref) - o[0, h]).max() < 1e-12
+
+
+# --------------------------------------------------------------------------- boosted newest frame (NEXT-4)
+def test_boost_with_the_buffer_frame_reduces_to_eq7_and_eq8():
+    """Re-encoding the newest frame as itself (n_boost = tpf, the ring's own K/V) must give
+    the plain instant cache (Eq. 7) and the plain final attention (Eq. 8)."""
+    cfg = synth.CONFIGS["c1"]
+    inp = StreamInputs(cfg, 0, 0)
+    for t in (0, 2, 9):
+        sch = step_schedule(cfg, t)
+        k, v = inp.frame_kv(sch.instant_frames[-1])
+        qi = inp.instant_q(t, sch.C_t)
+        a = O.instant_cache_output(sch, inp.sink(), inp.frame_kv, qi, cfg.rope_theta)
+        b = O.instant_cache_output_boosted(sch, inp.sink(), inp.frame_kv, qi, k, v, cfg.rope_theta)
+        assert np.array_equal(a, b)
+        q, ks, vs = inp.query(t)
+        a = O.attend_output(sch, inp.sink(), inp.frame_kv, q, ks, vs, cfg.rope_theta)
+        b = O.attend_output_boosted(sch, inp.sink(), inp.frame_kv, q, ks, vs, k, v, cfg.rope_theta)
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("n_boost", [1, 7])
+def test_boost_brute_force_full_history(n_boost):
+    """Pure-Python loops over the full token history: the buffer B_t is the last l_I frames
+    of the history; its newest frame is swapped for n_boost re-encoded tokens
+    in both the instant build and the final cache; ids consecutive from 0."""
+    cfg = _upd_cfg()
+    inp = StreamInputs(cfg, 0, 0)
+    sk, sv = inp.sink()
+    A, tpf, lI, lU = cfg.sink_tokens, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames
+    grp = cfg.num_q_heads // cfg.num_kv_heads
+    gen = np.random.default_rng(11)
+    history = []
+    for t in range(7):
+        fk, fv = inp.frame_kv(t)
+        history += [(k, v) for k, v in zip(fk, fv)]
+        sch = step_schedule(cfg, t)
+        kb = gen.standard_normal((n_boost, cfg.num_kv_heads, cfg.head_dim))
+        vb = gen.standard_normal((n_boost, cfg.num_kv_heads, cfg.head_dim))
+        inst = history[-min(t + 1, lI) * tpf:][:-tpf]           # buffer minus its newest frame
+        window = history[-min(t + 1, lI + lU) * tpf:][:-tpf]    # past + older instant frames
+        qi = gen.standard_normal((len(inst) + n_boost, cfg.num_q_heads, cfg.head_dim))
+        q, kq, vq = inp.query(t)
+        oi = O.instant_cache_output_boosted(sch, (sk, sv), inp.frame_kv, qi, kb, vb, cfg.rope_theta)
+        o = O.attend_output_boosted(sch, (sk, sv), inp.frame_kv, q, kq, vq, kb, vb, cfg.rope_theta)
+        for h in range(cfg.num_q_heads):
+            g = h // grp
+            base = [(j, list(sk[j, g]), list(sv[j, g])) for j in range(A)]
+            keys = base + [(A + n, list(k[g]), list(v[g])) for n, (k, v) in enumerate(inst)]
+            keys += [(A + len(inst) + j, list(kb[j, g]), list(vb[j, g])) for j in range(n_boost)]
+            for i in range(qi.shape[0]):
+                ref = _brute_attend(list(qi[i, h]), A + i, keys, cfg.rope_theta)
+                assert np.abs(np.array(ref) - oi[i, h]).max() < 1e-12
+            keys = base + [(A + n, list(k[g]), list(v[g])) for n, (k, v) in enumerate(window)]
+            keys += [(A + len(window) + j, list(kb[j, g]), list(vb[j, g])) for j in range(n_boost)]
+            L = len(keys)
+            keys += [(L + i, list(kq[i, g]), list(vq[i, g])) for i in range(q.shape[0])]
+            for i in range(q.shape[0]):
+                ref = _brute_attend(list(q[i, h]), L + i, keys, cfg.rope_theta)
+                assert np.abs(np.array(ref) - o[i, h]).max() < 1e-12
+
+
+def test_boost_leaves_older_instant_rows_and_ignores_the_past():
+    """Causality: instant tokens before the newest frame never see it, so their rows equal
+    the plain Eq. 7 rows; and the boosted build is independent of U."""
+    cfg = synth.CONFIGS["c1"]
+    inp = StreamInputs(cfg, 0, 0)
+    t = 9
+    sch = step_schedule(cfg, t)
+    qi = inp.instant_q(t, sch.C_t)
+    kb, vb = (x.double().numpy() for x in synth.boost_kv(cfg, 0, 0, t, 3 * cfg.tokens_per_frame))
+    older = sch.C_t - cfg.tokens_per_frame
+    q_b = np.concatenate([qi[:older], np.random.default_rng(5).standard_normal((kb.shape[0],) + qi.shape[1:])])
+    plain = O.instant_cache_output(sch, inp.sink(), inp.frame_kv, qi, cfg.rope_theta)
+    boosted = O.instant_cache_output_boosted(sch, inp.sink(), inp.frame_kv, q_b, kb, vb, cfg.rope_theta)
+    assert np.allclose(plain[:older], boosted[:older], rtol=0, atol=1e-13)
+    # poison every past frame: the build must not change
+    sch2 = O.StepSchedule(sch.t, sch.instant_frames, [], [], sch.tokens_per_frame, sch.sink_tokens)
+    again = O.instant_cache_output_boosted(sch2, inp.sink(), inp.frame_kv, q_b, kb, vb, cfg.rope_theta)
+    assert np.array_equal(boosted, again)

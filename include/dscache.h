@@ -146,6 +146,32 @@ dscache_status dscache_build_instant(dscache_t h, int32_t layer_begin, int32_t l
 dscache_status dscache_build_instant_newest(dscache_t h, int32_t layer_begin, int32_t layer_count,
                                             const void* q_new, void* o_new, void* stream);
 
+/* Fused all-gather epilogue of the KV-head split (P2): the attend
+ * of this handle's KV heads (Eq. 8, as dscache_attend) with every output row stored by the
+ * attention kernel itself to EACH of n_peers gathered-O buffers, instead of to a local O
+ * followed by an all-gather.  peer_o[j] is a device pointer mapped in this process (a local
+ * buffer, a P2P-enabled peer allocation, or a dscache_ipc_open mapping of another rank's
+ * buffer), bf16 [S][layer_count][n_q][hq_total][d]; q head h of this handle lands at head
+ * head_offset + h.  The stores are ordinary global stores on `stream`: the caller orders
+ * them before any reader (stream sync + barrier, or an event).  Other arguments as
+ * dscache_attend.  E_ARG unless 1 <= n_peers <= 8 with non-null pointers and
+ * head_offset + Hq <= hq_total; E_CONFIG off the tcgen05 path. */
+dscache_status dscache_attend_peers(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                                    const void* q, const void* k_self, const void* v_self, int32_t n_q,
+                                    void* const* peer_o, int32_t n_peers, int32_t hq_total, int32_t head_offset,
+                                    void* stream);
+
+/* CUDA IPC plumbing for dscache_attend_peers across processes of one node (NVLink /
+ * NVSwitch): dscache_ipc_handle writes the 64-byte IPC handle of the device allocation
+ * containing dev_ptr to handle_out and dev_ptr's byte offset inside it to *offset_out (a
+ * caching allocator hands out interior pointers); dscache_ipc_open maps another process's
+ * handle on `device` (lazy peer access enabled) and returns the allocation's base (add the
+ * offset); dscache_ipc_close unmaps it.  E_CUDA on any CUDA error (e.g. opening a handle in
+ * the process that exported it). */
+dscache_status dscache_ipc_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out);
+dscache_status dscache_ipc_open(int32_t device, const void* handle, void** dev_ptr_out);
+dscache_status dscache_ipc_close(int32_t device, void* dev_ptr);
+
 /* Resolution-boosted newest frame ("the buffer inputs may be temporarily
  * re-encoded, e.g. using a higher-resolution version of X_{t+1}, without modifying the
  * buffer itself"; PAPER.md:695 / Table "spa" PAPER.md:719-749).  The

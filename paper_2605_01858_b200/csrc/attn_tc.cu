@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 #endif
 #if DSC_EPIROT
-      if (w.staged && p.n_splits == 1 && p.split_only < 0) {
+      if (w.staged && p.n_splits == 1 && p.split_only < 0 && p.n_peers == 0) {
         // the rotation warpgroup writes O out.  l goes into Q tile qt of this item's buffer
         // (its last QK^T has completed; the buffer is refilled by the rotation warpgroup
         // itself, after this epilogue).  Waiting for the previous item's O release keeps the
@@ -491,7 +491,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(bar(B_OF + qt));      // O_qt may be overwritten by the next item
         }
         if (!valid_row) continue;
-        if (p.n_splits == 1 && p.split_only < 0) {
+        if (p.n_splits == 1 && p.split_only < 0 && p.n_peers > 0) {
+          // fused all-gather: the same row to every peer's gathered O (NVLink stores)
+          const long long prow = ((long long)w.pp * p.n_q + qi) * p.o_hq + p.o_head_off + h;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint32_t q[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              q[j] = pack_bf16(__uint_as_float(o[16 * v + 2 * j]) * inv, __uint_as_float(o[16 * v + 2 * j + 1]) * inv);
+#pragma unroll 1
+            for (int r = 0; r < p.n_peers; ++r)
+              stg256(reinterpret_cast<__nv_bfloat16*>(p.peer_o[r]) + prow * 128 + 64 * hf + 16 * v, q);
+          }
+        } else if (p.n_splits == 1 && p.split_only < 0) {
           // 32-byte stores (STG.256): each one fills a whole L2 sector of this thread's row
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) + orow * 128 + 64 * hf;
 #pragma unroll
@@ -569,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (q_next) prep_q(kk + 1, nidx_q);
         gt += w.n_tiles;
 #if DSC_EPIROT
-        if (p.n_splits == 1 && p.split_only < 0) {   // O epilogue of both Q tiles (see DSC_EPIROT)
+        if (p.n_splits == 1 && p.split_only < 0 && p.n_peers == 0) {   // O epilogue of both Q tiles (DSC_EPIROT)
           const uint32_t tq = tmem + ((uint32_t)((lt >> 5) * 32) << 16);
 #pragma unroll 1
           for (int qt = 0; qt < 2; ++qt) {
@@ -953,7 +966,10 @@ cudaError_t launch_attn_tc6(const AttnParams& pa, const AttnParams* pb, cudaStre
 #endif
 
 cudaError_t launch_attn_tc2(const AttnParams& pa, const AttnParams* pb, cudaStream_t st) {
-  if (DSC_V6) return launch_attn_tc6(pa, pb, st);
+  if (DSC_V6) {
+    if (pa.n_peers > 0 || (pb && pb->n_peers > 0)) return cudaErrorNotSupported;   // v6 has no peer epilogue
+    return launch_attn_tc6(pa, pb, st);
+  }
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -617,6 +617,67 @@ dscache_status dscache_attend_partial(dscache_t h, int32_t lb, int32_t lc, const
   return run_attention(h, p, h->impl_attend, 1, (cudaStream_t)stream);
 }
 
+dscache_status dscache_attend_peers(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                                    const void* v_self, int32_t n_q, void* const* peer_o, int32_t n_peers,
+                                    int32_t hq_total, int32_t head_offset, void* stream) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
+  if (!peer_o || n_peers < 1 || n_peers > dsc::kMaxPeers)
+    return fail(DSCACHE_E_ARG, "need 1 <= n_peers <= " + std::to_string(dsc::kMaxPeers) + " destination buffers");
+  for (int i = 0; i < n_peers; ++i)
+    if (!peer_o[i]) return fail(DSCACHE_E_ARG, "null peer_o[" + std::to_string(i) + "]");
+  if (head_offset < 0 || head_offset + h->cfg.num_q_heads > hq_total)
+    return fail(DSCACHE_E_ARG, "head_offset + Hq must be <= hq_total");
+  if (h->impl_attend != DSCACHE_IMPL_TC)
+    return fail(DSCACHE_E_CONFIG, "attend_peers runs on the tcgen05 path (bf16, d=128, split-half RoPE)");
+  dsc::AttnParams p{};
+  dscache_status s = prep_attend(h, lb, lc, q, k_self, v_self, n_q, n_q, peer_o[0], false, p);
+  if (s != DSCACHE_OK) return s;
+  for (int i = 0; i < n_peers; ++i) p.peer_o[i] = peer_o[i];
+  p.n_peers = n_peers; p.o_hq = hq_total; p.o_head_off = head_offset;
+  DeviceGuard dg(h->cfg.device);
+  return run_attention(h, p, h->impl_attend, 1, (cudaStream_t)stream);
+}
+
+dscache_status dscache_ipc_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out) {
+  if (!dev_ptr || !handle_out || !offset_out) return fail(DSCACHE_E_ARG, "null pointer");
+  // the handle names the whole allocation; report where dev_ptr sits inside it
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    DSC_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) return fail(DSCACHE_E_CUDA, "cuMemGetAddressRange unavailable");
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(DSCACHE_E_CUDA, "cuMemGetAddressRange failed (not a device allocation?)");
+  cudaIpcMemHandle_t hd;
+  DSC_CUDA(cudaIpcGetMemHandle(&hd, reinterpret_cast<void*>(base)));
+  std::memcpy(handle_out, &hd, sizeof(hd));
+  *offset_out = (int64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_ipc_open(int32_t device, const void* handle, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return fail(DSCACHE_E_ARG, "null pointer");
+  DeviceGuard dg(device);
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, sizeof(hd));
+  DSC_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, hd, cudaIpcMemLazyEnablePeerAccess));
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_ipc_close(int32_t device, void* dev_ptr) {
+  if (!dev_ptr) return fail(DSCACHE_E_ARG, "null pointer");
+  DeviceGuard dg(device);
+  DSC_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return DSCACHE_OK;
+}
+
 dscache_status dscache_combine_partials(dscache_t h, int32_t n_parts, int64_t rows, const float* o_parts,
                                         const float* lse_parts, void* o, void* stream) {
   if (!h) return fail(DSCACHE_E_ARG, "null handle");

@@ -11,6 +11,7 @@ constexpr int kTileN = 64;    // keys per attention tile (tcgen05 N of QK^T, K o
 constexpr int kTileM = 128;   // query rows per Q tile (tcgen05 M)
 constexpr int kMirror = 128;  // ring rows after slot R-1 mirroring slots [0, 128): a 128-row tile never wraps
 constexpr int kTraceEvents = 40, kTraceTiles = 64;
+constexpr int kMaxPeers = 8;  // fused all-gather epilogue: destinations of every O row
 
 // One attention launch (build_instant or attend) over P = S * layer_count problems.
 // Keys of problem p, kv head g, in logical order L = 0, 1, ...:
@@ -53,6 +54,11 @@ struct AttnParams {
   // per-CTA event timeline (profiling); null = off.  [ntrace_cta][kTraceEvents][kTraceTiles] clock64
   long long* trace; int ntrace_cta;
   int dtype;                                 // 0 bf16, 1 fp32
+  // fused all-gather epilogue (P2 over peer memory): n_peers > 0 stores O row
+  // (pp, i, h) to EVERY peer_o[j] (bf16 [P][n_q][o_hq][d]) at head o_head_off + h instead
+  // of to o; peer_o are device pointers mapped in this process (local, P2P or CUDA IPC)
+  void* peer_o[kMaxPeers];
+  int n_peers, o_hq, o_head_off;
   // staged build (tcgen05 path): the keys are rows [0, ring_count) of the per-step staging
   // buffers [S*N*Hkv][Rp][d] holding sink ++ instant window with K ALREADY rotated at ids
   // 0..ring_count-1 (stage_instant_kernel); A = 0, ring_start = 0, no K rotation in-kernel

@@ -361,6 +361,13 @@ __global__ void __launch_bounds__(128) combine_kernel(AttnParams p) {
   uint2 out;
   out.x = *reinterpret_cast<uint32_t*>(&a);
   out.y = *reinterpret_cast<uint32_t*>(&b);
+  if (p.n_peers > 0) {   // fused all-gather epilogue: row (pp, i, h) to every peer at head o_head_off + h
+    const long long h = row % p.Hq, pi = row / p.Hq;
+    const long long prow = pi * p.o_hq + p.o_head_off + h;
+    for (int r = 0; r < p.n_peers; ++r)
+      reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.peer_o[r]) + prow * p.d)[lane] = out;
+    return;
+  }
   reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.o) + row * p.d)[lane] = out;
 }
 

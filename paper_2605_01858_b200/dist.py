@@ -14,6 +14,12 @@ Two partitions, both from the north_star:
   Softmax attention is invariant to how its key set is split, so the merge is exact up
   to rounding; G = 8 works for Hkv = 4, where P2 cannot.
 
+P2 has two gather paths: the NCCL all-gather of O (gather_heads, the baseline) and the
+fused all-gather epilogue (PeerOutputs + kv_split_attend_fused): every rank's
+gathered-O buffer is mapped into every other rank through CUDA IPC, and the attention
+kernel's epilogue stores each output row straight into all of them over NVLink, so no
+collective runs on the data path -- only a barrier before the buffers are read.
+
 The collective backend is whatever the process group was created with: NCCL
 over NVLink on the GPU box, gloo on CPU for the multi-process tests.
 """
@@ -100,3 +106,49 @@ def context_parallel_attend(dsc, q, k_self, v_self, group=None, **kw) -> torch.T
     o_part, lse = dsc.attend_partial(q, k_self, v_self, rank, world, **kw)
     o_all, l_all = gather_partials(o_part, lse, group)
     return dsc.combine_partials(o_all, l_all)
+
+
+class PeerOutputs:
+    """Gathered-O buffers of every rank, mapped into this process (P2 fused all-gather).
+
+    Each rank allocates its own [S][N][n_q][Hq][d] buffer (`local`); the CUDA IPC handles
+    (plus offsets inside the allocations) are exchanged with all_gather_object over
+    `group`, and every peer's buffer is opened on this rank's device.  `ptrs` lists the
+    device pointers in rank order (this rank's own buffer in its slot).  `ipc` = (handle,
+    open, close) functions, the library's by default (injectable for CPU tests)."""
+
+    def __init__(self, shape, dtype, device, group=None, ipc=None):
+        import torch.distributed as dist
+        from . import dscache as D
+        self.get_handle, self.open, self.close_fn = ipc or (D.ipc_handle, D.ipc_open, D.ipc_close)
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.device = torch.device(device)
+        self.local = torch.empty(shape, dtype=dtype, device=self.device)
+        mine = self.get_handle(self.local)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self.ptrs, self._opened = [], []
+        for r, (handle, offset) in enumerate(allh):
+            if r == self.rank:
+                self.ptrs.append(self.local.data_ptr())
+            else:
+                base = self.open(self.device.index or 0, handle)
+                self._opened.append(base)
+                self.ptrs.append(base + offset)
+
+    def close(self):
+        for base in self._opened:
+            self.close_fn(self.device.index or 0, base)
+        self._opened = []
+
+
+def kv_split_attend_fused(dsc, q, k_self, v_self, peers: PeerOutputs, hq_total: int, head_offset: int,
+                          group=None, **kw) -> torch.Tensor:
+    """P2 with the fused all-gather epilogue: this rank's heads are written by its attention
+    kernel into every rank's gathered O; after the local stream is drained and all ranks
+    pass the barrier, peers.local holds the full [S][N][n_q][Hq][d] output."""
+    import torch.distributed as dist
+    dsc.attend_peers(q, k_self, v_self, peers.ptrs, hq_total, head_offset, **kw)
+    torch.cuda.current_stream(peers.device).synchronize()
+    dist.barrier(group)
+    return peers.local

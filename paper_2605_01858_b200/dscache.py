@@ -56,7 +56,8 @@ EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache
            "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
            "dscache_attn_impl", "dscache_last_error", "dscache_attend_partial", "dscache_combine_partials",
-           "dscache_build_instant_boost", "dscache_attend_boost"]
+           "dscache_build_instant_boost", "dscache_attend_boost", "dscache_attend_peers",
+           "dscache_ipc_handle", "dscache_ipc_open", "dscache_ipc_close"]
 
 _lib = None
 
@@ -95,6 +96,10 @@ def load_library(path: str = LIB_PATH):
         "dscache_combine_partials": ([P, I32, I64, P, P, P, P], I32),
         "dscache_build_instant_boost": ([P, I32, I32, P, P, P, I32, P, P], I32),
         "dscache_attend_boost": ([P, I32, I32, P, P, P, I32, P, P, I32, P, P], I32),
+        "dscache_attend_peers": ([P, I32, I32, P, P, P, I32, ctypes.POINTER(P), I32, I32, I32, P], I32),
+        "dscache_ipc_handle": ([P, P, ctypes.POINTER(I64)], I32),
+        "dscache_ipc_open": ([I32, P, ctypes.POINTER(P)], I32),
+        "dscache_ipc_close": ([I32, P], I32),
         "dscache_last_error": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -118,6 +123,29 @@ def _stream_ptr(stream) -> ctypes.c_void_p:
     if stream is None:
         stream = torch.cuda.current_stream()
     return ctypes.c_void_p(stream.cuda_stream)
+
+
+def ipc_handle(t: torch.Tensor):
+    """(64-byte CUDA IPC handle of the allocation holding t, byte offset of t inside it)."""
+    load_library()
+    buf = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    _check(_lib.dscache_ipc_handle(ctypes.c_void_p(t.data_ptr()), buf, ctypes.byref(off)))
+    return buf.raw, int(off.value)
+
+
+def ipc_open(device: int, handle: bytes) -> int:
+    """Map another process's IPC handle on `device`; returns the allocation base (int):
+    add the exporter's offset."""
+    load_library()
+    out = ctypes.c_void_p()
+    _check(_lib.dscache_ipc_open(int(device), ctypes.create_string_buffer(bytes(handle), 64), ctypes.byref(out)))
+    return int(out.value)
+
+
+def ipc_close(device: int, ptr: int):
+    load_library()
+    _check(_lib.dscache_ipc_close(int(device), ctypes.c_void_p(ptr)))
 
 
 class DSCache:
@@ -268,6 +296,27 @@ class DSCache:
         _check(_lib.dscache_attend_boost(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, _ptr(k_boost),
                                          _ptr(v_boost), n_boost, _ptr(o), _stream_ptr(stream)))
         return o
+
+    def attend_peers(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, peer_ptrs, hq_total: int,
+                     head_offset: int, layer_begin: int = 0, layer_count: Optional[int] = None, stream=None):
+        """Fused all-gather epilogue (P2): this handle's attend rows are stored by the kernel into
+        every gathered-O buffer in `peer_ptrs` (device pointers as ints, or tensors on this
+        device), bf16 [S][lc][n_q][hq_total][d], q head h at head_offset + h."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        n_q = int(q.shape[2])
+        self._t(q, "q", (c.num_streams, lc, n_q, c.num_q_heads, c.head_dim))
+        self._t(k_self, "k_self", (c.num_streams, lc, n_q, c.num_kv_heads, c.head_dim))
+        self._t(v_self, "v_self", k_self.shape)
+        ptrs = []
+        for x in peer_ptrs:
+            if isinstance(x, torch.Tensor):
+                self._t(x, "peer O", (c.num_streams, lc, n_q, hq_total, c.head_dim))
+                x = x.data_ptr()
+            ptrs.append(int(x))
+        arr = (ctypes.c_void_p * max(len(ptrs), 1))(*ptrs)
+        _check(_lib.dscache_attend_peers(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, arr, len(ptrs),
+                                         int(hq_total), int(head_offset), _stream_ptr(stream)))
 
     def attend_partial(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, part: int, n_parts: int,
                        layer_begin: int = 0, layer_count: Optional[int] = None, stream=None):

@@ -207,3 +207,44 @@ def test_partial_merge_single_process(n_parts):
     merged = merge_partials(torch.from_numpy(np.stack([p[0] for p in parts])),
                             torch.from_numpy(np.stack([p[1] for p in parts])))
     assert np.abs(merged.numpy() - _oracle_attend(cfg, 2, 7)).max() < 1e-12
+
+
+def _worker_peer_outputs(rank, world, port, out_q):
+    """PeerOutputs handle exchange (P2 fused all-gather) with a stand-in IPC layer: rank r's
+    handle is b"r<r>" with offset 16*r; opening it yields base 10**6*(r+1)."""
+    from paper_2605_01858_b200.dist import PeerOutputs
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    opened, closed = [], []
+
+    def handle(t):
+        return b"r%d" % rank, 16 * rank
+
+    def open_(dev, hd):
+        opened.append(hd)
+        return 10 ** 6 * (int(hd[1:]) + 1)
+
+    peers = PeerOutputs((2, 3), torch.float32, "cpu", ipc=(handle, open_, lambda dev, p: closed.append(p)))
+    want = [peers.local.data_ptr() if r == rank else 10 ** 6 * (r + 1) + 16 * r for r in range(world)]
+    ok = peers.ptrs == want and sorted(opened) == sorted(b"r%d" % r for r in range(world) if r != rank)
+    peers.close()
+    ok = ok and sorted(closed) == sorted(10 ** 6 * (r + 1) for r in range(world) if r != rank)
+    out_q.put((rank, ok))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_outputs_exchange_rank_order(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_peer_outputs, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res), res

@@ -349,21 +349,39 @@ def run_e2e(args, cfg, lcfg, dsc, S, dev, stream, world, kvsplit):
             o = gather_heads(o)
         ho.copy_(o, non_blocking=True)
         del oi
+    pipelined = fused and not (kvsplit and world > 1)
+    if pipelined:
+        # the public host-fed path: step i+1's H2D overlaps step i's kernels and step i-1's D2H
+        from paper_2605_01858_b200.pipeline import HostStepPipeline
+        pipe = HostStepPipeline(dsc, q)
+
+        def one():
+            pipe.submit(hk, hv, hqi, hq, hks, hvs, ho)
     one()
     torch.cuda.synchronize()
     barrier(world)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(steps):
-        one()
-    b.record(stream)
+    if pipelined:
+        pipe.synchronize()
+        a.record(pipe.h2d)          # before the first H2D of the timed steps
+        for _ in range(steps):
+            one()
+        pipe.d2h.wait_stream(pipe.compute)
+        b.record(pipe.d2h)          # after the last D2H
+    else:
+        a.record(stream)
+        for _ in range(steps):
+            one()
+        b.record(stream)
     torch.cuda.synchronize()
     ms = max_over_ranks(a.elapsed_time(b), world)
     return {"value": round(cfg.num_streams * steps / (ms / 1e3), 2), "unit": "frames/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
             "note": "pinned host inputs (frame K/V, Q_inst, Q, K_self, V_self) copied H2D and the query "
-                    "answer O copied D2H every step, through DSCache.step (or append_frame/build_instant/attend "
-                    "with --api split)"}
+                    "answer O copied D2H every step" + (
+                        ", through pipeline.HostStepPipeline (DSCache.step on a compute stream; the next step's "
+                        "H2D and the previous step's D2H overlap it, 2 buffer slots)" if pipelined else
+                        ", through DSCache.step (or append_frame/build_instant/attend with --api split), one stream")}
 
 
 # ----------------------------------------------------------------------------- oracle (cpu baseline / reference arm)

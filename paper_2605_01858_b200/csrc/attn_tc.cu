@@ -56,15 +56,31 @@ constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
 #ifndef DSC_QROT
 #define DSC_QROT 1
 #endif
-#ifndef DSC_QDB   // double-buffered Q tiles (next item's Q loaded + rotated during the current item)
-#define DSC_QDB DSC_QROT
+// DSC_QLDG 1: the rotation warpgroup reads Q rows from global into registers, rotates and
+// stores them once (else cp.async into the tile, then an in-place rotation pass)
+#ifndef DSC_QLDG
+#define DSC_QLDG 0
 #endif
-static_assert(!DSC_QROT || DSC_QDB, "DSC_QROT needs the Q double buffer");
+// DSC_QSINGLE 1: one Q tile set; the rotation warpgroup refills it for the next item as
+// soon as the current item's last QK^T has completed (B_QE is committed right after that
+// MMA, two tiles before the item ends), and the 64 KB the second set took become K/V
+// stages (5 + 5): more TMA loads in flight against the HBM latency
+#ifndef DSC_QSINGLE
+#define DSC_QSINGLE 0
+#endif
+#ifndef DSC_QDB   // double-buffered Q tiles (next item's Q loaded + rotated during the current item)
+#define DSC_QDB (DSC_QROT && !DSC_QSINGLE)
+#endif
+static_assert(!DSC_QROT || DSC_QDB || DSC_QSINGLE, "DSC_QROT needs the Q double buffer or DSC_QSINGLE");
+static_assert(!DSC_QSINGLE || (DSC_QROT && !DSC_QDB), "DSC_QSINGLE is the single-set variant of DSC_QROT");
+#if DSC_QSINGLE && defined(DSC_SORDER) && DSC_SORDER != 1
+#error "DSC_QSINGLE commits the Q-free barrier in the DSC_SORDER 1 MMA loop"
+#endif
 #ifndef DSC_KST
-#define DSC_KST (DSC_QDB ? 3 : 6)
+#define DSC_KST (DSC_QDB ? 3 : (DSC_QSINGLE ? 5 : 6))
 #endif
 #ifndef DSC_VST
-#define DSC_VST (DSC_QDB ? 3 : 4)
+#define DSC_VST (DSC_QDB ? 3 : (DSC_QSINGLE ? 5 : 4))
 #endif
 constexpr int KST = DSC_KST;                  // K stages (raw -> rotated in place)
 constexpr int VST = DSC_VST;                  // V stages
@@ -159,7 +175,7 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 #ifndef DSC_EPIROT
 #define DSC_EPIROT 0
 #endif
-static_assert(!DSC_EPIROT || DSC_QROT, "DSC_EPIROT hands the epilogue to the rotation warpgroup of DSC_QROT");
+static_assert(!DSC_EPIROT || (DSC_QROT && !DSC_QSINGLE), "DSC_EPIROT hands l over through the other Q set");
 // DSC_QFIRST 1: the next item's Q tile is published before the epilogue, so its first S
 // MMAs run while O is read out
 #ifndef DSC_QFIRST
@@ -555,15 +571,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Q tiles (both) of item k into Q buffer k & 1; the buffer's previous item (k - 2) must be
     // done with it (its last QK^T MMA committed to B_QE)
     auto prep_q = [&](int k, int qidx) {
-      const uint32_t qb = (uint32_t)(k & 1);
-      if (k >= 2) mbar_wait(bar(B_QE + qb), ((k - 2) >> 1) & 1);
+      const uint32_t qb = DSC_QDB ? (uint32_t)(k & 1) : 0u;
+      if (DSC_QDB && k >= 2) mbar_wait(bar(B_QE + qb), ((k - 2) >> 1) & 1);
+      if (!DSC_QDB && k >= 1) mbar_wait(bar(B_QE), (k - 1) & 1);   // item k-1's last QK^T done
       const AttnParams& pq = ITEM_PARAMS(qidx);
       const Item wq = decode_item(pq, ITEM_LOCAL(qidx));
 #pragma unroll 1
       for (int q = 0; q < 2; ++q) {
         const uint32_t qtile = sbase + OFF_Q + (qb * 2 + q) * kQBytes;
-        issue_q_tile(pq, wq, q, lt, qtile);
-        rotate_q_tile(pq, wq, q, lt, qtile, 6);
+        if (DSC_QLDG) {
+          load_rotate_q_tile(pq, wq, q, lt, qtile);
+        } else {
+          issue_q_tile(pq, wq, q, lt, qtile);
+          rotate_q_tile(pq, wq, q, lt, qtile, 6);
+        }
         mbar_arrive(bar(B_Q + qb * 2 + q));
       }
     };
@@ -664,7 +685,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(bar(B_KF + ks));
         if (lt == 0) TRACE(EV_KDONE, g);
 #if DSC_QROT
-        if (jj == min(1, w.n_tiles - 1) && q_next) prep_q(kk + 1, nidx_q);   // after the item's first K tiles
+        if (!DSC_QSINGLE && jj == min(1, w.n_tiles - 1) && q_next) prep_q(kk + 1, nidx_q);   // after the item's first K tiles
 #endif
         if (dbg && c8 == 0) {
 #pragma unroll
@@ -678,7 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
 #if DSC_QROT
-      if (w.n_tiles == 0 && q_next) prep_q(kk + 1, nidx_q);
+      if ((DSC_QSINGLE || w.n_tiles == 0) && q_next) prep_q(kk + 1, nidx_q);   // single set: after every K tile
 #endif
       gt += w.n_tiles;
     }
@@ -832,6 +853,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (kk == 0 && lane == 0 && q_lo == 0) TRACE(EV_Q, 0);
         if (n > 0) issue_s(p, w, gt, w.t_begin);
         if (n > 1) issue_s(p, w, gt + 1, w.t_begin + 1);
+        if (DSC_QSINGLE && n <= 2) mma_commit_w(bar(B_QE));   // the item's last QK^T is issued
         for (int jj = 0; jj < n; ++jj) {
           const int g = gt + jj, vs = g % VST, buf = g & 1;
           const int nu = tile_segments(p, w, w.t_begin + jj).width;
@@ -888,6 +910,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma_commit_w(bar(B_S + qt * 2 + buf));
             }
           }
+          if (DSC_QSINGLE && more && jj + 3 == n) mma_commit_w(bar(B_QE));   // S(n-1) issued: Q set free when done
           mma_commit_w(bar(B_VE + vs));
           if (more) mma_commit_w(bar(B_KE + ks2));
 #else
@@ -906,7 +929,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (jj + 2 < n) issue_s(p, w, g + 2, w.t_begin + jj + 2);
 #endif
         }
-        if (DSC_QROT) mma_commit_w(bar(B_QE + qbuf));   // Q buffer of this item free once its MMAs are done
+        if (DSC_QROT && !DSC_QSINGLE) mma_commit_w(bar(B_QE + qbuf));   // Q buffer of this item free once its MMAs are done
         gt += n;
       }
       // drain: the last V-free commit tracks every MMA of this CTA

@@ -568,5 +568,97 @@ __device__ __forceinline__ void rotate_q_tile(const AttnParams& p, const Item& w
   fence_proxy_async();
 }
 
+// Q tile qt of item w straight from global memory into registers, rotated there at the
+// query ids and stored once into the SW128 tile (no cp.async staging copy + re-read:
+// 64 KB less shared-memory traffic per Q tile pair).  Thread lt rotates frequencies
+// 8*c8 .. 8*c8+7 (16-byte chunk c8 of the low and the high 64-column block) of rows
+// rg8*8 .. +7; the 8 threads of a row read its 2 x 128 contiguous bytes.
+__device__ __forceinline__ uint4 ldg128(const void* ptr) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr));
+  return r;
+}
+__device__ __forceinline__ void load_rotate_q_tile(const AttnParams& p, const Item& w, int qt, int lt, uint32_t qtile) {
+  const float4* __restrict__ rp = p.rope_pairs;
+  const __nv_bfloat16* __restrict__ Qg = reinterpret_cast<const __nv_bfloat16*>(p.q);
+  const int c8 = lt & 7, rg8 = lt >> 3;
+  const int row0 = w.m0 + qt * 128 + rg8 * 8;
+  int i = row0 / p.grp, hh = row0 % p.grp;
+  const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
+  const __nv_bfloat16* qbase = Qg + ((long long)w.pp * p.n_q) * p.Hq * 128 + (long long)w.g * p.grp * 128 + 8 * c8;
+  float2 cth[4], sth[4], cs[4], sn[4];
+  const int p0 = row0 < w.rows_total ? p.q_pos0 + i : 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float4 t = rp[32 + 4 * c8 + j];
+    cth[j] = make_float2(t.x, t.y);
+    sth[j] = make_float2(t.z, t.w);
+    const float4 u = rp[(long long)p0 * 32 + 4 * c8 + j];
+    cs[j] = make_float2(u.x, u.y);
+    sn[j] = make_float2(u.z, u.w);
+  }
+  int prev = p0;
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {   // 4 rows per pass: 8 x 16-byte loads in flight
+    int pos[4];
+    uint4 lo[4], hi[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool ok = row0 + half * 4 + k < w.rows_total;
+      pos[k] = ok ? p.q_pos0 + i : -1;
+      if (dbg && c8 == 0 && hh == 0 && ok) p.dbg_pos[p.A + p.R + p.dbg_M + i] = pos[k];
+      if (ok) {
+        const __nv_bfloat16* src = qbase + ((long long)i * p.Hq + hh) * 128;
+        lo[k] = ldg128(src);
+        hi[k] = ldg128(src + 64);
+      } else {
+        lo[k] = hi[k] = make_uint4(0, 0, 0, 0);
+      }
+      if (++hh == p.grp) { hh = 0; ++i; }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = rg8 * 8 + half * 4 + k, pk = pos[k];
+      const uint32_t addr = qtile + r * 128 + ((c8 ^ (r & 7)) << 4);
+      uint4 ylo = make_uint4(0, 0, 0, 0), yhi = make_uint4(0, 0, 0, 0);
+      if (pk >= 0) {
+        if (pk == prev) {
+        } else if (pk == prev + 1) {   // next id: advance (cos, sin) by R(theta)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 nc = __ffma2_rn(cs[j], cth[j], __fmul2_rn(make_float2(-sn[j].x, -sn[j].y), sth[j]));
+            sn[j] = __ffma2_rn(sn[j], cth[j], __fmul2_rn(cs[j], sth[j]));
+            cs[j] = nc;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 t = rp[(long long)pk * 32 + 4 * c8 + j];
+            cs[j] = make_float2(t.x, t.y);
+            sn[j] = make_float2(t.z, t.w);
+          }
+        }
+        prev = pk;
+        uint32_t ol[4], oh[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 av = bf2(get_w(lo[k], j)), bv = bf2(get_w(hi[k], j));
+          const float2 yl = __ffma2_rn(av, cs[j], __fmul2_rn(make_float2(-bv.x, -bv.y), sn[j]));   // a cos - b sin
+          const float2 yh = __ffma2_rn(av, sn[j], __fmul2_rn(bv, cs[j]));                        // a sin + b cos
+          ol[j] = pack_bf16(yl.x, yl.y);
+          oh[j] = pack_bf16(yh.x, yh.y);
+        }
+        ylo = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+        yhi = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+      } else {
+        prev = -3;
+      }
+      sts128(addr, ylo);
+      sts128(addr + 16384, yhi);
+    }
+  }
+  fence_proxy_async();
+}
+
 }  // namespace tcc
 }  // namespace dsc

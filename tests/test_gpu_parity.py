@@ -533,6 +533,39 @@ def test_boost_abi_errors(lib):
     h.close()
 
 
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_host_pipeline_equals_device_step(lib, name):
+    """pipeline.HostStepPipeline (pinned host inputs, 3 streams, 2 slots) gives the same bits
+    as DSCache.step on device-resident inputs, step after step (warm-up with C_t < C included)."""
+    from paper_2605_01858_b200.pipeline import HostStepPipeline
+    cfg = synth.CONFIGS[name]
+    dev = torch.device("cuda", 0)
+    S, N, tpf, Hkv, Hq, d, A = (cfg.num_streams, cfg.num_layers, cfg.tokens_per_frame, cfg.num_kv_heads,
+                                cfg.num_q_heads, cfg.head_dim, cfg.sink_tokens)
+    C, q = cfg.C, cfg.query_tokens
+    g = torch.Generator().manual_seed(5)
+    r = lambda *sh: (torch.randn(sh, generator=g) * cfg.scale).to(cfg.torch_dtype).pin_memory()   # noqa: E731
+    a, b = D.DSCache.from_config(cfg), D.DSCache.from_config(cfg)
+    sk, sv = r(S, N, A, Hkv, d), r(S, N, A, Hkv, d)
+    for h in (a, b):
+        h.append_frame(sk.to(dev), sv.to(dev))
+    pipe = HostStepPipeline(b, q)
+    outs = []
+    for t in range(cfg.instant_frames + 3):
+        C_t = min(t + 1, cfg.instant_frames) * tpf
+        hk, hv, hqi = r(S, N, tpf, Hkv, d), r(S, N, tpf, Hkv, d), r(S, N, C_t, Hq, d)
+        hq, hks, hvs = r(S, N, q, Hq, d), r(S, N, q, Hkv, d), r(S, N, q, Hkv, d)
+        _, o_ref = a.step(hk.to(dev), hv.to(dev), hqi.to(dev), hq.to(dev), hks.to(dev), hvs.to(dev))
+        ho = torch.empty(S, N, q, Hq, d, dtype=cfg.torch_dtype).pin_memory()
+        pipe.submit(hk, hv, hqi, hq, hks, hvs, ho)
+        outs.append((o_ref, ho))
+    pipe.synchronize()
+    torch.cuda.synchronize()
+    for o_ref, ho in outs:
+        assert torch.equal(o_ref.cpu(), ho)
+    a.close(); b.close()
+
+
 def test_zz_print_report(lib):
     for r in REPORT:
         print("PARITY %-16s %-6s t=%-5d s=%-3d l=%-3d max_abs=%.3e rel_l2=%.3e" % r)

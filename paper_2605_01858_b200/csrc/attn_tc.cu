@@ -56,6 +56,11 @@ constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
 #ifndef DSC_QROT
 #define DSC_QROT 1
 #endif
+// DSC_PAIR 1: softmax / MMA handshakes per PAIR of 64-key tiles (128 keys): S single-
+// buffered per Q tile over both 64-column halves, PV(pair) then S(next pair) per Q tile
+#ifndef DSC_PAIR
+#define DSC_PAIR 0
+#endif
 // DSC_QLDG 1: the rotation warpgroup reads Q rows from global into registers, rotates and
 // stores them once (else cp.async into the tile, then an in-place rotation pass)
 #ifndef DSC_QLDG
@@ -176,6 +181,7 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 #define DSC_EPIROT 0
 #endif
 static_assert(!DSC_EPIROT || (DSC_QROT && !DSC_QSINGLE), "DSC_EPIROT hands l over through the other Q set");
+static_assert(!DSC_PAIR || (!DSC_EPIROT && !DSC_QSINGLE && DSC_QROT), "DSC_PAIR: QROT path");
 // DSC_QFIRST 1: the next item's Q tile is published before the epilogue, so its first S
 // MMAs run while O is read out
 #ifndef DSC_QFIRST
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(B_O + i), 1);
     }
     for (int i = 0; i < 2; ++i) mbar_init(bar(B_OF + i), 128);
-    for (int i = 0; i < 2; ++i) mbar_init(bar(B_QE + i), 1);   // Q buffer i free (MMA commit after an item)
+    for (int i = 0; i < 2; ++i) mbar_init(bar(B_QE + i), DSC_MMA2 ? 2 : 1);   // Q buffer i free (MMA commit(s) after an item)
     for (int i = 0; i < 2; ++i) mbar_init(bar(B_EP + i), 128); // l of a staged item handed to the rotation WG
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
@@ -280,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       rotate_q_tile(p0, w0, qt, lt, qtile_of(0), 2 + qt);
       mbar_arrive(qbar_of(0));
     }
-    int gt = 0, kk = 0;
+    int gt = 0, kk = 0, gp = 0;   // gp: tile pairs (DSC_PAIR)
     for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x, ++kk) {
       const AttnParams& p = ITEM_PARAMS(idx);
       const Item w = decode_item(p, ITEM_LOCAL(idx));
@@ -318,6 +324,128 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       float m = -INFINITY;
       float2 lsum2 = make_float2(0.f, 0.f);
+#if DSC_PAIR
+      // pairs of 64-key tiles (a, b) per handshake: S_qt(pair) fills both 64-column halves of
+      // the Q tile's S region, one max / rescale decision per 128 keys, P(a) -> cols 0..31,
+      // P(b) -> cols 64..95.  S is single-buffered per Q tile: S(pair + 1) is issued after
+      // PV(pair), so when S(pair) is in every earlier PV of this Q tile has completed and O
+      // can be rescaled without a wait.
+      for (int jp = 0; jp < n; jp += 2, ++gp) {
+        const bool hasb = jp + 1 < n;
+        auto vis = [&](int u, int& c_lo, int& c_hi) {
+          const TileSeg t = tile_segments(p, w, u);
+          if (!valid_row) {
+            c_lo = 0; c_hi = 0;
+          } else if (u < w.n_extra) {
+            c_lo = 0;
+            c_hi = min(max(min(A + w.n_self, max(A, lim - w.ring_count + 1)) - kKT * u, 0), kKT);
+          } else {
+            c_lo = t.lo0;
+            c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));
+          }
+          return t.width;
+        };
+        int alo, ahi, blo = 0, bhi = 0;
+        const int anu = vis(w.t_begin + jp, alo, ahi);
+        const int bnu = hasb ? vis(w.t_begin + jp + 1, blo, bhi) : 0;
+        mbar_wait(barS, gp & 1);
+        if (rloc == 0) TRACE(EV_S0 + qt, gt + jp);
+        if (warp_dead || DSC_ABL_SOFTMAX) {
+          mbar_arrive(barP);
+          continue;
+        }
+        tc_fence_after();
+        uint32_t r[64];
+        // (re)load one sub-tile's scores into r, invisible columns -> -inf; returns its max
+        auto load_sub = [&](uint32_t taddr, int nu, int c_lo, int c_hi) {
+          tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          if (nu > 32) tmem_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          tmem_wait_ld();
+          const bool partial = __any_sync(0xffffffffu, !(c_lo == 0 && c_hi == kKT));
+          if (partial) {
+            const unsigned span = (unsigned)max(c_hi - c_lo, 0);
+#pragma unroll
+            for (int c = 0; c < 64; ++c) r[c] = ((unsigned)(c - c_lo) < span) ? r[c] : 0xFF800000u;
+          }
+          float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) {
+            mx0 = fmax3f(mx0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+            mx1 = fmax3f(mx1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+            mx2 = fmax3f(mx2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
+            mx3 = fmax3f(mx3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
+          }
+          if (nu > 32) {
+#pragma unroll
+            for (int c = 32; c < 64; c += 8) {
+              mx0 = fmax3f(mx0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+              mx1 = fmax3f(mx1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+              mx2 = fmax3f(mx2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
+              mx3 = fmax3f(mx3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
+            }
+          }
+          return fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+        };
+        float mt = load_sub(tS0, anu, alo, ahi);
+        if (hasb) mt = fmaxf(mt, load_sub(tS0 + 64, bnu, blo, bhi));   // r now holds sub-tile b
+        const float m_tile = mt * sl2;
+        const bool upd = m_tile > m + kRescaleThreshold;
+        const bool need_o = upd && (m != -INFINITY);
+        const float f = need_o ? ex2(m - m_tile) : 1.f;
+        if (upd) {
+          lsum2.x *= f; lsum2.y *= f;
+          m = m_tile;
+        }
+        if (__any_sync(0xffffffffu, need_o)) {   // every earlier PV of this Q tile is complete
+#pragma unroll 1
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t o[32];
+            tmem_ld32(tO + ch * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+            tmem_st32(tO + ch * 32, o);
+          }
+        }
+        const float m_use = (m == -INFINITY) ? 0.f : m;
+        const float2 negm2 = make_float2(-m_use, -m_use);
+        float2 l0 = make_float2(0.f, 0.f), l1 = l0;
+        auto exp_store = [&](uint32_t taddr, int nu) {   // r (one sub-tile) -> P at taddr
+#pragma unroll
+          for (int cb = 0; cb < 64; cb += 32) {
+            if (cb == 32 && nu <= 32) break;
+#pragma unroll
+            for (int c = cb; c < cb + 32; c += 4) {
+              const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+              const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
+              float2 p0, p1;
+              if (DSC_ABL_EX2) { p0 = x0; p1 = x1; } else {
+                p0 = make_float2(ex2(x0.x), ex2(x0.y));
+                p1 = make_float2(ex2(x1.x), ex2(x1.y));
+              }
+              l0 = __fadd2_rn(l0, p0);
+              l1 = __fadd2_rn(l1, p1);
+              r[c >> 1] = pack_bf16(p0.x, p0.y);
+              r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
+            }
+          }
+          if (nu > 32) tmem_st32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          else tmem_st16(taddr, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+        };
+        if (hasb) {
+          exp_store(tS0 + 64, bnu);
+          tmem_wait_st();                         // r is reused for sub-tile a
+          (void)load_sub(tS0, anu, alo, ahi);
+        }
+        exp_store(tS0, anu);
+        lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(barP);
+        if (rloc == 0) TRACE(EV_P0 + qt, gt + jp);
+      }
+      gt += n;
+#else
       for (int jj = 0; jj < n; ++jj) {
         const int g = gt + jj;
         const int u = w.t_begin + jj;
@@ -452,6 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) TRACE(EV_PW0 + warp, g);
       }
       gt += n;
+#endif
 #if DSC_QROT
 #elif DSC_QDB
       if (has_next && n < 2) {     // a one-tile item never reached the in-loop rotation point
@@ -486,7 +615,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       // epilogue of the item: O / l once the last PV is done
       const float lsum = lsum2.x + lsum2.y;
+#if DSC_PAIR
+      mbar_wait(bar(B_O + qt * 2), kk & 1);   // one O commit per item
+#else
       mbar_wait(bar(B_O + qt * 2 + ((gt - 1) & 1)), ((gt - 1) >> 1) & 1);
+#endif
       if (rloc == 0) TRACE(EV_EPI0, gt);
       tc_fence_after();
       const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
@@ -843,7 +976,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit_w(bar(B_KE + ks));
         if (lane == 0 && q_lo == 0) TRACE(EV_QKI, g);
       };
-      int gt = 0, kk = 0;
+      int gt = 0, kk = 0, gp = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
         const ItemGeo p = item_geo(pa, pb, ITEM_B(idx));
         const Item w = decode_item(p, ITEM_LOCAL(idx));
@@ -851,6 +984,62 @@ __global__ void __launch_bounds__(kThreads, 1)
         qbuf = DSC_QDB ? (kk & 1) : 0;
         for (int qt = q_lo; qt < q_hi; ++qt) MWAIT(bar(B_Q + qbuf * 2 + qt), DSC_QDB ? ((kk >> 1) & 1) : (kk & 1));
         if (kk == 0 && lane == 0 && q_lo == 0) TRACE(EV_Q, 0);
+#if DSC_PAIR
+        {
+          // S(pair) for both Q tiles: tile a -> S cols 0..63, tile b -> cols 64..127
+          auto kbar = [&](int g) { return bar((DSC_QROT && w.staged ? B_KR : B_KF) + g % KST); };
+          auto wait_k = [&](int g, bool hb) {
+            MWAIT(kbar(g), (g / KST) & 1);
+            if (hb) MWAIT(kbar(g + 1), ((g + 1) / KST) & 1);
+            tc_fence_after();
+          };
+          auto width = [&](int g) { return tile_segments(p, w, w.t_begin + (g - gt)).width; };
+          if (n == 0) {
+            for (int qt = q_lo; qt < q_hi; ++qt) mma_commit_w(bar(B_O + qt * 2));   // keep the per-item O phase
+          } else {
+            const bool hb = n > 1;
+            wait_k(gt, hb);
+            const int na_ = width(gt), nb_ = hb ? width(gt + 1) : 0;
+#pragma unroll 1
+            for (int qt = q_lo; qt < q_hi; ++qt) {
+              issue_qk(qt, gt % KST, na_, 0);
+              if (hb) issue_qk(qt, (gt + 1) % KST, nb_, 1);
+              mma_commit_w(bar(B_S + qt * 2));
+            }
+            mma_commit_w(bar(B_KE + gt % KST));
+            if (hb) mma_commit_w(bar(B_KE + (gt + 1) % KST));
+          }
+          for (int jp = 0; jp < n; jp += 2, ++gp) {
+            const int a = gt + jp;
+            const bool hb = jp + 1 < n, more = jp + 2 < n, hb2 = jp + 3 < n;
+            const int na_ = width(a), nb_ = hb ? width(a + 1) : 0;
+            const int na2 = more ? width(a + 2) : 0, nb2 = hb2 ? width(a + 3) : 0;
+            MWAIT(bar(B_VF + a % VST), (a / VST) & 1);
+            if (hb) MWAIT(bar(B_VF + (a + 1) % VST), ((a + 1) / VST) & 1);
+#pragma unroll 1
+            for (int qt = q_lo; qt < q_hi; ++qt) {
+              MWAIT(bar(B_P + qt * 2), gp & 1);
+              if (jp == 0 && kk > 0) MWAIT(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
+              tc_fence_after();
+              issue_pv(qt, a % VST, jp > 0, na_, 0);
+              if (hb) issue_pv(qt, (a + 1) % VST, true, nb_, 1);
+              if (!more) mma_commit_w(bar(B_O + qt * 2));
+              if (more) {
+                if (qt == q_lo) wait_k(a + 2, hb2);
+                issue_qk(qt, (a + 2) % KST, na2, 0);
+                if (hb2) issue_qk(qt, (a + 3) % KST, nb2, 1);
+                mma_commit_w(bar(B_S + qt * 2));
+              }
+            }
+            mma_commit_w(bar(B_VE + a % VST));
+            if (hb) mma_commit_w(bar(B_VE + (a + 1) % VST));
+            if (more) {
+              mma_commit_w(bar(B_KE + (a + 2) % KST));
+              if (hb2) mma_commit_w(bar(B_KE + (a + 3) % KST));
+            }
+          }
+        }
+#else
         if (n > 0) issue_s(p, w, gt, w.t_begin);
         if (n > 1) issue_s(p, w, gt + 1, w.t_begin + 1);
         if (DSC_QSINGLE && n <= 2) mma_commit_w(bar(B_QE));   // the item's last QK^T is issued
@@ -929,6 +1118,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (jj + 2 < n) issue_s(p, w, g + 2, w.t_begin + jj + 2);
 #endif
         }
+#endif   // DSC_PAIR
         if (DSC_QROT && !DSC_QSINGLE) mma_commit_w(bar(B_QE + qbuf));   // Q buffer of this item free once its MMAs are done
         gt += n;
       }

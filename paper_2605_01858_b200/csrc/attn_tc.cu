@@ -141,6 +141,9 @@ static_assert(kNQT * 128 == kMBlockRows, "work items are 256-row m-blocks");
 #ifndef DSC_ABL_LOADS   // ablation: window K/V tiles are not loaded
 #define DSC_ABL_LOADS 0
 #endif
+#ifndef DSC_ABL_NOWAIT_V   // ablation: the MMA warp does not wait for V tiles to land (measured: no change on
+#define DSC_ABL_NOWAIT_V 0     // c5, so V arrival never gates the MMA; skipping the P or K waits breaks the phases)
+#endif
 #ifndef DSC_ABL_SMSP2   // ablation: the softmax warps sharing the MMA warp's sub-partition idle
 #define DSC_ABL_SMSP2 0
 #endif
@@ -1046,7 +1049,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int jj = 0; jj < n; ++jj) {
           const int g = gt + jj, vs = g % VST, buf = g & 1;
           const int nu = tile_segments(p, w, w.t_begin + jj).width;
-          MWAIT(bar(B_VF + vs), (g / VST) & 1);
+          if (!DSC_ABL_NOWAIT_V) MWAIT(bar(B_VF + vs), (g / VST) & 1);
           if (lane == 0 && q_lo == 0) TRACE(EV_VF, g);
 #if DSC_SORDER == 2
           // one burst per tile: every wait first (V(g), P0(g), P1(g), K(g+2) rotated), then

@@ -56,6 +56,18 @@ constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
 #ifndef DSC_QROT
 #define DSC_QROT 1
 #endif
+// DSC_Q0SM 1: the softmax warpgroups (idle until the first S) load + rotate the FIRST item's
+// Q tiles, so the rotation warpgroup starts on the first K tiles at once instead of after
+// both Q tiles (launch latency of small launches: c2 / c4 CTAs run only 1-3 items;
+// measured c2 +4.5%, c4 +3%, c5 +0.2%)
+#ifndef DSC_Q0SM
+#define DSC_Q0SM 1
+#endif
+// DSC_Q2ISSUE 1: the rotation warpgroup issues both Q tiles' cp.async before rotating either
+// (measured 1-3% slower on c2 / c4 / c5: off)
+#ifndef DSC_Q2ISSUE
+#define DSC_Q2ISSUE 0
+#endif
 // DSC_PAIR 1: softmax / MMA handshakes per PAIR of 64-key tiles (128 keys): S single-
 // buffered per Q tile over both 64-column halves, PV(pair) then S(next pair) per Q tile
 #ifndef DSC_PAIR
@@ -261,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (warp == 12 && lane == 0) TRACE(EV_START, 1);   // prologue timeline (trace builds): after the CTA sync
   // one CTA per SM allocates all 512 columns, so the allocation is column 0 of lane 0;
   // the MMA descriptors use that constant (uniform registers, no per-MMA moves)
   const uint32_t tmem_alloc = *tmem_slot;
@@ -282,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lt = threadIdx.x - qt * 128;           // 0..127 within the warpgroup
     auto qtile_of = [&](int kk) { return sbase + OFF_Q + (uint32_t)(((DSC_QDB ? (kk & 1) : 0) * 2 + qt) * kQBytes); };
     auto qbar_of = [&](int kk) { return bar(B_Q + (DSC_QDB ? (kk & 1) : 0) * 2 + qt); };
-    if (!DSC_QROT && blockIdx.x < (unsigned)n_role_items) {       // Q tile of the first item
+    if ((!DSC_QROT || DSC_Q0SM) && blockIdx.x < (unsigned)n_role_items) {   // Q tile of the first item
       const AttnParams& p0 = ITEM_PARAMS((int)blockIdx.x);
       const Item w0 = decode_item(p0, ITEM_LOCAL((int)blockIdx.x));
       issue_q_tile(p0, w0, qt, lt, qtile_of(0));
@@ -712,19 +725,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!DSC_QDB && k >= 1) mbar_wait(bar(B_QE), (k - 1) & 1);   // item k-1's last QK^T done
       const AttnParams& pq = ITEM_PARAMS(qidx);
       const Item wq = decode_item(pq, ITEM_LOCAL(qidx));
+      if (DSC_Q2ISSUE && !DSC_QLDG) {   // both tiles' loads in flight before the first wait
+        issue_q_tile(pq, wq, 0, lt, sbase + OFF_Q + (qb * 2) * kQBytes);
+        issue_q_tile(pq, wq, 1, lt, sbase + OFF_Q + (qb * 2 + 1) * kQBytes);
+      }
 #pragma unroll 1
       for (int q = 0; q < 2; ++q) {
         const uint32_t qtile = sbase + OFF_Q + (qb * 2 + q) * kQBytes;
         if (DSC_QLDG) {
           load_rotate_q_tile(pq, wq, q, lt, qtile);
         } else {
-          issue_q_tile(pq, wq, q, lt, qtile);
+          if (!DSC_Q2ISSUE) issue_q_tile(pq, wq, q, lt, qtile);
           rotate_q_tile(pq, wq, q, lt, qtile, 6);
         }
         mbar_arrive(bar(B_Q + qb * 2 + q));
       }
     };
-    if (blockIdx.x < (unsigned)n_role_items) prep_q(0, blockIdx.x);
+    if (!DSC_Q0SM && blockIdx.x < (unsigned)n_role_items) prep_q(0, blockIdx.x);   // (else the softmax WGs do it)
 #endif
     int gt = 0, kk = 0, ne = 0;   // ne: staged items whose epilogue this warpgroup ran (B_EP phase)
     for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x, ++kk) {
@@ -841,6 +858,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCopy));
+    if (warp == 12 && lane == 0) TRACE(EV_START, 2);   // after the register hand-off
     if (warp == 12 || warp == 13) {
       // ============================================================== copy warps (12: K, 13: V)
       const bool isk = warp == 12;
@@ -878,6 +896,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x) {
         const AttnParams& p = ITEM_PARAMS(idx);
         const Item w = decode_item(p, ITEM_LOCAL(idx));
+        if (isk && lane == 0 && idx == (int)blockIdx.x) TRACE(EV_START, 3);   // first item decoded
         const int A = p.A;
         const __nv_bfloat16* __restrict__ SX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.sink_k : p.sink_v);
         const __nv_bfloat16* __restrict__ XX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.self_k : p.self_v);

@@ -62,6 +62,8 @@ def main():
             end = int(tr[c, 12, 0]) - t0
             ntiles = int((tr[c, 8] != 0).sum())
             print(f"== {name} CTA {c}: tiles {ntiles}, total {end} cycles, Q ready at {int(tr[c, 10, 0]) - t0}")
+            pro = [int(tr[c, 11, j]) - t0 if int(tr[c, 11, j]) else -1 for j in (1, 2, 3)]
+            print(f"   prologue: CTA sync {pro[0]}, copy-WG setmaxnreg {pro[1]}, first item decoded {pro[2]}")
             cols = [0, 1, 2, 28, 3, 32, 13, 4, 6, 8, 33, 5, 7, 9, 34] + [22, 26]
             print("tile " + " ".join(f"{EV[e]:>8}" for e in cols))
             # steady-state summary over tiles 2..ntiles-2 (cycles): tile period at the S0 wait,

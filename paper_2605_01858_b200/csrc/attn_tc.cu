@@ -27,9 +27,10 @@
 //              tile (64 columns), row max, exps, P store
 //   warps 4-7  softmax of Q tile 1
 //   warps 8-11 rotation: every raw K tile in place in shared memory
-//              (LDS -> rotate -> STS), with R(p+1) = R(p) R(1) between consecutive ids
-//   (each softmax warpgroup loads + rotates the Q tile of its next item itself, as soon
-//    as it has consumed S of its last tile, before its epilogue)
+//              (LDS -> rotate -> STS), with R(p+1) = R(p) R(1) between consecutive ids,
+//              and the Q tiles of the NEXT item (loaded + rotated into the other Q set,
+//              DSC_QROT); the first item's Q tiles are prepared by the softmax warpgroups
+//              (DSC_Q0SM), which are idle until the first S arrives
 //   warp 12    K copy: raw K tiles -> SW128 smem; TMA (2 x 64x64 boxes) for window
 //              tiles, cp.async for sink/self tiles
 //   warp 13    V copy: same for V (K and V stage recycling is independent)

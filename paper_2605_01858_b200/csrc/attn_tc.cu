@@ -39,6 +39,10 @@
 // Registers (setmaxnreg): softmax 144, rotation 136, copy/MMA 88.
 #include "tc_common.cuh"
 
+#include <algorithm>
+#include <utility>
+#include <vector>
+
 namespace dsc {
 namespace tc {
 using namespace tcc;
@@ -189,10 +193,8 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 // there: staged K arrives rotated), so the softmax warpgroups go straight to the next item.
 // The softmax hands l over through the item's consumed Q tile (B_EP), the rotation
 // warpgroup reads O out of TMEM and releases it (B_OF) as the softmax would.
-#ifndef DSC_L2PF   // window K/V tiles prefetched into L2 this many tiles ahead of their TMA load
-                   // (0 = off: 2/4/8 measured 1-3% slower on c5 / c3)
-#define DSC_L2PF 0
-#endif
+// (DSC_L2PF, a TMA L2 prefetch of the K/V tiles 2-8 tiles ahead, measured 1-3% slower and
+// was removed)
 #ifndef DSC_EPIROT
 #define DSC_EPIROT 0
 #endif
@@ -282,6 +284,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t tmem = 0u;
 
   const int n_role_items = (DSC_ABL_MMAONLY && warp < 14) ? 0 : n_items;   // ablation: only the MMA issuer works
+  // this CTA's items, in order: the launcher's list-scheduled work list, else the stride
+  // blockIdx.x, + gridDim.x, ...  Every role walks the same sequence.
+  const int* __restrict__ sched = pa.sched_items;
+  const int sj0 = sched ? pa.sched_off[blockIdx.x] : 0;
+  const int n_my = sched ? pa.sched_off[blockIdx.x + 1] - sj0
+                         : (n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0);
+  const int n_my_role = (DSC_ABL_MMAONLY && warp < 14) ? 0 : n_my;
+  auto item_at = [&](int t) { return sched ? sched[sj0 + t] : (int)blockIdx.x + t * (int)gridDim.x; };
   if (warp < 8) {
     // ================================================================ softmax
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
@@ -296,20 +306,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lt = threadIdx.x - qt * 128;           // 0..127 within the warpgroup
     auto qtile_of = [&](int kk) { return sbase + OFF_Q + (uint32_t)(((DSC_QDB ? (kk & 1) : 0) * 2 + qt) * kQBytes); };
     auto qbar_of = [&](int kk) { return bar(B_Q + (DSC_QDB ? (kk & 1) : 0) * 2 + qt); };
-    if ((!DSC_QROT || DSC_Q0SM) && blockIdx.x < (unsigned)n_role_items) {   // Q tile of the first item
-      const AttnParams& p0 = ITEM_PARAMS((int)blockIdx.x);
-      const Item w0 = decode_item(p0, ITEM_LOCAL((int)blockIdx.x));
+    if ((!DSC_QROT || DSC_Q0SM) && n_my_role > 0) {   // Q tile of the first item
+      const int i0 = item_at(0);
+      const AttnParams& p0 = ITEM_PARAMS(i0);
+      const Item w0 = decode_item(p0, ITEM_LOCAL(i0));
       issue_q_tile(p0, w0, qt, lt, qtile_of(0));
       rotate_q_tile(p0, w0, qt, lt, qtile_of(0), 2 + qt);
       mbar_arrive(qbar_of(0));
     }
     int gt = 0, kk = 0, gp = 0;   // gp: tile pairs (DSC_PAIR)
-    for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x, ++kk) {
+    for (; kk < n_my_role; ++kk) {
+      const int idx = item_at(kk);
       const AttnParams& p = ITEM_PARAMS(idx);
       const Item w = decode_item(p, ITEM_LOCAL(idx));
       const int A = w.A;
       const int n = w.n_tiles;
-      const int nidx = idx + gridDim.x;
+      const int nidx = kk + 1 < n_my_role ? item_at(kk + 1) : n_items;
       const bool has_next = nidx < n_role_items;
 #if !DSC_QROT   // (with DSC_QROT the rotation warpgroup prepares the next item's Q)
       Item wn;
@@ -326,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int lim = valid_row ? p.q_pos0 + qi : -1;
       const bool warp_dead = __all_sync(0xffffffffu, !valid_row);
       if (DSC_QPREF) {   // warm L2 with this thread's Q row of the NEXT item (fetched at the item switch)
-        const int nidx = idx + gridDim.x;
+        const int nidx = kk + 1 < n_my_role ? item_at(kk + 1) : n_items;
         if (nidx < n_items) {
           const AttnParams& pn = ITEM_PARAMS(nidx);
           const Item wn = decode_item(pn, ITEM_LOCAL(nidx));
@@ -742,17 +754,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(bar(B_Q + qb * 2 + q));
       }
     };
-    if (!DSC_Q0SM && blockIdx.x < (unsigned)n_role_items) prep_q(0, blockIdx.x);   // (else the softmax WGs do it)
+    if (!DSC_Q0SM && n_my_role > 0) prep_q(0, item_at(0));   // (else the softmax WGs do it)
 #endif
     int gt = 0, kk = 0, ne = 0;   // ne: staged items whose epilogue this warpgroup ran (B_EP phase)
-    for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x, ++kk) {
+    for (; kk < n_my_role; ++kk) {
+      const int idx = item_at(kk);
       const AttnParams& p = ITEM_PARAMS(idx);
       const Item w = decode_item(p, ITEM_LOCAL(idx));
       const int A = p.A;
       const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
 #if DSC_QROT
-      const int nidx_q = idx + gridDim.x;
-      const bool q_next = nidx_q < n_role_items;
+      const bool q_next = kk + 1 < n_my_role;
+      const int nidx_q = q_next ? item_at(kk + 1) : n_items;
       if (w.staged) {   // no K to rotate: the MMA waits on the copy barrier; prepare the next Q
         if (q_next) prep_q(kk + 1, nidx_q);
         gt += w.n_tiles;
@@ -868,36 +881,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int off = isk ? OFF_K : OFF_V;
       const int b_full = isk ? B_KR : B_VF, b_free = isk ? B_KE : B_VE;
       int gt = 0;
-#if DSC_L2PF
-      // L2 prefetch cursor, DSC_L2PF window tiles ahead of the loads (across items): a TMA
-      // load issued when its stage frees then hits L2 instead of waiting ~5K clk on HBM
-      int pf_idx = blockIdx.x, pf_jj = -1;
-      Item pf_w;
-      auto pf_next = [&]() {
-        if (pf_idx >= n_role_items) return;
-        ++pf_jj;
-        while (true) {
-          if (pf_jj == 0) pf_w = decode_item(ITEM_PARAMS(pf_idx), ITEM_LOCAL(pf_idx));
-          if (pf_jj < pf_w.n_tiles) break;
-          pf_idx += gridDim.x;
-          pf_jj = 0;
-          if (pf_idx >= n_role_items) return;
-        }
-        const AttnParams& pq = ITEM_PARAMS(pf_idx);
-        const int u = pf_w.t_begin + pf_jj;
-        if (u < pf_w.n_extra || lane != 0) return;
-        const TileSeg t = tile_segments(pq, pf_w, u);
-        const CUtensorMap* tmap = isk ? &pq.tmap_k : &pq.tmap_v;
-        const int row = (int)(pf_w.head_row * pf_w.Rp) + t.slot0;
-        tma_prefetch_2d(tmap, 0, row);
-        tma_prefetch_2d(tmap, 64, row);
-      };
-      for (int i = 0; i < DSC_L2PF; ++i) pf_next();
-#endif
-      for (int idx = blockIdx.x; idx < n_role_items; idx += gridDim.x) {
+      for (int t = 0; t < n_my_role; ++t) {
+        const int idx = item_at(t);
         const AttnParams& p = ITEM_PARAMS(idx);
         const Item w = decode_item(p, ITEM_LOCAL(idx));
-        if (isk && lane == 0 && idx == (int)blockIdx.x) TRACE(EV_START, 3);   // first item decoded
+        if (isk && lane == 0 && t == 0) TRACE(EV_START, 3);   // first item decoded
         const int A = p.A;
         const __nv_bfloat16* __restrict__ SX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.sink_k : p.sink_v);
         const __nv_bfloat16* __restrict__ XX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.self_k : p.self_v);
@@ -940,9 +928,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (lane == 0) TRACE(isk ? EV_K_ISSUE : EV_V_ISSUE, g);
-#if DSC_L2PF
-          pf_next();
-#endif
           __syncwarp();
         }
         gt += w.n_tiles;
@@ -1000,7 +985,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && q_lo == 0) TRACE(EV_QKI, g);
       };
       int gt = 0, kk = 0, gp = 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++kk) {
+      for (; kk < n_my; ++kk) {
+        const int idx = item_at(kk);
         const ItemGeo p = item_geo(pa, pb, ITEM_B(idx));
         const Item w = decode_item(p, ITEM_LOCAL(idx));
         const int n = w.n_tiles;
@@ -1201,6 +1187,97 @@ cudaError_t launch_attn_tc6(const AttnParams& pa, const AttnParams* pb, cudaStre
 #define DSC_V6 0
 #endif
 
+// DSC_SCHED 1: per-CTA work lists by list scheduling -- items in launch order (attend first,
+// then build; longest first inside each), each to the CTA with the least work so far
+// (cost = its key tiles + kSwitchCost for the item switch).  The static stride gives CTA b
+// items b, b + grid, ...: with item lengths that differ a lot (c3: 224 attend items of 223
+// tiles on 148 CTAs, then 4.8K build items of 1-25 tiles) half the CTAs ran two attend
+// items AND a full share of builds.  Lists are cached per launch shape.
+#ifndef DSC_SCHED
+#define DSC_SCHED 1
+#endif
+#ifndef DSC_SCHED_STRIDE
+#define DSC_SCHED_STRIDE 0
+#endif
+namespace {
+constexpr int kSwitchCost = 2;
+struct SchedEntry {
+  std::vector<long long> key;
+  int* dev = nullptr;
+  size_t cap = 0;     // ints allocated
+  int device = -1;
+};
+long long item_tiles_host(const AttnParams& p, int local) { return tcc::decode_item(p, local).n_tiles; }
+
+// returns device [grid + 1 offsets | n items] for this launch shape (cached), or nullptr
+const int* sched_lists(const AttnParams& pa, const AttnParams* pb, long long na, long long nb, int ka, int kb,
+                       unsigned grid, cudaStream_t st) {
+  static SchedEntry cache[4];
+  static int next = 0;
+  int device = 0;
+  cudaGetDevice(&device);
+  std::vector<long long> key = {device, na, nb, ka, kb, grid};
+  for (const AttnParams* p : {&pa, pb}) {
+    if (!p) continue;
+    for (long long v : {(long long)p->n_splits, (long long)p->split_only, (long long)p->P, (long long)p->Hkv,
+                        (long long)p->n_mblocks, (long long)p->n_q, (long long)p->grp, (long long)p->q_pos0,
+                        (long long)p->A, (long long)p->ring_count, (long long)p->n_self,
+                        (long long)p->tiles_per_split})
+      key.push_back(v);
+  }
+  for (auto& e : cache)
+    if (e.dev && e.key == key) return e.dev;
+  const long long items = na + nb;
+  std::vector<int> off(grid + 1, 0), owner(items);
+  std::vector<long long> load(grid, 0);
+  // min-heap on (load, cta): each item in launch order goes to the least-loaded CTA
+  std::vector<std::pair<long long, int>> heap;
+  heap.reserve(grid);
+  for (unsigned b = 0; b < grid; ++b) heap.push_back({0, (int)b});
+  auto cmp = [](const std::pair<long long, int>& x, const std::pair<long long, int>& y) { return x > y; };
+  std::make_heap(heap.begin(), heap.end(), cmp);
+  for (long long I = 0; I < items; ++I) {
+    const bool isb = kb > 0 ? (I % (ka + kb)) >= ka : I >= na;
+    const long long local = kb > 0 ? (isb ? (I / (ka + kb)) * kb + (I % (ka + kb)) - ka : (I / (ka + kb)) * ka + (I % (ka + kb)))
+                                   : (isb ? I - na : I);
+    const long long cost = item_tiles_host(isb ? *pb : pa, (int)local) + kSwitchCost;
+#if DSC_SCHED_STRIDE   // debug: the lists reproduce the static stride
+    (void)cost;
+    owner[I] = (int)(I % grid);
+    ++off[owner[I] + 1];
+#else
+    std::pop_heap(heap.begin(), heap.end(), cmp);
+    const int b = heap.back().second;
+    owner[I] = b;
+    heap.back().first += cost;
+    std::push_heap(heap.begin(), heap.end(), cmp);   // (moves heap.back(): b saved above)
+    ++off[b + 1];
+#endif
+  }
+  for (unsigned b = 0; b < grid; ++b) off[b + 1] += off[b];
+  std::vector<int> host(grid + 1 + items);
+  std::copy(off.begin(), off.end(), host.begin());
+  std::vector<int> fill(off.begin(), off.end() - 1);
+  for (long long I = 0; I < items; ++I) host[grid + 1 + fill[owner[I]]++] = (int)I;   // increasing I per CTA
+  SchedEntry& e = cache[next];
+  next = (next + 1) % 4;
+  if (e.cap < host.size() || e.device != device) {
+    if (e.dev) cudaFree(e.dev);
+    e.dev = nullptr; e.cap = 0;
+    if (cudaMalloc(&e.dev, host.size() * sizeof(int)) != cudaSuccess) { cudaGetLastError(); e.key.clear(); return nullptr; }
+    e.cap = host.size();
+    e.device = device;
+  }
+  e.key = key;
+  // pageable source: staged synchronously, so `host` may go out of scope afterwards
+  if (cudaMemcpyAsync(e.dev, host.data(), host.size() * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    e.key.clear();
+    return nullptr;
+  }
+  return e.dev;
+}
+}  // namespace
+
 cudaError_t launch_attn_tc2(const AttnParams& pa, const AttnParams* pb, cudaStream_t st) {
   if (DSC_V6) {
     if (pa.n_peers > 0 || (pb && pb->n_peers > 0)) return cudaErrorNotSupported;   // v6 has no peer epilogue
@@ -1230,7 +1307,13 @@ cudaError_t launch_attn_tc2(const AttnParams& pa, const AttnParams* pb, cudaStre
     kb = (int)(nb / G);
   }
 #endif
-  tc::attn_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, st>>>(pa, pb ? *pb : pa, (int)na, (int)nb, ka, kb);
+  AttnParams qa = pa;
+  qa.sched_off = qa.sched_items = nullptr;
+  if (DSC_SCHED && grid > 0 && items > grid) {
+    const int* lists = sched_lists(pa, pb, na, nb, ka, kb, grid, st);
+    if (lists) { qa.sched_off = lists; qa.sched_items = lists + grid + 1; }
+  }
+  tc::attn_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, st>>>(qa, pb ? *pb : qa, (int)na, (int)nb, ka, kb);
   return cudaGetLastError();
 }
 

@@ -59,6 +59,10 @@ struct AttnParams {
   // of to o; peer_o are device pointers mapped in this process (local, P2P or CUDA IPC)
   void* peer_o[kMaxPeers];
   int n_peers, o_hq, o_head_off;
+  // per-CTA work lists of the tcgen05 kernel (set by its launcher, DSC_SCHED): CTA b runs
+  // the items sched_items[sched_off[b] .. sched_off[b+1]) in order; null = static stride
+  const int* sched_off;
+  const int* sched_items;
   // staged build (tcgen05 path): the keys are rows [0, ring_count) of the per-step staging
   // buffers [S*N*Hkv][Rp][d] holding sink ++ instant window with K ALREADY rotated at ids
   // 0..ring_count-1 (stage_instant_kernel); A = 0, ring_start = 0, no K rotation in-kernel

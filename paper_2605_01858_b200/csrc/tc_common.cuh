@@ -347,7 +347,7 @@ __device__ __forceinline__ ItemGeo item_geo(const AttnParams& pa, const AttnPara
   return q;
 }
 template <class PT>
-__device__ __forceinline__ Item decode_item(const PT& p, int idx) {
+__host__ __device__ __forceinline__ Item decode_item(const PT& p, int idx) {
   Item w;
   const bool one = p.split_only >= 0;          // context-parallel partial: one split per launch
   w.sp = one ? p.split_only : idx % p.n_splits;

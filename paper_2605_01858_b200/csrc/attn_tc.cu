@@ -1200,7 +1200,10 @@ cudaError_t launch_attn_tc6(const AttnParams& pa, const AttnParams* pb, cudaStre
 #define DSC_SCHED_STRIDE 0
 #endif
 namespace {
-constexpr int kSwitchCost = 2;
+#ifndef DSC_SWCOST
+#define DSC_SWCOST 2
+#endif
+constexpr int kSwitchCost = DSC_SWCOST;   // item-switch cost in key tiles (epilogue + pipeline refill)
 struct SchedEntry {
   std::vector<long long> key;
   int* dev = nullptr;

@@ -1209,6 +1209,7 @@ struct SchedEntry {
   int* dev = nullptr;
   size_t cap = 0;     // ints allocated
   int device = -1;
+  bool use = false;   // false: the static stride is within 2% of the list schedule's makespan
 };
 long long item_tiles_host(const AttnParams& p, int local) { return tcc::decode_item(p, local).n_tiles; }
 
@@ -1229,10 +1230,10 @@ const int* sched_lists(const AttnParams& pa, const AttnParams* pb, long long na,
       key.push_back(v);
   }
   for (auto& e : cache)
-    if (e.dev && e.key == key) return e.dev;
+    if (!e.key.empty() && e.key == key) return e.use ? e.dev : nullptr;
   const long long items = na + nb;
   std::vector<int> off(grid + 1, 0), owner(items);
-  std::vector<long long> load(grid, 0);
+  std::vector<long long> stride_load(grid, 0);
   // min-heap on (load, cta): each item in launch order goes to the least-loaded CTA
   std::vector<std::pair<long long, int>> heap;
   heap.reserve(grid);
@@ -1244,6 +1245,7 @@ const int* sched_lists(const AttnParams& pa, const AttnParams* pb, long long na,
     const long long local = kb > 0 ? (isb ? (I / (ka + kb)) * kb + (I % (ka + kb)) - ka : (I / (ka + kb)) * ka + (I % (ka + kb)))
                                    : (isb ? I - na : I);
     const long long cost = item_tiles_host(isb ? *pb : pa, (int)local) + kSwitchCost;
+    stride_load[I % grid] += cost;
 #if DSC_SCHED_STRIDE   // debug: the lists reproduce the static stride
     (void)cost;
     owner[I] = (int)(I % grid);
@@ -1258,12 +1260,20 @@ const int* sched_lists(const AttnParams& pa, const AttnParams* pb, long long na,
 #endif
   }
   for (unsigned b = 0; b < grid; ++b) off[b + 1] += off[b];
+  long long list_max = 0;
+  for (auto& h : heap) list_max = std::max(list_max, h.first);
+  const long long stride_max = *std::max_element(stride_load.begin(), stride_load.end());
+  // keep the stride (and its L2 locality: c5) unless the lists shorten the makespan by > 2%
+  const bool use = list_max * 50 < stride_max * 49;
   std::vector<int> host(grid + 1 + items);
   std::copy(off.begin(), off.end(), host.begin());
   std::vector<int> fill(off.begin(), off.end() - 1);
   for (long long I = 0; I < items; ++I) host[grid + 1 + fill[owner[I]]++] = (int)I;   // increasing I per CTA
   SchedEntry& e = cache[next];
   next = (next + 1) % 4;
+  e.key = key;
+  e.use = use;
+  if (!use) return nullptr;
   if (e.cap < host.size() || e.device != device) {
     if (e.dev) cudaFree(e.dev);
     e.dev = nullptr; e.cap = 0;
@@ -1271,7 +1281,6 @@ const int* sched_lists(const AttnParams& pa, const AttnParams* pb, long long na,
     e.cap = host.size();
     e.device = device;
   }
-  e.key = key;
   // pageable source: staged synchronously, so `host` may go out of scope afterwards
   if (cudaMemcpyAsync(e.dev, host.data(), host.size() * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess) {
     e.key.clear();

@@ -40,6 +40,7 @@
 #include "tc_common.cuh"
 
 #include <algorithm>
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -1218,6 +1219,8 @@ const int* sched_lists(const AttnParams& pa, const AttnParams* pb, long long na,
                        unsigned grid, cudaStream_t st) {
   static SchedEntry cache[4];
   static int next = 0;
+  static std::mutex mu;                 // handles may launch from several host threads
+  std::lock_guard<std::mutex> lock(mu);
   int device = 0;
   cudaGetDevice(&device);
   std::vector<long long> key = {device, na, nb, ka, kb, grid};

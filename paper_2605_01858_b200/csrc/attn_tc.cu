@@ -74,6 +74,11 @@ constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
 #ifndef DSC_Q2ISSUE
 #define DSC_Q2ISSUE 0
 #endif
+// DSC_LASTO 1: O_qt is committed once per item (after its last PV) instead of per tile: a
+// rescale waits on the V-stage-free commit of tile g-1 (PV0 and PV1 of g-1 complete)
+#ifndef DSC_LASTO
+#define DSC_LASTO 0
+#endif
 // DSC_PAIR 1: softmax / MMA handshakes per PAIR of 64-key tiles (128 keys): S single-
 // buffered per Q tile over both 64-column halves, PV(pair) then S(next pair) per Q tile
 #ifndef DSC_PAIR
@@ -201,6 +206,7 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 #endif
 static_assert(!DSC_EPIROT || (DSC_QROT && !DSC_QSINGLE), "DSC_EPIROT hands l over through the other Q set");
 static_assert(!DSC_PAIR || (!DSC_EPIROT && !DSC_QSINGLE && DSC_QROT), "DSC_PAIR: QROT path");
+static_assert(!DSC_LASTO || (!DSC_PAIR && !DSC_EPIROT && !DSC_MMA2 && DSC_SORDER == 1), "DSC_LASTO: SORDER 1 loop");
 // DSC_QFIRST 1: the next item's Q tile is published before the epilogue, so its first S
 // MMAs run while O is read out
 #ifndef DSC_QFIRST
@@ -558,7 +564,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (__any_sync(0xffffffffu, need_o)) {
           // O_qt holds P V up to tile g-1: wait for that PV, rescale in TMEM
+#if DSC_LASTO
+          // V stage of tile g-1 freed = PV0(g-1) and PV1(g-1) complete (no per-tile O commit)
+          mbar_wait(bar(B_VE + (g - 1) % VST), ((g - 1) / VST) & 1);
+#else
           mbar_wait(bar(B_O + qt * 2 + ((g - 1) & 1)), ((g - 1) >> 1) & 1);
+#endif
           tc_fence_after();
 #pragma unroll 1
           for (int ch = 0; ch < 4; ++ch) {
@@ -645,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       // epilogue of the item: O / l once the last PV is done
       const float lsum = lsum2.x + lsum2.y;
-#if DSC_PAIR
+#if DSC_PAIR || DSC_LASTO
       mbar_wait(bar(B_O + qt * 2), kk & 1);   // one O commit per item
 #else
       mbar_wait(bar(B_O + qt * 2 + ((gt - 1) & 1)), ((gt - 1) >> 1) & 1);
@@ -1053,6 +1064,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (n > 0) issue_s(p, w, gt, w.t_begin);
         if (n > 1) issue_s(p, w, gt + 1, w.t_begin + 1);
         if (DSC_QSINGLE && n <= 2) mma_commit_w(bar(B_QE));   // the item's last QK^T is issued
+        if (DSC_LASTO && n == 0)
+          for (int qt = q_lo; qt < q_hi; ++qt) mma_commit_w(bar(B_O + qt * 2));   // keep the per-item O phase
         for (int jj = 0; jj < n; ++jj) {
           const int g = gt + jj, vs = g % VST, buf = g & 1;
           const int nu = tile_segments(p, w, w.t_begin + jj).width;
@@ -1098,7 +1111,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) TRACE(EV_PV0 + qt, g);
             tc_fence_after();
             issue_pv(qt, vs, jj > 0, nu, buf);
-            mma_commit_w(bar(B_O + qt * 2 + buf));
+            if (!DSC_LASTO) mma_commit_w(bar(B_O + qt * 2 + buf));
+            else if (jj == n - 1) mma_commit_w(bar(B_O + qt * 2));   // one O commit per item (epilogue)
             if (lane == 0) TRACE(EV_PVI + qt, g);
             if (more) {
               if (qt == q_lo) {

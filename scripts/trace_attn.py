@@ -98,6 +98,15 @@ def main():
                 if qs is not None and e1 is not None:
                     sw.append((j, qs, ql - qs if ql else -1, qd - ql if (qd and ql) else -1, e0 - qd if (e0 and qd) else -1,
                                e1 - e0 if (e1 and e0) else -1))
+            # per-warp P arrival spread (the P barrier completes at the LAST warp) vs the MMA's
+            # PV issue: tiles 2..ntiles-2
+            spread, last_to_pv = [], []
+            for j in range(2, min(ntiles, 64) - 1):
+                pw = [ev(14 + w_, j) for w_ in range(4)]
+                if all(x is not None for x in pw) and ev(8, j) is not None:
+                    spread.append(max(pw) - min(pw))
+                    last_to_pv.append(ev(8, j) - max(pw))
+            print(f"   P0 warp spread (median) {med(spread)}, last P0 warp -> PV0 issue (median) {med(last_to_pv)}")
             for t in sw[:6]:
                 print(f"   switch @tile {t[0]}: start {t[1]}, Q cp.async issue {t[2]}, Q wait+rotate {t[3]}, "
                       f"wait last PV {t[4]}, O read+store {t[5]}")

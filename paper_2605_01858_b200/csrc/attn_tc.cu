@@ -20,7 +20,7 @@
 //   S[qt][b] = cols qt*128 + b*64 (b = g & 1)   O[qt] = cols 256 + qt*128
 // P(g) (bf16x2, 32 columns) overwrites the first half of S[qt][g&1] and feeds
 // O[qt] += P V as the TMEM A operand.  MMA issue order per tile g (after the item's
-// prologue S(g0), S(g0+1)): PV0(g) S0(g+2) PV1(g) S1(g+2).
+// prologue S(g0), S(g0+1)): PV0(g) PV1(g) S0(g+2) S1(g+2) (DSC_SORDER 0).
 //
 // CTA = 16 warps:
 //   warps 0-3  softmax of Q tile 0 (thread = query row = TMEM lane); one TMEM read per
@@ -77,7 +77,7 @@ constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
 // DSC_LASTO 1: O_qt is committed once per item (after its last PV) instead of per tile: a
 // rescale waits on the V-stage-free commit of tile g-1 (PV0 and PV1 of g-1 complete)
 #ifndef DSC_LASTO
-#define DSC_LASTO 0
+#define DSC_LASTO 1
 #endif
 // DSC_PAIR 1: softmax / MMA handshakes per PAIR of 64-key tiles (128 keys): S single-
 // buffered per Q tile over both 64-column halves, PV(pair) then S(next pair) per Q tile
@@ -101,9 +101,6 @@ constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
 #endif
 static_assert(!DSC_QROT || DSC_QDB || DSC_QSINGLE, "DSC_QROT needs the Q double buffer or DSC_QSINGLE");
 static_assert(!DSC_QSINGLE || (DSC_QROT && !DSC_QDB), "DSC_QSINGLE is the single-set variant of DSC_QROT");
-#if DSC_QSINGLE && defined(DSC_SORDER) && DSC_SORDER != 1
-#error "DSC_QSINGLE commits the Q-free barrier in the DSC_SORDER 1 MMA loop"
-#endif
 #ifndef DSC_KST
 #define DSC_KST (DSC_QDB ? 3 : (DSC_QSINGLE ? 5 : 6))
 #endif
@@ -181,9 +178,14 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 #ifndef DSC_QPREF
 #define DSC_QPREF 0
 #endif
-// DSC_SORDER 1: MMA order PV0(g) S0(g+2) PV1(g) S1(g+2) (else PV0 PV1 S0 S1)
+// DSC_SORDER: MMA order per tile -- 0 (default): PV0(g) PV1(g) S0(g+2) S1(g+2), two batches
+// (measured +1.2% c5 / +1.3% c3 over 1 in round 1's last session); 1: PV0(g) S0(g+2) PV1(g)
+// S1(g+2); 2: every wait first, then one burst
 #ifndef DSC_SORDER
-#define DSC_SORDER 1
+#define DSC_SORDER 0
+#endif
+#if DSC_QSINGLE && DSC_SORDER != 1
+#error "DSC_QSINGLE commits the Q-free barrier in the DSC_SORDER 1 MMA loop (build with DSC_SORDER=1)"
 #endif
 // DSC_QEARLY 1: the next item's Q cp.async are issued at the last tile's S wait (else
 // after the last tile)
@@ -206,7 +208,7 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 #endif
 static_assert(!DSC_EPIROT || (DSC_QROT && !DSC_QSINGLE), "DSC_EPIROT hands l over through the other Q set");
 static_assert(!DSC_PAIR || (!DSC_EPIROT && !DSC_QSINGLE && DSC_QROT), "DSC_PAIR: QROT path");
-static_assert(!DSC_LASTO || (!DSC_PAIR && !DSC_EPIROT && !DSC_MMA2 && DSC_SORDER == 1), "DSC_LASTO: SORDER 1 loop");
+static_assert(!DSC_LASTO || (!DSC_PAIR && !DSC_EPIROT && !DSC_MMA2 && DSC_SORDER != 2), "DSC_LASTO: SORDER 0/1 loops");
 // DSC_QFIRST 1: the next item's Q tile is published before the epilogue, so its first S
 // MMAs run while O is read out
 #ifndef DSC_QFIRST
@@ -1116,7 +1118,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) TRACE(EV_PVI + qt, g);
             if (more) {
               if (qt == q_lo) {
+                if (lane == 0) TRACE(EV_L + 5, g + 2);   // (trace) K wait entered
                 MWAIT(bar((DSC_QROT && w.staged ? B_KR : B_KF) + ks2), ((g + 2) / KST) & 1);
+                if (lane == 0) TRACE(EV_KF, g + 2);      // K(g+2) ready at the MMA
                 tc_fence_after();
               }
               issue_qk(qt, ks2, nu2, buf);
@@ -1134,7 +1138,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) TRACE(EV_PV0 + qt, g);
             tc_fence_after();
             issue_pv(qt, vs, jj > 0, nu, buf);
-            mma_commit_w(bar(B_O + qt * 2 + buf));
+            if (!DSC_LASTO) mma_commit_w(bar(B_O + qt * 2 + buf));
+            else if (jj == n - 1) mma_commit_w(bar(B_O + qt * 2));   // one O commit per item (epilogue)
             if (lane == 0) TRACE(EV_PVI + qt, g);
           }
           mma_commit_w(bar(B_VE + vs));

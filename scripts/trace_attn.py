@@ -107,6 +107,8 @@ def main():
                     spread.append(max(pw) - min(pw))
                     last_to_pv.append(ev(8, j) - max(pw))
             print(f"   P0 warp spread (median) {med(spread)}, last P0 warp -> PV0 issue (median) {med(last_to_pv)}")
+            kw = [ev(3, j) - ev(27, j) for j in range(4, min(ntiles, 64) - 1) if ev(3, j) is not None and ev(27, j) is not None]
+            print(f"   MMA K(g+2) wait (median / max) {med(kw)} / {max(kw) if kw else -1}")
             for t in sw[:6]:
                 print(f"   switch @tile {t[0]}: start {t[1]}, Q cp.async issue {t[2]}, Q wait+rotate {t[3]}, "
                       f"wait last PV {t[4]}, O read+store {t[5]}")

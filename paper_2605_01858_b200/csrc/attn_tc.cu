@@ -79,6 +79,11 @@ constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
 #ifndef DSC_LASTO
 #define DSC_LASTO 1
 #endif
+// DSC_PJOIN 1: one P-ready barrier per S buffer for BOTH softmax warpgroups (256 arrivals):
+// the MMA warp waits once per tile before PV0 PV1 instead of once per Q tile
+#ifndef DSC_PJOIN
+#define DSC_PJOIN 0
+#endif
 // DSC_PAIR 1: softmax / MMA handshakes per PAIR of 64-key tiles (128 keys): S single-
 // buffered per Q tile over both 64-column halves, PV(pair) then S(next pair) per Q tile
 #ifndef DSC_PAIR
@@ -209,6 +214,7 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 static_assert(!DSC_EPIROT || (DSC_QROT && !DSC_QSINGLE), "DSC_EPIROT hands l over through the other Q set");
 static_assert(!DSC_PAIR || (!DSC_EPIROT && !DSC_QSINGLE && DSC_QROT), "DSC_PAIR: QROT path");
 static_assert(!DSC_LASTO || (!DSC_PAIR && !DSC_EPIROT && !DSC_MMA2 && DSC_SORDER != 2), "DSC_LASTO: SORDER 0/1 loops");
+static_assert(!DSC_PJOIN || (!DSC_PAIR && !DSC_MMA2 && DSC_SORDER == 0), "DSC_PJOIN: SORDER 0 loop, one MMA warp");
 // DSC_QFIRST 1: the next item's Q tile is published before the epilogue, so its first S
 // MMAs run while O is read out
 #ifndef DSC_QFIRST
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(bar(B_S + i), 1);
-      mbar_init(bar(B_P + i), 128);
+      mbar_init(bar(B_P + i), DSC_PJOIN ? 256 : 128);   // PJOIN: both softmax WGs on B_P[buf]
       mbar_init(bar(B_O + i), 1);
     }
     for (int i = 0; i < 2; ++i) mbar_init(bar(B_OF + i), 128);
@@ -311,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tO = tmem + lane_off + (uint32_t)(256 + qt * 128);
     const float sl2 = p.scale_log2;
     const float2 scale2 = make_float2(sl2, sl2);
-    const uint32_t barS = bar(B_S + qt * 2), barP = bar(B_P + qt * 2);   // + 8 * buffer
+    const uint32_t barS = bar(B_S + qt * 2), barP = bar(B_P + (DSC_PJOIN ? 0 : qt * 2));   // + 8 * buffer
     const int lt = threadIdx.x - qt * 128;           // 0..127 within the warpgroup
     auto qtile_of = [&](int kk) { return sbase + OFF_Q + (uint32_t)(((DSC_QDB ? (kk & 1) : 0) * 2 + qt) * kQBytes); };
     auto qbar_of = [&](int kk) { return bar(B_Q + (DSC_QDB ? (kk & 1) : 0) * 2 + qt); };
@@ -1131,9 +1137,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit_w(bar(B_VE + vs));
           if (more) mma_commit_w(bar(B_KE + ks2));
 #else
+          if (DSC_PJOIN) MWAIT(bar(B_P + buf), (g >> 1) & 1);   // P(g) of both Q tiles: one wait
 #pragma unroll 1
           for (int qt = q_lo; qt < q_hi; ++qt) {
-            MWAIT(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
+            if (!DSC_PJOIN) MWAIT(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
             if (jj == 0 && kk > 0) MWAIT(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
             if (lane == 0) TRACE(EV_PV0 + qt, g);
             tc_fence_after();

@@ -254,6 +254,9 @@ def test_c5_multistream_sampled(lib):
 @pytest.mark.parametrize("name,steps,exact", [
     ("c2", [0, 3, 4, 36, 37, 63], [(0, 0)]),
     ("c5", [0, 36, 127], [(0, 0), (63, 3)]),
+    # c3 / c4: the fused launch runs on list-scheduled per-CTA work lists
+    ("c3", [0, 9, 75], [(0, 0), (0, 27)]),
+    ("c4", [0, 140], [(0, 0)]),
 ])
 def test_fused_step_parity_and_bitwise_equal_to_three_calls(lib, name, steps, exact):
     # dscache_step = append + build_instant + attend in one persistent tcgen05 launch:

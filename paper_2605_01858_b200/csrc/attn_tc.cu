@@ -213,7 +213,7 @@ constexpr int kPolyPerGroup = DSC_POLY;   // of every 8 columns of a full tile, 
 #endif
 static_assert(!DSC_EPIROT || (DSC_QROT && !DSC_QSINGLE), "DSC_EPIROT hands l over through the other Q set");
 static_assert(!DSC_PAIR || (!DSC_EPIROT && !DSC_QSINGLE && DSC_QROT), "DSC_PAIR: QROT path");
-static_assert(!DSC_LASTO || (!DSC_PAIR && !DSC_EPIROT && !DSC_MMA2 && DSC_SORDER != 2), "DSC_LASTO: SORDER 0/1 loops");
+static_assert(!DSC_LASTO || (!DSC_PAIR && !DSC_EPIROT && DSC_SORDER != 2), "DSC_LASTO: SORDER 0/1 loops");
 static_assert(!DSC_PJOIN || (!DSC_PAIR && !DSC_MMA2 && DSC_SORDER == 0), "DSC_PJOIN: SORDER 0 loop, one MMA warp");
 // DSC_QFIRST 1: the next item's Q tile is published before the epilogue, so its first S
 // MMAs run while O is read out

@@ -107,6 +107,15 @@ def main():
                     spread.append(max(pw) - min(pw))
                     last_to_pv.append(ev(8, j) - max(pw))
             print(f"   P0 warp spread (median) {med(spread)}, last P0 warp -> PV0 issue (median) {med(last_to_pv)}")
+            lag = [[] for _ in range(8)]
+            for j in range(2, min(ntiles, 64) - 1):
+                pw = [ev(14 + w_, j) for w_ in range(8)]
+                for h0 in (0, 4):
+                    grp_ = pw[h0:h0 + 4]
+                    if all(x is not None for x in grp_):
+                        for w_ in range(4):
+                            lag[h0 + w_].append(grp_[w_] - min(grp_))
+            print("   P lag behind the WG's first warp, median per softmax warp 0..7: " + " ".join(str(med(l)) for l in lag))
             kw = [ev(3, j) - ev(27, j) for j in range(4, min(ntiles, 64) - 1) if ev(3, j) is not None and ev(27, j) is not None]
             print(f"   MMA K(g+2) wait (median / max) {med(kw)} / {max(kw) if kw else -1}")
             for t in sw[:6]:

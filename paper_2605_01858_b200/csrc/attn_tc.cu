@@ -147,7 +147,25 @@ static_assert(kNQT * 128 == kMBlockRows, "work items are 256-row m-blocks");
 #ifndef DSC_ABL_MMAONLY
 #define DSC_ABL_MMAONLY 0
 #endif
-#define MWAIT(b, ph) do { if (!DSC_ABL_MMAONLY) mbar_wait((b), (ph)); } while (0)
+// DSC_MWSLEEP > 0: the MMA warp backs off with nanosleep(DSC_MWSLEEP) between failed polls,
+// leaving its sub-partition's issue slots to the two softmax warps that share it
+// (measured: 128 ns c5 +0.7%, c3 +0.8% over plain polling; 32 ns mixed)
+#ifndef DSC_MWSLEEP
+#define DSC_MWSLEEP 128
+#endif
+__device__ __forceinline__ void mma_wait(uint32_t b, uint32_t ph) {
+  if (DSC_MWSLEEP > 0) {
+    if (tcc::mbar_try(b, ph)) return;
+    const long long t0 = clock64();
+    do {
+      __nanosleep(DSC_MWSLEEP);
+      if (clock64() - t0 > (1ll << 31)) __trap();   // same watchdog as mbar_wait
+    } while (!tcc::mbar_try(b, ph));
+  } else {
+    tcc::mbar_wait(b, ph);
+  }
+}
+#define MWAIT(b, ph) do { if (!DSC_ABL_MMAONLY) mma_wait((b), (ph)); } while (0)
 #ifndef DSC_ABL_SOFTMAX
 #define DSC_ABL_SOFTMAX 0
 #endif

@@ -32,10 +32,16 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 // Watchdog: a pipeline bug must not hang the GPU -- trap after ~2^31 cycles (~1 s).
+// DSC_WSLEEP > 0: failed polls back off with nanosleep(DSC_WSLEEP), leaving the
+// sub-partition's issue slots to the warps that have work
+#ifndef DSC_WSLEEP
+#define DSC_WSLEEP 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (mbar_try(bar, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try(bar, parity)) {
+    if (DSC_WSLEEP > 0) __nanosleep(DSC_WSLEEP);
     if (clock64() - t0 > (1ll << 31)) __trap();
   }
 }

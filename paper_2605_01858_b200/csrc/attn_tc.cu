@@ -79,6 +79,11 @@ constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
 #ifndef DSC_LASTO
 #define DSC_LASTO 1
 #endif
+// DSC_EXBF 1: softmax exponentials as ex2.approx.bf16x2 (the exponent argument rounded to
+// bf16, two columns per MUFU op; P is bf16 for the PV MMA anyway and l sums that same P)
+#ifndef DSC_EXBF
+#define DSC_EXBF 0
+#endif
 // DSC_PJOIN 1: one P-ready barrier per S buffer for BOTH softmax warpgroups (256 arrivals):
 // the MMA warp waits once per tile before PV0 PV1 instead of once per Q tile
 #ifndef DSC_PJOIN
@@ -621,6 +626,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr bool poly_any = kPolyPerGroup > 0;
             const bool poly0 = poly_any && ((c % 8) + 2 > 8 - kPolyPerGroup);
             const bool poly1 = poly_any && ((c % 8) + 4 > 8 - kPolyPerGroup);
+            if (DSC_EXBF) {   // exponent rounded to bf16, one MUFU op per two columns; l sums the bf16 P
+              const uint32_t e0 = ex2_bf16x2(pack_bf16(x0.x, x0.y)), e1 = ex2_bf16x2(pack_bf16(x1.x, x1.y));
+              l0 = __fadd2_rn(l0, make_float2(bf_lo(e0), bf_hi(e0)));
+              l1 = __fadd2_rn(l1, make_float2(bf_lo(e1), bf_hi(e1)));
+              r[c >> 1] = e0;
+              r[(c >> 1) + 1] = e1;
+              continue;
+            }
             if (DSC_ABL_EX2) { p0 = x0; p1 = x1; } else {
               if (poly0 && !any_partial) p0 = exp2_poly2(x0); else p0 = make_float2(ex2(x0.x), ex2(x0.y));
               if (poly1 && !any_partial) p1 = exp2_poly2(x1); else p1 = make_float2(ex2(x1.x), ex2(x1.y));

@@ -139,7 +139,10 @@ static_assert(kRegSoftmax > kThreadRegs && kRegCopy < kThreadRegs, "softmax must
 constexpr int kSmemBytes = OFF_BAR + B_N * 8 + 16 + 1024;   // + tmem slot + alignment slack
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 static_assert(kKT == 64, "the S double buffer assumes 64-key tiles");
-constexpr float kRescaleThreshold = 8.0f;     // log2 units (factor 256)
+#ifndef DSC_RESCALE_T
+#define DSC_RESCALE_T 8.0f
+#endif
+constexpr float kRescaleThreshold = DSC_RESCALE_T;   // log2 units (8: factor 256)
 static_assert(kNQT * 128 == kMBlockRows, "work items are 256-row m-blocks");
 #ifndef DSC_POLY
 #define DSC_POLY 0

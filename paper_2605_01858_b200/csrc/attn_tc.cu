@@ -79,6 +79,10 @@ constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (16 KB)
 #ifndef DSC_LASTO
 #define DSC_LASTO 1
 #endif
+// DSC_OFHALF 1: O_qt is released to the next item in two column halves (see issue_pv_half)
+#ifndef DSC_OFHALF
+#define DSC_OFHALF 0
+#endif
 // DSC_EXBF 1: softmax exponentials as ex2.approx.bf16x2 (the exponent argument rounded to
 // bf16, two columns per MUFU op; P is bf16 for the PV MMA anyway and l sums that same P)
 #ifndef DSC_EXBF
@@ -130,7 +134,8 @@ constexpr int OFF_BAR = OFF_V + VST * kKVBytes;
 // behind (the parity test of mbarrier.try_wait cannot tell phase k from phase k+2): with S
 // prefetched two tiles ahead, PV(g-1) may still be pending when the softmax finishes tile g.
 constexpr int B_Q = 0, B_KR = 2 * kQBufs, B_KF = B_KR + KST, B_KE = B_KF + KST, B_VF = B_KE + KST, B_VE = B_VF + VST,
-              B_S = B_VE + VST, B_P = B_S + 4, B_O = B_P + 4, B_OF = B_O + 4, B_QE = B_OF + 2, B_EP = B_QE + 2, B_N = B_EP + 2;
+              B_S = B_VE + VST, B_P = B_S + 4, B_O = B_P + 4, B_OF = B_O + 4, B_QE = B_OF + 2, B_EP = B_QE + 2, B_OFH = B_EP + 2,
+              B_N = B_OFH + 2;
 // setmaxnreg budget per warpgroup: 2*softmax + rotation + copy/MMA <= 512 (x 128 threads)
 constexpr int kRegSoftmax = 144, kRegRotate = 136, kRegCopy = 88;
 static_assert(2 * kRegSoftmax + kRegRotate + kRegCopy <= 512, "setmaxnreg budget exceeds the 64K register file");
@@ -295,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(B_O + i), 1);
     }
     for (int i = 0; i < 2; ++i) mbar_init(bar(B_OF + i), 128);
+    for (int i = 0; i < 2; ++i) mbar_init(bar(B_OFH + i), 128);   // DSC_OFHALF: O columns 64..127 read
     for (int i = 0; i < 2; ++i) mbar_init(bar(B_QE + i), DSC_MMA2 ? 2 : 1);   // Q buffer i free (MMA commit(s) after an item)
     for (int i = 0; i < 2; ++i) mbar_init(bar(B_EP + i), 128); // l of a staged item handed to the rotation WG
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -711,14 +717,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int hf = 0; hf < 2; ++hf) {
         if (DSC_ABL_SWITCH & 2) {   // ablation: no O read-out / stores
-          if (hf == 1) { tc_fence_before(); mbar_arrive(bar(B_OF + qt)); }
+          if (hf == 1) {
+            tc_fence_before();
+            mbar_arrive(bar(B_OF + qt));
+            if (DSC_OFHALF) mbar_arrive(bar(B_OFH + qt));
+          }
           continue;
         }
         uint32_t o[64];
         tmem_ld32(tO + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
         tmem_ld32(tO + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
         tmem_wait_ld();
-        if (hf == 1) {
+        if (DSC_OFHALF) {
+          // each half of O_qt is released as soon as it is in registers: the next item's
+          // first PV writes columns 0..63 (B_OF) and 64..127 (B_OFH) as two N = 64 halves
+          tc_fence_before();
+          mbar_arrive(bar((hf == 0 ? B_OF : B_OFH) + qt));
+        } else if (hf == 1) {
           tc_fence_before();
           mbar_arrive(bar(B_OF + qt));      // O_qt may be overwritten by the next item
         }
@@ -1022,6 +1037,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (k8 < nk) mma_ts_w(d, a + k8 * 8, dv + (uint64_t)(k8 * 128), IPV, 1u);
         }
       };
+      // first PV of an item as two N = 64 column halves (DSC_OFHALF): V block `half` (columns
+      // 64*half .. +63 of the tile) into O_qt columns 64*half .. +63, no accumulate
+      auto issue_pv_half = [&](int qt, int vs, int nu, int buf, int half) {
+        constexpr uint32_t IPVH = idesc_bf16(128, 64, 0, 1);
+        const uint64_t dv = sdesc(sbase + OFF_V + vs * kKVBytes + half * kKVHalf, kKVHalf, 1024);
+        const uint32_t d = tmem + 256 + qt * 128 + half * 64, a = tmem + qt * 128 + buf * 64;
+        const int nk = nu >> 4;
+        mma_ts_w(d, a, dv, IPVH, 0u);
+#pragma unroll
+        for (int k8 = 1; k8 < kKT / 16; ++k8)
+          if (k8 < nk) mma_ts_w(d, a + k8 * 8, dv + (uint64_t)(k8 * 128), IPVH, 1u);
+      };
       // S of tile g for Q tile qt into buffer g & 1; K stage g % KST is free when both MMA
       // warps' QK^T of the tile are done (K-free barrier counts 2 commits)
       auto issue_s = [&](const ItemGeo& p, const Item& w, int g, int u) {
@@ -1175,10 +1202,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
           for (int qt = q_lo; qt < q_hi; ++qt) {
             if (!DSC_PJOIN) MWAIT(bar(B_P + qt * 2 + buf), (g >> 1) & 1);
+            if (DSC_OFHALF && jj == 0 && kk > 0) {
+              // first PV of the item in two column halves, each after its half of the
+              // previous item's O has been read out
+              MWAIT(bar(B_OF + qt), (kk - 1) & 1);
+              tc_fence_after();
+              issue_pv_half(qt, vs, nu, buf, 0);
+              MWAIT(bar(B_OFH + qt), (kk - 1) & 1);
+              tc_fence_after();
+              issue_pv_half(qt, vs, nu, buf, 1);
+            } else {
             if (jj == 0 && kk > 0) MWAIT(bar(B_OF + qt), (kk - 1) & 1);   // previous item's O read
             if (lane == 0) TRACE(EV_PV0 + qt, g);
             tc_fence_after();
             issue_pv(qt, vs, jj > 0, nu, buf);
+            }
             if (!DSC_LASTO) mma_commit_w(bar(B_O + qt * 2 + buf));
             else if (jj == n - 1) mma_commit_w(bar(B_O + qt * 2));   // one O commit per item (epilogue)
             if (lane == 0) TRACE(EV_PVI + qt, g);

@@ -22,6 +22,10 @@
 
 // DSC_SPLIT_DIV: the attend's key splits target num_sms / DSC_SPLIT_DIV work items when its
 // (problem, kv head, m-block) items cannot fill the SMs
+// DSC_STAGE_MIN: the build is staged when it has at least DSC_STAGE_MIN * num_sms items
+#ifndef DSC_STAGE_MIN
+#define DSC_STAGE_MIN 2LL
+#endif
 #ifndef DSC_SPLIT_DIV
 #define DSC_SPLIT_DIV 2   // measured vs 1: c4 +13.5%, c2 +24%, kvsplit +4.5% (3: c4 -5%)
 #endif
@@ -369,7 +373,7 @@ dscache_status prep_build(dscache_t h, int32_t lb, int32_t lc, const void* q_ins
   // Small launches (fewer build items than two waves of SMs, e.g. one stream x one layer)
   // are latency-bound: the extra staging launch costs more than the RoPE it saves there.
   const long long build_items = (long long)p.P * p.Hkv * p.n_mblocks;
-  if (h->impl_build == DSCACHE_IMPL_TC && h->stage_k && !h->dbg_build && build_items >= 2LL * h->num_sms) {
+  if (h->impl_build == DSCACHE_IMPL_TC && h->stage_k && !h->dbg_build && build_items >= DSC_STAGE_MIN * h->num_sms) {
     dsc::StageParams sp{};
     sp.sink_k = h->sink_k; sp.sink_v = h->sink_v; sp.ring_k = h->ring_k; sp.ring_v = h->ring_v;
     sp.stage_k = h->stage_k; sp.stage_v = h->stage_v; sp.rope_pairs = p.rope_pairs;

@@ -2,7 +2,7 @@
 # kvsplit, the default bench (with cpu_baseline), the reference arm, an ncu launch list,
 # --set full captures (fused step + split build / attend) and the append kernel's DRAM rate
 mkdir -p gpurun_out
-TAG=${1:-r11}
+TAG=${1:-r12}
 timeout -s KILL 1200 python -m pytest tests/test_gpu_parity.py -q -s -m gpu --timeout 1000 -p no:cacheprovider > gpurun_out/parity_$TAG.log 2>&1
 echo "parity rc=$?"; tail -2 gpurun_out/parity_$TAG.log
 timeout -s KILL 600 python -m pytest tests/test_gpu_peers.py -q -m gpu -p no:cacheprovider > gpurun_out/peers_$TAG.log 2>&1

@@ -1,0 +1,721 @@
+// K3/K4 v7: fused rotate-on-load RoPE + GQA flash attention on the sm_100a tensor cores
+// (tcgen05.mma, accumulators in TMEM) for both dscache_build_instant (Eq. 7: instant
+// tokens over [sink | instant], causal) and dscache_attend (Eq. 8 + self: the query chunk
+// over [sink | past | instant | self]).
+//
+// Position-agnostic encoding (Def. 4.1): the ring holds raw K; every K
+// tile of an attend item is rotated in shared memory at its use-time ids (consecutive from
+// 0) once for the 256 query rows that share it; a staged build reads K that
+// the staging kernel already rotated at the build ids.  Softmax a_ij = softmax(Q_i K_j /
+// sqrt(d)) in the exp2 domain with lazy rescale.
+//
+// Structure (one CTA per SM, persistent over work items = (problem, kv head, 256-row
+// m-block, key split)):
+//   * 128-key tiles: QK^T is one SS MMA of M = 128, N = 128 per K16 step (full tensor rate;
+//     N = 64 SS MMAs run at 2/3 rate, scripts/micro/mma_bench), PV a TS MMA (P in TMEM).
+//   * Two 128-row Q tiles per item ping-pong on the tensor core: while softmax warpgroup 0
+//     works on S0(j), the MMA computes PV1(j-1) and S1(j); while warpgroup 1 works on S1(j),
+//     PV0(j) and S0(j+1).  TMEM (512 columns): S0 = cols 0..127, S1 = 128..255, O0 = 256..383,
+//     O1 = 384..511; P_qt (bf16x2, 64 columns) overwrites the first half of S_qt and is the
+//     TMEM A operand of O_qt += P_qt V.  S_qt(j+1) is issued after PV_qt(j) (tcgen05 MMAs of
+//     one CTA execute in issue order), so the commit of S_qt(j) also tells the softmax that
+//     O_qt is quiescent (PV_qt(j-1) done): the lazy O rescale needs no extra wait.
+//   * Shared memory: 3 Q tile buffers (item k uses buffers (2k) % 3 and (2k+1) % 3, so the
+//     next item's first Q tile is loaded and rotated while the current item runs), 2 K and
+//     2 V stages of 32 KB (128 keys x 256 B, two 64-column SW128 blocks).
+//
+// CTA = 16 warps:
+//   warps 0-3  softmax of Q tile 0 (thread = query row = TMEM lane) + its O epilogue
+//   warps 4-7  softmax of Q tile 1
+//   warps 8-11 rotation: raw K tiles of attend items in place in smem, and the Q tiles of
+//              every later item (cp.async + rotation at the query ids); the first item's Q
+//              tiles are prepared by the softmax warpgroups (idle until the first S)
+//   warp 12    K copy (TMA box 64 cols x 128 rows; cp.async for sink/self tiles)
+//   warp 13    V copy
+//   warp 14    TMEM allocator + MMA issuer (whole warp, one elected lane issues)
+//   warp 15    idle
+#include "tc_common.cuh"
+
+#include <algorithm>
+#include <mutex>
+#include <utility>
+#include <vector>
+
+namespace dsc {
+namespace fa {
+using namespace tcc;
+
+constexpr int BN = 128;                       // keys per K/V tile
+constexpr int kWarps = 16;
+constexpr int kThreads = kWarps * 32;
+constexpr int kQBytes = 128 * 128 * 2;        // one 128-row Q tile (2 x 64-column SW128 blocks)
+constexpr int kKVHalf = BN * 128;             // one 64-column SW128 block of a K/V tile (16 KB)
+constexpr int kKVBytes = 2 * kKVHalf;         // one K or V tile (32 KB)
+constexpr int NQB = 3;                        // Q tile buffers
+#ifndef FA_KST
+#define FA_KST 2
+#endif
+#ifndef FA_VST
+#define FA_VST 2
+#endif
+constexpr int KST = FA_KST, VST = FA_VST;
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = OFF_Q + NQB * kQBytes;
+constexpr int OFF_V = OFF_K + KST * kKVBytes;
+constexpr int OFF_BAR = OFF_V + VST * kKVBytes;
+// barriers (8 B each)
+constexpr int B_QR = 0;                 // [NQB] Q tile buffer ready (128 arrivals)
+constexpr int B_QF = B_QR + NQB;        // [NQB] Q tile buffer free (MMA commit after its item's last QK^T)
+constexpr int B_KR = B_QF + NQB;        // [KST] K landed (TMA tx / copy warp arrive)
+constexpr int B_KF = B_KR + KST;        // [KST] K rotated (128 arrivals; attend tiles only)
+constexpr int B_KE = B_KF + KST;        // [KST] K stage free (commit after S1)
+constexpr int B_VR = B_KE + KST;        // [VST] V landed
+constexpr int B_VE = B_VR + VST;        // [VST] V stage free (commit after PV1)
+constexpr int B_S = B_VE + VST;         // [2] S_qt ready (commit)
+constexpr int B_P = B_S + 2;            // [2] P_qt ready (128 arrivals)
+constexpr int B_O = B_P + 2;            // [2] O_qt final for the item (commit after its last PV)
+constexpr int B_OF = B_O + 2;           // [2] O_qt read out by the epilogue (128 arrivals)
+constexpr int B_N = B_OF + 2;
+constexpr int kSmemBytes = OFF_BAR + B_N * 8 + 16 + 1024;   // + tmem slot + alignment slack
+static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+// setmaxnreg budget: 2 softmax warpgroups + rotation + (copy, MMA) <= 512 per thread x 128
+#ifndef FA_REG_SM
+#define FA_REG_SM 160
+#endif
+constexpr int kRegSoftmax = FA_REG_SM, kRegRotate = 128, kRegCopy = 512 - 2 * FA_REG_SM - 128;
+static_assert(kRegCopy >= 40, "copy/MMA warps need registers");
+static_assert(kRegCopy % 8 == 0 && kRegSoftmax % 8 == 0, "setmaxnreg takes multiples of 8");
+constexpr float kRescaleThreshold = 8.0f;    // log2 units: move the running max only when it grew by > 2^8
+// exponentials of a full tile: of every 16 columns, FA_POLY go through exp2_poly2 on the FMA
+// pipe (the MUFU pipe's 16 ex2/clk/SM exactly matches the tensor rate at d = 128)
+#ifndef FA_POLY
+#define FA_POLY 4
+#endif
+static_assert(FA_POLY >= 0 && FA_POLY <= 16 && FA_POLY % 4 == 0, "poly columns per 16: multiple of 4");
+
+// S = Q K^T over K = 128 (8 x K16), N = tile width: A (Q tile, 128 rows) and B (K tile,
+// 128 rows) SW128 K-major; the second 64-column block of either is +16 KB (1024 x 16 B).
+__device__ __forceinline__ void mma_qk(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred e;\n.reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n"
+      "add.s64 a1, %1, 2; add.s64 a2, %1, 4; add.s64 a3, %1, 6;\n"
+      "add.s64 a4, %1, 1024; add.s64 a5, %1, 1026; add.s64 a6, %1, 1028; add.s64 a7, %1, 1030;\n"
+      "add.s64 b1, %2, 2; add.s64 b2, %2, 4; add.s64 b3, %2, 6;\n"
+      "add.s64 b4, %2, 1024; add.s64 b5, %2, 1026; add.s64 b6, %2, 1028; add.s64 b7, %2, 1030;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, 1;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc)
+      : "memory");
+}
+// O += P V over a full 128-key tile (8 x K16): A (P) in TMEM, 8 columns per K16 step; B (V)
+// MN-major SW128, 16 keys = 2048 B (128 x 16 B) per step.  acc = 0 overwrites O.
+__device__ __forceinline__ void mma_pv8(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred e, p;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7;\n.reg .b32 t1, t2, t3, t4, t5, t6, t7;\n"
+      "add.s64 b1, %2, 128; add.s64 b2, %2, 256; add.s64 b3, %2, 384;\n"
+      "add.s64 b4, %2, 512; add.s64 b5, %2, 640; add.s64 b6, %2, 768; add.s64 b7, %2, 896;\n"
+      "add.u32 t1, %1, 8; add.u32 t2, %1, 16; add.u32 t3, %1, 24;\n"
+      "add.u32 t4, %1, 32; add.u32 t5, %1, 40; add.u32 t6, %1, 48; add.u32 t7, %1, 56;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t1], b1, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t2], b2, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t3], b3, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t4], b4, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t5], b5, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t6], b6, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t7], b7, %3, 1;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32x(uint32_t taddr, uint32_t* r) {
+  tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+}
+
+// The integer fields decode_item needs, selected per item from the two launch parameter
+// blocks (build / attend of a fused step) with constant-offset loads.
+__device__ __forceinline__ ItemGeo geo(const AttnParams& pa, const AttnParams& pb, bool isb) { return item_geo(pa, pb, isb); }
+
+// ------------------------------------------------------------------ kernel
+// Items [0, na) use pa, [na, na + nb) use pb (the fused step: attend items first, then the
+// build items).
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fa_kernel(const __grid_constant__ AttnParams pa, const __grid_constant__ AttnParams pb, int na, int nb) {
+  const AttnParams& p = pa;   // launch-wide fields (rope table, trace) are shared
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bar0 = sbase + OFF_BAR;
+  auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + B_N * 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_items = na + nb;
+#define ITEM_B(I) ((I) >= na)
+#define ITEM_PARAMS(I) (ITEM_B(I) ? pb : pa)
+#define ITEM_LOCAL(I) (ITEM_B(I) ? (I) - na : (I))
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NQB; ++i) {
+      mbar_init(bar(B_QR + i), 128);
+      mbar_init(bar(B_QF + i), 1);
+    }
+    for (int i = 0; i < KST; ++i) {
+      mbar_init(bar(B_KR + i), 1);
+      mbar_init(bar(B_KF + i), 128);
+      mbar_init(bar(B_KE + i), 1);
+    }
+    for (int i = 0; i < VST; ++i) {
+      mbar_init(bar(B_VR + i), 1);
+      mbar_init(bar(B_VE + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(B_S + i), 1);
+      mbar_init(bar(B_P + i), 128);
+      mbar_init(bar(B_O + i), 1);
+      mbar_init(bar(B_OF + i), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async();
+  }
+  if (warp == 14) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (warp == 12 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pa.tmap_k)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pa.tmap_v)) : "memory");
+    if (nb > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pb.tmap_k)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pb.tmap_v)) : "memory");
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // all 512 columns of this SM's TMEM: the allocation starts at lane 0, column 0; the
+  // descriptors take the returned base (no assumption about its value)
+  const uint32_t tmem = *tmem_slot;
+
+  // this CTA's items, in order: the launcher's list-scheduled work list, else the stride
+  // blockIdx.x, + gridDim.x, ...  Every role walks the same sequence.
+  const int* __restrict__ sched = pa.sched_items;
+  const int sj0 = sched ? pa.sched_off[blockIdx.x] : 0;
+  const int n_my = sched ? pa.sched_off[blockIdx.x + 1] - sj0
+                         : (n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0);
+  auto item_at = [&](int t) { return sched ? sched[sj0 + t] : (int)blockIdx.x + t * (int)gridDim.x; };
+  // Q tile use u = 2 * item + qt lives in buffer u % 3
+  auto qbuf_addr = [&](int u) { return sbase + OFF_Q + (uint32_t)((u % NQB) * kQBytes); };
+
+  if (warp < 8) {
+    // ================================================================ softmax + epilogue
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
+    const int qt = warp >> 2, quarter = warp & 3;
+    const int rloc = quarter * 32 + lane;
+    const int lt = threadIdx.x - qt * 128;           // 0..127 within the warpgroup
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_off + (uint32_t)(qt * 128);
+    const uint32_t tO = tmem + lane_off + (uint32_t)(256 + qt * 128);
+    const float sl2 = p.scale_log2;
+    const float2 scale2 = make_float2(sl2, sl2);
+    const uint32_t barS = bar(B_S + qt), barP = bar(B_P + qt);
+    if (n_my > 0) {   // Q tile qt of the first item (use qt -> buffer qt)
+      const int i0 = item_at(0);
+      const AttnParams& p0 = ITEM_PARAMS(i0);
+      const Item w0 = decode_item<BN>(p0, ITEM_LOCAL(i0));
+      issue_q_tile(p0, w0, qt, lt, qbuf_addr(qt));
+      rotate_q_tile(p0, w0, qt, lt, qbuf_addr(qt), 2 + qt);
+      mbar_arrive(bar(B_QR + qt));
+    }
+    int g = 0;
+    for (int kk = 0; kk < n_my; ++kk) {
+      const int idx = item_at(kk);
+      const AttnParams& p = ITEM_PARAMS(idx);
+      const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
+      const int A = w.A;
+      const int n = w.n_tiles;
+      const int rglob = w.m0 + qt * 128 + rloc;
+      const bool valid_row = rglob < w.rows_total;
+      const int qi = valid_row ? rglob / p.grp : 0;
+      const int lim = valid_row ? p.q_pos0 + qi : -1;
+      const bool warp_dead = __all_sync(0xffffffffu, !valid_row);
+      float m = -INFINITY;
+      float2 lsum2 = make_float2(0.f, 0.f);
+      uint32_t r[64];
+      for (int jj = 0; jj < n; ++jj, ++g) {
+        const int u = w.t_begin + jj;
+        const TileSeg t = tile_segments<BN>(p, w, u);
+        const int nu = t.width;                    // S columns [0, nu) hold this tile's scores
+        int c_lo, c_hi;
+        if (!valid_row) {
+          c_lo = 0; c_hi = 0;
+        } else if (u < w.n_extra) {                // sink always visible, self row j iff its id <= lim
+          c_lo = 0;
+          c_hi = min(max(min(A + w.n_self, max(A, lim - w.ring_count + 1)) - BN * u, 0), BN);
+        } else {
+          c_lo = t.lo0;
+          c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));   // id pos0 + c <= lim
+        }
+        mbar_wait(barS, g & 1);
+        if (warp_dead) {   // all 32 rows are padding: their P / O are never used
+          mbar_arrive(barP);
+          continue;
+        }
+        tc_fence_after();
+        // The tile's scores in two 64-column halves (64 registers each; the running max is
+        // updated lazily per half).  Half A's P words stay in registers until half B is done:
+        // if B moves the max, they are rescaled with O.
+        uint32_t pa[32];
+        float2 l0 = make_float2(0.f, 0.f), l1 = l0;
+        // load one half's (up to) 64 scores; invisible columns (and columns >= nu, which
+        // are never loaded) -> -inf; returns the half's max (scaled to log2 units) and
+        // whether any lane of the warp masked something
+        auto load_half = [&](int c0, bool& partial) {
+          tmem_ld32x(tS + c0, &r[0]);
+          if (nu > c0 + 32) tmem_ld32x(tS + c0 + 32, &r[32]);
+          tmem_wait_ld();
+          partial = __any_sync(0xffffffffu, !(c_lo <= c0 && c_hi >= c0 + 64));
+          if (partial) {
+            const unsigned span = (unsigned)max(c_hi - c_lo, 0);
+#pragma unroll
+            for (int c = 0; c < 64; ++c) r[c] = ((unsigned)(c0 + c - c_lo) < span) ? r[c] : 0xFF800000u;
+          }
+          float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < 64; c += 8) {     // 3-input max (FMNMX3): 2 columns per instruction
+            mx0 = fmax3f(mx0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+            mx1 = fmax3f(mx1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+            mx2 = fmax3f(mx2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
+            mx3 = fmax3f(mx3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
+          }
+          return fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+        };
+        // lazy rescale: move the running max only when it grew by > 2^8.  The TMEM load /
+        // store of O is warp-collective, so the O decision is taken per warp.  O_qt is
+        // quiescent: S_qt(g) was issued after PV_qt(g-1) and its commit covers both.
+        // Returns the factor applied to what was accumulated before (1 if m stayed).
+        auto update_max = [&](float m_half) {
+          const bool upd = m_half > m + kRescaleThreshold;
+          const bool need_o = upd && (m != -INFINITY);
+          const float f = need_o ? ex2(m - m_half) : 1.f;
+          if (upd) {
+            lsum2.x *= f; lsum2.y *= f;
+            l0.x *= f; l0.y *= f; l1.x *= f; l1.y *= f;
+            m = m_half;
+          }
+          if (__any_sync(0xffffffffu, need_o)) {
+#pragma unroll 1
+            for (int ch = 0; ch < 4; ++ch) {
+              uint32_t o[32];
+              tmem_ld32(tO + ch * 32, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+              tmem_st32(tO + ch * 32, o);
+            }
+            tmem_wait_st();
+          }
+          return f;
+        };
+        // P = 2^(s*scale - m) (masked -> 2^-inf = 0) of one half, packed bf16x2 into dst[0..31]
+        auto exp_half = [&](uint32_t* dst, int ncols, bool partial) {
+          const float m_use = (m == -INFINITY) ? 0.f : m;
+          const float2 negm2 = make_float2(-m_use, -m_use);
+#pragma unroll
+          for (int cb = 0; cb < 64; cb += 32) {
+            if (cb < ncols) {
+#pragma unroll
+              for (int c = cb; c < cb + 32; c += 4) {
+                const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+                const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
+                float2 p0, p1;
+                const bool poly = (c % 16) >= 16 - FA_POLY;
+                if (poly && !partial) {
+                  p0 = exp2_poly2(x0);
+                  p1 = exp2_poly2(x1);
+                } else {
+                  p0 = make_float2(ex2(x0.x), ex2(x0.y));
+                  p1 = make_float2(ex2(x1.x), ex2(x1.y));
+                }
+                l0 = __fadd2_rn(l0, p0);
+                l1 = __fadd2_rn(l1, p1);
+                dst[c >> 1] = pack_bf16(p0.x, p0.y);
+                dst[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
+              }
+            }
+          }
+        };
+        bool partA, partB;
+        update_max(load_half(0, partA));
+        exp_half(pa, nu, partA);
+        if (nu > 64) {
+          const float f = update_max(load_half(64, partB));
+          if (f != 1.f) {   // half A was exponentiated against the old max (rare)
+#pragma unroll
+            for (int c = 0; c < 32; ++c) pa[c] = pack_bf16(bf_lo(pa[c]) * f, bf_hi(pa[c]) * f);
+          }
+          exp_half(r, nu - 64, partB);
+          tmem_st32(tS, pa);
+          tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        } else {
+          tmem_st32(tS, pa);
+        }
+        lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(barP);
+      }
+      // ---- epilogue of the item: O / l once the last PV is done
+      const float lsum = lsum2.x + lsum2.y;
+      mbar_wait(bar(B_O + qt), kk & 1);
+      tc_fence_after();
+      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+      const int h = valid_row ? w.g * p.grp + rglob % p.grp : 0;
+      const long long orow = ((long long)w.pp * p.n_q + qi) * p.Hq + h;
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        tmem_ld32x(tO + 64 * hf, &r[0]);
+        tmem_ld32x(tO + 64 * hf + 32, &r[32]);
+        tmem_wait_ld();
+        if (hf == 1) {
+          tc_fence_before();
+          mbar_arrive(bar(B_OF + qt));      // O_qt may be overwritten by the next item's first PV
+        }
+        if (!valid_row) continue;
+        if (p.n_splits == 1 && p.split_only < 0) {
+          uint32_t q[8];
+          if (p.n_peers > 0) {
+            // fused all-gather: the same row to every peer's gathered O (NVLink stores)
+            const long long prow = ((long long)w.pp * p.n_q + qi) * p.o_hq + p.o_head_off + h;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                q[j] = pack_bf16(__uint_as_float(r[16 * v + 2 * j]) * inv, __uint_as_float(r[16 * v + 2 * j + 1]) * inv);
+#pragma unroll 1
+              for (int pr = 0; pr < p.n_peers; ++pr)
+                stg256(reinterpret_cast<__nv_bfloat16*>(p.peer_o[pr]) + prow * 128 + 64 * hf + 16 * v, q);
+            }
+          } else {
+            // 32-byte stores (STG.256): each one fills a whole L2 sector of this thread's row
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) + orow * 128 + 64 * hf;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                q[j] = pack_bf16(__uint_as_float(r[16 * v + 2 * j]) * inv, __uint_as_float(r[16 * v + 2 * j + 1]) * inv);
+              stg256(dst + 16 * v, q);
+            }
+          }
+        } else {
+          const long long rows = (long long)p.P * p.n_q * p.Hq;
+          const long long slot = p.split_only >= 0 ? 0 : w.sp;
+          float4* dst = reinterpret_cast<float4*>(p.ws_o + (slot * rows + orow) * 128 + 64 * hf);
+#pragma unroll
+          for (int v = 0; v < 16; ++v)
+            dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv, __uint_as_float(r[4 * v + 1]) * inv,
+                                 __uint_as_float(r[4 * v + 2]) * inv, __uint_as_float(r[4 * v + 3]) * inv);
+          if (hf == 0) p.ws_lse[slot * rows + orow] = lsum > 0.f ? m + __log2f(lsum) : -INFINITY;
+        }
+      }
+    }
+  } else if (warp < 12) {
+    // ================================================================ rotation (K tiles) + Q prep
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegRotate));
+    const int lt = threadIdx.x - 256;
+    const int c8 = lt & 7;             // frequencies 8*c8 .. 8*c8+7
+    const int rg = lt >> 3;            // rows rg*8 .. rg*8+7 of a 128-row tile
+    const float4* __restrict__ rp = p.rope_pairs;
+    float2 cth[4], sth[4];             // R(theta_f) = table entry of id 1
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 t = rp[32 + 4 * c8 + j];
+      cth[j] = make_float2(t.x, t.y);
+      sth[j] = make_float2(t.z, t.w);
+    }
+    // Q tile use qu (= 2 * item + qt) of item qidx: buffer qu % 3, free once use qu - 3's
+    // last QK^T has completed
+    auto prep_q = [&](int qu, int qidx) {
+      if (qu >= NQB) mbar_wait(bar(B_QF + qu % NQB), ((qu - NQB) / NQB) & 1);
+      const AttnParams& pq = ITEM_PARAMS(qidx);
+      const Item wq = decode_item<BN>(pq, ITEM_LOCAL(qidx));
+      issue_q_tile(pq, wq, qu & 1, lt, qbuf_addr(qu));
+      rotate_q_tile(pq, wq, qu & 1, lt, qbuf_addr(qu), 6);
+      mbar_arrive(bar(B_QR + qu % NQB));
+    };
+    int gt = 0;
+    uint32_t kf_ph = 0;   // phase bit per K stage of the rotated-tile barrier B_KF
+    for (int kk = 0; kk < n_my; ++kk) {
+      const int idx = item_at(kk);
+      const AttnParams& p = ITEM_PARAMS(idx);
+      const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
+      const int A = w.A;
+      const bool q_next = kk + 1 < n_my;
+      const int nidx = q_next ? item_at(kk + 1) : 0;
+      const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
+      if (w.staged || w.n_tiles == 0) {
+        if (q_next) prep_q(2 * kk + 2, nidx);
+      } else {
+        for (int jj = 0; jj < w.n_tiles; ++jj) {
+          const int g = gt + jj, u = w.t_begin + jj, ks = g % KST;
+          const TileSeg t = tile_segments<BN>(p, w, u);
+          int kpos[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) kpos[k] = seg_pos(t, rg * 8 + k);
+          int p0 = -1;
+#pragma unroll
+          for (int k = 7; k >= 0; --k)
+            if (kpos[k] >= 0) p0 = kpos[k];
+          float4 pre[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) pre[j] = rp[(long long)max(p0, 0) * 32 + 4 * c8 + j];
+          mbar_wait(bar(B_KR + ks), (g / KST) & 1);
+          if (rg * 8 < t.width)   // rows >= width are never read by the MMA
+            rotate_rows<2, kKVHalf>(sbase + OFF_K + ks * kKVBytes, rg * 8, c8, rp, cth, sth, kpos, pre, max(p0, 0));
+          fence_proxy_async();
+          mbar_arrive(bar(B_KF + ks));
+          kf_ph ^= 1u << ks;
+          if (dbg && c8 == 0) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int rr = rg * 8 + k;
+              const int x = BN * u + rr;
+              int slot = t.slot0 + rr;
+              if (slot >= p.R) slot -= p.R;
+              if (kpos[k] >= 0)
+                p.dbg_pos[(u < w.n_extra) ? (x < A ? x : p.dbg_A + p.dbg_R + (x - A)) : p.dbg_A + slot] = kpos[k];
+            }
+          }
+          if (jj == 0 && q_next) prep_q(2 * kk + 2, nidx);   // next item's Q tile 0 after the first K tile
+        }
+      }
+      if (q_next) prep_q(2 * kk + 3, nidx);   // Q tile 1: its buffer frees after this item's last S0
+      gt += w.n_tiles;
+    }
+    (void)kf_ph;
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCopy));
+    if (warp == 12 || warp == 13) {
+      // ============================================================== copy warps (12: K, 13: V)
+      const bool isk = warp == 12;
+      const int nst = isk ? KST : VST;
+      const int off = isk ? OFF_K : OFF_V;
+      const int b_full = isk ? B_KR : B_VR, b_free = isk ? B_KE : B_VE;
+      int gt = 0;
+      for (int kk = 0; kk < n_my; ++kk) {
+        const int idx = item_at(kk);
+        const AttnParams& p = ITEM_PARAMS(idx);
+        const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
+        const int A = p.A;
+        const __nv_bfloat16* __restrict__ SX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.sink_k : p.sink_v);
+        const __nv_bfloat16* __restrict__ XX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.self_k : p.self_v);
+#pragma unroll 1
+        for (int jj = 0; jj < w.n_tiles; ++jj) {
+          const int g = gt + jj, u = w.t_begin + jj, st = g % nst;
+          if (g >= nst) mbar_wait(bar(b_free + st), ((g - nst) / nst) & 1);
+          const uint32_t dst = sbase + off + st * kKVBytes;
+          const TileSeg t = tile_segments<BN>(p, w, u);
+          if (u < w.n_extra) {
+            // sink rows (x < A) + self rows (A <= x < A + n_self), zeros up to the tile width
+            const int nit = t.width >> 1;   // 16 chunks of 16 B per row, 32 lanes
+#pragma unroll 1
+            for (int it = 0; it < nit; ++it) {
+              const int id = it * 32 + lane;
+              const int rr = id >> 4, ch = id & 15;
+              const int x = BN * u + rr;
+              const __nv_bfloat16* src = nullptr;
+              if (x < A) src = SX + (w.head_row * A + x) * 128;
+              else if (x < A + w.n_self) src = XX + (((long long)w.pp * w.n_self + (x - A)) * p.Hkv + w.g) * 128;
+              const uint32_t d = dst + (ch >> 3) * kKVHalf + rr * 128 + (((ch & 7) ^ (rr & 7)) << 4);
+              cp_async16(d, src ? (const void*)(src + 8 * ch) : (const void*)SX, src ? 16u : 0u);
+            }
+            cp_async_wait_all();
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(b_full + st));
+          } else if (lane == 0) {
+            // logical window tile: one 128-row box per 64-column block (ring mirror or staging rows)
+            const CUtensorMap* tmap = isk ? &p.tmap_k : &p.tmap_v;
+            const int row = (int)(w.head_row * w.Rp) + t.slot0;
+            mbar_arrive_tx(bar(b_full + st), kKVBytes);
+            tma_load_2d(dst, tmap, 0, row, bar(b_full + st));
+            tma_load_2d(dst + kKVHalf, tmap, 64, row, bar(b_full + st));
+          }
+          __syncwarp();
+        }
+        gt += w.n_tiles;
+      }
+    } else if (warp == 14) {
+      // ============================================================== MMA issuer
+      constexpr uint32_t IQK0 = idesc_bf16(128, 0, 0, 0);    // S = Q K^T, both K-major; N = tile width
+      constexpr uint32_t IPV = idesc_bf16(128, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
+      auto issue_qk = [&](int qu, int ks, int nu, int qt) {
+        const uint64_t da = sdesc(qbuf_addr(qu), 16, 1024);
+        const uint64_t db = sdesc(sbase + OFF_K + ks * kKVBytes, 16, 1024);
+        mma_qk(tmem + qt * 128, da, db, IQK0 | ((uint32_t)(nu >> 3) << 17));
+      };
+      auto issue_pv = [&](int qt, int vs, bool acc, int nu) {
+        const uint64_t dv = sdesc(sbase + OFF_V + vs * kKVBytes, kKVHalf, 1024);
+        const uint32_t d = tmem + 256 + qt * 128, a = tmem + qt * 128;
+        if (nu == BN) {
+          mma_pv8(d, a, dv, IPV, acc ? 1u : 0u);
+        } else {
+          const int nk = nu >> 4;
+          mma_ts_w(d, a, dv, IPV, acc ? 1u : 0u);
+#pragma unroll 1
+          for (int k8 = 1; k8 < nk; ++k8) mma_ts_w(d, a + k8 * 8, dv + (uint64_t)(k8 * 128), IPV, 1u);
+        }
+      };
+      uint32_t kf_ph = 0;   // B_KF phase bit per K stage (only rotated tiles arrive there)
+      auto wait_k = [&](const Item& w, int g) {
+        const int ks = g % KST;
+        if (w.staged) {
+          mbar_wait(bar(B_KR + ks), (g / KST) & 1);
+        } else {
+          mbar_wait(bar(B_KF + ks), (kf_ph >> ks) & 1);
+          kf_ph ^= 1u << ks;
+        }
+        tc_fence_after();
+      };
+      int gt = 0;
+      for (int kk = 0; kk < n_my; ++kk) {
+        const int idx = item_at(kk);
+        const ItemGeo p = geo(pa, pb, ITEM_B(idx));
+        const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
+        const int n = w.n_tiles;
+        const int qu0 = 2 * kk, qu1 = 2 * kk + 1;
+        if (n == 0) {   // keep every per-item phase: O ready (zeros), Q buffers released
+          for (int qt = 0; qt < 2; ++qt) {
+            if (kk > 0) mbar_wait(bar(B_OF + qt), (kk - 1) & 1);
+            mma_commit_w(bar(B_O + qt));
+          }
+          mbar_wait(bar(B_QR + qu0 % NQB), (qu0 / NQB) & 1);
+          mbar_wait(bar(B_QR + qu1 % NQB), (qu1 / NQB) & 1);
+          mma_commit_w(bar(B_QF + qu0 % NQB));
+          mma_commit_w(bar(B_QF + qu1 % NQB));
+          continue;
+        }
+        int nu = tile_segments<BN>(p, w, w.t_begin).width;
+        // prologue: S0(gt), S1(gt)
+        wait_k(w, gt);
+        mbar_wait(bar(B_QR + qu0 % NQB), (qu0 / NQB) & 1);
+        tc_fence_after();
+        issue_qk(qu0, gt % KST, nu, 0);
+        mma_commit_w(bar(B_S + 0));
+        if (n == 1) mma_commit_w(bar(B_QF + qu0 % NQB));
+        mbar_wait(bar(B_QR + qu1 % NQB), (qu1 / NQB) & 1);
+        tc_fence_after();
+        issue_qk(qu1, gt % KST, nu, 1);
+        mma_commit_w(bar(B_S + 1));
+        mma_commit_w(bar(B_KE + gt % KST));
+        if (n == 1) mma_commit_w(bar(B_QF + qu1 % NQB));
+        for (int jj = 0; jj < n; ++jj) {
+          const int g = gt + jj, vs = g % VST;
+          const bool more = jj + 1 < n;
+          const int nu2 = more ? tile_segments<BN>(p, w, w.t_begin + jj + 1).width : 0;
+          mbar_wait(bar(B_VR + vs), (g / VST) & 1);
+          // ---- Q tile 0: PV0(g), then S0(g+1) into the columns P0(g) occupied
+          mbar_wait(bar(B_P + 0), g & 1);
+          if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + 0), (kk - 1) & 1);   // previous item's O0 read out
+          tc_fence_after();
+          issue_pv(0, vs, jj > 0, nu);
+          if (!more) mma_commit_w(bar(B_O + 0));
+          if (more) {
+            wait_k(w, g + 1);
+            issue_qk(qu0, (g + 1) % KST, nu2, 0);
+            mma_commit_w(bar(B_S + 0));
+            if (jj + 2 == n) mma_commit_w(bar(B_QF + qu0 % NQB));   // the item's last S0 issued
+          }
+          // ---- Q tile 1
+          mbar_wait(bar(B_P + 1), g & 1);
+          if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + 1), (kk - 1) & 1);
+          tc_fence_after();
+          issue_pv(1, vs, jj > 0, nu);
+          mma_commit_w(bar(B_VE + vs));
+          if (!more) mma_commit_w(bar(B_O + 1));
+          if (more) {
+            issue_qk(qu1, (g + 1) % KST, nu2, 1);
+            mma_commit_w(bar(B_S + 1));
+            mma_commit_w(bar(B_KE + (g + 1) % KST));
+            if (jj + 2 == n) mma_commit_w(bar(B_QF + qu1 % NQB));
+          }
+          nu = nu2;
+        }
+        gt += n;
+      }
+      // drain: the last V-free commit tracks every MMA of this CTA
+      if (gt > 0) mbar_wait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 14) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+#undef ITEM_B
+#undef ITEM_PARAMS
+#undef ITEM_LOCAL
+}
+
+}  // namespace fa
+
+int attn_fa_smem_bytes() { return fa::kSmemBytes; }
+
+namespace {
+// per-device one-time kernel attributes (a process may drive handles on several GPUs)
+std::mutex g_cfg_mu;
+uint64_t g_cfg_done = 0;
+int g_num_sms[64] = {0};
+cudaError_t configure_device(int* num_sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(g_cfg_mu);
+  if (dev < 64 && (g_cfg_done >> dev) & 1) { *num_sms = g_num_sms[dev]; return cudaSuccess; }
+  e = cudaFuncSetAttribute(fa::attn_fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  int sms = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64) { g_cfg_done |= 1ull << dev; g_num_sms[dev] = sms; }
+  *num_sms = sms;
+  return cudaSuccess;
+}
+}  // namespace
+
+long long attn_fa_items(const AttnParams& p) {
+  return (long long)p.P * p.Hkv * p.n_mblocks * (p.split_only >= 0 ? 1 : p.n_splits);
+}
+long long attn_fa_item_tiles(const AttnParams& p, int local) { return tcc::decode_item<fa::BN>(p, local).n_tiles; }
+
+cudaError_t launch_attn_fa(const AttnParams& pa, const AttnParams* pb, SchedCache* cache, cudaStream_t st) {
+  int num_sms = 0;
+  cudaError_t e = configure_device(&num_sms);
+  if (e != cudaSuccess) return e;
+  const long long na = attn_fa_items(pa), nb = pb ? attn_fa_items(*pb) : 0;
+  const long long items = na + nb;
+  if (items == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)(items < num_sms ? items : num_sms);
+  AttnParams qa = pa;
+  qa.sched_off = qa.sched_items = nullptr;
+  if (cache && items > grid) {
+    const int* lists = sched_lists(cache, pa, pb, na, nb, grid, &attn_fa_item_tiles, st);
+    if (lists) { qa.sched_off = lists; qa.sched_items = lists + grid + 1; }
+  }
+  fa::attn_fa_kernel<<<grid, fa::kThreads, fa::kSmemBytes, st>>>(qa, pb ? *pb : qa, (int)na, (int)nb);
+  return cudaGetLastError();
+}
+
+}  // namespace dsc

@@ -96,6 +96,10 @@ struct dscache_s {
   int ntrace = 0;
   int impl_build = DSCACHE_IMPL_SIMT, impl_attend = DSCACHE_IMPL_SIMT;
   int num_sms = 148;
+  // tcgen05 kernel: v7 (attn_fa.cu, 128-key tiles) or v5 (attn_tc.cu, 64-key tiles);
+  // DSC_KERNEL=tc selects v5 at create
+  int tile_n = dsc::kTileNFa;
+  dsc::SchedCache* sched = nullptr;   // v7 per-CTA work lists, owned by the handle
   CUtensorMap tmap_k{}, tmap_v{};
   // staged build (tcgen05): per-step copy of sink ++ instant window, K pre-rotated
   void* stage_k = nullptr;
@@ -161,6 +165,7 @@ void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c.head_dim));
   p.dtype = c.dtype;
   p.dbg_M = std::max(h->C, c.max_query_tokens);
+  p.dbg_A = c.sink_tokens; p.dbg_R = h->R;
   p.tmap_k = h->tmap_k; p.tmap_v = h->tmap_v;
   p.staged = 0;
   p.trace = h->trace; p.ntrace_cta = h->ntrace;
@@ -179,11 +184,17 @@ dscache_status grow_ws(dscache_t h, size_t bytes) {
   return DSCACHE_OK;
 }
 
+// the tcgen05 attention launch of this handle's kernel version (pb: the build items of a fused step)
+cudaError_t launch_tc(dscache_t h, const dsc::AttnParams& pa, const dsc::AttnParams* pb, cudaStream_t st) {
+  if (h->tile_n == dsc::kTileNFa) return dsc::launch_attn_fa(pa, pb, h->sched, st);
+  return pb ? dsc::launch_attn_tc2(pa, pb, st) : dsc::launch_attn_tc(pa, st);
+}
+
 dscache_status run_attention(dscache_t h, dsc::AttnParams& p, int impl, int kind, cudaStream_t st) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->prof) { e0 = h->take_event(); e1 = h->take_event(); cudaEventRecord(e0, st); }
   cudaError_t e;
-  if (impl == DSCACHE_IMPL_TC) e = dsc::launch_attn_tc(p, st);
+  if (impl == DSCACHE_IMPL_TC) e = launch_tc(h, p, nullptr, st);
   else e = dsc::launch_attn_simt(p, st);
   h->launches++;
   if (e == cudaSuccess && p.n_splits > 1 && p.split_only < 0) { e = dsc::launch_combine(p, st); h->launches++; }
@@ -244,6 +255,11 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   h->sink_filled.assign(c.num_layers, c.sink_tokens == 0 ? 1 : 0);
   h->last_evicted.assign(c.num_layers, -1);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, c.device);
+  {
+    const char* kern = std::getenv("DSC_KERNEL");
+    h->tile_n = (kern && std::strcmp(kern, "tc") == 0) ? dsc::kTileN : dsc::kTileNFa;
+  }
+  h->sched = dsc::sched_cache_new();
   if (c.attn_impl == DSCACHE_IMPL_SIMT) {
     h->impl_build = h->impl_attend = DSCACHE_IMPL_SIMT;
   } else {
@@ -272,8 +288,8 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   if (e == cudaSuccess) e = dsc::launch_rope_table(h->rope, h->npos, c.head_dim, c.rope_theta, 0);
   if (e == cudaSuccess && (h->impl_build == DSCACHE_IMPL_TC || h->impl_attend == DSCACHE_IMPL_TC)) {
     const unsigned long long rows = (unsigned long long)heads * h->Rp;
-    e = dsc::make_ring_tmap(&h->tmap_k, h->ring_k, rows);
-    if (e == cudaSuccess) e = dsc::make_ring_tmap(&h->tmap_v, h->ring_v, rows);
+    e = dsc::make_kv_tmap(&h->tmap_k, h->ring_k, rows, h->tile_n);
+    if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_v, h->ring_v, rows, h->tile_n);
   }
   if (e == cudaSuccess && h->impl_build == DSCACHE_IMPL_TC && h->C > 0) {
     h->stage_rows = c.sink_tokens + h->C;
@@ -281,8 +297,8 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
     if (cudaMalloc(&h->stage_k, sb) != cudaSuccess || cudaMalloc(&h->stage_v, sb) != cudaSuccess) return oom("staging");
     e = cudaMemset(h->stage_k, 0, sb);
     if (e == cudaSuccess) e = cudaMemset(h->stage_v, 0, sb);
-    if (e == cudaSuccess) e = dsc::make_stage_tmap(&h->tmap_sk, h->stage_k, (unsigned long long)heads * h->stage_rows);
-    if (e == cudaSuccess) e = dsc::make_stage_tmap(&h->tmap_sv, h->stage_v, (unsigned long long)heads * h->stage_rows);
+    if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_sk, h->stage_k, (unsigned long long)heads * h->stage_rows, h->tile_n);
+    if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_sv, h->stage_v, (unsigned long long)heads * h->stage_rows, h->tile_n);
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -305,6 +321,7 @@ dscache_status dscache_destroy(dscache_t h) {
   cudaFree(h->stage_k); cudaFree(h->stage_v);
   cudaFree(h->boost_k); cudaFree(h->boost_v);
   cudaFree(h->bstage_k); cudaFree(h->bstage_v);
+  dsc::sched_cache_free(h->sched);
   delete h;
   return DSCACHE_OK;
 }
@@ -456,7 +473,7 @@ dscache_status prep_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, c
   if (impl == DSCACHE_IMPL_TC) {
     // split the key range when (problem, kv head, m-block) work items cannot fill the SMs
     // sink/self tiles + logical window tiles (see tc_common.cuh tile_segments)
-    const int BN = dsc::kTileN;
+    const int BN = h->tile_n;
     const int tiles = std::max(1, (p.A + n_self + BN - 1) / BN + (p.ring_count + BN - 1) / BN);
     const int items = p.P * p.Hkv * p.n_mblocks;
     int splits = 1;
@@ -541,8 +558,8 @@ dscache_status dscache_build_instant_boost(dscache_t h, int32_t lb, int32_t lc, 
         cudaGetLastError();
         return fail(DSCACHE_E_OOM, "boost staging allocation failed");
       }
-      DSC_CUDA(dsc::make_stage_tmap(&h->tmap_bk, h->bstage_k, (unsigned long long)heads * rows));
-      DSC_CUDA(dsc::make_stage_tmap(&h->tmap_bv, h->bstage_v, (unsigned long long)heads * rows));
+      DSC_CUDA(dsc::make_kv_tmap(&h->tmap_bk, h->bstage_k, (unsigned long long)heads * rows, h->tile_n));
+      DSC_CUDA(dsc::make_kv_tmap(&h->tmap_bv, h->bstage_v, (unsigned long long)heads * rows, h->tile_n));
       h->bstage_rows = rows;
     }
     dsc::StageParams sp{};
@@ -615,7 +632,7 @@ dscache_status dscache_attend_partial(dscache_t h, int32_t lb, int32_t lc, const
   if (s != DSCACHE_OK) return s;
   // the key tiles of every item (sink/self tiles, then logical window tiles), cut into n_parts
   // contiguous ranges; part `part` is computed here
-  const int BN = dsc::kTileN;
+  const int BN = h->tile_n;
   const int tiles = (p.A + n_q + BN - 1) / BN + (p.ring_count + BN - 1) / BN;
   const int tps = (tiles + n_parts - 1) / n_parts;
   if ((long long)(n_parts - 1) * tps >= tiles)
@@ -734,7 +751,7 @@ dscache_status dscache_step(dscache_t h, int32_t lb, int32_t lc, const void* k_f
   // one persistent tcgen05 launch: the attend items (longest) first, then the build items
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->prof) { e0 = h->take_event(); e1 = h->take_event(); cudaEventRecord(e0, st); }
-  cudaError_t e = dsc::launch_attn_tc2(pa, &pb, st);
+  cudaError_t e = launch_tc(h, pa, &pb, st);
   h->launches++;
   if (e == cudaSuccess && pa.n_splits > 1) { e = dsc::launch_combine(pa, st); h->launches++; }
   if (h->prof) {

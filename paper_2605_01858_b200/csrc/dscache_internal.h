@@ -49,8 +49,10 @@ struct AttnParams {
   float* ws_lse;                             // [n_splits][P][n_q][Hq]
   // tcgen05 kernel work decomposition
   int n_mblocks;                             // ceil(n_q * grp / (2 * kTileM))
-  // debug export (K7); null = off
-  int* dbg_pos; int dbg_M;
+  // debug export (K7); null = off.  Layout [dbg_A sink ids | dbg_R ring-slot ids | dbg_M self ids |
+  // query ids], indexed with the RING geometry (dbg_A, dbg_R) even when the launch reads a
+  // staging buffer (staged build: A = 0, R = staging rows)
+  int* dbg_pos; int dbg_M; int dbg_A, dbg_R;
   // per-CTA event timeline (profiling); null = off.  [ntrace_cta][kTraceEvents][kTraceTiles] clock64
   long long* trace; int ntrace_cta;
   int dtype;                                 // 0 bf16, 1 fp32
@@ -112,6 +114,18 @@ cudaError_t launch_combine(const AttnParams& p, cudaStream_t st);
 cudaError_t launch_combine_partials(int n, long long rows, int d, const float* o_parts, const float* lse, void* o,
                                     cudaStream_t st);
 int attn_tc_smem_bytes();
+// v7 kernel (attn_fa.cu): 128-key tiles, Q-tile ping-pong; work lists from a per-handle cache
+struct SchedCache;
+SchedCache* sched_cache_new();
+void sched_cache_free(SchedCache* c);
+// device work lists [grid + 1 offsets | items] for this launch shape, or nullptr (static stride)
+const int* sched_lists(SchedCache* cache, const AttnParams& pa, const AttnParams* pb, long long na, long long nb,
+                       unsigned grid, long long (*item_tiles)(const AttnParams&, int), cudaStream_t st);
+cudaError_t launch_attn_fa(const AttnParams& pa, const AttnParams* pb, SchedCache* cache, cudaStream_t st);
+int attn_fa_smem_bytes();
+constexpr int kTileNFa = 128;  // keys per tile of the v7 kernel
+// K/V tensor map: [rows][128] bf16, box 64 columns x box_rows rows, SW128
+cudaError_t make_kv_tmap(CUtensorMap* map, void* base, unsigned long long rows, int box_rows);
 // encode the 2-D ring tensor map (bf16, d = 128) used by the tcgen05 kernel
 cudaError_t make_ring_tmap(CUtensorMap* map, void* base, unsigned long long rows);
 cudaError_t make_stage_tmap(CUtensorMap* map, void* base, unsigned long long rows);

@@ -358,7 +358,7 @@ __device__ __forceinline__ ItemGeo item_geo(const AttnParams& pa, const AttnPara
 #undef DSC_SEL
   return q;
 }
-template <class PT>
+template <int BN = kTileN, class PT>
 __host__ __device__ __forceinline__ Item decode_item(const PT& p, int idx) {
   Item w;
   const bool one = p.split_only >= 0;          // context-parallel partial: one split per launch
@@ -393,8 +393,8 @@ __host__ __device__ __forceinline__ Item decode_item(const PT& p, int idx) {
   w.cnt = min(max(lim_max - p.A + 1, 0), p.ring_count);
   w.A = p.A; w.n_self = p.n_self; w.ring_count = p.ring_count; w.ring_start = p.ring_start; w.R = p.R;
   w.Rp = p.Rp; w.staged = p.staged;
-  w.n_extra = (p.A + p.n_self + kTileN - 1) / kTileN;
-  const int total = w.n_extra + (w.cnt + kTileN - 1) / kTileN;
+  w.n_extra = (p.A + p.n_self + BN - 1) / BN;
+  const int total = w.n_extra + (w.cnt + BN - 1) / BN;
   w.t_begin = min(w.sp * p.tiles_per_split, total);
   w.n_tiles = min(total, w.t_begin + p.tiles_per_split) - w.t_begin;
   return w;
@@ -415,19 +415,19 @@ struct TileSeg {
   int width;
 };
 
-template <class PT>
+template <int BN = kTileN, class PT>
 __device__ __forceinline__ TileSeg tile_segments(const PT&, const Item& w, int u) {
   TileSeg t;
   int valid;
   if (u < w.n_extra) {
-    const int x0 = kTileN * u;
-    t.lo0 = 0; t.hi0 = min(max(w.A - x0, 0), kTileN); t.pos0_0 = x0;
-    t.lo1 = t.hi0; t.hi1 = min(max(w.A + w.n_self - x0, 0), kTileN); t.pos0_1 = w.ring_count + x0;
+    const int x0 = BN * u;
+    t.lo0 = 0; t.hi0 = min(max(w.A - x0, 0), BN); t.pos0_0 = x0;
+    t.lo1 = t.hi0; t.hi1 = min(max(w.A + w.n_self - x0, 0), BN); t.pos0_1 = w.ring_count + x0;
     t.slot0 = -1;
     valid = t.hi1;
   } else {
-    const int base = kTileN * (u - w.n_extra);
-    valid = min(w.cnt - base, kTileN);
+    const int base = BN * (u - w.n_extra);
+    valid = min(w.cnt - base, BN);
     t.lo0 = 0; t.hi0 = valid; t.pos0_0 = w.A + base;
     t.lo1 = 0; t.hi1 = 0; t.pos0_1 = 0;
     int s0 = w.ring_start + base;
@@ -563,7 +563,7 @@ __device__ __forceinline__ void rotate_q_tile(const AttnParams& p, const Item& w
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     pos[k] = (row0 + k < w.rows_total) ? p.q_pos0 + i : -1;
-    if (dbg && c8 == 0 && hh == 0 && pos[k] >= 0) p.dbg_pos[p.A + p.R + p.dbg_M + i] = pos[k];
+    if (dbg && c8 == 0 && hh == 0 && pos[k] >= 0) p.dbg_pos[p.dbg_A + p.dbg_R + p.dbg_M + i] = pos[k];
     if (++hh == p.grp) { hh = 0; ++i; }
   }
   const int p0 = max(pos[0], 0);
@@ -618,7 +618,7 @@ __device__ __forceinline__ void load_rotate_q_tile(const AttnParams& p, const It
     for (int k = 0; k < 4; ++k) {
       const bool ok = row0 + half * 4 + k < w.rows_total;
       pos[k] = ok ? p.q_pos0 + i : -1;
-      if (dbg && c8 == 0 && hh == 0 && ok) p.dbg_pos[p.A + p.R + p.dbg_M + i] = pos[k];
+      if (dbg && c8 == 0 && hh == 0 && ok) p.dbg_pos[p.dbg_A + p.dbg_R + p.dbg_M + i] = pos[k];
       if (ok) {
         const __nv_bfloat16* src = qbase + ((long long)i * p.Hq + hh) * 128;
         lo[k] = ldg128(src);

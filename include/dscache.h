@@ -330,6 +330,14 @@ dscache_status dscache_profile_read(dscache_t h, double* ms_build, double* ms_at
  * handle: DSCACHE_IMPL_TC or DSCACHE_IMPL_SIMT. */
 int32_t dscache_attn_impl(dscache_t h, int32_t which);
 
+/* Debug: pipeline-watchdog records of the tcgen05 kernel.  With the environment variable
+ * DSC_WATCHDOG=1 set before the first launch, a kernel wait that spins ~2^31 cycles writes
+ * (cta, warp, barrier index, parity, clock) into host-mapped memory before trapping; this
+ * copies n uint64 words of that record (word 0 = number of records, then 4 words each) to
+ * out.  The memory is host memory, so it stays readable after the context has died.
+ * Returns 0, or -1 when the watchdog record is not enabled. */
+int32_t dscache_watchdog_read(uint64_t* out, int32_t n);
+
 /* Thread-local message of the last failing call ("" if none). */
 const char* dscache_last_error(void);
 

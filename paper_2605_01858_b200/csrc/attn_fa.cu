@@ -37,6 +37,8 @@
 #include "tc_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -80,18 +82,54 @@ constexpr int kSmemBytes = OFF_BAR + B_N * 8 + 16 + 1024;   // + tmem slot + ali
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 // setmaxnreg budget: 2 softmax warpgroups + rotation + (copy, MMA) <= 512 per thread x 128
 #ifndef FA_REG_SM
-#define FA_REG_SM 160
+#define FA_REG_SM 152
 #endif
-constexpr int kRegSoftmax = FA_REG_SM, kRegRotate = 128, kRegCopy = 512 - 2 * FA_REG_SM - 128;
+constexpr int kRegSoftmax = FA_REG_SM, kRegRotate = 136, kRegCopy = 512 - 2 * FA_REG_SM - 136;
 static_assert(kRegCopy >= 40, "copy/MMA warps need registers");
-static_assert(kRegCopy % 8 == 0 && kRegSoftmax % 8 == 0, "setmaxnreg takes multiples of 8");
+static_assert(kRegCopy % 8 == 0 && kRegSoftmax % 8 == 0 && kRegRotate % 8 == 0, "setmaxnreg takes multiples of 8");
+static_assert(kRegSoftmax > 128 && kRegCopy < 128, "launch allocation is 128 per thread: softmax grows, copy/MMA shrink");
 constexpr float kRescaleThreshold = 8.0f;    // log2 units: move the running max only when it grew by > 2^8
-// exponentials of a full tile: of every 16 columns, FA_POLY go through exp2_poly2 on the FMA
-// pipe (the MUFU pipe's 16 ex2/clk/SM exactly matches the tensor rate at d = 128)
-#ifndef FA_POLY
-#define FA_POLY 4
+
+// ablation knobs (timing experiments only; results are wrong when set): FA_ABL_SOFTMAX skips
+// the softmax body, FA_ABL_ROT the K rotation, FA_ABL_EPI the O read-out and stores,
+// FA_ABL_Q the Q loads + rotation, FA_ABL_PV the PV MMAs
+#ifndef FA_ABL_SOFTMAX
+#define FA_ABL_SOFTMAX 0
 #endif
-static_assert(FA_POLY >= 0 && FA_POLY <= 16 && FA_POLY % 4 == 0, "poly columns per 16: multiple of 4");
+#ifndef FA_ABL_ROT
+#define FA_ABL_ROT 0
+#endif
+#ifndef FA_ABL_EPI
+#define FA_ABL_EPI 0
+#endif
+#ifndef FA_ABL_Q
+#define FA_ABL_Q 0
+#endif
+#ifndef FA_ABL_PV
+#define FA_ABL_PV 0
+#endif
+// FA_TRACE 1 (profiling variant): clock64 of pipeline events into p.trace, layout
+// [ntrace_cta][kFtEvents][kFtIdx] for the first ntrace_cta CTAs; per-tile events are indexed
+// by the CTA's tile counter g, per-item events by the CTA's item counter
+#ifndef FA_TRACE
+#define FA_TRACE 0
+#endif
+constexpr int kFtEvents = 32, kFtIdx = 1024;
+enum {
+  FT_MMA_P0 = 0, FT_MMA_P1, FT_MMA_K, FT_MMA_V, FT_SM0_S, FT_SM0_P, FT_SM1_S, FT_SM1_P, FT_ROT_KR, FT_ROT_KF,
+  FT_CPK, FT_CPV,                                                                // per tile
+  FT_MMA_ITEM = 12, FT_MMA_Q0, FT_MMA_Q1, FT_EPI0_O, FT_EPI0_END, FT_QE_START, FT_QE_END, FT_QO_START, FT_QO_FREE,
+  FT_QO_END, FT_MMA_OF, FT_EPI1_O, FT_EPI1_END, FT_END,                           // per item
+  FT_SMX_LD0 = 26, FT_SMX_EX0, FT_SMX_LD1, FT_SMX_EX1                               // per tile, warp 0 steps
+};
+#if FA_TRACE
+#define FT(ev, i)                                                                                      \
+  do {                                                                                                 \
+    if (ft_cta && (i) < kFtIdx) ft_cta[(ev) * kFtIdx + (i)] = clock64();                                \
+  } while (0)
+#else
+#define FT(ev, i) do { } while (0)
+#endif
 
 // S = Q K^T over K = 128 (8 x K16), N = tile width: A (Q tile, 128 rows) and B (K tile,
 // 128 rows) SW128 K-major; the second 64-column block of either is +16 KB (1024 x 16 B).
@@ -137,8 +175,118 @@ __device__ __forceinline__ void mma_pv8(uint32_t d_tmem, uint32_t a_tmem, uint64
       : "memory");
 }
 
+// Watchdog record (debugging a pipeline deadlock): a wait that spins ~2^31 cycles writes
+// (cta, warp, barrier index, parity, clock) into a host-mapped buffer, readable after the
+// context has died, then traps.  Null (default) = just trap.
+__device__ unsigned long long* g_fa_wd = nullptr;
+__device__ __noinline__ void fa_wd_fail(uint32_t bar_off, uint32_t parity) {
+  unsigned long long* wd = g_fa_wd;
+  if (wd) {
+    const unsigned long long i = atomicAdd(wd, 1ull);
+    if (i < 64) {
+      volatile unsigned long long* rec = wd + 1 + 4 * i;
+      rec[0] = blockIdx.x;
+      rec[1] = threadIdx.x >> 5;
+      rec[2] = ((unsigned long long)bar_off << 32) | parity;
+      rec[3] = clock64();
+      __threadfence_system();
+    }
+  }
+  __trap();
+}
+__device__ __forceinline__ void fwait(uint32_t bar, uint32_t parity, uint32_t bar0) {
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity)) {
+    if (clock64() - t0 > (1ll << 31)) fa_wd_fail((bar - bar0) / 8, parity);
+  }
+}
+
+// 2^x on the MUFU (not volatile: the compiler may schedule it like any arithmetic)
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ void tmem_ld32x(uint32_t taddr, uint32_t* r) {
   tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+}
+
+// Q tile qt of item w (rows m0 + 128 qt .. +127 = (query, head) pairs) loaded straight from
+// global memory into registers and rotated there at the query ids; the caller stores the 16
+// chunks into the SW128 tile once its buffer is free (so the HBM latency of the load runs
+// before the wait, not after it).  Thread lt holds frequencies 8*c8 .. 8*c8+7 (16-byte chunk
+// c8 of the low and the high 64-column block) of rows rg8*8 .. +7.
+__device__ __forceinline__ void load_rotate_q_regs(const AttnParams& p, const Item& w, int qt, int lt,
+                                                   uint4 (&lo)[8], uint4 (&hi)[8]) {
+  const float4* __restrict__ rp = p.rope_pairs;
+  const __nv_bfloat16* __restrict__ Qg = reinterpret_cast<const __nv_bfloat16*>(p.q);
+  const int c8 = lt & 7, rg8 = lt >> 3;
+  const int row0 = w.m0 + qt * 128 + rg8 * 8;
+  const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0 && c8 == 0;
+  const __nv_bfloat16* qbase = Qg + ((long long)w.pp * p.n_q) * p.Hq * 128 + (long long)w.g * p.grp * 128 + 8 * c8;
+  int pos[8];
+  {
+    int i = row0 / p.grp, hh = row0 % p.grp;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {   // all 16 loads in flight before any use
+      const bool ok = row0 + k < w.rows_total;
+      pos[k] = ok ? p.q_pos0 + i : -1;
+      if (dbg && hh == 0 && ok) p.dbg_pos[p.dbg_A + p.dbg_R + p.dbg_M + i] = pos[k];
+      if (ok) {
+        const __nv_bfloat16* src = qbase + ((long long)i * p.Hq + hh) * 128;
+        lo[k] = ldg128(src);
+        hi[k] = ldg128(src + 64);
+      } else {
+        lo[k] = hi[k] = make_uint4(0, 0, 0, 0);
+      }
+      if (++hh == p.grp) { hh = 0; ++i; }
+    }
+  }
+  float2 cth[4], sth[4], cs[4], sn[4];
+  const int p0 = max(pos[0], 0);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float4 t = rp[32 + 4 * c8 + j];
+    cth[j] = make_float2(t.x, t.y);
+    sth[j] = make_float2(t.z, t.w);
+    const float4 u = rp[(long long)p0 * 32 + 4 * c8 + j];
+    cs[j] = make_float2(u.x, u.y);
+    sn[j] = make_float2(u.z, u.w);
+  }
+  int prev = p0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int pk = pos[k];
+    if (pk < 0) continue;   // padding row: zeros
+    if (pk == prev + 1) {   // next query id: advance (cos, sin) by R(theta)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 nc = __ffma2_rn(cs[j], cth[j], __fmul2_rn(make_float2(-sn[j].x, -sn[j].y), sth[j]));
+        sn[j] = __ffma2_rn(sn[j], cth[j], __fmul2_rn(cs[j], sth[j]));
+        cs[j] = nc;
+      }
+    } else if (pk != prev) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 t = rp[(long long)pk * 32 + 4 * c8 + j];
+        cs[j] = make_float2(t.x, t.y);
+        sn[j] = make_float2(t.z, t.w);
+      }
+    }
+    prev = pk;
+    uint32_t ol[4], oh[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 av = bf2(get_w(lo[k], j)), bv = bf2(get_w(hi[k], j));
+      const float2 yl = __ffma2_rn(av, cs[j], __fmul2_rn(make_float2(-bv.x, -bv.y), sn[j]));   // a cos - b sin
+      const float2 yh = __ffma2_rn(av, sn[j], __fmul2_rn(bv, cs[j]));                        // a sin + b cos
+      ol[j] = pack_bf16(yl.x, yl.y);
+      oh[j] = pack_bf16(yh.x, yh.y);
+    }
+    lo[k] = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+    hi[k] = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+  }
 }
 
 // The integer fields decode_item needs, selected per item from the two launch parameter
@@ -151,6 +299,10 @@ __device__ __forceinline__ ItemGeo geo(const AttnParams& pa, const AttnParams& p
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fa_kernel(const __grid_constant__ AttnParams pa, const __grid_constant__ AttnParams pb, int na, int nb) {
   const AttnParams& p = pa;   // launch-wide fields (rope table, trace) are shared
+#if FA_TRACE
+  long long* const ft_cta = (pa.trace && blockIdx.x < (unsigned)pa.ntrace_cta)
+                                ? pa.trace + (long long)blockIdx.x * kFtEvents * kFtIdx : nullptr;
+#endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(smem_raw) + 1023u) & ~1023u;
@@ -229,209 +381,212 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sl2 = p.scale_log2;
     const float2 scale2 = make_float2(sl2, sl2);
     const uint32_t barS = bar(B_S + qt), barP = bar(B_P + qt);
-    if (n_my > 0) {   // Q tile qt of the first item (use qt -> buffer qt)
-      const int i0 = item_at(0);
-      const AttnParams& p0 = ITEM_PARAMS(i0);
-      const Item w0 = decode_item<BN>(p0, ITEM_LOCAL(i0));
-      issue_q_tile(p0, w0, qt, lt, qbuf_addr(qt));
-      rotate_q_tile(p0, w0, qt, lt, qbuf_addr(qt), 2 + qt);
-      mbar_arrive(bar(B_QR + qt));
-    }
+    // The epilogue of item k (O / l -> global) runs after the FIRST tile of item k+1: the
+    // softmax of that tile is not delayed by it, only the next item's first PV waits for
+    // the O read-out (B_OF).  O_qt(k) is final by then: PV_qt(last of k) was issued before
+    // S_qt(first of k+1).  One call site: kk = n_my is a virtual item without tiles.
     int g = 0;
-    for (int kk = 0; kk < n_my; ++kk) {
-      const int idx = item_at(kk);
+    int idx_e = -1;               // item whose epilogue is pending
+    float m_e = 0.f, lsum_e = 0.f;
+    for (int kk = 0; kk <= n_my; ++kk) {
+      const bool real = kk < n_my;
+      const int idx = real ? item_at(kk) : 0;
       const AttnParams& p = ITEM_PARAMS(idx);
       const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
       const int A = w.A;
-      const int n = w.n_tiles;
+      const int n = real ? w.n_tiles : 0;
       const int rglob = w.m0 + qt * 128 + rloc;
-      const bool valid_row = rglob < w.rows_total;
+      const bool valid_row = real && rglob < w.rows_total;
       const int qi = valid_row ? rglob / p.grp : 0;
       const int lim = valid_row ? p.q_pos0 + qi : -1;
       const bool warp_dead = __all_sync(0xffffffffu, !valid_row);
       float m = -INFINITY;
       float2 lsum2 = make_float2(0.f, 0.f);
       uint32_t r[64];
-      for (int jj = 0; jj < n; ++jj, ++g) {
-        const int u = w.t_begin + jj;
-        const TileSeg t = tile_segments<BN>(p, w, u);
-        const int nu = t.width;                    // S columns [0, nu) hold this tile's scores
-        int c_lo, c_hi;
-        if (!valid_row) {
-          c_lo = 0; c_hi = 0;
-        } else if (u < w.n_extra) {                // sink always visible, self row j iff its id <= lim
-          c_lo = 0;
-          c_hi = min(max(min(A + w.n_self, max(A, lim - w.ring_count + 1)) - BN * u, 0), BN);
-        } else {
-          c_lo = t.lo0;
-          c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));   // id pos0 + c <= lim
-        }
-        mbar_wait(barS, g & 1);
-        if (warp_dead) {   // all 32 rows are padding: their P / O are never used
-          mbar_arrive(barP);
-          continue;
-        }
-        tc_fence_after();
-        // The tile's scores in two 64-column halves (64 registers each; the running max is
-        // updated lazily per half).  Half A's P words stay in registers until half B is done:
-        // if B moves the max, they are rescaled with O.
-        uint32_t pa[32];
-        float2 l0 = make_float2(0.f, 0.f), l1 = l0;
-        // load one half's (up to) 64 scores; invisible columns (and columns >= nu, which
-        // are never loaded) -> -inf; returns the half's max (scaled to log2 units) and
-        // whether any lane of the warp masked something
-        auto load_half = [&](int c0, bool& partial) {
-          tmem_ld32x(tS + c0, &r[0]);
-          if (nu > c0 + 32) tmem_ld32x(tS + c0 + 32, &r[32]);
-          tmem_wait_ld();
-          partial = __any_sync(0xffffffffu, !(c_lo <= c0 && c_hi >= c0 + 64));
-          if (partial) {
-            const unsigned span = (unsigned)max(c_hi - c_lo, 0);
-#pragma unroll
-            for (int c = 0; c < 64; ++c) r[c] = ((unsigned)(c0 + c - c_lo) < span) ? r[c] : 0xFF800000u;
+      const int n1 = n > 0 ? n : 1;
+      for (int jj = 0; jj < n1; ++jj) {
+        if (real) {
+          const int u = w.t_begin + jj;
+          const TileSeg t = tile_segments<BN>(p, w, u);
+          const int nu = t.width;                    // S columns [0, nu) hold this tile's scores
+          int c_lo, c_hi;
+          if (!valid_row) {
+            c_lo = 0; c_hi = 0;
+          } else if (u < w.n_extra) {                // sink always visible, self row j iff its id <= lim
+            c_lo = 0;
+            c_hi = min(max(min(A + w.n_self, max(A, lim - w.ring_count + 1)) - BN * u, 0), BN);
+          } else {
+            c_lo = t.lo0;
+            c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));   // id pos0 + c <= lim
           }
-          float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll
-          for (int c = 0; c < 64; c += 8) {     // 3-input max (FMNMX3): 2 columns per instruction
-            mx0 = fmax3f(mx0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
-            mx1 = fmax3f(mx1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
-            mx2 = fmax3f(mx2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
-            mx3 = fmax3f(mx3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
-          }
-          return fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
-        };
-        // lazy rescale: move the running max only when it grew by > 2^8.  The TMEM load /
-        // store of O is warp-collective, so the O decision is taken per warp.  O_qt is
-        // quiescent: S_qt(g) was issued after PV_qt(g-1) and its commit covers both.
-        // Returns the factor applied to what was accumulated before (1 if m stayed).
-        auto update_max = [&](float m_half) {
-          const bool upd = m_half > m + kRescaleThreshold;
-          const bool need_o = upd && (m != -INFINITY);
-          const float f = need_o ? ex2(m - m_half) : 1.f;
-          if (upd) {
-            lsum2.x *= f; lsum2.y *= f;
-            l0.x *= f; l0.y *= f; l1.x *= f; l1.y *= f;
-            m = m_half;
-          }
-          if (__any_sync(0xffffffffu, need_o)) {
+          fwait(barS, g & 1, bar0);
+          if (rloc == 0) FT(qt ? FT_SM1_S : FT_SM0_S, g);
+          if (warp_dead || FA_ABL_SOFTMAX) {   // all 32 rows are padding: their P / O are never used
+            mbar_arrive(barP);
+          } else {
+            tc_fence_after();
+            // The tile's scores in 64-column halves (64 registers; one copy of the code, not
+            // unrolled over the halves).  The running max is updated lazily per half; P of a
+            // half goes to TMEM at once (P words 32h..32h+31 alias S columns already read).  If
+            // half 1 moves the max, half 0's P words are rescaled in TMEM (rare).
+            float2 l0 = make_float2(0.f, 0.f), l1 = l0;
+            const int nh = nu > 64 ? 2 : 1;
 #pragma unroll 1
-            for (int ch = 0; ch < 4; ++ch) {
-              uint32_t o[32];
-              tmem_ld32(tO + ch * 32, o);
+            for (int hf = 0; hf < nh; ++hf) {
+              const int c0 = 64 * hf;
+              tmem_ld32x(tS + c0, &r[0]);
+              if (nu > c0 + 32) tmem_ld32x(tS + c0 + 32, &r[32]);
               tmem_wait_ld();
+              if (warp == 0 && lane == 0) FT(hf ? FT_SMX_LD1 : FT_SMX_LD0, g);
+              // invisible columns (and columns >= nu, which are never loaded) -> -inf
+              const bool partial = __any_sync(0xffffffffu, !(c_lo <= c0 && c_hi >= c0 + 64));
+              if (partial) {
+                const unsigned span = (unsigned)max(c_hi - c_lo, 0);
+                const int off = c0 - c_lo;
 #pragma unroll
-              for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
-              tmem_st32(tO + ch * 32, o);
-            }
-            tmem_wait_st();
-          }
-          return f;
-        };
-        // P = 2^(s*scale - m) (masked -> 2^-inf = 0) of one half, packed bf16x2 into dst[0..31]
-        auto exp_half = [&](uint32_t* dst, int ncols, bool partial) {
-          const float m_use = (m == -INFINITY) ? 0.f : m;
-          const float2 negm2 = make_float2(-m_use, -m_use);
+                for (int c = 0; c < 64; ++c) r[c] = ((unsigned)(off + c) < span) ? r[c] : 0xFF800000u;
+              }
+              float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-          for (int cb = 0; cb < 64; cb += 32) {
-            if (cb < ncols) {
+              for (int c = 0; c < 64; c += 8) {     // 3-input max (FMNMX3): 2 columns per instruction
+                mx0 = fmax3f(mx0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+                mx1 = fmax3f(mx1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+                mx2 = fmax3f(mx2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
+                mx3 = fmax3f(mx3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
+              }
+              const float m_half = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+              // lazy rescale: move the running max only when it grew by > 2^8.  The TMEM load /
+              // store of O is warp-collective, so the O decision is taken per warp.  O_qt is
+              // quiescent: S_qt(g) was issued after PV_qt(g-1) and its commit covers both.
+              const bool upd = m_half > m + kRescaleThreshold;
+              const bool need_o = upd && (m != -INFINITY);
+              const float f = need_o ? ex2f(m - m_half) : 1.f;
+              if (upd) {
+                lsum2.x *= f; lsum2.y *= f;
+                l0.x *= f; l0.y *= f; l1.x *= f; l1.y *= f;
+                m = m_half;
+              }
+              if (__any_sync(0xffffffffu, need_o)) {
+#pragma unroll 1
+                for (int ch = 0; ch < 4; ++ch) {
+                  uint32_t o[32];
+                  tmem_ld32(tO + ch * 32, o);
+                  tmem_wait_ld();
 #pragma unroll
-              for (int c = cb; c < cb + 32; c += 4) {
+                  for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+                  tmem_st32(tO + ch * 32, o);
+                }
+                if (hf == 1) {   // half 0's P was exponentiated against the old max
+                  uint32_t o[32];
+                  tmem_ld32(tS, o);
+                  tmem_wait_ld();
+#pragma unroll
+                  for (int c = 0; c < 32; ++c) o[c] = pack_bf16(bf_lo(o[c]) * f, bf_hi(o[c]) * f);
+                  tmem_st32(tS, o);
+                }
+                tmem_wait_st();
+              }
+              // P = 2^(s*scale - m) (masked -> 2^-inf = 0) packed bf16x2 into r[0..31]
+              const float m_use = (m == -INFINITY) ? 0.f : m;
+              const float2 negm2 = make_float2(-m_use, -m_use);
+#pragma unroll
+              for (int c = 0; c < 64; c += 4) {
                 const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
                 const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
-                float2 p0, p1;
-                const bool poly = (c % 16) >= 16 - FA_POLY;
-                if (poly && !partial) {
-                  p0 = exp2_poly2(x0);
-                  p1 = exp2_poly2(x1);
-                } else {
-                  p0 = make_float2(ex2(x0.x), ex2(x0.y));
-                  p1 = make_float2(ex2(x1.x), ex2(x1.y));
-                }
+                const float2 p0 = make_float2(ex2f(x0.x), ex2f(x0.y));
+                const float2 p1 = make_float2(ex2f(x1.x), ex2f(x1.y));
                 l0 = __fadd2_rn(l0, p0);
                 l1 = __fadd2_rn(l1, p1);
-                dst[c >> 1] = pack_bf16(p0.x, p0.y);
-                dst[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
+                r[c >> 1] = pack_bf16(p0.x, p0.y);
+                r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
+              }
+              tmem_st32(tS + 32 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+              if (warp == 0 && lane == 0) FT(hf ? FT_SMX_EX1 : FT_SMX_EX0, g);
+            }
+            lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(barP);
+            if (rloc == 0) FT(qt ? FT_SM1_P : FT_SM0_P, g);
+          }
+          ++g;
+        }
+        if (jj == 0 && idx_e >= 0) {
+          // ---- epilogue of the previous item
+          const AttnParams& p = ITEM_PARAMS(idx_e);
+          const Item w = decode_item<BN>(p, ITEM_LOCAL(idx_e));
+          const int rglob = w.m0 + qt * 128 + rloc;
+          const bool valid_row = rglob < w.rows_total;
+          const int qi = valid_row ? rglob / p.grp : 0;
+          const float lsum = lsum_e, m = m_e;
+          fwait(bar(B_O + qt), (kk - 1) & 1, bar0);
+          if (rloc == 0) FT(qt ? FT_EPI1_O : FT_EPI0_O, kk - 1);
+          tc_fence_after();
+          if (FA_ABL_EPI) {
+            tc_fence_before();
+            mbar_arrive(bar(B_OF + qt));
+          } else {
+            const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+            const int h = valid_row ? w.g * p.grp + rglob % p.grp : 0;
+            const long long orow = ((long long)w.pp * p.n_q + qi) * p.Hq + h;
+#pragma unroll 1
+            for (int hf = 0; hf < 2; ++hf) {
+              tmem_ld32x(tO + 64 * hf, &r[0]);
+              tmem_ld32x(tO + 64 * hf + 32, &r[32]);
+              tmem_wait_ld();
+              if (hf == 1) {
+                tc_fence_before();
+                mbar_arrive(bar(B_OF + qt));      // O_qt may be overwritten by the next item's first PV
+              }
+              if (!valid_row) continue;
+              if (p.n_splits == 1 && p.split_only < 0) {
+                uint32_t q[8];
+                if (p.n_peers > 0) {
+                  // fused all-gather: the same row to every peer's gathered O (NVLink stores)
+                  const long long prow = ((long long)w.pp * p.n_q + qi) * p.o_hq + p.o_head_off + h;
+#pragma unroll
+                  for (int v = 0; v < 4; ++v) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                      q[j] = pack_bf16(__uint_as_float(r[16 * v + 2 * j]) * inv, __uint_as_float(r[16 * v + 2 * j + 1]) * inv);
+#pragma unroll 1
+                    for (int pr = 0; pr < p.n_peers; ++pr)
+                      stg256(reinterpret_cast<__nv_bfloat16*>(p.peer_o[pr]) + prow * 128 + 64 * hf + 16 * v, q);
+                  }
+                } else {
+                  // 32-byte stores (STG.256): each one fills a whole L2 sector of this thread's row
+                  __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) + orow * 128 + 64 * hf;
+#pragma unroll
+                  for (int v = 0; v < 4; ++v) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                      q[j] = pack_bf16(__uint_as_float(r[16 * v + 2 * j]) * inv, __uint_as_float(r[16 * v + 2 * j + 1]) * inv);
+                    stg256(dst + 16 * v, q);
+                  }
+                }
+              } else {
+                const long long rows = (long long)p.P * p.n_q * p.Hq;
+                const long long slot = p.split_only >= 0 ? 0 : w.sp;
+                float4* dst = reinterpret_cast<float4*>(p.ws_o + (slot * rows + orow) * 128 + 64 * hf);
+#pragma unroll
+                for (int v = 0; v < 16; ++v)
+                  dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv, __uint_as_float(r[4 * v + 1]) * inv,
+                                       __uint_as_float(r[4 * v + 2]) * inv, __uint_as_float(r[4 * v + 3]) * inv);
+                if (hf == 0) p.ws_lse[slot * rows + orow] = lsum > 0.f ? m + __log2f(lsum) : -INFINITY;
               }
             }
           }
-        };
-        bool partA, partB;
-        update_max(load_half(0, partA));
-        exp_half(pa, nu, partA);
-        if (nu > 64) {
-          const float f = update_max(load_half(64, partB));
-          if (f != 1.f) {   // half A was exponentiated against the old max (rare)
-#pragma unroll
-            for (int c = 0; c < 32; ++c) pa[c] = pack_bf16(bf_lo(pa[c]) * f, bf_hi(pa[c]) * f);
-          }
-          exp_half(r, nu - 64, partB);
-          tmem_st32(tS, pa);
-          tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-        } else {
-          tmem_st32(tS, pa);
-        }
-        lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(barP);
-      }
-      // ---- epilogue of the item: O / l once the last PV is done
-      const float lsum = lsum2.x + lsum2.y;
-      mbar_wait(bar(B_O + qt), kk & 1);
-      tc_fence_after();
-      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
-      const int h = valid_row ? w.g * p.grp + rglob % p.grp : 0;
-      const long long orow = ((long long)w.pp * p.n_q + qi) * p.Hq + h;
-#pragma unroll 1
-      for (int hf = 0; hf < 2; ++hf) {
-        tmem_ld32x(tO + 64 * hf, &r[0]);
-        tmem_ld32x(tO + 64 * hf + 32, &r[32]);
-        tmem_wait_ld();
-        if (hf == 1) {
-          tc_fence_before();
-          mbar_arrive(bar(B_OF + qt));      // O_qt may be overwritten by the next item's first PV
-        }
-        if (!valid_row) continue;
-        if (p.n_splits == 1 && p.split_only < 0) {
-          uint32_t q[8];
-          if (p.n_peers > 0) {
-            // fused all-gather: the same row to every peer's gathered O (NVLink stores)
-            const long long prow = ((long long)w.pp * p.n_q + qi) * p.o_hq + p.o_head_off + h;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                q[j] = pack_bf16(__uint_as_float(r[16 * v + 2 * j]) * inv, __uint_as_float(r[16 * v + 2 * j + 1]) * inv);
-#pragma unroll 1
-              for (int pr = 0; pr < p.n_peers; ++pr)
-                stg256(reinterpret_cast<__nv_bfloat16*>(p.peer_o[pr]) + prow * 128 + 64 * hf + 16 * v, q);
-            }
-          } else {
-            // 32-byte stores (STG.256): each one fills a whole L2 sector of this thread's row
-            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) + orow * 128 + 64 * hf;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                q[j] = pack_bf16(__uint_as_float(r[16 * v + 2 * j]) * inv, __uint_as_float(r[16 * v + 2 * j + 1]) * inv);
-              stg256(dst + 16 * v, q);
-            }
-          }
-        } else {
-          const long long rows = (long long)p.P * p.n_q * p.Hq;
-          const long long slot = p.split_only >= 0 ? 0 : w.sp;
-          float4* dst = reinterpret_cast<float4*>(p.ws_o + (slot * rows + orow) * 128 + 64 * hf);
-#pragma unroll
-          for (int v = 0; v < 16; ++v)
-            dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv, __uint_as_float(r[4 * v + 1]) * inv,
-                                 __uint_as_float(r[4 * v + 2]) * inv, __uint_as_float(r[4 * v + 3]) * inv);
-          if (hf == 0) p.ws_lse[slot * rows + orow] = lsum > 0.f ? m + __log2f(lsum) : -INFINITY;
+          if (rloc == 0) FT(qt ? FT_EPI1_END : FT_EPI0_END, kk - 1);
         }
       }
+      idx_e = real ? idx : -1;
+      m_e = m;
+      lsum_e = lsum2.x + lsum2.y;
     }
   } else if (warp < 12) {
     // ================================================================ rotation (K tiles) + Q prep
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegRotate));
+    if constexpr (kRegRotate > 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegRotate));
+    else if constexpr (kRegRotate < 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegRotate));
     const int lt = threadIdx.x - 256;
     const int c8 = lt & 7;             // frequencies 8*c8 .. 8*c8+7
     const int rg = lt >> 3;            // rows rg*8 .. rg*8+7 of a 128-row tile
@@ -446,63 +601,86 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Q tile use qu (= 2 * item + qt) of item qidx: buffer qu % 3, free once use qu - 3's
     // last QK^T has completed
     auto prep_q = [&](int qu, int qidx) {
-      if (qu >= NQB) mbar_wait(bar(B_QF + qu % NQB), ((qu - NQB) / NQB) & 1);
+      if (lt == 0) FT((qu & 1) ? FT_QO_START : FT_QE_START, qu >> 1);
       const AttnParams& pq = ITEM_PARAMS(qidx);
       const Item wq = decode_item<BN>(pq, ITEM_LOCAL(qidx));
-      issue_q_tile(pq, wq, qu & 1, lt, qbuf_addr(qu));
-      rotate_q_tile(pq, wq, qu & 1, lt, qbuf_addr(qu), 6);
+      uint4 lo[8], hi[8];
+      if (!FA_ABL_Q) load_rotate_q_regs(pq, wq, qu & 1, lt, lo, hi);
+      if (qu >= NQB) fwait(bar(B_QF + qu % NQB), ((qu - NQB) / NQB) & 1, bar0);
+      if (lt == 0 && (qu & 1)) FT(FT_QO_FREE, qu >> 1);
+      if (!FA_ABL_Q) {
+        const uint32_t qtile = qbuf_addr(qu);
+        const int c8 = lt & 7, rg8 = lt >> 3;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int r = rg8 * 8 + k;
+          const uint32_t a = qtile + r * 128 + ((c8 ^ (r & 7)) << 4);
+          sts128(a, lo[k]);
+          sts128(a + 16384, hi[k]);
+        }
+        fence_proxy_async();
+      }
       mbar_arrive(bar(B_QR + qu % NQB));
+      if (lt == 0) FT((qu & 1) ? FT_QO_END : FT_QE_END, qu >> 1);
     };
+    // Job order (one call site each for the Q prep and the K rotation, so each is inlined
+    // once): a virtual item -1 prepares item 0's Q tiles; item kk with rotated K tiles runs
+    // K(0), Q0(kk+1), K(1) .. K(n-1), Q1(kk+1); an item without (staged build) runs Q0(kk+1),
+    // Q1(kk+1).  Q0(kk+1)'s buffer is free early (item kk-1's Q1), Q1(kk+1)'s only after
+    // item kk's last S0: every K tile of item kk is rotated before that wait.
     int gt = 0;
-    uint32_t kf_ph = 0;   // phase bit per K stage of the rotated-tile barrier B_KF
-    for (int kk = 0; kk < n_my; ++kk) {
-      const int idx = item_at(kk);
-      const AttnParams& p = ITEM_PARAMS(idx);
-      const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
-      const int A = w.A;
+    for (int kk = -1; kk < n_my; ++kk) {
       const bool q_next = kk + 1 < n_my;
       const int nidx = q_next ? item_at(kk + 1) : 0;
+      const int idx = kk >= 0 ? item_at(kk) : nidx;
+      const AttnParams& p = ITEM_PARAMS(idx);
+      const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
+      const bool rot = kk >= 0 && !w.staged && w.n_tiles > 0;
+      const int nk = rot ? w.n_tiles : 0;
+      const int njobs = nk + 2;
+      const int A = w.A;
       const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
-      if (w.staged || w.n_tiles == 0) {
-        if (q_next) prep_q(2 * kk + 2, nidx);
-      } else {
-        for (int jj = 0; jj < w.n_tiles; ++jj) {
-          const int g = gt + jj, u = w.t_begin + jj, ks = g % KST;
-          const TileSeg t = tile_segments<BN>(p, w, u);
-          int kpos[8];
+#pragma unroll 1
+      for (int t = 0; t < njobs; ++t) {
+        const bool is_q = rot ? (t == 1 || t == njobs - 1) : true;
+        if (is_q) {
+          if (q_next) prep_q(2 * kk + 2 + (rot ? (t == 1 ? 0 : 1) : t), nidx);   // Q tile 0 / 1 of item kk+1
+          continue;
+        }
+        const int jj = t == 0 ? 0 : t - 1;
+        const int g = gt + jj, u = w.t_begin + jj, ks = g % KST;
+        const TileSeg tg = tile_segments<BN>(p, w, u);
+        int kpos[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) kpos[k] = seg_pos(t, rg * 8 + k);
-          int p0 = -1;
+        for (int k = 0; k < 8; ++k) kpos[k] = seg_pos(tg, rg * 8 + k);
+        int p0 = -1;
 #pragma unroll
-          for (int k = 7; k >= 0; --k)
-            if (kpos[k] >= 0) p0 = kpos[k];
-          float4 pre[4];
+        for (int k = 7; k >= 0; --k)
+          if (kpos[k] >= 0) p0 = kpos[k];
+        float4 pre[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) pre[j] = rp[(long long)max(p0, 0) * 32 + 4 * c8 + j];
-          mbar_wait(bar(B_KR + ks), (g / KST) & 1);
-          if (rg * 8 < t.width)   // rows >= width are never read by the MMA
-            rotate_rows<2, kKVHalf>(sbase + OFF_K + ks * kKVBytes, rg * 8, c8, rp, cth, sth, kpos, pre, max(p0, 0));
-          fence_proxy_async();
-          mbar_arrive(bar(B_KF + ks));
-          kf_ph ^= 1u << ks;
-          if (dbg && c8 == 0) {
+        for (int j = 0; j < 4; ++j) pre[j] = rp[(long long)max(p0, 0) * 32 + 4 * c8 + j];
+        fwait(bar(B_KR + ks), (g / KST) & 1, bar0);
+        if (lt == 0) FT(FT_ROT_KR, g);
+        if (rg * 8 < tg.width && !FA_ABL_ROT)   // rows >= width are never read by the MMA
+          rotate_rows<2, kKVHalf>(sbase + OFF_K + ks * kKVBytes, rg * 8, c8, rp, cth, sth, kpos, pre, max(p0, 0));
+        fence_proxy_async();
+        mbar_arrive(bar(B_KF + ks));
+        if (lt == 0) FT(FT_ROT_KF, g);
+        if (dbg && c8 == 0) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const int rr = rg * 8 + k;
-              const int x = BN * u + rr;
-              int slot = t.slot0 + rr;
-              if (slot >= p.R) slot -= p.R;
-              if (kpos[k] >= 0)
-                p.dbg_pos[(u < w.n_extra) ? (x < A ? x : p.dbg_A + p.dbg_R + (x - A)) : p.dbg_A + slot] = kpos[k];
-            }
+          for (int k = 0; k < 8; ++k) {
+            const int rr = rg * 8 + k;
+            const int x = BN * u + rr;
+            int slot = tg.slot0 + rr;
+            if (slot >= p.R) slot -= p.R;
+            if (kpos[k] >= 0)
+              p.dbg_pos[(u < w.n_extra) ? (x < A ? x : p.dbg_A + p.dbg_R + (x - A)) : p.dbg_A + slot] = kpos[k];
           }
-          if (jj == 0 && q_next) prep_q(2 * kk + 2, nidx);   // next item's Q tile 0 after the first K tile
         }
       }
-      if (q_next) prep_q(2 * kk + 3, nidx);   // Q tile 1: its buffer frees after this item's last S0
-      gt += w.n_tiles;
+      if (kk >= 0) gt += w.n_tiles;
     }
-    (void)kf_ph;
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCopy));
     if (warp == 12 || warp == 13) {
@@ -522,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int jj = 0; jj < w.n_tiles; ++jj) {
           const int g = gt + jj, u = w.t_begin + jj, st = g % nst;
-          if (g >= nst) mbar_wait(bar(b_free + st), ((g - nst) / nst) & 1);
+          if (g >= nst) fwait(bar(b_free + st), ((g - nst) / nst) & 1, bar0);
           const uint32_t dst = sbase + off + st * kKVBytes;
           const TileSeg t = tile_segments<BN>(p, w, u);
           if (u < w.n_extra) {
@@ -547,6 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // logical window tile: one 128-row box per 64-column block (ring mirror or staging rows)
             const CUtensorMap* tmap = isk ? &p.tmap_k : &p.tmap_v;
             const int row = (int)(w.head_row * w.Rp) + t.slot0;
+            FT(isk ? FT_CPK : FT_CPV, g);
             mbar_arrive_tx(bar(b_full + st), kKVBytes);
             tma_load_2d(dst, tmap, 0, row, bar(b_full + st));
             tma_load_2d(dst + kKVHalf, tmap, 64, row, bar(b_full + st));
@@ -565,6 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_qk(tmem + qt * 128, da, db, IQK0 | ((uint32_t)(nu >> 3) << 17));
       };
       auto issue_pv = [&](int qt, int vs, bool acc, int nu) {
+        if (FA_ABL_PV) return;
         const uint64_t dv = sdesc(sbase + OFF_V + vs * kKVBytes, kKVHalf, 1024);
         const uint32_t d = tmem + 256 + qt * 128, a = tmem + qt * 128;
         if (nu == BN) {
@@ -576,85 +756,125 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k8 = 1; k8 < nk; ++k8) mma_ts_w(d, a + k8 * 8, dv + (uint64_t)(k8 * 128), IPV, 1u);
         }
       };
+      // What the issue loop needs of an item (few registers: this warp runs with kRegCopy).
+      struct MI {
+        int n, t_begin, staged, n_extra, aps, cnt;
+      };
+      auto mi_of = [&](int kk) {
+        const int idx = item_at(kk);
+        const ItemGeo p = geo(pa, pb, ITEM_B(idx));
+        const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
+        MI m;
+        m.n = w.n_tiles; m.t_begin = w.t_begin; m.staged = w.staged; m.n_extra = w.n_extra;
+        m.aps = w.A + w.n_self; m.cnt = w.cnt;
+        return m;
+      };
+      // tile width (valid keys rounded up to 16) of tile jj of an item: tile_segments' rule
+      auto width_of = [&](const MI& m, int jj) {
+        const int u = m.t_begin + jj;
+        const int valid = u < m.n_extra ? min(max(m.aps - BN * u, 0), BN) : min(m.cnt - BN * (u - m.n_extra), BN);
+        return (valid + 15) & ~15;
+      };
       uint32_t kf_ph = 0;   // B_KF phase bit per K stage (only rotated tiles arrive there)
-      auto wait_k = [&](const Item& w, int g) {
+      auto wait_kmi = [&](const MI& m, int g) {
         const int ks = g % KST;
-        if (w.staged) {
-          mbar_wait(bar(B_KR + ks), (g / KST) & 1);
+        if (m.staged) {
+          fwait(bar(B_KR + ks), (g / KST) & 1, bar0);
         } else {
-          mbar_wait(bar(B_KF + ks), (kf_ph >> ks) & 1);
+          fwait(bar(B_KF + ks), (kf_ph >> ks) & 1, bar0);
           kf_ph ^= 1u << ks;
         }
         tc_fence_after();
       };
+      // Every item has n >= 1 tiles (the host splits never leave a split empty, a causal
+      // m-block always sees a key).  The issue order is one stream across items: the next
+      // item's S0(0) follows this item's last PV0, its S1(0) the last PV1, exactly as S(g+1)
+      // follows PV(g) inside an item, so an item switch costs the tensor core nothing but the
+      // O read-out of the epilogue (B_OF) before the next item's first PV.
       int gt = 0;
-      for (int kk = 0; kk < n_my; ++kk) {
-        const int idx = item_at(kk);
-        const ItemGeo p = geo(pa, pb, ITEM_B(idx));
-        const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
-        const int n = w.n_tiles;
-        const int qu0 = 2 * kk, qu1 = 2 * kk + 1;
-        if (n == 0) {   // keep every per-item phase: O ready (zeros), Q buffers released
-          for (int qt = 0; qt < 2; ++qt) {
-            if (kk > 0) mbar_wait(bar(B_OF + qt), (kk - 1) & 1);
-            mma_commit_w(bar(B_O + qt));
-          }
-          mbar_wait(bar(B_QR + qu0 % NQB), (qu0 / NQB) & 1);
-          mbar_wait(bar(B_QR + qu1 % NQB), (qu1 / NQB) & 1);
-          mma_commit_w(bar(B_QF + qu0 % NQB));
-          mma_commit_w(bar(B_QF + qu1 % NQB));
-          continue;
-        }
-        int nu = tile_segments<BN>(p, w, w.t_begin).width;
-        // prologue: S0(gt), S1(gt)
-        wait_k(w, gt);
-        mbar_wait(bar(B_QR + qu0 % NQB), (qu0 / NQB) & 1);
+      MI cur = {};
+      if (n_my > 0) {
+        cur = mi_of(0);
+        const int nu = width_of(cur, 0);
+        if (lane == 0) FT(FT_MMA_ITEM, 0);
+        wait_kmi(cur, 0);
+        fwait(bar(B_QR + 0), 0, bar0);
         tc_fence_after();
-        issue_qk(qu0, gt % KST, nu, 0);
+        issue_qk(0, 0, nu, 0);
         mma_commit_w(bar(B_S + 0));
-        if (n == 1) mma_commit_w(bar(B_QF + qu0 % NQB));
-        mbar_wait(bar(B_QR + qu1 % NQB), (qu1 / NQB) & 1);
+        if (cur.n == 1) mma_commit_w(bar(B_QF + 0));
+        fwait(bar(B_QR + 1), 0, bar0);
         tc_fence_after();
-        issue_qk(qu1, gt % KST, nu, 1);
+        issue_qk(1, 0, nu, 1);
         mma_commit_w(bar(B_S + 1));
-        mma_commit_w(bar(B_KE + gt % KST));
-        if (n == 1) mma_commit_w(bar(B_QF + qu1 % NQB));
+        mma_commit_w(bar(B_KE + 0));
+        if (cur.n == 1) mma_commit_w(bar(B_QF + 1));
+      }
+      for (int kk = 0; kk < n_my; ++kk) {
+        const int n = cur.n;
+        const bool has_next = kk + 1 < n_my;
+        const MI nxt = has_next ? mi_of(kk + 1) : cur;
+        int nu = width_of(cur, 0);
         for (int jj = 0; jj < n; ++jj) {
           const int g = gt + jj, vs = g % VST;
-          const bool more = jj + 1 < n;
-          const int nu2 = more ? tile_segments<BN>(p, w, w.t_begin + jj + 1).width : 0;
-          mbar_wait(bar(B_VR + vs), (g / VST) & 1);
-          // ---- Q tile 0: PV0(g), then S0(g+1) into the columns P0(g) occupied
-          mbar_wait(bar(B_P + 0), g & 1);
-          if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + 0), (kk - 1) & 1);   // previous item's O0 read out
+          const bool last = jj + 1 == n;
+          // the next S pair: tile jj+1 of this item, or tile 0 of the next item
+          const bool nx = !last || has_next;
+          const MI& wn = last ? nxt : cur;
+          const int qn = last ? 2 * (kk + 1) : 2 * kk;          // its Q tile uses (qn, qn + 1)
+          const int jn = last ? 0 : jj + 1;
+          const int nu2 = nx ? width_of(wn, jn) : 0;
+          const bool last_s = jn + 1 == wn.n;                    // that S pair is its item's last
+          fwait(bar(B_VR + vs), (g / VST) & 1, bar0);
+          if (lane == 0) FT(FT_MMA_V, g);
+          // ---- Q tile 0: PV0(g), then S0(next) into the columns P0(g) occupied
+          fwait(bar(B_P + 0), g & 1, bar0);
+          if (lane == 0) FT(FT_MMA_P0, g);
+          if (jj == 0 && kk > 0) fwait(bar(B_OF + 0), (kk - 1) & 1, bar0);   // previous item's O0 read out
+          if (lane == 0 && jj == 0) FT(FT_MMA_OF, kk);
           tc_fence_after();
           issue_pv(0, vs, jj > 0, nu);
-          if (!more) mma_commit_w(bar(B_O + 0));
-          if (more) {
-            wait_k(w, g + 1);
-            issue_qk(qu0, (g + 1) % KST, nu2, 0);
+          if (last) mma_commit_w(bar(B_O + 0));
+          if (nx) {
+            wait_kmi(wn, g + 1);
+            if (lane == 0) FT(FT_MMA_K, g + 1);
+            if (last) {
+              if (lane == 0) FT(FT_MMA_ITEM, kk + 1);
+              fwait(bar(B_QR + qn % NQB), (qn / NQB) & 1, bar0);
+              if (lane == 0) FT(FT_MMA_Q0, kk + 1);
+              tc_fence_after();
+            }
+            issue_qk(qn, (g + 1) % KST, nu2, 0);
             mma_commit_w(bar(B_S + 0));
-            if (jj + 2 == n) mma_commit_w(bar(B_QF + qu0 % NQB));   // the item's last S0 issued
+            if (last_s) mma_commit_w(bar(B_QF + qn % NQB));
           }
           // ---- Q tile 1
-          mbar_wait(bar(B_P + 1), g & 1);
-          if (jj == 0 && kk > 0) mbar_wait(bar(B_OF + 1), (kk - 1) & 1);
+          fwait(bar(B_P + 1), g & 1, bar0);
+          if (lane == 0) FT(FT_MMA_P1, g);
+          if (jj == 0 && kk > 0) fwait(bar(B_OF + 1), (kk - 1) & 1, bar0);
           tc_fence_after();
           issue_pv(1, vs, jj > 0, nu);
           mma_commit_w(bar(B_VE + vs));
-          if (!more) mma_commit_w(bar(B_O + 1));
-          if (more) {
-            issue_qk(qu1, (g + 1) % KST, nu2, 1);
+          if (last) mma_commit_w(bar(B_O + 1));
+          if (nx) {
+            if (last) {
+              fwait(bar(B_QR + (qn + 1) % NQB), ((qn + 1) / NQB) & 1, bar0);
+              if (lane == 0) FT(FT_MMA_Q1, kk + 1);
+              tc_fence_after();
+            }
+            issue_qk(qn + 1, (g + 1) % KST, nu2, 1);
             mma_commit_w(bar(B_S + 1));
             mma_commit_w(bar(B_KE + (g + 1) % KST));
-            if (jj + 2 == n) mma_commit_w(bar(B_QF + qu1 % NQB));
+            if (last_s) mma_commit_w(bar(B_QF + (qn + 1) % NQB));
           }
           nu = nu2;
         }
         gt += n;
+        cur = nxt;
       }
       // drain: the last V-free commit tracks every MMA of this CTA
-      if (gt > 0) mbar_wait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1);
+      if (gt > 0) fwait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1, bar0);
+      if (lane == 0) FT(FT_END, 0);
     }
   }
 
@@ -700,9 +920,36 @@ long long attn_fa_items(const AttnParams& p) {
 }
 long long attn_fa_item_tiles(const AttnParams& p, int local) { return tcc::decode_item<fa::BN>(p, local).n_tiles; }
 
+// DSC_WATCHDOG=1: pipeline waits that time out leave a record in host-mapped memory
+// (dscache_watchdog_read) before trapping
+static unsigned long long* g_wd_host = nullptr;
+cudaError_t fa_watchdog_setup() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  done = true;
+  const char* e = std::getenv("DSC_WATCHDOG");
+  if (!e || e[0] != '1') return cudaSuccess;
+  void* hp = nullptr;
+  cudaError_t r = cudaHostAlloc(&hp, 4096, cudaHostAllocMapped);
+  if (r != cudaSuccess) return r;
+  std::memset(hp, 0, 4096);
+  g_wd_host = static_cast<unsigned long long*>(hp);
+  void* dp = nullptr;
+  r = cudaHostGetDevicePointer(&dp, hp, 0);
+  if (r != cudaSuccess) return r;
+  return cudaMemcpyToSymbol(fa::g_fa_wd, &dp, sizeof(dp));
+}
+int fa_watchdog_read(unsigned long long* out, int n) {
+  if (!g_wd_host) return -1;
+  for (int i = 0; i < n && i < 512; ++i) out[i] = reinterpret_cast<volatile unsigned long long*>(g_wd_host)[i];
+  return 0;
+}
+
 cudaError_t launch_attn_fa(const AttnParams& pa, const AttnParams* pb, SchedCache* cache, cudaStream_t st) {
   int num_sms = 0;
   cudaError_t e = configure_device(&num_sms);
+  if (e != cudaSuccess) return e;
+  e = fa_watchdog_setup();
   if (e != cudaSuccess) return e;
   const long long na = attn_fa_items(pa), nb = pb ? attn_fa_items(*pb) : 0;
   const long long items = na + nb;

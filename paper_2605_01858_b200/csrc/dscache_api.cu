@@ -884,6 +884,11 @@ dscache_status dscache_profile_read(dscache_t h, double* ms_build, double* ms_at
   return DSCACHE_OK;
 }
 
+int32_t dscache_watchdog_read(uint64_t* out, int32_t n) {
+  if (!out || n < 1) return -1;
+  return dsc::fa_watchdog_read(reinterpret_cast<unsigned long long*>(out), n);
+}
+
 int32_t dscache_attn_impl(dscache_t h, int32_t which) {
   if (!h) return -1;
   return which == 0 ? h->impl_build : h->impl_attend;

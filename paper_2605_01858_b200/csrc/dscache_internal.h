@@ -123,6 +123,7 @@ const int* sched_lists(SchedCache* cache, const AttnParams& pa, const AttnParams
                        unsigned grid, long long (*item_tiles)(const AttnParams&, int), cudaStream_t st);
 cudaError_t launch_attn_fa(const AttnParams& pa, const AttnParams* pb, SchedCache* cache, cudaStream_t st);
 int attn_fa_smem_bytes();
+int fa_watchdog_read(unsigned long long* out, int n);   // debug record (DSC_WATCHDOG=1)
 constexpr int kTileNFa = 128;  // keys per tile of the v7 kernel
 // K/V tensor map: [rows][128] bf16, box 64 columns x box_rows rows, SW128
 cudaError_t make_kv_tmap(CUtensorMap* map, void* base, unsigned long long rows, int box_rows);

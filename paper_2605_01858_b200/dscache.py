@@ -55,7 +55,7 @@ class State(ctypes.Structure):
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
            "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
-           "dscache_attn_impl", "dscache_last_error", "dscache_attend_partial", "dscache_combine_partials",
+           "dscache_attn_impl", "dscache_watchdog_read", "dscache_last_error", "dscache_attend_partial", "dscache_combine_partials",
            "dscache_build_instant_boost", "dscache_attend_boost", "dscache_attend_peers",
            "dscache_ipc_handle", "dscache_ipc_open", "dscache_ipc_close"]
 
@@ -92,6 +92,7 @@ def load_library(path: str = LIB_PATH):
         "dscache_profile_read": ([P, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(I64),
                                   ctypes.POINTER(I64), ctypes.POINTER(I64), I32], I32),
         "dscache_attn_impl": ([P, I32], I32),
+        "dscache_watchdog_read": ([P, I32], I32),
         "dscache_attend_partial": ([P, I32, I32, P, P, P, I32, I32, I32, P, P, P], I32),
         "dscache_combine_partials": ([P, I32, I64, P, P, P, P], I32),
         "dscache_build_instant_boost": ([P, I32, I32, P, P, P, I32, P, P], I32),
@@ -455,9 +456,9 @@ class DSCache:
         _check(_lib.dscache_set_debug(self._h, _ptr(build_pos), _ptr(attend_pos), int(bool(poison))))
 
     def set_trace(self, buf: Optional[torch.Tensor], ntrace_cta: int = 1):
-        """buf: int64 CUDA tensor of ntrace_cta*32*64 entries (None = off)."""
-        if buf is not None and (buf.dtype != torch.int64 or buf.numel() < ntrace_cta * 40 * 64):
-            raise ValueError("trace buffer must be int64 with ntrace_cta*32*64 entries")
+        """buf: int64 CUDA tensor of ntrace_cta*32*1024 entries (v7 FA_TRACE layout; None = off)."""
+        if buf is not None and (buf.dtype != torch.int64 or buf.numel() < ntrace_cta * 32 * 1024):
+            raise ValueError("trace buffer must be int64 with ntrace_cta*32*1024 entries")
         self._trace = buf
         _check(_lib.dscache_set_trace(self._h, _ptr(buf), int(ntrace_cta)))
 
@@ -476,3 +477,14 @@ class DSCache:
         names = {IMPL_TC: "tcgen05", IMPL_SIMT: "simt"}
         return {"build_instant": names.get(_lib.dscache_attn_impl(self._h, 0)),
                 "attend": names.get(_lib.dscache_attn_impl(self._h, 1))}
+
+
+def watchdog_records():
+    """Debug: the tcgen05 kernel's watchdog records (DSC_WATCHDOG=1), as a list of
+    (cta, warp, barrier index, parity, clock); readable after a trapped kernel."""
+    buf = (ctypes.c_uint64 * 257)()
+    if _lib.dscache_watchdog_read(buf, 257) != 0:
+        return None
+    n = min(int(buf[0]), 64)
+    return [(int(buf[1 + 4 * i]), int(buf[2 + 4 * i]), int(buf[3 + 4 * i]) >> 32, int(buf[3 + 4 * i]) & 0xFFFFFFFF,
+             int(buf[4 + 4 * i])) for i in range(n)]

@@ -108,6 +108,15 @@ constexpr float kRescaleThreshold = 8.0f;    // log2 units: move the running max
 #ifndef FA_ABL_PV
 #define FA_ABL_PV 0
 #endif
+// FA_MMA2 1: two MMA-issuing warps, warp 14 for Q tile 0 and warp 15 for Q tile 1, so each
+// tile's PV -> S chain is issued as soon as its own P is in (stage-free barriers count 2)
+#ifndef FA_MMA2
+#define FA_MMA2 1
+#endif
+// FA_TURN 1: the softmax warpgroups take turns (named barriers 1, 2) instead of running at once
+#ifndef FA_TURN
+#define FA_TURN 0
+#endif
 // FA_TRACE 1 (profiling variant): clock64 of pipeline events into p.trace, layout
 // [ntrace_cta][kFtEvents][kFtIdx] for the first ntrace_cta CTAs; per-tile events are indexed
 // by the CTA's tile counter g, per-item events by the CTA's item counter
@@ -120,7 +129,8 @@ enum {
   FT_CPK, FT_CPV,                                                                // per tile
   FT_MMA_ITEM = 12, FT_MMA_Q0, FT_MMA_Q1, FT_EPI0_O, FT_EPI0_END, FT_QE_START, FT_QE_END, FT_QO_START, FT_QO_FREE,
   FT_QO_END, FT_MMA_OF, FT_EPI1_O, FT_EPI1_END, FT_END,                           // per item
-  FT_SMX_LD0 = 26, FT_SMX_EX0, FT_SMX_LD1, FT_SMX_EX1                               // per tile, warp 0 steps
+  FT_SMX_LD0 = 26, FT_SMX_EX0, FT_SMX_LD1, FT_SMX_EX1,                              // per tile, warp 0 steps
+  FT_MMA_PV0I = 30, FT_MMA_S0I                                                      // per tile, MMA issue done
 };
 #if FA_TRACE
 #define FT(ev, i)                                                                                      \
@@ -289,9 +299,24 @@ __device__ __forceinline__ void load_rotate_q_regs(const AttnParams& p, const It
   }
 }
 
-// The integer fields decode_item needs, selected per item from the two launch parameter
-// blocks (build / attend of a fused step) with constant-offset loads.
-__device__ __forceinline__ ItemGeo geo(const AttnParams& pa, const AttnParams& pb, bool isb) { return item_geo(pa, pb, isb); }
+// Item of a host-decoded record (sched.cu item_table): per-item fields from the record,
+// per-launch ones from its parameter block
+__device__ __forceinline__ Item item_of(const AttnParams& p, const ItemRec& r) {
+  Item w;
+  w.pp = r.pp; w.g = r.flags >> 8; w.sp = r.sp; w.mb = r.m0 >> 8;
+  w.head_row = r.head_row; w.m0 = r.m0; w.rows_total = p.n_q * p.grp; w.cnt = r.cnt;
+  w.n_extra = (p.A + p.n_self + BN - 1) / BN; w.t_begin = r.t_begin; w.n_tiles = r.n_tiles;
+  w.A = p.A; w.n_self = p.n_self; w.ring_count = p.ring_count; w.ring_start = p.ring_start; w.R = p.R;
+  w.Rp = p.Rp; w.staged = p.staged;
+  return w;
+}
+__device__ __forceinline__ ItemRec load_rec(const ItemRec* __restrict__ recs, int i) {
+  const int4 a = __ldg(reinterpret_cast<const int4*>(recs + i));
+  const int4 b = __ldg(reinterpret_cast<const int4*>(recs + i) + 1);
+  ItemRec r;
+  r.pp = a.x; r.head_row = a.y; r.m0 = a.z; r.t_begin = a.w; r.n_tiles = b.x; r.cnt = b.y; r.flags = b.z; r.sp = b.w;
+  return r;
+}
 
 // ------------------------------------------------------------------ kernel
 // Items [0, na) use pa, [na, na + nb) use pb (the fused step: attend items first, then the
@@ -312,9 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = na + nb;
-#define ITEM_B(I) ((I) >= na)
-#define ITEM_PARAMS(I) (ITEM_B(I) ? pb : pa)
-#define ITEM_LOCAL(I) (ITEM_B(I) ? (I) - na : (I))
+#define REC_PARAMS(R) (((R).flags & 1) ? pb : pa)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NQB; ++i) {
@@ -324,11 +347,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < KST; ++i) {
       mbar_init(bar(B_KR + i), 1);
       mbar_init(bar(B_KF + i), 128);
-      mbar_init(bar(B_KE + i), 1);
+      mbar_init(bar(B_KE + i), FA_MMA2 ? 2 : 1);   // one commit per MMA issuer
     }
     for (int i = 0; i < VST; ++i) {
       mbar_init(bar(B_VR + i), 1);
-      mbar_init(bar(B_VE + i), 1);
+      mbar_init(bar(B_VE + i), FA_MMA2 ? 2 : 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(B_S + i), 1);
@@ -359,13 +382,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // descriptors take the returned base (no assumption about its value)
   const uint32_t tmem = *tmem_slot;
 
-  // this CTA's items, in order: the launcher's list-scheduled work list, else the stride
-  // blockIdx.x, + gridDim.x, ...  Every role walks the same sequence.
-  const int* __restrict__ sched = pa.sched_items;
-  const int sj0 = sched ? pa.sched_off[blockIdx.x] : 0;
-  const int n_my = sched ? pa.sched_off[blockIdx.x + 1] - sj0
-                         : (n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0);
-  auto item_at = [&](int t) { return sched ? sched[sj0 + t] : (int)blockIdx.x + t * (int)gridDim.x; };
+  // this CTA's items, in order: host-decoded records (sched.cu item_table); every role walks
+  // the same sequence
+  const ItemRec* __restrict__ recs = pa.item_recs + pa.item_off[blockIdx.x];
+  const int n_my = pa.item_off[blockIdx.x + 1] - pa.item_off[blockIdx.x];
   // Q tile use u = 2 * item + qt lives in buffer u % 3
   auto qbuf_addr = [&](int u) { return sbase + OFF_Q + (uint32_t)((u % NQB) * kQBytes); };
 
@@ -390,9 +410,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m_e = 0.f, lsum_e = 0.f;
     for (int kk = 0; kk <= n_my; ++kk) {
       const bool real = kk < n_my;
-      const int idx = real ? item_at(kk) : 0;
-      const AttnParams& p = ITEM_PARAMS(idx);
-      const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
+      const ItemRec rec = load_rec(recs, real ? kk : 0);
+      const AttnParams& p = REC_PARAMS(rec);
+      const Item w = item_of(p, rec);
       const int A = w.A;
       const int n = real ? w.n_tiles : 0;
       const int rglob = w.m0 + qt * 128 + rloc;
@@ -421,6 +441,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           fwait(barS, g & 1, bar0);
           if (rloc == 0) FT(qt ? FT_SM1_S : FT_SM0_S, g);
+          // turn-taking (FA_TURN): the two warpgroups' softmaxes alternate instead of sharing
+          // the MUFU pipe; WG0 takes tile 0 without waiting
+          if (FA_TURN && !(qt == 0 && g == 0)) named_bar_sync(1 + qt, 256);
           if (warp_dead || FA_ABL_SOFTMAX) {   // all 32 rows are padding: their P / O are never used
             mbar_arrive(barP);
           } else {
@@ -509,12 +532,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(barP);
             if (rloc == 0) FT(qt ? FT_SM1_P : FT_SM0_P, g);
           }
+          // hand the turn over (WG1's very last tile has no successor turn to grant)
+          if (FA_TURN && !(qt == 1 && kk == n_my - 1 && jj == n - 1)) named_bar_arrive(2 - qt, 256);
           ++g;
         }
         if (jj == 0 && idx_e >= 0) {
           // ---- epilogue of the previous item
-          const AttnParams& p = ITEM_PARAMS(idx_e);
-          const Item w = decode_item<BN>(p, ITEM_LOCAL(idx_e));
+          const ItemRec rec = load_rec(recs, idx_e);
+          const AttnParams& p = REC_PARAMS(rec);
+          const Item w = item_of(p, rec);
           const int rglob = w.m0 + qt * 128 + rloc;
           const bool valid_row = rglob < w.rows_total;
           const int qi = valid_row ? rglob / p.grp : 0;
@@ -579,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (rloc == 0) FT(qt ? FT_EPI1_END : FT_EPI0_END, kk - 1);
         }
       }
-      idx_e = real ? idx : -1;
+      idx_e = real ? kk : -1;
       m_e = m;
       lsum_e = lsum2.x + lsum2.y;
     }
@@ -602,8 +628,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // last QK^T has completed
     auto prep_q = [&](int qu, int qidx) {
       if (lt == 0) FT((qu & 1) ? FT_QO_START : FT_QE_START, qu >> 1);
-      const AttnParams& pq = ITEM_PARAMS(qidx);
-      const Item wq = decode_item<BN>(pq, ITEM_LOCAL(qidx));
+      const ItemRec rq = load_rec(recs, qidx);
+      const AttnParams& pq = REC_PARAMS(rq);
+      const Item wq = item_of(pq, rq);
       uint4 lo[8], hi[8];
       if (!FA_ABL_Q) load_rotate_q_regs(pq, wq, qu & 1, lt, lo, hi);
       if (qu >= NQB) fwait(bar(B_QF + qu % NQB), ((qu - NQB) / NQB) & 1, bar0);
@@ -631,10 +658,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     int gt = 0;
     for (int kk = -1; kk < n_my; ++kk) {
       const bool q_next = kk + 1 < n_my;
-      const int nidx = q_next ? item_at(kk + 1) : 0;
-      const int idx = kk >= 0 ? item_at(kk) : nidx;
-      const AttnParams& p = ITEM_PARAMS(idx);
-      const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
+      const int nidx = q_next ? kk + 1 : 0;
+      const ItemRec rec = load_rec(recs, kk >= 0 ? kk : nidx);
+      const AttnParams& p = REC_PARAMS(rec);
+      const Item w = item_of(p, rec);
       const bool rot = kk >= 0 && !w.staged && w.n_tiles > 0;
       const int nk = rot ? w.n_tiles : 0;
       const int njobs = nk + 2;
@@ -691,9 +718,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int b_full = isk ? B_KR : B_VR, b_free = isk ? B_KE : B_VE;
       int gt = 0;
       for (int kk = 0; kk < n_my; ++kk) {
-        const int idx = item_at(kk);
-        const AttnParams& p = ITEM_PARAMS(idx);
-        const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
+        const ItemRec rec = load_rec(recs, kk);
+        const AttnParams& p = REC_PARAMS(rec);
+        const Item w = item_of(p, rec);
         const int A = p.A;
         const __nv_bfloat16* __restrict__ SX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.sink_k : p.sink_v);
         const __nv_bfloat16* __restrict__ XX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.self_k : p.self_v);
@@ -734,8 +761,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         gt += w.n_tiles;
       }
-    } else if (warp == 14) {
-      // ============================================================== MMA issuer
+    } else if (warp == 14 || (FA_MMA2 && warp == 15)) {
+      // ============================================================== MMA issuer(s)
       constexpr uint32_t IQK0 = idesc_bf16(128, 0, 0, 0);    // S = Q K^T, both K-major; N = tile width
       constexpr uint32_t IPV = idesc_bf16(128, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
       auto issue_qk = [&](int qu, int ks, int nu, int qt) {
@@ -761,12 +788,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         int n, t_begin, staged, n_extra, aps, cnt;
       };
       auto mi_of = [&](int kk) {
-        const int idx = item_at(kk);
-        const ItemGeo p = geo(pa, pb, ITEM_B(idx));
-        const Item w = decode_item<BN>(p, ITEM_LOCAL(idx));
+        const ItemRec r = load_rec(recs, kk);
+        const bool isb = r.flags & 1;
+        const int A = isb ? pb.A : pa.A, n_self = isb ? pb.n_self : pa.n_self;
         MI m;
-        m.n = w.n_tiles; m.t_begin = w.t_begin; m.staged = w.staged; m.n_extra = w.n_extra;
-        m.aps = w.A + w.n_self; m.cnt = w.cnt;
+        m.n = r.n_tiles; m.t_begin = r.t_begin; m.staged = isb ? pb.staged : pa.staged;
+        m.n_extra = (A + n_self + BN - 1) / BN; m.aps = A + n_self; m.cnt = r.cnt;
         return m;
       };
       // tile width (valid keys rounded up to 16) of tile jj of an item: tile_segments' rule
@@ -791,6 +818,67 @@ __global__ void __launch_bounds__(kThreads, 1)
       // item's S0(0) follows this item's last PV0, its S1(0) the last PV1, exactly as S(g+1)
       // follows PV(g) inside an item, so an item switch costs the tensor core nothing but the
       // O read-out of the epilogue (B_OF) before the next item's first PV.
+#if FA_MMA2
+      const int mq = warp - 14;   // the Q tile whose MMAs this warp issues
+      int gt = 0;
+      MI cur = {};
+      if (n_my > 0) {
+        cur = mi_of(0);
+        const int nu = width_of(cur, 0);
+        if (lane == 0 && mq == 0) FT(FT_MMA_ITEM, 0);
+        wait_kmi(cur, 0);
+        fwait(bar(B_QR + mq), 0, bar0);
+        tc_fence_after();
+        issue_qk(mq, 0, nu, mq);
+        mma_commit_w(bar(B_S + mq));
+        mma_commit_w(bar(B_KE + 0));
+        if (cur.n == 1) mma_commit_w(bar(B_QF + mq));
+      }
+      for (int kk = 0; kk < n_my; ++kk) {
+        const int n = cur.n;
+        const bool has_next = kk + 1 < n_my;
+        const MI nxt = has_next ? mi_of(kk + 1) : cur;
+        int nu = width_of(cur, 0);
+        for (int jj = 0; jj < n; ++jj) {
+          const int g = gt + jj, vs = g % VST;
+          const bool last = jj + 1 == n;
+          const bool nx = !last || has_next;
+          const MI& wn = last ? nxt : cur;
+          const int qn = (last ? 2 * (kk + 1) : 2 * kk) + mq;   // Q tile use of the next S
+          const int jn = last ? 0 : jj + 1;
+          const int nu2 = nx ? width_of(wn, jn) : 0;
+          const bool last_s = jn + 1 == wn.n;
+          fwait(bar(B_VR + vs), (g / VST) & 1, bar0);
+          fwait(bar(B_P + mq), g & 1, bar0);
+          if (lane == 0) FT(mq ? FT_MMA_P1 : FT_MMA_P0, g);
+          if (jj == 0 && kk > 0) fwait(bar(B_OF + mq), (kk - 1) & 1, bar0);   // previous item's O read out
+          if (lane == 0 && jj == 0 && mq == 0) FT(FT_MMA_OF, kk);
+          tc_fence_after();
+          issue_pv(mq, vs, jj > 0, nu);
+          if (lane == 0 && mq == 0) FT(FT_MMA_PV0I, g);
+          mma_commit_w(bar(B_VE + vs));
+          if (last) mma_commit_w(bar(B_O + mq));
+          if (nx) {
+            wait_kmi(wn, g + 1);
+            if (lane == 0 && mq == 0) FT(FT_MMA_K, g + 1);
+            if (last) {
+              if (lane == 0 && mq == 0) FT(FT_MMA_ITEM, kk + 1);
+              fwait(bar(B_QR + qn % NQB), (qn / NQB) & 1, bar0);
+              if (lane == 0) FT(mq ? FT_MMA_Q1 : FT_MMA_Q0, kk + 1);
+              tc_fence_after();
+            }
+            issue_qk(qn, (g + 1) % KST, nu2, mq);
+            if (lane == 0 && mq == 0) FT(FT_MMA_S0I, g + 1);
+            mma_commit_w(bar(B_S + mq));
+            mma_commit_w(bar(B_KE + (g + 1) % KST));
+            if (last_s) mma_commit_w(bar(B_QF + qn % NQB));
+          }
+          nu = nu2;
+        }
+        gt += n;
+        cur = nxt;
+      }
+#else
       int gt = 0;
       MI cur = {};
       if (n_my > 0) {
@@ -834,6 +922,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0 && jj == 0) FT(FT_MMA_OF, kk);
           tc_fence_after();
           issue_pv(0, vs, jj > 0, nu);
+          if (lane == 0) FT(FT_MMA_PV0I, g);
           if (last) mma_commit_w(bar(B_O + 0));
           if (nx) {
             wait_kmi(wn, g + 1);
@@ -845,6 +934,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_fence_after();
             }
             issue_qk(qn, (g + 1) % KST, nu2, 0);
+            if (lane == 0) FT(FT_MMA_S0I, g + 1);
             mma_commit_w(bar(B_S + 0));
             if (last_s) mma_commit_w(bar(B_QF + qn % NQB));
           }
@@ -872,6 +962,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         gt += n;
         cur = nxt;
       }
+#endif
       // drain: the last V-free commit tracks every MMA of this CTA
       if (gt > 0) fwait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1, bar0);
       if (lane == 0) FT(FT_END, 0);
@@ -884,9 +975,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 14) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
-#undef ITEM_B
-#undef ITEM_PARAMS
-#undef ITEM_LOCAL
+#undef REC_PARAMS
 }
 
 }  // namespace fa
@@ -918,7 +1007,14 @@ cudaError_t configure_device(int* num_sms) {
 long long attn_fa_items(const AttnParams& p) {
   return (long long)p.P * p.Hkv * p.n_mblocks * (p.split_only >= 0 ? 1 : p.n_splits);
 }
-long long attn_fa_item_tiles(const AttnParams& p, int local) { return tcc::decode_item<fa::BN>(p, local).n_tiles; }
+// the host decode of one work item (the kernel reads these records instead of decoding)
+ItemRec attn_fa_decode(const AttnParams& p, int local, int isb) {
+  const tcc::Item w = tcc::decode_item<fa::BN>(p, local);
+  ItemRec r;
+  r.pp = w.pp; r.head_row = (int)w.head_row; r.m0 = w.m0; r.t_begin = w.t_begin; r.n_tiles = w.n_tiles;
+  r.cnt = w.cnt; r.flags = isb | (w.g << 8); r.sp = w.sp;
+  return r;
+}
 
 // DSC_WATCHDOG=1: pipeline waits that time out leave a record in host-mapped memory
 // (dscache_watchdog_read) before trapping
@@ -957,10 +1053,10 @@ cudaError_t launch_attn_fa(const AttnParams& pa, const AttnParams* pb, SchedCach
   const unsigned grid = (unsigned)(items < num_sms ? items : num_sms);
   AttnParams qa = pa;
   qa.sched_off = qa.sched_items = nullptr;
-  if (cache && items > grid) {
-    const int* lists = sched_lists(cache, pa, pb, na, nb, grid, &attn_fa_item_tiles, st);
-    if (lists) { qa.sched_off = lists; qa.sched_items = lists + grid + 1; }
-  }
+  const int* off = nullptr;
+  qa.item_recs = item_table(cache, pa, pb, na, nb, grid, &attn_fa_decode, &off, st);
+  qa.item_off = off;
+  if (!qa.item_recs) return cudaErrorMemoryAllocation;
   fa::attn_fa_kernel<<<grid, fa::kThreads, fa::kSmemBytes, st>>>(qa, pb ? *pb : qa, (int)na, (int)nb);
   return cudaGetLastError();
 }

@@ -20,6 +20,13 @@ constexpr int kMaxPeers = 8;  // fused all-gather epilogue: destinations of ever
 //   [A+ring_count, +n_self) self rows            (position L)
 // Query row i (i < n_q) of q head h sits at position q_pos0 + i and sees key L iff
 // L <= q_pos0 + i.  Ids are contiguous from 0.
+// A work item of the v7 kernel decoded on the host (sched.cu): what every role needs of it,
+// so the kernel's roles do no index arithmetic per item.  flags: bit 0 = item of the second
+// launch block (pb), bits 8.. = kv head g.
+struct ItemRec {
+  int pp, head_row, m0, t_begin, n_tiles, cnt, flags, sp;
+};
+
 struct AttnParams {
   // problems
   int P, S, layer_count, layer_begin, N_total;
@@ -65,6 +72,9 @@ struct AttnParams {
   // the items sched_items[sched_off[b] .. sched_off[b+1]) in order; null = static stride
   const int* sched_off;
   const int* sched_items;
+  // v7 kernel: CTA b runs the host-decoded items item_recs[item_off[b] .. item_off[b+1])
+  const int* item_off;
+  const ItemRec* item_recs;
   // staged build (tcgen05 path): the keys are rows [0, ring_count) of the per-step staging
   // buffers [S*N*Hkv][Rp][d] holding sink ++ instant window with K ALREADY rotated at ids
   // 0..ring_count-1 (stage_instant_kernel); A = 0, ring_start = 0, no K rotation in-kernel
@@ -121,6 +131,11 @@ void sched_cache_free(SchedCache* c);
 // device work lists [grid + 1 offsets | items] for this launch shape, or nullptr (static stride)
 const int* sched_lists(SchedCache* cache, const AttnParams& pa, const AttnParams* pb, long long na, long long nb,
                        unsigned grid, long long (*item_tiles)(const AttnParams&, int), cudaStream_t st);
+// v7: per-CTA lists of host-decoded items (list-scheduled where that beats the stride by > 2%);
+// *off = device [grid + 1] offsets, return = device records; nullptr on failure
+using ItemDecoder = ItemRec (*)(const AttnParams& p, int local, int isb);
+const ItemRec* item_table(SchedCache* cache, const AttnParams& pa, const AttnParams* pb, long long na, long long nb,
+                          unsigned grid, ItemDecoder dec, const int** off, cudaStream_t st);
 cudaError_t launch_attn_fa(const AttnParams& pa, const AttnParams* pb, SchedCache* cache, cudaStream_t st);
 int attn_fa_smem_bytes();
 int fa_watchdog_read(unsigned long long* out, int n);   // debug record (DSC_WATCHDOG=1)

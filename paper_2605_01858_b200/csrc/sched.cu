@@ -15,6 +15,7 @@
 #include "dscache_internal.h"
 
 #include <algorithm>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -29,6 +30,7 @@ struct SchedCache {
     cudaStream_t stream = nullptr;
   };
   std::map<std::vector<long long>, Entry> entries;
+  std::map<std::vector<long long>, Entry> tables;   // v7 item tables: [grid + 1 offsets | pad | ItemRec[]]
   std::mutex mu;
   size_t bytes = 0;
 };
@@ -37,10 +39,11 @@ SchedCache* sched_cache_new() { return new SchedCache(); }
 
 void sched_cache_free(SchedCache* c) {
   if (!c) return;
-  for (auto& kv : c->entries) {
-    if (kv.second.ready) cudaEventDestroy(kv.second.ready);
-    if (kv.second.dev) cudaFree(kv.second.dev);
-  }
+  for (auto* m : {&c->entries, &c->tables})
+    for (auto& kv : *m) {
+      if (kv.second.ready) cudaEventDestroy(kv.second.ready);
+      if (kv.second.dev) cudaFree(kv.second.dev);
+    }
   delete c;
 }
 
@@ -119,6 +122,94 @@ const int* sched_lists(SchedCache* cache, const AttnParams& pa, const AttnParams
   }
   cache->entries.emplace(std::move(key), e);
   return e.dev;
+}
+
+namespace {
+std::vector<long long> shape_key(int device, const AttnParams& pa, const AttnParams* pb, long long na, long long nb,
+                                 unsigned grid) {
+  std::vector<long long> key = {device, na, nb, (long long)grid};
+  for (const AttnParams* p : {&pa, pb}) {
+    if (!p) continue;
+    for (long long v : {(long long)p->n_splits, (long long)p->split_only, (long long)p->P, (long long)p->Hkv,
+                        (long long)p->n_mblocks, (long long)p->n_q, (long long)p->grp, (long long)p->q_pos0,
+                        (long long)p->A, (long long)p->ring_count, (long long)p->n_self,
+                        (long long)p->tiles_per_split, (long long)p->layer_count, (long long)p->layer_begin,
+                        (long long)p->N_total, (long long)p->Rp, (long long)p->staged})
+      key.push_back(v);
+  }
+  return key;
+}
+}  // namespace
+
+const ItemRec* item_table(SchedCache* cache, const AttnParams& pa, const AttnParams* pb, long long na, long long nb,
+                          unsigned grid, ItemDecoder dec, const int** off_out, cudaStream_t st) {
+  if (!cache) return nullptr;
+  std::lock_guard<std::mutex> lock(cache->mu);
+  int device = 0;
+  cudaGetDevice(&device);
+  std::vector<long long> key = shape_key(device, pa, pb, na, nb, grid);
+  const size_t off_bytes = ((grid + 1) * sizeof(int) + 31) & ~size_t(31);
+  auto it = cache->tables.find(key);
+  if (it != cache->tables.end()) {
+    const SchedCache::Entry& e = it->second;
+    if (!e.dev) return nullptr;
+    if (e.stream != st && e.ready) cudaStreamWaitEvent(st, e.ready, 0);
+    *off_out = e.dev;
+    return reinterpret_cast<const ItemRec*>(reinterpret_cast<const char*>(e.dev) + off_bytes);
+  }
+  const long long items = na + nb;
+  std::vector<ItemRec> rec(items);
+  for (long long I = 0; I < items; ++I) {
+    const bool isb = I >= na;
+    rec[I] = dec(isb ? *pb : pa, (int)(isb ? I - na : I), isb ? 1 : 0);
+  }
+  // list scheduling vs the static stride (cost = key tiles + the item-switch cost)
+  std::vector<int> owner(items);
+  std::vector<long long> stride_load(grid, 0);
+  std::vector<std::pair<long long, int>> heap;
+  heap.reserve(grid);
+  for (unsigned b = 0; b < grid; ++b) heap.push_back({0, (int)b});
+  auto cmp = [](const std::pair<long long, int>& x, const std::pair<long long, int>& y) { return x > y; };
+  std::make_heap(heap.begin(), heap.end(), cmp);
+  for (long long I = 0; I < items; ++I) {
+    const long long cost = rec[I].n_tiles + kSwitchCost;
+    stride_load[I % grid] += cost;
+    std::pop_heap(heap.begin(), heap.end(), cmp);
+    owner[I] = heap.back().second;
+    heap.back().first += cost;
+    std::push_heap(heap.begin(), heap.end(), cmp);
+  }
+  long long list_max = 0;
+  for (auto& h : heap) list_max = std::max(list_max, h.first);
+  const long long stride_max = *std::max_element(stride_load.begin(), stride_load.end());
+  if (!(list_max * 50 < stride_max * 49))
+    for (long long I = 0; I < items; ++I) owner[I] = (int)(I % grid);
+  std::vector<int> off(grid + 1, 0);
+  for (long long I = 0; I < items; ++I) ++off[owner[I] + 1];
+  for (unsigned b = 0; b < grid; ++b) off[b + 1] += off[b];
+  std::vector<char> host(off_bytes + items * sizeof(ItemRec), 0);
+  std::memcpy(host.data(), off.data(), (grid + 1) * sizeof(int));
+  ItemRec* dst = reinterpret_cast<ItemRec*>(host.data() + off_bytes);
+  std::vector<int> fill(off.begin(), off.end() - 1);
+  for (long long I = 0; I < items; ++I) dst[fill[owner[I]]++] = rec[I];   // increasing I per CTA
+  SchedCache::Entry e;
+  if (cache->bytes + host.size() > kMaxCacheBytes) return nullptr;
+  if (cudaMalloc(&e.dev, host.size()) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (cudaMemcpyAsync(e.dev, host.data(), host.size(), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e.ready, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(e.ready, st) != cudaSuccess) {
+    cudaGetLastError();
+    if (e.ready) cudaEventDestroy(e.ready);
+    cudaFree(e.dev);
+    return nullptr;
+  }
+  e.stream = st;
+  cache->bytes += host.size();
+  cache->tables.emplace(std::move(key), e);
+  *off_out = e.dev;
+  return reinterpret_cast<const ItemRec*>(reinterpret_cast<const char*>(e.dev) + off_bytes);
 }
 
 // 2-D tensor map of a K/V row buffer [rows][128] bf16 (ring + mirror rows, or a staging

@@ -22,7 +22,7 @@ NE, NI = 32, 1024
 EV = {"MMA_P0": 0, "MMA_P1": 1, "MMA_K": 2, "MMA_V": 3, "SM0_S": 4, "SM0_P": 5, "SM1_S": 6, "SM1_P": 7,
       "ROT_KR": 8, "ROT_KF": 9, "CPK": 10, "CPV": 11, "MMA_ITEM": 12, "MMA_Q0": 13, "MMA_Q1": 14, "EPI0_O": 15,
       "EPI0_END": 16, "QE_START": 17, "QE_END": 18, "QO_START": 19, "QO_FREE": 20, "QO_END": 21, "MMA_OF": 22,
-      "EPI1_O": 23, "EPI1_END": 24, "END": 25, "SMX_LD0": 26, "SMX_EX0": 27, "SMX_LD1": 28, "SMX_EX1": 29}
+      "EPI1_O": 23, "EPI1_END": 24, "END": 25, "SMX_LD0": 26, "SMX_EX0": 27, "SMX_LD1": 28, "SMX_EX1": 29, "MMA_PV0I": 30, "MMA_S0I": 31}
 
 
 def main():
@@ -86,6 +86,9 @@ def main():
             q0, q1, of = rel("MMA_Q0", i), rel("MMA_Q1", i), rel("MMA_OF", i)
             print(f" item {i:3d}: start {st:8d}  Q0 +{(q0 or st) - st:5d} Q1 +{(q1 or st) - st:5d} OF +{(of or st) - st:5d}"
                   f"  tiles {len(tiles):3d}  dur {((nx or st) - st):7d}  per tile {((nx or st) - st) / max(len(tiles), 1):7.0f}")
+            print(f"    epi0 of prev: O-ready {rel('EPI0_O', i - 1) if i else None} end {rel('EPI0_END', i - 1) if i else None}"
+                  f"  epi1: O-ready {rel('EPI1_O', i - 1) if i else None} end {rel('EPI1_END', i - 1) if i else None}"
+                  f"  Q0 prep {rel('QE_START', i)}..{rel('QE_END', i)}  Q1 prep {rel('QO_START', i)} free {rel('QO_FREE', i)} end {rel('QO_END', i)}")
             for g_ in tiles[:args.tiles]:
                 s0, p0_, s1, p1 = rel("SM0_S", g_), rel("SM0_P", g_), rel("SM1_S", g_), rel("SM1_P", g_)
                 print(f"    g {g_:4d}: S0 {s0} P0 {p0_} (sm {p0_ - s0 if s0 and p0_ else '-'})  S1 {s1} P1 {p1} "
@@ -102,6 +105,14 @@ def main():
             if all(x is not None for x in ev):
                 for (k_, a_, b_) in zip(parts, ev, ev[1:]):
                     parts[k_].append(b_ - a_)
+        mparts = {"P0->PV0issued": [], "PV0issued->Kready": [], "Kready->S0issued": [], "S0issued->S0done": []}
+        for g_ in range(ntile - 1):
+            ev = [rel("MMA_P0", g_), rel("MMA_PV0I", g_), rel("MMA_K", g_ + 1), rel("MMA_S0I", g_ + 1), rel("SM0_S", g_ + 1)]
+            if all(x is not None for x in ev):
+                for (k_, a_, b_) in zip(mparts, ev, ev[1:]):
+                    mparts[k_].append(b_ - a_)
+        if mparts["P0->PV0issued"]:
+            print(" MMA warp steps (median clk): " + ", ".join(f"{k_} {sorted(v)[len(v) // 2]}" for k_, v in mparts.items()))
         if parts["S->ld0"]:
             print(" softmax0 warp0 steps (median clk): " + ", ".join(
                 f"{k_} {sorted(v)[len(v) // 2]}" for k_, v in parts.items()))

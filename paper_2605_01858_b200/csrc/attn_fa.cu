@@ -77,8 +77,11 @@ constexpr int B_S = B_VE + VST;         // [2] S_qt ready (commit)
 constexpr int B_P = B_S + 2;            // [2] P_qt ready (128 arrivals)
 constexpr int B_O = B_P + 2;            // [2] O_qt final for the item (commit after its last PV)
 constexpr int B_OF = B_O + 2;           // [2] O_qt read out by the epilogue (128 arrivals)
-constexpr int B_N = B_OF + 2;
-constexpr int kSmemBytes = OFF_BAR + B_N * 8 + 16 + 1024;   // + tmem slot + alignment slack
+constexpr int B_LR = B_OF + 2;          // 1/l of an item's 256 rows written (256 softmax arrivals)
+constexpr int B_LF = B_LR + 1;          // ... and read by the epilogue warpgroup (128 arrivals)
+constexpr int B_N = B_LF + 1;
+constexpr int OFF_L = OFF_BAR + B_N * 8 + 16;                  // 1/l handoff [256] fp32
+constexpr int kSmemBytes = OFF_L + 256 * 4 + 1024;             // + alignment slack
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 // setmaxnreg budget: 2 softmax warpgroups + rotation + (copy, MMA) <= 512 per thread x 128
 #ifndef FA_REG_SM
@@ -334,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bar0 = sbase + OFF_BAR;
   auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + B_N * 8);
+  float* lbuf = reinterpret_cast<float*>(smem + OFF_L);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = na + nb;
@@ -358,6 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(B_P + i), 128);
       mbar_init(bar(B_O + i), 1);
       mbar_init(bar(B_OF + i), 128);
+    }
+    {
+      mbar_init(bar(B_LR), 256);
+      mbar_init(bar(B_LF), 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
@@ -406,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the O read-out (B_OF).  O_qt(k) is final by then: PV_qt(last of k) was issued before
     // S_qt(first of k+1).  One call site: kk = n_my is a virtual item without tiles.
     int g = 0;
+    int ne = 0;                   // items whose O the rotation warpgroup writes out (B_LR / B_LF phases)
     int idx_e = -1;               // item whose epilogue is pending
     float m_e = 0.f, lsum_e = 0.f;
     for (int kk = 0; kk <= n_my; ++kk) {
@@ -565,32 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_arrive(bar(B_OF + qt));      // O_qt may be overwritten by the next item's first PV
               }
               if (!valid_row) continue;
-              if (p.n_splits == 1 && p.split_only < 0) {
-                uint32_t q[8];
-                if (p.n_peers > 0) {
-                  // fused all-gather: the same row to every peer's gathered O (NVLink stores)
-                  const long long prow = ((long long)w.pp * p.n_q + qi) * p.o_hq + p.o_head_off + h;
-#pragma unroll
-                  for (int v = 0; v < 4; ++v) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                      q[j] = pack_bf16(__uint_as_float(r[16 * v + 2 * j]) * inv, __uint_as_float(r[16 * v + 2 * j + 1]) * inv);
-#pragma unroll 1
-                    for (int pr = 0; pr < p.n_peers; ++pr)
-                      stg256(reinterpret_cast<__nv_bfloat16*>(p.peer_o[pr]) + prow * 128 + 64 * hf + 16 * v, q);
-                  }
-                } else {
-                  // 32-byte stores (STG.256): each one fills a whole L2 sector of this thread's row
-                  __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) + orow * 128 + 64 * hf;
-#pragma unroll
-                  for (int v = 0; v < 4; ++v) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                      q[j] = pack_bf16(__uint_as_float(r[16 * v + 2 * j]) * inv, __uint_as_float(r[16 * v + 2 * j + 1]) * inv);
-                    stg256(dst + 16 * v, q);
-                  }
-                }
-              } else {
+              {   // split-KV / context-parallel partial: fp32 O / l and log2-sum-exp per split
                 const long long rows = (long long)p.P * p.n_q * p.Hq;
                 const long long slot = p.split_only >= 0 ? 0 : w.sp;
                 float4* dst = reinterpret_cast<float4*>(p.ws_o + (slot * rows + orow) * 128 + 64 * hf);
@@ -605,7 +589,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (rloc == 0) FT(qt ? FT_EPI1_END : FT_EPI0_END, kk - 1);
         }
       }
-      idx_e = real ? kk : -1;
+      // plain / peer-store launches: the rotation warpgroup writes O out (rot_epilogue), this
+      // warpgroup only hands over 1/l and goes straight to the next item
+      const bool roe = real && p.n_splits == 1 && p.split_only < 0;
+      if (roe) {
+        const float ls = lsum2.x + lsum2.y;
+        if (ne > 0) fwait(bar(B_LF), (ne - 1) & 1, bar0);
+        lbuf[qt * 128 + rloc] = ls > 0.f ? 1.f / ls : 0.f;
+        mbar_arrive(bar(B_LR));
+        ++ne;
+      }
+      idx_e = real && !roe ? kk : -1;
       m_e = m;
       lsum_e = lsum2.x + lsum2.y;
     }
@@ -649,6 +643,59 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_arrive(bar(B_QR + qu % NQB));
       if (lt == 0) FT((qu & 1) ? FT_QO_END : FT_QE_END, qu >> 1);
+    };
+    // Epilogue of item kk for plain / peer-store launches: O / l -> bf16 rows.  Runs here, not
+    // on the softmax warpgroups, so their next item starts at once; thread lt owns row lt of
+    // both Q tiles (warp 8 + lt/32 reads TMEM lane quarter lt/32).
+    int ne = 0;
+    auto rot_epilogue = [&](int kk) {
+      const ItemRec rec = load_rec(recs, kk);
+      const AttnParams& p = REC_PARAMS(rec);
+      const Item w = item_of(p, rec);
+      fwait(bar(B_LR), ne & 1, bar0);
+      const float inv0 = lbuf[lt], inv1 = lbuf[128 + lt];
+      mbar_arrive(bar(B_LF));
+      ++ne;
+      const uint32_t lane_off = (uint32_t)((lt >> 5) * 32) << 16;
+#pragma unroll 1
+      for (int qt = 0; qt < 2; ++qt) {
+        fwait(bar(B_O + qt), kk & 1, bar0);
+        if (lt == 0) FT(qt ? FT_EPI1_O : FT_EPI0_O, kk);
+        tc_fence_after();
+        const int rglob = w.m0 + qt * 128 + lt;
+        const bool valid_row = rglob < w.rows_total;
+        const int qi = valid_row ? rglob / p.grp : 0;
+        const int h = valid_row ? w.g * p.grp + rglob % p.grp : 0;
+        const float inv = qt ? inv1 : inv0;
+        const uint32_t tO = tmem + lane_off + (uint32_t)(256 + qt * 128);
+        uint32_t r[64];
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+          tmem_ld32x(tO + 64 * hf, &r[0]);
+          tmem_ld32x(tO + 64 * hf + 32, &r[32]);
+          tmem_wait_ld();
+          if (hf == 1) {
+            tc_fence_before();
+            mbar_arrive(bar(B_OF + qt));   // O_qt may be overwritten by the next item's first PV
+          }
+          if (!valid_row || FA_ABL_EPI) continue;
+          uint32_t q[8];
+          const bool peers = p.n_peers > 0;
+          const long long row = peers ? ((long long)w.pp * p.n_q + qi) * p.o_hq + p.o_head_off + h
+                                      : ((long long)w.pp * p.n_q + qi) * p.Hq + h;
+          const int nd = peers ? p.n_peers : 1;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              q[j] = pack_bf16(__uint_as_float(r[16 * v + 2 * j]) * inv, __uint_as_float(r[16 * v + 2 * j + 1]) * inv);
+#pragma unroll 1
+            for (int d = 0; d < nd; ++d)
+              stg256(reinterpret_cast<__nv_bfloat16*>(peers ? p.peer_o[d] : p.o) + row * 128 + 64 * hf + 16 * v, q);
+          }
+        }
+        if (lt == 0) FT(qt ? FT_EPI1_END : FT_EPI0_END, kk);
+      }
     };
     // Job order (one call site each for the Q prep and the K rotation, so each is inlined
     // once): a virtual item -1 prepares item 0's Q tiles; item kk with rotated K tiles runs
@@ -706,6 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (kk >= 0 && p.n_splits == 1 && p.split_only < 0) rot_epilogue(kk);
       if (kk >= 0) gt += w.n_tiles;
     }
   } else {

@@ -293,9 +293,10 @@ dscache_status dscache_copy_sink(dscache_t h, int32_t stream_idx, int32_t layer,
                                  void* k_host, void* v_host);
 
 /* Debug exports (K7).  build_pos / attend_pos: NULL = off, else DEVICE int32
- * buffers of dscache_debug_len(h) entries which the attention kernels fill, for
- * (stream 0, first layer of the call, kv head 0), with the position ids they
- * actually applied: [0,A) sink keys, [A,A+R) ring slot -> id (untouched if the
+ * buffers of num_streams * num_layers * dscache_debug_len(h) entries, one block of
+ * dscache_debug_len(h) per (stream, layer) ([S][N][len], int32), which the attention and
+ * staging kernels fill, for kv head 0 of every (stream, layer) of a call (fused
+ * dscache_step and staged builds included), with the position ids they actually applied: [0,A) sink keys, [A,A+R) ring slot -> id (untouched if the
  * slot is not in the window), [A+R, A+R+M) self keys, [A+R+M, A+R+2M) queries,
  * M = max(C, q_max).  poison != 0: after each append the slots of the frame just
  * evicted are overwritten with a large finite sentinel (finite, not NaN). */

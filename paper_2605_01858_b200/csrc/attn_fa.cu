@@ -47,7 +47,7 @@ namespace dsc {
 namespace fa {
 using namespace tcc;
 
-constexpr int BN = 128;                       // keys per K/V tile
+constexpr int BN = kTileN;                    // keys per K/V tile (128)
 constexpr int kWarps = 16;
 constexpr int kThreads = kWarps * 32;
 constexpr int kQBytes = 128 * 128 * 2;        // one 128-row Q tile (2 x 64-column SW128 blocks)
@@ -110,15 +110,6 @@ constexpr float kRescaleThreshold = 8.0f;    // log2 units: move the running max
 #endif
 #ifndef FA_ABL_PV
 #define FA_ABL_PV 0
-#endif
-// FA_MMA2 1: two MMA-issuing warps, warp 14 for Q tile 0 and warp 15 for Q tile 1, so each
-// tile's PV -> S chain is issued as soon as its own P is in (stage-free barriers count 2)
-#ifndef FA_MMA2
-#define FA_MMA2 1
-#endif
-// FA_TURN 1: the softmax warpgroups take turns (named barriers 1, 2) instead of running at once
-#ifndef FA_TURN
-#define FA_TURN 0
 #endif
 // FA_TRACE 1 (profiling variant): clock64 of pipeline events into p.trace, layout
 // [ntrace_cta][kFtEvents][kFtIdx] for the first ntrace_cta CTAs; per-tile events are indexed
@@ -236,7 +227,9 @@ __device__ __forceinline__ void load_rotate_q_regs(const AttnParams& p, const It
   const __nv_bfloat16* __restrict__ Qg = reinterpret_cast<const __nv_bfloat16*>(p.q);
   const int c8 = lt & 7, rg8 = lt >> 3;
   const int row0 = w.m0 + qt * 128 + rg8 * 8;
-  const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0 && c8 == 0;
+  // debug export (set_debug): every problem, kv head 0, block [head_row / Hkv] of the buffer
+  const bool dbg = p.dbg_pos != nullptr && w.g == 0 && c8 == 0;
+  int* const dbgp = dbg ? p.dbg_pos + (w.head_row / p.Hkv) * p.dbg_len : nullptr;
   const __nv_bfloat16* qbase = Qg + ((long long)w.pp * p.n_q) * p.Hq * 128 + (long long)w.g * p.grp * 128 + 8 * c8;
   int pos[8];
   {
@@ -245,7 +238,7 @@ __device__ __forceinline__ void load_rotate_q_regs(const AttnParams& p, const It
     for (int k = 0; k < 8; ++k) {   // all 16 loads in flight before any use
       const bool ok = row0 + k < w.rows_total;
       pos[k] = ok ? p.q_pos0 + i : -1;
-      if (dbg && hh == 0 && ok) p.dbg_pos[p.dbg_A + p.dbg_R + p.dbg_M + i] = pos[k];
+      if (dbg && hh == 0 && ok) dbgp[p.dbg_A + p.dbg_R + p.dbg_M + i] = pos[k];
       if (ok) {
         const __nv_bfloat16* src = qbase + ((long long)i * p.Hq + hh) * 128;
         lo[k] = ldg128(src);
@@ -351,11 +344,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < KST; ++i) {
       mbar_init(bar(B_KR + i), 1);
       mbar_init(bar(B_KF + i), 128);
-      mbar_init(bar(B_KE + i), FA_MMA2 ? 2 : 1);   // one commit per MMA issuer
+      mbar_init(bar(B_KE + i), 2);   // one commit per MMA issuer
     }
     for (int i = 0; i < VST; ++i) {
       mbar_init(bar(B_VR + i), 1);
-      mbar_init(bar(B_VE + i), FA_MMA2 ? 2 : 1);
+      mbar_init(bar(B_VE + i), 2);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(B_S + i), 1);
@@ -450,9 +443,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           fwait(barS, g & 1, bar0);
           if (rloc == 0) FT(qt ? FT_SM1_S : FT_SM0_S, g);
-          // turn-taking (FA_TURN): the two warpgroups' softmaxes alternate instead of sharing
-          // the MUFU pipe; WG0 takes tile 0 without waiting
-          if (FA_TURN && !(qt == 0 && g == 0)) named_bar_sync(1 + qt, 256);
           if (warp_dead || FA_ABL_SOFTMAX) {   // all 32 rows are padding: their P / O are never used
             mbar_arrive(barP);
           } else {
@@ -541,8 +531,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(barP);
             if (rloc == 0) FT(qt ? FT_SM1_P : FT_SM0_P, g);
           }
-          // hand the turn over (WG1's very last tile has no successor turn to grant)
-          if (FA_TURN && !(qt == 1 && kk == n_my - 1 && jj == n - 1)) named_bar_arrive(2 - qt, 256);
           ++g;
         }
         if (jj == 0 && idx_e >= 0) {
@@ -713,7 +701,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nk = rot ? w.n_tiles : 0;
       const int njobs = nk + 2;
       const int A = w.A;
-      const bool dbg = p.dbg_pos != nullptr && w.pp == 0 && w.g == 0;
+      const bool dbg = p.dbg_pos != nullptr && w.g == 0;   // every problem, kv head 0
+      int* const dbgp = dbg ? p.dbg_pos + (w.head_row / p.Hkv) * p.dbg_len : nullptr;
 #pragma unroll 1
       for (int t = 0; t < njobs; ++t) {
         const bool is_q = rot ? (t == 1 || t == njobs - 1) : true;
@@ -749,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int slot = tg.slot0 + rr;
             if (slot >= p.R) slot -= p.R;
             if (kpos[k] >= 0)
-              p.dbg_pos[(u < w.n_extra) ? (x < A ? x : p.dbg_A + p.dbg_R + (x - A)) : p.dbg_A + slot] = kpos[k];
+              dbgp[(u < w.n_extra) ? (x < A ? x : p.dbg_A + p.dbg_R + (x - A)) : p.dbg_A + slot] = kpos[k];
           }
         }
       }
@@ -809,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         gt += w.n_tiles;
       }
-    } else if (warp == 14 || (FA_MMA2 && warp == 15)) {
+    } else if (warp == 14 || warp == 15) {
       // ============================================================== MMA issuer(s)
       constexpr uint32_t IQK0 = idesc_bf16(128, 0, 0, 0);    // S = Q K^T, both K-major; N = tile width
       constexpr uint32_t IPV = idesc_bf16(128, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
@@ -866,7 +855,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       // item's S0(0) follows this item's last PV0, its S1(0) the last PV1, exactly as S(g+1)
       // follows PV(g) inside an item, so an item switch costs the tensor core nothing but the
       // O read-out of the epilogue (B_OF) before the next item's first PV.
-#if FA_MMA2
       const int mq = warp - 14;   // the Q tile whose MMAs this warp issues
       int gt = 0;
       MI cur = {};
@@ -926,91 +914,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         gt += n;
         cur = nxt;
       }
-#else
-      int gt = 0;
-      MI cur = {};
-      if (n_my > 0) {
-        cur = mi_of(0);
-        const int nu = width_of(cur, 0);
-        if (lane == 0) FT(FT_MMA_ITEM, 0);
-        wait_kmi(cur, 0);
-        fwait(bar(B_QR + 0), 0, bar0);
-        tc_fence_after();
-        issue_qk(0, 0, nu, 0);
-        mma_commit_w(bar(B_S + 0));
-        if (cur.n == 1) mma_commit_w(bar(B_QF + 0));
-        fwait(bar(B_QR + 1), 0, bar0);
-        tc_fence_after();
-        issue_qk(1, 0, nu, 1);
-        mma_commit_w(bar(B_S + 1));
-        mma_commit_w(bar(B_KE + 0));
-        if (cur.n == 1) mma_commit_w(bar(B_QF + 1));
-      }
-      for (int kk = 0; kk < n_my; ++kk) {
-        const int n = cur.n;
-        const bool has_next = kk + 1 < n_my;
-        const MI nxt = has_next ? mi_of(kk + 1) : cur;
-        int nu = width_of(cur, 0);
-        for (int jj = 0; jj < n; ++jj) {
-          const int g = gt + jj, vs = g % VST;
-          const bool last = jj + 1 == n;
-          // the next S pair: tile jj+1 of this item, or tile 0 of the next item
-          const bool nx = !last || has_next;
-          const MI& wn = last ? nxt : cur;
-          const int qn = last ? 2 * (kk + 1) : 2 * kk;          // its Q tile uses (qn, qn + 1)
-          const int jn = last ? 0 : jj + 1;
-          const int nu2 = nx ? width_of(wn, jn) : 0;
-          const bool last_s = jn + 1 == wn.n;                    // that S pair is its item's last
-          fwait(bar(B_VR + vs), (g / VST) & 1, bar0);
-          if (lane == 0) FT(FT_MMA_V, g);
-          // ---- Q tile 0: PV0(g), then S0(next) into the columns P0(g) occupied
-          fwait(bar(B_P + 0), g & 1, bar0);
-          if (lane == 0) FT(FT_MMA_P0, g);
-          if (jj == 0 && kk > 0) fwait(bar(B_OF + 0), (kk - 1) & 1, bar0);   // previous item's O0 read out
-          if (lane == 0 && jj == 0) FT(FT_MMA_OF, kk);
-          tc_fence_after();
-          issue_pv(0, vs, jj > 0, nu);
-          if (lane == 0) FT(FT_MMA_PV0I, g);
-          if (last) mma_commit_w(bar(B_O + 0));
-          if (nx) {
-            wait_kmi(wn, g + 1);
-            if (lane == 0) FT(FT_MMA_K, g + 1);
-            if (last) {
-              if (lane == 0) FT(FT_MMA_ITEM, kk + 1);
-              fwait(bar(B_QR + qn % NQB), (qn / NQB) & 1, bar0);
-              if (lane == 0) FT(FT_MMA_Q0, kk + 1);
-              tc_fence_after();
-            }
-            issue_qk(qn, (g + 1) % KST, nu2, 0);
-            if (lane == 0) FT(FT_MMA_S0I, g + 1);
-            mma_commit_w(bar(B_S + 0));
-            if (last_s) mma_commit_w(bar(B_QF + qn % NQB));
-          }
-          // ---- Q tile 1
-          fwait(bar(B_P + 1), g & 1, bar0);
-          if (lane == 0) FT(FT_MMA_P1, g);
-          if (jj == 0 && kk > 0) fwait(bar(B_OF + 1), (kk - 1) & 1, bar0);
-          tc_fence_after();
-          issue_pv(1, vs, jj > 0, nu);
-          mma_commit_w(bar(B_VE + vs));
-          if (last) mma_commit_w(bar(B_O + 1));
-          if (nx) {
-            if (last) {
-              fwait(bar(B_QR + (qn + 1) % NQB), ((qn + 1) / NQB) & 1, bar0);
-              if (lane == 0) FT(FT_MMA_Q1, kk + 1);
-              tc_fence_after();
-            }
-            issue_qk(qn + 1, (g + 1) % KST, nu2, 1);
-            mma_commit_w(bar(B_S + 1));
-            mma_commit_w(bar(B_KE + (g + 1) % KST));
-            if (last_s) mma_commit_w(bar(B_QF + (qn + 1) % NQB));
-          }
-          nu = nu2;
-        }
-        gt += n;
-        cur = nxt;
-      }
-#endif
       // drain: the last V-free commit tracks every MMA of this CTA
       if (gt > 0) fwait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1, bar0);
       if (lane == 0) FT(FT_END, 0);
@@ -1100,7 +1003,6 @@ cudaError_t launch_attn_fa(const AttnParams& pa, const AttnParams* pb, SchedCach
   if (items == 0) return cudaSuccess;
   const unsigned grid = (unsigned)(items < num_sms ? items : num_sms);
   AttnParams qa = pa;
-  qa.sched_off = qa.sched_items = nullptr;
   const int* off = nullptr;
   qa.item_recs = item_table(cache, pa, pb, na, nb, grid, &attn_fa_decode, &off, st);
   qa.item_off = off;

@@ -96,10 +96,7 @@ struct dscache_s {
   int ntrace = 0;
   int impl_build = DSCACHE_IMPL_SIMT, impl_attend = DSCACHE_IMPL_SIMT;
   int num_sms = 148;
-  // tcgen05 kernel: v7 (attn_fa.cu, 128-key tiles) or v5 (attn_tc.cu, 64-key tiles);
-  // DSC_KERNEL=tc selects v5 at create
-  int tile_n = dsc::kTileNFa;
-  dsc::SchedCache* sched = nullptr;   // v7 per-CTA work lists, owned by the handle
+  dsc::SchedCache* sched = nullptr;   // per-CTA item tables of the tcgen05 kernel, owned by the handle
   CUtensorMap tmap_k{}, tmap_v{};
   // staged build (tcgen05): per-step copy of sink ++ instant window, K pre-rotated
   void* stage_k = nullptr;
@@ -166,6 +163,7 @@ void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
   p.dtype = c.dtype;
   p.dbg_M = std::max(h->C, c.max_query_tokens);
   p.dbg_A = c.sink_tokens; p.dbg_R = h->R;
+  p.dbg_len = c.sink_tokens + h->R + 2 * p.dbg_M;
   p.tmap_k = h->tmap_k; p.tmap_v = h->tmap_v;
   p.staged = 0;
   p.trace = h->trace; p.ntrace_cta = h->ntrace;
@@ -184,10 +182,9 @@ dscache_status grow_ws(dscache_t h, size_t bytes) {
   return DSCACHE_OK;
 }
 
-// the tcgen05 attention launch of this handle's kernel version (pb: the build items of a fused step)
+// the tcgen05 attention launch (pb: the build items of a fused step)
 cudaError_t launch_tc(dscache_t h, const dsc::AttnParams& pa, const dsc::AttnParams* pb, cudaStream_t st) {
-  if (h->tile_n == dsc::kTileNFa) return dsc::launch_attn_fa(pa, pb, h->sched, st);
-  return pb ? dsc::launch_attn_tc2(pa, pb, st) : dsc::launch_attn_tc(pa, st);
+  return dsc::launch_attn_fa(pa, pb, h->sched, st);
 }
 
 dscache_status run_attention(dscache_t h, dsc::AttnParams& p, int impl, int kind, cudaStream_t st) {
@@ -255,10 +252,6 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   h->sink_filled.assign(c.num_layers, c.sink_tokens == 0 ? 1 : 0);
   h->last_evicted.assign(c.num_layers, -1);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, c.device);
-  {
-    const char* kern = std::getenv("DSC_KERNEL");
-    h->tile_n = (kern && std::strcmp(kern, "tc") == 0) ? dsc::kTileN : dsc::kTileNFa;
-  }
   h->sched = dsc::sched_cache_new();
   if (c.attn_impl == DSCACHE_IMPL_SIMT) {
     h->impl_build = h->impl_attend = DSCACHE_IMPL_SIMT;
@@ -288,8 +281,8 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   if (e == cudaSuccess) e = dsc::launch_rope_table(h->rope, h->npos, c.head_dim, c.rope_theta, 0);
   if (e == cudaSuccess && (h->impl_build == DSCACHE_IMPL_TC || h->impl_attend == DSCACHE_IMPL_TC)) {
     const unsigned long long rows = (unsigned long long)heads * h->Rp;
-    e = dsc::make_kv_tmap(&h->tmap_k, h->ring_k, rows, h->tile_n);
-    if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_v, h->ring_v, rows, h->tile_n);
+    e = dsc::make_kv_tmap(&h->tmap_k, h->ring_k, rows, dsc::kTileN);
+    if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_v, h->ring_v, rows, dsc::kTileN);
   }
   if (e == cudaSuccess && h->impl_build == DSCACHE_IMPL_TC && h->C > 0) {
     h->stage_rows = c.sink_tokens + h->C;
@@ -297,8 +290,8 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
     if (cudaMalloc(&h->stage_k, sb) != cudaSuccess || cudaMalloc(&h->stage_v, sb) != cudaSuccess) return oom("staging");
     e = cudaMemset(h->stage_k, 0, sb);
     if (e == cudaSuccess) e = cudaMemset(h->stage_v, 0, sb);
-    if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_sk, h->stage_k, (unsigned long long)heads * h->stage_rows, h->tile_n);
-    if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_sv, h->stage_v, (unsigned long long)heads * h->stage_rows, h->tile_n);
+    if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_sk, h->stage_k, (unsigned long long)heads * h->stage_rows, dsc::kTileN);
+    if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_sv, h->stage_v, (unsigned long long)heads * h->stage_rows, dsc::kTileN);
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -390,13 +383,14 @@ dscache_status prep_build(dscache_t h, int32_t lb, int32_t lc, const void* q_ins
   // Small launches (fewer build items than two waves of SMs, e.g. one stream x one layer)
   // are latency-bound: the extra staging launch costs more than the RoPE it saves there.
   const long long build_items = (long long)p.P * p.Hkv * p.n_mblocks;
-  if (h->impl_build == DSCACHE_IMPL_TC && h->stage_k && !h->dbg_build && build_items >= DSC_STAGE_MIN * h->num_sms) {
+  if (h->impl_build == DSCACHE_IMPL_TC && h->stage_k && build_items >= DSC_STAGE_MIN * h->num_sms) {
     dsc::StageParams sp{};
     sp.sink_k = h->sink_k; sp.sink_v = h->sink_v; sp.ring_k = h->ring_k; sp.ring_v = h->ring_v;
     sp.stage_k = h->stage_k; sp.stage_v = h->stage_v; sp.rope_pairs = p.rope_pairs;
     sp.S = p.S; sp.layer_count = lc; sp.layer_begin = lb; sp.N_total = p.N_total; sp.Hkv = p.Hkv;
     sp.A = p.A; sp.R = h->R; sp.Rp_ring = h->Rp; sp.inst_start = sc.inst_start;
     sp.rows = p.A + sc.C_t; sp.rows_stage = h->stage_rows;
+    sp.dbg_pos = h->dbg_build; sp.dbg_len = p.dbg_len;   // the staging kernel applies the build key ids
     *stage = sp;
     p.staged = 1;
     p.A = 0; p.ring_start = 0; p.ring_count = sp.rows; p.R = h->stage_rows; p.Rp = h->stage_rows;
@@ -473,7 +467,7 @@ dscache_status prep_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, c
   if (impl == DSCACHE_IMPL_TC) {
     // split the key range when (problem, kv head, m-block) work items cannot fill the SMs
     // sink/self tiles + logical window tiles (see tc_common.cuh tile_segments)
-    const int BN = h->tile_n;
+    const int BN = dsc::kTileN;
     const int tiles = std::max(1, (p.A + n_self + BN - 1) / BN + (p.ring_count + BN - 1) / BN);
     const int items = p.P * p.Hkv * p.n_mblocks;
     int splits = 1;
@@ -558,8 +552,8 @@ dscache_status dscache_build_instant_boost(dscache_t h, int32_t lb, int32_t lc, 
         cudaGetLastError();
         return fail(DSCACHE_E_OOM, "boost staging allocation failed");
       }
-      DSC_CUDA(dsc::make_kv_tmap(&h->tmap_bk, h->bstage_k, (unsigned long long)heads * rows, h->tile_n));
-      DSC_CUDA(dsc::make_kv_tmap(&h->tmap_bv, h->bstage_v, (unsigned long long)heads * rows, h->tile_n));
+      DSC_CUDA(dsc::make_kv_tmap(&h->tmap_bk, h->bstage_k, (unsigned long long)heads * rows, dsc::kTileN));
+      DSC_CUDA(dsc::make_kv_tmap(&h->tmap_bv, h->bstage_v, (unsigned long long)heads * rows, dsc::kTileN));
       h->bstage_rows = rows;
     }
     dsc::StageParams sp{};
@@ -632,7 +626,7 @@ dscache_status dscache_attend_partial(dscache_t h, int32_t lb, int32_t lc, const
   if (s != DSCACHE_OK) return s;
   // the key tiles of every item (sink/self tiles, then logical window tiles), cut into n_parts
   // contiguous ranges; part `part` is computed here
-  const int BN = h->tile_n;
+  const int BN = dsc::kTileN;
   const int tiles = (p.A + n_q + BN - 1) / BN + (p.ring_count + BN - 1) / BN;
   const int tps = (tiles + n_parts - 1) / n_parts;
   if ((long long)(n_parts - 1) * tps >= tiles)
@@ -740,8 +734,7 @@ dscache_status dscache_step(dscache_t h, int32_t lb, int32_t lc, const void* k_f
     DSC_CUDA(dsc::launch_stage_instant(sp, st));
     h->launches++;
   }
-  const bool debug = h->dbg_build || h->dbg_attend;
-  if (empty || debug || h->impl_build != DSCACHE_IMPL_TC || h->impl_attend != DSCACHE_IMPL_TC) {
+  if (empty || h->impl_build != DSCACHE_IMPL_TC || h->impl_attend != DSCACHE_IMPL_TC) {
     if (!empty) {
       s = run_attention(h, pb, h->impl_build, 0, st);
       if (s != DSCACHE_OK) return s;
@@ -839,7 +832,7 @@ dscache_status dscache_copy_sink(dscache_t h, int32_t s_idx, int32_t layer, void
 
 int32_t dscache_debug_len(dscache_t h) {
   if (!h) return 0;
-  return h->cfg.sink_tokens + h->R + 2 * std::max(h->C, h->cfg.max_query_tokens);
+  return h->cfg.sink_tokens + h->R + 2 * std::max(h->C, h->cfg.max_query_tokens);   // per problem
 }
 
 dscache_status dscache_set_debug(dscache_t h, int32_t* build_pos, int32_t* attend_pos, int32_t poison) {

@@ -7,10 +7,9 @@
 
 namespace dsc {
 
-constexpr int kTileN = 64;    // keys per attention tile (tcgen05 N of QK^T, K of PV)
+constexpr int kTileN = 128;   // keys per K/V tile of the tcgen05 kernel (N of QK^T, K of PV)
 constexpr int kTileM = 128;   // query rows per Q tile (tcgen05 M)
 constexpr int kMirror = 128;  // ring rows after slot R-1 mirroring slots [0, 128): a 128-row tile never wraps
-constexpr int kTraceEvents = 40, kTraceTiles = 64;
 constexpr int kMaxPeers = 8;  // fused all-gather epilogue: destinations of every O row
 
 // One attention launch (build_instant or attend) over P = S * layer_count problems.
@@ -55,12 +54,13 @@ struct AttnParams {
   float* ws_o;                               // [n_splits][P][n_q][Hq][d]
   float* ws_lse;                             // [n_splits][P][n_q][Hq]
   // tcgen05 kernel work decomposition
-  int n_mblocks;                             // ceil(n_q * grp / (2 * kTileM))
+  int n_mblocks;                             // ceil(n_q * grp / (2 * kTileM)): 256-row m-blocks
   // debug export (K7); null = off.  Layout [dbg_A sink ids | dbg_R ring-slot ids | dbg_M self ids |
   // query ids], indexed with the RING geometry (dbg_A, dbg_R) even when the launch reads a
   // staging buffer (staged build: A = 0, R = staging rows)
   int* dbg_pos; int dbg_M; int dbg_A, dbg_R;
-  // per-CTA event timeline (profiling); null = off.  [ntrace_cta][kTraceEvents][kTraceTiles] clock64
+  int dbg_len;                               // entries per problem: the buffer is [S][N][dbg_len], kv head 0
+  // per-CTA event timeline (FA_TRACE profiling builds); null = off.  [ntrace_cta][32][1024] clock64
   long long* trace; int ntrace_cta;
   int dtype;                                 // 0 bf16, 1 fp32
   // fused all-gather epilogue (P2 over peer memory): n_peers > 0 stores O row
@@ -68,18 +68,15 @@ struct AttnParams {
   // of to o; peer_o are device pointers mapped in this process (local, P2P or CUDA IPC)
   void* peer_o[kMaxPeers];
   int n_peers, o_hq, o_head_off;
-  // per-CTA work lists of the tcgen05 kernel (set by its launcher, DSC_SCHED): CTA b runs
-  // the items sched_items[sched_off[b] .. sched_off[b+1]) in order; null = static stride
-  const int* sched_off;
-  const int* sched_items;
-  // v7 kernel: CTA b runs the host-decoded items item_recs[item_off[b] .. item_off[b+1])
+  // CTA b of the tcgen05 kernel runs the host-decoded items item_recs[item_off[b] .. item_off[b+1])
+  // in order (set by its launcher from the handle's item-table cache)
   const int* item_off;
   const ItemRec* item_recs;
   // staged build (tcgen05 path): the keys are rows [0, ring_count) of the per-step staging
   // buffers [S*N*Hkv][Rp][d] holding sink ++ instant window with K ALREADY rotated at ids
   // 0..ring_count-1 (stage_instant_kernel); A = 0, ring_start = 0, no K rotation in-kernel
   int staged;
-  // TMA descriptors of the K / V rings viewed as [S*N*Hkv*R rows][128] bf16, box 64 x 128, SW128
+  // TMA descriptors of the K / V rings viewed as [S*N*Hkv*Rp rows][128] bf16, box 64 x kTileN, SW128
   CUtensorMap tmap_k;
   CUtensorMap tmap_v;
 };
@@ -109,6 +106,8 @@ struct StageParams {
   // frame boost_k/v [S][layer_count][rows - A - n_older][Hkv][d] instead of the ring; null = off
   const void* boost_k; const void* boost_v;
   int n_older;
+  // debug export (set_debug): the build key ids applied, [S][N][dbg_len] at [A + slot] / [row]
+  int* dbg_pos; int dbg_len;
 };
 
 // kernels (launchers return cudaGetLastError())
@@ -116,22 +115,17 @@ cudaError_t launch_stage_instant(const StageParams& p, cudaStream_t st);
 cudaError_t launch_rope_table(float2* table, int npos, int d, double theta, cudaStream_t st);
 cudaError_t launch_append(const AppendParams& p, cudaStream_t st);
 cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t st);
-cudaError_t launch_attn_tc(const AttnParams& p, cudaStream_t st);
-// one persistent launch over the items of pa (first) and then those of *pb (same handle)
-cudaError_t launch_attn_tc2(const AttnParams& pa, const AttnParams* pb, cudaStream_t st);
 cudaError_t launch_combine(const AttnParams& p, cudaStream_t st);
 // O (bf16 [rows][d]) = merge of n fp32 partials o_parts [n][rows][d] with log2-sum-exps lse [n][rows]
 cudaError_t launch_combine_partials(int n, long long rows, int d, const float* o_parts, const float* lse, void* o,
                                     cudaStream_t st);
-int attn_tc_smem_bytes();
-// v7 kernel (attn_fa.cu): 128-key tiles, Q-tile ping-pong; work lists from a per-handle cache
+// the tcgen05 attention kernel (attn_fa.cu): one persistent launch over the items of pa and
+// then those of *pb (a fused step: attend + build_instant of the same handle); per-CTA item
+// tables come from the handle's cache
 struct SchedCache;
 SchedCache* sched_cache_new();
 void sched_cache_free(SchedCache* c);
-// device work lists [grid + 1 offsets | items] for this launch shape, or nullptr (static stride)
-const int* sched_lists(SchedCache* cache, const AttnParams& pa, const AttnParams* pb, long long na, long long nb,
-                       unsigned grid, long long (*item_tiles)(const AttnParams&, int), cudaStream_t st);
-// v7: per-CTA lists of host-decoded items (list-scheduled where that beats the stride by > 2%);
+// per-CTA lists of host-decoded items (list-scheduled where that beats the stride by > 2%);
 // *off = device [grid + 1] offsets, return = device records; nullptr on failure
 using ItemDecoder = ItemRec (*)(const AttnParams& p, int local, int isb);
 const ItemRec* item_table(SchedCache* cache, const AttnParams& pa, const AttnParams* pb, long long na, long long nb,
@@ -139,11 +133,7 @@ const ItemRec* item_table(SchedCache* cache, const AttnParams& pa, const AttnPar
 cudaError_t launch_attn_fa(const AttnParams& pa, const AttnParams* pb, SchedCache* cache, cudaStream_t st);
 int attn_fa_smem_bytes();
 int fa_watchdog_read(unsigned long long* out, int n);   // debug record (DSC_WATCHDOG=1)
-constexpr int kTileNFa = 128;  // keys per tile of the v7 kernel
 // K/V tensor map: [rows][128] bf16, box 64 columns x box_rows rows, SW128
 cudaError_t make_kv_tmap(CUtensorMap* map, void* base, unsigned long long rows, int box_rows);
-// encode the 2-D ring tensor map (bf16, d = 128) used by the tcgen05 kernel
-cudaError_t make_ring_tmap(CUtensorMap* map, void* base, unsigned long long rows);
-cudaError_t make_stage_tmap(CUtensorMap* map, void* base, unsigned long long rows);
 
 }  // namespace dsc

@@ -185,6 +185,13 @@ __global__ void __launch_bounds__(256) stage_instant_kernel(StageParams p) {
     }
     dk[c8] = make_uint4(ol[0], ol[1], ol[2], ol[3]);
     dk[c8 + 8] = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+    // debug export: the build id this K row was rotated at, by sink row / ring slot (kv head 0)
+    if (p.dbg_pos && g == 0 && c8 == 0 && p.boost_k == nullptr) {
+      int* const dbgp = p.dbg_pos + (s * p.N_total + p.layer_begin + l) * p.dbg_len;
+      int slot = p.inst_start + row - p.A;
+      if (slot >= p.R) slot -= p.R;
+      dbgp[row < p.A ? row : p.A + slot] = row;
+    }
     dv[c8] = sv[c8];
     dv[c8 + 8] = sv[c8 + 8];
   }
@@ -269,8 +276,10 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnParams p) {
   rotate<D>(q, p.rope, qpos, lane, p.rope_style);
   const float scale = rsqrtf((float)D);
 
-  const bool dbg = p.dbg_pos && pp == 0 && g == 0 && h == 0;
-  if (dbg && lane == 0) p.dbg_pos[p.A + p.R + p.dbg_M + i] = qpos;
+  // debug export: every problem, q head 0, block [s * N_total + layer] of the buffer
+  const bool dbg = p.dbg_pos && g == 0 && h == 0;
+  int* const dbgp = dbg ? p.dbg_pos + (head_row / p.Hkv) * p.dbg_len : nullptr;
+  if (dbg && lane == 0) dbgp[p.dbg_A + p.dbg_R + p.dbg_M + i] = qpos;
   const bool dbg_keys = dbg && i == p.n_q - 1;
 
   const int n_keys = p.A + p.ring_count + p.n_self;
@@ -282,17 +291,17 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnParams p) {
     const T *kr, *vr;
     if (L < p.A) {
       kr = SK + (head_row * p.A + L) * D; vr = SV + (head_row * p.A + L) * D;
-      if (dbg_keys && lane == 0) p.dbg_pos[L] = L;
+      if (dbg_keys && lane == 0) dbgp[L] = L;
     } else if (L < p.A + p.ring_count) {
       int slot = p.ring_start + (L - p.A);
       if (slot >= p.R) slot -= p.R;
       kr = RK + (head_row * p.Rp + slot) * D; vr = RV + (head_row * p.Rp + slot) * D;
-      if (dbg_keys && lane == 0) p.dbg_pos[p.A + slot] = L;
+      if (dbg_keys && lane == 0) dbgp[p.dbg_A + slot] = L;
     } else {
       const int j = L - p.A - p.ring_count;
       kr = XK + (((long long)pp * p.n_self + j) * p.Hkv + g) * D;
       vr = XV + (((long long)pp * p.n_self + j) * p.Hkv + g) * D;
-      if (dbg_keys && lane == 0) p.dbg_pos[p.A + p.R + j] = L;
+      if (dbg_keys && lane == 0) dbgp[p.dbg_A + p.dbg_R + j] = L;
     }
     float kx[E], vx[E];
 #pragma unroll

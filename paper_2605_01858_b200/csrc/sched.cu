@@ -29,8 +29,7 @@ struct SchedCache {
     cudaEvent_t ready = nullptr;  // upload done
     cudaStream_t stream = nullptr;
   };
-  std::map<std::vector<long long>, Entry> entries;
-  std::map<std::vector<long long>, Entry> tables;   // v7 item tables: [grid + 1 offsets | pad | ItemRec[]]
+  std::map<std::vector<long long>, Entry> tables;   // item tables: [grid + 1 offsets | pad | ItemRec[]]
   std::mutex mu;
   size_t bytes = 0;
 };
@@ -39,11 +38,10 @@ SchedCache* sched_cache_new() { return new SchedCache(); }
 
 void sched_cache_free(SchedCache* c) {
   if (!c) return;
-  for (auto* m : {&c->entries, &c->tables})
-    for (auto& kv : *m) {
-      if (kv.second.ready) cudaEventDestroy(kv.second.ready);
-      if (kv.second.dev) cudaFree(kv.second.dev);
-    }
+  for (auto& kv : c->tables) {
+    if (kv.second.ready) cudaEventDestroy(kv.second.ready);
+    if (kv.second.dev) cudaFree(kv.second.dev);
+  }
   delete c;
 }
 
@@ -51,78 +49,6 @@ namespace {
 constexpr long long kSwitchCost = 2;              // item-switch cost in key tiles
 constexpr size_t kMaxCacheBytes = 256ull << 20;   // beyond this, new shapes fall back to the stride
 }  // namespace
-
-const int* sched_lists(SchedCache* cache, const AttnParams& pa, const AttnParams* pb, long long na, long long nb,
-                       unsigned grid, long long (*item_tiles)(const AttnParams&, int), cudaStream_t st) {
-  if (!cache) return nullptr;
-  std::lock_guard<std::mutex> lock(cache->mu);
-  int device = 0;
-  cudaGetDevice(&device);
-  std::vector<long long> key = {device, na, nb, (long long)grid};
-  for (const AttnParams* p : {&pa, pb}) {
-    if (!p) continue;
-    for (long long v : {(long long)p->n_splits, (long long)p->split_only, (long long)p->P, (long long)p->Hkv,
-                        (long long)p->n_mblocks, (long long)p->n_q, (long long)p->grp, (long long)p->q_pos0,
-                        (long long)p->A, (long long)p->ring_count, (long long)p->n_self,
-                        (long long)p->tiles_per_split})
-      key.push_back(v);
-  }
-  auto it = cache->entries.find(key);
-  if (it != cache->entries.end()) {
-    const SchedCache::Entry& e = it->second;
-    if (e.dev && e.stream != st && e.ready) cudaStreamWaitEvent(st, e.ready, 0);
-    return e.dev;
-  }
-  const long long items = na + nb;
-  std::vector<int> off(grid + 1, 0), owner(items);
-  std::vector<long long> stride_load(grid, 0);
-  std::vector<std::pair<long long, int>> heap;   // min-heap on (load, cta)
-  heap.reserve(grid);
-  for (unsigned b = 0; b < grid; ++b) heap.push_back({0, (int)b});
-  auto cmp = [](const std::pair<long long, int>& x, const std::pair<long long, int>& y) { return x > y; };
-  std::make_heap(heap.begin(), heap.end(), cmp);
-  for (long long I = 0; I < items; ++I) {
-    const bool isb = I >= na;
-    const long long cost = item_tiles(isb ? *pb : pa, (int)(isb ? I - na : I)) + kSwitchCost;
-    stride_load[I % grid] += cost;
-    std::pop_heap(heap.begin(), heap.end(), cmp);
-    const int b = heap.back().second;
-    owner[I] = b;
-    heap.back().first += cost;
-    std::push_heap(heap.begin(), heap.end(), cmp);
-    ++off[b + 1];
-  }
-  for (unsigned b = 0; b < grid; ++b) off[b + 1] += off[b];
-  long long list_max = 0;
-  for (auto& h : heap) list_max = std::max(list_max, h.first);
-  const long long stride_max = *std::max_element(stride_load.begin(), stride_load.end());
-  SchedCache::Entry e;
-  const bool use = list_max * 50 < stride_max * 49;
-  const size_t need = (grid + 1 + items) * sizeof(int);
-  if (use && cache->bytes + need <= kMaxCacheBytes) {
-    std::vector<int> host(grid + 1 + items);
-    std::copy(off.begin(), off.end(), host.begin());
-    std::vector<int> fill(off.begin(), off.end() - 1);
-    for (long long I = 0; I < items; ++I) host[grid + 1 + fill[owner[I]]++] = (int)I;   // increasing I per CTA
-    if (cudaMalloc(&e.dev, need) != cudaSuccess) {
-      cudaGetLastError();
-      return nullptr;   // not cached: the next call retries
-    }
-    // pageable source: staged before the call returns, so `host` may go out of scope
-    if (cudaMemcpyAsync(e.dev, host.data(), need, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaEventCreateWithFlags(&e.ready, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventRecord(e.ready, st) != cudaSuccess) {
-      cudaGetLastError();
-      if (e.ready) cudaEventDestroy(e.ready);
-      cudaFree(e.dev);
-      return nullptr;
-    }
-    e.stream = st;
-    cache->bytes += need;
-  }
-  cache->entries.emplace(std::move(key), e);
-  return e.dev;
-}
 
 namespace {
 std::vector<long long> shape_key(int device, const AttnParams& pa, const AttnParams* pb, long long na, long long nb,

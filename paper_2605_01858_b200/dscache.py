@@ -449,9 +449,11 @@ class DSCache:
 
     def set_debug(self, build_pos: Optional[torch.Tensor] = None, attend_pos: Optional[torch.Tensor] = None,
                   poison: bool = False):
+        need = self.cfg.num_streams * self.cfg.num_layers * self.debug_len()
         for t in (build_pos, attend_pos):
-            if t is not None and (t.dtype != torch.int32 or t.device != self.device or t.numel() < self.debug_len()):
-                raise ValueError("debug buffers must be int32 CUDA tensors of debug_len() entries")
+            if t is not None and (t.dtype != torch.int32 or t.device != self.device or t.numel() < need):
+                raise ValueError("debug buffers must be int32 CUDA tensors of num_streams*num_layers*debug_len() "
+                                 "entries ([S][N][debug_len])")
         self._dbg = (build_pos, attend_pos)   # keep alive
         _check(_lib.dscache_set_debug(self._h, _ptr(build_pos), _ptr(attend_pos), int(bool(poison))))
 

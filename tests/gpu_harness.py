@@ -27,6 +27,8 @@ def run_stream(cfg, capture_steps, exact, impl=D.IMPL_AUTO, debug=False, poison=
                layer_by_layer=False, n_q=None, past_override=None, update_lL=None, fused=False):
     """Returns {t: {(s,l): (o_inst cpu, o cpu)}, "ring": {(t,s,l): (k,v)}, "dbg": {t: (b,a)}, "state": {t: st}}.
 
+    "dbg" arrays are [S][N][debug_len]: the ids each (stream, layer) applied (kv head 0).
+
     past_override(s, l, f) -> (k, v) or None lets a test replace past frames (decoupling test).
     fused=True runs captured steps through DSCache.step (append + build + attend in one call)."""
     dev = torch.device("cuda", 0)
@@ -38,8 +40,9 @@ def run_stream(cfg, capture_steps, exact, impl=D.IMPL_AUTO, debug=False, poison=
     dbg_b = dbg_a = None
     if debug or poison:
         if debug:
-            dbg_b = torch.full((dsc.debug_len(),), -1, dtype=torch.int32, device=dev)
-            dbg_a = torch.full((dsc.debug_len(),), -1, dtype=torch.int32, device=dev)
+            dbg_shape = (cfg.num_streams, cfg.num_layers, dsc.debug_len())   # one block per (stream, layer)
+            dbg_b = torch.full(dbg_shape, -1, dtype=torch.int32, device=dev)
+            dbg_a = torch.full(dbg_shape, -1, dtype=torch.int32, device=dev)
         dsc.set_debug(dbg_b, dbg_a, poison)
     A, tpf, Hkv, Hq, d = cfg.sink_tokens, cfg.tokens_per_frame, cfg.num_kv_heads, cfg.num_q_heads, cfg.head_dim
     if A > 0:

@@ -140,35 +140,73 @@ def test_poison_evicted_slots_and_outputs_unchanged(lib):
         assert torch.all(k[:, slots].float() > 1e29)
 
 
+def _check_ids(cfg, dbg_b, dbg_a, t, what=""):
+    """Bit-exact position ids one (stream, layer) applied at step t (its debug block)."""
+    R = (cfg.past_frames + cfg.instant_frames + 1) * cfg.tokens_per_frame
+    A = cfg.sink_tokens
+    M = max(cfg.C, cfg.query_tokens)
+    sch = step_schedule(cfg, t)
+    bk, bq, ak, aq = O.position_ids(sch, cfg.query_tokens)
+    # attend: sink ids, ring slot -> id, self ids, query ids
+    assert np.array_equal(dbg_a[:A], ak[:A]), what
+    frames = sch.past_frames + sch.instant_frames
+    slots = np.concatenate([O.ring_slots(f, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames)
+                            for f in frames])
+    assert np.array_equal(dbg_a[A + slots], ak[A:A + len(slots)]), what
+    in_window = np.zeros(R, bool); in_window[slots] = True
+    assert np.all(dbg_a[A:A + R][~in_window] == -1), what
+    nq = cfg.query_tokens
+    assert np.array_equal(dbg_a[A + R:A + R + nq], ak[A + len(slots):]), what
+    assert np.array_equal(dbg_a[A + R + M:A + R + M + nq], aq), what
+    # build: sink ids, instant slots -> A + i, query ids A + i
+    islots = np.concatenate([O.ring_slots(f, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames)
+                             for f in sch.instant_frames])
+    assert np.array_equal(dbg_b[:A], bk[:A]), what
+    assert np.array_equal(dbg_b[A + islots], bk[A:]), what
+    assert np.array_equal(dbg_b[A + R + M:A + R + M + sch.C_t], bq), what
+
+
 @pytest.mark.parametrize("name", ["c1", "c2"])
 def test_debug_position_ids_bit_exact(lib, name):
     cfg = synth.CONFIGS[name]
     steps = [0, 3, 37] if name == "c2" else [0, 3, 7, 19]
     res = run_stream(cfg, steps, [(0, 0)], debug=True)
-    R = (cfg.past_frames + cfg.instant_frames + 1) * cfg.tokens_per_frame
-    A = cfg.sink_tokens
-    M = max(cfg.C, cfg.query_tokens)
+    for t in steps:
+        dbg_b, dbg_a = (x[0, 0] for x in res["dbg"][t])
+        _check_ids(cfg, dbg_b, dbg_a, t, f"{name} t={t}")
+
+
+@pytest.mark.parametrize("name,steps,exact", [
+    # the bench's own path: dscache_step (one fused launch, staged pre-rotated build window)
+    ("c5", [0, 35, 36, 127], [(0, 0), (0, 3), (7, 0), (7, 3), (63, 0), (63, 3)]),
+    ("c3", [0, 71, 72, 255], [(0, 0), (0, 13), (0, 27)]),
+])
+def test_fused_step_ring_eviction_ids_bit_exact(lib, name, steps, exact):
+    """Ring slot contents, eviction bookkeeping and every applied position id, bit-exact,
+    through dscache_step on the configurations the bench times (c5: 64 streams x 4 layers;
+    c3: 28 layers), plus value parity of the same fused steps."""
+    cfg = synth.CONFIGS[name]
+    res = run_stream(cfg, steps, exact, fused=True, debug=True, ring_capture=exact)
+    _check_steps(cfg, res, steps, exact, tag="-fused-exact")
     for t in steps:
         sch = step_schedule(cfg, t)
-        bk, bq, ak, aq = O.position_ids(sch, cfg.query_tokens)
+        st = res["state"][t]
+        assert st["past_tokens"] == sch.P_t and st["instant_tokens"] == sch.C_t
+        assert st["last_evicted_frame"] == (sch.evicted[0] if sch.evicted else -1)
         dbg_b, dbg_a = res["dbg"][t]
-        # attend: sink ids, ring slot -> id, self ids, query ids
-        assert np.array_equal(dbg_a[:A], ak[:A])
-        frames = sch.past_frames + sch.instant_frames
-        slots = np.concatenate([O.ring_slots(f, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames)
-                                for f in frames])
-        assert np.array_equal(dbg_a[A + slots], ak[A:A + len(slots)])
-        in_window = np.zeros(R, bool); in_window[slots] = True
-        assert np.all(dbg_a[A:A + R][~in_window] == -1)
-        nq = cfg.query_tokens
-        assert np.array_equal(dbg_a[A + R:A + R + nq], ak[A + len(slots):])
-        assert np.array_equal(dbg_a[A + R + M:A + R + M + nq], aq)
-        # build: sink ids, instant slots -> A + i, query ids A + i
-        islots = np.concatenate([O.ring_slots(f, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames)
-                                 for f in sch.instant_frames])
-        assert np.array_equal(dbg_b[:A], bk[:A])
-        assert np.array_equal(dbg_b[A + islots], bk[A:])
-        assert np.array_equal(dbg_b[A + R + M:A + R + M + sch.C_t], bq)
+        for (s, l) in exact:
+            _check_ids(cfg, dbg_b[s, l], dbg_a[s, l], t, f"{name} t={t} s={s} l={l}")
+            exp = expected_ring(cfg, sch, StreamInputs(cfg, s, l))
+            slots = np.array(sorted(exp))
+            ek = np.stack([exp[int(x)][0] for x in slots], axis=1)   # [Hkv, n, d]
+            ev = np.stack([exp[int(x)][1] for x in slots], axis=1)
+            k, v = res["ring"][(t, s, l)]
+            assert np.array_equal(k[:, slots].double().numpy(), ek), (name, t, s, l)
+            assert np.array_equal(v[:, slots].double().numpy(), ev), (name, t, s, l)
+        # every other (stream, layer) applied the same ids (kv head 0 of each block)
+        ref_b, ref_a = dbg_b[exact[0]], dbg_a[exact[0]]
+        assert np.array_equal(dbg_a.reshape(-1, dbg_a.shape[-1]), np.broadcast_to(ref_a, (dbg_a.shape[0] * dbg_a.shape[1], ref_a.shape[0])))
+        assert np.array_equal(dbg_b.reshape(-1, dbg_b.shape[-1]), np.broadcast_to(ref_b, (dbg_b.shape[0] * dbg_b.shape[1], ref_b.shape[0])))
 
 
 def test_decoupling_instant_independent_of_past(lib):
@@ -228,7 +266,7 @@ def test_logical_tiles_mirror_and_narrow_widths(lib, variant):
 
 def test_c3_28_layers_sampled(lib):
     cfg = synth.CONFIGS["c3"]
-    steps = [0, 7, 8, 71, 72, 100]
+    steps = [0, 7, 8, 71, 72, 100, 255]
     exact = [(0, 0), (0, 13), (0, 27)]
     res = run_stream(cfg, steps, exact)
     _check_steps(cfg, res, steps, exact)
@@ -240,7 +278,7 @@ def test_c4_long_stream_sampled(lib):
     res = run_stream(cfg, steps, [(0, 0)], debug=True)
     _check_steps(cfg, res, steps, [(0, 0)])
     dbg_b, dbg_a = res["dbg"][4095]
-    assert dbg_a.max() == 26723 and dbg_a.max() < cfg.max_position
+    assert dbg_a[0, 0].max() == 26723 and dbg_a.max() < cfg.max_position
 
 
 def test_c5_multistream_sampled(lib):

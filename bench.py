@@ -52,6 +52,27 @@ def peaks():
 
 
 # ----------------------------------------------------------------------------- workload arithmetic
+def traffic_key(args, world: int) -> str:
+    return f"{args.config}|{args.mode}|{args.api}|boost{args.boost:g}|world{world}|layerseq{int(args.layer_seq)}"
+
+
+def config_dict(cfg, args, world: int, S_local=None):
+    """The `config` object of the JSON line, shared by both arms (same workload description)."""
+    A, P, C, q = steady_counts(cfg)
+    par = "single GPU"
+    if world > 1:
+        par = {"kvsplit": f"KV-head split x{world} (NCCL all-gather of O)",
+               "context": f"context split x{world} (NCCL all-gather of partials + merge)"}.get(
+                   args.mode, f"stream partition x{world}")
+    return {"workload": f"{cfg.name}: {cfg.num_streams} streams x {cfg.num_layers} layers, Hq={cfg.num_q_heads} "
+                        f"Hkv={cfg.num_kv_heads} d={cfg.head_dim}, tpf={cfg.tokens_per_frame}, A={A}, "
+                        f"W={cfg.past_frames}f, C={cfg.instant_frames}f, q={q}",
+            "config_id": cfg.name, "streams": cfg.num_streams, "layers": cfg.num_layers, "query_tokens": q,
+            "parallelism": par, "mode": args.mode, "api": args.api, "layer_sequential": bool(args.layer_seq),
+            "n_boost": int(round(args.boost * cfg.tokens_per_frame)) if args.boost > 0 else 0,
+            "steady_state": True}
+
+
 def steady_counts(cfg, n_q=None):
     """Steady-state token counts per (stream, layer): A, P = W, C, q."""
     n_q = cfg.query_tokens if n_q is None else n_q
@@ -85,7 +106,26 @@ def bytes_per_unit(cfg):
 
 
 # ----------------------------------------------------------------------------- clocks
+def clock_snapshot(device_index: int):
+    """One nvidia-smi reading (sm MHz, max MHz, active reasons), or None."""
+    q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    try:
+        out = subprocess.run(["nvidia-smi", "-i", str(device_index), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=10).stdout.strip().split(",")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        return {"sm_mhz": float(out[0]), "sm_max_mhz": float(out[1]),
+                "reasons": [n for n, v in zip(names, out[2:6]) if v.strip().lower().startswith("active")]}
+    except Exception:
+        return None
+
+
 class ClockSampler:
+    """nvidia-smi sampling every 50 ms while the GPU runs the step loop.  The sampled window
+    covers the timed steps and, when they take less than HOLD_S, untimed repetitions of the
+    same step right after them (so short timed regions still get clock samples)."""
+    HOLD_S = 0.3
+
     def __init__(self, device_index: int):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -163,7 +203,15 @@ def run_ours(args, cfg, world, rank, local):
     from paper_2605_01858_b200 import dscache as D
     dev = torch.device("cuda", local)
     kvsplit = args.mode == "kvsplit"
-    if kvsplit:
+    context = args.mode == "context"
+    if context:
+        # P3: one stream, every rank holds its whole cache and attends over 1/G of its keys;
+        # the (O_r, lse_r) partials are all-gathered (NCCL) and merged by the combine kernel
+        cfg = cfg.replace(num_streams=1)
+        lcfg = cfg
+        S = 1
+        dsc = D.DSCache.from_config(lcfg, device=local)
+    elif kvsplit:
         # P2: one stream, rank r holds KV heads [r*Hkv/G, (r+1)*Hkv/G) and their q heads
         from paper_2605_01858_b200.dist import kv_head_partition
         kv_lo, kv_n, q_lo, q_n = kv_head_partition(cfg.num_q_heads, cfg.num_kv_heads, world, rank)
@@ -188,6 +236,8 @@ def run_ours(args, cfg, world, rank, local):
     # device-resident synthetic input pool (values cycle; positions / slots never repeat)
     POOL = 4
     frames = [(rnd(S, N, tpf, Hkv, d), rnd(S, N, tpf, Hkv, d)) for _ in range(POOL)]
+    if args.layer_seq and S != 1:
+        raise SystemExit("--layer-seq times one stream's layers in order (c3); use a single-stream config")
     n_boost = int(round(args.boost * tpf)) if args.boost > 0 else 0
     Cq = C - tpf + n_boost if n_boost else C          # instant rows built per step
     q_inst = [rnd(S, N, Cq, Hq, d) for _ in range(2)]
@@ -210,7 +260,21 @@ def run_ours(args, cfg, world, rank, local):
     def step(i):
         t = tcount[0]
         qq = qry[i & 1]
-        if n_boost:     # NEXT-4 resolution boost: the newest frame re-encoded (n_boost tokens)
+        if context:     # P3 (NEXT-4): key-range split of one stream's attend, partials merged
+            from paper_2605_01858_b200.dist import context_parallel_attend
+            dsc.append_frame(*frames[t % POOL])
+            dsc.build_instant(q_inst[i & 1], o_inst)
+            if world > 1:
+                gathered[0] = context_parallel_attend(dsc, qq[0], qq[1], qq[2])
+            else:
+                dsc.attend(qq[0], qq[1], qq[2], o)
+        elif args.layer_seq:   # layer r+1 consumes layer r: one fused step per layer, in order
+            fk, fv = frames[t % POOL]
+            for l in range(N):
+                dsc.step(fk[:, l:l + 1], fv[:, l:l + 1], q_inst[i & 1][:, l:l + 1], qq[0][:, l:l + 1],
+                         qq[1][:, l:l + 1], qq[2][:, l:l + 1], o_inst=o_inst[:, l:l + 1], o=o[:, l:l + 1],
+                         layer_begin=l, layer_count=1)
+        elif n_boost:     # NEXT-4 resolution boost: the newest frame re-encoded (n_boost tokens)
             dsc.append_frame(*frames[t % POOL])
             dsc.build_instant_boost(q_inst[i & 1], *boost_kv[i & 1], o_inst=o_inst)
             dsc.attend_boost(qq[0], qq[1], qq[2], *boost_kv[i & 1], o=o)
@@ -237,6 +301,7 @@ def run_ours(args, cfg, world, rank, local):
     dsc.profile_read(reset=True)
     barrier(world)
     torch.cuda.synchronize()
+    snap_before = clock_snapshot(local) if rank == 0 else None
     clocks = ClockSampler(local) if rank == 0 else None
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if flush:
@@ -255,9 +320,22 @@ def run_ours(args, cfg, world, rank, local):
         ev[0][1].record(stream)
         torch.cuda.synchronize()
         total_ms = ev[0][0].elapsed_time(ev[0][1])
+    if clocks:
+        # short timed regions: keep the same step loop running (untimed) so the sampler sees
+        # the clocks of this workload for at least HOLD_S
+        t_hold = time.perf_counter()
+        i = args.steps
+        while time.perf_counter() - t_hold < clocks.HOLD_S - total_ms / 1e3:
+            for _ in range(4):
+                step(i)
+                i += 1
+            torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
     clk = clocks.stop() if clocks else None
+    if clk is not None:
+        clk["window"] = "timed steps + untimed repetitions of the same step up to %.1f s" % ClockSampler.HOLD_S
+        clk["snapshot_before"], clk["snapshot_after"] = snap_before, clock_snapshot(local)
     prof = dsc.profile_read(reset=True)
     dsc.profile(False)
     t_max = max_over_ranks(total_ms, world)
@@ -279,27 +357,27 @@ def run_ours(args, cfg, world, rank, local):
     pk = peaks()
     achieved = (attn_flops_step_local * args.steps) / (attn_ms / 1e3) / 1e12 if attn_ms > 0 else None
     step_tflops = attn_flops_step_local * args.steps / (total_ms / 1e3) / 1e12
-    traffic = None
+    # DRAM bytes per attention launch from an ncu --set full capture of exactly this launch
+    # shape (profiles/ncu_traffic.json, written by scripts/summarize_profile.py); null if
+    # this (config, mode, api, boost, world, layers-seq) combination was never captured
+    traffic, traffic_tag = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(cfg.name, {}).get("attn_tc_kernel_dram_bytes_per_launch")
+            rec = json.load(open(tp)).get(traffic_key(args, world), {})
+            traffic, traffic_tag = rec.get("dram_bytes_per_launch"), rec.get("tag")
         except Exception:
             traffic = None
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "strong",
+        "scaling": "strong",   # the config's total work (all its streams) is fixed as N grows
         "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.num_streams} streams x {cfg.num_layers} layers, Hq={Hq} Hkv={Hkv} "
-                               f"d={d}, tpf={tpf}, A={A}, W={cfg.past_frames}f, C={cfg.instant_frames}f, q={q}",
-                   "config_id": cfg.name, "streams": cfg.num_streams, "layers": N, "query_tokens": q,
-                   "parallelism": (f"KV-head split x{world} (NCCL all-gather of O)" if kvsplit else
-                                   f"stream partition x{world}") if world > 1 else "single GPU",
-                   "mode": args.mode, "api": "boost (split calls)" if n_boost else args.api,
-                   "n_boost": n_boost,
-                   "l2": "flushed between steps" if flush else "inputs larger than L2 (ring %.2f GB)" % (ring_bytes / 1e9),
-                   "steady_state": True, "input_pool": f"{POOL} distinct frames cycled (positions never repeat)"},
+        "config": dict(config_dict(cfg, args, world),
+                       l2=("flushed between steps" if flush else "inputs larger than L2 (ring %.2f GB)" % (ring_bytes / 1e9)),
+                       input_pool=f"{POOL} distinct frames cycled (positions never repeat)"),
+        "value_is": "aggregate frames/s over all streams and GPUs (one frame per stream per step); "
+                    "frames_per_s_per_stream = value / streams",
         "frames_per_s_per_stream": round(value / cfg.num_streams, 3),
         "attention_tflops_per_gpu_step": round(step_tflops, 2),
         "attention_pct_peak_step": round(100 * step_tflops / pk["bf16_tflops"], 2),
@@ -312,7 +390,9 @@ def run_ours(args, cfg, world, rank, local):
                      "peak_sustained": pk.get("bf16_tflops_sustained"),
                      "frac_vs_sustained": (round(achieved / pk["bf16_tflops_sustained"], 4)
                                            if achieved and pk.get("bf16_tflops_sustained") else None),
-                     "traffic": traffic, "launches": n_launch,
+                     "traffic": traffic, "traffic_source": (f"ncu --set full, profiles/{traffic_tag}_ncu_full.md"
+                                                            if traffic else "not captured for this launch shape"),
+                     "launches": n_launch,
                      "algorithmic_flops_per_launch": (attn_flops_step_local * args.steps) / max(n_launch, 1)},
         "gpu_launches": prof["kernel_launches"],
         "attn_impl": impl,
@@ -413,7 +493,7 @@ def oracle_sample(cfg, budget_s: float):
     per_unit = float(np.mean(times))
     step_s = per_unit * cfg.num_streams * cfg.num_layers
     return {"value": round(cfg.num_streams / step_s, 6), "unit": "frames/s", "cores": threads,
-            "kind": "oracle",
+            "kind": "oracle", "units": units,
             "sample": f"{units} steady-state (stream, layer) units of {cfg.name} (build_instant + attend, fp64 "
                       f"numpy), {per_unit:.3f} s/unit, extrapolated to {cfg.num_streams * cfg.num_layers} "
                       f"units per step",
@@ -444,11 +524,52 @@ def run_reference(args, cfg):
             "warmup": args.warmup, "ms_per_step": round(1e3 * cfg.num_streams / value, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": cfg.name, "config_id": cfg.name, "streams": cfg.num_streams,
-                       "layers": cfg.num_layers, "note": "fp64 CPU oracle (oracle/), the tier's reference arm"},
+            "config": config_dict(cfg, args, 1),
+            "reference_note": "fp64 CPU oracle (oracle/), the tier's reference arm: each timed step runs a "
+                              "bounded sample of (stream, layer) units and is extrapolated to the full step",
+            "extrapolated": True, "units_run": [r["units"] for r in per_step],
             "cpu_baseline": {"value": round(value, 6), "unit": "frames/s", "cores": cb["cores"], "kind": "oracle",
                              "sample": cb["sample"], "cpu": cb["cpu"]},
             "e2e": {"value": round(value, 6), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def _free_port() -> int:
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def dry_run(args, cfg):
+    """Every rank computes what it would hold (P1 streams / P2 KV heads / P3 key split) and
+    rank 0 prints the gathered plan: the N-rank launch path without GPU work."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    from paper_2605_01858_b200.dist import kv_head_partition, stream_partition
+    if args.mode in ("kvsplit", "context"):
+        cfg = cfg.replace(num_streams=1)   # the single-stream modes (as run_ours)
+    if args.mode == "kvsplit":
+        part = dict(zip(("kv_lo", "kv_count", "q_lo", "q_count"),
+                        kv_head_partition(cfg.num_q_heads, cfg.num_kv_heads, world, rank)))
+    elif args.mode == "context":
+        part = {"key_part": rank, "key_parts": world}
+    else:
+        lo, hi = stream_partition(cfg.num_streams, world, rank)
+        part = {"streams": [lo, hi]}
+    part["rank"] = rank
+    plan = [part]
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        plan = [None] * world
+        dist.all_gather_object(plan, part)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "mode": args.mode, "config": config_dict(cfg, args, world),
+                          "partition": plan}), flush=True)
+    return 0
 
 
 def main():
@@ -458,8 +579,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="streams", choices=["streams", "kvsplit"],
-                    help="streams: P1 stream partition (default); kvsplit: P2 KV-head split of one stream")
+    ap.add_argument("--mode", default="streams", choices=["streams", "kvsplit", "context"],
+                    help="streams: P1 stream partition (default); kvsplit: P2 KV-head split of one stream; "
+                         "context: P3 key-range split of one stream's attend (NEXT-4)")
+    ap.add_argument("--layer-seq", action="store_true",
+                    help="one fused step per layer, layers in order (a real model's dependency; c3)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch the N ranks and print each rank's partition, no GPU work (gloo without CUDA)")
     ap.add_argument("--api", default="fused", choices=["fused", "split"],
                     help="fused: DSCache.step (one attention launch per step); split: three calls")
     ap.add_argument("--boost", type=float, default=0.0,
@@ -470,6 +596,18 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     cfg = synth.CONFIGS[args.config]
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not launched by torchrun: launch N ranks of this same command (one process per GPU)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if world_env != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world_env}: launch N ranks with torchrun "
+                                   f"or omit WORLD_SIZE"}), flush=True)
+        return 2
+    if args.dry_run:
+        return dry_run(args, cfg)
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         if rank != 0:

@@ -77,15 +77,10 @@ struct dscache_s {
   void* sink_k = nullptr;
   void* sink_v = nullptr;
   float2* rope = nullptr;
-  float* ws = nullptr;       // split-KV workspace (grown on demand)
-  size_t ws_bytes = 0;
   void* bstage_k = nullptr;  // staged boosted build: sink ++ older instant ++ boosted frame (grown on demand)
   void* bstage_v = nullptr;
   int bstage_rows = 0;
   CUtensorMap tmap_bk{}, tmap_bv{};
-  void* boost_k = nullptr;   // [boost | self] key gather of dscache_attend_boost (grown on demand)
-  void* boost_v = nullptr;
-  size_t boost_bytes = 0;
   std::vector<int64_t> frames;
   std::vector<int> sink_filled;
   std::vector<int64_t> last_evicted;
@@ -170,15 +165,28 @@ void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
   p.n_splits = 1; p.tiles_per_split = 1 << 30; p.split_only = -1;
 }
 
-dscache_status grow_ws(dscache_t h, size_t bytes) {
-  if (bytes <= h->ws_bytes) return DSCACHE_OK;
-  if (h->ws) cudaFree(h->ws);
-  h->ws = nullptr; h->ws_bytes = 0;
-  if (cudaMalloc(&h->ws, bytes) != cudaSuccess) {
-    cudaGetLastError();
-    return fail(DSCACHE_E_OOM, "split-KV workspace allocation failed");
+// Per-call scratch, stream-ordered (cudaMallocAsync / cudaFreeAsync on the call's stream):
+// calls for different layer ranges may run on different streams concurrently, so no
+// scratch is shared between calls (a per-handle workspace was).
+struct StreamScratch {
+  void* ptr = nullptr;
+  cudaStream_t st = nullptr;
+  ~StreamScratch() { if (ptr) cudaFreeAsync(ptr, st); }
+  bool alloc(size_t bytes, cudaStream_t s) {
+    st = s;
+    if (cudaMallocAsync(&ptr, bytes, s) != cudaSuccess) { cudaGetLastError(); ptr = nullptr; return false; }
+    return true;
   }
-  h->ws_bytes = bytes;
+};
+
+// split-KV attend: the fp32 partials [splits][rows][d] + log2-sum-exps [splits][rows]
+dscache_status alloc_ws(dsc::AttnParams& p, StreamScratch& ws, cudaStream_t st) {
+  if (p.n_splits <= 1 || p.split_only >= 0 || p.ws_o) return DSCACHE_OK;
+  const size_t rows = (size_t)p.P * p.n_q * p.Hq;
+  if (!ws.alloc((size_t)p.n_splits * rows * (p.d + 1) * sizeof(float), st))
+    return fail(DSCACHE_E_OOM, "split-KV workspace allocation failed");
+  p.ws_o = static_cast<float*>(ws.ptr);
+  p.ws_lse = p.ws_o + (size_t)p.n_splits * rows * p.d;
   return DSCACHE_OK;
 }
 
@@ -188,6 +196,9 @@ cudaError_t launch_tc(dscache_t h, const dsc::AttnParams& pa, const dsc::AttnPar
 }
 
 dscache_status run_attention(dscache_t h, dsc::AttnParams& p, int impl, int kind, cudaStream_t st) {
+  StreamScratch ws;
+  dscache_status ss = alloc_ws(p, ws, st);
+  if (ss != DSCACHE_OK) return ss;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->prof) { e0 = h->take_event(); e1 = h->take_event(); cudaEventRecord(e0, st); }
   cudaError_t e;
@@ -310,9 +321,8 @@ dscache_status dscache_destroy(dscache_t h) {
   for (auto& ev : h->pending) { cudaEventDestroy(ev.a); cudaEventDestroy(ev.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
   cudaFree(h->ring_k); cudaFree(h->ring_v); cudaFree(h->sink_k); cudaFree(h->sink_v);
-  cudaFree(h->rope); cudaFree(h->ws);
+  cudaFree(h->rope);
   cudaFree(h->stage_k); cudaFree(h->stage_v);
-  cudaFree(h->boost_k); cudaFree(h->boost_v);
   cudaFree(h->bstage_k); cudaFree(h->bstage_v);
   dsc::sched_cache_free(h->sched);
   delete h;
@@ -478,14 +488,7 @@ dscache_status prep_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, c
       p.tiles_per_split = (tiles + splits - 1) / splits;
       splits = (tiles + p.tiles_per_split - 1) / p.tiles_per_split;
     }
-    p.n_splits = splits;
-    if (splits > 1) {
-      const size_t rows = (size_t)p.P * n_q * p.Hq;
-      dscache_status gs = grow_ws(h, (size_t)splits * rows * (p.d + 1) * sizeof(float));
-      if (gs != DSCACHE_OK) return gs;
-      p.ws_o = h->ws;
-      p.ws_lse = h->ws + (size_t)splits * rows * p.d;
-    }
+    p.n_splits = splits;   // the workspace is allocated per call on its stream (alloc_ws)
   }
   return DSCACHE_OK;
 }
@@ -588,26 +591,20 @@ dscache_status dscache_attend_boost(dscache_t h, int32_t lb, int32_t lc, const v
   const size_t P = (size_t)c.num_streams * lc;
   const size_t need = P * (size_t)(n_boost + n_q) * row;
   DeviceGuard dg(c.device);
-  if (need > h->boost_bytes) {
-    cudaFree(h->boost_k); cudaFree(h->boost_v);
-    h->boost_k = h->boost_v = nullptr; h->boost_bytes = 0;
-    if (cudaMalloc(&h->boost_k, need) != cudaSuccess || cudaMalloc(&h->boost_v, need) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(DSCACHE_E_OOM, "boost scratch allocation failed");
-    }
-    h->boost_bytes = need;
-  }
-  dsc::AttnParams p{};
-  s = prep_attend(h, lb, lc, q, h->boost_k, h->boost_v, n_boost + n_q, n_q, o, false, p, c.tokens_per_frame);
-  if (s != DSCACHE_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
+  // per-call gather buffers, stream-ordered (no scratch shared between calls)
+  StreamScratch bk, bv;
+  if (!bk.alloc(need, st) || !bv.alloc(need, st)) return fail(DSCACHE_E_OOM, "boost scratch allocation failed");
+  dsc::AttnParams p{};
+  s = prep_attend(h, lb, lc, q, bk.ptr, bv.ptr, n_boost + n_q, n_q, o, false, p, c.tokens_per_frame);
+  if (s != DSCACHE_OK) return s;
   // self segment [boosted frame | query chunk] per problem: [P][n_boost + n_q][Hkv][d]
   const size_t pitch = (size_t)(n_boost + n_q) * row;
-  DSC_CUDA(cudaMemcpy2DAsync(h->boost_k, pitch, k_boost, n_boost * row, n_boost * row, P, cudaMemcpyDeviceToDevice, st));
-  DSC_CUDA(cudaMemcpy2DAsync(h->boost_v, pitch, v_boost, n_boost * row, n_boost * row, P, cudaMemcpyDeviceToDevice, st));
-  DSC_CUDA(cudaMemcpy2DAsync((char*)h->boost_k + n_boost * row, pitch, k_self, n_q * row, n_q * row, P,
+  DSC_CUDA(cudaMemcpy2DAsync(bk.ptr, pitch, k_boost, n_boost * row, n_boost * row, P, cudaMemcpyDeviceToDevice, st));
+  DSC_CUDA(cudaMemcpy2DAsync(bv.ptr, pitch, v_boost, n_boost * row, n_boost * row, P, cudaMemcpyDeviceToDevice, st));
+  DSC_CUDA(cudaMemcpy2DAsync((char*)bk.ptr + n_boost * row, pitch, k_self, n_q * row, n_q * row, P,
                              cudaMemcpyDeviceToDevice, st));
-  DSC_CUDA(cudaMemcpy2DAsync((char*)h->boost_v + n_boost * row, pitch, v_self, n_q * row, n_q * row, P,
+  DSC_CUDA(cudaMemcpy2DAsync((char*)bv.ptr + n_boost * row, pitch, v_self, n_q * row, n_q * row, P,
                              cudaMemcpyDeviceToDevice, st));
   return run_attention(h, p, h->impl_attend, 1, st);
 }
@@ -742,6 +739,9 @@ dscache_status dscache_step(dscache_t h, int32_t lb, int32_t lc, const void* k_f
     return run_attention(h, pa, h->impl_attend, 1, st);
   }
   // one persistent tcgen05 launch: the attend items (longest) first, then the build items
+  StreamScratch ws;
+  s = alloc_ws(pa, ws, st);
+  if (s != DSCACHE_OK) return s;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->prof) { e0 = h->take_event(); e1 = h->take_event(); cudaEventRecord(e0, st); }
   cudaError_t e = launch_tc(h, pa, &pb, st);

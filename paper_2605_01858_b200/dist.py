@@ -111,30 +111,41 @@ def context_parallel_attend(dsc, q, k_self, v_self, group=None, **kw) -> torch.T
 class PeerOutputs:
     """Gathered-O buffers of every rank, mapped into this process (P2 fused all-gather).
 
-    Each rank allocates its own [S][N][n_q][Hq][d] buffer (`local`); the CUDA IPC handles
-    (plus offsets inside the allocations) are exchanged with all_gather_object over
-    `group`, and every peer's buffer is opened on this rank's device.  `ptrs` lists the
-    device pointers in rank order (this rank's own buffer in its slot).  `ipc` = (handle,
-    open, close) functions, the library's by default (injectable for CPU tests)."""
+    Each rank allocates `nbuf` (default 2) buffers [S][N][n_q][Hq][d] of its own (`locals`);
+    the CUDA IPC handles (plus offsets inside the allocations) are exchanged with
+    all_gather_object over `group`, and every peer's buffers are opened on this rank's device.
+    `ptrs[b]` lists buffer b's device pointers in rank order (this rank's own in its slot).
+    Steps alternate buffers (kv_split_attend_fused): a step's output stays valid while the
+    next step runs, and no rank's stores of step i+1 can land in a buffer a peer is still
+    reading from step i (the write-after-read hazard of a single buffer).
+    `ipc` = (handle, open, close) functions, the library's by default (injectable for CPU tests)."""
 
-    def __init__(self, shape, dtype, device, group=None, ipc=None):
+    def __init__(self, shape, dtype, device, group=None, ipc=None, nbuf: int = 2):
         import torch.distributed as dist
         from . import dscache as D
         self.get_handle, self.open, self.close_fn = ipc or (D.ipc_handle, D.ipc_open, D.ipc_close)
         self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
         self.device = torch.device(device)
-        self.local = torch.empty(shape, dtype=dtype, device=self.device)
-        mine = self.get_handle(self.local)
+        self.group = group
+        self.locals = [torch.empty(shape, dtype=dtype, device=self.device) for _ in range(nbuf)]
+        self.step = 0
+        mine = [self.get_handle(t) for t in self.locals]
         allh = [None] * self.world
         dist.all_gather_object(allh, mine, group=group)
-        self.ptrs, self._opened = [], []
-        for r, (handle, offset) in enumerate(allh):
-            if r == self.rank:
-                self.ptrs.append(self.local.data_ptr())
-            else:
-                base = self.open(self.device.index or 0, handle)
-                self._opened.append(base)
-                self.ptrs.append(base + offset)
+        self.ptrs, self._opened = [[] for _ in range(nbuf)], []
+        for r, handles in enumerate(allh):
+            for b, (handle, offset) in enumerate(handles):
+                if r == self.rank:
+                    self.ptrs[b].append(self.locals[b].data_ptr())
+                else:
+                    base = self.open(self.device.index or 0, handle)
+                    self._opened.append(base)
+                    self.ptrs[b].append(base + offset)
+
+    @property
+    def local(self):
+        """The buffer the next step writes."""
+        return self.locals[self.step % len(self.locals)]
 
     def close(self):
         for base in self._opened:
@@ -142,13 +153,29 @@ class PeerOutputs:
         self._opened = []
 
 
+def stores_complete(group=None, device=None):
+    """Every rank's kernels enqueued so far on its current stream (including their peer
+    stores) have completed.  NCCL: a stream-ordered all_reduce of one element, no host sync
+    (it can only finish once every rank's stream has reached it); other backends: drain the
+    stream, then a host barrier."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        flag = torch.zeros(1, dtype=torch.int32, device=device)
+        dist.all_reduce(flag, group=group)
+    else:
+        torch.cuda.current_stream(device).synchronize()
+        dist.barrier(group)
+
+
 def kv_split_attend_fused(dsc, q, k_self, v_self, peers: PeerOutputs, hq_total: int, head_offset: int,
                           group=None, **kw) -> torch.Tensor:
     """P2 with the fused all-gather epilogue: this rank's heads are written by its attention
-    kernel into every rank's gathered O; after the local stream is drained and all ranks
-    pass the barrier, peers.local holds the full [S][N][n_q][Hq][d] output."""
-    import torch.distributed as dist
-    dsc.attend_peers(q, k_self, v_self, peers.ptrs, hq_total, head_offset, **kw)
-    torch.cuda.current_stream(peers.device).synchronize()
-    dist.barrier(group)
-    return peers.local
+    kernel into every rank's copy of the step's gathered O (buffer step % nbuf); once every
+    rank's stores are complete (stores_complete: stream-ordered on NCCL) it holds the full
+    [S][N][n_q][Hq][d] output.  The returned tensor stays valid until the call after next."""
+    b = peers.step % len(peers.locals)
+    out = peers.locals[b]
+    dsc.attend_peers(q, k_self, v_self, peers.ptrs[b], hq_total, head_offset, **kw)
+    stores_complete(group if group is not None else peers.group, peers.device)
+    peers.step += 1
+    return out

@@ -28,9 +28,12 @@ class HostStepPipeline:
 
         def e(*shape):
             return torch.empty(shape, dtype=dt, device=dev)
-        self.slots = [dict(k=e(S, N, tpf, Hkv, d), v=e(S, N, tpf, Hkv, d), qi=e(S, N, C, Hq, d),
+        # q_inst / O_inst are flat per slot: a step with C_t < C instant rows (warm-up) uses the
+        # first S*N*C_t*Hq*d elements as a contiguous [S][N][C_t][Hq][d] view -- no temporary
+        # is ever created outside the pipeline's own streams
+        self.slots = [dict(k=e(S, N, tpf, Hkv, d), v=e(S, N, tpf, Hkv, d), qi=e(S * N * C * Hq * d),
                            q=e(S, N, n_q, Hq, d), ks=e(S, N, n_q, Hkv, d), vs=e(S, N, n_q, Hkv, d),
-                           oi=e(S, N, C, Hq, d), o=e(S, N, n_q, Hq, d)) for _ in range(depth)]
+                           oi=e(S * N * C * Hq * d), o=e(S, N, n_q, Hq, d)) for _ in range(depth)]
         self.h2d, self.compute, self.d2h = (torch.cuda.Stream(dev) for _ in range(3))
         ev = lambda: [torch.cuda.Event() for _ in range(depth)]   # noqa: E731
         self.loaded, self.in_free, self.computed, self.out_free = ev(), ev(), ev(), ev()
@@ -44,19 +47,20 @@ class HostStepPipeline:
         s = self.i % self.depth
         b = self.slots[s]
         n_inst = hqi.shape[2]
+        S, N, _, Hq, d = hqi.shape
+        qi = b["qi"][:S * N * n_inst * Hq * d].view(S, N, n_inst, Hq, d)
+        oi = b["oi"][:S * N * n_inst * Hq * d].view(S, N, n_inst, Hq, d)
         self.h2d.wait_event(self.in_free[s])
         with torch.cuda.stream(self.h2d):
             b["k"].copy_(hk, non_blocking=True)
             b["v"].copy_(hv, non_blocking=True)
-            b["qi"][:, :, :n_inst].copy_(hqi, non_blocking=True)
+            qi.copy_(hqi, non_blocking=True)
             b["q"].copy_(hq, non_blocking=True)
             b["ks"].copy_(hks, non_blocking=True)
             b["vs"].copy_(hvs, non_blocking=True)
             self.loaded[s].record(self.h2d)
         self.compute.wait_event(self.loaded[s])
         self.compute.wait_event(self.out_free[s])
-        qi = b["qi"] if n_inst == b["qi"].shape[2] else b["qi"][:, :, :n_inst].contiguous()
-        oi = b["oi"] if n_inst == b["oi"].shape[2] else None
         self.dsc.step(b["k"], b["v"], qi, b["q"], b["ks"], b["vs"], o_inst=oi, o=b["o"], layer_begin=self.lb,
                       layer_count=self.lc, stream=self.compute)
         self.in_free[s].record(self.compute)
@@ -65,7 +69,7 @@ class HostStepPipeline:
         with torch.cuda.stream(self.d2h):
             ho.copy_(b["o"], non_blocking=True)
             if o_inst_host is not None:
-                o_inst_host.copy_(b["oi"][:, :, :n_inst], non_blocking=True)
+                o_inst_host.copy_(oi, non_blocking=True)
             self.out_free[s].record(self.d2h)
         self.i += 1
         return self.out_free[s]

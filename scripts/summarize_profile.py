@@ -1,10 +1,12 @@
 """Summarise an ncu launch list + a --set full capture into profiles/ (committed).
 
-    python scripts/summarize_profile.py TAG [config]
+    python scripts/summarize_profile.py TAG [config] [traffic key]
 
 Reads gpurun_out/launches_TAG.csv, gpurun_out/prof_TAG.ncu-rep, gpurun_out/bench_TAG.json
 and writes profiles/TAG_launches.md, profiles/TAG_ncu_full.md, profiles/TAG_bench.json and
-updates profiles/ncu_traffic.json (DRAM bytes per attention launch, read by bench.py).
+updates profiles/ncu_traffic.json (DRAM bytes per attention launch, read by bench.py) under
+the traffic key bench.traffic_key gives the profiled command (default "<config>|streams|
+fused|boost0|world1|layerseq0").
 """
 import csv
 import io
@@ -70,6 +72,7 @@ KEYS = [
 def main():
     tag = sys.argv[1]
     cfg = sys.argv[2] if len(sys.argv) > 2 else "c5"
+    tkey = sys.argv[3] if len(sys.argv) > 3 else f"{cfg}|streams|fused|boost0|world1|layerseq0"
     os.makedirs(P, exist_ok=True)
     table, agg = launches(tag)
     open(os.path.join(P, f"{tag}_launches.md"), "w").write(
@@ -78,7 +81,7 @@ def main():
         "(fill, warm-up, timed steps, e2e).  Per-launch times are cold-cache and serialised: "
         "compare shares, not absolutes.\n\n" + table + "\n")
     recs = ncu_raw(tag)
-    lines = [f"# ncu --set full of attn_tc_kernel ({tag}, {cfg})\n"]
+    lines = [f"# ncu --set full of attn_fa_kernel ({tag}, {cfg})\n"]
 
     def section(recs, title, labels):
         lines.append(f"## {title}\n")
@@ -100,7 +103,7 @@ def main():
             stalls.append(", ".join(f"{n} {100 * v / tot:.0f}%" for v, n in sorted(items, reverse=True)[:6]))
         lines.append("\nTop warp-stall reasons (pc sampling): " + " / ".join(stalls) + "\n")
 
-    section(recs, "Fused step launch (the bench's dominant kernel): `-k regex:attn_tc -s 4 -c 1`, "
+    section(recs, "Fused step launch (the bench's dominant kernel): `-k regex:attn_fa -s 4 -c 1`, "
             "one c5 step = build_instant + attend items in one persistent launch", ["fused step"])
     split_rep = os.path.join(G, f"prof_split_{tag}.ncu-rep")
     if os.path.exists(split_rep):
@@ -123,7 +126,7 @@ def main():
     per = [b(r, "dram__bytes_read.sum") + b(r, "dram__bytes_write.sum") for r in recs]
     tp = os.path.join(P, "ncu_traffic.json")
     d = json.load(open(tp)) if os.path.exists(tp) else {}
-    d[cfg] = {"attn_tc_kernel_dram_bytes_per_launch": sum(per) / len(per), "per_launch": per, "tag": tag}
+    d[tkey] = {"dram_bytes_per_launch": sum(per) / len(per), "per_launch": per, "tag": tag}
     json.dump(d, open(tp, "w"), indent=1)
     bj = os.path.join(G, f"bench_{tag}.json")
     if os.path.exists(bj):

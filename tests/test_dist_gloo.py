@@ -210,26 +210,35 @@ def test_partial_merge_single_process(n_parts):
 
 
 def _worker_peer_outputs(rank, world, port, out_q):
-    """PeerOutputs handle exchange (P2 fused all-gather) with a stand-in IPC layer: rank r's
-    handle is b"r<r>" with offset 16*r; opening it yields base 10**6*(r+1)."""
+    """PeerOutputs handle exchange (P2 fused all-gather, two buffers per rank) with a stand-in
+    IPC layer: rank r's buffer b has handle b"r<r>b<b>" with offset 16*r + b; opening it
+    yields base 10**6*(r+1) + 1000*b."""
     from paper_2605_01858_b200.dist import PeerOutputs
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    opened, closed = [], []
+    opened, closed, made = [], [], []
 
     def handle(t):
-        return b"r%d" % rank, 16 * rank
+        b = len(made)
+        made.append(t)
+        return b"r%db%d" % (rank, b), 16 * rank + b
 
     def open_(dev, hd):
         opened.append(hd)
-        return 10 ** 6 * (int(hd[1:]) + 1)
+        r, b = (int(x) for x in hd[1:].split(b"b"))
+        return 10 ** 6 * (r + 1) + 1000 * b
 
     peers = PeerOutputs((2, 3), torch.float32, "cpu", ipc=(handle, open_, lambda dev, p: closed.append(p)))
-    want = [peers.local.data_ptr() if r == rank else 10 ** 6 * (r + 1) + 16 * r for r in range(world)]
-    ok = peers.ptrs == want and sorted(opened) == sorted(b"r%d" % r for r in range(world) if r != rank)
+    ok = len(peers.locals) == 2 and peers.local is peers.locals[0]
+    for b in range(2):
+        want = [peers.locals[b].data_ptr() if r == rank else 10 ** 6 * (r + 1) + 1000 * b + 16 * r + b
+                for r in range(world)]
+        ok = ok and peers.ptrs[b] == want
+    ok = ok and sorted(opened) == sorted(b"r%db%d" % (r, b) for r in range(world) if r != rank for b in range(2))
     peers.close()
-    ok = ok and sorted(closed) == sorted(10 ** 6 * (r + 1) for r in range(world) if r != rank)
+    ok = ok and sorted(closed) == sorted(10 ** 6 * (r + 1) + 1000 * b for r in range(world) if r != rank
+                                         for b in range(2))
     out_q.put((rank, ok))
     dist.barrier()
     dist.destroy_process_group()

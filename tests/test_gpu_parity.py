@@ -596,14 +596,16 @@ def test_host_pipeline_equals_device_step(lib, name):
         C_t = min(t + 1, cfg.instant_frames) * tpf
         hk, hv, hqi = r(S, N, tpf, Hkv, d), r(S, N, tpf, Hkv, d), r(S, N, C_t, Hq, d)
         hq, hks, hvs = r(S, N, q, Hq, d), r(S, N, q, Hkv, d), r(S, N, q, Hkv, d)
-        _, o_ref = a.step(hk.to(dev), hv.to(dev), hqi.to(dev), hq.to(dev), hks.to(dev), hvs.to(dev))
+        oi_ref, o_ref = a.step(hk.to(dev), hv.to(dev), hqi.to(dev), hq.to(dev), hks.to(dev), hvs.to(dev))
         ho = torch.empty(S, N, q, Hq, d, dtype=cfg.torch_dtype).pin_memory()
-        pipe.submit(hk, hv, hqi, hq, hks, hvs, ho)
-        outs.append((o_ref, ho))
+        hoi = torch.empty(S, N, C_t, Hq, d, dtype=cfg.torch_dtype).pin_memory()
+        pipe.submit(hk, hv, hqi, hq, hks, hvs, ho, o_inst_host=hoi)
+        outs.append((o_ref, ho, oi_ref, hoi))
     pipe.synchronize()
     torch.cuda.synchronize()
-    for o_ref, ho in outs:
+    for o_ref, ho, oi_ref, hoi in outs:
         assert torch.equal(o_ref.cpu(), ho)
+        assert torch.equal(oi_ref.cpu(), hoi)   # O_inst of warm-up steps (C_t < C) included
     a.close(); b.close()
 
 

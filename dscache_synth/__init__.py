@@ -29,10 +29,12 @@ INST_Q = 4                     # instant-build queries at step t              [C
 QRY_Q, QRY_K, QRY_V = 5, 6, 7  # query chunk at step t (K/V transient)        [q][Hq|Hkv][d]
 UPD_Q = 8                      # queries of the frame leaving the buffer at t [tpf][Hq][d]
 BST_K, BST_V = 9, 10           # re-encoded (boosted) newest frame at step t  [n_boost][Hkv][d]
+IK_K, IK_V = 11, 12            # real-model mode: the step's instant K/V (Eq. 7 output) [C_t][Hkv][d]
+PST_K, PST_V = 13, 14          # real-model mode: frame f's Eq. 5 K/V (stored in U)    [tpf][Hkv][d]
 
 KIND_NAMES = {SINK_K: "SINK_K", SINK_V: "SINK_V", FRM_K: "FRM_K", FRM_V: "FRM_V",
               INST_Q: "INST_Q", QRY_Q: "QRY_Q", QRY_K: "QRY_K", QRY_V: "QRY_V", UPD_Q: "UPD_Q",
-              BST_K: "BST_K", BST_V: "BST_V"}
+              BST_K: "BST_K", BST_V: "BST_V", IK_K: "IK_K", IK_V: "IK_V", PST_K: "PST_K", PST_V: "PST_V"}
 
 
 @dataclasses.dataclass(frozen=True)
@@ -116,6 +118,20 @@ def boost_kv(cfg: StreamConfig, stream: int, layer: int, step: int, n_boost: int
     """Raw K/V of the newest frame re-encoded at a higher resolution (n_boost tokens)."""
     shp = (n_boost, cfg.num_kv_heads, cfg.head_dim)
     return draw(cfg, stream, layer, BST_K, step, shp), draw(cfg, stream, layer, BST_V, step, shp)
+
+
+def instant_kv(cfg: StreamConfig, stream: int, layer: int, step: int, n_inst: int):
+    """Real-model mode: the K/V the caller's Eq. 7 build produced for the step's C_t instant
+    tokens (fresh every step: the instant cache is rebuilt per step)."""
+    shp = (n_inst, cfg.num_kv_heads, cfg.head_dim)
+    return draw(cfg, stream, layer, IK_K, step, shp), draw(cfg, stream, layer, IK_V, step, shp)
+
+
+def past_kv(cfg: StreamConfig, stream: int, layer: int, frame: int):
+    """Real-model mode: frame f's K/V from its Eq. 5 update (stored in U when it leaves the
+    buffer); distinct from any instant K/V of the same frame."""
+    shp = (cfg.tokens_per_frame, cfg.num_kv_heads, cfg.head_dim)
+    return draw(cfg, stream, layer, PST_K, frame, shp), draw(cfg, stream, layer, PST_V, frame, shp)
 
 
 def batch_boost_kv(cfg: StreamConfig, step: int, n_boost: int, streams=None, layers=None):

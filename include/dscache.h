@@ -61,6 +61,12 @@ typedef enum {
 enum { DSCACHE_DTYPE_BF16 = 0, DSCACHE_DTYPE_FP32 = 1 };
 enum { DSCACHE_ROPE_SPLIT_HALF = 0,   /* pairs (i, i+d/2): Qwen2 / LLaVA-OV-7B (reading Q7, default) */
        DSCACHE_ROPE_ADJACENT = 1 };   /* pairs (2i, 2i+1)                                            */
+enum { DSCACHE_INSTANT_RING = 0,     /* synthetic phi: a frame's K/V enter the ring on arrival and serve
+                                        as its instant K/V for l_I steps, then as past (reading Q2)   */
+       DSCACHE_INSTANT_EXTERNAL = 1 }; /* real-model mode: the instant segment's K/V
+                                        are the caller's Eq. 7 output for this step; a frame enters
+                                        the ring only when it leaves the buffer, with the K/V of its
+                                        Eq. 5 update (dscache_append_past)                          */
 enum { DSCACHE_IMPL_AUTO = 0,         /* tcgen05 kernel when eligible, else the SIMT kernel          */
        DSCACHE_IMPL_TC = 1,           /* force tcgen05 (E_CONFIG unless bf16, d=128, split-half RoPE)    */
        DSCACHE_IMPL_SIMT = 2 };       /* force the fp32 CUDA-core kernel                             */
@@ -86,6 +92,7 @@ typedef struct {
   int32_t dtype;            /* DSCACHE_DTYPE_*                                                     */
   int32_t device;           /* CUDA device ordinal the handle lives on                             */
   int32_t attn_impl;        /* DSCACHE_IMPL_*                                                      */
+  int32_t instant_source;   /* DSCACHE_INSTANT_RING (default) or DSCACHE_INSTANT_EXTERNAL          */
 } dscache_config;
 
 typedef struct {
@@ -99,6 +106,9 @@ typedef struct {
   int32_t instant_slot;        /* ring slot of the oldest instant token                            */
   int32_t max_key_id;          /* largest context key id of attend: A + P_t + C_t - 1              */
   int32_t max_query_id;        /* largest query id of attend with n_q = q_max                      */
+  int32_t next_instant_tokens; /* C_{t+1}: instant tokens after the next frame (q_inst rows of the
+                                  next dscache_step)                                                */
+  int32_t instant_capacity;    /* C = l_I * tpf (the largest C_t)                                   */
 } dscache_state;
 
 /* Create a handle: validates the configuration, allocates the ring
@@ -203,6 +213,41 @@ dscache_status dscache_attend_boost(dscache_t h, int32_t layer_begin, int32_t la
                                     const void* q, const void* k_self, const void* v_self, int32_t n_q,
                                     const void* k_boost, const void* v_boost, int32_t n_boost, void* o,
                                     void* stream);
+
+/* Real-model mode (config.instant_source = DSCACHE_INSTANT_EXTERNAL).
+ * The instant cache I = phi(B, C_a) of Eq. 7 is new K/V for the buffer's
+ * tokens built from a sink-only context, and the frame leaving the buffer gets yet another
+ * K/V from the cumulative update phi(X_{t-l_I}, [C_a, zeta(U_{t-1})]) of Eq. 5
+ * -- the same frame has different instant and past K/V.  In this mode:
+ *
+ * dscache_append_past: advances the layer range to step t (frame t arrived) and, once
+ * t >= l_I, stores the Eq. 5 K/V of the frame leaving the buffer (frame t - l_I) into its
+ * ring slots ((f*tpf + j) mod R, as the raw frames of the default mode); eviction and
+ * position ids follow the same closed form (P_t, C_t).  k_past, v_past:
+ * [S][layer_count][n_tokens][Hkv][d], n_tokens = tpf when t >= l_I, else 0 (pointers may be
+ * NULL).  The first call of a layer with A > 0 must instead be dscache_append_frame with the
+ * sink.  dscache_update_attend then runs the Eq. 5 attention of that frame over [sink |
+ * zeta(U_{t-1}) | its own K/V just stored].  E_ARG for a wrong n_tokens, E_CONFIG in the
+ * default mode. */
+dscache_status dscache_append_past(dscache_t h, int32_t layer_begin, int32_t layer_count, const void* k_past,
+                                   const void* v_past, int32_t n_tokens, void* stream);
+
+/* Eq. 7 with the caller's instant K/V: the C_t instant tokens attend causally over
+ * [sink | k_inst] with ids 0.., query i at A + i.
+ *   q_inst, o_inst : [S][layer_count][C_t][Hq][d];  k_inst, v_inst : [S][layer_count][C_t][Hkv][d]
+ * (raw, un-rotated).  E_CONFIG in the default mode, E_STATE before the sink and first step. */
+dscache_status dscache_build_instant_ext(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                                         const void* q_inst, const void* k_inst, const void* v_inst, void* o_inst,
+                                         void* stream);
+
+/* Eq. 8 with the caller's instant K/V: the query chunk over [sink | past (ring, P_t) | k_inst
+ * (C_t) | self (n_q)], ids contiguous from 0, query i at A + P_t + C_t + i, causal inside the
+ * chunk.  Layouts as dscache_attend plus k_inst / v_inst as dscache_build_instant_ext; the
+ * [instant | self] keys are gathered into per-call stream-ordered scratch.  E_CONFIG in the
+ * default mode; otherwise errors as dscache_attend. */
+dscache_status dscache_attend_ext(dscache_t h, int32_t layer_begin, int32_t layer_count, const void* q,
+                                  const void* k_self, const void* v_self, int32_t n_q, const void* k_inst,
+                                  const void* v_inst, void* o, void* stream);
 
 /* Attention of an n_q-token query chunk over [C_a | U | I | self] (Eq. 8 plus the
  * chunk's own K/V, which are used and then discarded: PAPER.md:212/699).  Ids:

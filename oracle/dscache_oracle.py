@@ -19,6 +19,9 @@ What it computes (per stream s, per layer r; everything in float64):
   Eq. 2 PAPER.md:141-146);
 * the resolution-boosted newest frame: the instant cache
   and the final attention with the buffer's newest input re-encoded (SURVEY NEXT-4);
+* the real-model mode: Eq. 7 / Eq. 8 with the step's instant K/V supplied
+  by the caller and U holding each frame's Eq. 5 K/V (instant_cache_output_ext,
+  attend_output_ext; the Eq. 5 attention is cumulative_update_output over those K/V);
 * decoding over C_{t+1}: the last tokens of [query chunk | generated
   tokens] attend over [C_a, U, I, self] (SURVEY NEXT-2);
 * the cumulative-update attention inside phi(X_{t-l_I}, [C_a, zeta(U_{t-1})]) of
@@ -265,6 +268,37 @@ def attend_output_boosted(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarra
     frames = list(sched.past_frames) + list(sched.instant_frames)[:-1]
     ks = _cat([sk] + [frame_kv(f)[0] for f in frames] + [k_boost, k_self], hkv, d)
     vs = _cat([sv] + [frame_kv(f)[1] for f in frames] + [v_boost, v_self], hkv, d)
+    L_ctx = ks.shape[0] - q.shape[0]
+    pos_k = np.arange(ks.shape[0])
+    pos_q = L_ctx + np.arange(q.shape[0])
+    return gqa_attention(np.asarray(q, np.float64), pos_q, ks, vs, pos_k, theta, style)
+
+
+def instant_cache_output_ext(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], k_inst: np.ndarray,
+                             v_inst: np.ndarray, q_inst: np.ndarray, theta: float, style: int = SPLIT_HALF) -> np.ndarray:
+    """Eq. 7 in the real-model mode: I = phi(B_t, C_a) where the buffer tokens'
+    K/V are the caller's (k_inst, v_inst [C_t, Hkv, d], the step's instant K/V).
+    Context [C_a | instant tokens] with ids 0..; query i at A + i, causal."""
+    sk, sv = sink
+    hkv, d = sk.shape[1], sk.shape[2]
+    ks = _cat([sk, k_inst], hkv, d)
+    vs = _cat([sv, v_inst], hkv, d)
+    pos_k = np.arange(ks.shape[0])
+    pos_q = sk.shape[0] + np.arange(q_inst.shape[0])
+    return gqa_attention(np.asarray(q_inst, np.float64), pos_q, ks, vs, pos_k, theta, style)
+
+
+def attend_output_ext(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], past_kv: FrameFn,
+                      k_inst: np.ndarray, v_inst: np.ndarray, q: np.ndarray, k_self: np.ndarray, v_self: np.ndarray,
+                      theta: float, style: int = SPLIT_HALF) -> np.ndarray:
+    """Eq. 8 in the real-model mode: C_t = [C_a, U_t, I_t] where U_t's frames
+    carry the K/V of their Eq. 5 update (past_kv(f)) and I_t is the step's
+    instant K/V (k_inst, v_inst) -- a frame in the instant window is NOT read from U.
+    Plus the query chunk's own K/V; ids contiguous from 0, queries causal inside the chunk."""
+    sk, sv = sink
+    hkv, d = sk.shape[1], sk.shape[2]
+    ks = _cat([sk] + [past_kv(f)[0] for f in sched.past_frames] + [k_inst, k_self], hkv, d)
+    vs = _cat([sv] + [past_kv(f)[1] for f in sched.past_frames] + [v_inst, v_self], hkv, d)
     L_ctx = ks.shape[0] - q.shape[0]
     pos_k = np.arange(ks.shape[0])
     pos_q = L_ctx + np.arange(q.shape[0])

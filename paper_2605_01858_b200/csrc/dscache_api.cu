@@ -141,6 +141,16 @@ dscache_status check_layers(dscache_t h, int lb, int lc) {
   return DSCACHE_OK;
 }
 
+dscache_status need_mode(dscache_t h, int mode, const char* what) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  if (h->cfg.instant_source != mode)
+    return fail(DSCACHE_E_CONFIG, std::string(what) + (mode == DSCACHE_INSTANT_EXTERNAL
+                                                           ? " needs instant_source = DSCACHE_INSTANT_EXTERNAL"
+                                                           : " reads the ring's instant frames: not in the "
+                                                             "external-instant (real-model) mode"));
+  return DSCACHE_OK;
+}
+
 bool tc_eligible(const dscache_config& c) {
   return c.dtype == DSCACHE_DTYPE_BF16 && c.head_dim == 128 && c.rope_style == DSCACHE_ROPE_SPLIT_HALF;
 }
@@ -236,6 +246,8 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   if (c.dtype != DSCACHE_DTYPE_BF16 && c.dtype != DSCACHE_DTYPE_FP32) return fail(DSCACHE_E_CONFIG, "dtype");
   if (c.rope_style != DSCACHE_ROPE_SPLIT_HALF && c.rope_style != DSCACHE_ROPE_ADJACENT)
     return fail(DSCACHE_E_CONFIG, "rope_style");
+  if (c.instant_source != DSCACHE_INSTANT_RING && c.instant_source != DSCACHE_INSTANT_EXTERNAL)
+    return fail(DSCACHE_E_CONFIG, "instant_source");
   if (!(c.rope_theta > 1.0)) return fail(DSCACHE_E_CONFIG, "rope_theta must be > 1");
   const int64_t W = (int64_t)c.past_frames * c.tokens_per_frame, C = (int64_t)c.instant_frames * c.tokens_per_frame;
   // largest id any attention applies: attend A+W+C+q_max-1, update attention (Eq. 5) A+W+tpf-1
@@ -352,6 +364,8 @@ dscache_status dscache_append_frame(dscache_t h, int32_t lb, int32_t lc, const v
     for (int l = lb; l < lb + lc; ++l) h->sink_filled[l] = 1;
     return DSCACHE_OK;
   }
+  if (c.instant_source != DSCACHE_INSTANT_RING)
+    return fail(DSCACHE_E_CONFIG, "external-instant (real-model) mode: frames enter the ring via dscache_append_past");
   if (n_tokens != c.tokens_per_frame)
     return fail(DSCACHE_E_ARG, "frame append must carry tokens_per_frame = " + std::to_string(c.tokens_per_frame) +
                                    " tokens, got " + std::to_string(n_tokens));
@@ -412,6 +426,7 @@ dscache_status prep_build(dscache_t h, int32_t lb, int32_t lc, const void* q_ins
 
 dscache_status dscache_build_instant(dscache_t h, int32_t lb, int32_t lc, const void* q_inst, void* o_inst,
                                      void* stream) {
+  if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "build_instant");
   dsc::AttnParams p{};
   dsc::StageParams sp{};
   bool empty = false;
@@ -427,6 +442,7 @@ dscache_status dscache_build_instant(dscache_t h, int32_t lb, int32_t lc, const 
 
 dscache_status dscache_build_instant_newest(dscache_t h, int32_t lb, int32_t lc, const void* q_new, void* o_new,
                                             void* stream) {
+  if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "build_instant_newest");
   dscache_status s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
   if (!h->sink_filled[lb] || h->frames[lb] < 1)
@@ -505,6 +521,7 @@ dscache_status attend_common(dscache_t h, int32_t lb, int32_t lc, const void* q,
 
 dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                               const void* v_self, int32_t n_q, void* o, void* stream) {
+  if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "attend");
   if (h && (n_q < 1 || n_q > h->cfg.max_query_tokens))
     return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
   return attend_common(h, lb, lc, q, k_self, v_self, n_q, n_q, o, stream, true);
@@ -512,40 +529,37 @@ dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q
 
 dscache_status dscache_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                               const void* v_self, int32_t n_self, int32_t n_q, void* o, void* stream) {
+  if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "decode");
   return attend_common(h, lb, lc, q, k_self, v_self, n_self, n_q, o, stream, false);
 }
 
-dscache_status dscache_build_instant_boost(dscache_t h, int32_t lb, int32_t lc, const void* q_inst,
-                                           const void* k_boost, const void* v_boost, int32_t n_boost, void* o_inst,
-                                           void* stream) {
-  dscache_status s = check_layers(h, lb, lc);
-  if (s != DSCACHE_OK) return s;
-  if (!h->sink_filled[lb] || h->frames[lb] < 1)
-    return fail(DSCACHE_E_STATE, "build_instant_boost before the sink and the first frame were appended");
-  if (h->cfg.instant_frames < 1) return fail(DSCACHE_E_CONFIG, "l_I = 0: there is no instant cache");
-  if (!q_inst || !k_boost || !v_boost || !o_inst) return fail(DSCACHE_E_ARG, "null q_inst/k_boost/v_boost/o_inst");
-  if (n_boost < 1) return fail(DSCACHE_E_ARG, "n_boost must be >= 1");
+namespace {
+// Eq. 7 over [sink | ring_older instant tokens of the ring (from the oldest instant slot) |
+// n_inst caller tokens (k_inst, v_inst: [S][lc][n_inst][Hkv][d])]: the ring_older + n_inst
+// queries at ids A + i, causal.  Serves the resolution boost (ring_older = C_t - tpf: the
+// newest frame re-encoded) and the real-model mode (ring_older = 0: every instant K/V from
+// the caller).
+dscache_status build_with_inst(dscache_t h, int32_t lb, int32_t lc, const void* q_inst, const void* k_inst,
+                               const void* v_inst, int32_t n_inst, int ring_older, void* o_inst, cudaStream_t st) {
   const Schedule sc = h->schedule(lb);
-  const int older = sc.C_t - h->cfg.tokens_per_frame;   // instant tokens before the newest frame
-  if ((int64_t)h->cfg.sink_tokens + older + n_boost > h->cfg.max_position)
-    return fail(DSCACHE_E_POS_OVERFLOW, "A + C_t - tpf + n_boost exceeds max_position");
+  if ((int64_t)h->cfg.sink_tokens + ring_older + n_inst > h->cfg.max_position)
+    return fail(DSCACHE_E_POS_OVERFLOW, "A + instant tokens exceeds max_position");
   DeviceGuard dg(h->cfg.device);
-  // keys: sink | ring window of the older instant frames | boosted frame as the self
-  // segment (ids A + older + j); queries: ids A + i over [older | boosted]
+  // keys: sink | ring window of the older instant frames | caller tokens as the self
+  // segment (ids A + ring_older + j); queries: ids A + i over [older | caller tokens]
   dsc::AttnParams p{};
   fill_common(h, p, lb, lc);
-  p.q = q_inst; p.o = o_inst; p.n_q = older + n_boost; p.q_pos0 = h->cfg.sink_tokens;
-  p.ring_start = sc.inst_start; p.ring_count = older;
-  p.self_k = k_boost; p.self_v = v_boost; p.n_self = n_boost;
+  p.q = q_inst; p.o = o_inst; p.n_q = ring_older + n_inst; p.q_pos0 = h->cfg.sink_tokens;
+  p.ring_start = sc.inst_start; p.ring_count = ring_older;
+  p.self_k = k_inst; p.self_v = v_inst; p.n_self = n_inst;
   p.dbg_pos = nullptr;
   p.n_mblocks = (p.n_q * p.grp + 2 * dsc::kTileM - 1) / (2 * dsc::kTileM);
-  cudaStream_t st = (cudaStream_t)stream;
   const long long build_items = (long long)p.P * p.Hkv * p.n_mblocks;
   if (h->impl_build == DSCACHE_IMPL_TC && build_items >= 2LL * h->num_sms) {
-    // staged as the plain build: [sink | older instant | boosted frame] once per (stream,
-    // layer, kv head), K rotated at ids 0.., read by TMA (the boosted frame otherwise goes
+    // staged as the plain build: [sink | older instant | caller tokens] once per (stream,
+    // layer, kv head), K rotated at ids 0.., read by TMA (the caller tokens otherwise go
     // through the per-item sink/self loads)
-    const int rows = h->cfg.sink_tokens + older + n_boost;
+    const int rows = h->cfg.sink_tokens + ring_older + n_inst;
     if (rows > h->bstage_rows) {
       cudaFree(h->bstage_k); cudaFree(h->bstage_v);
       h->bstage_k = h->bstage_v = nullptr; h->bstage_rows = 0;
@@ -553,7 +567,7 @@ dscache_status dscache_build_instant_boost(dscache_t h, int32_t lb, int32_t lc, 
       const size_t sb = heads * rows * h->cfg.head_dim * h->elem;
       if (cudaMalloc(&h->bstage_k, sb) != cudaSuccess || cudaMalloc(&h->bstage_v, sb) != cudaSuccess) {
         cudaGetLastError();
-        return fail(DSCACHE_E_OOM, "boost staging allocation failed");
+        return fail(DSCACHE_E_OOM, "instant staging allocation failed");
       }
       DSC_CUDA(dsc::make_kv_tmap(&h->tmap_bk, h->bstage_k, (unsigned long long)heads * rows, dsc::kTileN));
       DSC_CUDA(dsc::make_kv_tmap(&h->tmap_bv, h->bstage_v, (unsigned long long)heads * rows, dsc::kTileN));
@@ -565,7 +579,7 @@ dscache_status dscache_build_instant_boost(dscache_t h, int32_t lb, int32_t lc, 
     sp.S = p.S; sp.layer_count = lc; sp.layer_begin = lb; sp.N_total = p.N_total; sp.Hkv = p.Hkv;
     sp.A = p.A; sp.R = h->R; sp.Rp_ring = h->Rp; sp.inst_start = sc.inst_start;
     sp.rows = rows; sp.rows_stage = h->bstage_rows;
-    sp.boost_k = k_boost; sp.boost_v = v_boost; sp.n_older = older;
+    sp.boost_k = k_inst; sp.boost_v = v_inst; sp.n_older = ring_older;
     DSC_CUDA(dsc::launch_stage_instant(sp, st));
     h->launches++;
     p.staged = 1;
@@ -576,42 +590,130 @@ dscache_status dscache_build_instant_boost(dscache_t h, int32_t lb, int32_t lc, 
   return run_attention(h, p, h->impl_build, 0, st);
 }
 
+// Eq. 8 over [sink | ring window minus its newest ring_drop tokens | n_inst caller tokens |
+// self (n_q)]: the [caller tokens | self] keys are gathered into per-call stream-ordered
+// scratch [P][n_inst + n_q][Hkv][d] and passed as the self segment.
+dscache_status attend_with_inst(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                                const void* v_self, int32_t n_q, const void* k_inst, const void* v_inst,
+                                int32_t n_inst, int ring_drop, void* o, cudaStream_t st) {
+  const dscache_config& c = h->cfg;
+  const size_t row = (size_t)c.num_kv_heads * c.head_dim * h->elem;      // one token of one problem
+  const size_t P = (size_t)c.num_streams * lc;
+  const size_t need = P * (size_t)(n_inst + n_q) * row;
+  DeviceGuard dg(c.device);
+  StreamScratch bk, bv;
+  if (!bk.alloc(need, st) || !bv.alloc(need, st)) return fail(DSCACHE_E_OOM, "instant gather scratch allocation failed");
+  dsc::AttnParams p{};
+  dscache_status s = prep_attend(h, lb, lc, q, bk.ptr, bv.ptr, n_inst + n_q, n_q, o, false, p, ring_drop);
+  if (s != DSCACHE_OK) return s;
+  // self segment [caller tokens | query chunk] per problem: [P][n_inst + n_q][Hkv][d]
+  const size_t pitch = (size_t)(n_inst + n_q) * row;
+  DSC_CUDA(cudaMemcpy2DAsync(bk.ptr, pitch, k_inst, n_inst * row, n_inst * row, P, cudaMemcpyDeviceToDevice, st));
+  DSC_CUDA(cudaMemcpy2DAsync(bv.ptr, pitch, v_inst, n_inst * row, n_inst * row, P, cudaMemcpyDeviceToDevice, st));
+  DSC_CUDA(cudaMemcpy2DAsync((char*)bk.ptr + n_inst * row, pitch, k_self, n_q * row, n_q * row, P,
+                             cudaMemcpyDeviceToDevice, st));
+  DSC_CUDA(cudaMemcpy2DAsync((char*)bv.ptr + n_inst * row, pitch, v_self, n_q * row, n_q * row, P,
+                             cudaMemcpyDeviceToDevice, st));
+  return run_attention(h, p, h->impl_attend, 1, st);
+}
+
+}  // namespace
+
+dscache_status dscache_build_instant_boost(dscache_t h, int32_t lb, int32_t lc, const void* q_inst,
+                                           const void* k_boost, const void* v_boost, int32_t n_boost, void* o_inst,
+                                           void* stream) {
+  dscache_status s = need_mode(h, DSCACHE_INSTANT_RING, "build_instant_boost");
+  if (s == DSCACHE_OK) s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  if (!h->sink_filled[lb] || h->frames[lb] < 1)
+    return fail(DSCACHE_E_STATE, "build_instant_boost before the sink and the first frame were appended");
+  if (h->cfg.instant_frames < 1) return fail(DSCACHE_E_CONFIG, "l_I = 0: there is no instant cache");
+  if (!q_inst || !k_boost || !v_boost || !o_inst) return fail(DSCACHE_E_ARG, "null q_inst/k_boost/v_boost/o_inst");
+  if (n_boost < 1) return fail(DSCACHE_E_ARG, "n_boost must be >= 1");
+  const int older = h->schedule(lb).C_t - h->cfg.tokens_per_frame;   // instant tokens before the newest frame
+  return build_with_inst(h, lb, lc, q_inst, k_boost, v_boost, n_boost, older, o_inst, (cudaStream_t)stream);
+}
+
 dscache_status dscache_attend_boost(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                                     const void* v_self, int32_t n_q, const void* k_boost, const void* v_boost,
                                     int32_t n_boost, void* o, void* stream) {
-  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  dscache_status s = need_mode(h, DSCACHE_INSTANT_RING, "attend_boost");
+  if (s != DSCACHE_OK) return s;
   if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
   if (h->cfg.instant_frames < 1) return fail(DSCACHE_E_CONFIG, "l_I = 0: there is no instant frame to boost");
   if (!k_boost || !v_boost || !k_self || !v_self) return fail(DSCACHE_E_ARG, "null k/v pointers");
   if (n_boost < 1) return fail(DSCACHE_E_ARG, "n_boost must be >= 1");
-  dscache_status s = check_layers(h, lb, lc);
+  s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
+  return attend_with_inst(h, lb, lc, q, k_self, v_self, n_q, k_boost, v_boost, n_boost, h->cfg.tokens_per_frame, o,
+                          (cudaStream_t)stream);
+}
+
+dscache_status dscache_append_past(dscache_t h, int32_t lb, int32_t lc, const void* k, const void* v,
+                                   int32_t n_tokens, void* stream) {
+  dscache_status s = need_mode(h, DSCACHE_INSTANT_EXTERNAL, "append_past");
+  if (s == DSCACHE_OK) s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  if (!h->sink_filled[lb]) return fail(DSCACHE_E_STATE, "append_past before the sink was appended");
   const dscache_config& c = h->cfg;
-  const size_t row = (size_t)c.num_kv_heads * c.head_dim * h->elem;      // one token of one problem
-  const size_t P = (size_t)c.num_streams * lc;
-  const size_t need = P * (size_t)(n_boost + n_q) * row;
+  const int64_t t = h->frames[lb];                  // the step this call advances to
+  const int64_t leave = t - c.instant_frames;       // frame leaving the buffer at step t (Eq. 3)
+  const int need = leave >= 0 ? c.tokens_per_frame : 0;
+  if (n_tokens != need)
+    return fail(DSCACHE_E_ARG, "append_past at step " + std::to_string(t) + " must carry " + std::to_string(need) +
+                                   " tokens (the Eq. 5 K/V of frame t - l_I), got " + std::to_string(n_tokens));
   DeviceGuard dg(c.device);
-  cudaStream_t st = (cudaStream_t)stream;
-  // per-call gather buffers, stream-ordered (no scratch shared between calls)
-  StreamScratch bk, bv;
-  if (!bk.alloc(need, st) || !bv.alloc(need, st)) return fail(DSCACHE_E_OOM, "boost scratch allocation failed");
-  dsc::AttnParams p{};
-  s = prep_attend(h, lb, lc, q, bk.ptr, bv.ptr, n_boost + n_q, n_q, o, false, p, c.tokens_per_frame);
+  if (need > 0) {
+    if (!k || !v) return fail(DSCACHE_E_ARG, "null k_past/v_past");
+    dsc::AppendParams p{};
+    p.k = k; p.v = v;
+    p.S = c.num_streams; p.layer_count = lc; p.layer_begin = lb; p.N_total = c.num_layers; p.Hkv = c.num_kv_heads;
+    p.row_bytes = c.head_dim * h->elem; p.elem_bytes = h->elem; p.n = n_tokens; p.poison_slot0 = -1;
+    p.dst_k = h->ring_k; p.dst_v = h->ring_v; p.rows_dst = h->Rp; p.mirror_R = h->R;
+    p.slot0 = (int)((leave * c.tokens_per_frame) % h->R);
+    const int64_t ev = t - c.instant_frames - c.past_frames;   // Eq. 6: same closed form
+    if (h->poison && ev >= 0) p.poison_slot0 = (int)((ev * c.tokens_per_frame) % h->R);
+    DSC_CUDA(dsc::launch_append(p, (cudaStream_t)stream));
+    h->launches++;
+  }
+  const int64_t ev = t - c.instant_frames - c.past_frames;
+  for (int l = lb; l < lb + lc; ++l) { h->frames[l] = t + 1; h->last_evicted[l] = ev >= 0 ? ev : -1; }
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_build_instant_ext(dscache_t h, int32_t lb, int32_t lc, const void* q_inst, const void* k_inst,
+                                         const void* v_inst, void* o_inst, void* stream) {
+  dscache_status s = need_mode(h, DSCACHE_INSTANT_EXTERNAL, "build_instant_ext");
+  if (s == DSCACHE_OK) s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
-  // self segment [boosted frame | query chunk] per problem: [P][n_boost + n_q][Hkv][d]
-  const size_t pitch = (size_t)(n_boost + n_q) * row;
-  DSC_CUDA(cudaMemcpy2DAsync(bk.ptr, pitch, k_boost, n_boost * row, n_boost * row, P, cudaMemcpyDeviceToDevice, st));
-  DSC_CUDA(cudaMemcpy2DAsync(bv.ptr, pitch, v_boost, n_boost * row, n_boost * row, P, cudaMemcpyDeviceToDevice, st));
-  DSC_CUDA(cudaMemcpy2DAsync((char*)bk.ptr + n_boost * row, pitch, k_self, n_q * row, n_q * row, P,
-                             cudaMemcpyDeviceToDevice, st));
-  DSC_CUDA(cudaMemcpy2DAsync((char*)bv.ptr + n_boost * row, pitch, v_self, n_q * row, n_q * row, P,
-                             cudaMemcpyDeviceToDevice, st));
-  return run_attention(h, p, h->impl_attend, 1, st);
+  if (!h->sink_filled[lb] || h->frames[lb] < 1)
+    return fail(DSCACHE_E_STATE, "build_instant_ext before the sink and the first step");
+  const int C_t = h->schedule(lb).C_t;
+  if (C_t == 0) return DSCACHE_OK;                  // l_I = 0: no instant cache
+  if (!q_inst || !k_inst || !v_inst || !o_inst) return fail(DSCACHE_E_ARG, "null q_inst/k_inst/v_inst/o_inst");
+  return build_with_inst(h, lb, lc, q_inst, k_inst, v_inst, C_t, 0, o_inst, (cudaStream_t)stream);
+}
+
+dscache_status dscache_attend_ext(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                                  const void* v_self, int32_t n_q, const void* k_inst, const void* v_inst, void* o,
+                                  void* stream) {
+  dscache_status s = need_mode(h, DSCACHE_INSTANT_EXTERNAL, "attend_ext");
+  if (s != DSCACHE_OK) return s;
+  if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
+  s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  if (!h->sink_filled[lb] || h->frames[lb] < 1) return fail(DSCACHE_E_STATE, "attend_ext before the sink and the first step");
+  if (!k_self || !v_self) return fail(DSCACHE_E_ARG, "null k_self/v_self");
+  const int C_t = h->schedule(lb).C_t;
+  if (C_t > 0 && (!k_inst || !v_inst)) return fail(DSCACHE_E_ARG, "null k_inst/v_inst");
+  // the ring holds only past frames in this mode: its window minus the C_t instant tokens
+  return attend_with_inst(h, lb, lc, q, k_self, v_self, n_q, k_inst, v_inst, C_t, C_t, o, (cudaStream_t)stream);
 }
 
 dscache_status dscache_attend_partial(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                                       const void* v_self, int32_t n_q, int32_t part, int32_t n_parts, float* o_part,
                                       float* lse_part, void* stream) {
+  if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "attend_partial");
   if (!h) return fail(DSCACHE_E_ARG, "null handle");
   if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
   if (n_parts < 1 || part < 0 || part >= n_parts) return fail(DSCACHE_E_ARG, "need 0 <= part < n_parts");
@@ -638,6 +740,7 @@ dscache_status dscache_attend_partial(dscache_t h, int32_t lb, int32_t lc, const
 dscache_status dscache_attend_peers(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                                     const void* v_self, int32_t n_q, void* const* peer_o, int32_t n_peers,
                                     int32_t hq_total, int32_t head_offset, void* stream) {
+  if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "attend_peers");
   if (!h) return fail(DSCACHE_E_ARG, "null handle");
   if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
   if (!peer_o || n_peers < 1 || n_peers > dsc::kMaxPeers)
@@ -711,6 +814,7 @@ dscache_status dscache_combine_partials(dscache_t h, int32_t n_parts, int64_t ro
 dscache_status dscache_step(dscache_t h, int32_t lb, int32_t lc, const void* k_frame, const void* v_frame,
                             const void* q_inst, void* o_inst, const void* q, const void* k_self, const void* v_self,
                             int32_t n_q, void* o, void* stream) {
+  if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "step");
   if (!h) return fail(DSCACHE_E_ARG, "null handle");
   if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
   dscache_status cs = check_layers(h, lb, lc);
@@ -796,6 +900,9 @@ dscache_status dscache_get_state(dscache_t h, int32_t layer, dscache_state* out)
     st.tail_slot = sc.ring_start; st.instant_slot = sc.inst_start;
   }
   st.max_key_id = h->cfg.sink_tokens + st.past_tokens + st.instant_tokens - 1;
+  st.next_instant_tokens =
+      (int32_t)(std::min<int64_t>(h->frames[layer] + 1, h->cfg.instant_frames) * h->cfg.tokens_per_frame);
+  st.instant_capacity = h->C;
   st.max_query_id = st.max_key_id + h->cfg.max_query_tokens;
   *out = st;
   return DSCACHE_OK;

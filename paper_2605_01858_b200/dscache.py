@@ -22,6 +22,7 @@ STATUS_NAMES = {0: "OK", -1: "E_ARG", -2: "E_CONFIG", -3: "E_POS_OVERFLOW", -4: 
 DTYPE_BF16, DTYPE_FP32 = 0, 1
 ROPE_SPLIT_HALF, ROPE_ADJACENT = 0, 1
 IMPL_AUTO, IMPL_TC, IMPL_SIMT = 0, 1, 2
+INSTANT_RING, INSTANT_EXTERNAL = 0, 1
 
 
 class DSCacheError(RuntimeError):
@@ -38,7 +39,8 @@ class Config(ctypes.Structure):
                 ("past_frames", ctypes.c_int32), ("instant_frames", ctypes.c_int32),
                 ("max_query_tokens", ctypes.c_int32), ("max_position", ctypes.c_int32),
                 ("rope_theta", ctypes.c_double), ("rope_style", ctypes.c_int32),
-                ("dtype", ctypes.c_int32), ("device", ctypes.c_int32), ("attn_impl", ctypes.c_int32)]
+                ("dtype", ctypes.c_int32), ("device", ctypes.c_int32), ("attn_impl", ctypes.c_int32),
+                ("instant_source", ctypes.c_int32)]
 
 
 class State(ctypes.Structure):
@@ -46,13 +48,15 @@ class State(ctypes.Structure):
                 ("sink_filled", ctypes.c_int32), ("past_tokens", ctypes.c_int32),
                 ("instant_tokens", ctypes.c_int32), ("ring_slots", ctypes.c_int32),
                 ("tail_slot", ctypes.c_int32), ("instant_slot", ctypes.c_int32),
-                ("max_key_id", ctypes.c_int32), ("max_query_id", ctypes.c_int32)]
+                ("max_key_id", ctypes.c_int32), ("max_query_id", ctypes.c_int32),
+                ("next_instant_tokens", ctypes.c_int32), ("instant_capacity", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
+           "dscache_append_past", "dscache_build_instant_ext", "dscache_attend_ext",
            "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
            "dscache_attn_impl", "dscache_watchdog_read", "dscache_last_error", "dscache_attend_partial", "dscache_combine_partials",
@@ -97,6 +101,9 @@ def load_library(path: str = LIB_PATH):
         "dscache_combine_partials": ([P, I32, I64, P, P, P, P], I32),
         "dscache_build_instant_boost": ([P, I32, I32, P, P, P, I32, P, P], I32),
         "dscache_attend_boost": ([P, I32, I32, P, P, P, I32, P, P, I32, P, P], I32),
+        "dscache_append_past": ([P, I32, I32, P, P, I32, P], I32),
+        "dscache_build_instant_ext": ([P, I32, I32, P, P, P, P, P], I32),
+        "dscache_attend_ext": ([P, I32, I32, P, P, P, I32, P, P, P, P], I32),
         "dscache_attend_peers": ([P, I32, I32, P, P, P, I32, ctypes.POINTER(P), I32, I32, I32, P], I32),
         "dscache_ipc_handle": ([P, P, ctypes.POINTER(I64)], I32),
         "dscache_ipc_open": ([I32, P, ctypes.POINTER(P)], I32),
@@ -156,18 +163,19 @@ class DSCache:
                  head_dim: int, tokens_per_frame: int, sink_tokens: int, past_frames: int,
                  instant_frames: int, max_query_tokens: int, rope_theta: float,
                  max_position: int = 32768, dtype: str = "bf16", rope_style: int = ROPE_SPLIT_HALF,
-                 device: int = 0, kv_head_offset: int = 0, attn_impl: int = IMPL_AUTO):
+                 device: int = 0, kv_head_offset: int = 0, attn_impl: int = IMPL_AUTO,
+                 instant_source: int = INSTANT_RING):
         lib = load_library()
         self.torch_dtype = torch.bfloat16 if dtype == "bf16" else torch.float32
         self.cfg = Config(num_streams, num_layers, num_q_heads, num_kv_heads, head_dim, kv_head_offset,
                           tokens_per_frame, sink_tokens, past_frames, instant_frames, max_query_tokens,
                           max_position, float(rope_theta), rope_style,
-                          DTYPE_BF16 if dtype == "bf16" else DTYPE_FP32, device, attn_impl)
+                          DTYPE_BF16 if dtype == "bf16" else DTYPE_FP32, device, attn_impl, instant_source)
         self.device = torch.device("cuda", device)
         h = ctypes.c_void_p()
         _check(lib.dscache_create(ctypes.byref(self.cfg), ctypes.byref(h)))
         self._h = h
-        self.R = (past_frames + instant_frames + 1) * tokens_per_frame
+        self.R = self.state(0)["ring_slots"]   # from the library (it owns the layout)
 
     @classmethod
     def from_config(cls, cfg, device: int = 0, **kw):
@@ -298,6 +306,57 @@ class DSCache:
                                          _ptr(v_boost), n_boost, _ptr(o), _stream_ptr(stream)))
         return o
 
+    # ------------------------------------------------------------------ real-model mode (NEXT-1)
+    def append_past(self, k_past: Optional[torch.Tensor], v_past: Optional[torch.Tensor], layer_begin: int = 0,
+                    layer_count: Optional[int] = None, stream=None):
+        """Advance to the next step; once a frame leaves the buffer, store its Eq. 5 K/V
+        ([S][lc][tpf][Hkv][d]; None while nothing leaves)."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        n = 0
+        if k_past is not None:
+            n = int(k_past.shape[2])
+            self._t(k_past, "k_past", (c.num_streams, lc, n, c.num_kv_heads, c.head_dim))
+            self._t(v_past, "v_past", k_past.shape)
+        _check(_lib.dscache_append_past(self._h, lb, lc, _ptr(k_past), _ptr(v_past), n, _stream_ptr(stream)))
+
+    def build_instant_ext(self, q_inst: torch.Tensor, k_inst: torch.Tensor, v_inst: torch.Tensor,
+                          o_inst: Optional[torch.Tensor] = None, layer_begin: int = 0,
+                          layer_count: Optional[int] = None, stream=None) -> torch.Tensor:
+        """Eq. 7 with the caller's instant K/V ([S][lc][C_t][Hkv][d])."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        C_t = self.state(lb)["instant_tokens"]
+        self._t(q_inst, "q_inst", (c.num_streams, lc, C_t, c.num_q_heads, c.head_dim))
+        self._t(k_inst, "k_inst", (c.num_streams, lc, C_t, c.num_kv_heads, c.head_dim))
+        self._t(v_inst, "v_inst", k_inst.shape)
+        if o_inst is None:
+            o_inst = torch.empty(q_inst.shape, dtype=self.torch_dtype, device=self.device)
+        self._t(o_inst, "o_inst", q_inst.shape)
+        _check(_lib.dscache_build_instant_ext(self._h, lb, lc, _ptr(q_inst), _ptr(k_inst), _ptr(v_inst), _ptr(o_inst),
+                                              _stream_ptr(stream)))
+        return o_inst
+
+    def attend_ext(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, k_inst: torch.Tensor,
+                   v_inst: torch.Tensor, o: Optional[torch.Tensor] = None, layer_begin: int = 0,
+                   layer_count: Optional[int] = None, stream=None) -> torch.Tensor:
+        """Eq. 8 over [sink | past (ring) | caller instant K/V | self]."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        n_q = int(q.shape[2])
+        C_t = self.state(lb)["instant_tokens"]
+        self._t(q, "q", (c.num_streams, lc, n_q, c.num_q_heads, c.head_dim))
+        self._t(k_self, "k_self", (c.num_streams, lc, n_q, c.num_kv_heads, c.head_dim))
+        self._t(v_self, "v_self", k_self.shape)
+        self._t(k_inst, "k_inst", (c.num_streams, lc, C_t, c.num_kv_heads, c.head_dim))
+        self._t(v_inst, "v_inst", k_inst.shape)
+        if o is None:
+            o = torch.empty(q.shape, dtype=self.torch_dtype, device=self.device)
+        self._t(o, "o", q.shape)
+        _check(_lib.dscache_attend_ext(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, _ptr(k_inst),
+                                       _ptr(v_inst), _ptr(o), _stream_ptr(stream)))
+        return o
+
     def attend_peers(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, peer_ptrs, hq_total: int,
                      head_offset: int, layer_begin: int = 0, layer_count: Optional[int] = None, stream=None):
         """Fused all-gather epilogue (P2): this handle's attend rows are stored by the kernel into
@@ -359,7 +418,7 @@ class DSCache:
         c = self.cfg
         fshape = (c.num_streams, lc, c.tokens_per_frame, c.num_kv_heads, c.head_dim)
         self._t(k, "k", fshape); self._t(v, "v", fshape)
-        C_t = min(self.state(lb)["frames_seen"] + 1, c.instant_frames) * c.tokens_per_frame
+        C_t = self.state(lb)["next_instant_tokens"]   # the library's closed form (C_{t+1})
         ishape = (c.num_streams, lc, C_t, c.num_q_heads, c.head_dim)
         self._t(q_inst, "q_inst", ishape)
         if o_inst is None:

@@ -694,3 +694,90 @@ def test_boost_leaves_older_instant_rows_and_ignores_the_past():
     sch2 = O.StepSchedule(sch.t, sch.instant_frames, [], [], sch.tokens_per_frame, sch.sink_tokens)
     again = O.instant_cache_output_boosted(sch2, inp.sink(), inp.frame_kv, q_b, kb, vb, cfg.rope_theta)
     assert np.array_equal(boosted, again)
+
+
+# --------------------------------------------------------------------------- real-model mode (NEXT-1)
+def test_ext_with_the_buffer_kv_reduces_to_eq7_and_eq8():
+    """Supplying the buffer frames' own K/V as the instant K/V and the frame K/V as the
+    Eq. 5 K/V must give the ring-mode Eq. 7 / Eq. 8 results exactly (same keys, same order)."""
+    cfg = synth.CONFIGS["c1"]
+    inp = StreamInputs(cfg, 0, 0)
+    for t in (0, 2, 9):
+        sch = step_schedule(cfg, t)
+        ki = np.concatenate([inp.frame_kv(f)[0] for f in sch.instant_frames])
+        vi = np.concatenate([inp.frame_kv(f)[1] for f in sch.instant_frames])
+        qi = inp.instant_q(t, sch.C_t)
+        a = O.instant_cache_output(sch, inp.sink(), inp.frame_kv, qi, cfg.rope_theta)
+        b = O.instant_cache_output_ext(sch, inp.sink(), ki, vi, qi, cfg.rope_theta)
+        assert np.array_equal(a, b)
+        q, ks, vs = inp.query(t)
+        a = O.attend_output(sch, inp.sink(), inp.frame_kv, q, ks, vs, cfg.rope_theta)
+        b = O.attend_output_ext(sch, inp.sink(), inp.frame_kv, ki, vi, q, ks, vs, cfg.rope_theta)
+        assert np.array_equal(a, b)
+
+
+def _np(x):
+    return x.double().numpy()
+
+
+def test_ext_brute_force_full_history():
+    """Pure-Python loops over the full token history in the real-model mode: U holds, for
+    each frame that left the buffer, the K/V of its Eq. 5 update, the newest
+    l_U of them (Eq. 6); I_t is the step's own instant K/V (Eq. 7), distinct
+    from anything in U; [C_a, U_t, I_t] (Eq. 8) plus the query chunk, ids 0..."""
+    cfg = _upd_cfg()
+    inp = StreamInputs(cfg, 0, 0)
+    sk, sv = inp.sink()
+    A, tpf, lI, lU = cfg.sink_tokens, cfg.tokens_per_frame, cfg.instant_frames, cfg.past_frames
+    grp = cfg.num_q_heads // cfg.num_kv_heads
+    pkv = lambda f: tuple(_np(x) for x in synth.past_kv(cfg, 0, 0, f))   # noqa: E731
+    left = []   # frames that left the buffer, oldest first: (k, v) per token of past_kv
+    for t in range(cfg.num_frames):
+        if t - lI >= 0:
+            pk, pv = pkv(t - lI)
+            left += list(zip(pk, pv))
+        sch = step_schedule(cfg, t)
+        C_t = min(t + 1, lI) * tpf
+        ki, vi = (_np(x) for x in synth.instant_kv(cfg, 0, 0, t, C_t))
+        qi = inp.instant_q(t, C_t)
+        q, kq, vq = inp.query(t)
+        oi = O.instant_cache_output_ext(sch, (sk, sv), ki, vi, qi, cfg.rope_theta)
+        o = O.attend_output_ext(sch, (sk, sv), pkv, ki, vi, q, kq, vq, cfg.rope_theta)
+        past = left[-lU * tpf:] if lU > 0 else []
+        for h in range(cfg.num_q_heads):
+            g = h // grp
+            base = [(j, list(sk[j, g]), list(sv[j, g])) for j in range(A)]
+            keys = base + [(A + n, list(ki[n, g]), list(vi[n, g])) for n in range(C_t)]
+            for i in range(C_t):
+                ref = _brute_attend(list(qi[i, h]), A + i, keys, cfg.rope_theta)
+                assert np.abs(np.array(ref) - oi[i, h]).max() < 1e-12
+            keys = base + [(A + n, list(k[g]), list(v[g])) for n, (k, v) in enumerate(past)]
+            keys += [(A + len(past) + n, list(ki[n, g]), list(vi[n, g])) for n in range(C_t)]
+            L = len(keys)
+            keys += [(L + i, list(kq[i, g]), list(vq[i, g])) for i in range(q.shape[0])]
+            for i in range(q.shape[0]):
+                ref = _brute_attend(list(q[i, h]), L + i, keys, cfg.rope_theta)
+                assert np.abs(np.array(ref) - o[i, h]).max() < 1e-12
+
+
+def test_ext_reads_the_instant_kv_not_u_for_buffer_frames():
+    """Negative control + causality: poisoning the Eq. 5 K/V of frames still in the buffer
+    changes nothing (I_t, not U, holds them: PAPER.md:226, 230), while swapping the instant
+    K/V for the frames' Eq. 5 K/V does change the answer."""
+    cfg = _upd_cfg()
+    inp = StreamInputs(cfg, 0, 0)
+    t = 9
+    sch = step_schedule(cfg, t)
+    C_t = sch.C_t
+    ki, vi = (_np(x) for x in synth.instant_kv(cfg, 0, 0, t, C_t))
+    q, kq, vq = inp.query(t)
+    pkv = lambda f: tuple(_np(x) for x in synth.past_kv(cfg, 0, 0, f))   # noqa: E731
+    inst = set(sch.instant_frames)
+    poisoned = lambda f: tuple(np.full_like(x, 1e3) for x in pkv(f)) if f in inst else pkv(f)   # noqa: E731
+    a = O.attend_output_ext(sch, inp.sink(), pkv, ki, vi, q, kq, vq, cfg.rope_theta)
+    b = O.attend_output_ext(sch, inp.sink(), poisoned, ki, vi, q, kq, vq, cfg.rope_theta)
+    assert np.array_equal(a, b)
+    k2 = np.concatenate([pkv(f)[0] for f in sch.instant_frames])
+    v2 = np.concatenate([pkv(f)[1] for f in sch.instant_frames])
+    c = O.attend_output_ext(sch, inp.sink(), pkv, k2, v2, q, kq, vq, cfg.rope_theta)
+    assert np.abs(a - c).max() > 1e-3

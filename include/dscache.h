@@ -156,6 +156,28 @@ dscache_status dscache_build_instant(dscache_t h, int32_t layer_begin, int32_t l
 dscache_status dscache_build_instant_newest(dscache_t h, int32_t layer_begin, int32_t layer_count,
                                             const void* q_new, void* o_new, void* stream);
 
+/* The approximate instant cache as a library-driven state machine ("an extra
+ * periodically refreshed cache for recent frames, enabling reuse of buffer-frame caches";
+ * Table approx_cache periods 4/8/16; reading Q23).  The caller owns a persistent
+ * row ring o_ring [S][layer_count][C][Hq][d], C = l_I*tpf: the rows of frame f live at ring
+ * rows (f mod l_I)*tpf .. +tpf.  At step t (frame t the newest appended):
+ *   refresh  (t mod period == 0, or the rows in o_ring are not this handle's rows of step t-1
+ *            for the same period / o_ring / layer range): every buffer frame's rows are rebuilt
+ *            as dscache_build_instant; q_rows holds the C_t instant queries oldest first;
+ *   otherwise: only frame t's rows are built (as dscache_build_instant_newest, q_rows = its
+ *            tpf queries); the rows of frames t-l_I+1..t-1 stay as built at their own step
+ *            or at the last refresh.
+ * So frame f's rows at step t are the Eq. 7 rows of step s_f = max(f, last refresh <= t):
+ * context [sink | frames max(0, s_f-l_I+1) .. f], ids 0...  period = 1 is the
+ * exact Eq. 7 build every step.  dscache_instant_approx_rows returns in *n_rows the query rows
+ * the next dscache_build_instant_approx with these arguments takes (C_t or tpf); a mismatched
+ * n_rows is E_ARG.  E_ARG for period < 1 or null pointers, E_CONFIG when l_I = 0 or in the
+ * external-instant mode, E_STATE before the sink and the first frame. */
+dscache_status dscache_instant_approx_rows(dscache_t h, int32_t layer_begin, int32_t layer_count, int32_t period,
+                                           const void* o_ring, int32_t* n_rows);
+dscache_status dscache_build_instant_approx(dscache_t h, int32_t layer_begin, int32_t layer_count, int32_t period,
+                                            const void* q_rows, int32_t n_rows, void* o_ring, void* stream);
+
 /* Fused all-gather epilogue of the KV-head split (P2): the attend
  * of this handle's KV heads (Eq. 8, as dscache_attend) with every output row stored by the
  * attention kernel itself to EACH of n_peers gathered-O buffers, instead of to a local O

@@ -22,6 +22,9 @@ What it computes (per stream s, per layer r; everything in float64):
 * the real-model mode: Eq. 7 / Eq. 8 with the step's instant K/V supplied
   by the caller and U holding each frame's Eq. 5 K/V (instant_cache_output_ext,
   attend_output_ext; the Eq. 5 attention is cumulative_update_output over those K/V);
+* the approximate instant cache: full Eq. 7 rebuilds
+  every `period` steps, the newest frame's rows alone in between, older rows reused
+  (instant_cache_output_approx);
 * decoding over C_{t+1}: the last tokens of [query chunk | generated
   tokens] attend over [C_a, U, I, self] (SURVEY NEXT-2);
 * the cumulative-update attention inside phi(X_{t-l_I}, [C_a, zeta(U_{t-1})]) of
@@ -303,6 +306,51 @@ def attend_output_ext(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], 
     pos_k = np.arange(ks.shape[0])
     pos_q = L_ctx + np.arange(q.shape[0])
     return gqa_attention(np.asarray(q, np.float64), pos_q, ks, vs, pos_k, theta, style)
+
+
+def instant_cache_output_approx(t_last: int, period: int, instant_frames: int, past_frames: int,
+                                tokens_per_frame: int, sink: Tuple[np.ndarray, np.ndarray], frame_kv: FrameFn,
+                                q_at: Callable[[int, int], np.ndarray], theta: float, style: int = SPLIT_HALF,
+                                capture: Sequence[int] = ()):
+    """Approximate instant cache ("an extra periodically refreshed cache for
+    recent frames, enabling reuse of buffer-frame caches"; DESIGN.md reading
+    Q23), replayed from step 0 to t_last in the paper's order:
+
+    * step s is a refresh when s mod period == 0: every buffer frame's instant rows are
+      rebuilt, i.e. Eq. 7 (instant_cache_output) at step s with the step's C_s queries;
+    * otherwise only the newest frame's rows are computed -- the last tpf rows of Eq. 7 at
+      step s (its tokens at ids A + C_s - tpf + j over [C_a | B_s]) -- and every other buffer
+      frame keeps the rows it already had;
+    * a frame leaving the buffer (Eq. 3) drops its rows.
+
+    q_at(s, C_s) -> the C_s instant queries of step s, oldest first (a non-refresh step reads
+    only its last tpf).  Returns {s: rows [C_s, Hq, d] of B_s, oldest frame first} for s in
+    capture (default: t_last only)."""
+    tpf = tokens_per_frame
+    sk, sv = sink
+    A = sk.shape[0]
+    hkv, d = sk.shape[1], sk.shape[2]
+    capture = set(capture) if capture else {t_last}
+    rows = {}
+    out = {}
+    for s in range(t_last + 1):
+        sch = schedule_fifo(s, instant_frames, past_frames, tpf, A)
+        q = np.asarray(q_at(s, sch.C_t), np.float64)
+        if s % period == 0:
+            o = instant_cache_output(sch, sink, frame_kv, q, theta, style)
+            for k, f in enumerate(sch.instant_frames):
+                rows[f] = o[k * tpf:(k + 1) * tpf]
+        else:
+            ks = _cat([sk] + [frame_kv(f)[0] for f in sch.instant_frames], hkv, d)
+            vs = _cat([sv] + [frame_kv(f)[1] for f in sch.instant_frames], hkv, d)
+            pos_q = A + sch.C_t - tpf + np.arange(tpf)
+            rows[s] = gqa_attention(q[sch.C_t - tpf:], pos_q, ks, vs, np.arange(ks.shape[0]), theta, style)
+        for f in list(rows):
+            if f not in sch.instant_frames:
+                del rows[f]
+        if s in capture:
+            out[s] = np.concatenate([rows[f] for f in sch.instant_frames])
+    return out
 
 
 def decode_output(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], frame_kv: FrameFn,

@@ -669,8 +669,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!valid_row || FA_ABL_EPI) continue;
           uint32_t q[8];
           const bool peers = p.n_peers > 0;
+          int oq = qi + p.o_rot;   // o_rot = 0 unless ring-ordered output (o_rows > 0)
+          if (p.o_rows > 0 && oq >= p.o_rows) oq -= p.o_rows;
           const long long row = peers ? ((long long)w.pp * p.n_q + qi) * p.o_hq + p.o_head_off + h
-                                      : ((long long)w.pp * p.n_q + qi) * p.Hq + h;
+                                      : ((long long)w.pp * (p.o_rows > 0 ? p.o_rows : p.n_q) + oq) * p.Hq + h;
           const int nd = peers ? p.n_peers : 1;
 #pragma unroll
           for (int v = 0; v < 4; ++v) {

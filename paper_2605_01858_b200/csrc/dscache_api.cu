@@ -84,6 +84,12 @@ struct dscache_s {
   std::vector<int64_t> frames;
   std::vector<int> sink_filled;
   std::vector<int64_t> last_evicted;
+  // approximate instant cache (NEXT-3): per layer, the step of the last approximate build, its
+  // period, and the (o_ring, layer_count) of that call at its layer_begin
+  std::vector<int64_t> approx_last;
+  std::vector<int> approx_period;
+  std::vector<const void*> approx_ring;
+  std::vector<int> approx_lc;
   int* dbg_build = nullptr;
   int* dbg_attend = nullptr;
   int poison = 0;
@@ -273,6 +279,10 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   h->npos = c.max_position;   // RoPE table covers every id < max_position (decode ids grow per token)
   h->frames.assign(c.num_layers, 0);
   h->sink_filled.assign(c.num_layers, c.sink_tokens == 0 ? 1 : 0);
+  h->approx_last.assign(c.num_layers, -1);
+  h->approx_period.assign(c.num_layers, 0);
+  h->approx_ring.assign(c.num_layers, nullptr);
+  h->approx_lc.assign(c.num_layers, 0);
   h->last_evicted.assign(c.num_layers, -1);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, c.device);
   h->sched = dsc::sched_cache_new();
@@ -440,19 +450,20 @@ dscache_status dscache_build_instant(dscache_t h, int32_t lb, int32_t lc, const 
   return run_attention(h, p, h->impl_build, 0, (cudaStream_t)stream);
 }
 
-dscache_status dscache_build_instant_newest(dscache_t h, int32_t lb, int32_t lc, const void* q_new, void* o_new,
-                                            void* stream) {
-  if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "build_instant_newest");
+namespace {
+// Parameters of the newest frame's Eq. 7 rows: its tpf queries attend causally over [sink |
+// instant window] at ids A + C_t - tpf + j (the rows of build_instant a causal mask makes
+// independent of the other instant queries).
+dscache_status prep_newest(dscache_t h, int32_t lb, int32_t lc, const void* q_new, void* o_new, dsc::AttnParams& p) {
   dscache_status s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
   if (!h->sink_filled[lb] || h->frames[lb] < 1)
-    return fail(DSCACHE_E_STATE, "build_instant_newest before the sink and the first frame were appended");
+    return fail(DSCACHE_E_STATE, "newest-frame build before the sink and the first frame were appended");
   if (h->cfg.instant_frames < 1) return fail(DSCACHE_E_CONFIG, "l_I = 0: there is no instant cache");
-  if (!q_new || !o_new) return fail(DSCACHE_E_ARG, "null q_new/o_new");
-  DeviceGuard dg(h->cfg.device);
+  if (!q_new || !o_new) return fail(DSCACHE_E_ARG, "null q/o");
   const Schedule sc = h->schedule(lb);
   const int tpf = h->cfg.tokens_per_frame;
-  dsc::AttnParams p{};
+  p = dsc::AttnParams{};
   fill_common(h, p, lb, lc);
   p.q = q_new; p.o = o_new; p.n_q = tpf;
   p.q_pos0 = h->cfg.sink_tokens + sc.C_t - tpf;   // the newest frame's tokens are the last tpf instant ids
@@ -460,7 +471,86 @@ dscache_status dscache_build_instant_newest(dscache_t h, int32_t lb, int32_t lc,
   p.self_k = p.self_v = nullptr; p.n_self = 0;
   p.dbg_pos = nullptr;
   p.n_mblocks = (p.n_q * p.grp + 2 * dsc::kTileM - 1) / (2 * dsc::kTileM);
+  return DSCACHE_OK;
+}
+
+// Approximate instant cache (NEXT-3, reading Q23): a refresh rebuilds every buffer
+// frame's rows; between refreshes only the newest frame's rows are built.  A step refreshes
+// when t is a multiple of the period or when the rows in o_ring are not the previous step's
+// (first call, a skipped step, another period, another buffer or layer range).
+bool approx_refresh(dscache_t h, int32_t lb, int32_t lc, int32_t period, const void* o_ring, int64_t t) {
+  if (t % period == 0) return true;
+  if (h->approx_ring[lb] != o_ring || h->approx_lc[lb] != lc) return true;
+  for (int l = lb; l < lb + lc; ++l)
+    if (h->approx_last[l] != t - 1 || h->approx_period[l] != period) return true;
+  return false;
+}
+}  // namespace
+
+dscache_status dscache_build_instant_newest(dscache_t h, int32_t lb, int32_t lc, const void* q_new, void* o_new,
+                                            void* stream) {
+  if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "build_instant_newest");
+  dsc::AttnParams p{};
+  dscache_status s = prep_newest(h, lb, lc, q_new, o_new, p);
+  if (s != DSCACHE_OK) return s;
+  DeviceGuard dg(h->cfg.device);
   return run_attention(h, p, h->impl_build, 0, (cudaStream_t)stream);
+}
+
+dscache_status dscache_instant_approx_rows(dscache_t h, int32_t lb, int32_t lc, int32_t period, const void* o_ring,
+                                           int32_t* n_rows) {
+  dscache_status s = need_mode(h, DSCACHE_INSTANT_RING, "instant_approx_rows");
+  if (s == DSCACHE_OK) s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  if (!n_rows) return fail(DSCACHE_E_ARG, "null n_rows");
+  if (period < 1) return fail(DSCACHE_E_ARG, "period must be >= 1");
+  if (!h->sink_filled[lb] || h->frames[lb] < 1)
+    return fail(DSCACHE_E_STATE, "approximate build before the sink and the first frame were appended");
+  if (h->cfg.instant_frames < 1) return fail(DSCACHE_E_CONFIG, "l_I = 0: there is no instant cache");
+  const int64_t t = h->frames[lb] - 1;
+  *n_rows = approx_refresh(h, lb, lc, period, o_ring, t) ? h->schedule(lb).C_t : h->cfg.tokens_per_frame;
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_build_instant_approx(dscache_t h, int32_t lb, int32_t lc, int32_t period, const void* q_rows,
+                                            int32_t n_rows, void* o_ring, void* stream) {
+  int32_t need = 0;
+  dscache_status s = dscache_instant_approx_rows(h, lb, lc, period, o_ring, &need);
+  if (s != DSCACHE_OK) return s;
+  if (n_rows != need)
+    return fail(DSCACHE_E_ARG, "approximate build at this step takes " + std::to_string(need) + " query rows (" +
+                                   (need == h->cfg.tokens_per_frame && need != h->schedule(lb).C_t ? "newest frame" : "refresh") +
+                                   "), got " + std::to_string(n_rows));
+  if (!q_rows || !o_ring) return fail(DSCACHE_E_ARG, "null q_rows/o_ring");
+  const dscache_config& c = h->cfg;
+  const int64_t t = h->frames[lb] - 1;
+  const int tpf = c.tokens_per_frame, lI = c.instant_frames;
+  const bool refresh = approx_refresh(h, lb, lc, period, o_ring, t);
+  DeviceGuard dg(c.device);
+  dsc::AttnParams p{};
+  if (refresh) {
+    // every buffer frame f in max(0, t-l_I+1)..t: row i (frame b + i/tpf) lands at ring row
+    // ((b + i/tpf) mod l_I) * tpf + i mod tpf = (i + (b mod l_I) * tpf) mod C
+    dsc::StageParams sp{};
+    bool empty = false;
+    s = prep_build(h, lb, lc, q_rows, o_ring, p, &empty, &sp);
+    if (s != DSCACHE_OK) return s;
+    const int64_t b = t - lI + 1 > 0 ? t - lI + 1 : 0;
+    p.o_rows = h->C; p.o_rot = (int)(b % lI) * tpf;
+    if (p.staged) {
+      DSC_CUDA(dsc::launch_stage_instant(sp, (cudaStream_t)stream));
+      h->launches++;
+    }
+  } else {
+    s = prep_newest(h, lb, lc, q_rows, o_ring, p);
+    if (s != DSCACHE_OK) return s;
+    p.o_rows = h->C; p.o_rot = (int)(t % lI) * tpf;
+  }
+  s = run_attention(h, p, h->impl_build, 0, (cudaStream_t)stream);
+  if (s != DSCACHE_OK) return s;
+  for (int l = lb; l < lb + lc; ++l) { h->approx_last[l] = t; h->approx_period[l] = period; }
+  h->approx_ring[lb] = o_ring; h->approx_lc[lb] = lc;
+  return DSCACHE_OK;
 }
 
 namespace {

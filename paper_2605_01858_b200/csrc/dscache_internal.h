@@ -68,6 +68,9 @@ struct AttnParams {
   // of to o; peer_o are device pointers mapped in this process (local, P2P or CUDA IPC)
   void* peer_o[kMaxPeers];
   int n_peers, o_hq, o_head_off;
+  // ring-ordered output (approximate instant cache, NEXT-3): o_rows > 0 stores query row i of
+  // problem pp at row pp * o_rows + (i + o_rot) mod o_rows of o (o_rot < o_rows, n_q <= o_rows)
+  int o_rows, o_rot;
   // CTA b of the tcgen05 kernel runs the host-decoded items item_recs[item_off[b] .. item_off[b+1])
   // in order (set by its launcher from the handle's item-table cache)
   const int* item_off;

@@ -326,7 +326,9 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnParams p) {
     m = mn;
   }
   const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
-  T* orow = reinterpret_cast<T*>(p.o) + (((long long)pp * p.n_q + i) * p.Hq + h) * D;
+  int oi = i + p.o_rot;
+  if (p.o_rows > 0 && oi >= p.o_rows) oi -= p.o_rows;
+  T* orow = reinterpret_cast<T*>(p.o) + (((long long)pp * (p.o_rows > 0 ? p.o_rows : p.n_q) + oi) * p.Hq + h) * D;
 #pragma unroll
   for (int k = 0; k < E; ++k) orow[elem_of<D>(lane, k, p.rope_style)] = from_f<T>(acc[k] * inv);
 }

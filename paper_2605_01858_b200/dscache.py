@@ -57,7 +57,8 @@ class State(ctypes.Structure):
 
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
            "dscache_append_past", "dscache_build_instant_ext", "dscache_attend_ext",
-           "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
+           "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest",
+           "dscache_instant_approx_rows", "dscache_build_instant_approx", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
            "dscache_attn_impl", "dscache_watchdog_read", "dscache_last_error", "dscache_attend_partial", "dscache_combine_partials",
            "dscache_build_instant_boost", "dscache_attend_boost", "dscache_attend_peers",
@@ -85,6 +86,8 @@ def load_library(path: str = LIB_PATH):
         "dscache_update_attend": ([P, I32, I32, P, P, I32, P], I32),
         "dscache_decode": ([P, I32, I32, P, P, P, I32, I32, P, P], I32),
         "dscache_build_instant_newest": ([P, I32, I32, P, P, P], I32),
+        "dscache_instant_approx_rows": ([P, I32, I32, I32, P, ctypes.POINTER(ctypes.c_int32)], I32),
+        "dscache_build_instant_approx": ([P, I32, I32, I32, P, I32, P, P], I32),
         "dscache_step": ([P, I32, I32, P, P, P, P, P, P, P, I32, P, P], I32),
         "dscache_get_state": ([P, I32, ctypes.POINTER(State)], I32),
         "dscache_copy_ring": ([P, I32, I32, P, P], I32),
@@ -447,6 +450,35 @@ class DSCache:
         self._t(o_new, "o_new", shape)
         _check(_lib.dscache_build_instant_newest(self._h, lb, lc, _ptr(q_new), _ptr(o_new), _stream_ptr(stream)))
         return o_new
+
+    def approx_ring(self, layer_count: Optional[int] = None) -> torch.Tensor:
+        """A row ring for build_instant_approx: [S][lc][C][Hq][d], frame f at rows (f mod l_I)*tpf."""
+        c = self.cfg
+        lc = c.num_layers if layer_count is None else layer_count
+        return torch.zeros((c.num_streams, lc, c.instant_frames * c.tokens_per_frame, c.num_q_heads, c.head_dim),
+                           dtype=self.torch_dtype, device=self.device)
+
+    def approx_rows(self, o_ring: torch.Tensor, period: int, layer_begin: int = 0,
+                    layer_count: Optional[int] = None) -> int:
+        """Query rows the next build_instant_approx takes: C_t on a refresh, tpf otherwise."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        n = ctypes.c_int32()
+        _check(_lib.dscache_instant_approx_rows(self._h, lb, lc, int(period), _ptr(o_ring), ctypes.byref(n)))
+        return n.value
+
+    def build_instant_approx(self, q_rows: torch.Tensor, o_ring: torch.Tensor, period: int, layer_begin: int = 0,
+                             layer_count: Optional[int] = None, stream=None) -> torch.Tensor:
+        """Approximate instant cache (NEXT-3): refresh every `period` steps, otherwise only the
+        newest frame's rows; o_ring [S][lc][C][Hq][d] is updated in place (see approx_ring)."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        n = int(q_rows.shape[2])
+        self._t(q_rows, "q_rows", (c.num_streams, lc, n, c.num_q_heads, c.head_dim))
+        self._t(o_ring, "o_ring", (c.num_streams, lc, c.instant_frames * c.tokens_per_frame, c.num_q_heads,
+                                   c.head_dim))
+        _check(_lib.dscache_build_instant_approx(self._h, lb, lc, int(period), _ptr(q_rows), n, _ptr(o_ring),
+                                                 _stream_ptr(stream)))
+        return o_ring
 
     def decode(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, o: Optional[torch.Tensor] = None,
                layer_begin: int = 0, layer_count: Optional[int] = None, stream=None) -> torch.Tensor:

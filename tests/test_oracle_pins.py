@@ -781,3 +781,86 @@ def test_ext_reads_the_instant_kv_not_u_for_buffer_frames():
     v2 = np.concatenate([pkv(f)[1] for f in sch.instant_frames])
     c = O.attend_output_ext(sch, inp.sink(), pkv, k2, v2, q, kq, vq, cfg.rope_theta)
     assert np.abs(a - c).max() > 1e-3
+
+
+# --------------------------------------------------------------------------- approximate instant cache (NEXT-3)
+def _approx(cfg, inp, t, period, capture=()):
+    return O.instant_cache_output_approx(t, period, cfg.instant_frames, cfg.past_frames, cfg.tokens_per_frame,
+                                         inp.sink(), inp.frame_kv, inp.instant_q, cfg.rope_theta,
+                                         capture=capture)
+
+
+def test_approx_period_one_and_refresh_steps_are_exact_eq7():
+    """period = 1 rebuilds every step (the exact Eq. 7 cache); with any period, a refresh step
+    (t mod period == 0) equals the exact build of that step ("periodically refreshed")."""
+    cfg = synth.CONFIGS["c1"].replace(instant_frames=4)
+    inp = StreamInputs(cfg, 0, 0)
+    steps = list(range(12))
+    for period, check in ((1, steps), (4, [0, 4, 8]), (3, [0, 3, 6, 9])):
+        got = _approx(cfg, inp, max(steps), period, capture=steps)
+        for t in check:
+            sch = step_schedule(cfg, t)
+            ref = O.instant_cache_output(sch, inp.sink(), inp.frame_kv, inp.instant_q(t, sch.C_t), cfg.rope_theta)
+            assert np.allclose(got[t], ref, rtol=0, atol=1e-13), (period, t)
+
+
+def test_approx_incremental_rows_are_the_last_rows_of_eq7():
+    """Between refreshes the newest frame's rows are the last tpf rows of the exact Eq. 7
+    build of that step (causality: they do not see the other instant queries)."""
+    cfg = synth.CONFIGS["c1"].replace(instant_frames=4)
+    inp = StreamInputs(cfg, 0, 0)
+    tpf = cfg.tokens_per_frame
+    got = _approx(cfg, inp, 11, 5, capture=range(12))
+    for t in (1, 2, 7, 11):
+        sch = step_schedule(cfg, t)
+        ref = O.instant_cache_output(sch, inp.sink(), inp.frame_kv, inp.instant_q(t, sch.C_t), cfg.rope_theta)
+        assert np.allclose(got[t][-tpf:], ref[-tpf:], rtol=0, atol=1e-13)
+
+
+@pytest.mark.parametrize("period", [2, 3, 100])
+def test_approx_brute_force_closed_form(period):
+    """Pure-Python loops: frame f's rows at step t were built at s_f = max(f, P*floor(t/P))
+    with the queries of step s_f, over [sink | frames max(0, s_f - l_I + 1) .. f] at ids 0..
+    (PAPER.md:236); a frame is never rebuilt between refreshes ("reuse of
+    buffer-frame caches").  period 100 > t: purely incremental rows (s_f = f for f > 0)."""
+    cfg = synth.StreamConfig("apx", 97, 1, 1, 4, 2, 8, 1e4, 3, 2, 0, 3, 1, 10, "fp32", 1.0)
+    inp = StreamInputs(cfg, 0, 0)
+    sk, sv = inp.sink()
+    A, tpf, lI = cfg.sink_tokens, cfg.tokens_per_frame, cfg.instant_frames
+    grp = cfg.num_q_heads // cfg.num_kv_heads
+    steps = list(range(cfg.num_frames))
+    got = _approx(cfg, inp, max(steps), period, capture=steps)
+    for t in steps:
+        r = period * (t // period)
+        buf = list(range(max(0, t - lI + 1), t + 1))
+        assert got[t].shape[0] == len(buf) * tpf
+        for n, f in enumerate(buf):
+            s_f = max(f, r)
+            b = max(0, s_f - lI + 1)
+            ctx = list(range(b, f + 1))
+            qs = inp.instant_q(s_f, (min(s_f + 1, lI)) * tpf)
+            for h in range(cfg.num_q_heads):
+                g = h // grp
+                keys = [(j, list(sk[j, g]), list(sv[j, g])) for j in range(A)]
+                for m, fr in enumerate(ctx):
+                    fk, fv = inp.frame_kv(fr)
+                    keys += [(A + m * tpf + j, list(fk[j, g]), list(fv[j, g])) for j in range(tpf)]
+                for j in range(tpf):
+                    row = (f - b) * tpf + j
+                    ref = _brute_attend(list(qs[row, h]), A + row, keys, cfg.rope_theta)
+                    assert np.abs(np.array(ref) - got[t][n * tpf + j, h]).max() < 1e-12, (t, f, j, h)
+
+
+def test_approx_differs_from_exact_between_refreshes():
+    """Negative control: between refreshes, once a frame has left the buffer since the older
+    rows were built, the reused rows differ from the exact Eq. 7 rows (the "residual
+    accumulation" of PAPER.md:779); the newest frame's rows never do."""
+    cfg = synth.CONFIGS["c1"].replace(instant_frames=4)
+    inp = StreamInputs(cfg, 0, 0)
+    tpf = cfg.tokens_per_frame
+    t = 10                                  # period 8: refresh at 8, l_I = 4
+    got = _approx(cfg, inp, t, 8)[t]
+    sch = step_schedule(cfg, t)
+    ref = O.instant_cache_output(sch, inp.sink(), inp.frame_kv, inp.instant_q(t, sch.C_t), cfg.rope_theta)
+    assert np.abs(got[:-tpf] - ref[:-tpf]).max() > 1e-3
+    assert np.allclose(got[-tpf:], ref[-tpf:], rtol=0, atol=1e-13)

@@ -53,7 +53,12 @@ def peaks():
 
 # ----------------------------------------------------------------------------- workload arithmetic
 def traffic_key(args, world: int) -> str:
-    return f"{args.config}|{args.mode}|{args.api}|boost{args.boost:g}|world{world}|layerseq{int(args.layer_seq)}"
+    key = f"{args.config}|{args.mode}|{args.api}|boost{args.boost:g}|world{world}|layerseq{int(args.layer_seq)}"
+    if getattr(args, "approx", 0):
+        key += f"|approx{args.approx}"
+    if getattr(args, "instant_frames", None):
+        key += f"|lI{args.instant_frames}"
+    return key
 
 
 def config_dict(cfg, args, world: int, S_local=None):
@@ -70,6 +75,7 @@ def config_dict(cfg, args, world: int, S_local=None):
             "config_id": cfg.name, "streams": cfg.num_streams, "layers": cfg.num_layers, "query_tokens": q,
             "parallelism": par, "mode": args.mode, "api": args.api, "layer_sequential": bool(args.layer_seq),
             "n_boost": int(round(args.boost * cfg.tokens_per_frame)) if args.boost > 0 else 0,
+            "approx_period": getattr(args, "approx", 0) or None,
             "steady_state": True}
 
 
@@ -79,15 +85,19 @@ def steady_counts(cfg, n_q=None):
     return cfg.sink_tokens, cfg.W, cfg.C, n_q
 
 
-def flops_per_unit(cfg, n_boost=0):
+def flops_per_unit(cfg, n_boost=0, newest_only=False):
     """Algorithmic FLOPs of one (stream, layer) step: 4 * d * Hq * visible (query, key) pairs.
     build: instant token i sees A + i + 1 keys; attend: query i sees A + P + C + i + 1 keys.
-    With a boosted newest frame (n_boost tokens) the instant segment holds C - tpf + n_boost."""
+    With a boosted newest frame (n_boost tokens) the instant segment holds C - tpf + n_boost.
+    newest_only (approximate instant cache between refreshes): only the last tpf instant rows."""
     A, P, C, q = steady_counts(cfg)
     if n_boost:
         C = C - cfg.tokens_per_frame + n_boost
     k = 4 * cfg.head_dim * cfg.num_q_heads
     build = k * (C * A + C * (C + 1) // 2)
+    if newest_only:
+        first = C - cfg.tokens_per_frame          # rows C - tpf .. C - 1
+        build = k * (cfg.tokens_per_frame * A + (C * (C + 1) - first * (first + 1)) // 2)
     attend = k * (q * (A + P + C) + q * (q + 1) // 2)
     return build, attend
 
@@ -256,6 +266,15 @@ def run_ours(args, cfg, world, rank, local):
     gathered = [None]
 
     fused = args.api == "fused"
+    approx = getattr(args, "approx", 0)
+    if approx:
+        if args.layer_seq or n_boost or context or kvsplit:
+            raise SystemExit("--approx runs the stream-partition mode with split calls")
+        ring = dsc.approx_ring()
+        q_new = [rnd(S, N, tpf, Hq, d) for _ in range(2)]
+    fb_full, fa_ = flops_per_unit(lcfg, n_boost)
+    fb_new, _ = flops_per_unit(lcfg, n_boost, newest_only=True)
+    build_flops = [0]          # per (stream, layer), summed over the counted steps
 
     def step(i):
         t = tcount[0]
@@ -278,6 +297,12 @@ def run_ours(args, cfg, world, rank, local):
             dsc.append_frame(*frames[t % POOL])
             dsc.build_instant_boost(q_inst[i & 1], *boost_kv[i & 1], o_inst=o_inst)
             dsc.attend_boost(qq[0], qq[1], qq[2], *boost_kv[i & 1], o=o)
+        elif approx:    # NEXT-3: refresh every `approx` steps, otherwise the newest frame's rows only
+            dsc.append_frame(*frames[t % POOL])
+            n = dsc.approx_rows(ring, approx)
+            dsc.build_instant_approx(q_inst[i & 1] if n != tpf or C == tpf else q_new[i & 1], ring, approx)
+            build_flops[0] += fb_full if n != tpf or C == tpf else fb_new
+            dsc.attend(qq[0], qq[1], qq[2], o)
         elif fused:     # dscache_step: append + build_instant + attend, one attention launch
             dsc.step(*frames[t % POOL], q_inst[i & 1], qq[0], qq[1], qq[2], o_inst=o_inst, o=o)
         else:
@@ -299,6 +324,7 @@ def run_ours(args, cfg, world, rank, local):
 
     dsc.profile(True)
     dsc.profile_read(reset=True)
+    build_flops[0] = 0
     barrier(world)
     torch.cuda.synchronize()
     snap_before = clock_snapshot(local) if rank == 0 else None
@@ -320,6 +346,10 @@ def run_ours(args, cfg, world, rank, local):
         ev[0][1].record(stream)
         torch.cuda.synchronize()
         total_ms = ev[0][0].elapsed_time(ev[0][1])
+    timed_build_flops = build_flops[0]
+    # the attention launches of exactly the timed steps (the clock hold loop below is not profiled)
+    prof = dsc.profile_read(reset=True)
+    dsc.profile(False)
     if clocks:
         # short timed regions: keep the same step loop running (untimed) so the sampler sees
         # the clocks of this workload for at least HOLD_S
@@ -336,18 +366,18 @@ def run_ours(args, cfg, world, rank, local):
     if clk is not None:
         clk["window"] = "timed steps + untimed repetitions of the same step up to %.1f s" % ClockSampler.HOLD_S
         clk["snapshot_before"], clk["snapshot_after"] = snap_before, clock_snapshot(local)
-    prof = dsc.profile_read(reset=True)
-    dsc.profile(False)
     t_max = max_over_ranks(total_ms, world)
 
     # e2e: the same step through the public API with pinned host buffers, H2D of every
     # input of the step and D2H of the query answer O inside the timed region
-    e2e = (run_e2e(args, cfg, lcfg, dsc, S, dev, stream, world, kvsplit) if not n_boost else
-           {"skipped": "boost mode times the device-resident path only"})
+    e2e = (run_e2e(args, cfg, lcfg, dsc, S, dev, stream, world, kvsplit) if not (n_boost or approx) else
+           {"skipped": ("boost" if n_boost else "approx") + " mode times the device-resident path only"})
     impl = dsc.attn_impl()
     dsc.close()
 
     fb, fa = flops_per_unit(lcfg, n_boost)
+    if approx:
+        fb = timed_build_flops / args.steps     # refresh / newest-only mix of the timed steps
     units = S * N
     frames_total = cfg.num_streams * args.steps
     value = frames_total / (t_max / 1e3)
@@ -590,12 +620,17 @@ def main():
                     help="fused: DSCache.step (one attention launch per step); split: three calls")
     ap.add_argument("--boost", type=float, default=0.0,
                     help="> 0: resolution-boosted newest frame with boost*tpf tokens (SURVEY NEXT-4), split calls")
+    ap.add_argument("--approx", type=int, default=0,
+                    help="> 0: approximate instant cache refreshed every APPROX steps (SURVEY NEXT-3), split calls")
+    ap.add_argument("--instant-frames", type=int, default=None, help="override l_I of the config (frames)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = synth.CONFIGS[args.config]
+    if args.instant_frames is not None:
+        cfg = cfg.replace(instant_frames=args.instant_frames)
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # not launched by torchrun: launch N ranks of this same command (one process per GPU)

@@ -115,6 +115,20 @@ def bytes_per_unit(cfg):
     return build, attend, append
 
 
+class L2Flush:
+    """Evicts the working set from L2 between timed steps by READING a buffer twice the L2
+    size: the lines it leaves behind are clean, so the next step pays no write-back of the
+    flush itself (a write-based flush leaves ~126 MB of dirty lines that the timed kernel
+    would have to write back)."""
+
+    def __init__(self, dev):
+        self.buf = torch.ones(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+        self.out = torch.empty((), dtype=torch.float32, device=dev)
+
+    def __call__(self):
+        torch.amax(self.buf, dim=0, out=self.out)
+
+
 # ----------------------------------------------------------------------------- clocks
 def clock_snapshot(device_index: int):
     """One nvidia-smi reading (sm MHz, max MHz, active reasons), or None."""
@@ -316,7 +330,7 @@ def run_ours(args, cfg, world, rank, local):
 
     ring_bytes = 2 * S * N * Hkv * dsc.R * d * (2 if cfg.dtype == "bf16" else 4)
     flush = ring_bytes < 2 * L2_BYTES
-    scratch = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if flush else None
+    scratch = L2Flush(dev) if flush else None
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -333,7 +347,7 @@ def run_ours(args, cfg, world, rank, local):
     if flush:
         total_ms = 0.0
         for i in range(args.steps):
-            scratch.zero_()
+            scratch()
             ev[i][0].record(stream)
             step(i)
             ev[i][1].record(stream)
@@ -404,7 +418,7 @@ def run_ours(args, cfg, world, rank, local):
         "scaling": "strong",   # the config's total work (all its streams) is fixed as N grows
         "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32", "data": "synthetic",
         "config": dict(config_dict(cfg, args, world),
-                       l2=("flushed between steps" if flush else "inputs larger than L2 (ring %.2f GB)" % (ring_bytes / 1e9)),
+                       l2=("flushed between steps (read-only flush of 2x L2)" if flush else "inputs larger than L2 (ring %.2f GB)" % (ring_bytes / 1e9)),
                        input_pool=f"{POOL} distinct frames cycled (positions never repeat)"),
         "value_is": "aggregate frames/s over all streams and GPUs (one frame per stream per step); "
                     "frames_per_s_per_stream = value / streams",
@@ -430,6 +444,123 @@ def run_ours(args, cfg, world, rank, local):
         "e2e": e2e,
     }
     return line
+
+
+def decode_bytes_per_unit(cfg, n_self, n_q, past_tokens=None):
+    """Algorithmic HBM bytes of one (stream, layer) decode launch: every key of [sink | past |
+    instant | self] read once per KV head (K and V), the n_q query rows read, O written."""
+    A, P, C, _ = steady_counts(cfg)
+    P = P if past_tokens is None else past_tokens
+    e = 2 if cfg.dtype == "bf16" else 4
+    keys = A + P + C + n_self
+    return keys * 2 * cfg.num_kv_heads * cfg.head_dim * e + 2 * n_q * cfg.num_q_heads * cfg.head_dim * e
+
+
+def run_decode(args, cfg, world, rank, local):
+    """--mode decode: one autoregressive token per stream per
+    step over C_{t+1} = [sink | past | instant] plus the transient self segment (the query
+    chunk and the tokens generated so far, n_self = q + G), for every layer; memory-bound."""
+    from paper_2605_01858_b200 import dscache as D
+    dev = torch.device("cuda", local)
+    lo, hi = stream_range(cfg.num_streams, world, rank)
+    S = hi - lo
+    lcfg = cfg.replace(num_streams=S)
+    n_q = args.decode_nq
+    n_self = cfg.query_tokens + args.decode_gen
+    lcfg = lcfg.replace(query_tokens=max(cfg.query_tokens, n_self))
+    dsc = D.DSCache.from_config(lcfg, device=local)
+    A, P, C, _ = steady_counts(cfg)
+    N, Hq, Hkv, d, tpf = cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.tokens_per_frame
+    dt = cfg.torch_dtype
+    g = torch.Generator(device=dev)
+    g.manual_seed(2000 + rank)
+
+    def rnd(*shape):
+        return (torch.randn(shape, device=dev, generator=g) * cfg.scale).to(dt)
+    if A > 0:
+        dsc.append_frame(rnd(S, N, A, Hkv, d), rnd(S, N, A, Hkv, d))
+    fk, fv = rnd(S, N, tpf, Hkv, d), rnd(S, N, tpf, Hkv, d)
+    for _ in range(cfg.instant_frames + cfg.past_frames):
+        dsc.append_frame(fk, fv)
+    assert dsc.state(0)["past_tokens"] == P and dsc.state(0)["instant_tokens"] == C
+    qs = [rnd(S, N, n_q, Hq, d) for _ in range(2)]
+    ks, vs = rnd(S, N, n_self, Hkv, d), rnd(S, N, n_self, Hkv, d)
+    o = torch.empty(S, N, n_q, Hq, d, dtype=dt, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    stride = args.decode_stride
+
+    def step(i):
+        if stride > 1:
+            dsc.decode(qs[i & 1], ks, vs, o=o, past_stride=stride)
+        else:
+            dsc.decode(qs[i & 1], ks, vs, o=o)
+
+    ring_bytes = 2 * S * N * Hkv * dsc.R * d * (2 if cfg.dtype == "bf16" else 4)
+    flush = ring_bytes < 2 * L2_BYTES
+    scratch = L2Flush(dev) if flush else None
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    dsc.profile(True)
+    dsc.profile_read(reset=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local) if rank == 0 else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if flush:
+        for i in range(args.steps):
+            scratch()
+            ev[i][0].record(stream)
+            step(i)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    else:
+        ev[0][0].record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev[0][1].record(stream)
+        torch.cuda.synchronize()
+        total_ms = ev[0][0].elapsed_time(ev[0][1])
+    prof = dsc.profile_read(reset=True)
+    dsc.profile(False)
+    if clocks:
+        t_hold = time.perf_counter()
+        i = args.steps
+        while time.perf_counter() - t_hold < clocks.HOLD_S - total_ms / 1e3:
+            for _ in range(16):
+                step(i)
+                i += 1
+            torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop() if clocks else None
+    impl = dsc.attn_impl()
+    kept_past = P if stride <= 1 else ((cfg.past_frames + stride - 1) // stride) * tpf
+    dsc.close()
+    t_max = max_over_ranks(total_ms, world)
+    units = S * N
+    bytes_step = units * decode_bytes_per_unit(cfg, n_self, n_q, kept_past)
+    attn_ms = prof["ms_attend"] + prof["ms_build"]
+    pk = peaks()
+    achieved = bytes_step * args.steps / (attn_ms / 1e3) / 1e9 if attn_ms > 0 else None
+    value = cfg.num_streams * args.steps / (t_max / 1e3)
+    return {
+        "metric": "decode tokens/s (one token per stream per step, all layers) and HBM GB/s", "value": round(value, 2),
+        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32", "data": "synthetic",
+        "config": dict(config_dict(cfg, args, world), decode_n_q=n_q, decode_n_self=n_self, past_stride=stride,
+                       kept_past_tokens=kept_past,
+                       l2=("flushed between steps (read-only flush of 2x L2)" if flush else "inputs larger than L2 (ring %.2f GB)" % (ring_bytes / 1e9))),
+        "value_is": "aggregate decode tokens/s over all streams (each token passes every layer of the handle)",
+        "roofline": {"bound": "hbm", "kernel": impl.get("attend") if isinstance(impl, dict) else str(impl),
+                     "achieved": round(achieved, 1) if achieved else None, "peak": pk["hbm_gbs"],
+                     "peak_source": pk["source"] + " HBM copy", "unit": "GB/s",
+                     "frac": round(achieved / pk["hbm_gbs"], 4) if achieved else None, "traffic": None,
+                     "algorithmic_bytes_per_step": bytes_step, "launches": prof["n_build"] + prof["n_attend"]},
+        "gpu_launches": prof["kernel_launches"], "attn_impl": impl, "clocks": clk,
+        "e2e": {"skipped": "decode mode times the device-resident path only"},
+    }
 
 
 def run_e2e(args, cfg, lcfg, dsc, S, dev, stream, world, kvsplit):
@@ -609,7 +740,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="streams", choices=["streams", "kvsplit", "context"],
+    ap.add_argument("--mode", default="streams", choices=["streams", "kvsplit", "context", "decode"],
                     help="streams: P1 stream partition (default); kvsplit: P2 KV-head split of one stream; "
                          "context: P3 key-range split of one stream's attend (NEXT-4)")
     ap.add_argument("--layer-seq", action="store_true",
@@ -623,6 +754,10 @@ def main():
     ap.add_argument("--approx", type=int, default=0,
                     help="> 0: approximate instant cache refreshed every APPROX steps (SURVEY NEXT-3), split calls")
     ap.add_argument("--instant-frames", type=int, default=None, help="override l_I of the config (frames)")
+    ap.add_argument("--decode-gen", type=int, default=16, help="decode mode: tokens generated so far (self = q + G)")
+    ap.add_argument("--decode-nq", type=int, default=1, help="decode mode: query rows per launch")
+    ap.add_argument("--decode-stride", type=int, default=1,
+                    help="decode mode: keep every STRIDE-th past frame (zeta_decode, PAPER.md:695)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
@@ -650,9 +785,9 @@ def main():
         print(json.dumps(run_reference(args, cfg)), flush=True)
         return 0
     world, rank, local = dist_setup(args.gpus)
-    line = run_ours(args, cfg, world, rank, local)
+    line = run_decode(args, cfg, world, rank, local) if args.mode == "decode" else run_ours(args, cfg, world, rank, local)
     if rank == 0:
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and args.mode != "decode":
             line["cpu_baseline"] = oracle_sample(cfg, args.cpu_budget)
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -298,6 +298,20 @@ dscache_status dscache_decode(dscache_t h, int32_t layer_begin, int32_t layer_co
                               const void* q, const void* k_self, const void* v_self, int32_t n_self,
                               int32_t n_q, void* o, void* stream);
 
+/* Decoding over a sampled cumulative cache (zeta_decode: "we also sample the
+ * cumulative KV cache at 0.5 FPS during decoding"; reading Q24): as dscache_decode,
+ * but the past segment keeps only every past_stride-th frame of U, anchored at its newest
+ * frame (frames j = n_past-1, n_past-1-stride, ... >= 0, oldest first); the kept keys get
+ * contiguous ids: sink 0..A-1, kept past A.., instant, then self.
+ * past_stride = 1 is dscache_decode.  The memory-bound decode kernel serves bf16, d = 128,
+ * split-half RoPE and n_q * Hq/Hkv <= 16 (one 16-row tile per kv head, all q heads of the
+ * group sharing every K/V byte read); other decodes run through the attention kernel and
+ * accept past_stride = 1 only (E_CONFIG otherwise).  E_ARG for past_stride < 1; other
+ * errors as dscache_decode (the position check uses the kept past). */
+dscache_status dscache_decode_sampled(dscache_t h, int32_t layer_begin, int32_t layer_count,
+                                      const void* q, const void* k_self, const void* v_self, int32_t n_self,
+                                      int32_t n_q, int32_t past_stride, void* o, void* stream);
+
 /* Cumulative-update attention of Eq. 5: at step t
  * the input X_{t-l_I} that just left the buffer is encoded as phi(X_{t-l_I},
  * [C_a, zeta(U_{t-1})]); this call runs its attention: each of the tpf tokens of frame

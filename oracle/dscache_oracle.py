@@ -26,7 +26,8 @@ What it computes (per stream s, per layer r; everything in float64):
   every `period` steps, the newest frame's rows alone in between, older rows reused
   (instant_cache_output_approx);
 * decoding over C_{t+1}: the last tokens of [query chunk | generated
-  tokens] attend over [C_a, U, I, self] (SURVEY NEXT-2);
+  tokens] attend over [C_a, U, I, self], optionally with U sampled at a
+  frame stride (decode_output_sampled, PAPER.md:695);
 * the cumulative-update attention inside phi(X_{t-l_I}, [C_a, zeta(U_{t-1})]) of
   Eq. 5: the input leaving the buffer attends to the sink, the
   newest l_L frames of U_{t-1} and itself (SURVEY NEXT-1);
@@ -368,6 +369,20 @@ def decode_output(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], fram
     pos_k = np.arange(ks.shape[0])
     pos_q = ks.shape[0] - q_last.shape[0] + np.arange(q_last.shape[0])
     return gqa_attention(np.asarray(q_last, np.float64), pos_q, ks, vs, pos_k, theta, style)
+
+
+def decode_output_sampled(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], frame_kv: FrameFn,
+                          q_last: np.ndarray, k_self: np.ndarray, v_self: np.ndarray, stride: int, theta: float,
+                          style: int = SPLIT_HALF) -> np.ndarray:
+    """Decoding over a sampled cumulative cache ("sample the cumulative KV cache
+    at 0.5 FPS during decoding"; reading Q24): of U_t (oldest first) keep every
+    stride-th frame counting back from the newest, then decode exactly as decode_output over
+    [sink | kept past | instant | self] with ids consecutive from 0."""
+    U = list(sched.past_frames)
+    kept = U[::-1][::stride][::-1]
+    sampled = StepSchedule(sched.t, list(sched.instant_frames), kept, list(sched.evicted), sched.tokens_per_frame,
+                           sched.sink_tokens)
+    return decode_output(sampled, sink, frame_kv, q_last, k_self, v_self, theta, style)
 
 
 def cumulative_update_output(t: int, instant_frames: int, past_frames: int, active_frames: int,

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdscache.so")
-SOURCES = ["dscache_api.cu", "kernels_common.cu", "attn_fa.cu", "sched.cu"]
+SOURCES = ["dscache_api.cu", "kernels_common.cu", "attn_fa.cu", "sched.cu", "decode.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

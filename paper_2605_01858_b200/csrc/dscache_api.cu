@@ -92,6 +92,7 @@ struct dscache_s {
   std::vector<int> approx_lc;
   int* dbg_build = nullptr;
   int* dbg_attend = nullptr;
+  int* dec_counters = nullptr;   // decode split-KV tickets, one per (stream, layer, kv head), zero at rest
   int poison = 0;
   long long* trace = nullptr;
   int ntrace = 0;
@@ -346,6 +347,7 @@ dscache_status dscache_destroy(dscache_t h) {
   cudaFree(h->rope);
   cudaFree(h->stage_k); cudaFree(h->stage_v);
   cudaFree(h->bstage_k); cudaFree(h->bstage_v);
+  cudaFree(h->dec_counters);
   dsc::sched_cache_free(h->sched);
   delete h;
   return DSCACHE_OK;
@@ -617,9 +619,97 @@ dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q
   return attend_common(h, lb, lc, q, k_self, v_self, n_q, n_q, o, stream, true);
 }
 
+namespace {
+// The memory-bound decode kernel (decode.cu) serves bf16, d = 128, split-half RoPE and up to
+// 16 query rows (n_q * Hq/Hkv) per kv head; anything else runs through the attention kernel.
+bool decode_kernel_ok(dscache_t h, int n_q) {
+  return tc_eligible(h->cfg) && n_q * (h->cfg.num_q_heads / h->cfg.num_kv_heads) <= 16;
+}
+
+dscache_status run_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self, const void* v_self,
+                          int32_t n_self, int32_t n_q, int32_t stride, void* o, cudaStream_t st) {
+  dscache_status s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  if (!h->sink_filled[lb] || h->frames[lb] < 1)
+    return fail(DSCACHE_E_STATE, "decode before the sink and the first frame were appended");
+  if (n_q < 1 || n_q > n_self) return fail(DSCACHE_E_ARG, "need 1 <= n_q <= n_self");
+  if (!q || !k_self || !v_self || !o) return fail(DSCACHE_E_ARG, "null q/k_self/v_self/o");
+  const dscache_config& c = h->cfg;
+  const Schedule sc = h->schedule(lb);
+  const int tpf = c.tokens_per_frame;
+  const int past_frames = sc.P_t / tpf;
+  const int kept = (past_frames + stride - 1) / stride;
+  const int64_t n_keys = (int64_t)c.sink_tokens + (int64_t)kept * tpf + sc.C_t + n_self;
+  if (n_keys > c.max_position) return fail(DSCACHE_E_POS_OVERFLOW, "A + kept past + C_t + n_self exceeds max_position");
+  DeviceGuard dg(c.device);
+  dsc::DecodeParams p{};
+  p.P = c.num_streams * lc; p.layer_count = lc; p.layer_begin = lb; p.N_total = c.num_layers;
+  p.Hq = c.num_q_heads; p.Hkv = c.num_kv_heads; p.grp = c.num_q_heads / c.num_kv_heads;
+  p.q = q; p.o = o; p.n_q = n_q;
+  p.sink_k = h->sink_k; p.sink_v = h->sink_v; p.A = c.sink_tokens;
+  p.ring_k = h->ring_k; p.ring_v = h->ring_v; p.R = h->R; p.Rp = h->Rp;
+  p.past_start = sc.ring_start; p.tpf = tpf; p.past_frames = past_frames; p.stride = stride; p.kept_frames = kept;
+  p.inst_start = sc.inst_start; p.inst_count = sc.C_t;
+  p.self_k = k_self; p.self_v = v_self; p.n_self = n_self;
+  p.n_keys = (int)n_keys;
+  p.q_pos0 = (int)(n_keys - n_q);
+  p.rope_pairs = reinterpret_cast<const float4*>(h->rope + (size_t)h->npos * (c.head_dim / 2));
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c.head_dim));
+  p.dbg_pos = h->dbg_attend;
+  p.dbg_M = std::max(h->C, c.max_query_tokens); p.dbg_A = c.sink_tokens; p.dbg_R = h->R;
+  p.dbg_len = c.sink_tokens + h->R + 2 * p.dbg_M;
+  // one wave of CTAs: split each (problem, kv head)'s keys when there are fewer of them than
+  // SMs, keeping at least one 16-key warp tile per warp in every split
+  const int units = p.P * p.Hkv;
+  const int wtiles = (int)((n_keys + 15) / 16);
+  int splits = 1;
+  if (units < h->num_sms) splits = std::max(1, std::min((h->num_sms + units - 1) / units, wtiles / 8));
+  p.wtiles_per_split = (wtiles + splits - 1) / splits;
+  splits = (wtiles + p.wtiles_per_split - 1) / p.wtiles_per_split;
+  p.n_splits = splits;
+  StreamScratch ws;
+  if (splits > 1) {
+    if (!h->dec_counters) {
+      const size_t n = (size_t)c.num_streams * c.num_layers * c.num_kv_heads;
+      if (cudaMalloc(&h->dec_counters, n * sizeof(int)) != cudaSuccess) { cudaGetLastError(); return fail(DSCACHE_E_OOM, "decode counters"); }
+      if (cudaMemset(h->dec_counters, 0, n * sizeof(int)) != cudaSuccess) return fail(DSCACHE_E_CUDA, "decode counters");
+    }
+    const size_t rows = (size_t)p.P * n_q * c.num_q_heads;
+    if (!ws.alloc((size_t)splits * rows * (c.head_dim + 1) * sizeof(float), st))
+      return fail(DSCACHE_E_OOM, "decode split-KV workspace");
+    p.ws_o = static_cast<float*>(ws.ptr);
+    p.ws_lse = p.ws_o + (size_t)splits * rows * c.head_dim;
+    p.counters = h->dec_counters;
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->prof) { e0 = h->take_event(); e1 = h->take_event(); cudaEventRecord(e0, st); }
+  cudaError_t e = dsc::launch_decode(p, st);
+  h->launches++;
+  if (h->prof) {
+    cudaEventRecord(e1, st);
+    h->pending.push_back({e0, e1, 1});
+  }
+  if (e != cudaSuccess) return fail(DSCACHE_E_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
+  return DSCACHE_OK;
+}
+}  // namespace
+
 dscache_status dscache_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                               const void* v_self, int32_t n_self, int32_t n_q, void* o, void* stream) {
+  return dscache_decode_sampled(h, lb, lc, q, k_self, v_self, n_self, n_q, 1, o, stream);
+}
+
+dscache_status dscache_decode_sampled(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                                      const void* v_self, int32_t n_self, int32_t n_q, int32_t past_stride, void* o,
+                                      void* stream) {
   if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "decode");
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  if (past_stride < 1) return fail(DSCACHE_E_ARG, "past_stride must be >= 1");
+  if (decode_kernel_ok(h, n_q) && h->impl_attend == DSCACHE_IMPL_TC)
+    return run_decode(h, lb, lc, q, k_self, v_self, n_self, n_q, past_stride, o, (cudaStream_t)stream);
+  if (past_stride != 1)
+    return fail(DSCACHE_E_CONFIG, "past_stride > 1 needs the decode kernel (bf16, d = 128, split-half RoPE, "
+                                  "n_q * Hq/Hkv <= 16)");
   return attend_common(h, lb, lc, q, k_self, v_self, n_self, n_q, o, stream, false);
 }
 

@@ -84,6 +84,31 @@ struct AttnParams {
   CUtensorMap tmap_v;
 };
 
+// Memory-bound decode: n_q * grp <= 16 query rows of one
+// (problem, kv head) over the logical keys [sink A | kept past | instant | self], ids 0.. in
+// that order.  The past is sampled at a frame stride anchored at its newest frame
+// (zeta_decode; stride 1 keeps every frame): kept frame kk (0 = oldest kept)
+// is past frame j = past_frames - 1 - stride * (kept_frames - 1 - kk), tokens at ring slots
+// (past_start + j * tpf + tok) mod R.  Instant token u is slot (inst_start + u) mod R.
+struct DecodeParams {
+  int P, layer_count, layer_begin, N_total, Hq, Hkv, grp;
+  const void* q; void* o; int n_q;             // [P][n_q][Hq][d]
+  const void* sink_k; const void* sink_v; int A;
+  const void* ring_k; const void* ring_v; int R, Rp;
+  int past_start, tpf, past_frames, stride, kept_frames;
+  int inst_start, inst_count;
+  const void* self_k; const void* self_v; int n_self;   // [P][n_self][Hkv][d]
+  int q_pos0;                                  // id of query row 0 (its token is self token n_self - n_q)
+  int n_keys;                                  // A + kept_frames * tpf + inst_count + n_self
+  const float4* rope_pairs;
+  float scale_log2;
+  int n_splits, wtiles_per_split;              // key range split in 16-key warp tiles
+  float* ws_o; float* ws_lse;                  // [n_splits][P*n_q*Hq][d], [n_splits][P*n_q*Hq]
+  int* counters;                               // per (stream, layer, kv head) ticket, zero between launches
+  int* dbg_pos; int dbg_len, dbg_A, dbg_R, dbg_M;   // debug id export (kv head 0), null = off
+};
+cudaError_t launch_decode(const DecodeParams& p, cudaStream_t st);
+
 struct AppendParams {
   const void* k; const void* v;              // [S][lc][n][Hkv][d]
   void* dst_k; void* dst_v;                  // ring [S][N][Hkv][Rp][d] or sink [S][N][Hkv][A][d]

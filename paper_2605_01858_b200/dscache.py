@@ -58,7 +58,7 @@ class State(ctypes.Structure):
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
            "dscache_append_past", "dscache_build_instant_ext", "dscache_attend_ext",
            "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest",
-           "dscache_instant_approx_rows", "dscache_build_instant_approx", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
+           "dscache_instant_approx_rows", "dscache_build_instant_approx", "dscache_decode_sampled", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
            "dscache_attn_impl", "dscache_watchdog_read", "dscache_last_error", "dscache_attend_partial", "dscache_combine_partials",
            "dscache_build_instant_boost", "dscache_attend_boost", "dscache_attend_peers",
@@ -85,6 +85,7 @@ def load_library(path: str = LIB_PATH):
         "dscache_attend": ([P, I32, I32, P, P, P, I32, P, P], I32),
         "dscache_update_attend": ([P, I32, I32, P, P, I32, P], I32),
         "dscache_decode": ([P, I32, I32, P, P, P, I32, I32, P, P], I32),
+        "dscache_decode_sampled": ([P, I32, I32, P, P, P, I32, I32, I32, P, P], I32),
         "dscache_build_instant_newest": ([P, I32, I32, P, P, P], I32),
         "dscache_instant_approx_rows": ([P, I32, I32, I32, P, ctypes.POINTER(ctypes.c_int32)], I32),
         "dscache_build_instant_approx": ([P, I32, I32, I32, P, I32, P, P], I32),
@@ -481,9 +482,11 @@ class DSCache:
         return o_ring
 
     def decode(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, o: Optional[torch.Tensor] = None,
-               layer_begin: int = 0, layer_count: Optional[int] = None, stream=None) -> torch.Tensor:
+               layer_begin: int = 0, layer_count: Optional[int] = None, stream=None,
+               past_stride: int = 1) -> torch.Tensor:
         """Decode (NEXT-2): q [S][lc][n_q][Hq][d] = the last n_q tokens of the self segment
-        k_self/v_self [S][lc][n_self][Hkv][d] (query chunk + generated tokens)."""
+        k_self/v_self [S][lc][n_self][Hkv][d] (query chunk + generated tokens).  past_stride > 1
+        keeps every past_stride-th past frame (zeta_decode)."""
         lb, lc = self._layers(layer_begin, layer_count)
         c = self.cfg
         n_q, n_self = int(q.shape[2]), int(k_self.shape[2])
@@ -493,8 +496,8 @@ class DSCache:
         if o is None:
             o = torch.empty(q.shape, dtype=self.torch_dtype, device=self.device)
         self._t(o, "o", q.shape)
-        _check(_lib.dscache_decode(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_self, n_q, _ptr(o),
-                                   _stream_ptr(stream)))
+        _check(_lib.dscache_decode_sampled(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_self, n_q,
+                                           int(past_stride), _ptr(o), _stream_ptr(stream)))
         return o
 
     def update_attend(self, q_upd: torch.Tensor, o_upd: Optional[torch.Tensor] = None,

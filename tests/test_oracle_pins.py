@@ -864,3 +864,47 @@ def test_approx_differs_from_exact_between_refreshes():
     ref = O.instant_cache_output(sch, inp.sink(), inp.frame_kv, inp.instant_q(t, sch.C_t), cfg.rope_theta)
     assert np.abs(got[:-tpf] - ref[:-tpf]).max() > 1e-3
     assert np.allclose(got[-tpf:], ref[-tpf:], rtol=0, atol=1e-13)
+
+
+# --------------------------------------------------------------------------- sampled decode (zeta_decode)
+def test_decode_sampled_stride_one_is_decode():
+    cfg = synth.CONFIGS["c1"]
+    inp = StreamInputs(cfg, 0, 0)
+    sch = step_schedule(cfg, 12)
+    q, ks, vs = inp.query(12)
+    a = O.decode_output(sch, inp.sink(), inp.frame_kv, q[-1:], ks, vs, cfg.rope_theta)
+    b = O.decode_output_sampled(sch, inp.sink(), inp.frame_kv, q[-1:], ks, vs, 1, cfg.rope_theta)
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("stride", [2, 3, 50])
+def test_decode_sampled_brute_force(stride):
+    """PAPER.md:695 ("sample the cumulative KV cache at 0.5 FPS during decoding", stride 2 at
+    1 FPS): pure-Python attention of one decode token over [sink | past frames f with
+    (newest past frame - f) % stride == 0 | instant | self], ids consecutive from 0.  A
+    stride beyond l_U keeps the newest past frame alone."""
+    cfg = synth.StreamConfig("dec", 96, 1, 1, 4, 2, 8, 1e4, 2, 2, 6, 2, 3, 14, "fp32", 1.0)
+    inp = StreamInputs(cfg, 0, 0)
+    t = 12
+    sch = step_schedule(cfg, t)
+    sk, sv = inp.sink()
+    q, kq, vq = inp.query(t)
+    grp = cfg.num_q_heads // cfg.num_kv_heads
+    newest = t - cfg.instant_frames                      # newest frame of U_t (Eq. 3 / 5)
+    oldest = newest - cfg.past_frames + 1
+    kept = [f for f in range(oldest, newest + 1) if (newest - f) % stride == 0]
+    o = O.decode_output_sampled(sch, (sk, sv), inp.frame_kv, q[-1:], kq, vq, stride, cfg.rope_theta)
+    if stride > cfg.past_frames:
+        assert kept == [newest]
+    for h in range(cfg.num_q_heads):
+        gh = h // grp
+        keys = [(j, list(sk[j, gh]), list(sv[j, gh])) for j in range(cfg.sink_tokens)]
+        n = cfg.sink_tokens
+        for f in kept + list(range(t - cfg.instant_frames + 1, t + 1)):
+            fk, fv = inp.frame_kv(f)
+            for j in range(cfg.tokens_per_frame):
+                keys.append((n, list(fk[j, gh]), list(fv[j, gh]))); n += 1
+        for j in range(len(kq)):
+            keys.append((n, list(kq[j, gh]), list(vq[j, gh]))); n += 1
+        ref = _brute_attend(list(q[-1, h]), n - 1, keys, cfg.rope_theta)
+        assert np.abs(np.array(ref) - o[0, h]).max() < 1e-12

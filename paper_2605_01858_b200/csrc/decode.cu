@@ -4,15 +4,18 @@
 //
 // One CTA = one (problem, kv head, key split); its n_q * grp <= 16 query rows (every q head
 // of the GQA group, every query token) form ONE m16 tile, so each K/V byte is read from HBM
-// once per kv head and feeds all grp q heads.  The key range is cut into 16-key warp tiles;
-// each of the 8 warps streams its own tiles through a private 3-stage cp.async ring
-// (8 KB per stage: 16 rows of K and of V, 16-byte chunks XOR-swizzled by row), so the main
-// loop has no CTA-wide barrier.  Per warp tile:
-//   * K is rotated by R(j), j = key - n0 (0..15), in the mma B fragments (registers), from
-//     a 16-row table slice that stays in L1;
-//   * the queries are rotated by R(m - n0) straight into mma.sync A fragments, so
-//     (R(m - n0) q) . (R(j) k) = (R(m) q) . (R(n0 + j) k) -- the use-time RoPE of
-//     Def. 4.1 without a per-key trip to the full position table;
+// once per kv head and feeds all grp q heads.  The CTA streams 128-key tiles through a
+// 3-stage ring (64 KB of K and V per stage in the TMA 128-byte swizzle, plus the two RoPE
+// table rows that rotate the queries for that tile, one mbarrier per stage): a tile that is
+// one consecutive run of ring slots (the common case) is four TMA boxes; sink / self /
+// sampled-past boundary tiles fall back to per-thread cp.async into the same layout.
+// Per tile:
+//   * the queries are rotated once by R(m - n0) (n0 = the tile's first id) into a shared
+//     bf16 tile that every warp reads with ldmatrix;
+//   * warp w owns keys 16w .. 16w+15 of the tile and rotates their K by R(j), j = 16w + ..,
+//     in its mma B fragments, with the R(j) table held in registers for the whole kernel:
+//     (R(m - n0) q) . (R(j) k) = (R(m) q) . (R(n0 + j) k) -- the use-time RoPE of Def. 4.1
+//      without any per-key table traffic;
 //   * S = Q K^T (16 x 16 x 128) and O += P V (16 x 128 x 16) on mma.sync.m16n8k16 bf16 with
 //     fp32 accumulation (the work is a 16-row GEMV pair, HBM-bound; tcgen05's 128-row M
 //     would be 7/128 used at n_q = 1), online softmax in the log2 domain per warp.
@@ -28,22 +31,27 @@ namespace dsc {
 namespace {
 
 constexpr int kWarps = 8;
-constexpr int kKeys = 16;                        // keys per warp tile
+constexpr int kWarpKeys = 16;                    // keys of a tile each warp owns
+constexpr int kTileKeys = kWarps * kWarpKeys;    // 128 keys per CTA tile
 constexpr int kStages = 3;
 constexpr int kRowBytes = 256;                   // d = 128 bf16
 constexpr int kTabBytes = 2 * 512;               // RoPE rows R(m - n0) of query tokens 0, 1
-constexpr int kStageBytes = 2 * kKeys * kRowBytes + kTabBytes;   // K, V, then the q table rows
-constexpr int kWarpBytes = kStages * kStageBytes;
-constexpr int kSmemBytes = kWarps * kWarpBytes;      // 216 KB; the merge reuses it
+// stage = K then V, each as two 64-column halves of [128 rows][128 B] in the TMA 128-byte
+// swizzle (16-byte chunk c of row r at r*128 + ((c ^ (r & 7)) << 4)), then the table rows
+constexpr int kHalfBytes = kTileKeys * 128;
+constexpr int kVOff = 2 * kHalfBytes;
+constexpr int kTabOff = 4 * kHalfBytes;
+constexpr int kStageBytes = kTabOff + kTabBytes;   // 65 KB (a multiple of 1024: SW128 alignment)
+constexpr int kQRawOff = kStages * kStageBytes;  // fp32 raw queries [16][128]
+constexpr int kQRotOff = kQRawOff + 16 * 128 * 4;   // bf16 rotated queries [16][256 B], swizzled
+constexpr int kBarOff = kQRotOff + 16 * kRowBytes;  // one mbarrier per stage
+constexpr int kSmemBytes = kBarOff + 64;            // 211 KB; the merge reuses the stages
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -66,9 +74,42 @@ __device__ __forceinline__ uint32_t pk(float lo, float hi) {
 __device__ __forceinline__ float2 unpk(uint32_t w) {
   return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
 }
-// byte offset of 16-byte chunk c of row r inside a [16][256 B] tile (chunk XOR row swizzle:
+// byte offset of 16-byte chunk c of row r inside a [rows][256 B] tile (chunk XOR row swizzle:
 // the 8 rows an ldmatrix phase reads land in 8 distinct bank groups)
 __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * kRowBytes + ((c ^ (r & 7)) << 4)); }
+// byte offset of 16-byte chunk c (0..15) of key row r inside a K or V stage tile (SW128 halves)
+__device__ __forceinline__ uint32_t swz2(int r, int c) {
+  return (uint32_t)((c >> 3) * kHalfBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+__device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_cp_arrive(uint32_t bar) {   // arrives once this thread's cp.asyncs land
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 
 // source row of logical key x of (problem pp, head row hr): [sink | kept past | instant | self]
 __device__ __forceinline__ long long key_row(const DecodeParams& p, int pp, long long hr, int g, int x, int& kind,
@@ -95,61 +136,73 @@ __device__ __forceinline__ long long key_row(const DecodeParams& p, int pp, long
   return ((long long)pp * p.n_self + x) * p.Hkv + g;
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeParams p) {
+__global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int split = blockIdx.x % p.n_splits;
   const int unit = blockIdx.x / p.n_splits;
   const int g = unit % p.Hkv, pp = unit / p.Hkv;
   const int s = pp / p.layer_count, l = pp % p.layer_count;
   const long long hr = ((long long)s * p.N_total + p.layer_begin + l) * p.Hkv + g;   // head row
-  const __nv_bfloat16* Q = reinterpret_cast<const __nv_bfloat16*>(p.q);
   const int rows = p.n_q * p.grp;                 // <= 16
-  const int wt_total = (p.n_keys + kKeys - 1) / kKeys;
-  const int wt0 = split * p.wtiles_per_split;
-  const int wt1 = min(wt_total, wt0 + p.wtiles_per_split);
+  const int tiles = (p.n_keys + kTileKeys - 1) / kTileKeys;
+  const int tb0 = split * p.tiles_per_split;
+  const int tb1 = min(tiles, tb0 + p.tiles_per_split);
+  const int n_my = max(tb1 - tb0, 0);
   int* const dbgp = (p.dbg_pos && g == 0) ? p.dbg_pos + (hr / p.Hkv) * p.dbg_len : nullptr;
+  const uint32_t sbase = smem_u32(smem);
 
-  // raw queries of this lane's fragment rows (g8 = lane/4 and g8 + 8), k-step kk dims
-  // 16kk + {2t, 2t+1, 2t+8, 2t+9}; row r = qi * grp + hh
-  const int g8 = lane >> 2, t4 = lane & 3;
-  float qf[2][8][4];
-  int qpos[2], qrow[2];   // query id and query token index of the lane's two fragment rows
-#pragma unroll
-  for (int h2 = 0; h2 < 2; ++h2) {
-    const int r = g8 + 8 * h2;
-    const bool valid = r < rows;
-    const int qi = valid ? r / p.grp : 0, hh = valid ? r % p.grp : 0;
-    qpos[h2] = valid ? p.q_pos0 + qi : -1;
-    qrow[h2] = qi;
-    const __nv_bfloat16* qr = Q + (((long long)pp * p.n_q + qi) * p.Hq + g * p.grp + hh) * 128;
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const float2 a = valid ? unpk(*reinterpret_cast<const uint32_t*>(qr + 16 * kk + 2 * t4)) : make_float2(0.f, 0.f);
-      const float2 b = valid ? unpk(*reinterpret_cast<const uint32_t*>(qr + 16 * kk + 2 * t4 + 8)) : make_float2(0.f, 0.f);
-      qf[h2][kk][0] = a.x; qf[h2][kk][1] = a.y; qf[h2][kk][2] = b.x; qf[h2][kk][3] = b.y;
-    }
-  }
-  const bool two_halves = rows > 8;
-  if (dbgp && split == 0 && warp == 0 && lane < p.n_q) dbgp[p.dbg_A + p.dbg_R + p.dbg_M + lane] = p.q_pos0 + lane;
-
-  // per-warp cp.async ring: lanes 2r, 2r+1 load key r of the warp tile, lane parity picking
-  // the even / odd 16-byte chunks, so each copy instruction covers whole 32-byte sectors of
-  // 16 rows; one source-row lookup per lane per tile
-  unsigned char* wbuf = smem + warp * kWarpBytes;
-  const uint32_t wbase = smem_u32(wbuf);
+  // ---- cp.async producer (all 256 threads): threads 2r, 2r+1 load key r of the tile, the
+  // thread parity picking the even / odd 16-byte chunks (whole 32-byte sectors per copy)
   const __nv_bfloat16* SK = reinterpret_cast<const __nv_bfloat16*>(p.sink_k);
   const __nv_bfloat16* SV = reinterpret_cast<const __nv_bfloat16*>(p.sink_v);
   const __nv_bfloat16* RK = reinterpret_cast<const __nv_bfloat16*>(p.ring_k);
   const __nv_bfloat16* RV = reinterpret_cast<const __nv_bfloat16*>(p.ring_v);
   const __nv_bfloat16* XK = reinterpret_cast<const __nv_bfloat16*>(p.self_k);
   const __nv_bfloat16* XV = reinterpret_cast<const __nv_bfloat16*>(p.self_v);
-  const int lr = lane >> 1, lhalf = lane & 1;
-  auto issue = [&](int it, int stage) {
-    const int wt = wt0 + warp + it * kWarps;
-    if (wt < wt1) {
-      const uint32_t sb = wbase + stage * kStageBytes;
-      const int x = wt * kKeys + lr;
+  const int lr = tid >> 1, lhalf = tid & 1;
+  // ring keys [ring0, ring1): kept past then instant, slots consecutive from past_start when
+  // every past frame is kept (stride 1); with a stride, runs inside one kept frame or inside
+  // the instant window are consecutive
+  const int ring0 = p.A, past_end = p.A + p.kept_frames * p.tpf, ring1 = past_end + p.inst_count;
+  const int n_tab = min(p.n_q, 2);
+  if (tid < kStages) bar_init(sbase + kBarOff + 8 * tid, kWarps * 32 + 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  auto issue = [&](int it) {
+    if (it >= n_my) return;
+    const int tile = tb0 + it;
+    const int stage = it % kStages;
+    const uint32_t sb = sbase + stage * kStageBytes;
+    const uint32_t bar = sbase + kBarOff + 8 * stage;
+    const int n0 = tile * kTileKeys, n1 = n0 + kTileKeys - 1;
+    bool tma = n0 >= ring0 && n1 < ring1;
+    if (tma && p.stride != 1 && n0 < past_end)
+      tma = n1 < past_end && (n0 - p.A) / p.tpf == (n1 - p.A) / p.tpf;
+    // query tokens 0 and 1's rotation rows R(m - n0): one bulk copy (rows base, base + 1; the
+    // rows of a query token before the tile are never used: all its keys here are masked)
+    const int base = p.q_pos0 - n0;
+    const uint32_t tab_bytes = base >= 0 ? n_tab * 512 : 512;
+    if (tma) {
+      int kind = 0, slot = 0;
+      const long long row0 = key_row(p, pp, hr, g, n0, kind, slot);
+      if (tid == 0) {
+        bar_arrive_tx(bar, 4 * kHalfBytes + tab_bytes);
+        tma2d(sb, &p.tmap_k, 0, (int)row0, bar);
+        tma2d(sb + kHalfBytes, &p.tmap_k, 64, (int)row0, bar);
+        tma2d(sb + kVOff, &p.tmap_v, 0, (int)row0, bar);
+        tma2d(sb + kVOff + kHalfBytes, &p.tmap_v, 64, (int)row0, bar);
+        if (base >= 0) bulk_g2s(sb + kTabOff, p.rope_pairs + (long long)base * 32, tab_bytes, bar);
+        else bulk_g2s(sb + kTabOff + 512, p.rope_pairs, 512, bar);
+      }
+      bar_arrive(bar);
+      if (dbgp && lhalf == 0) {
+        int sl = slot + lr;
+        if (sl >= p.R) sl -= p.R;
+        dbgp[p.dbg_A + sl] = n0 + lr;
+      }
+    } else {
+      const int x = n0 + lr;
       const bool valid = x < p.n_keys;
       int kind = 0, slot = 0;
       const long long row = valid ? key_row(p, pp, hr, g, x, kind, slot) : 0;
@@ -158,97 +211,128 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodePara
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int c = 2 * j + lhalf;
-        cp16(sb + swz(lr, c), ks + 8 * c, valid);
-        cp16(sb + kKeys * kRowBytes + swz(lr, c), vs + 8 * c, valid);
+        cp16(sb + swz2(lr, c), ks + 8 * c, valid);
+        cp16(sb + kVOff + swz2(lr, c), vs + 8 * c, valid);
       }
+      if (tid == 0) {
+        bar_arrive_tx(bar, tab_bytes);
+        if (base >= 0) bulk_g2s(sb + kTabOff, p.rope_pairs + (long long)base * 32, tab_bytes, bar);
+        else bulk_g2s(sb + kTabOff + 512, p.rope_pairs, 512, bar);
+      }
+      bar_cp_arrive(bar);
       if (dbgp && valid && lhalf == 0)
         dbgp[kind == 0 ? slot : kind == 1 ? p.dbg_A + slot : p.dbg_A + p.dbg_R + slot] = x;
-      // the table rows that rotate query tokens 0 and 1 for this tile, prefetched with it
-#pragma unroll
-      for (int qd = 0; qd < 2; ++qd)
-        if (qd < p.n_q) {
-          const int delta = max(p.q_pos0 + qd - wt * kKeys, 0);
-          cp16(sb + 2 * kKeys * kRowBytes + qd * 512 + lane * 16, p.rope_pairs + (long long)delta * 32 + lane, true);
-        }
     }
-    cp_commit();   // possibly empty: keeps the group count uniform
   };
+#pragma unroll 1
+  for (int i = 0; i < kStages - 1; ++i) issue(i);
+
+  // ---- raw queries (fp32, smem) and the rotated-query tile (zero rows beyond `rows`)
+  float* qraw = reinterpret_cast<float*>(smem + kQRawOff);
+  unsigned char* qrot = smem + kQRotOff;
+  const __nv_bfloat16* Q = reinterpret_cast<const __nv_bfloat16*>(p.q);
+  for (int i = tid; i < 16 * 128; i += blockDim.x) {
+    const int r = i >> 7, d = i & 127;
+    float v = 0.f;
+    if (r < rows) {
+      const int qi = r / p.grp, hh = r % p.grp;
+      v = __bfloat162float(Q[(((long long)pp * p.n_q + qi) * p.Hq + g * p.grp + hh) * 128 + d]);
+    }
+    qraw[i] = v;
+  }
+  for (int i = tid; i < 16 * kRowBytes / 16; i += blockDim.x) reinterpret_cast<uint4*>(qrot)[i] = make_uint4(0, 0, 0, 0);
+  if (dbgp && split == 0 && tid < p.n_q) dbgp[p.dbg_A + p.dbg_R + p.dbg_M + tid] = p.q_pos0 + tid;
+
+  // ---- per-lane constants: fragment rows g8, g8 + 8 (their query ids), and the R(j) table
+  // of the lane's two keys (j = 16 warp + g8 (+8)) at its 16 frequencies f = 16kk + 8hf + 2t
+  const int g8 = lane >> 2, t4 = lane & 3;
+  int qpos[2];
+#pragma unroll
+  for (int h2 = 0; h2 < 2; ++h2) {
+    const int r = g8 + 8 * h2;
+    qpos[h2] = r < rows ? p.q_pos0 + r / p.grp : -1;
+  }
+  float4 kt[4][4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      kt[kk][e] = __ldg(p.rope_pairs + (kWarpKeys * warp + 8 * (e >> 1) + g8) * 32 + 8 * kk + 4 * (e & 1) + t4);
 
   float o[16][4];
 #pragma unroll
   for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
   float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+  // q rotation work of this thread: row qr_r, frequencies qr_f .. qr_f + 3
+  const int qr_r = tid >> 4, qr_f = (tid & 15) * 4;
 
-  const int my_tiles = wt1 - wt0 > warp ? (wt1 - wt0 - warp + kWarps - 1) / kWarps : 0;
-#pragma unroll 1
-  for (int i = 0; i < kStages - 1; ++i) issue(i, i);
-  for (int it = 0; it < my_tiles; ++it) {
-    issue(it + kStages - 1, (it + kStages - 1) % kStages);
-    cp_wait<kStages - 1>();
-    __syncwarp();
+  for (int it = 0; it < n_my; ++it) {
     const int stage = it % kStages;
-    const uint32_t kb = wbase + stage * kStageBytes, vb = kb + kKeys * kRowBytes;
-    const int n0 = (wt0 + warp + it * kWarps) * kKeys;
+    bar_wait(sbase + kBarOff + 8 * stage, (it / kStages) & 1);   // tile it landed (TMA or cp.async)
+    __syncthreads();                   // every warp is done with tile it-1
+    issue(it + kStages - 1);           // into the stage tile it-1 used
+    const uint32_t kb = sbase + stage * kStageBytes, vb = kb + kVOff;
+    const int n0 = (tb0 + it) * kTileKeys;
 
-    // queries rotated by R(m - n0) into A fragments (rows g8, g8 + 8)
-    uint32_t a[8][4];
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      if (h2 == 1 && !two_halves) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) a[kk][1] = a[kk][3] = 0u;
-        break;
+    // queries rotated by R(m - n0) (bf16, swizzled), shared by the 8 warps
+    if (qr_r < rows) {
+      const int qi = qr_r / p.grp;
+      const float4* ts;
+      if (qi < 2) {
+        ts = reinterpret_cast<const float4*>(smem + stage * kStageBytes + kTabOff + qi * 512);
+      } else {
+        ts = p.rope_pairs + (long long)max(p.q_pos0 + qi - n0, 0) * 32;
       }
-      const int delta = max(qpos[h2] - n0, 0);
-      const float4* tb = p.rope_pairs + (long long)delta * 32;
-      const float4* ts = reinterpret_cast<const float4*>(wbuf + stage * kStageBytes + 2 * kKeys * kRowBytes +
-                                                         qrow[h2] * 512);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {            // dims 16kk + 2t (+8 for hf = 1)
-          const float4 cs = qrow[h2] < 2 ? ts[8 * kk + t4 + 4 * hf] : __ldg(tb + 8 * kk + t4 + 4 * hf);
-          const float x0 = qf[h2][kk][2 * hf], x1 = qf[h2][kk][2 * hf + 1];
-          const float y0 = qf[h2][kk + 4][2 * hf], y1 = qf[h2][kk + 4][2 * hf + 1];
-          a[kk][2 * hf + h2] = pk(x0 * cs.x - y0 * cs.z, x1 * cs.y - y1 * cs.w);
-          a[kk + 4][2 * hf + h2] = pk(x0 * cs.z + y0 * cs.x, x1 * cs.w + y1 * cs.y);
-        }
-      }
+      const float4 c0 = ts[qr_f / 2], c1 = ts[qr_f / 2 + 1];
+      const float4 x = *reinterpret_cast<const float4*>(qraw + qr_r * 128 + qr_f);
+      const float4 y = *reinterpret_cast<const float4*>(qraw + qr_r * 128 + 64 + qr_f);
+      uint2 lo, hi;
+      lo.x = pk(x.x * c0.x - y.x * c0.z, x.y * c0.y - y.y * c0.w);
+      lo.y = pk(x.z * c1.x - y.z * c1.z, x.w * c1.y - y.w * c1.w);
+      hi.x = pk(x.x * c0.z + y.x * c0.x, x.y * c0.w + y.y * c0.y);
+      hi.y = pk(x.z * c1.z + y.z * c1.x, x.w * c1.w + y.w * c1.y);
+      *reinterpret_cast<uint2*>(qrot + swz(qr_r, qr_f >> 3) + (qr_f & 7) * 2) = lo;
+      *reinterpret_cast<uint2*>(qrot + swz(qr_r, 8 + (qr_f >> 3)) + (qr_f & 7) * 2) = hi;
     }
+    __syncthreads();                   // rotated queries ready
 
-    // S = Q K^T over the 16 keys (two n8 tiles).  The K B fragments are rotated by R(j) in
-    // registers (j = key within the tile: the lane holds keys g8 and 8 + g8, dims
-    // 16kk + 8hf + 2t, +1 in k-step kk and their split-half partners + 64 in k-step kk + 4)
+    // S = Q K^T over this warp's 16 keys; K B fragments rotated by R(j) in registers (the lane
+    // holds keys g8, 8 + g8 at dims 16kk + 8hf + 2t, +1 and their partners + 64 in kk + 4)
     float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     {
-      const int key = (lane & 7) + 8 * (lane >> 4);
+      const uint32_t qb = sbase + kQRotOff;
+      const int arow = (lane & 7) + 8 * ((lane >> 3) & 1), asel = lane >> 4;
+      const int key = kWarpKeys * warp + (lane & 7) + 8 * (lane >> 4);
       const int hsel = (lane >> 3) & 1;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        uint32_t lo[4], hi[4];
-        ldsm4(kb + swz(key, 2 * kk + hsel), lo[0], lo[1], lo[2], lo[3]);
-        ldsm4(kb + swz(key, 2 * (kk + 4) + hsel), hi[0], hi[1], hi[2], hi[3]);
+        uint32_t a0[4], a1[4], lo[4], hi[4];
+        ldsm4(qb + swz(arow, 2 * kk + asel), a0[0], a0[1], a0[2], a0[3]);
+        ldsm4(qb + swz(arow, 2 * (kk + 4) + asel), a1[0], a1[1], a1[2], a1[3]);
+        ldsm4(kb + swz2(key, 2 * kk + hsel), lo[0], lo[1], lo[2], lo[3]);
+        ldsm4(kb + swz2(key, 2 * (kk + 4) + hsel), hi[0], hi[1], hi[2], hi[3]);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {   // e = 2 * n-tile + hf
-          const float4 cs = __ldg(p.rope_pairs + (8 * (e >> 1) + g8) * 32 + 8 * kk + 4 * (e & 1) + t4);
+          const float4 cs = kt[kk][e];
           const float2 x = unpk(lo[e]), y = unpk(hi[e]);
           lo[e] = pk(x.x * cs.x - y.x * cs.z, x.y * cs.y - y.y * cs.w);
           hi[e] = pk(x.x * cs.z + y.x * cs.x, x.y * cs.w + y.y * cs.y);
         }
-        mma16816(sc[0], a[kk], lo[0], lo[1]);
-        mma16816(sc[1], a[kk], lo[2], lo[3]);
-        mma16816(sc[0], a[kk + 4], hi[0], hi[1]);
-        mma16816(sc[1], a[kk + 4], hi[2], hi[3]);
+        mma16816(sc[0], a0, lo[0], lo[1]);
+        mma16816(sc[1], a0, lo[2], lo[3]);
+        mma16816(sc[0], a1, hi[0], hi[1]);
+        mma16816(sc[1], a1, hi[2], hi[3]);
       }
     }
     // mask (beyond the keys, or after the row's own query id: causal inside the self
     // segment), online softmax in the log2 domain
+    const int kbase = n0 + kWarpKeys * warp + 2 * t4;
     float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int key = n0 + 8 * nt + 2 * t4 + (e & 1);
+        const int key = kbase + 8 * nt + (e & 1);
         const int h2 = e >> 1;
         const bool vis = key < p.n_keys && key <= qpos[h2];
         const float v = vis ? sc[nt][e] * p.scale_log2 : -INFINITY;
@@ -283,12 +367,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodePara
     // O = O * corr + P V (the rescale is skipped when no row's max moved: corr == 1 exactly)
     const bool rescale = __any_sync(0xffffffffu, corr[0] != 1.f || corr[1] != 1.f);
     {
-      const int key = (lane & 7) + 8 * ((lane >> 3) & 1);
+      const int key = kWarpKeys * warp + (lane & 7) + 8 * ((lane >> 3) & 1);
       const int csel = lane >> 4;
 #pragma unroll
       for (int nt = 0; nt < 16; nt += 2) {
         uint32_t b0, b1, b2, b3;
-        ldsm4t(vb + swz(key, nt + csel), b0, b1, b2, b3);
+        ldsm4t(vb + swz2(key, nt + csel), b0, b1, b2, b3);
         if (rescale) {
           o[nt][0] *= corr[0]; o[nt][1] *= corr[0]; o[nt][2] *= corr[1]; o[nt][3] *= corr[1];
           o[nt + 1][0] *= corr[0]; o[nt + 1][1] *= corr[0]; o[nt + 1][2] *= corr[1]; o[nt + 1][3] *= corr[1];
@@ -297,9 +381,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodePara
         mma16816(o[nt + 1], pa, b2, b3);
       }
     }
-    __syncwarp();
   }
-  cp_wait<0>();
+  const bool two_halves = rows > 8;
 
   // ---- merge the 8 warps: (m, l) per row, each warp's O slice in smem, summed with weights
   l_run[0] += __shfl_xor_sync(0xffffffffu, l_run[0], 1);
@@ -325,7 +408,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodePara
     }
   }
   __syncthreads();
-  const int tid = threadIdx.x;
   const long long rows_total = (long long)p.P * p.n_q * p.Hq;
   __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(p.o);
   for (int i = tid; i < rows * 32; i += blockDim.x) {   // 4 dims per thread

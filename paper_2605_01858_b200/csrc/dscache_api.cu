@@ -656,16 +656,17 @@ dscache_status run_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, co
   p.rope_pairs = reinterpret_cast<const float4*>(h->rope + (size_t)h->npos * (c.head_dim / 2));
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c.head_dim));
   p.dbg_pos = h->dbg_attend;
+  p.tmap_k = h->tmap_k; p.tmap_v = h->tmap_v;
   p.dbg_M = std::max(h->C, c.max_query_tokens); p.dbg_A = c.sink_tokens; p.dbg_R = h->R;
   p.dbg_len = c.sink_tokens + h->R + 2 * p.dbg_M;
   // one wave of CTAs: split each (problem, kv head)'s keys when there are fewer of them than
   // SMs, keeping at least one 16-key warp tile per warp in every split
   const int units = p.P * p.Hkv;
-  const int wtiles = (int)((n_keys + 15) / 16);
+  const int tiles = (int)((n_keys + 127) / 128);
   int splits = 1;
-  if (units < h->num_sms) splits = std::max(1, std::min((h->num_sms + units - 1) / units, wtiles / 8));
-  p.wtiles_per_split = (wtiles + splits - 1) / splits;
-  splits = (wtiles + p.wtiles_per_split - 1) / p.wtiles_per_split;
+  if (units < h->num_sms) splits = std::max(1, std::min((h->num_sms + units - 1) / units, tiles));
+  p.tiles_per_split = (tiles + splits - 1) / splits;
+  splits = (tiles + p.tiles_per_split - 1) / p.tiles_per_split;
   p.n_splits = splits;
   StreamScratch ws;
   if (splits > 1) {

@@ -102,10 +102,13 @@ struct DecodeParams {
   int n_keys;                                  // A + kept_frames * tpf + inst_count + n_self
   const float4* rope_pairs;
   float scale_log2;
-  int n_splits, wtiles_per_split;              // key range split in 16-key warp tiles
+  int n_splits, tiles_per_split;               // key range split in 128-key tiles
   float* ws_o; float* ws_lse;                  // [n_splits][P*n_q*Hq][d], [n_splits][P*n_q*Hq]
   int* counters;                               // per (stream, layer, kv head) ticket, zero between launches
   int* dbg_pos; int dbg_len, dbg_A, dbg_R, dbg_M;   // debug id export (kv head 0), null = off
+  // TMA descriptors of the K / V rings ([S*N*Hkv*Rp rows][128] bf16, box 64 x 128, SW128):
+  // 128-key tiles that are one consecutive ring run load with four TMA boxes
+  CUtensorMap tmap_k, tmap_v;
 };
 cudaError_t launch_decode(const DecodeParams& p, cudaStream_t st);
 

@@ -553,7 +553,9 @@ def run_decode(args, cfg, world, rank, local):
                        kept_past_tokens=kept_past,
                        l2=("flushed between steps (read-only flush of 2x L2)" if flush else "inputs larger than L2 (ring %.2f GB)" % (ring_bytes / 1e9))),
         "value_is": "aggregate decode tokens/s over all streams (each token passes every layer of the handle)",
-        "roofline": {"bound": "hbm", "kernel": impl.get("attend") if isinstance(impl, dict) else str(impl),
+        "roofline": {"bound": "hbm", "kernel": ("decode_kernel (mma.sync m16n8k16, GQA rows packed per kv head, TMA ring tiles)"
+                                                if cfg.dtype == "bf16" and cfg.head_dim == 128 and n_q * (Hq // Hkv) <= 16
+                                                else "attention kernel (n_q * Hq/Hkv > 16 or not bf16/d128)"),
                      "achieved": round(achieved, 1) if achieved else None, "peak": pk["hbm_gbs"],
                      "peak_source": pk["source"] + " HBM copy", "unit": "GB/s",
                      "frac": round(achieved / pk["hbm_gbs"], 4) if achieved else None, "traffic": None,

@@ -231,14 +231,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
   float* qraw = reinterpret_cast<float*>(smem + kQRawOff);
   unsigned char* qrot = smem + kQRotOff;
   const __nv_bfloat16* Q = reinterpret_cast<const __nv_bfloat16*>(p.q);
-  for (int i = tid; i < 16 * 128; i += blockDim.x) {
-    const int r = i >> 7, d = i & 127;
-    float v = 0.f;
+  {   // one 16-byte load per thread: row tid / 16, dims 8 * (tid % 16) ..
+    const int r = tid >> 4, c = (tid & 15) * 8;
+    uint4 w = make_uint4(0, 0, 0, 0);
     if (r < rows) {
       const int qi = r / p.grp, hh = r % p.grp;
-      v = __bfloat162float(Q[(((long long)pp * p.n_q + qi) * p.Hq + g * p.grp + hh) * 128 + d]);
+      w = __ldg(reinterpret_cast<const uint4*>(Q + (((long long)pp * p.n_q + qi) * p.Hq + g * p.grp + hh) * 128 + c));
     }
-    qraw[i] = v;
+    const float2 a = unpk(w.x), b = unpk(w.y), e = unpk(w.z), f = unpk(w.w);
+    *reinterpret_cast<float4*>(qraw + r * 128 + c) = make_float4(a.x, a.y, b.x, b.y);
+    *reinterpret_cast<float4*>(qraw + r * 128 + c + 4) = make_float4(e.x, e.y, f.x, f.y);
   }
   for (int i = tid; i < 16 * kRowBytes / 16; i += blockDim.x) reinterpret_cast<uint4*>(qrot)[i] = make_uint4(0, 0, 0, 0);
   if (dbgp && split == 0 && tid < p.n_q) dbgp[p.dbg_A + p.dbg_R + p.dbg_M + tid] = p.q_pos0 + tid;

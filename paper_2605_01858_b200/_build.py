@@ -73,7 +73,9 @@ def build_variant(name: str, defines) -> str:
 
 
 if __name__ == "__main__":
-    if "--variant" in sys.argv:      # --variant NAME DEF1 DEF2 ...
+    if "--checked" in sys.argv:      # the DSC_CHECK bounds-check build (scripts/gpu_checked.sh)
+        print(build_variant("checked", ["DSC_CHECK=1"]))
+    elif "--variant" in sys.argv:      # --variant NAME DEF1 DEF2 ...
         i = sys.argv.index("--variant")
         print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
     else:

@@ -183,6 +183,7 @@ __device__ __forceinline__ void mma_pv8(uint32_t d_tmem, uint32_t a_tmem, uint64
 // (cta, warp, barrier index, parity, clock) into a host-mapped buffer, readable after the
 // context has died, then traps.  Null (default) = just trap.
 __device__ unsigned long long* g_fa_wd = nullptr;
+__device__ long long g_fa_wd_lim = 1ll << 31;   // clk before a stuck wait traps (DSC_WATCHDOG_CLK)
 __device__ __noinline__ void fa_wd_fail(uint32_t bar_off, uint32_t parity) {
   unsigned long long* wd = g_fa_wd;
   if (wd) {
@@ -202,7 +203,7 @@ __device__ __forceinline__ void fwait(uint32_t bar, uint32_t parity, uint32_t ba
   if (mbar_try(bar, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try(bar, parity)) {
-    if (clock64() - t0 > (1ll << 31)) fa_wd_fail((bar - bar0) / 8, parity);
+    if (clock64() - t0 > g_fa_wd_lim) fa_wd_fail((bar - bar0) / 8, parity);
   }
 }
 
@@ -241,6 +242,7 @@ __device__ __forceinline__ void load_rotate_q_regs(const AttnParams& p, const It
       if (dbg && hh == 0 && ok) dbgp[p.dbg_A + p.dbg_R + p.dbg_M + i] = pos[k];
       if (ok) {
         const __nv_bfloat16* src = qbase + ((long long)i * p.Hq + hh) * 128;
+        DSC_ASSERT(i < p.n_q && w.pp < p.P, "attn_fa Q row");
         lo[k] = ldg128(src);
         hi[k] = ldg128(src + 64);
       } else {
@@ -565,6 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               {   // split-KV / context-parallel partial: fp32 O / l and log2-sum-exp per split
                 const long long rows = (long long)p.P * p.n_q * p.Hq;
                 const long long slot = p.split_only >= 0 ? 0 : w.sp;
+                DSC_ASSERT(slot < max(p.n_splits, 1) && orow < rows, "attn_fa split partial row");
                 float4* dst = reinterpret_cast<float4*>(p.ws_o + (slot * rows + orow) * 128 + 64 * hf);
 #pragma unroll
                 for (int v = 0; v < 16; ++v)
@@ -673,6 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (p.o_rows > 0 && oq >= p.o_rows) oq -= p.o_rows;
           const long long row = peers ? ((long long)w.pp * p.n_q + qi) * p.o_hq + p.o_head_off + h
                                       : ((long long)w.pp * (p.o_rows > 0 ? p.o_rows : p.n_q) + oq) * p.Hq + h;
+          DSC_ASSERT(qi < p.n_q && w.pp < p.P && h < p.Hq && oq < (p.o_rows > 0 ? p.o_rows : p.n_q), "attn_fa O row");
           const int nd = peers ? p.n_peers : 1;
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
@@ -780,6 +784,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const __nv_bfloat16* src = nullptr;
               if (x < A) src = SX + (w.head_row * A + x) * 128;
               else if (x < A + w.n_self) src = XX + (((long long)w.pp * w.n_self + (x - A)) * p.Hkv + w.g) * 128;
+              DSC_ASSERT(w.head_row < (long long)p.S * p.N_total * p.Hkv && w.pp < p.P && rr < BN, "attn_fa sink/self row");
               const uint32_t d = dst + (ch >> 3) * kKVHalf + rr * 128 + (((ch & 7) ^ (rr & 7)) << 4);
               cp_async16(d, src ? (const void*)(src + 8 * ch) : (const void*)SX, src ? 16u : 0u);
             }
@@ -791,6 +796,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             // logical window tile: one 128-row box per 64-column block (ring mirror or staging rows)
             const CUtensorMap* tmap = isk ? &p.tmap_k : &p.tmap_v;
             const int row = (int)(w.head_row * w.Rp) + t.slot0;
+            // the box starts inside this head's rows; a staged window's last box may run past
+            // them (rows >= the tile width are masked; past the tensor end TMA fills zeros)
+            DSC_ASSERT(t.slot0 >= 0 && t.slot0 < w.Rp && (w.staged || t.slot0 + BN <= w.Rp) &&
+                           w.head_row < (long long)p.S * p.N_total * p.Hkv,
+                       "attn_fa TMA box rows");
             FT(isk ? FT_CPK : FT_CPV, g);
             mbar_arrive_tx(bar(b_full + st), kKVBytes);
             tma_load_2d(dst, tmap, 0, row, bar(b_full + st));
@@ -971,20 +981,32 @@ ItemRec attn_fa_decode(const AttnParams& p, int local, int isb) {
 
 // DSC_WATCHDOG=1: pipeline waits that time out leave a record in host-mapped memory
 // (dscache_watchdog_read) before trapping
+// DSC_WATCHDOG_CLK=N: the timeout in clk (0 = never trap; e.g. under compute-sanitizer,
+// which slows every wait by orders of magnitude)
 static unsigned long long* g_wd_host = nullptr;
 cudaError_t fa_watchdog_setup() {
-  static bool done = false;
-  if (done) return cudaSuccess;
-  done = true;
+  static unsigned done_mask = 0;   // per device: the symbols live in each device's module
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 32 && (done_mask & (1u << dev))) return cudaSuccess;
+  if (dev < 32) done_mask |= 1u << dev;
+  if (const char* c = std::getenv("DSC_WATCHDOG_CLK")) {
+    long long lim = std::atoll(c);
+    if (lim <= 0) lim = 0x7fffffffffffffffll;
+    cudaError_t r = cudaMemcpyToSymbol(fa::g_fa_wd_lim, &lim, sizeof(lim));
+    if (r != cudaSuccess) return r;
+  }
   const char* e = std::getenv("DSC_WATCHDOG");
   if (!e || e[0] != '1') return cudaSuccess;
-  void* hp = nullptr;
-  cudaError_t r = cudaHostAlloc(&hp, 4096, cudaHostAllocMapped);
-  if (r != cudaSuccess) return r;
-  std::memset(hp, 0, 4096);
-  g_wd_host = static_cast<unsigned long long*>(hp);
+  if (!g_wd_host) {
+    void* hp = nullptr;
+    cudaError_t r = cudaHostAlloc(&hp, 4096, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (r != cudaSuccess) return r;
+    std::memset(hp, 0, 4096);
+    g_wd_host = static_cast<unsigned long long*>(hp);
+  }
   void* dp = nullptr;
-  r = cudaHostGetDevicePointer(&dp, hp, 0);
+  cudaError_t r = cudaHostGetDevicePointer(&dp, g_wd_host, 0);
   if (r != cudaSuccess) return r;
   return cudaMemcpyToSymbol(fa::g_fa_wd, &dp, sizeof(dp));
 }

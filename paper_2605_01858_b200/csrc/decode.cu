@@ -128,11 +128,14 @@ __device__ __forceinline__ long long key_row(const DecodeParams& p, int pp, long
       off = p.past_start + j * p.tpf + tok;
     }
     if (off >= p.R) off -= p.R;                    // off < 2R: start < R, run length <= R
+    DSC_ASSERT(off >= 0 && off < p.R && (x < past ? (p.stride == 1 || (x / p.tpf) < p.kept_frames) : true),
+               "decode ring slot");
     kind = 1; slot = off;
     return hr * p.Rp + off;
   }
   x -= past + p.inst_count;
   kind = 2; slot = x;
+  DSC_ASSERT(x < p.n_self && pp < p.P, "decode self row");
   return ((long long)pp * p.n_self + x) * p.Hkv + g;
 }
 
@@ -186,6 +189,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
     if (tma) {
       int kind = 0, slot = 0;
       const long long row0 = key_row(p, pp, hr, g, n0, kind, slot);
+      DSC_ASSERT(kind == 1 && slot + kTileKeys <= p.Rp, "decode TMA box rows");
       if (tid == 0) {
         bar_arrive_tx(bar, 4 * kHalfBytes + tab_bytes);
         tma2d(sb, &p.tmap_k, 0, (int)row0, bar);
@@ -431,6 +435,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
     const float inv = L > 0.f ? 1.f / L : 0.f;
     const int qi = r / p.grp, h = g * p.grp + r % p.grp;
     const long long orow = ((long long)pp * p.n_q + qi) * p.Hq + h;
+    DSC_ASSERT(qi < p.n_q && h < p.Hq && orow < rows_total && split < p.n_splits, "decode O / partial row");
     if (p.n_splits == 1) {
       uint2 w;
       w.x = pk(v.x * inv, v.y * inv);

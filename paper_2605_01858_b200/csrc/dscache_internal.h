@@ -5,6 +5,29 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+// DSC_CHECK=1 builds (scripts/gpu_checked.sh): device-side bounds checks on every global
+// address the kernels form (rows of the ring / sink / self / Q / O / workspaces, TMA boxes),
+// trapping with the failing site -- the in-house substitute for compute-sanitizer, which is
+// closed on the GPU pool.  Off (compiled out) in the product library.
+#ifndef DSC_CHECK
+#define DSC_CHECK 0
+#endif
+#if DSC_CHECK
+#include <cstdio>
+#define DSC_ASSERT(cond, what)                                                                         \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("DSC_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                       \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define DSC_ASSERT(cond, what) \
+  do {                         \
+  } while (0)
+#endif
+
 namespace dsc {
 
 constexpr int kTileN = 128;   // keys per K/V tile of the tcgen05 kernel (N of QK^T, K of PV)

@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(256) append_kernel(AppendParams p) {
     const long long s = r / p.layer_count;
     const long long head = ((s * p.N_total + p.layer_begin + l) * p.Hkv + g) * p.rows_dst;
     const int slot = p.slot0 + j;
+    DSC_ASSERT(slot >= 0 && slot < (p.mirror_R > 0 ? p.mirror_R : p.rows_dst) && s < p.S, "append destination row");
     *mirror = (p.mirror_R > 0 && slot < kMirror) ? (head + p.mirror_R + slot) * cpr + c : -1;
     return (head + slot) * cpr + c;
   };
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(256) stage_instant_kernel(StageParams p) {
       sk = reinterpret_cast<const uint4*>(p.ring_k) + (head * p.Rp_ring + slot) * 16;
       sv = reinterpret_cast<const uint4*>(p.ring_v) + (head * p.Rp_ring + slot) * 16;
     }
+    DSC_ASSERT(row < p.rows_stage && s < p.S, "stage destination row");
     uint4* dk = reinterpret_cast<uint4*>(p.stage_k) + (head * p.rows_stage + row) * 16;
     uint4* dv = reinterpret_cast<uint4*>(p.stage_v) + (head * p.rows_stage + row) * 16;
     const uint4 lo = sk[c8], hi = sk[c8 + 8];
@@ -295,10 +297,12 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnParams p) {
     } else if (L < p.A + p.ring_count) {
       int slot = p.ring_start + (L - p.A);
       if (slot >= p.R) slot -= p.R;
+      DSC_ASSERT(slot >= 0 && slot < p.R, "simt ring slot");
       kr = RK + (head_row * p.Rp + slot) * D; vr = RV + (head_row * p.Rp + slot) * D;
       if (dbg_keys && lane == 0) dbgp[p.dbg_A + slot] = L;
     } else {
       const int j = L - p.A - p.ring_count;
+      DSC_ASSERT(j < p.n_self, "simt self row");
       kr = XK + (((long long)pp * p.n_self + j) * p.Hkv + g) * D;
       vr = XV + (((long long)pp * p.n_self + j) * p.Hkv + g) * D;
       if (dbg_keys && lane == 0) dbgp[p.dbg_A + p.dbg_R + j] = L;

@@ -58,6 +58,8 @@ def traffic_key(args, world: int) -> str:
         key += f"|approx{args.approx}"
     if getattr(args, "instant_frames", None):
         key += f"|lI{args.instant_frames}"
+    if args.mode == "decode":
+        key += f"|nq{args.decode_nq}|gen{args.decode_gen}|stride{args.decode_stride}"
     return key
 
 
@@ -540,6 +542,14 @@ def run_decode(args, cfg, world, rank, local):
     t_max = max_over_ranks(total_ms, world)
     units = S * N
     bytes_step = units * decode_bytes_per_unit(cfg, n_self, n_q, kept_past)
+    traffic, traffic_tag = None, None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            rec = json.load(open(tp)).get(traffic_key(args, world), {})
+            traffic, traffic_tag = rec.get("dram_bytes_per_launch"), rec.get("tag")
+        except Exception:
+            traffic = None
     attn_ms = prof["ms_attend"] + prof["ms_build"]
     pk = peaks()
     achieved = bytes_step * args.steps / (attn_ms / 1e3) / 1e9 if attn_ms > 0 else None
@@ -558,7 +568,9 @@ def run_decode(args, cfg, world, rank, local):
                                                 else "attention kernel (n_q * Hq/Hkv > 16 or not bf16/d128)"),
                      "achieved": round(achieved, 1) if achieved else None, "peak": pk["hbm_gbs"],
                      "peak_source": pk["source"] + " HBM copy", "unit": "GB/s",
-                     "frac": round(achieved / pk["hbm_gbs"], 4) if achieved else None, "traffic": None,
+                     "frac": round(achieved / pk["hbm_gbs"], 4) if achieved else None, "traffic": traffic,
+                     "traffic_source": (f"ncu --set full, profiles/{traffic_tag}_ncu_full.md" if traffic
+                                        else "not captured for this launch shape"),
                      "algorithmic_bytes_per_step": bytes_step, "launches": prof["n_build"] + prof["n_attend"]},
         "gpu_launches": prof["kernel_launches"], "attn_impl": impl, "clocks": clk,
         "e2e": {"skipped": "decode mode times the device-resident path only"},

@@ -76,12 +76,13 @@ def main():
     os.makedirs(P, exist_ok=True)
     table, agg = launches(tag)
     open(os.path.join(P, f"{tag}_launches.md"), "w").write(
-        f"# ncu launch list ({tag}): `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` ({cfg})\n\n"
+        f"# ncu launch list ({tag}): `{os.environ.get('LCMD', 'python bench.py --steps 2 --warmup 3 --no-cpu-baseline --config ' + cfg)}`\n\n"
         "`ncu --metrics gpu__time_duration.sum --clock-control none`; every kernel of the run "
         "(fill, warm-up, timed steps, e2e).  Per-launch times are cold-cache and serialised: "
         "compare shares, not absolutes.\n\n" + table + "\n")
     recs = ncu_raw(tag)
-    lines = [f"# ncu --set full of attn_fa_kernel ({tag}, {cfg})\n"]
+    kname = os.environ.get("KNAME", "attn_fa_kernel")
+    lines = [f"# ncu --set full of {kname} ({tag}, {cfg})\n"]
 
     def section(recs, title, labels):
         lines.append(f"## {title}\n")
@@ -103,8 +104,8 @@ def main():
             stalls.append(", ".join(f"{n} {100 * v / tot:.0f}%" for v, n in sorted(items, reverse=True)[:6]))
         lines.append("\nTop warp-stall reasons (pc sampling): " + " / ".join(stalls) + "\n")
 
-    section(recs, "Fused step launch (the bench's dominant kernel): `-k regex:attn_fa -s 4 -c 1`, "
-            "one c5 step = build_instant + attend items in one persistent launch", ["fused step"])
+    section(recs, os.environ.get("STITLE", "Fused step launch (the bench's dominant kernel): `-k regex:attn_fa -s 4 -c 1`, "
+            f"one {cfg} step = build_instant + attend items in one persistent launch"), [os.environ.get("SLABEL", "fused step")])
     split_rep = os.path.join(G, f"prof_split_{tag}.ncu-rep")
     if os.path.exists(split_rep):
         txt = subprocess.run(["ncu", "-i", split_rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout

@@ -32,8 +32,8 @@
 //              tiles are prepared by the softmax warpgroups (idle until the first S)
 //   warp 12    K copy (TMA box 64 cols x 128 rows; cp.async for sink/self tiles)
 //   warp 13    V copy
-//   warp 14    TMEM allocator + MMA issuer (whole warp, one elected lane issues)
-//   warp 15    idle
+//   warp 14    TMEM allocator + MMA issuer of Q tile 0 (S0, PV0; one elected lane issues)
+//   warp 15    MMA issuer of Q tile 1 (S1, PV1); both commit to the shared K / V free barriers
 #include "tc_common.cuh"
 
 #include <algorithm>

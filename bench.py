@@ -280,6 +280,10 @@ def run_ours(args, cfg, world, rank, local):
     tcount = [fill]
 
     gathered = [None]
+    hgather = None
+    if kvsplit and world > 1:
+        from paper_2605_01858_b200.dist import AsyncHeadGather
+        hgather = AsyncHeadGather((S, N, q, Hq, d), dt, dev, nbuf=2)
 
     fused = args.api == "fused"
     approx = getattr(args, "approx", 0)
@@ -295,6 +299,7 @@ def run_ours(args, cfg, world, rank, local):
     def step(i):
         t = tcount[0]
         qq = qry[i & 1]
+        o_ = hgather.slot(stream) if hgather is not None else o   # P2: rotating O slots (side-stream gather)
         if context:     # P3 (NEXT-4): key-range split of one stream's attend, partials merged
             from paper_2605_01858_b200.dist import context_parallel_attend
             dsc.append_frame(*frames[t % POOL])
@@ -320,14 +325,13 @@ def run_ours(args, cfg, world, rank, local):
             build_flops[0] += fb_full if n != tpf or C == tpf else fb_new
             dsc.attend(qq[0], qq[1], qq[2], o)
         elif fused:     # dscache_step: append + build_instant + attend, one attention launch
-            dsc.step(*frames[t % POOL], q_inst[i & 1], qq[0], qq[1], qq[2], o_inst=o_inst, o=o)
+            dsc.step(*frames[t % POOL], q_inst[i & 1], qq[0], qq[1], qq[2], o_inst=o_inst, o=o_)
         else:
             dsc.append_frame(*frames[t % POOL])
             dsc.build_instant(q_inst[i & 1], o_inst)
-            dsc.attend(qq[0], qq[1], qq[2], o)
-        if kvsplit and world > 1:           # the only exchange of P2: head-major all-gather of O
-            from paper_2605_01858_b200.dist import gather_heads
-            gathered[0] = gather_heads(o)
+            dsc.attend(qq[0], qq[1], qq[2], o_)
+        if kvsplit and world > 1:           # the only exchange of P2: head-major all-gather of O,
+            gathered[0] = hgather.launch(stream)   # on a side stream, overlapped with the next step
         tcount[0] += 1
 
     ring_bytes = 2 * S * N * Hkv * dsc.R * d * (2 if cfg.dtype == "bf16" else 4)
@@ -352,6 +356,8 @@ def run_ours(args, cfg, world, rank, local):
             scratch()
             ev[i][0].record(stream)
             step(i)
+            if hgather is not None:
+                hgather.wait(stream)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         total_ms = sum(a.elapsed_time(b) for a, b in ev)
@@ -359,6 +365,8 @@ def run_ours(args, cfg, world, rank, local):
         ev[0][0].record(stream)
         for i in range(args.steps):
             step(i)
+        if hgather is not None:
+            hgather.wait(stream)            # the last step's gather is part of the timed work
         ev[0][1].record(stream)
         torch.cuda.synchronize()
         total_ms = ev[0][0].elapsed_time(ev[0][1])

@@ -14,7 +14,8 @@ Two partitions, both from the north_star:
   Softmax attention is invariant to how its key set is split, so the merge is exact up
   to rounding; G = 8 works for Hkv = 4, where P2 cannot.
 
-P2 has two gather paths: the NCCL all-gather of O (gather_heads, the baseline) and the
+P2 has two gather paths: the NCCL all-gather of O (gather_heads; AsyncHeadGather runs it on
+a side stream overlapped with the next step's kernels) and the
 fused all-gather epilogue (PeerOutputs + kv_split_attend_fused): every rank's
 gathered-O buffer is mapped into every other rank through CUDA IPC, and the attention
 kernel's epilogue stores each output row straight into all of them over NVLink, so no
@@ -71,6 +72,57 @@ def gather_heads(o_local: torch.Tensor, group=None) -> torch.Tensor:
         dist.all_gather(list(out.unbind(0)), hm, group=group)
     full = out.reshape((world * hm.shape[0],) + tuple(hm.shape[1:]))   # [Hq][S][N][q][d]
     return full.permute(1, 2, 3, 0, 4)
+
+
+class AsyncHeadGather:
+    """P2's all-gather of O on a side stream, overlapped with the next step's kernels.
+
+    `nbuf` O slots rotate: step i's attend writes `slot()` (= slot i % nbuf), `launch()`
+    records an event on the compute stream and runs the head-major all-gather of that slot
+    on the side stream (NCCL waits for the side stream, which waits for the event), and the
+    attend of step i + nbuf -- which overwrites the slot -- first waits for that gather's
+    completion event.  `launch()` returns the gathered [S][N][n_q][Hq][d] tensor, valid once
+    `wait(stream)` has made `stream` wait for it.  On CPU tensors (gloo tests) everything
+    runs synchronously in the same order."""
+
+    def __init__(self, local_shape, dtype, device, group=None, nbuf: int = 2):
+        self.group, self.nbuf, self.i = group, nbuf, 0
+        self.device = torch.device(device)
+        self.slots = [torch.empty(local_shape, dtype=dtype, device=self.device) for _ in range(nbuf)]
+        self.cuda = self.device.type == "cuda"
+        self.side = torch.cuda.Stream(self.device) if self.cuda else None
+        self.ready = [torch.cuda.Event() for _ in range(nbuf)] if self.cuda else None
+        self.done = [torch.cuda.Event() for _ in range(nbuf)] if self.cuda else None
+        self.used = [False] * nbuf
+        self.out = [None] * nbuf
+
+    def slot(self, stream=None) -> torch.Tensor:
+        """The O buffer of this step; `stream` (the compute stream) waits until the gather
+        that last read it has finished."""
+        b = self.i % self.nbuf
+        if self.cuda and self.used[b]:
+            (stream or torch.cuda.current_stream(self.device)).wait_event(self.done[b])
+        return self.slots[b]
+
+    def launch(self, stream=None) -> torch.Tensor:
+        b = self.i % self.nbuf
+        if self.cuda:
+            st = stream or torch.cuda.current_stream(self.device)
+            self.ready[b].record(st)
+            self.side.wait_event(self.ready[b])
+            with torch.cuda.stream(self.side):
+                self.out[b] = gather_heads(self.slots[b], self.group)
+            self.done[b].record(self.side)
+        else:
+            self.out[b] = gather_heads(self.slots[b], self.group)
+        self.used[b] = True
+        self.i += 1
+        return self.out[b]
+
+    def wait(self, stream=None):
+        """Make `stream` wait for every gather launched so far."""
+        if self.cuda:
+            (stream or torch.cuda.current_stream(self.device)).wait_stream(self.side)
 
 
 def merge_partials(o_parts: torch.Tensor, lse_parts: torch.Tensor) -> torch.Tensor:

@@ -94,6 +94,27 @@ def _worker_kv_split(rank, world, port, out_q):
     dist.destroy_process_group()
 
 
+def _worker_async_gather(rank, world, port, out_q):
+    """AsyncHeadGather over 3 steps with 2 rotating slots: each step's gathered output is the
+    unsharded oracle of that step (the slot reuse never leaks the previous step's heads)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_01858_b200.dist import AsyncHeadGather
+    cfg = _small_cfg()
+    heads = kv_head_partition(cfg.num_q_heads, cfg.num_kv_heads, world, rank)
+    g = AsyncHeadGather((1, 1, cfg.query_tokens, heads[3], cfg.head_dim), torch.float64, "cpu", nbuf=2)
+    outs = []
+    for t in (5, 6, 7):
+        g.slot().copy_(torch.from_numpy(_oracle_attend(cfg, 0, t, heads))[None, None])
+        outs.append(g.launch())
+    g.wait()
+    if rank == 0:
+        out_q.put([o[0, 0].numpy() for o in outs])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def _worker_streams(rank, world, port, out_q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -130,6 +151,13 @@ def test_kv_head_split_allgather_matches_unsharded_oracle():
     ref = _oracle_attend(_small_cfg(), 0, 6)
     assert full.shape == ref.shape
     assert np.abs(full - ref).max() < 1e-12
+
+
+def test_async_head_gather_rotating_slots():
+    outs = _run(_worker_async_gather)
+    for t, full in zip((5, 6, 7), outs):
+        ref = _oracle_attend(_small_cfg(), 0, t)
+        assert np.abs(full - ref).max() < 1e-12
 
 
 def test_stream_partition_two_ranks_matches_single_process():

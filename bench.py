@@ -435,7 +435,7 @@ def run_ours(args, cfg, world, rank, local):
         "frames_per_s_per_stream": round(value / cfg.num_streams, 3),
         "attention_tflops_per_gpu_step": round(step_tflops, 2),
         "attention_pct_peak_step": round(100 * step_tflops / pk["bf16_tflops"], 2),
-        "roofline": {"bound": "tensor", "kernel": "attn_tc_kernel (tcgen05 rotate-on-load flash attention)",
+        "roofline": {"bound": "tensor", "kernel": "attn_fa_kernel (v7 tcgen05 rotate-on-load GQA flash attention)",
                      "achieved": round(achieved, 2) if achieved else None, "peak": pk["bf16_tflops"],
                      "peak_source": pk["source"] + " bf16 burst", "unit": "TFLOP/s",
                      "frac": round(achieved / pk["bf16_tflops"], 4) if achieved else None,

@@ -385,17 +385,14 @@ dscache_status dscache_set_debug(dscache_t h, int32_t* build_pos, int32_t* atten
 int32_t        dscache_debug_len(dscache_t h);
 
 /* Per-CTA event timeline of the tcgen05 attention kernel (profiling aid).  Recorded only
- * by a library built with -DDSC_TRACE=1 (scripts/trace_attn.py builds that variant); the
- * production library accepts the call and records nothing.  buf: DEVICE int64 buffer of
- * ntrace_cta * 40 * 64 entries (NULL = off): for the first ntrace_cta CTAs of each launch,
- * clock64() at [cta][event][tile] for events 0 K tile issued, 1 V tile issued, 2 raw K
- * landed, 3 rotated K seen by the MMA issuer, 4/5 S0/S1 seen by softmax, 6/7 P0/P1
- * written, 8/9 PV0/PV1 about to be issued, 10 Q ready, 11 CTA start, 12 CTA end (tile
- * index 0 for 10-12), 13 V seen by the MMA issuer, 14..21 P written by softmax warp 0..7,
- * 22 softmax warp 0 scores loaded, 26 P packed, 28 K rotated, 29..31 item switch (Q
- * published / loaded / started, indexed by the next item's first tile), 32 S issued,
- * 33/34 PV0/PV1 issued, 35/36 epilogue start / stores issued; tiles (64 keys each)
- * >= 64 are not recorded. */
+ * by a library built with -DFA_TRACE=1 (scripts/trace_fa.py builds that variant and prints
+ * the timeline); the production library accepts the call and records nothing.  buf: DEVICE
+ * int64 buffer of ntrace_cta * 32 * 1024 entries (NULL = off): for the first ntrace_cta CTAs
+ * of each launch, clock64() at [cta][event][index] for the 32 events of attn_fa.cu (FT_*:
+ * per tile, the MMA issuers' waits for P0 / P1 / K / V and their S / PV issue, S seen and P
+ * written by each softmax warpgroup, K landed and rotated, the copy warps' issues, the
+ * softmax phases of warp 0; per item, item start, Q tiles ready, O read out, epilogue and
+ * Q-prep boundaries; the CTA end).  Indices >= 1024 are not recorded. */
 dscache_status dscache_set_trace(dscache_t h, int64_t* buf, int32_t ntrace_cta);
 
 /* Profiling: when enabled, every attention/combine kernel launch is bracketed by

@@ -31,7 +31,7 @@ reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
 addr_line = {}
-want = "attn_fa_kernel" if "attn_fa" in kname else "attn_tc_kernel"
+want = "attn_fa_kernel"
 for cub in glob.glob(os.path.join(tmp, "*.cubin")):
     dis = subprocess.run(["nvdisasm", "-gi", "-c", cub], capture_output=True, text=True).stdout
     if want not in dis:

@@ -161,3 +161,46 @@ def test_attend_peers_across_processes_cuda_ipc(lib, world):
     for (rank, ok, ma, rl) in res:
         assert ok, f"rank {rank}: {ma}"
     assert all(p.exitcode == 0 for p in procs)
+
+
+def _async_gather_worker(port, out_q):
+    """One NCCL rank on cuda:0 (world 1): AsyncHeadGather's side-stream gather after attends
+    on a compute stream, 3 steps over 2 rotating O slots."""
+    import torch.distributed as dist
+    from paper_2605_01858_b200.dist import AsyncHeadGather
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    cfg = synth.CONFIGS["c2"]
+    heads = kv_head_partition(cfg.num_q_heads, cfg.num_kv_heads, 1, 0)
+    h, q, ks, vs = _shard_stream(cfg, heads, 20, dev)
+    comp = torch.cuda.Stream(dev)
+    g = AsyncHeadGather(tuple(q.shape), q.dtype, dev, nbuf=2)
+    outs = []
+    with torch.cuda.stream(comp):
+        for _ in range(3):
+            o = g.slot(comp)
+            h.attend(q, ks, vs, o, stream=comp)
+            outs.append(g.launch(comp))
+        g.wait(comp)
+    comp.synchronize()
+    ref = h.attend(q, ks, vs)
+    torch.cuda.synchronize()
+    out_q.put([float((x - ref).abs().max()) for x in outs])
+    dist.destroy_process_group()
+    h.close()
+
+
+def test_async_head_gather_side_stream_nccl(lib):
+    import multiprocessing as mp
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_async_gather_worker, args=(port, q))
+    p.start()
+    diffs = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert all(d == 0.0 for d in diffs), diffs   # the gather of one rank is its own output, bit for bit

@@ -394,6 +394,9 @@ def run_ours(args, cfg, world, rank, local):
 
     # e2e: the same step through the public API with pinned host buffers, H2D of every
     # input of the step and D2H of the query answer O inside the timed region
+    graph = None
+    if getattr(args, "graph", False) and not (context or kvsplit or args.layer_seq):
+        graph = time_graph(args, dsc, step, scratch, dev)
     e2e = (run_e2e(args, cfg, lcfg, dsc, S, dev, stream, world, kvsplit) if not (n_boost or approx) else
            {"skipped": ("boost" if n_boost else "approx") + " mode times the device-resident path only"})
     impl = dsc.attn_impl()
@@ -453,7 +456,95 @@ def run_ours(args, cfg, world, rank, local):
         "clocks": clk,
         "e2e": e2e,
     }
+    if graph is not None:
+        graph["value"] = round(cfg.num_streams / (graph["ms_per_step"] / 1e3), 2)
+        line["graph"] = graph
+    if getattr(args, "whole_stream", False) and world == 1 and not (context or kvsplit or args.layer_seq):
+        line["whole_stream"] = time_whole_stream(cfg, dev)
     return line
+
+
+def time_graph(args, dsc, step, flush, dev):
+    """The same steady-state step sequence replayed from one CUDA graph (SURVEY §8(d) graph
+    vs eager): K steps are captured once (the library's host bookkeeping runs at capture;
+    the launches' ring offsets and ids are baked in, so a replay re-executes those K steps'
+    work -- a timing device, not a stream continuation).  With an L2 flush between steps the
+    flushes are captured too and a flush-only graph's time is subtracted."""
+    K = args.steps
+    s = torch.cuda.Stream(dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s):
+        for i in range(2):                  # warm on the capture stream (launch shapes cached)
+            step(i)
+    torch.cuda.synchronize()
+
+    def capture(body):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
+            for i in range(K):
+                body(i)
+        return g
+
+    def timed(g):
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            a.record(s)
+            g.replay()
+            b.record(s)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
+    def body(i):
+        if flush is not None:
+            flush()
+        step(i)
+    try:
+        ms = timed(capture(body))
+        ms_flush = timed(capture(lambda i: flush())) if flush is not None else 0.0
+    except Exception as e:          # capture not possible for this mode: say why, keep the line
+        return {"skipped": f"graph capture failed: {type(e).__name__}: {str(e)[:120]}"}
+    return {"ms_per_step": round((ms - ms_flush) / K, 4), "steps_captured": K,
+            "flush_ms_subtracted_per_step": round(ms_flush / K, 4),
+            "note": "the timed steps replayed from one CUDA graph (no host launch overhead); eager = ms_per_step"}
+
+
+def time_whole_stream(cfg, dev):
+    """Whole-stream average next to the steady state: a fresh handle fed every
+    frame of the config's stream from frame 0 (warm-up steps with a partial window included),
+    one fused step per frame, timed end to end on the device."""
+    from paper_2605_01858_b200 import dscache as D
+    S, N, A, tpf, Hkv, Hq, d = (cfg.num_streams, cfg.num_layers, cfg.sink_tokens, cfg.tokens_per_frame,
+                                cfg.num_kv_heads, cfg.num_q_heads, cfg.head_dim)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+
+    def rnd(*shape):
+        return (torch.randn(shape, device=dev, generator=g) * cfg.scale).to(cfg.torch_dtype)
+    h = D.DSCache.from_config(cfg, device=dev.index or 0)
+    fk, fv = rnd(S, N, tpf, Hkv, d), rnd(S, N, tpf, Hkv, d)
+    qi_full = rnd(S * N * cfg.C * Hq * d)
+    q, ks, vs = rnd(S, N, cfg.query_tokens, Hq, d), rnd(S, N, cfg.query_tokens, Hkv, d), rnd(S, N, cfg.query_tokens, Hkv, d)
+    o = torch.empty(S, N, cfg.query_tokens, Hq, d, dtype=cfg.torch_dtype, device=dev)
+    oi_full = torch.empty(S * N * cfg.C * Hq * d, dtype=cfg.torch_dtype, device=dev)
+    if A > 0:
+        h.append_frame(rnd(S, N, A, Hkv, d), rnd(S, N, A, Hkv, d))
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for t in range(cfg.num_frames):
+        n_inst = h.state(0)["next_instant_tokens"]
+        qi = qi_full[:S * N * n_inst * Hq * d].view(S, N, n_inst, Hq, d)
+        oi = oi_full[:S * N * n_inst * Hq * d].view(S, N, n_inst, Hq, d)
+        h.step(fk, fv, qi, q, ks, vs, o_inst=oi, o=o)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    h.close()
+    return {"frames": cfg.num_frames, "ms_total": round(ms, 3), "ms_per_step": round(ms / cfg.num_frames, 4),
+            "value": round(S * cfg.num_frames / (ms / 1e3), 2), "unit": "frames/s",
+            "note": "fresh handle, every frame of the stream from frame 0 (partial windows included), device time"}
 
 
 def decode_bytes_per_unit(cfg, n_self, n_q, past_tokens=None):
@@ -780,6 +871,9 @@ def main():
     ap.add_argument("--decode-nq", type=int, default=1, help="decode mode: query rows per launch")
     ap.add_argument("--decode-stride", type=int, default=1,
                     help="decode mode: keep every STRIDE-th past frame (zeta_decode, PAPER.md:695)")
+    ap.add_argument("--graph", action="store_true", help="also time the timed steps replayed from one CUDA graph")
+    ap.add_argument("--whole-stream", action="store_true",
+                    help="also time a fresh handle over every frame of the config's stream (whole-stream average)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()

@@ -79,7 +79,9 @@ const ItemRec* item_table(SchedCache* cache, const AttnParams& pa, const AttnPar
   if (it != cache->tables.end()) {
     const SchedCache::Entry& e = it->second;
     if (!e.dev) return nullptr;
-    if (e.stream != st && e.ready) cudaStreamWaitEvent(st, e.ready, 0);
+    // another stream uploaded it: wait for the upload unless it has already landed (so a
+    // steady-state step can be captured into a CUDA graph on another stream)
+    if (e.stream != st && e.ready && cudaEventQuery(e.ready) != cudaSuccess) cudaStreamWaitEvent(st, e.ready, 0);
     *off_out = e.dev;
     return reinterpret_cast<const ItemRec*>(reinterpret_cast<const char*>(e.dev) + off_bytes);
   }
@@ -120,7 +122,9 @@ const ItemRec* item_table(SchedCache* cache, const AttnParams& pa, const AttnPar
   for (long long I = 0; I < items; ++I) dst[fill[owner[I]]++] = rec[I];   // increasing I per CTA
   SchedCache::Entry e;
   if (cache->bytes + host.size() > kMaxCacheBytes) return nullptr;
-  if (cudaMalloc(&e.dev, host.size()) != cudaSuccess) {
+  // stream-ordered allocation: no implicit synchronisation, so a new launch shape (every
+  // warm-up step of a stream has one) does not drain the GPU pipeline
+  if (cudaMallocAsync(&e.dev, host.size(), st) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
@@ -128,7 +132,7 @@ const ItemRec* item_table(SchedCache* cache, const AttnParams& pa, const AttnPar
       cudaEventCreateWithFlags(&e.ready, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(e.ready, st) != cudaSuccess) {
     cudaGetLastError();
     if (e.ready) cudaEventDestroy(e.ready);
-    cudaFree(e.dev);
+    cudaFreeAsync(e.dev, st);
     return nullptr;
   }
   e.stream = st;

@@ -12,6 +12,8 @@
 #include "../../include/dscache.h"
 #include "dscache_internal.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -233,6 +235,15 @@ dscache_status run_attention(dscache_t h, dsc::AttnParams& p, int impl, int kind
 
 }  // namespace
 
+namespace {
+// NVTX range around every public call that launches work (SURVEY §5 tracing): named after
+// the C entry point, visible in Nsight Systems / ncu --nvtx; a no-op without a tool.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 extern "C" {
 
 const char* dscache_last_error(void) { return g_err.c_str(); }
@@ -355,6 +366,7 @@ dscache_status dscache_destroy(dscache_t h) {
 
 dscache_status dscache_append_frame(dscache_t h, int32_t lb, int32_t lc, const void* k, const void* v,
                                     int32_t n_tokens, void* stream) {
+  NvtxRange nvtx_("dscache_append_frame");
   dscache_status s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
   if (!k || !v) return fail(DSCACHE_E_ARG, "null k/v");
@@ -438,6 +450,7 @@ dscache_status prep_build(dscache_t h, int32_t lb, int32_t lc, const void* q_ins
 
 dscache_status dscache_build_instant(dscache_t h, int32_t lb, int32_t lc, const void* q_inst, void* o_inst,
                                      void* stream) {
+  NvtxRange nvtx_("dscache_build_instant");
   if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "build_instant");
   dsc::AttnParams p{};
   dsc::StageParams sp{};
@@ -491,6 +504,7 @@ bool approx_refresh(dscache_t h, int32_t lb, int32_t lc, int32_t period, const v
 
 dscache_status dscache_build_instant_newest(dscache_t h, int32_t lb, int32_t lc, const void* q_new, void* o_new,
                                             void* stream) {
+  NvtxRange nvtx_("dscache_build_instant_newest");
   if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "build_instant_newest");
   dsc::AttnParams p{};
   dscache_status s = prep_newest(h, lb, lc, q_new, o_new, p);
@@ -516,6 +530,7 @@ dscache_status dscache_instant_approx_rows(dscache_t h, int32_t lb, int32_t lc, 
 
 dscache_status dscache_build_instant_approx(dscache_t h, int32_t lb, int32_t lc, int32_t period, const void* q_rows,
                                             int32_t n_rows, void* o_ring, void* stream) {
+  NvtxRange nvtx_("dscache_build_instant_approx");
   int32_t need = 0;
   dscache_status s = dscache_instant_approx_rows(h, lb, lc, period, o_ring, &need);
   if (s != DSCACHE_OK) return s;
@@ -613,6 +628,7 @@ dscache_status attend_common(dscache_t h, int32_t lb, int32_t lc, const void* q,
 
 dscache_status dscache_attend(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                               const void* v_self, int32_t n_q, void* o, void* stream) {
+  NvtxRange nvtx_("dscache_attend");
   if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "attend");
   if (h && (n_q < 1 || n_q > h->cfg.max_query_tokens))
     return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
@@ -703,6 +719,7 @@ dscache_status dscache_decode(dscache_t h, int32_t lb, int32_t lc, const void* q
 dscache_status dscache_decode_sampled(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                                       const void* v_self, int32_t n_self, int32_t n_q, int32_t past_stride, void* o,
                                       void* stream) {
+  NvtxRange nvtx_("dscache_decode_sampled");
   if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "decode");
   if (!h) return fail(DSCACHE_E_ARG, "null handle");
   if (past_stride < 1) return fail(DSCACHE_E_ARG, "past_stride must be >= 1");
@@ -803,6 +820,7 @@ dscache_status attend_with_inst(dscache_t h, int32_t lb, int32_t lc, const void*
 dscache_status dscache_build_instant_boost(dscache_t h, int32_t lb, int32_t lc, const void* q_inst,
                                            const void* k_boost, const void* v_boost, int32_t n_boost, void* o_inst,
                                            void* stream) {
+  NvtxRange nvtx_("dscache_build_instant_boost");
   dscache_status s = need_mode(h, DSCACHE_INSTANT_RING, "build_instant_boost");
   if (s == DSCACHE_OK) s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
@@ -818,6 +836,7 @@ dscache_status dscache_build_instant_boost(dscache_t h, int32_t lb, int32_t lc, 
 dscache_status dscache_attend_boost(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                                     const void* v_self, int32_t n_q, const void* k_boost, const void* v_boost,
                                     int32_t n_boost, void* o, void* stream) {
+  NvtxRange nvtx_("dscache_attend_boost");
   dscache_status s = need_mode(h, DSCACHE_INSTANT_RING, "attend_boost");
   if (s != DSCACHE_OK) return s;
   if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
@@ -832,6 +851,7 @@ dscache_status dscache_attend_boost(dscache_t h, int32_t lb, int32_t lc, const v
 
 dscache_status dscache_append_past(dscache_t h, int32_t lb, int32_t lc, const void* k, const void* v,
                                    int32_t n_tokens, void* stream) {
+  NvtxRange nvtx_("dscache_append_past");
   dscache_status s = need_mode(h, DSCACHE_INSTANT_EXTERNAL, "append_past");
   if (s == DSCACHE_OK) s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
@@ -864,6 +884,7 @@ dscache_status dscache_append_past(dscache_t h, int32_t lb, int32_t lc, const vo
 
 dscache_status dscache_build_instant_ext(dscache_t h, int32_t lb, int32_t lc, const void* q_inst, const void* k_inst,
                                          const void* v_inst, void* o_inst, void* stream) {
+  NvtxRange nvtx_("dscache_build_instant_ext");
   dscache_status s = need_mode(h, DSCACHE_INSTANT_EXTERNAL, "build_instant_ext");
   if (s == DSCACHE_OK) s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
@@ -878,6 +899,7 @@ dscache_status dscache_build_instant_ext(dscache_t h, int32_t lb, int32_t lc, co
 dscache_status dscache_attend_ext(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                                   const void* v_self, int32_t n_q, const void* k_inst, const void* v_inst, void* o,
                                   void* stream) {
+  NvtxRange nvtx_("dscache_attend_ext");
   dscache_status s = need_mode(h, DSCACHE_INSTANT_EXTERNAL, "attend_ext");
   if (s != DSCACHE_OK) return s;
   if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
@@ -894,6 +916,7 @@ dscache_status dscache_attend_ext(dscache_t h, int32_t lb, int32_t lc, const voi
 dscache_status dscache_attend_partial(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                                       const void* v_self, int32_t n_q, int32_t part, int32_t n_parts, float* o_part,
                                       float* lse_part, void* stream) {
+  NvtxRange nvtx_("dscache_attend_partial");
   if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "attend_partial");
   if (!h) return fail(DSCACHE_E_ARG, "null handle");
   if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
@@ -921,6 +944,7 @@ dscache_status dscache_attend_partial(dscache_t h, int32_t lb, int32_t lc, const
 dscache_status dscache_attend_peers(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                                     const void* v_self, int32_t n_q, void* const* peer_o, int32_t n_peers,
                                     int32_t hq_total, int32_t head_offset, void* stream) {
+  NvtxRange nvtx_("dscache_attend_peers");
   if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "attend_peers");
   if (!h) return fail(DSCACHE_E_ARG, "null handle");
   if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
@@ -982,6 +1006,7 @@ dscache_status dscache_ipc_close(int32_t device, void* dev_ptr) {
 
 dscache_status dscache_combine_partials(dscache_t h, int32_t n_parts, int64_t rows, const float* o_parts,
                                         const float* lse_parts, void* o, void* stream) {
+  NvtxRange nvtx_("dscache_combine_partials");
   if (!h) return fail(DSCACHE_E_ARG, "null handle");
   if (n_parts < 1 || rows < 1 || !o_parts || !lse_parts || !o) return fail(DSCACHE_E_ARG, "bad combine arguments");
   if (h->cfg.dtype != DSCACHE_DTYPE_BF16 || h->cfg.head_dim != 128)
@@ -995,6 +1020,7 @@ dscache_status dscache_combine_partials(dscache_t h, int32_t n_parts, int64_t ro
 dscache_status dscache_step(dscache_t h, int32_t lb, int32_t lc, const void* k_frame, const void* v_frame,
                             const void* q_inst, void* o_inst, const void* q, const void* k_self, const void* v_self,
                             int32_t n_q, void* o, void* stream) {
+  NvtxRange nvtx_("dscache_step");
   if (h && h->cfg.instant_source != DSCACHE_INSTANT_RING) return need_mode(h, DSCACHE_INSTANT_RING, "step");
   if (!h) return fail(DSCACHE_E_ARG, "null handle");
   if (n_q < 1 || n_q > h->cfg.max_query_tokens) return fail(DSCACHE_E_ARG, "n_q must be in [1, max_query_tokens]");
@@ -1042,6 +1068,7 @@ dscache_status dscache_step(dscache_t h, int32_t lb, int32_t lc, const void* k_f
 
 dscache_status dscache_update_attend(dscache_t h, int32_t lb, int32_t lc, const void* q_upd, void* o_upd,
                                      int32_t active_frames, void* stream) {
+  NvtxRange nvtx_("dscache_update_attend");
   dscache_status s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
   const dscache_config& c = h->cfg;

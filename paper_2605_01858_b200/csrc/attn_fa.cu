@@ -27,9 +27,9 @@
 // CTA = 16 warps:
 //   warps 0-3  softmax of Q tile 0 (thread = query row = TMEM lane) + its O epilogue
 //   warps 4-7  softmax of Q tile 1
-//   warps 8-11 rotation: raw K tiles of attend items in place in smem, and the Q tiles of
-//              every later item (cp.async + rotation at the query ids); the first item's Q
-//              tiles are prepared by the softmax warpgroups (idle until the first S)
+//   warps 8-11 rotation: raw K tiles of attend items in place in smem, the Q tiles of every
+//              item (loaded and rotated in registers at the query ids, then stored) one item
+//              ahead, and the O epilogue of plain launches
 //   warp 12    K copy (TMA box 64 cols x 128 rows; cp.async for sink/self tiles)
 //   warp 13    V copy
 //   warp 14    TMEM allocator + MMA issuer of Q tile 0 (S0, PV0; one elected lane issues)

@@ -395,7 +395,7 @@ def run_ours(args, cfg, world, rank, local):
     # e2e: the same step through the public API with pinned host buffers, H2D of every
     # input of the step and D2H of the query answer O inside the timed region
     graph = None
-    if getattr(args, "graph", False) and not (context or kvsplit or args.layer_seq):
+    if getattr(args, "graph", False) and world == 1 and not (context or kvsplit or args.layer_seq or n_boost or approx):
         graph = time_graph(args, dsc, step, scratch, dev)
     e2e = (run_e2e(args, cfg, lcfg, dsc, S, dev, stream, world, kvsplit) if not (n_boost or approx) else
            {"skipped": ("boost" if n_boost else "approx") + " mode times the device-resident path only"})
@@ -459,7 +459,8 @@ def run_ours(args, cfg, world, rank, local):
     if graph is not None:
         graph["value"] = round(cfg.num_streams / (graph["ms_per_step"] / 1e3), 2)
         line["graph"] = graph
-    if getattr(args, "whole_stream", False) and world == 1 and not (context or kvsplit or args.layer_seq):
+    if getattr(args, "whole_stream", False) and world == 1 and not (context or kvsplit or args.layer_seq or n_boost
+                                                                     or approx):
         line["whole_stream"] = time_whole_stream(cfg, dev)
     return line
 
@@ -871,14 +872,18 @@ def main():
     ap.add_argument("--decode-nq", type=int, default=1, help="decode mode: query rows per launch")
     ap.add_argument("--decode-stride", type=int, default=1,
                     help="decode mode: keep every STRIDE-th past frame (zeta_decode, PAPER.md:695)")
-    ap.add_argument("--graph", action="store_true", help="also time the timed steps replayed from one CUDA graph")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the graph-replay and whole-stream timings added to the line at N = 1")
+    ap.add_argument("--graph", action="store_true", help="(default at N = 1) time the timed steps replayed from one CUDA graph")
     ap.add_argument("--whole-stream", action="store_true",
-                    help="also time a fresh handle over every frame of the config's stream (whole-stream average)")
+                    help="(default at N = 1) time a fresh handle over every frame of the config's stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if not args.no_extras and int(os.environ.get("WORLD_SIZE", "1")) == 1 and args.gpus == 1:
+        args.graph = args.whole_stream = True
     cfg = synth.CONFIGS[args.config]
     if args.instant_frames is not None:
         cfg = cfg.replace(instant_frames=args.instant_frames)

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--lib", default=None)
     ap.add_argument("--items", type=int, default=12, help="items printed per CTA")
     ap.add_argument("--tiles", type=int, default=4, help="tiles printed per item")
+    ap.add_argument("--first-item", type=int, default=0, help="first item printed per CTA")
     args = ap.parse_args()
     lib = args.lib or _B.build_variant("trace", ["FA_TRACE=1"])
     _D.load_library(lib)
@@ -82,7 +83,7 @@ def main():
                 gi += 1
             rows.append((i, starts[i], nxt, tiles))
         sm_lat = []
-        for i, st, nx, tiles in rows[:args.items]:
+        for i, st, nx, tiles in rows[args.first_item:args.first_item + args.items]:
             q0, q1, of = rel("MMA_Q0", i), rel("MMA_Q1", i), rel("MMA_OF", i)
             print(f" item {i:3d}: start {st:8d}  Q0 +{(q0 or st) - st:5d} Q1 +{(q1 or st) - st:5d} OF +{(of or st) - st:5d}"
                   f"  tiles {len(tiles):3d}  dur {((nx or st) - st):7d}  per tile {((nx or st) - st) / max(len(tiles), 1):7.0f}")

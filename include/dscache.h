@@ -271,6 +271,16 @@ dscache_status dscache_attend_ext(dscache_t h, int32_t layer_begin, int32_t laye
                                   const void* k_self, const void* v_self, int32_t n_q, const void* k_inst,
                                   const void* v_inst, void* o, void* stream);
 
+/* Decoding in the real-model mode (PAPER.md:128 over C_{t+1} = [C_a, U, I], Q25): the last
+ * n_q tokens of an n_self-token self segment (the query chunk and the tokens generated so
+ * far) attend over [sink | past (ring, P_t) | k_inst (C_t) | self], ids contiguous from 0,
+ * causal inside self.  k_inst / v_inst are the step's instant K/V as for dscache_attend_ext;
+ * q [S][lc][n_q][Hq][d], k_self / v_self [S][lc][n_self][Hkv][d], o like q.  E_ARG unless
+ * 1 <= n_q <= n_self; E_CONFIG in the default mode; other errors as dscache_decode. */
+dscache_status dscache_decode_ext(dscache_t h, int32_t layer_begin, int32_t layer_count, const void* q,
+                                  const void* k_self, const void* v_self, int32_t n_self, int32_t n_q,
+                                  const void* k_inst, const void* v_inst, void* o, void* stream);
+
 /* Attention of an n_q-token query chunk over [C_a | U | I | self] (Eq. 8 plus the
  * chunk's own K/V, which are used and then discarded: PAPER.md:212/699).  Ids:
  * sink 0..A-1, past+instant A..A+P_t+C_t-1 (oldest first), query/self token i at

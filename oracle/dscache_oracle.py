@@ -298,7 +298,8 @@ def attend_output_ext(sched: StepSchedule, sink: Tuple[np.ndarray, np.ndarray], 
     """Eq. 8 in the real-model mode: C_t = [C_a, U_t, I_t] where U_t's frames
     carry the K/V of their Eq. 5 update (past_kv(f)) and I_t is the step's
     instant K/V (k_inst, v_inst) -- a frame in the instant window is NOT read from U.
-    Plus the query chunk's own K/V; ids contiguous from 0, queries causal inside the chunk."""
+    Plus the self segment's K/V (the query chunk, and while decoding the tokens generated so
+    far: PAPER.md:128); q are its LAST q.shape[0] tokens; ids contiguous from 0, causal."""
     sk, sv = sink
     hkv, d = sk.shape[1], sk.shape[2]
     ks = _cat([sk] + [past_kv(f)[0] for f in sched.past_frames] + [k_inst, k_self], hkv, d)

@@ -791,26 +791,31 @@ dscache_status build_with_inst(dscache_t h, int32_t lb, int32_t lc, const void* 
 // Eq. 8 over [sink | ring window minus its newest ring_drop tokens | n_inst caller tokens |
 // self (n_q)]: the [caller tokens | self] keys are gathered into per-call stream-ordered
 // scratch [P][n_inst + n_q][Hkv][d] and passed as the self segment.
+// n_self >= n_q: the self segment holds n_self tokens (the query chunk, plus during decoding
+// the tokens generated so far) and the queries are its last n_q (n_self = n_q for an attend).
 dscache_status attend_with_inst(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
                                 const void* v_self, int32_t n_q, const void* k_inst, const void* v_inst,
-                                int32_t n_inst, int ring_drop, void* o, cudaStream_t st) {
+                                int32_t n_inst, int ring_drop, void* o, cudaStream_t st, int32_t n_self = -1) {
+  if (n_self < 0) n_self = n_q;
   const dscache_config& c = h->cfg;
   const size_t row = (size_t)c.num_kv_heads * c.head_dim * h->elem;      // one token of one problem
   const size_t P = (size_t)c.num_streams * lc;
-  const size_t need = P * (size_t)(n_inst + n_q) * row;
+  const size_t need = P * (size_t)(n_inst + n_self) * row;
   DeviceGuard dg(c.device);
   StreamScratch bk, bv;
   if (!bk.alloc(need, st) || !bv.alloc(need, st)) return fail(DSCACHE_E_OOM, "instant gather scratch allocation failed");
   dsc::AttnParams p{};
-  dscache_status s = prep_attend(h, lb, lc, q, bk.ptr, bv.ptr, n_inst + n_q, n_q, o, false, p, ring_drop);
+  dscache_status s = prep_attend(h, lb, lc, q, bk.ptr, bv.ptr, n_inst + n_self, n_q, o, false, p, ring_drop);
   if (s != DSCACHE_OK) return s;
-  // self segment [caller tokens | query chunk] per problem: [P][n_inst + n_q][Hkv][d]
-  const size_t pitch = (size_t)(n_inst + n_q) * row;
-  DSC_CUDA(cudaMemcpy2DAsync(bk.ptr, pitch, k_inst, n_inst * row, n_inst * row, P, cudaMemcpyDeviceToDevice, st));
-  DSC_CUDA(cudaMemcpy2DAsync(bv.ptr, pitch, v_inst, n_inst * row, n_inst * row, P, cudaMemcpyDeviceToDevice, st));
-  DSC_CUDA(cudaMemcpy2DAsync((char*)bk.ptr + n_inst * row, pitch, k_self, n_q * row, n_q * row, P,
+  // self segment [caller tokens | self tokens] per problem: [P][n_inst + n_self][Hkv][d]
+  const size_t pitch = (size_t)(n_inst + n_self) * row;
+  if (n_inst > 0) {
+    DSC_CUDA(cudaMemcpy2DAsync(bk.ptr, pitch, k_inst, n_inst * row, n_inst * row, P, cudaMemcpyDeviceToDevice, st));
+    DSC_CUDA(cudaMemcpy2DAsync(bv.ptr, pitch, v_inst, n_inst * row, n_inst * row, P, cudaMemcpyDeviceToDevice, st));
+  }
+  DSC_CUDA(cudaMemcpy2DAsync((char*)bk.ptr + n_inst * row, pitch, k_self, n_self * row, n_self * row, P,
                              cudaMemcpyDeviceToDevice, st));
-  DSC_CUDA(cudaMemcpy2DAsync((char*)bv.ptr + n_inst * row, pitch, v_self, n_q * row, n_q * row, P,
+  DSC_CUDA(cudaMemcpy2DAsync((char*)bv.ptr + n_inst * row, pitch, v_self, n_self * row, n_self * row, P,
                              cudaMemcpyDeviceToDevice, st));
   return run_attention(h, p, h->impl_attend, 1, st);
 }
@@ -911,6 +916,22 @@ dscache_status dscache_attend_ext(dscache_t h, int32_t lb, int32_t lc, const voi
   if (C_t > 0 && (!k_inst || !v_inst)) return fail(DSCACHE_E_ARG, "null k_inst/v_inst");
   // the ring holds only past frames in this mode: its window minus the C_t instant tokens
   return attend_with_inst(h, lb, lc, q, k_self, v_self, n_q, k_inst, v_inst, C_t, C_t, o, (cudaStream_t)stream);
+}
+
+dscache_status dscache_decode_ext(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,
+                                  const void* v_self, int32_t n_self, int32_t n_q, const void* k_inst,
+                                  const void* v_inst, void* o, void* stream) {
+  NvtxRange nvtx_("dscache_decode_ext");
+  dscache_status s = need_mode(h, DSCACHE_INSTANT_EXTERNAL, "decode_ext");
+  if (s != DSCACHE_OK) return s;
+  if (n_q < 1 || n_q > n_self) return fail(DSCACHE_E_ARG, "need 1 <= n_q <= n_self");
+  s = check_layers(h, lb, lc);
+  if (s != DSCACHE_OK) return s;
+  if (!h->sink_filled[lb] || h->frames[lb] < 1) return fail(DSCACHE_E_STATE, "decode_ext before the sink and the first step");
+  if (!q || !k_self || !v_self || !o) return fail(DSCACHE_E_ARG, "null q/k_self/v_self/o");
+  const int C_t = h->schedule(lb).C_t;
+  if (C_t > 0 && (!k_inst || !v_inst)) return fail(DSCACHE_E_ARG, "null k_inst/v_inst");
+  return attend_with_inst(h, lb, lc, q, k_self, v_self, n_q, k_inst, v_inst, C_t, C_t, o, (cudaStream_t)stream, n_self);
 }
 
 dscache_status dscache_attend_partial(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self,

@@ -56,7 +56,7 @@ class State(ctypes.Structure):
 
 
 EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache_build_instant",
-           "dscache_append_past", "dscache_build_instant_ext", "dscache_attend_ext",
+           "dscache_append_past", "dscache_build_instant_ext", "dscache_attend_ext", "dscache_decode_ext",
            "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest",
            "dscache_instant_approx_rows", "dscache_build_instant_approx", "dscache_decode_sampled", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
@@ -108,6 +108,7 @@ def load_library(path: str = LIB_PATH):
         "dscache_append_past": ([P, I32, I32, P, P, I32, P], I32),
         "dscache_build_instant_ext": ([P, I32, I32, P, P, P, P, P], I32),
         "dscache_attend_ext": ([P, I32, I32, P, P, P, I32, P, P, P, P], I32),
+        "dscache_decode_ext": ([P, I32, I32, P, P, P, I32, I32, P, P, P, P], I32),
         "dscache_attend_peers": ([P, I32, I32, P, P, P, I32, ctypes.POINTER(P), I32, I32, I32, P], I32),
         "dscache_ipc_handle": ([P, P, ctypes.POINTER(I64)], I32),
         "dscache_ipc_open": ([I32, P, ctypes.POINTER(P)], I32),
@@ -359,6 +360,27 @@ class DSCache:
         self._t(o, "o", q.shape)
         _check(_lib.dscache_attend_ext(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_q, _ptr(k_inst),
                                        _ptr(v_inst), _ptr(o), _stream_ptr(stream)))
+        return o
+
+    def decode_ext(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, k_inst: torch.Tensor,
+                   v_inst: torch.Tensor, o: Optional[torch.Tensor] = None, layer_begin: int = 0,
+                   layer_count: Optional[int] = None, stream=None) -> torch.Tensor:
+        """Decode over [sink | past (ring) | caller instant K/V | self]: q = the last n_q of the
+        n_self self tokens (real-model mode)."""
+        lb, lc = self._layers(layer_begin, layer_count)
+        c = self.cfg
+        n_q, n_self = int(q.shape[2]), int(k_self.shape[2])
+        C_t = self.state(lb)["instant_tokens"]
+        self._t(q, "q", (c.num_streams, lc, n_q, c.num_q_heads, c.head_dim))
+        self._t(k_self, "k_self", (c.num_streams, lc, n_self, c.num_kv_heads, c.head_dim))
+        self._t(v_self, "v_self", k_self.shape)
+        self._t(k_inst, "k_inst", (c.num_streams, lc, C_t, c.num_kv_heads, c.head_dim))
+        self._t(v_inst, "v_inst", k_inst.shape)
+        if o is None:
+            o = torch.empty(q.shape, dtype=self.torch_dtype, device=self.device)
+        self._t(o, "o", q.shape)
+        _check(_lib.dscache_decode_ext(self._h, lb, lc, _ptr(q), _ptr(k_self), _ptr(v_self), n_self, n_q,
+                                       _ptr(k_inst), _ptr(v_inst), _ptr(o), _stream_ptr(stream)))
         return o
 
     def attend_peers(self, q: torch.Tensor, k_self: torch.Tensor, v_self: torch.Tensor, peer_ptrs, hq_total: int,

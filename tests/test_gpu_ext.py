@@ -108,6 +108,54 @@ def test_ext_c5_multistream(lib):
     check_ext(cfg, [2, 36, 127], [(0, 0), (7, 3), (63, 1)], l_L=8)
 
 
+@pytest.mark.parametrize("name,t", [("c1", 9), ("c2", 3), ("c2", 40), ("c5", 36)])
+def test_ext_decode_parity(lib, name, t):
+    """dscache_decode_ext: the last n_q of n_self self tokens over [sink | U (Eq. 5 K/V) |
+    the step's instant K/V | self] vs the oracle."""
+    cfg = synth.CONFIGS[name]
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(99)
+    exact = [(0, 0)] if cfg.num_streams == 1 else [(0, 0), (63, 3)]
+    n_self, n_q = cfg.query_tokens + 5, 2
+    dsc = D.DSCache.from_config(cfg.replace(query_tokens=n_self), instant_source=D.INSTANT_EXTERNAL)
+    A, tpf, Hkv, Hq, d, lI = (cfg.sink_tokens, cfg.tokens_per_frame, cfg.num_kv_heads, cfg.num_q_heads,
+                              cfg.head_dim, cfg.instant_frames)
+    skv = {sl: synth.sink_kv(cfg, *sl) for sl in exact}
+    dsc.append_frame(_batch(cfg, (A, Hkv, d), exact, lambda s, l: skv[(s, l)][0], dev, gen),
+                     _batch(cfg, (A, Hkv, d), exact, lambda s, l: skv[(s, l)][1], dev, gen))
+    for step in range(t + 1):
+        e = step - lI
+        if e >= 0:
+            pk = {sl: synth.past_kv(cfg, *sl, e) for sl in exact}
+            dsc.append_past(_batch(cfg, (tpf, Hkv, d), exact, lambda s, l: pk[(s, l)][0], dev, gen),
+                            _batch(cfg, (tpf, Hkv, d), exact, lambda s, l: pk[(s, l)][1], dev, gen))
+        else:
+            dsc.append_past(None, None)
+    C_t = dsc.state(0)["instant_tokens"]
+    ikv = {sl: synth.instant_kv(cfg, *sl, t, C_t) for sl in exact}
+    ki = _batch(cfg, (C_t, Hkv, d), exact, lambda s, l: ikv[(s, l)][0], dev, gen)
+    vi = _batch(cfg, (C_t, Hkv, d), exact, lambda s, l: ikv[(s, l)][1], dev, gen)
+    g = torch.Generator().manual_seed(5)
+    selfkv = {sl: ((torch.randn(n_self, Hkv, d, generator=g) * cfg.scale).to(cfg.torch_dtype),
+                   (torch.randn(n_self, Hkv, d, generator=g) * cfg.scale).to(cfg.torch_dtype),
+                   (torch.randn(n_q, Hq, d, generator=g) * cfg.scale).to(cfg.torch_dtype)) for sl in exact}
+    ks = _batch(cfg, (n_self, Hkv, d), exact, lambda s, l: selfkv[(s, l)][0], dev, gen)
+    vs = _batch(cfg, (n_self, Hkv, d), exact, lambda s, l: selfkv[(s, l)][1], dev, gen)
+    q = _batch(cfg, (n_q, Hq, d), exact, lambda s, l: selfkv[(s, l)][2], dev, gen)
+    o = dsc.decode_ext(q, ks, vs, ki, vi)
+    torch.cuda.synchronize()
+    sch = step_schedule(cfg, t)
+    for (s, l) in exact:
+        inp = StreamInputs(cfg, s, l)
+        pkv = lambda f, s=s, l=l: tuple(_np(x) for x in synth.past_kv(cfg, s, l, f))   # noqa: E731
+        kk_, vv_ = (_np(x) for x in ikv[(s, l)])
+        ref = O.attend_output_ext(sch, inp.sink(), pkv, kk_, vv_, _np(selfkv[(s, l)][2]), _np(selfkv[(s, l)][0]),
+                                  _np(selfkv[(s, l)][1]), cfg.rope_theta)
+        assert_close(o[s, l].float().cpu(), ref, cfg.dtype, f"{name} decode_ext t={t} s={s} l={l}")
+    dsc.close()
+
+
 def test_ext_differs_from_ring_mode(lib):
     """Negative control: the same ring content read through the default mode (ring K/V
     for the buffer frames) gives a different Eq. 8 answer than the caller's instant K/V."""

@@ -908,3 +908,22 @@ def test_decode_sampled_brute_force(stride):
             keys.append((n, list(kq[j, gh]), list(vq[j, gh]))); n += 1
         ref = _brute_attend(list(q[-1, h]), n - 1, keys, cfg.rope_theta)
         assert np.abs(np.array(ref) - o[0, h]).max() < 1e-12
+
+
+def test_ext_decode_reduces_to_decode():
+    """Real-model decoding (the last n_q of n_self self tokens over [C_a, U, I, self]) with the
+    buffer's own K/V as the instant K/V and the frame K/V as U equals decode_output."""
+    cfg = synth.CONFIGS["c1"]
+    inp = StreamInputs(cfg, 0, 0)
+    t = 11
+    sch = step_schedule(cfg, t)
+    ki = np.concatenate([inp.frame_kv(f)[0] for f in sch.instant_frames])
+    vi = np.concatenate([inp.frame_kv(f)[1] for f in sch.instant_frames])
+    q, ks, vs = inp.query(t)
+    gen = np.random.default_rng(21)
+    kg = np.concatenate([ks, gen.standard_normal((3,) + ks.shape[1:])])
+    vg = np.concatenate([vs, gen.standard_normal((3,) + vs.shape[1:])])
+    qg = gen.standard_normal((2,) + q.shape[1:])
+    a = O.decode_output(sch, inp.sink(), inp.frame_kv, qg, kg, vg, cfg.rope_theta)
+    b = O.attend_output_ext(sch, inp.sink(), inp.frame_kv, ki, vi, qg, kg, vg, cfg.rope_theta)
+    assert np.array_equal(a, b)

@@ -112,11 +112,16 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 
 // source row of logical key x of (problem pp, head row hr): [sink | kept past | instant | self]
+template <bool EXT>
 __device__ __forceinline__ long long key_row(const DecodeParams& p, int pp, long long hr, int g, int x, int& kind,
                                              int& slot) {
   if (x < p.A) { kind = 0; slot = x; return hr * p.A + x; }
   x -= p.A;
   const int past = p.kept_frames * p.tpf;
+  if (EXT && x >= past && x < past + p.inst_count) {   // real-model mode: caller's instant K/V
+    kind = 3; slot = x - past;
+    return ((long long)pp * p.inst_count + (x - past)) * p.Hkv + g;
+  }
   if (x < past + p.inst_count) {
     int off;
     if (p.stride == 1 || x >= past) {
@@ -139,6 +144,8 @@ __device__ __forceinline__ long long key_row(const DecodeParams& p, int pp, long
   return ((long long)pp * p.n_self + x) * p.Hkv + g;
 }
 
+// EXT: real-model mode (the instant keys come from the caller's k_inst, not the ring)
+template <bool EXT>
 __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -163,11 +170,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
   const __nv_bfloat16* RV = reinterpret_cast<const __nv_bfloat16*>(p.ring_v);
   const __nv_bfloat16* XK = reinterpret_cast<const __nv_bfloat16*>(p.self_k);
   const __nv_bfloat16* XV = reinterpret_cast<const __nv_bfloat16*>(p.self_v);
+  const __nv_bfloat16* IK = reinterpret_cast<const __nv_bfloat16*>(p.inst_k);
+  const __nv_bfloat16* IV = reinterpret_cast<const __nv_bfloat16*>(p.inst_v);
   const int lr = tid >> 1, lhalf = tid & 1;
   // ring keys [ring0, ring1): kept past then instant, slots consecutive from past_start when
   // every past frame is kept (stride 1); with a stride, runs inside one kept frame or inside
   // the instant window are consecutive
-  const int ring0 = p.A, past_end = p.A + p.kept_frames * p.tpf, ring1 = past_end + p.inst_count;
+  const int ring0 = p.A, past_end = p.A + p.kept_frames * p.tpf;
+  const int ring1 = past_end + (EXT ? 0 : p.inst_count);   // real-model mode: instant not in the ring
   const int n_tab = min(p.n_q, 2);
   if (tid < kStages) bar_init(sbase + kBarOff + 8 * tid, kWarps * 32 + 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -188,7 +198,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
     const uint32_t tab_bytes = base >= 0 ? n_tab * 512 : 512;
     if (tma) {
       int kind = 0, slot = 0;
-      const long long row0 = key_row(p, pp, hr, g, n0, kind, slot);
+      const long long row0 = key_row<EXT>(p, pp, hr, g, n0, kind, slot);
       DSC_ASSERT(kind == 1 && slot + kTileKeys <= p.Rp, "decode TMA box rows");
       if (tid == 0) {
         bar_arrive_tx(bar, 4 * kHalfBytes + tab_bytes);
@@ -209,9 +219,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
       const int x = n0 + lr;
       const bool valid = x < p.n_keys;
       int kind = 0, slot = 0;
-      const long long row = valid ? key_row(p, pp, hr, g, x, kind, slot) : 0;
-      const __nv_bfloat16* ks = (kind == 0 ? SK : kind == 1 ? RK : XK) + row * 128;
-      const __nv_bfloat16* vs = (kind == 0 ? SV : kind == 1 ? RV : XV) + row * 128;
+      const long long row = valid ? key_row<EXT>(p, pp, hr, g, x, kind, slot) : 0;
+      const __nv_bfloat16* ks = (kind == 0 ? SK : kind == 1 ? RK : (!EXT || kind == 2) ? XK : IK) + row * 128;
+      const __nv_bfloat16* vs = (kind == 0 ? SV : kind == 1 ? RV : (!EXT || kind == 2) ? XV : IV) + row * 128;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int c = 2 * j + lhalf;
@@ -224,7 +234,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
         else bulk_g2s(sb + kTabOff + 512, p.rope_pairs, 512, bar);
       }
       bar_cp_arrive(bar);
-      if (dbgp && valid && lhalf == 0)
+      if (dbgp && valid && lhalf == 0 && (!EXT || kind != 3))
         dbgp[kind == 0 ? slot : kind == 1 ? p.dbg_A + slot : p.dbg_A + p.dbg_R + slot] = x;
     }
   };
@@ -507,13 +517,16 @@ cudaError_t launch_decode(const DecodeParams& p, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 31 && !(configured_mask & (1 << dev))) {
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e != cudaSuccess) return e;
     configured_mask |= 1 << dev;
   }
   const long long blocks = (long long)p.P * p.Hkv * p.n_splits;
   if (blocks == 0) return cudaSuccess;
-  decode_kernel<<<(unsigned)blocks, kWarps * 32, kSmemBytes, st>>>(p);
+  if (p.inst_k != nullptr) decode_kernel<true><<<(unsigned)blocks, kWarps * 32, kSmemBytes, st>>>(p);
+  else decode_kernel<false><<<(unsigned)blocks, kWarps * 32, kSmemBytes, st>>>(p);
   return cudaGetLastError();
 }
 

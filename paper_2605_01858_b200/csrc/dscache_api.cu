@@ -643,7 +643,8 @@ bool decode_kernel_ok(dscache_t h, int n_q) {
 }
 
 dscache_status run_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, const void* k_self, const void* v_self,
-                          int32_t n_self, int32_t n_q, int32_t stride, void* o, cudaStream_t st) {
+                          int32_t n_self, int32_t n_q, int32_t stride, void* o, cudaStream_t st,
+                          const void* k_inst = nullptr, const void* v_inst = nullptr) {
   dscache_status s = check_layers(h, lb, lc);
   if (s != DSCACHE_OK) return s;
   if (!h->sink_filled[lb] || h->frames[lb] < 1)
@@ -653,6 +654,7 @@ dscache_status run_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, co
   const dscache_config& c = h->cfg;
   const Schedule sc = h->schedule(lb);
   const int tpf = c.tokens_per_frame;
+  // (real-model mode: the ring holds the same past; the C_t instant keys come from k_inst)
   const int past_frames = sc.P_t / tpf;
   const int kept = (past_frames + stride - 1) / stride;
   const int64_t n_keys = (int64_t)c.sink_tokens + (int64_t)kept * tpf + sc.C_t + n_self;
@@ -667,6 +669,7 @@ dscache_status run_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, co
   p.past_start = sc.ring_start; p.tpf = tpf; p.past_frames = past_frames; p.stride = stride; p.kept_frames = kept;
   p.inst_start = sc.inst_start; p.inst_count = sc.C_t;
   p.self_k = k_self; p.self_v = v_self; p.n_self = n_self;
+  p.inst_k = k_inst; p.inst_v = v_inst;
   p.n_keys = (int)n_keys;
   p.q_pos0 = (int)(n_keys - n_q);
   p.rope_pairs = reinterpret_cast<const float4*>(h->rope + (size_t)h->npos * (c.head_dim / 2));
@@ -931,6 +934,8 @@ dscache_status dscache_decode_ext(dscache_t h, int32_t lb, int32_t lc, const voi
   if (!q || !k_self || !v_self || !o) return fail(DSCACHE_E_ARG, "null q/k_self/v_self/o");
   const int C_t = h->schedule(lb).C_t;
   if (C_t > 0 && (!k_inst || !v_inst)) return fail(DSCACHE_E_ARG, "null k_inst/v_inst");
+  if (C_t > 0 && decode_kernel_ok(h, n_q) && h->impl_attend == DSCACHE_IMPL_TC)   // the memory-bound decode kernel
+    return run_decode(h, lb, lc, q, k_self, v_self, n_self, n_q, 1, o, (cudaStream_t)stream, k_inst, v_inst);
   return attend_with_inst(h, lb, lc, q, k_self, v_self, n_q, k_inst, v_inst, C_t, C_t, o, (cudaStream_t)stream, n_self);
 }
 

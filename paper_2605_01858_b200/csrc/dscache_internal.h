@@ -121,6 +121,7 @@ struct DecodeParams {
   int past_start, tpf, past_frames, stride, kept_frames;
   int inst_start, inst_count;
   const void* self_k; const void* self_v; int n_self;   // [P][n_self][Hkv][d]
+  const void* inst_k; const void* inst_v;      // real-model mode: the instant keys [P][inst_count][Hkv][d], else null
   int q_pos0;                                  // id of query row 0 (its token is self token n_self - n_q)
   int n_keys;                                  // A + kept_frames * tpf + inst_count + n_self
   const float4* rope_pairs;

@@ -315,9 +315,9 @@ dscache_status dscache_decode(dscache_t h, int32_t layer_begin, int32_t layer_co
  * contiguous ids: sink 0..A-1, kept past A.., instant, then self.
  * past_stride = 1 is dscache_decode.  The memory-bound decode kernel serves bf16, d = 128,
  * split-half RoPE and n_q * Hq/Hkv <= 16 (one 16-row tile per kv head, all q heads of the
- * group sharing every K/V byte read); other decodes run through the attention kernel and
- * accept past_stride = 1 only (E_CONFIG otherwise).  E_ARG for past_stride < 1; other
- * errors as dscache_decode (the position check uses the kept past). */
+ * group sharing every K/V byte read); other decodes run through the attention kernel, or
+ * with past_stride > 1 through the SIMT kernel.  E_ARG for past_stride < 1; other errors
+ * as dscache_decode. */
 dscache_status dscache_decode_sampled(dscache_t h, int32_t layer_begin, int32_t layer_count,
                                       const void* q, const void* k_self, const void* v_self, int32_t n_self,
                                       int32_t n_q, int32_t past_stride, void* o, void* stream);

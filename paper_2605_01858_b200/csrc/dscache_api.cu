@@ -728,10 +728,21 @@ dscache_status dscache_decode_sampled(dscache_t h, int32_t lb, int32_t lc, const
   if (past_stride < 1) return fail(DSCACHE_E_ARG, "past_stride must be >= 1");
   if (decode_kernel_ok(h, n_q) && h->impl_attend == DSCACHE_IMPL_TC)
     return run_decode(h, lb, lc, q, k_self, v_self, n_self, n_q, past_stride, o, (cudaStream_t)stream);
-  if (past_stride != 1)
-    return fail(DSCACHE_E_CONFIG, "past_stride > 1 needs the decode kernel (bf16, d = 128, split-half RoPE, "
-                                  "n_q * Hq/Hkv <= 16)");
-  return attend_common(h, lb, lc, q, k_self, v_self, n_self, n_q, o, stream, false);
+  if (past_stride == 1) return attend_common(h, lb, lc, q, k_self, v_self, n_self, n_q, o, stream, false);
+  // sampled past off the decode kernel (fp32, d = 64, adjacent RoPE, or > 16 query rows):
+  // the SIMT kernel with the stride's slot map
+  dsc::AttnParams p{};
+  dscache_status s = prep_attend(h, lb, lc, q, k_self, v_self, n_self, n_q, o, false, p);
+  if (s != DSCACHE_OK) return s;
+  const Schedule sc = h->schedule(lb);
+  const int tpf = h->cfg.tokens_per_frame;
+  const int past_frames = sc.P_t / tpf, kept = (past_frames + past_stride - 1) / past_stride;
+  p.past_stride = past_stride; p.stride_tpf = tpf; p.stride_past_frames = past_frames; p.stride_kept_frames = kept;
+  p.ring_count = kept * tpf + sc.C_t;
+  p.q_pos0 = h->cfg.sink_tokens + p.ring_count + (n_self - n_q);
+  p.n_splits = 1; p.tiles_per_split = 1 << 30;
+  DeviceGuard dg(h->cfg.device);
+  return run_attention(h, p, DSCACHE_IMPL_SIMT, 1, (cudaStream_t)stream);
 }
 
 namespace {

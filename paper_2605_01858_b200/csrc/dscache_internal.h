@@ -64,6 +64,9 @@ struct AttnParams {
   const void* ring_k; const void* ring_v;   // [S][N][Hkv][Rp][d]: slots [0, R) + mirror of slots [0, 128)
   int R, Rp;                                 // ring slots, rows per head (R + kMirror)
   int ring_start, ring_count;
+  // SIMT kernel only: the past sampled at a frame stride (decode_sampled off the decode kernel):
+  // ring keys [0, kept*tpf) are kept past frames (newest-anchored), then the instant window
+  int past_stride, stride_tpf, stride_past_frames, stride_kept_frames;
   const void* self_k; const void* self_v;   // [P][n_self][Hkv][d]
   int n_self;
   // rope

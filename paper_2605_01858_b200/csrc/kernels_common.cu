@@ -295,8 +295,21 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnParams p) {
       kr = SK + (head_row * p.A + L) * D; vr = SV + (head_row * p.A + L) * D;
       if (dbg_keys && lane == 0) dbgp[L] = L;
     } else if (L < p.A + p.ring_count) {
-      int slot = p.ring_start + (L - p.A);
-      if (slot >= p.R) slot -= p.R;
+      const int x = L - p.A;
+      int slot;
+      if (p.past_stride > 1) {
+        const int kept = p.stride_kept_frames * p.stride_tpf;
+        if (x < kept) {
+          const int kk = x / p.stride_tpf, tok = x - kk * p.stride_tpf;
+          const int j = p.stride_past_frames - 1 - p.past_stride * (p.stride_kept_frames - 1 - kk);
+          slot = (p.ring_start + j * p.stride_tpf + tok) % p.R;
+        } else {
+          slot = (p.ring_start + p.stride_past_frames * p.stride_tpf + (x - kept)) % p.R;
+        }
+      } else {
+        slot = p.ring_start + x;
+        if (slot >= p.R) slot -= p.R;
+      }
       DSC_ASSERT(slot >= 0 && slot < p.R, "simt ring slot");
       kr = RK + (head_row * p.Rp + slot) * D; vr = RV + (head_row * p.Rp + slot) * D;
       if (dbg_keys && lane == 0) dbgp[p.dbg_A + slot] = L;

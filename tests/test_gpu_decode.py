@@ -113,8 +113,16 @@ def test_decode_kernel_ids_bit_exact(lib, stride):
     assert np.array_equal(blk[A + R + M:A + R + M + n_q], L + n_self - n_q + np.arange(n_q))
 
 
+@pytest.mark.parametrize("stride", [2, 3])
+def test_decode_sampled_off_the_decode_kernel(lib, stride):
+    """The sampled past through the SIMT kernel: fp32 (c1) and bf16 with more than 16 query
+    rows per kv head (c2, n_q = 3 -> 21 rows)."""
+    check_decode(synth.CONFIGS["c1"].replace(num_frames=40), 19, [(0, 0)], 12, 2, stride)
+    check_decode(synth.CONFIGS["c2"], 40, [(0, 0)], 70, 3, stride)
+
+
 def test_decode_stride_errors(lib):
-    cfg = synth.CONFIGS["c1"]          # fp32: no decode kernel, stride 1 only
+    cfg = synth.CONFIGS["c1"]
     dsc = D.DSCache.from_config(cfg)
     dev = torch.device("cuda", 0)
     z = torch.zeros(1, 1, cfg.sink_tokens, cfg.num_kv_heads, cfg.head_dim, device=dev)
@@ -124,9 +132,6 @@ def test_decode_stride_errors(lib):
     q = torch.zeros(1, 1, 1, cfg.num_q_heads, cfg.head_dim, device=dev)
     kv = torch.zeros(1, 1, 2, cfg.num_kv_heads, cfg.head_dim, device=dev)
     dsc.decode(q, kv, kv)
-    with pytest.raises(D.DSCacheError) as e:
-        dsc.decode(q, kv, kv, past_stride=2)
-    assert e.value.status == D.E_CONFIG
     with pytest.raises(D.DSCacheError) as e:
         dsc.decode(q, kv, kv, past_stride=0)
     assert e.value.status == D.E_ARG

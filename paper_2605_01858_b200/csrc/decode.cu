@@ -463,9 +463,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
   __threadfence();
   __syncthreads();
   if (tid == 0) {
-    const int ticket = atomicAdd(p.counters + hr, 1);
+    const int ticket = atomicAdd(p.counters + unit, 1);   // this call's zeroed ticket of (problem, kv head)
     last = ticket == p.n_splits - 1;
-    if (last) p.counters[hr] = 0;                   // ready for the next launch (stream-ordered)
   }
   __syncthreads();
   if (!last) return;

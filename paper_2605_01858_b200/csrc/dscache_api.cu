@@ -94,7 +94,6 @@ struct dscache_s {
   std::vector<int> approx_lc;
   int* dbg_build = nullptr;
   int* dbg_attend = nullptr;
-  int* dec_counters = nullptr;   // decode split-KV tickets, one per (stream, layer, kv head), zero at rest
   int poison = 0;
   long long* trace = nullptr;
   int ntrace = 0;
@@ -358,7 +357,6 @@ dscache_status dscache_destroy(dscache_t h) {
   cudaFree(h->rope);
   cudaFree(h->stage_k); cudaFree(h->stage_v);
   cudaFree(h->bstage_k); cudaFree(h->bstage_v);
-  cudaFree(h->dec_counters);
   dsc::sched_cache_free(h->sched);
   delete h;
   return DSCACHE_OK;
@@ -689,17 +687,17 @@ dscache_status run_decode(dscache_t h, int32_t lb, int32_t lc, const void* q, co
   p.n_splits = splits;
   StreamScratch ws;
   if (splits > 1) {
-    if (!h->dec_counters) {
-      const size_t n = (size_t)c.num_streams * c.num_layers * c.num_kv_heads;
-      if (cudaMalloc(&h->dec_counters, n * sizeof(int)) != cudaSuccess) { cudaGetLastError(); return fail(DSCACHE_E_OOM, "decode counters"); }
-      if (cudaMemset(h->dec_counters, 0, n * sizeof(int)) != cudaSuccess) return fail(DSCACHE_E_CUDA, "decode counters");
-    }
+    // per-call workspace: the partials, their log2-sum-exps and one zeroed ticket per
+    // (problem, kv head), so concurrent decodes on different streams share nothing
     const size_t rows = (size_t)p.P * n_q * c.num_q_heads;
-    if (!ws.alloc((size_t)splits * rows * (c.head_dim + 1) * sizeof(float), st))
+    const size_t fl = (size_t)splits * rows * (c.head_dim + 1);
+    if (!ws.alloc(fl * sizeof(float) + (size_t)units * sizeof(int), st))
       return fail(DSCACHE_E_OOM, "decode split-KV workspace");
     p.ws_o = static_cast<float*>(ws.ptr);
     p.ws_lse = p.ws_o + (size_t)splits * rows * c.head_dim;
-    p.counters = h->dec_counters;
+    p.counters = reinterpret_cast<int*>(p.ws_o + fl);
+    if (cudaMemsetAsync(p.counters, 0, (size_t)units * sizeof(int), st) != cudaSuccess)
+      return fail(DSCACHE_E_CUDA, "decode tickets");
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->prof) { e0 = h->take_event(); e1 = h->take_event(); cudaEventRecord(e0, st); }

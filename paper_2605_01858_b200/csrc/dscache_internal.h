@@ -131,7 +131,7 @@ struct DecodeParams {
   float scale_log2;
   int n_splits, tiles_per_split;               // key range split in 128-key tiles
   float* ws_o; float* ws_lse;                  // [n_splits][P*n_q*Hq][d], [n_splits][P*n_q*Hq]
-  int* counters;                               // per (stream, layer, kv head) ticket, zero between launches
+  int* counters;                               // per-call tickets, one per (problem, kv head), zeroed
   int* dbg_pos; int dbg_len, dbg_A, dbg_R, dbg_M;   // debug id export (kv head 0), null = off
   // TMA descriptors of the K / V rings ([S*N*Hkv*Rp rows][128] bf16, box 64 x 128, SW128):
   // 128-key tiles that are one consecutive ring run load with four TMA boxes

@@ -478,7 +478,8 @@ class DSCache:
         """A row ring for build_instant_approx: [S][lc][C][Hq][d], frame f at rows (f mod l_I)*tpf."""
         c = self.cfg
         lc = c.num_layers if layer_count is None else layer_count
-        return torch.zeros((c.num_streams, lc, c.instant_frames * c.tokens_per_frame, c.num_q_heads, c.head_dim),
+        C = self.state(0)["instant_capacity"]   # C = l_I * tpf, from the library
+        return torch.zeros((c.num_streams, lc, C, c.num_q_heads, c.head_dim),
                            dtype=self.torch_dtype, device=self.device)
 
     def approx_rows(self, o_ring: torch.Tensor, period: int, layer_begin: int = 0,
@@ -497,7 +498,7 @@ class DSCache:
         c = self.cfg
         n = int(q_rows.shape[2])
         self._t(q_rows, "q_rows", (c.num_streams, lc, n, c.num_q_heads, c.head_dim))
-        self._t(o_ring, "o_ring", (c.num_streams, lc, c.instant_frames * c.tokens_per_frame, c.num_q_heads,
+        self._t(o_ring, "o_ring", (c.num_streams, lc, self.state(lb)["instant_capacity"], c.num_q_heads,
                                    c.head_dim))
         _check(_lib.dscache_build_instant_approx(self._h, lb, lc, int(period), _ptr(q_rows), n, _ptr(o_ring),
                                                  _stream_ptr(stream)))

@@ -24,7 +24,7 @@ class HostStepPipeline:
         self.lc = c.num_layers - layer_begin if layer_count is None else layer_count
         dev, dt = dsc.device, dsc.torch_dtype
         S, N, tpf, Hkv, Hq, d = c.num_streams, self.lc, c.tokens_per_frame, c.num_kv_heads, c.num_q_heads, c.head_dim
-        C = c.instant_frames * tpf
+        C = dsc.state(layer_begin)["instant_capacity"]   # C = l_I * tpf, from the library
 
         def e(*shape):
             return torch.empty(shape, dtype=dt, device=dev)

@@ -104,6 +104,8 @@ def softmax_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, visible: np.n
     query sees at least itself).
     """
     d = q.shape[-1]
+    if q.shape[0] == 0 or k.shape[0] == 0:   # an empty attention (e.g. no instant cache: l_I = 0)
+        return np.zeros((q.shape[0], v.shape[-1]), np.float64)
     s = (q @ k.T) / math.sqrt(d)
     s = np.where(visible, s, -np.inf)
     m = np.max(s, axis=1, keepdims=True)

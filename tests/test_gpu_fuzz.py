@@ -63,3 +63,34 @@ def test_fuzz_fused_step(lib, idx):
     exact = sorted({(0, 0), (cfg.num_streams - 1, cfg.num_layers - 1)})
     res = run_stream(cfg, steps, exact, fused=True)
     _check_steps(cfg, res, steps, exact, style=style, tag=f"-fuzzstep{idx}")
+
+
+@pytest.mark.parametrize("idx", [i for i, (c, st) in enumerate(CASES) if st == O.SPLIT_HALF])
+def test_fuzz_decode(lib, idx):
+    """Decode (and the sampled past) on the same shapes: the decode kernel where it applies
+    (bf16, d 128, <= 16 query rows per kv head), else the attention or SIMT kernel."""
+    from tests.test_gpu_decode import check_decode
+    cfg, _ = CASES[idx]
+    n_q = 1 + idx % 2
+    stride = 1 + (idx // 2) % 3
+    exact = sorted({(0, 0), (cfg.num_streams - 1, cfg.num_layers - 1)})
+    check_decode(cfg, cfg.num_frames - 1, exact, cfg.query_tokens + 3, n_q, stride)
+
+
+@pytest.mark.parametrize("idx", [i for i, (c, st) in enumerate(CASES) if st == O.SPLIT_HALF and c.instant_frames > 0])
+def test_fuzz_approx(lib, idx):
+    """The approximate instant cache (refresh state machine) on the same shapes, every step."""
+    from tests.test_gpu_approx import check_approx
+    cfg, _ = CASES[idx]
+    period = 1 + idx % 4
+    check_approx(cfg, period, list(range(cfg.num_frames)), sorted({(0, 0), (cfg.num_streams - 1, cfg.num_layers - 1)}))
+
+
+@pytest.mark.parametrize("idx", [i for i, (c, st) in enumerate(CASES) if st == O.SPLIT_HALF])
+def test_fuzz_ext(lib, idx):
+    """The real-model mode (caller instant K/V, Eq. 5 K/V in U, Eq. 5 attention) on the same shapes."""
+    from tests.test_gpu_ext import check_ext
+    cfg, _ = CASES[idx]
+    steps = sorted({0, cfg.instant_frames + cfg.past_frames, cfg.num_frames - 1})
+    check_ext(cfg, steps, sorted({(0, 0), (cfg.num_streams - 1, cfg.num_layers - 1)}),
+              l_L=max(1, cfg.past_frames) if cfg.past_frames > 0 else None)

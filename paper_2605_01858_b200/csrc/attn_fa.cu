@@ -943,6 +943,734 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace fa
 
+// ==========================================================================================
+// v8: the CTA-pair kernel (tcgen05.mma.cta_group::2, M = 256).  Same work items, same Eq. 7 /
+// Eq. 8 arithmetic as v7; the 256 query rows of an item are split over the two SMs of a
+// cluster (CTA r holds Q rows 128 r .. 128 r + 127 of the m-block and owns TMEM lanes = those
+// rows), each 128-key tile is split by the B operand's N: CTA r loads and rotates keys
+// [r nu/2, (r + 1) nu/2) of the tile for QK^T and the d columns [64 r, 64 r + 64) of all
+// its V rows for PV (scripts/micro/pair_mma_test.cu checks these layouts and the full
+// 8190 flop/clk/SM rate of the pair MMA).  Per SM that halves the K rotation, the Q prep,
+// the O epilogue and the shared-memory operand traffic of a tile, and it frees TMEM:
+//   S[2] = cols 0..255 (double-buffered: S(g+1) is computed while the softmax works on S(g)),
+//   O[2] = cols 256..511 (double-buffered by item: an item's epilogue overlaps the next item).
+// The leader CTA (rank 0) issues every MMA; its waits gather arrivals from both CTAs
+// (remote mbarrier arrives), its commits are multicast to both.
+//   warps 0-3  softmax of this CTA's 128 rows (thread = row = TMEM lane), (l, m) per item
+//   warps 4-7  K rotation of this CTA's key half, the Q tile prep one item ahead, the epilogue
+//   warp 8     K copy (TMA 64 x 64 boxes / cp.async sink+self rows), warp 9 V copy
+//   warp 10    TMEM allocation; MMA issuer (leader)
+//   warp 11    forwarder: locally landed V (and pre-rotated staged K) -> the leader's barriers
+namespace pr {
+using namespace tcc;
+using fa::fwait;
+using fa::ex2f;
+using fa::tmem_ld32x;
+using fa::load_rotate_q_regs;
+using fa::item_of;
+using fa::load_rec;
+
+constexpr int BN = kTileN;
+constexpr int kWarps = 12;
+constexpr int kThreads = kWarps * 32;
+constexpr int kQBytes = 128 * 128 * 2;    // this CTA's Q tile: two 64-column SW128 blocks of 128 rows
+constexpr int kKHalf = 64 * 128;          // one 64-column SW128 block of this CTA's <= 64 keys (8 KB)
+constexpr int kKBytes = 2 * kKHalf;
+constexpr int kVBytes = 128 * 128;        // 128 keys x this CTA's 64 d columns (16 KB)
+constexpr int NQB = 2, KST = 4, VST = 3;
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = OFF_Q + NQB * kQBytes;
+constexpr int OFF_V = OFF_K + KST * kKBytes;
+constexpr int OFF_BAR = OFF_V + VST * kVBytes;
+enum {
+  B_QR = 0,             // [2] Q buffer ready (leader: 4 warps x 2 CTAs)
+  B_QF = B_QR + 2,      // [2] Q buffer free (commit after its item's last QK^T)
+  B_KR = B_QF + 2,      // [KST] K half landed in this CTA (TMA tx / cp.async)
+  B_KF = B_KR + KST,    // [KST] K tile ready for the MMA (leader: 8 = rotation warps, or forwarders x 4)
+  B_KE = B_KF + KST,    // [KST] K stage free (commit)
+  B_VL = B_KE + KST,    // [VST] V landed in this CTA
+  B_VR = B_VL + VST,    // [VST] V ready (leader: 2 forwarders)
+  B_VE = B_VR + VST,    // [VST] V stage free = PV done (commit)
+  B_S = B_VE + VST,     // [2] S buffer ready (commit)
+  B_P = B_S + 2,        // [2] P ready (leader: 8)
+  B_O = B_P + 2,        // [2] O buffer final for its item (commit)
+  B_OF = B_O + 2,       // [2] O buffer read out (leader: 8)
+  B_LR = B_OF + 2,      // [2] (l, m) of an item's rows written (128 softmax threads)
+  B_LF = B_LR + 2,      // [2] ... read by the epilogue (128)
+  B_N = B_LF + 2
+};
+constexpr int OFF_L = OFF_BAR + B_N * 8 + 8;                  // (l, m) handoff [2][128] float2
+constexpr int kSmemBytes = OFF_L + 2 * 128 * 8 + 1024;
+static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+constexpr float kRescaleThreshold = 8.0f;
+// ablation knobs (timing experiments only; results are wrong when set)
+#ifndef PR_ABL_SM
+#define PR_ABL_SM 0
+#endif
+#ifndef PR_ABL_Q
+#define PR_ABL_Q 0
+#endif
+#ifndef PR_ABL_EPI
+#define PR_ABL_EPI 0
+#endif
+#ifndef PR_ABL_ROT
+#define PR_ABL_ROT 0
+#endif
+
+// PR_TRACE 1 (profiling variant): clock64 of pipeline events into p.trace for the first
+// ntrace_cta CTAs, [cta][kPtEvents][kPtIdx]; per-tile events by the global tile g, per-item by item
+#ifndef PR_TRACE
+#define PR_TRACE 0
+#endif
+constexpr int kPtEvents = 32, kPtIdx = 1024;
+enum {
+  PT_S_ISS = 0, PT_PV_ISS, PT_KF_OK, PT_VR_OK, PT_P_OK, PT_SM_S, PT_SM_P, PT_CPK, PT_CPV, PT_FWV, PT_ROT,   // per tile
+  PT_ITEM = 12, PT_Q_START, PT_Q_FREE, PT_Q_END, PT_EPI_O, PT_EPI_END, PT_QR_OK, PT_OF_OK, PT_END,           // per item
+  PT_KR_FW = 21
+};
+#if PR_TRACE
+#define PT(ev, i)                                                                                      \
+  do {                                                                                                 \
+    if (pt_cta && (i) < kPtIdx) pt_cta[(ev) * kPtIdx + (i)] = clock64();                                \
+  } while (0)
+#else
+#define PT(ev, i) do { } while (0)
+#endif
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same offset in the leader CTA (rank 0)
+__device__ __forceinline__ uint32_t map_lead(uint32_t a) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(a));
+  return r;
+}
+// remote arrive with the default .release.cta semantics (the producer's writes are ordered for
+// the consumer by the proxy / tcgen05 fences before it; .release.cluster compiles to a GPU-scope
+// MEMBAR before every arrival)
+__device__ __forceinline__ void arrive_cl(uint32_t cbar, uint32_t cnt) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0], %1;" ::"r"(cbar), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_cl(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  return ok != 0;
+}
+// wait on a barrier that collects arrivals from both CTAs (cluster-scope acquire)
+__device__ __forceinline__ void cwait(uint32_t bar, uint32_t parity, uint32_t bar0) {
+  if (mbar_try_cl(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_cl(bar, parity)) {
+    if (clock64() - t0 > fa::g_fa_wd_lim) fa::fa_wd_fail((bar - bar0) / 8, parity);
+  }
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// commit of the pair's MMAs, arriving on the barrier at this offset in BOTH CTAs
+__device__ __forceinline__ void commit2_w(uint32_t bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+          bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// S = Q K^T (M = 256 over the pair, K = 128 as 8 x K16): A = Q tile (second 64-column block
+// +16 KB = 1024 units), B = this CTA's key half (second block +8 KB = 512 units)
+__device__ __forceinline__ void mma2_qk(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred e;\n.reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n"
+      "add.s64 a1, %1, 2; add.s64 a2, %1, 4; add.s64 a3, %1, 6;\n"
+      "add.s64 a4, %1, 1024; add.s64 a5, %1, 1026; add.s64 a6, %1, 1028; add.s64 a7, %1, 1030;\n"
+      "add.s64 b1, %2, 2; add.s64 b2, %2, 4; add.s64 b3, %2, 6;\n"
+      "add.s64 b4, %2, 512; add.s64 b5, %2, 514; add.s64 b6, %2, 516; add.s64 b7, %2, 518;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a4, b4, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a5, b5, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a6, b6, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a7, b7, %3, 1;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc)
+      : "memory");
+}
+// O += P V over a full 128-key tile: A = P in TMEM (8 columns per K16 step), B = V rows
+// (MN-major SW128, 16 keys = 2048 B = 128 units per step)
+__device__ __forceinline__ void mma2_pv8(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred e, p;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7;\n.reg .b32 t1, t2, t3, t4, t5, t6, t7;\n"
+      "add.s64 b1, %2, 128; add.s64 b2, %2, 256; add.s64 b3, %2, 384;\n"
+      "add.s64 b4, %2, 512; add.s64 b5, %2, 640; add.s64 b6, %2, 768; add.s64 b7, %2, 896;\n"
+      "add.u32 t1, %1, 8; add.u32 t2, %1, 16; add.u32 t3, %1, 24;\n"
+      "add.u32 t4, %1, 32; add.u32 t5, %1, 40; add.u32 t6, %1, 48; add.u32 t7, %1, 56;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t1], b1, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t2], b2, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t3], b3, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t4], b4, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t5], b5, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t6], b6, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t7], b7, %3, 1;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_pv1(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// the pair's tile width: valid keys rounded up to 32, so each CTA's half is a multiple of 16
+__device__ __forceinline__ int width2(const TileSeg& t) { return (t.width + 31) & ~31; }
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    attn_pair_kernel(const __grid_constant__ AttnParams pa, const __grid_constant__ AttnParams pb, int na, int nb) {
+  const AttnParams& p = pa;   // launch-wide fields (rope table) are shared
+#if PR_TRACE
+  long long* const pt_cta = (pa.trace && blockIdx.x < (unsigned)pa.ntrace_cta)
+                                ? pa.trace + (long long)blockIdx.x * kPtEvents * kPtIdx : nullptr;
+#endif
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bar0 = sbase + OFF_BAR;
+  auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
+  const uint32_t lbar0 = map_lead(bar0);   // the leader's barriers in the cluster window
+  auto lbar = [&](int i) { return lbar0 + 8u * (uint32_t)i; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + B_N * 8);
+  float2* lbuf = reinterpret_cast<float2*>(smem + OFF_L);
+  const int rank = (int)cta_rank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#define REC_PARAMS(R) (((R).flags & 1) ? pb : pa)
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(B_QR + i), 8);
+      mbar_init(bar(B_QF + i), 1);
+      mbar_init(bar(B_S + i), 1);
+      mbar_init(bar(B_P + i), 8);
+      mbar_init(bar(B_O + i), 1);
+      mbar_init(bar(B_OF + i), 8);
+      mbar_init(bar(B_LR + i), 128);
+      mbar_init(bar(B_LF + i), 128);
+    }
+    for (int i = 0; i < KST; ++i) {
+      mbar_init(bar(B_KR + i), 1);
+      mbar_init(bar(B_KF + i), 8);
+      mbar_init(bar(B_KE + i), 1);
+    }
+    for (int i = 0; i < VST; ++i) {
+      mbar_init(bar(B_VL + i), 1);
+      mbar_init(bar(B_VR + i), 2);
+      mbar_init(bar(B_VE + i), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async();
+  }
+  if (warp == 10) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (warp == 8 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pa.tmap_k64)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pa.tmap_v)) : "memory");
+    if (nb > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pb.tmap_k64)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pb.tmap_v)) : "memory");
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // this cluster's items (both CTAs walk the same list)
+  const int cl = blockIdx.x >> 1;
+  const ItemRec* __restrict__ recs = pa.item_recs + pa.item_off[cl];
+  const int n_my = pa.item_off[cl + 1] - pa.item_off[cl];
+  auto qbuf_addr = [&](int k) { return sbase + OFF_Q + (uint32_t)((k & 1) * kQBytes); };
+
+  if (warp < 4) {
+    // ================================================================ softmax
+    const int rloc = warp * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const float sl2 = p.scale_log2;
+    const float2 scale2 = make_float2(sl2, sl2);
+    int g = 0;
+    for (int kk = 0; kk < n_my; ++kk) {
+      const ItemRec rec = load_rec(recs, kk);
+      const AttnParams& p = REC_PARAMS(rec);
+      const Item w = item_of(p, rec);
+      const int A = w.A;
+      const int n = w.n_tiles;
+      const int rglob = w.m0 + rank * 128 + rloc;
+      const bool valid_row = rglob < w.rows_total;
+      const int qi = valid_row ? rglob / p.grp : 0;
+      const int lim = valid_row ? p.q_pos0 + qi : -1;
+      const bool warp_dead = __all_sync(0xffffffffu, !valid_row);
+      const uint32_t tO = tmem + lane_off + (uint32_t)(256 + (kk & 1) * 128);
+      float m = -INFINITY;
+      float2 lsum2 = make_float2(0.f, 0.f);
+      uint32_t r[64];
+      for (int jj = 0; jj < n; ++jj, ++g) {
+        const int u = w.t_begin + jj;
+        const TileSeg t = tile_segments<BN>(p, w, u);
+        const int nu = width2(t);
+        int c_lo, c_hi;
+        if (!valid_row) {
+          c_lo = 0; c_hi = 0;
+        } else if (u < w.n_extra) {
+          c_lo = 0;
+          c_hi = min(max(min(A + w.n_self, max(A, lim - w.ring_count + 1)) - BN * u, 0), BN);
+        } else {
+          c_lo = t.lo0;
+          c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));
+        }
+        const uint32_t tS = tmem + lane_off + (uint32_t)((g & 1) * 128);
+        fwait(bar(B_S + (g & 1)), (g >> 1) & 1, bar0);
+        if (rloc == 0) PT(PT_SM_S, g);
+        if (!warp_dead && !PR_ABL_SM) {
+          tc_fence_after();
+          float2 l0 = make_float2(0.f, 0.f), l1 = l0;
+          const int nh = nu > 64 ? 2 : 1;
+#pragma unroll 1
+          for (int hf = 0; hf < nh; ++hf) {
+            const int c0 = 64 * hf;
+            tmem_ld32x(tS + c0, &r[0]);
+            if (nu > c0 + 32) tmem_ld32x(tS + c0 + 32, &r[32]);
+            tmem_wait_ld();
+            const bool partial = __any_sync(0xffffffffu, !(c_lo <= c0 && c_hi >= c0 + 64));
+            if (partial) {
+              const unsigned span = (unsigned)max(c_hi - c_lo, 0);
+              const int off = c0 - c_lo;
+#pragma unroll
+              for (int c = 0; c < 64; ++c) r[c] = ((unsigned)(off + c) < span) ? r[c] : 0xFF800000u;
+            }
+            float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 64; c += 8) {
+              mx0 = fmax3f(mx0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+              mx1 = fmax3f(mx1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+              mx2 = fmax3f(mx2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
+              mx3 = fmax3f(mx3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
+            }
+            const float m_half = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+            // lazy rescale (2^8): O holds this item's sum only from tile 1 on (tile 0's PV
+            // overwrites it), and then PV(g-1) must have completed before O is touched
+            const bool upd = m_half > m + kRescaleThreshold;
+            const bool need_o = upd && (m != -INFINITY);
+            const float f = need_o ? ex2f(m - m_half) : 1.f;
+            if (upd) {
+              lsum2.x *= f; lsum2.y *= f;
+              l0.x *= f; l0.y *= f; l1.x *= f; l1.y *= f;
+              m = m_half;
+            }
+            if (__any_sync(0xffffffffu, need_o)) {
+              if (jj > 0) {
+                fwait(bar(B_VE + (g - 1) % VST), ((g - 1) / VST) & 1, bar0);
+                tc_fence_after();
+#pragma unroll 1
+                for (int ch = 0; ch < 4; ++ch) {
+                  uint32_t o[32];
+                  tmem_ld32(tO + ch * 32, o);
+                  tmem_wait_ld();
+#pragma unroll
+                  for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+                  tmem_st32(tO + ch * 32, o);
+                }
+              }
+              if (hf == 1) {   // half 0's P was exponentiated against the old max
+                uint32_t o[32];
+                tmem_ld32(tS, o);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) o[c] = pack_bf16(bf_lo(o[c]) * f, bf_hi(o[c]) * f);
+                tmem_st32(tS, o);
+              }
+              tmem_wait_st();
+            }
+            const float m_use = (m == -INFINITY) ? 0.f : m;
+            const float2 negm2 = make_float2(-m_use, -m_use);
+#pragma unroll
+            for (int c = 0; c < 64; c += 4) {
+              const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+              const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
+              const float2 p0 = make_float2(ex2f(x0.x), ex2f(x0.y));
+              const float2 p1 = make_float2(ex2f(x1.x), ex2f(x1.y));
+              l0 = __fadd2_rn(l0, p0);
+              l1 = __fadd2_rn(l1, p1);
+              r[c >> 1] = pack_bf16(p0.x, p0.y);
+              r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
+            }
+            tmem_st32(tS + 32 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          }
+          lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
+          tmem_wait_st();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_cl(lbar(B_P + (g & 1)), 1);
+        if (rloc == 0) PT(PT_SM_P, g);
+      }
+      // the item's (l, m) for the epilogue warpgroup
+      if (kk >= 2) fwait(bar(B_LF + (kk & 1)), ((kk - 2) >> 1) & 1, bar0);
+      lbuf[(kk & 1) * 128 + rloc] = make_float2(lsum2.x + lsum2.y, m);
+      mbar_arrive(bar(B_LR + (kk & 1)));
+    }
+  } else if (warp < 8) {
+    // ================================================================ rotation + Q prep + epilogue
+    const int lt = threadIdx.x - 128;
+    const int c8 = lt & 7;             // frequencies 8*c8 .. 8*c8+7
+    const int rg = lt >> 3;            // key rows rg*4 .. rg*4+3 of this CTA's half
+    const float4* __restrict__ rp = p.rope_pairs;
+    float2 cth[4], sth[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 t = rp[32 + 4 * c8 + j];
+      cth[j] = make_float2(t.x, t.y);
+      sth[j] = make_float2(t.z, t.w);
+    }
+    auto prep_q = [&](int kq) {
+      const ItemRec rq = load_rec(recs, kq);
+      const AttnParams& pq = REC_PARAMS(rq);
+      const Item wq = item_of(pq, rq);
+      uint4 lo[8], hi[8];
+      if (lt == 0) PT(PT_Q_START, kq);
+      if (!PR_ABL_Q) load_rotate_q_regs(pq, wq, rank, lt, lo, hi);
+      if (kq >= NQB) fwait(bar(B_QF + (kq & 1)), ((kq - NQB) >> 1) & 1, bar0);
+      if (lt == 0) PT(PT_Q_FREE, kq);
+      const uint32_t qtile = qbuf_addr(kq);
+      const int rg8 = lt >> 3;
+#pragma unroll
+      for (int k = 0; k < 8 * (1 - PR_ABL_Q); ++k) {
+        const int r = rg8 * 8 + k;
+        const uint32_t a = qtile + r * 128 + ((c8 ^ (r & 7)) << 4);
+        sts128(a, lo[k]);
+        sts128(a + 16384, hi[k]);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) arrive_cl(lbar(B_QR + (kq & 1)), 1);
+      if (lt == 0) PT(PT_Q_END, kq);
+    };
+    auto epilogue = [&](int ke) {
+      const ItemRec rec = load_rec(recs, ke);
+      const AttnParams& p = REC_PARAMS(rec);
+      const Item w = item_of(p, rec);
+      fwait(bar(B_LR + (ke & 1)), (ke >> 1) & 1, bar0);
+      const float2 lm = lbuf[(ke & 1) * 128 + lt];
+      mbar_arrive(bar(B_LF + (ke & 1)));
+      fwait(bar(B_O + (ke & 1)), (ke >> 1) & 1, bar0);
+      if (lt == 0) PT(PT_EPI_O, ke);
+      tc_fence_after();
+      const int rglob = w.m0 + rank * 128 + lt;
+      const bool valid_row = rglob < w.rows_total;
+      const int qi = valid_row ? rglob / p.grp : 0;
+      const int h = valid_row ? w.g * p.grp + rglob % p.grp : 0;
+      const float lsum = lm.x;
+      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+      const bool part = p.n_splits > 1 || p.split_only >= 0;
+      const uint32_t tO = tmem + ((uint32_t)((lt >> 5) * 32) << 16) + (uint32_t)(256 + (ke & 1) * 128);
+      uint32_t r[64];
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        if (!PR_ABL_EPI) {
+          tmem_ld32x(tO + 64 * hf, &r[0]);
+          tmem_ld32x(tO + 64 * hf + 32, &r[32]);
+          tmem_wait_ld();
+        }
+        if (hf == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_cl(lbar(B_OF + (ke & 1)), 1);   // the O buffer may take item ke + 2
+        }
+        if (!valid_row || PR_ABL_EPI) continue;
+        if (part) {   // split-KV / context-parallel partial: fp32 O / l and log2-sum-exp per split
+          const long long orow = ((long long)w.pp * p.n_q + qi) * p.Hq + h;
+          const long long rows = (long long)p.P * p.n_q * p.Hq;
+          const long long slot = p.split_only >= 0 ? 0 : w.sp;
+          DSC_ASSERT(slot < max(p.n_splits, 1) && orow < rows, "attn_pair split partial row");
+          float4* dst = reinterpret_cast<float4*>(p.ws_o + (slot * rows + orow) * 128 + 64 * hf);
+#pragma unroll
+          for (int v = 0; v < 16; ++v)
+            dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv, __uint_as_float(r[4 * v + 1]) * inv,
+                                 __uint_as_float(r[4 * v + 2]) * inv, __uint_as_float(r[4 * v + 3]) * inv);
+          if (hf == 0) p.ws_lse[slot * rows + orow] = lsum > 0.f ? lm.y + __log2f(lsum) : -INFINITY;
+        } else {
+          uint32_t q[8];
+          const bool peers = p.n_peers > 0;
+          int oq = qi + p.o_rot;   // o_rot = 0 unless ring-ordered output (o_rows > 0)
+          if (p.o_rows > 0 && oq >= p.o_rows) oq -= p.o_rows;
+          const long long row = peers ? ((long long)w.pp * p.n_q + qi) * p.o_hq + p.o_head_off + h
+                                      : ((long long)w.pp * (p.o_rows > 0 ? p.o_rows : p.n_q) + oq) * p.Hq + h;
+          DSC_ASSERT(qi < p.n_q && w.pp < p.P && h < p.Hq && oq < (p.o_rows > 0 ? p.o_rows : p.n_q), "attn_pair O row");
+          const int nd = peers ? p.n_peers : 1;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              q[j] = pack_bf16(__uint_as_float(r[16 * v + 2 * j]) * inv, __uint_as_float(r[16 * v + 2 * j + 1]) * inv);
+#pragma unroll 1
+            for (int d = 0; d < nd; ++d)
+              stg256(reinterpret_cast<__nv_bfloat16*>(peers ? p.peer_o[d] : p.o) + row * 128 + 64 * hf + 16 * v, q);
+          }
+        }
+      }
+      if (lt == 0) PT(PT_EPI_END, ke);
+    };
+    // jobs of item kk: its raw K tiles rotated (this CTA's half; none for a staged build),
+    // item kk+1's Q tile after the first of them, then item kk-1's epilogue
+    int gt = 0;
+    if (n_my > 0) prep_q(0);
+    for (int kk = 0; kk < n_my; ++kk) {
+      const ItemRec rec = load_rec(recs, kk);
+      const AttnParams& p = REC_PARAMS(rec);
+      const Item w = item_of(p, rec);
+      const bool rot = !w.staged;
+      const int A = w.A;
+      const bool dbg = p.dbg_pos != nullptr && w.g == 0;   // every problem, kv head 0
+      int* const dbgp = dbg ? p.dbg_pos + (w.head_row / p.Hkv) * p.dbg_len : nullptr;
+      if (rot) {
+#pragma unroll 1
+        for (int jj = 0; jj < w.n_tiles; ++jj) {
+          const int g = gt + jj, u = w.t_begin + jj, ks = g % KST;
+          const TileSeg tg = tile_segments<BN>(p, w, u);
+          const int nh = width2(tg) >> 1;
+          int kpos[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int lr = rg * 4 + k;
+            kpos[k] = lr < nh ? seg_pos(tg, rank * nh + lr) : -1;
+          }
+          int p0 = -1;
+#pragma unroll
+          for (int k = 3; k >= 0; --k)
+            if (kpos[k] >= 0) p0 = kpos[k];
+          float4 pre[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) pre[j] = rp[(long long)max(p0, 0) * 32 + 4 * c8 + j];
+          fwait(bar(B_KR + ks), (g / KST) & 1, bar0);
+          if (rg * 4 < nh && !PR_ABL_ROT)   // rows >= nh are never read by the MMA
+            rotate_rows<1, kKHalf>(sbase + OFF_K + ks * kKBytes, rg * 4, c8, rp, cth, sth, kpos, pre, max(p0, 0));
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) arrive_cl(lbar(B_KF + ks), 1);
+          if (lt == 0) PT(PT_ROT, g);
+          if (dbg && c8 == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int rr = rank * nh + rg * 4 + k;
+              const int x = BN * u + rr;
+              int slot = tg.slot0 + rr;
+              if (slot >= p.R) slot -= p.R;
+              if (kpos[k] >= 0)
+                dbgp[(u < w.n_extra) ? (x < A ? x : p.dbg_A + p.dbg_R + (x - A)) : p.dbg_A + slot] = kpos[k];
+            }
+          }
+          if (jj == 0 && kk + 1 < n_my) prep_q(kk + 1);
+        }
+      } else if (kk + 1 < n_my) {
+        prep_q(kk + 1);
+      }
+      if (kk >= 1) epilogue(kk - 1);
+      gt += w.n_tiles;
+    }
+    if (n_my > 0) epilogue(n_my - 1);
+  } else if (warp == 8 || warp == 9) {
+    // ================================================================ copy warps (8: K half, 9: V columns)
+    const bool isk = warp == 8;
+    int gt = 0;
+    for (int kk = 0; kk < n_my; ++kk) {
+      const ItemRec rec = load_rec(recs, kk);
+      const AttnParams& p = REC_PARAMS(rec);
+      const Item w = item_of(p, rec);
+      const int A = p.A;
+      const __nv_bfloat16* __restrict__ SX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.sink_k : p.sink_v);
+      const __nv_bfloat16* __restrict__ XX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.self_k : p.self_v);
+#pragma unroll 1
+      for (int jj = 0; jj < w.n_tiles; ++jj) {
+        const int g = gt + jj, u = w.t_begin + jj;
+        const int nst = isk ? KST : VST, st = g % nst;
+        if (g >= nst) fwait(bar((isk ? B_KE : B_VE) + st), ((g - nst) / nst) & 1, bar0);
+        const uint32_t full = bar((isk ? B_KR : B_VL) + st);
+        const uint32_t dst = sbase + (isk ? OFF_K + st * kKBytes : OFF_V + st * kVBytes);
+        const TileSeg t = tile_segments<BN>(p, w, u);
+        const int nu = width2(t), nh = nu >> 1;
+        if (u < w.n_extra) {
+          // sink rows (x < A) + self rows (A <= x < A + n_self), zeros up to the pair width
+          const int nrows = isk ? nh : nu;
+          const int cpr = isk ? 16 : 8;          // 16-byte chunks per row this CTA loads
+          const int key0 = isk ? rank * nh : 0;
+          const int col0 = isk ? 0 : 64 * rank;
+#pragma unroll 1
+          for (int id = lane; id < nrows * cpr; id += 32) {
+            const int rr = id / cpr, ch = id % cpr;
+            const int x = BN * u + key0 + rr;
+            const __nv_bfloat16* src = nullptr;
+            if (x < A) src = SX + ((long long)w.head_row * A + x) * 128;
+            else if (x < A + w.n_self) src = XX + (((long long)w.pp * w.n_self + (x - A)) * p.Hkv + w.g) * 128;
+            DSC_ASSERT(w.head_row < (long long)p.S * p.N_total * p.Hkv && w.pp < p.P, "attn_pair sink/self row");
+            const uint32_t d = isk ? dst + (ch >> 3) * kKHalf + rr * 128 + (((ch & 7) ^ (rr & 7)) << 4)
+                                   : dst + rr * 128 + ((ch ^ (rr & 7)) << 4);
+            cp_async16(d, src ? (const void*)(src + col0 + 8 * ch) : (const void*)SX, src ? 16u : 0u);
+          }
+          cp_async_wait_all();
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(full);
+        } else if (lane == 0) {
+          const int row = (int)(w.head_row * w.Rp) + t.slot0;
+          DSC_ASSERT(t.slot0 >= 0 && t.slot0 < w.Rp && (w.staged || t.slot0 + BN <= w.Rp) &&
+                         w.head_row < (long long)p.S * p.N_total * p.Hkv,
+                     "attn_pair TMA box rows");
+          PT(isk ? PT_CPK : PT_CPV, g);
+          if (isk) {
+            mbar_arrive_tx(full, kKBytes);
+            tma_load_2d(dst, &p.tmap_k64, 0, row + rank * nh, full);
+            tma_load_2d(dst + kKHalf, &p.tmap_k64, 64, row + rank * nh, full);
+          } else {
+            mbar_arrive_tx(full, kVBytes);
+            tma_load_2d(dst, &p.tmap_v, 64 * rank, row, full);
+          }
+        }
+        __syncwarp();
+      }
+      gt += w.n_tiles;
+    }
+  } else if (warp == 11) {
+    // ================================================================ forwarder
+    if (lane == 0) {
+      int gt = 0;
+      for (int kk = 0; kk < n_my; ++kk) {
+        const ItemRec rec = load_rec(recs, kk);
+        const bool staged = REC_PARAMS(rec).staged;
+        const int n = rec.n_tiles;
+#pragma unroll 1
+        for (int jj = 0; jj < n; ++jj) {
+          const int g = gt + jj;
+          if (staged) {   // pre-rotated K: landed = ready
+            fwait(bar(B_KR + g % KST), (g / KST) & 1, bar0);
+            arrive_cl(lbar(B_KF + g % KST), 4);
+            PT(PT_KR_FW, g);
+          }
+          fwait(bar(B_VL + g % VST), (g / VST) & 1, bar0);
+          arrive_cl(lbar(B_VR + g % VST), 1);
+          PT(PT_FWV, g);
+        }
+        gt += n;
+      }
+    }
+  } else if (warp == 10 && rank == 0) {
+    // ================================================================ MMA issuer (leader)
+    constexpr uint32_t IQK0 = idesc_bf16(256, 0, 0, 0);    // S = Q K^T, both K-major; N = pair width
+    constexpr uint32_t IPV = idesc_bf16(256, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
+    struct MI {
+      int n, t_begin, n_extra, aps, cnt;
+    };
+    auto mi_of = [&](int kk) {
+      const ItemRec r = load_rec(recs, kk);
+      const bool isb = r.flags & 1;
+      const int A = isb ? pb.A : pa.A, n_self = isb ? pb.n_self : pa.n_self;
+      MI m;
+      m.n = r.n_tiles; m.t_begin = r.t_begin;
+      m.n_extra = (A + n_self + BN - 1) / BN; m.aps = A + n_self; m.cnt = r.cnt;
+      return m;
+    };
+    auto width_of = [&](const MI& m, int jj) {   // tile_segments' valid keys, rounded up to 32
+      const int u = m.t_begin + jj;
+      const int valid = u < m.n_extra ? min(max(m.aps - BN * u, 0), BN) : min(m.cnt - BN * (u - m.n_extra), BN);
+      return (valid + 31) & ~31;
+    };
+    auto issue_s = [&](const MI& m, int k, int jj, int g) {
+      const int ks = g % KST, qb = k & 1;
+      if (jj == 0) cwait(bar(B_QR + qb), (k >> 1) & 1, bar0);
+      if (jj == 0 && lane == 0) PT(PT_QR_OK, k);
+      cwait(bar(B_KF + ks), (g / KST) & 1, bar0);
+      if (lane == 0) PT(PT_KF_OK, g);
+      tc_fence_after();
+      const int nu = width_of(m, jj);
+      const uint64_t da = sdesc(qbuf_addr(k), 16, 1024);
+      const uint64_t db = sdesc(sbase + OFF_K + ks * kKBytes, 16, 1024);
+      mma2_qk(tmem + (uint32_t)((g & 1) * 128), da, db, IQK0 | ((uint32_t)(nu >> 3) << 17));
+      commit2_w(bar(B_S + (g & 1)));
+      commit2_w(bar(B_KE + ks));
+      if (jj + 1 == m.n) commit2_w(bar(B_QF + qb));
+      if (lane == 0) PT(PT_S_ISS, g);
+      if (jj == 0 && lane == 0) PT(PT_ITEM, k);
+    };
+    auto issue_pv = [&](const MI& m, int k, int jj, int g) {
+      const int vs = g % VST;
+      cwait(bar(B_VR + vs), (g / VST) & 1, bar0);
+      if (lane == 0) PT(PT_VR_OK, g);
+      cwait(bar(B_P + (g & 1)), (g >> 1) & 1, bar0);
+      if (lane == 0) PT(PT_P_OK, g);
+      if (jj == 0 && k >= 2) cwait(bar(B_OF + (k & 1)), ((k - 2) >> 1) & 1, bar0);
+      if (jj == 0 && lane == 0) PT(PT_OF_OK, k);
+      tc_fence_after();
+      const int nu = width_of(m, jj);
+      const uint64_t dv = sdesc(sbase + OFF_V + vs * kVBytes, 16, 1024);
+      const uint32_t d = tmem + (uint32_t)(256 + (k & 1) * 128), a = tmem + (uint32_t)((g & 1) * 128);
+      const uint32_t acc = jj > 0 ? 1u : 0u;
+      if (nu == BN) {
+        mma2_pv8(d, a, dv, IPV, acc);
+      } else {
+        mma2_pv1(d, a, dv, IPV, acc);
+#pragma unroll 1
+        for (int k8 = 1; k8 < (nu >> 4); ++k8) mma2_pv1(d, a + k8 * 8, dv + (uint64_t)(k8 * 128), IPV, 1u);
+      }
+      commit2_w(bar(B_VE + vs));
+      if (jj + 1 == m.n) commit2_w(bar(B_O + (k & 1)));
+      if (lane == 0) PT(PT_PV_ISS, g);
+    };
+    // one issue stream across items, S one tile ahead of PV: S(g+1), then PV(g)
+    int gt = 0;
+    if (n_my > 0) {
+      MI cur = mi_of(0);
+      issue_s(cur, 0, 0, 0);
+      for (int kk = 0; kk < n_my; ++kk) {
+        const bool has_next = kk + 1 < n_my;
+        const MI nxt = has_next ? mi_of(kk + 1) : cur;
+        for (int jj = 0; jj < cur.n; ++jj) {
+          const int g = gt + jj;
+          if (jj + 1 < cur.n) issue_s(cur, kk, jj + 1, g + 1);
+          else if (has_next) issue_s(nxt, kk + 1, 0, g + 1);
+          issue_pv(cur, kk, jj, g);
+        }
+        gt += cur.n;
+        cur = nxt;
+      }
+      fwait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1, bar0);
+      if (lane == 0) PT(PT_END, 0);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 10) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+#undef REC_PARAMS
+}
+
+}  // namespace pr
+
 int attn_fa_smem_bytes() { return fa::kSmemBytes; }
 
 namespace {
@@ -957,6 +1685,8 @@ cudaError_t configure_device(int* num_sms) {
   std::lock_guard<std::mutex> lock(g_cfg_mu);
   if (dev < 64 && (g_cfg_done >> dev) & 1) { *num_sms = g_num_sms[dev]; return cudaSuccess; }
   e = cudaFuncSetAttribute(fa::attn_fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(pr::attn_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pr::kSmemBytes);
   if (e != cudaSuccess) return e;
   int sms = 0;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1016,6 +1746,15 @@ int fa_watchdog_read(unsigned long long* out, int n) {
   return 0;
 }
 
+// DSC_FA=8 selects the CTA-pair kernel (v8), default: the single-CTA v7 kernel
+static bool pair_kernel_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("DSC_FA");
+    return e && e[0] == '8';
+  }();
+  return on;
+}
+
 cudaError_t launch_attn_fa(const AttnParams& pa, const AttnParams* pb, SchedCache* cache, cudaStream_t st) {
   int num_sms = 0;
   cudaError_t e = configure_device(&num_sms);
@@ -1025,6 +1764,18 @@ cudaError_t launch_attn_fa(const AttnParams& pa, const AttnParams* pb, SchedCach
   const long long na = attn_fa_items(pa), nb = pb ? attn_fa_items(*pb) : 0;
   const long long items = na + nb;
   if (items == 0) return cudaSuccess;
+  if (pair_kernel_on() && (!pa.trace || PR_TRACE)) {
+    // v8: one item per CTA pair, num_sms / 2 clusters
+    const long long ncl_max = num_sms / 2;
+    const unsigned ncl = (unsigned)(items < ncl_max ? items : ncl_max);
+    AttnParams qa = pa;
+    const int* off = nullptr;
+    qa.item_recs = item_table(cache, pa, pb, na, nb, ncl, &attn_fa_decode, &off, st);
+    qa.item_off = off;
+    if (!qa.item_recs) return cudaErrorMemoryAllocation;
+    pr::attn_pair_kernel<<<2 * ncl, pr::kThreads, pr::kSmemBytes, st>>>(qa, pb ? *pb : qa, (int)na, (int)nb);
+    return cudaGetLastError();
+  }
   const unsigned grid = (unsigned)(items < num_sms ? items : num_sms);
   AttnParams qa = pa;
   const int* off = nullptr;

@@ -82,7 +82,7 @@ struct dscache_s {
   void* bstage_k = nullptr;  // staged boosted build: sink ++ older instant ++ boosted frame (grown on demand)
   void* bstage_v = nullptr;
   int bstage_rows = 0;
-  CUtensorMap tmap_bk{}, tmap_bv{};
+  CUtensorMap tmap_bk{}, tmap_bv{}, tmap_bk64{};
   std::vector<int64_t> frames;
   std::vector<int> sink_filled;
   std::vector<int64_t> last_evicted;
@@ -100,12 +100,12 @@ struct dscache_s {
   int impl_build = DSCACHE_IMPL_SIMT, impl_attend = DSCACHE_IMPL_SIMT;
   int num_sms = 148;
   dsc::SchedCache* sched = nullptr;   // per-CTA item tables of the tcgen05 kernel, owned by the handle
-  CUtensorMap tmap_k{}, tmap_v{};
+  CUtensorMap tmap_k{}, tmap_v{}, tmap_k64{};
   // staged build (tcgen05): per-step copy of sink ++ instant window, K pre-rotated
   void* stage_k = nullptr;
   void* stage_v = nullptr;
   int stage_rows = 0;          // A + C
-  CUtensorMap tmap_sk{}, tmap_sv{};
+  CUtensorMap tmap_sk{}, tmap_sv{}, tmap_sk64{};
   // profiling
   int prof = 0;
   struct Ev { cudaEvent_t a, b; int kind; };
@@ -177,7 +177,7 @@ void fill_common(dscache_t h, dsc::AttnParams& p, int lb, int lc) {
   p.dbg_M = std::max(h->C, c.max_query_tokens);
   p.dbg_A = c.sink_tokens; p.dbg_R = h->R;
   p.dbg_len = c.sink_tokens + h->R + 2 * p.dbg_M;
-  p.tmap_k = h->tmap_k; p.tmap_v = h->tmap_v;
+  p.tmap_k = h->tmap_k; p.tmap_v = h->tmap_v; p.tmap_k64 = h->tmap_k64;
   p.staged = 0;
   p.trace = h->trace; p.ntrace_cta = h->ntrace;
   p.n_splits = 1; p.tiles_per_split = 1 << 30; p.split_only = -1;
@@ -326,6 +326,7 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
   if (e == cudaSuccess && (h->impl_build == DSCACHE_IMPL_TC || h->impl_attend == DSCACHE_IMPL_TC)) {
     const unsigned long long rows = (unsigned long long)heads * h->Rp;
     e = dsc::make_kv_tmap(&h->tmap_k, h->ring_k, rows, dsc::kTileN);
+    if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_k64, h->ring_k, rows, dsc::kTileN / 2);
     if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_v, h->ring_v, rows, dsc::kTileN);
   }
   if (e == cudaSuccess && h->impl_build == DSCACHE_IMPL_TC && h->C > 0) {
@@ -335,6 +336,8 @@ dscache_status dscache_create(const dscache_config* cfg, dscache_t* out) {
     e = cudaMemset(h->stage_k, 0, sb);
     if (e == cudaSuccess) e = cudaMemset(h->stage_v, 0, sb);
     if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_sk, h->stage_k, (unsigned long long)heads * h->stage_rows, dsc::kTileN);
+    if (e == cudaSuccess)
+      e = dsc::make_kv_tmap(&h->tmap_sk64, h->stage_k, (unsigned long long)heads * h->stage_rows, dsc::kTileN / 2);
     if (e == cudaSuccess) e = dsc::make_kv_tmap(&h->tmap_sv, h->stage_v, (unsigned long long)heads * h->stage_rows, dsc::kTileN);
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -440,7 +443,7 @@ dscache_status prep_build(dscache_t h, int32_t lb, int32_t lc, const void* q_ins
     *stage = sp;
     p.staged = 1;
     p.A = 0; p.ring_start = 0; p.ring_count = sp.rows; p.R = h->stage_rows; p.Rp = h->stage_rows;
-    p.tmap_k = h->tmap_sk; p.tmap_v = h->tmap_sv;
+    p.tmap_k = h->tmap_sk; p.tmap_v = h->tmap_sv; p.tmap_k64 = h->tmap_sk64;
   }
   return DSCACHE_OK;
 }
@@ -780,6 +783,7 @@ dscache_status build_with_inst(dscache_t h, int32_t lb, int32_t lc, const void* 
         return fail(DSCACHE_E_OOM, "instant staging allocation failed");
       }
       DSC_CUDA(dsc::make_kv_tmap(&h->tmap_bk, h->bstage_k, (unsigned long long)heads * rows, dsc::kTileN));
+      DSC_CUDA(dsc::make_kv_tmap(&h->tmap_bk64, h->bstage_k, (unsigned long long)heads * rows, dsc::kTileN / 2));
       DSC_CUDA(dsc::make_kv_tmap(&h->tmap_bv, h->bstage_v, (unsigned long long)heads * rows, dsc::kTileN));
       h->bstage_rows = rows;
     }
@@ -795,7 +799,7 @@ dscache_status build_with_inst(dscache_t h, int32_t lb, int32_t lc, const void* 
     p.staged = 1;
     p.A = 0; p.ring_start = 0; p.ring_count = rows; p.R = h->bstage_rows; p.Rp = h->bstage_rows;
     p.self_k = p.self_v = nullptr; p.n_self = 0;
-    p.tmap_k = h->tmap_bk; p.tmap_v = h->tmap_bv;
+    p.tmap_k = h->tmap_bk; p.tmap_v = h->tmap_bv; p.tmap_k64 = h->tmap_bk64;
   }
   return run_attention(h, p, h->impl_build, 0, st);
 }

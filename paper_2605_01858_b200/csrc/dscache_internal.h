@@ -108,6 +108,8 @@ struct AttnParams {
   // TMA descriptors of the K / V rings viewed as [S*N*Hkv*Rp rows][128] bf16, box 64 x kTileN, SW128
   CUtensorMap tmap_k;
   CUtensorMap tmap_v;
+  // the pair kernel's K half-tiles: the same K rows, box 64 columns x 64 rows
+  CUtensorMap tmap_k64;
 };
 
 // Memory-bound decode: n_q * grp <= 16 query rows of one

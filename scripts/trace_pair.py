@@ -1,0 +1,115 @@
+"""Event timeline of the v8 pair kernel (attn_fa.cu namespace pr, PR_TRACE=1 variant) on one
+steady-state fused step (dscache_step) of a BASELINE config.
+
+    python scripts/trace_pair.py [--config c5] [--lib PATH] [--items 8] [--first-item 0]
+
+Leader CTA (0): per tile the MMA warp's issue times of S(g) and PV(g), when its waits were
+satisfied (K ready, V ready, P ready), and the leader's own softmax S -> P span; per item the
+Q-ready / O-free waits and the rotation warpgroup's Q prep and epilogue spans.  clock64 is
+per SM, so only events of one CTA are compared.
+"""
+import argparse
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2605_01858_b200 import _build as _B  # noqa: E402
+from paper_2605_01858_b200 import dscache as _D  # noqa: E402
+
+NE, NI = 32, 1024
+EV = dict(S_ISS=0, PV_ISS=1, KF_OK=2, VR_OK=3, P_OK=4, SM_S=5, SM_P=6, CPK=7, CPV=8, FWV=9, ROT=10,
+          ITEM=12, Q_START=13, Q_FREE=14, Q_END=15, EPI_O=16, EPI_END=17, QR_OK=18, OF_OK=19, END=20, KR_FW=21)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--lib", default=None)
+    ap.add_argument("--items", type=int, default=8)
+    ap.add_argument("--first-item", type=int, default=0)
+    ap.add_argument("--tiles", type=int, default=6)
+    args = ap.parse_args()
+    lib = args.lib or _B.build_variant("ptrace", ["PR_TRACE=1"])
+    _D.load_library(lib)
+    import dscache_synth as synth
+    from paper_2605_01858_b200 import dscache as D
+    cfg = synth.CONFIGS[args.config]
+    dev = torch.device("cuda", 0)
+    h = D.DSCache.from_config(cfg)
+    S, N, A, tpf, Hkv, Hq, d = (cfg.num_streams, cfg.num_layers, cfg.sink_tokens, cfg.tokens_per_frame,
+                                cfg.num_kv_heads, cfg.num_q_heads, cfg.head_dim)
+    g = torch.Generator(device=dev).manual_seed(0)
+
+    def r(*s):
+        return (torch.randn(s, device=dev, generator=g) * cfg.scale).to(torch.bfloat16)
+    h.append_frame(r(S, N, A, Hkv, d), r(S, N, A, Hkv, d))
+    for _ in range(cfg.instant_frames + cfg.past_frames - 1):
+        h.append_frame(r(S, N, tpf, Hkv, d), r(S, N, tpf, Hkv, d))
+    C, q = cfg.C, cfg.query_tokens
+    k, v = r(S, N, tpf, Hkv, d), r(S, N, tpf, Hkv, d)
+    qi, qq, kk, vv = r(S, N, C, Hq, d), r(S, N, q, Hq, d), r(S, N, q, Hkv, d), r(S, N, q, Hkv, d)
+    for _ in range(3):
+        h.step(k, v, qi, qq, kk, vv)
+    torch.cuda.synchronize()
+    nct = 2
+    buf = torch.zeros(nct * NE * NI, dtype=torch.int64, device=dev)
+    h.set_trace(buf, nct)
+    h.step(k, v, qi, qq, kk, vv)
+    torch.cuda.synchronize()
+    h.set_trace(None)
+    tr = buf.view(nct, NE, NI).cpu()
+    t = tr[0]
+    t0 = int(t[EV["ITEM"], 0])
+
+    def ev(e, i, tt=t, base=t0):
+        x = int(tt[EV[e], i])
+        return x - base if x else None
+    n_items = int((t[EV["ITEM"]] > 0).sum())
+    n_tiles = int((t[EV["PV_ISS"]] > 0).sum())
+    end = ev("END", 0)
+    print(f"=== leader CTA 0: {n_items} items, {n_tiles} tiles, end {end} clk, {end / max(n_tiles, 1):.0f} clk per tile")
+    # item boundaries in global tiles (S issue order: an item's first S follows PV of the previous)
+    item_start_clk = [ev("ITEM", i) for i in range(n_items)]
+    s_iss = [ev("S_ISS", gg) for gg in range(n_tiles)]
+    bounds = []
+    gi = 0
+    for i in range(n_items):
+        while gi < n_tiles and (s_iss[gi] is None or s_iss[gi] < item_start_clk[i]):
+            gi += 1
+        bounds.append(gi)
+    bounds.append(n_tiles)
+    for i in range(args.first_item, min(n_items, args.first_item + args.items)):
+        g0, g1 = bounds[i], bounds[i + 1]
+        span = (ev("ITEM", i + 1) if i + 1 < n_items else end) - ev("ITEM", i)
+        print(f"item {i}: tiles {g0}..{g1 - 1} ({g1 - g0}), span {span} clk ({span / max(g1 - g0, 1):.0f}/tile)  "
+              f"QR_ok {ev('QR_OK', i)} OF_ok {ev('OF_OK', i)} | Qprep [{ev('Q_START', i)}, free {ev('Q_FREE', i)}, "
+              f"end {ev('Q_END', i)}] epi [O {ev('EPI_O', i)}, end {ev('EPI_END', i)}]")
+        for gg in range(g0, min(g1, g0 + args.tiles)):
+            f = {e: ev(e, gg) for e in ("S_ISS", "PV_ISS", "KF_OK", "VR_OK", "P_OK", "SM_S", "SM_P", "CPK", "CPV", "FWV", "ROT", "KR_FW")}
+            print("   g%-4d " % gg + " ".join(f"{k}={v}" for k, v in f.items()))
+    # steady-state period statistics over all tiles
+    import statistics as st
+
+    def dif(a, b):
+        out = []
+        for gg in range(n_tiles):
+            x, y = ev(a, gg), ev(b, gg)
+            if x is not None and y is not None:
+                out.append(x - y)
+        return out
+    for name, a, b in [("S issue -> softmax sees S", "SM_S", "S_ISS"), ("softmax S -> P", "SM_P", "SM_S"),
+                       ("softmax P -> MMA P ok", "P_OK", "SM_P"), ("P ok -> PV issued", "PV_ISS", "P_OK"),
+                       ("V TMA -> fwd", "FWV", "CPV"), ("K TMA -> fwd", "KR_FW", "CPK")]:
+        d_ = dif(a, b)
+        if d_:
+            print(f"{name:28s}: median {st.median(d_):7.0f}  p90 {sorted(d_)[int(0.9 * len(d_))]:7.0f}  n {len(d_)}")
+    per = [s_iss[gg + 1] - s_iss[gg] for gg in range(n_tiles - 1) if s_iss[gg] is not None and s_iss[gg + 1] is not None]
+    if per:
+        print(f"S issue period: median {st.median(per):.0f}")
+
+
+if __name__ == "__main__":
+    main()

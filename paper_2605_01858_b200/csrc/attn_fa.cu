@@ -952,15 +952,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 // its V rows for PV (scripts/micro/pair_mma_test.cu checks these layouts and the full
 // 8190 flop/clk/SM rate of the pair MMA).  Per SM that halves the K rotation, the Q prep,
 // the O epilogue and the shared-memory operand traffic of a tile, and it frees TMEM:
-//   S[2] = cols 0..255 (double-buffered: S(g+1) is computed while the softmax works on S(g)),
-//   O[2] = cols 256..511 (double-buffered by item: an item's epilogue overlaps the next item).
+//   S[3] = cols 0..383: S is issued two tiles ahead of PV (S(g+2), then PV(g)), so the
+//          softmax finds S(g+1) done when it finishes S(g);
+//   O    = cols 384..511, read out by the epilogue as soon as its item's last PV is done.
 // The leader CTA (rank 0) issues every MMA; its waits gather arrivals from both CTAs
 // (remote mbarrier arrives), its commits are multicast to both.
-//   warps 0-3  softmax of this CTA's 128 rows (thread = row = TMEM lane), (l, m) per item
-//   warps 4-7  K rotation of this CTA's key half, the Q tile prep one item ahead, the epilogue
-//   warp 8     K copy (TMA 64 x 64 boxes / cp.async sink+self rows), warp 9 V copy
-//   warp 10    TMEM allocation; MMA issuer (leader)
-//   warp 11    forwarder: locally landed V (and pre-rotated staged K) -> the leader's barriers
+//   warps 0-7  softmax: warps w and w + 4 share the 32 rows of TMEM lane quarter w % 4, warp
+//              w < 4 owns score columns 0..63, w >= 4 columns 64..127; the row max is
+//              exchanged through shared memory once per tile (then P needs no re-scaling)
+//   warps 8-11 K rotation of this CTA's key half, the Q tile prep one item ahead, the epilogue
+//   warp 12    K copy (TMA 64 x 64 boxes / cp.async sink+self rows), warp 13 V copy
+//   warp 14    TMEM allocation; MMA issuer (leader)
+//   warp 15    forwarder: locally landed V (and pre-rotated staged K) -> the leader's barriers
 namespace pr {
 using namespace tcc;
 using fa::fwait;
@@ -971,7 +974,7 @@ using fa::item_of;
 using fa::load_rec;
 
 constexpr int BN = kTileN;
-constexpr int kWarps = 12;
+constexpr int kWarps = 16;
 constexpr int kThreads = kWarps * 32;
 constexpr int kQBytes = 128 * 128 * 2;    // this CTA's Q tile: two 64-column SW128 blocks of 128 rows
 constexpr int kKHalf = 64 * 128;          // one 64-column SW128 block of this CTA's <= 64 keys (8 KB)
@@ -982,6 +985,7 @@ constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + NQB * kQBytes;
 constexpr int OFF_V = OFF_K + KST * kKBytes;
 constexpr int OFF_BAR = OFF_V + VST * kVBytes;
+constexpr int NSB = 3;                    // S buffers in TMEM
 enum {
   B_QR = 0,             // [2] Q buffer ready (leader: 4 warps x 2 CTAs)
   B_QF = B_QR + 2,      // [2] Q buffer free (commit after its item's last QK^T)
@@ -991,16 +995,17 @@ enum {
   B_VL = B_KE + KST,    // [VST] V landed in this CTA
   B_VR = B_VL + VST,    // [VST] V ready (leader: 2 forwarders)
   B_VE = B_VR + VST,    // [VST] V stage free = PV done (commit)
-  B_S = B_VE + VST,     // [2] S buffer ready (commit)
-  B_P = B_S + 2,        // [2] P ready (leader: 8)
-  B_O = B_P + 2,        // [2] O buffer final for its item (commit)
-  B_OF = B_O + 2,       // [2] O buffer read out (leader: 8)
-  B_LR = B_OF + 2,      // [2] (l, m) of an item's rows written (128 softmax threads)
+  B_S = B_VE + VST,     // [NSB] S buffer ready (commit)
+  B_P = B_S + NSB,      // [NSB] P ready (leader: 8 softmax warps x 2 CTAs)
+  B_O = B_P + NSB,      // O final for its item (commit)
+  B_OF = B_O + 1,       // O read out (leader: 4 warps x 2 CTAs)
+  B_LR = B_OF + 1,      // [2] (l, m) of an item's rows written (256 softmax threads)
   B_LF = B_LR + 2,      // [2] ... read by the epilogue (128)
   B_N = B_LF + 2
 };
-constexpr int OFF_L = OFF_BAR + B_N * 8 + 8;                  // (l, m) handoff [2][128] float2
-constexpr int kSmemBytes = OFF_L + 2 * 128 * 8 + 1024;
+constexpr int OFF_L = OFF_BAR + B_N * 8 + 8;                  // (l, m) handoff [2 items][2 halves][128] float2
+constexpr int OFF_X = OFF_L + 2 * 2 * 128 * 8;                // row max exchange [2 tiles][2 halves][128] float
+constexpr int kSmemBytes = OFF_X + 2 * 2 * 128 * 4 + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 constexpr float kRescaleThreshold = 8.0f;
 // ablation knobs (timing experiments only; results are wrong when set)
@@ -1026,7 +1031,7 @@ constexpr int kPtEvents = 32, kPtIdx = 1024;
 enum {
   PT_S_ISS = 0, PT_PV_ISS, PT_KF_OK, PT_VR_OK, PT_P_OK, PT_SM_S, PT_SM_P, PT_CPK, PT_CPV, PT_FWV, PT_ROT,   // per tile
   PT_ITEM = 12, PT_Q_START, PT_Q_FREE, PT_Q_END, PT_EPI_O, PT_EPI_END, PT_QR_OK, PT_OF_OK, PT_END,           // per item
-  PT_KR_FW = 21
+  PT_KR_FW = 21, PT_S_MMA = 22, PT_PV_MMA = 23, PT_S_FENCE = 24, PT_ROT_PRE = 25, PT_ROT_KR = 26, PT_ROT_RR = 27   // per tile
 };
 #if PR_TRACE
 #define PT(ev, i)                                                                                      \
@@ -1059,6 +1064,16 @@ __device__ __forceinline__ bool mbar_try_cl(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred P1;\n"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  return ok != 0;
+}
+// non-blocking phase test (try_wait may suspend the thread until the phase completes)
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
       "selp.u32 %0, 1, 0, P1;\n}\n"
       : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
   return ok != 0;
@@ -1136,6 +1151,9 @@ __device__ __forceinline__ void mma2_pv1(uint32_t d_tmem, uint32_t a_tmem, uint6
 // the pair's tile width: valid keys rounded up to 32, so each CTA's half is a multiple of 16
 __device__ __forceinline__ int width2(const TileSeg& t) { return (t.width + 31) & ~31; }
 
+constexpr int kRegSoftmax = 136, kRegAux = 168, kRegMisc = 72;   // setmaxnreg: 2 x 136 + 168 + 72 = 512
+static_assert(2 * kRegSoftmax + kRegAux + kRegMisc <= 512, "register budget");
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_pair_kernel(const __grid_constant__ AttnParams pa, const __grid_constant__ AttnParams pb, int na, int nb) {
   const AttnParams& p = pa;   // launch-wide fields (rope table) are shared
@@ -1152,6 +1170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   auto lbar = [&](int i) { return lbar0 + 8u * (uint32_t)i; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + B_N * 8);
   float2* lbuf = reinterpret_cast<float2*>(smem + OFF_L);
+  float* xbuf = reinterpret_cast<float*>(smem + OFF_X);
   const int rank = (int)cta_rank();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #define REC_PARAMS(R) (((R).flags & 1) ? pb : pa)
@@ -1160,13 +1179,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(B_QR + i), 8);
       mbar_init(bar(B_QF + i), 1);
-      mbar_init(bar(B_S + i), 1);
-      mbar_init(bar(B_P + i), 8);
-      mbar_init(bar(B_O + i), 1);
-      mbar_init(bar(B_OF + i), 8);
-      mbar_init(bar(B_LR + i), 128);
+      mbar_init(bar(B_LR + i), 256);
       mbar_init(bar(B_LF + i), 128);
     }
+    for (int i = 0; i < NSB; ++i) {
+      mbar_init(bar(B_S + i), 1);
+      mbar_init(bar(B_P + i), 16);
+    }
+    mbar_init(bar(B_O), 1);
+    mbar_init(bar(B_OF), 8);
     for (int i = 0; i < KST; ++i) {
       mbar_init(bar(B_KR + i), 1);
       mbar_init(bar(B_KF + i), 8);
@@ -1180,12 +1201,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
   }
-  if (warp == 10) {
+  if (warp == 14) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
-  if (warp == 8 && lane == 0) {
+  if (warp == 12 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pa.tmap_k64)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pa.tmap_v)) : "memory");
     if (nb > 0) {
@@ -1204,11 +1225,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const ItemRec* __restrict__ recs = pa.item_recs + pa.item_off[cl];
   const int n_my = pa.item_off[cl + 1] - pa.item_off[cl];
   auto qbuf_addr = [&](int k) { return sbase + OFF_Q + (uint32_t)((k & 1) * kQBytes); };
+  const uint32_t tO_base = tmem + (uint32_t)(NSB * 128);
 
-  if (warp < 4) {
-    // ================================================================ softmax
-    const int rloc = warp * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  if (warp < 8) {
+    // ================================================================ softmax (64 columns per thread)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
+    const int quarter = warp & 3, hc = warp >> 2;    // lane quarter, column half
+    const int rloc = quarter * 32 + lane;
+    const int c0 = 64 * hc;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tO = tO_base + lane_off + (uint32_t)c0;
     const float sl2 = p.scale_log2;
     const float2 scale2 = make_float2(sl2, sl2);
     int g = 0;
@@ -1222,8 +1248,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const bool valid_row = rglob < w.rows_total;
       const int qi = valid_row ? rglob / p.grp : 0;
       const int lim = valid_row ? p.q_pos0 + qi : -1;
-      const bool warp_dead = __all_sync(0xffffffffu, !valid_row);
-      const uint32_t tO = tmem + lane_off + (uint32_t)(256 + (kk & 1) * 128);
+      const bool warp_dead = __all_sync(0xffffffffu, !valid_row);   // same for both halves of a quarter
       float m = -INFINITY;
       float2 lsum2 = make_float2(0.f, 0.f);
       uint32_t r[64];
@@ -1241,100 +1266,92 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           c_lo = t.lo0;
           c_hi = max(c_lo, min(t.hi0, lim - t.pos0_0 + 1));
         }
-        const uint32_t tS = tmem + lane_off + (uint32_t)((g & 1) * 128);
-        fwait(bar(B_S + (g & 1)), (g >> 1) & 1, bar0);
-        if (rloc == 0) PT(PT_SM_S, g);
+        const int sb = g % NSB;
+        const uint32_t tS = tmem + lane_off + (uint32_t)(sb * 128);
+        fwait(bar(B_S + sb), (g / NSB) & 1, bar0);
+        if (rloc == 0 && hc == 0) PT(PT_SM_S, g);
         if (!warp_dead && !PR_ABL_SM) {
           tc_fence_after();
-          float2 l0 = make_float2(0.f, 0.f), l1 = l0;
-          const int nh = nu > 64 ? 2 : 1;
-#pragma unroll 1
-          for (int hf = 0; hf < nh; ++hf) {
-            const int c0 = 64 * hf;
-            tmem_ld32x(tS + c0, &r[0]);
-            if (nu > c0 + 32) tmem_ld32x(tS + c0 + 32, &r[32]);
-            tmem_wait_ld();
-            const bool partial = __any_sync(0xffffffffu, !(c_lo <= c0 && c_hi >= c0 + 64));
-            if (partial) {
-              const unsigned span = (unsigned)max(c_hi - c_lo, 0);
-              const int off = c0 - c_lo;
+          // this half's scores (columns >= nu are never loaded: masked below)
+          if (nu > c0) tmem_ld32x(tS + c0, &r[0]);
+          if (nu > c0 + 32) tmem_ld32x(tS + c0 + 32, &r[32]);
+          tmem_wait_ld();
+          const bool partial = __any_sync(0xffffffffu, !(c_lo <= c0 && c_hi >= c0 + 64));
+          if (partial) {
+            const unsigned span = (unsigned)max(c_hi - c_lo, 0);
+            const int off = c0 - c_lo;
 #pragma unroll
-              for (int c = 0; c < 64; ++c) r[c] = ((unsigned)(off + c) < span) ? r[c] : 0xFF800000u;
-            }
-            float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < 64; c += 8) {
-              mx0 = fmax3f(mx0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
-              mx1 = fmax3f(mx1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
-              mx2 = fmax3f(mx2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
-              mx3 = fmax3f(mx3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
-            }
-            const float m_half = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
-            // lazy rescale (2^8): O holds this item's sum only from tile 1 on (tile 0's PV
-            // overwrites it), and then PV(g-1) must have completed before O is touched
-            const bool upd = m_half > m + kRescaleThreshold;
-            const bool need_o = upd && (m != -INFINITY);
-            const float f = need_o ? ex2f(m - m_half) : 1.f;
-            if (upd) {
-              lsum2.x *= f; lsum2.y *= f;
-              l0.x *= f; l0.y *= f; l1.x *= f; l1.y *= f;
-              m = m_half;
-            }
-            if (__any_sync(0xffffffffu, need_o)) {
-              if (jj > 0) {
-                fwait(bar(B_VE + (g - 1) % VST), ((g - 1) / VST) & 1, bar0);
-                tc_fence_after();
-#pragma unroll 1
-                for (int ch = 0; ch < 4; ++ch) {
-                  uint32_t o[32];
-                  tmem_ld32(tO + ch * 32, o);
-                  tmem_wait_ld();
-#pragma unroll
-                  for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
-                  tmem_st32(tO + ch * 32, o);
-                }
-              }
-              if (hf == 1) {   // half 0's P was exponentiated against the old max
-                uint32_t o[32];
-                tmem_ld32(tS, o);
-                tmem_wait_ld();
-#pragma unroll
-                for (int c = 0; c < 32; ++c) o[c] = pack_bf16(bf_lo(o[c]) * f, bf_hi(o[c]) * f);
-                tmem_st32(tS, o);
-              }
-              tmem_wait_st();
-            }
-            const float m_use = (m == -INFINITY) ? 0.f : m;
-            const float2 negm2 = make_float2(-m_use, -m_use);
-#pragma unroll
-            for (int c = 0; c < 64; c += 4) {
-              const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
-              const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
-              const float2 p0 = make_float2(ex2f(x0.x), ex2f(x0.y));
-              const float2 p1 = make_float2(ex2f(x1.x), ex2f(x1.y));
-              l0 = __fadd2_rn(l0, p0);
-              l1 = __fadd2_rn(l1, p1);
-              r[c >> 1] = pack_bf16(p0.x, p0.y);
-              r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
-            }
-            tmem_st32(tS + 32 * hf, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+            for (int c = 0; c < 64; ++c) r[c] = ((unsigned)(off + c) < span) ? r[c] : 0xFF800000u;
           }
+          float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < 64; c += 8) {
+            mx0 = fmax3f(mx0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+            mx1 = fmax3f(mx1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+            mx2 = fmax3f(mx2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
+            mx3 = fmax3f(mx3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
+          }
+          // row max over both halves: exchange with the other warp of this lane quarter (both
+          // have loaded their S columns before either writes P over S columns 0..63)
+          float* xb = xbuf + (g & 1) * 256;
+          xb[hc * 128 + rloc] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+          const float m_tile = fmaxf(xb[rloc], xb[128 + rloc]) * sl2;
+          // lazy rescale (2^8): O holds this item's sum only from tile 1 on (tile 0's PV
+          // overwrites it), and then PV(g-1) must have completed before O is touched
+          const bool upd = m_tile > m + kRescaleThreshold;
+          const bool need_o = upd && (m != -INFINITY);
+          const float f = need_o ? ex2f(m - m_tile) : 1.f;
+          if (upd) {
+            lsum2.x *= f; lsum2.y *= f;
+            m = m_tile;
+          }
+          if (__any_sync(0xffffffffu, need_o) && jj > 0) {
+            fwait(bar(B_VE + (g - 1) % VST), ((g - 1) / VST) & 1, bar0);
+            tc_fence_after();
+#pragma unroll 1
+            for (int ch = 0; ch < 2; ++ch) {   // this half's 64 O columns
+              uint32_t o[32];
+              tmem_ld32(tO + ch * 32, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+              tmem_st32(tO + ch * 32, o);
+            }
+          }
+          // P = 2^(s*scale - m) (masked -> 0) packed bf16x2 into r[0..31] -> P words 32 hc ..
+          const float m_use = (m == -INFINITY) ? 0.f : m;
+          const float2 negm2 = make_float2(-m_use, -m_use);
+          float2 l0 = make_float2(0.f, 0.f), l1 = l0;
+#pragma unroll
+          for (int c = 0; c < 64; c += 4) {
+            const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+            const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])), scale2, negm2);
+            const float2 p0 = make_float2(ex2f(x0.x), ex2f(x0.y));
+            const float2 p1 = make_float2(ex2f(x1.x), ex2f(x1.y));
+            l0 = __fadd2_rn(l0, p0);
+            l1 = __fadd2_rn(l1, p1);
+            r[c >> 1] = pack_bf16(p0.x, p0.y);
+            r[(c >> 1) + 1] = pack_bf16(p1.x, p1.y);
+          }
+          tmem_st32(tS + 32 * hc, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
           lsum2 = __fadd2_rn(lsum2, __fadd2_rn(l0, l1));
           tmem_wait_st();
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) arrive_cl(lbar(B_P + (g & 1)), 1);
-        if (rloc == 0) PT(PT_SM_P, g);
+        if (lane == 0) arrive_cl(lbar(B_P + sb), 1);
+        if (rloc == 0 && hc == 0) PT(PT_SM_P, g);
       }
-      // the item's (l, m) for the epilogue warpgroup
+      // the item's (l, m) of this half for the epilogue warpgroup
       if (kk >= 2) fwait(bar(B_LF + (kk & 1)), ((kk - 2) >> 1) & 1, bar0);
-      lbuf[(kk & 1) * 128 + rloc] = make_float2(lsum2.x + lsum2.y, m);
+      lbuf[((kk & 1) * 2 + hc) * 128 + rloc] = make_float2(lsum2.x + lsum2.y, m);
       mbar_arrive(bar(B_LR + (kk & 1)));
     }
-  } else if (warp < 8) {
+  } else if (warp < 12) {
     // ================================================================ rotation + Q prep + epilogue
-    const int lt = threadIdx.x - 128;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegAux));
+    const int lt = threadIdx.x - 256;
     const int c8 = lt & 7;             // frequencies 8*c8 .. 8*c8+7
     const int rg = lt >> 3;            // key rows rg*4 .. rg*4+3 of this CTA's half
     const float4* __restrict__ rp = p.rope_pairs;
@@ -1368,51 +1385,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (lane == 0) arrive_cl(lbar(B_QR + (kq & 1)), 1);
       if (lt == 0) PT(PT_Q_END, kq);
     };
+    // item ke's O: read out of TMEM at once (the next item's first PV waits for it), then / l
     auto epilogue = [&](int ke) {
       const ItemRec rec = load_rec(recs, ke);
       const AttnParams& p = REC_PARAMS(rec);
       const Item w = item_of(p, rec);
       fwait(bar(B_LR + (ke & 1)), (ke >> 1) & 1, bar0);
-      const float2 lm = lbuf[(ke & 1) * 128 + lt];
+      const float2 lm0 = lbuf[((ke & 1) * 2 + 0) * 128 + lt], lm1 = lbuf[((ke & 1) * 2 + 1) * 128 + lt];
       mbar_arrive(bar(B_LF + (ke & 1)));
-      fwait(bar(B_O + (ke & 1)), (ke >> 1) & 1, bar0);
-      if (lt == 0) PT(PT_EPI_O, ke);
-      tc_fence_after();
       const int rglob = w.m0 + rank * 128 + lt;
       const bool valid_row = rglob < w.rows_total;
       const int qi = valid_row ? rglob / p.grp : 0;
       const int h = valid_row ? w.g * p.grp + rglob % p.grp : 0;
-      const float lsum = lm.x;
+      const float lsum = lm0.x + lm1.x;
       const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
       const bool part = p.n_splits > 1 || p.split_only >= 0;
-      const uint32_t tO = tmem + ((uint32_t)((lt >> 5) * 32) << 16) + (uint32_t)(256 + (ke & 1) * 128);
+      fwait(bar(B_O), ke & 1, bar0);
+      if (lt == 0) PT(PT_EPI_O, ke);
+      tc_fence_after();
+      const uint32_t tO = tO_base + ((uint32_t)((lt >> 5) * 32) << 16);
       uint32_t r[64];
+      if (!part) {
+        uint32_t pk[64];   // O / l as bf16 pairs: the O columns leave TMEM before any store
 #pragma unroll 1
-      for (int hf = 0; hf < 2; ++hf) {
-        if (!PR_ABL_EPI) {
-          tmem_ld32x(tO + 64 * hf, &r[0]);
-          tmem_ld32x(tO + 64 * hf + 32, &r[32]);
-          tmem_wait_ld();
-        }
-        if (hf == 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) arrive_cl(lbar(B_OF + (ke & 1)), 1);   // the O buffer may take item ke + 2
-        }
-        if (!valid_row || PR_ABL_EPI) continue;
-        if (part) {   // split-KV / context-parallel partial: fp32 O / l and log2-sum-exp per split
-          const long long orow = ((long long)w.pp * p.n_q + qi) * p.Hq + h;
-          const long long rows = (long long)p.P * p.n_q * p.Hq;
-          const long long slot = p.split_only >= 0 ? 0 : w.sp;
-          DSC_ASSERT(slot < max(p.n_splits, 1) && orow < rows, "attn_pair split partial row");
-          float4* dst = reinterpret_cast<float4*>(p.ws_o + (slot * rows + orow) * 128 + 64 * hf);
+        for (int hf = 0; hf < 2; ++hf) {
+          if (!PR_ABL_EPI) {
+            tmem_ld32x(tO + 64 * hf, &r[0]);
+            tmem_ld32x(tO + 64 * hf + 32, &r[32]);
+            tmem_wait_ld();
+          }
 #pragma unroll
-          for (int v = 0; v < 16; ++v)
-            dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv, __uint_as_float(r[4 * v + 1]) * inv,
-                                 __uint_as_float(r[4 * v + 2]) * inv, __uint_as_float(r[4 * v + 3]) * inv);
-          if (hf == 0) p.ws_lse[slot * rows + orow] = lsum > 0.f ? lm.y + __log2f(lsum) : -INFINITY;
-        } else {
-          uint32_t q[8];
+          for (int j = 0; j < 32; ++j)
+            pk[32 * hf + j] = pack_bf16(__uint_as_float(r[2 * j]) * inv, __uint_as_float(r[2 * j + 1]) * inv);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_cl(lbar(B_OF), 1);   // O may take item ke + 1
+        if (valid_row && !PR_ABL_EPI) {
           const bool peers = p.n_peers > 0;
           int oq = qi + p.o_rot;   // o_rot = 0 unless ring-ordered output (o_rows > 0)
           if (p.o_rows > 0 && oq >= p.o_rows) oq -= p.o_rows;
@@ -1420,58 +1429,105 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                       : ((long long)w.pp * (p.o_rows > 0 ? p.o_rows : p.n_q) + oq) * p.Hq + h;
           DSC_ASSERT(qi < p.n_q && w.pp < p.P && h < p.Hq && oq < (p.o_rows > 0 ? p.o_rows : p.n_q), "attn_pair O row");
           const int nd = peers ? p.n_peers : 1;
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              q[j] = pack_bf16(__uint_as_float(r[16 * v + 2 * j]) * inv, __uint_as_float(r[16 * v + 2 * j + 1]) * inv);
 #pragma unroll 1
-            for (int d = 0; d < nd; ++d)
-              stg256(reinterpret_cast<__nv_bfloat16*>(peers ? p.peer_o[d] : p.o) + row * 128 + 64 * hf + 16 * v, q);
+          for (int d = 0; d < nd; ++d) {
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(peers ? p.peer_o[d] : p.o) + row * 128;
+#pragma unroll
+            for (int v = 0; v < 8; ++v) stg256(dst + 16 * v, *reinterpret_cast<const uint32_t(*)[8]>(&pk[8 * v]));
           }
+        }
+      } else {
+        // split-KV / context-parallel partial: fp32 O / l and log2-sum-exp per split
+        const long long orow = ((long long)w.pp * p.n_q + qi) * p.Hq + h;
+        const long long rows = (long long)p.P * p.n_q * p.Hq;
+        const long long slot = p.split_only >= 0 ? 0 : w.sp;
+        DSC_ASSERT(!valid_row || (slot < max(p.n_splits, 1) && orow < rows), "attn_pair split partial row");
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+          tmem_ld32x(tO + 64 * hf, &r[0]);
+          tmem_ld32x(tO + 64 * hf + 32, &r[32]);
+          tmem_wait_ld();
+          if (hf == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_cl(lbar(B_OF), 1);
+          }
+          if (!valid_row) continue;
+          float4* dst = reinterpret_cast<float4*>(p.ws_o + (slot * rows + orow) * 128 + 64 * hf);
+#pragma unroll
+          for (int v = 0; v < 16; ++v)
+            dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv, __uint_as_float(r[4 * v + 1]) * inv,
+                                 __uint_as_float(r[4 * v + 2]) * inv, __uint_as_float(r[4 * v + 3]) * inv);
+          if (hf == 0) p.ws_lse[slot * rows + orow] = lsum > 0.f ? lm0.y + __log2f(lsum) : -INFINITY;
         }
       }
       if (lt == 0) PT(PT_EPI_END, ke);
     };
-    // jobs of item kk: its raw K tiles rotated (this CTA's half; none for a staged build),
-    // item kk+1's Q tile after the first of them, then item kk-1's epilogue
-    int gt = 0;
-    if (n_my > 0) prep_q(0);
-    for (int kk = 0; kk < n_my; ++kk) {
-      const ItemRec rec = load_rec(recs, kk);
+    // Jobs in global tile order: tile g's K half rotated (raw K only), item k+1's Q after the
+    // first tile of item k, and item e's epilogue once the tiles whose QK^T precede e's last
+    // PV in the issue order (S runs two tiles ahead) are rotated.
+    int gt = 0, ep = 0;   // ep: next item to write out
+    int ep_last = n_my > 0 ? load_rec(recs, 0).n_tiles - 1 : 0;   // global index of item ep's last tile
+    int qn = 0;           // next item whose Q tile to prepare
+    for (int kk = 0; kk <= n_my; ++kk) {
+      const bool real = kk < n_my;
+      const ItemRec rec = load_rec(recs, real ? kk : 0);
       const AttnParams& p = REC_PARAMS(rec);
       const Item w = item_of(p, rec);
-      const bool rot = !w.staged;
+      const bool rot = real && !w.staged;
       const int A = w.A;
       const bool dbg = p.dbg_pos != nullptr && w.g == 0;   // every problem, kv head 0
       int* const dbgp = dbg ? p.dbg_pos + (w.head_row / p.Hkv) * p.dbg_len : nullptr;
-      if (rot) {
+      const int n = real ? w.n_tiles : 1;
 #pragma unroll 1
-        for (int jj = 0; jj < w.n_tiles; ++jj) {
-          const int g = gt + jj, u = w.t_begin + jj, ks = g % KST;
-          const TileSeg tg = tile_segments<BN>(p, w, u);
-          const int nh = width2(tg) >> 1;
+      for (int jj = 0; jj < n; ++jj) {
+        const int g = gt + jj, u = w.t_begin + jj, ks = g % KST;
+        if (rot) {
+          // this thread's 4 key rows: lr = rg*4 .. rg*4+3 of the CTA's half (tile rows rank*nh + lr)
+          int nh, p0 = -1;
+          bool consec;
           int kpos[4];
+          const uint32_t tile = sbase + OFF_K + ks * kKBytes;
+          if (u >= w.n_extra) {   // window tile: ids A + 128 b + row, rows < valid
+            const int base = BN * (u - w.n_extra);
+            const int valid = min(w.cnt - base, BN);
+            nh = (((valid + 15) & ~15) + 31 & ~31) >> 1;
+            const int row0 = rank * nh + rg * 4;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int lr = rg * 4 + k;
-            kpos[k] = lr < nh ? seg_pos(tg, rank * nh + lr) : -1;
+            for (int k = 0; k < 4; ++k) kpos[k] = (rg * 4 + k < nh && row0 + k < valid) ? w.A + base + row0 + k : -1;
+            consec = row0 + 3 < valid && rg * 4 + 3 < nh;
+          } else {
+            const TileSeg tg = tile_segments<BN>(p, w, u);
+            nh = width2(tg) >> 1;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int lr = rg * 4 + k;
+              kpos[k] = lr < nh ? seg_pos(tg, rank * nh + lr) : -1;
+            }
+            consec = false;
           }
-          int p0 = -1;
 #pragma unroll
           for (int k = 3; k >= 0; --k)
             if (kpos[k] >= 0) p0 = kpos[k];
           float4 pre[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) pre[j] = rp[(long long)max(p0, 0) * 32 + 4 * c8 + j];
+          if (lt == 0) PT(PT_ROT_PRE, g);
           fwait(bar(B_KR + ks), (g / KST) & 1, bar0);
-          if (rg * 4 < nh && !PR_ABL_ROT)   // rows >= nh are never read by the MMA
-            rotate_rows<1, kKHalf>(sbase + OFF_K + ks * kKBytes, rg * 4, c8, rp, cth, sth, kpos, pre, max(p0, 0));
+          if (lt == 0) PT(PT_ROT_KR, g);
+          if (!PR_ABL_ROT) {
+            if (__all_sync(0xffffffffu, consec))
+              rotate4_consec<kKHalf>(tile, rg * 4, c8, cth, sth, pre);
+            else if (rg * 4 < nh)   // rows >= nh are never read by the MMA
+              rotate_rows<1, kKHalf>(tile, rg * 4, c8, rp, cth, sth, kpos, pre, max(p0, 0));
+          }
+          if (lt == 0) PT(PT_ROT_RR, g);
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) arrive_cl(lbar(B_KF + ks), 1);
           if (lt == 0) PT(PT_ROT, g);
           if (dbg && c8 == 0) {
+            const TileSeg tg = tile_segments<BN>(p, w, u);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const int rr = rank * nh + rg * 4 + k;
@@ -1482,180 +1538,216 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 dbgp[(u < w.n_extra) ? (x < A ? x : p.dbg_A + p.dbg_R + (x - A)) : p.dbg_A + slot] = kpos[k];
             }
           }
-          if (jj == 0 && kk + 1 < n_my) prep_q(kk + 1);
         }
-      } else if (kk + 1 < n_my) {
-        prep_q(kk + 1);
-      }
-      if (kk >= 1) epilogue(kk - 1);
-      gt += w.n_tiles;
-    }
-    if (n_my > 0) epilogue(n_my - 1);
-  } else if (warp == 8 || warp == 9) {
-    // ================================================================ copy warps (8: K half, 9: V columns)
-    const bool isk = warp == 8;
-    int gt = 0;
-    for (int kk = 0; kk < n_my; ++kk) {
-      const ItemRec rec = load_rec(recs, kk);
-      const AttnParams& p = REC_PARAMS(rec);
-      const Item w = item_of(p, rec);
-      const int A = p.A;
-      const __nv_bfloat16* __restrict__ SX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.sink_k : p.sink_v);
-      const __nv_bfloat16* __restrict__ XX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.self_k : p.self_v);
+        // Q tiles of items up to kk + 1 (item 0's and 1's after item 0's first K tile)
+        if (jj == 0) {
 #pragma unroll 1
-      for (int jj = 0; jj < w.n_tiles; ++jj) {
-        const int g = gt + jj, u = w.t_begin + jj;
-        const int nst = isk ? KST : VST, st = g % nst;
-        if (g >= nst) fwait(bar((isk ? B_KE : B_VE) + st), ((g - nst) / nst) & 1, bar0);
-        const uint32_t full = bar((isk ? B_KR : B_VL) + st);
-        const uint32_t dst = sbase + (isk ? OFF_K + st * kKBytes : OFF_V + st * kVBytes);
-        const TileSeg t = tile_segments<BN>(p, w, u);
-        const int nu = width2(t), nh = nu >> 1;
-        if (u < w.n_extra) {
-          // sink rows (x < A) + self rows (A <= x < A + n_self), zeros up to the pair width
-          const int nrows = isk ? nh : nu;
-          const int cpr = isk ? 16 : 8;          // 16-byte chunks per row this CTA loads
-          const int key0 = isk ? rank * nh : 0;
-          const int col0 = isk ? 0 : 64 * rank;
-#pragma unroll 1
-          for (int id = lane; id < nrows * cpr; id += 32) {
-            const int rr = id / cpr, ch = id % cpr;
-            const int x = BN * u + key0 + rr;
-            const __nv_bfloat16* src = nullptr;
-            if (x < A) src = SX + ((long long)w.head_row * A + x) * 128;
-            else if (x < A + w.n_self) src = XX + (((long long)w.pp * w.n_self + (x - A)) * p.Hkv + w.g) * 128;
-            DSC_ASSERT(w.head_row < (long long)p.S * p.N_total * p.Hkv && w.pp < p.P, "attn_pair sink/self row");
-            const uint32_t d = isk ? dst + (ch >> 3) * kKHalf + rr * 128 + (((ch & 7) ^ (rr & 7)) << 4)
-                                   : dst + rr * 128 + ((ch ^ (rr & 7)) << 4);
-            cp_async16(d, src ? (const void*)(src + col0 + 8 * ch) : (const void*)SX, src ? 16u : 0u);
-          }
-          cp_async_wait_all();
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(full);
-        } else if (lane == 0) {
-          const int row = (int)(w.head_row * w.Rp) + t.slot0;
-          DSC_ASSERT(t.slot0 >= 0 && t.slot0 < w.Rp && (w.staged || t.slot0 + BN <= w.Rp) &&
-                         w.head_row < (long long)p.S * p.N_total * p.Hkv,
-                     "attn_pair TMA box rows");
-          PT(isk ? PT_CPK : PT_CPV, g);
-          if (isk) {
-            mbar_arrive_tx(full, kKBytes);
-            tma_load_2d(dst, &p.tmap_k64, 0, row + rank * nh, full);
-            tma_load_2d(dst + kKHalf, &p.tmap_k64, 64, row + rank * nh, full);
-          } else {
-            mbar_arrive_tx(full, kVBytes);
-            tma_load_2d(dst, &p.tmap_v, 64 * rank, row, full);
-          }
+          for (; qn <= kk + 1 && qn < n_my; ++qn) prep_q(qn);
         }
-        __syncwarp();
+        // epilogue of item ep once tile last(ep) + 2 is rotated (its S goes out before the
+        // next item's first PV, which waits for this read-out)
+#pragma unroll 1
+        while (ep < kk && (!real || ep_last + 2 <= g)) {
+          epilogue(ep);
+          ++ep;
+          if (ep < n_my) ep_last += load_rec(recs, ep).n_tiles;
+        }
       }
-      gt += w.n_tiles;
+      if (real) gt += w.n_tiles;
     }
-  } else if (warp == 11) {
-    // ================================================================ forwarder
-    if (lane == 0) {
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegMisc));
+    if (warp == 12 || warp == 13) {
+      // ============================================================== copy warps (12: K half, 13: V columns)
+      const bool isk = warp == 12;
       int gt = 0;
       for (int kk = 0; kk < n_my; ++kk) {
         const ItemRec rec = load_rec(recs, kk);
-        const bool staged = REC_PARAMS(rec).staged;
-        const int n = rec.n_tiles;
+        const AttnParams& p = REC_PARAMS(rec);
+        const Item w = item_of(p, rec);
+        const int A = p.A;
+        const __nv_bfloat16* __restrict__ SX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.sink_k : p.sink_v);
+        const __nv_bfloat16* __restrict__ XX = reinterpret_cast<const __nv_bfloat16*>(isk ? p.self_k : p.self_v);
 #pragma unroll 1
-        for (int jj = 0; jj < n; ++jj) {
-          const int g = gt + jj;
-          if (staged) {   // pre-rotated K: landed = ready
-            fwait(bar(B_KR + g % KST), (g / KST) & 1, bar0);
-            arrive_cl(lbar(B_KF + g % KST), 4);
-            PT(PT_KR_FW, g);
+        for (int jj = 0; jj < w.n_tiles; ++jj) {
+          const int g = gt + jj, u = w.t_begin + jj;
+          const int nst = isk ? KST : VST, st = g % nst;
+          if (g >= nst) fwait(bar((isk ? B_KE : B_VE) + st), ((g - nst) / nst) & 1, bar0);
+          const uint32_t full = bar((isk ? B_KR : B_VL) + st);
+          const uint32_t dst = sbase + (isk ? OFF_K + st * kKBytes : OFF_V + st * kVBytes);
+          const TileSeg t = tile_segments<BN>(p, w, u);
+          const int nu = width2(t), nh = nu >> 1;
+          if (u < w.n_extra) {
+            // sink rows (x < A) + self rows (A <= x < A + n_self), zeros up to the pair width
+            const int nrows = isk ? nh : nu;
+            const int cpr = isk ? 16 : 8;          // 16-byte chunks per row this CTA loads
+            const int key0 = isk ? rank * nh : 0;
+            const int col0 = isk ? 0 : 64 * rank;
+#pragma unroll 1
+            for (int id = lane; id < nrows * cpr; id += 32) {
+              const int rr = id / cpr, ch = id % cpr;
+              const int x = BN * u + key0 + rr;
+              const __nv_bfloat16* src = nullptr;
+              if (x < A) src = SX + ((long long)w.head_row * A + x) * 128;
+              else if (x < A + w.n_self) src = XX + (((long long)w.pp * w.n_self + (x - A)) * p.Hkv + w.g) * 128;
+              DSC_ASSERT(w.head_row < (long long)p.S * p.N_total * p.Hkv && w.pp < p.P, "attn_pair sink/self row");
+              const uint32_t d = isk ? dst + (ch >> 3) * kKHalf + rr * 128 + (((ch & 7) ^ (rr & 7)) << 4)
+                                     : dst + rr * 128 + ((ch ^ (rr & 7)) << 4);
+              cp_async16(d, src ? (const void*)(src + col0 + 8 * ch) : (const void*)SX, src ? 16u : 0u);
+            }
+            cp_async_wait_all();
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full);
+          } else if (lane == 0) {
+            const int row = (int)(w.head_row * w.Rp) + t.slot0;
+            DSC_ASSERT(t.slot0 >= 0 && t.slot0 < w.Rp && (w.staged || t.slot0 + BN <= w.Rp) &&
+                           w.head_row < (long long)p.S * p.N_total * p.Hkv,
+                       "attn_pair TMA box rows");
+            PT(isk ? PT_CPK : PT_CPV, g);
+            if (isk) {
+              mbar_arrive_tx(full, kKBytes);
+              tma_load_2d(dst, &p.tmap_k64, 0, row + rank * nh, full);
+              tma_load_2d(dst + kKHalf, &p.tmap_k64, 64, row + rank * nh, full);
+            } else {
+              mbar_arrive_tx(full, kVBytes);
+              tma_load_2d(dst, &p.tmap_v, 64 * rank, row, full);
+            }
           }
-          fwait(bar(B_VL + g % VST), (g / VST) & 1, bar0);
-          arrive_cl(lbar(B_VR + g % VST), 1);
-          PT(PT_FWV, g);
+          __syncwarp();
         }
-        gt += n;
+        gt += w.n_tiles;
       }
-    }
-  } else if (warp == 10 && rank == 0) {
-    // ================================================================ MMA issuer (leader)
-    constexpr uint32_t IQK0 = idesc_bf16(256, 0, 0, 0);    // S = Q K^T, both K-major; N = pair width
-    constexpr uint32_t IPV = idesc_bf16(256, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
-    struct MI {
-      int n, t_begin, n_extra, aps, cnt;
-    };
-    auto mi_of = [&](int kk) {
-      const ItemRec r = load_rec(recs, kk);
-      const bool isb = r.flags & 1;
-      const int A = isb ? pb.A : pa.A, n_self = isb ? pb.n_self : pa.n_self;
-      MI m;
-      m.n = r.n_tiles; m.t_begin = r.t_begin;
-      m.n_extra = (A + n_self + BN - 1) / BN; m.aps = A + n_self; m.cnt = r.cnt;
-      return m;
-    };
-    auto width_of = [&](const MI& m, int jj) {   // tile_segments' valid keys, rounded up to 32
-      const int u = m.t_begin + jj;
-      const int valid = u < m.n_extra ? min(max(m.aps - BN * u, 0), BN) : min(m.cnt - BN * (u - m.n_extra), BN);
-      return (valid + 31) & ~31;
-    };
-    auto issue_s = [&](const MI& m, int k, int jj, int g) {
-      const int ks = g % KST, qb = k & 1;
-      if (jj == 0) cwait(bar(B_QR + qb), (k >> 1) & 1, bar0);
-      if (jj == 0 && lane == 0) PT(PT_QR_OK, k);
-      cwait(bar(B_KF + ks), (g / KST) & 1, bar0);
-      if (lane == 0) PT(PT_KF_OK, g);
-      tc_fence_after();
-      const int nu = width_of(m, jj);
-      const uint64_t da = sdesc(qbuf_addr(k), 16, 1024);
-      const uint64_t db = sdesc(sbase + OFF_K + ks * kKBytes, 16, 1024);
-      mma2_qk(tmem + (uint32_t)((g & 1) * 128), da, db, IQK0 | ((uint32_t)(nu >> 3) << 17));
-      commit2_w(bar(B_S + (g & 1)));
-      commit2_w(bar(B_KE + ks));
-      if (jj + 1 == m.n) commit2_w(bar(B_QF + qb));
-      if (lane == 0) PT(PT_S_ISS, g);
-      if (jj == 0 && lane == 0) PT(PT_ITEM, k);
-    };
-    auto issue_pv = [&](const MI& m, int k, int jj, int g) {
-      const int vs = g % VST;
-      cwait(bar(B_VR + vs), (g / VST) & 1, bar0);
-      if (lane == 0) PT(PT_VR_OK, g);
-      cwait(bar(B_P + (g & 1)), (g >> 1) & 1, bar0);
-      if (lane == 0) PT(PT_P_OK, g);
-      if (jj == 0 && k >= 2) cwait(bar(B_OF + (k & 1)), ((k - 2) >> 1) & 1, bar0);
-      if (jj == 0 && lane == 0) PT(PT_OF_OK, k);
-      tc_fence_after();
-      const int nu = width_of(m, jj);
-      const uint64_t dv = sdesc(sbase + OFF_V + vs * kVBytes, 16, 1024);
-      const uint32_t d = tmem + (uint32_t)(256 + (k & 1) * 128), a = tmem + (uint32_t)((g & 1) * 128);
-      const uint32_t acc = jj > 0 ? 1u : 0u;
-      if (nu == BN) {
-        mma2_pv8(d, a, dv, IPV, acc);
-      } else {
-        mma2_pv1(d, a, dv, IPV, acc);
+    } else if (warp == 15) {
+      // ============================================================== forwarder
+      if (lane == 0) {
+        int gt = 0;
+        for (int kk = 0; kk < n_my; ++kk) {
+          const ItemRec rec = load_rec(recs, kk);
+          const bool staged = REC_PARAMS(rec).staged;
+          const int n = rec.n_tiles;
 #pragma unroll 1
-        for (int k8 = 1; k8 < (nu >> 4); ++k8) mma2_pv1(d, a + k8 * 8, dv + (uint64_t)(k8 * 128), IPV, 1u);
-      }
-      commit2_w(bar(B_VE + vs));
-      if (jj + 1 == m.n) commit2_w(bar(B_O + (k & 1)));
-      if (lane == 0) PT(PT_PV_ISS, g);
-    };
-    // one issue stream across items, S one tile ahead of PV: S(g+1), then PV(g)
-    int gt = 0;
-    if (n_my > 0) {
-      MI cur = mi_of(0);
-      issue_s(cur, 0, 0, 0);
-      for (int kk = 0; kk < n_my; ++kk) {
-        const bool has_next = kk + 1 < n_my;
-        const MI nxt = has_next ? mi_of(kk + 1) : cur;
-        for (int jj = 0; jj < cur.n; ++jj) {
-          const int g = gt + jj;
-          if (jj + 1 < cur.n) issue_s(cur, kk, jj + 1, g + 1);
-          else if (has_next) issue_s(nxt, kk + 1, 0, g + 1);
-          issue_pv(cur, kk, jj, g);
+          for (int jj = 0; jj < n; ++jj) {
+            const int g = gt + jj;
+            if (staged) {   // pre-rotated K: landed = ready
+              fwait(bar(B_KR + g % KST), (g / KST) & 1, bar0);
+              arrive_cl(lbar(B_KF + g % KST), 4);
+              PT(PT_KR_FW, g);
+            }
+            fwait(bar(B_VL + g % VST), (g / VST) & 1, bar0);
+            arrive_cl(lbar(B_VR + g % VST), 1);
+            PT(PT_FWV, g);
+          }
+          gt += n;
         }
-        gt += cur.n;
-        cur = nxt;
       }
-      fwait(bar(B_VE + (gt - 1) % VST), ((gt - 1) / VST) & 1, bar0);
-      if (lane == 0) PT(PT_END, 0);
+    } else if (warp == 14 && rank == 0) {
+      // ============================================================== MMA issuer (leader)
+      constexpr uint32_t IQK0 = idesc_bf16(256, 0, 0, 0);    // S = Q K^T, both K-major; N = pair width
+      constexpr uint32_t IPV = idesc_bf16(256, 128, 0, 1);   // O += P V, P from TMEM, V MN-major
+      struct MI {
+        int n, t_begin, n_extra, aps, cnt;
+      };
+      auto mi_of = [&](int kk) {
+        const ItemRec r = load_rec(recs, kk);
+        const bool isb = r.flags & 1;
+        const int A = isb ? pb.A : pa.A, n_self = isb ? pb.n_self : pa.n_self;
+        MI m;
+        m.n = r.n_tiles; m.t_begin = r.t_begin;
+        m.n_extra = (A + n_self + BN - 1) / BN; m.aps = A + n_self; m.cnt = r.cnt;
+        return m;
+      };
+      auto width_of = [&](const MI& m, int jj) {   // tile_segments' valid keys, rounded up to 32
+        const int u = m.t_begin + jj;
+        const int valid = u < m.n_extra ? min(max(m.aps - BN * u, 0), BN) : min(m.cnt - BN * (u - m.n_extra), BN);
+        return (valid + 31) & ~31;
+      };
+      // S(g) of item k, local tile jj: ready once the item's Q tile (jj = 0) and the K tile are
+      auto ready_s = [&](int k, int jj, int g) {
+        if (jj == 0 && !mbar_test(bar(B_QR + (k & 1)), (k >> 1) & 1)) return false;
+        return mbar_test(bar(B_KF + g % KST), (g / KST) & 1);
+      };
+      auto issue_s = [&](const MI& m, int k, int jj, int g) {
+        const int ks = g % KST, qb = k & 1, sb = g % NSB;
+        if (lane == 0) PT(PT_KF_OK, g);
+        tc_fence_after();
+        const int nu = width_of(m, jj);
+        const uint64_t da = sdesc(qbuf_addr(k), 16, 1024);
+        const uint64_t db = sdesc(sbase + OFF_K + ks * kKBytes, 16, 1024);
+        if (lane == 0) PT(PT_S_FENCE, g);
+        mma2_qk(tmem + (uint32_t)(sb * 128), da, db, IQK0 | ((uint32_t)(nu >> 3) << 17));
+        if (lane == 0) PT(PT_S_MMA, g);
+        commit2_w(bar(B_S + sb));
+        commit2_w(bar(B_KE + ks));
+        if (jj + 1 == m.n) commit2_w(bar(B_QF + qb));
+        if (lane == 0) PT(PT_S_ISS, g);
+        if (jj == 0 && lane == 0) PT(PT_ITEM, k);
+      };
+      // PV(g): V tile, P (both CTAs) and, for an item's first PV, the previous item's O read out
+      auto ready_pv = [&](int k, int jj, int g) {
+        if (!mbar_test(bar(B_VR + g % VST), (g / VST) & 1)) return false;
+        if (!mbar_test(bar(B_P + g % NSB), (g / NSB) & 1)) return false;
+        return !(jj == 0 && k >= 1) || mbar_test(bar(B_OF), (k - 1) & 1);
+      };
+      auto issue_pv = [&](const MI& m, int k, int jj, int g) {
+        const int vs = g % VST, sb = g % NSB;
+        if (lane == 0) PT(PT_P_OK, g);
+        tc_fence_after();
+        const int nu = width_of(m, jj);
+        const uint64_t dv = sdesc(sbase + OFF_V + vs * kVBytes, 16, 1024);
+        const uint32_t d = tO_base, a = tmem + (uint32_t)(sb * 128);
+        const uint32_t acc = jj > 0 ? 1u : 0u;
+        if (nu == BN) {
+          mma2_pv8(d, a, dv, IPV, acc);
+        } else {
+          mma2_pv1(d, a, dv, IPV, acc);
+#pragma unroll 1
+          for (int k8 = 1; k8 < (nu >> 4); ++k8) mma2_pv1(d, a + k8 * 8, dv + (uint64_t)(k8 * 128), IPV, 1u);
+        }
+        if (lane == 0) PT(PT_PV_MMA, g);
+        commit2_w(bar(B_VE + vs));
+        if (jj + 1 == m.n) commit2_w(bar(B_O));
+        if (lane == 0) PT(PT_PV_ISS, g);
+      };
+      // Two cursors over the same tile sequence, each issued as soon as its operands are
+      // ready: S(s) at most two tiles ahead of the next PV (S buffer s % 3 held P(s - 3),
+      // whose PV is then already issued: tcgen05 MMAs of one thread execute in order), and
+      // PV(v) after S(v).  A late K tile no longer holds back a PV whose P is ready.
+      if (n_my > 0) {
+        int s_k = 0, s_jj = 0, s_g = 0, v_k = 0, v_jj = 0, v_g = 0;
+        MI s_m = mi_of(0), v_m = s_m;
+        long long t_idle = 0;
+        while (v_k < n_my) {
+          bool did = false;
+          if (s_k < n_my && s_g <= v_g + 2 && ready_s(s_k, s_jj, s_g)) {
+            issue_s(s_m, s_k, s_jj, s_g);
+            ++s_g;
+            if (++s_jj == s_m.n) {
+              s_jj = 0;
+              if (++s_k < n_my) s_m = mi_of(s_k);
+            }
+            did = true;
+          }
+          if (v_g < s_g && ready_pv(v_k, v_jj, v_g)) {
+            issue_pv(v_m, v_k, v_jj, v_g);
+            ++v_g;
+            if (++v_jj == v_m.n) {
+              v_jj = 0;
+              if (++v_k < n_my) v_m = mi_of(v_k);
+            }
+            did = true;
+          }
+          if (did) {
+            t_idle = 0;
+          } else {   // both queues blocked: back off briefly instead of spinning on the SMSP
+            __nanosleep(32);
+            if (t_idle == 0) t_idle = clock64();
+            else if (clock64() - t_idle > fa::g_fa_wd_lim) fa::fa_wd_fail(B_P, v_g);
+          }
+        }
+        fwait(bar(B_VE + (v_g - 1) % VST), ((v_g - 1) / VST) & 1, bar0);
+        if (lane == 0) PT(PT_END, 0);
+      }
     }
   }
 
@@ -1663,7 +1755,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __syncthreads();
   cluster_sync_all();
   tc_fence_after();
-  if (warp == 10) {
+  if (warp == 14) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 #undef REC_PARAMS

@@ -316,5 +316,46 @@ __device__ __forceinline__ void rotate_rows(uint32_t tile, int r0, int c8, const
   }
 }
 
+// rotate_rows for 4 rows r0 .. r0+3 with CONSECUTIVE ids p0 .. p0+3 (a window tile: no
+// per-row branches): (cs, sn) start at the table entry of p0 and advance by R(theta) per row
+template <int HI>
+__device__ __forceinline__ void rotate4_consec(uint32_t tile, int r0, int c8, const float2 (&cth)[4],
+                                               const float2 (&sth)[4], const float4 (&pre)[4]) {
+  float2 cs[4], sn[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) { cs[j] = make_float2(pre[j].x, pre[j].y); sn[j] = make_float2(pre[j].z, pre[j].w); }
+  uint4 lo[4], hi[4];
+  uint32_t addr[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = r0 + k;
+    addr[k] = tile + r * 128 + ((c8 ^ (r & 7)) << 4);
+    lo[k] = lds128(addr[k]);
+    hi[k] = lds128(addr[k] + HI);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k > 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 nc = __ffma2_rn(cs[j], cth[j], __fmul2_rn(make_float2(-sn[j].x, -sn[j].y), sth[j]));
+        sn[j] = __ffma2_rn(sn[j], cth[j], __fmul2_rn(cs[j], sth[j]));
+        cs[j] = nc;
+      }
+    }
+    uint32_t ol[4], oh[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 av = bf2(get_w(lo[k], j)), bv = bf2(get_w(hi[k], j));
+      const float2 yl = __ffma2_rn(av, cs[j], __fmul2_rn(make_float2(-bv.x, -bv.y), sn[j]));   // a cos - b sin
+      const float2 yh = __ffma2_rn(av, sn[j], __fmul2_rn(bv, cs[j]));                        // a sin + b cos
+      ol[j] = pack_bf16(yl.x, yl.y);
+      oh[j] = pack_bf16(yh.x, yh.y);
+    }
+    sts128(addr[k], make_uint4(ol[0], ol[1], ol[2], ol[3]));
+    sts128(addr[k] + HI, make_uint4(oh[0], oh[1], oh[2], oh[3]));
+  }
+}
+
 }  // namespace tcc
 }  // namespace dsc

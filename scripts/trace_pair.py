@@ -21,7 +21,8 @@ from paper_2605_01858_b200 import dscache as _D  # noqa: E402
 
 NE, NI = 32, 1024
 EV = dict(S_ISS=0, PV_ISS=1, KF_OK=2, VR_OK=3, P_OK=4, SM_S=5, SM_P=6, CPK=7, CPV=8, FWV=9, ROT=10,
-          ITEM=12, Q_START=13, Q_FREE=14, Q_END=15, EPI_O=16, EPI_END=17, QR_OK=18, OF_OK=19, END=20, KR_FW=21)
+          ITEM=12, Q_START=13, Q_FREE=14, Q_END=15, EPI_O=16, EPI_END=17, QR_OK=18, OF_OK=19, END=20, KR_FW=21,
+          S_MMA=22, PV_MMA=23, S_FENCE=24, ROT_PRE=25, ROT_KR=26, ROT_RR=27)
 
 
 def main():
@@ -102,13 +103,57 @@ def main():
         return out
     for name, a, b in [("S issue -> softmax sees S", "SM_S", "S_ISS"), ("softmax S -> P", "SM_P", "SM_S"),
                        ("softmax P -> MMA P ok", "P_OK", "SM_P"), ("P ok -> PV issued", "PV_ISS", "P_OK"),
-                       ("V TMA -> fwd", "FWV", "CPV"), ("K TMA -> fwd", "KR_FW", "CPK")]:
-        d_ = dif(a, b)
+                       ("V TMA -> fwd", "FWV", "CPV"), ("K TMA -> fwd", "KR_FW", "CPK"),
+                       ("MMA: KF ok -> fence done", "S_FENCE", "KF_OK"), ("MMA: 8 QK MMAs", "S_MMA", "S_FENCE"),
+                       ("MMA: S commits", "S_ISS", "S_MMA"), ("MMA: P ok -> PV MMAs done", "PV_MMA", "P_OK"),
+                       ("MMA: PV commits", "PV_ISS", "PV_MMA"), ("rot: pre -> KR ok", "ROT_KR", "ROT_PRE"),
+                       ("rot: KR ok -> rotated", "ROT_RR", "ROT_KR"), ("rot: rotated -> arrived", "ROT", "ROT_RR"),
+                       ("MMA: PV(g) -> S(g+3) start", None, None)]:
+        d_ = dif(a, b) if a else [ev("KF_OK", gg + 3) - ev("PV_ISS", gg) for gg in range(n_tiles - 3)
+                                   if ev("KF_OK", gg + 3) is not None and ev("PV_ISS", gg) is not None]
         if d_:
             print(f"{name:28s}: median {st.median(d_):7.0f}  p90 {sorted(d_)[int(0.9 * len(d_))]:7.0f}  n {len(d_)}")
     per = [s_iss[gg + 1] - s_iss[gg] for gg in range(n_tiles - 1) if s_iss[gg] is not None and s_iss[gg + 1] is not None]
     if per:
         print(f"S issue period: median {st.median(per):.0f}")
+    # the peer (CTA 1): its own clock; intervals only
+    tp = tr[1]
+
+    def evp(e, i):
+        x = int(tp[EV[e], i])
+        return x if x else None
+    print("=== peer CTA 1 (own clock)")
+    for name, a, b in [("softmax S -> P", "SM_P", "SM_S"), ("V TMA -> fwd", "FWV", "CPV"),
+                       ("softmax P(g) -> S(g+1) seen", None, None)]:
+        d_ = []
+        for gg in range(n_tiles - 1):
+            if a is None:
+                x, y = evp("SM_S", gg + 1), evp("SM_P", gg)
+            else:
+                x, y = evp(a, gg), evp(b, gg)
+            if x is not None and y is not None:
+                d_.append(x - y)
+        if d_:
+            print(f"{name:28s}: median {st.median(d_):7.0f}  p90 {sorted(d_)[int(0.9 * len(d_))]:7.0f}  n {len(d_)}")
+    d_ = [ev("ROT_PRE", gg + 1) - ev("ROT", gg) for gg in range(n_tiles - 1)
+          if ev("ROT_PRE", gg + 1) is not None and ev("ROT", gg) is not None]
+    if d_:
+        print(f"rot: arrived(g) -> pre(g+1) : median {st.median(d_):7.0f}")
+    for name, e in [("peer S seen period", "SM_S"), ("peer V fwd period", "FWV"), ("peer V TMA period", "CPV")]:
+        xs = [evp(e, gg) for gg in range(n_tiles)]
+        pp = [xs[i + 1] - xs[i] for i in range(len(xs) - 1) if xs[i] is not None and xs[i + 1] is not None]
+        if pp:
+            print(f"{name:28s}: median {st.median(pp):7.0f}")
+    d_ = []
+    for gg in range(n_tiles - 1):
+        x, y = ev("SM_S", gg + 1), ev("SM_P", gg)
+        if x is not None and y is not None:
+            d_.append(x - y)
+    if d_:
+        print(f"leader softmax P(g) -> S(g+1) seen: median {st.median(d_):7.0f}")
+    for gg in range(200, 204):
+        print("   peer g%-4d " % gg + " ".join(f"{k}={(evp(k, gg) or 0) - (evp('SM_S', 200) or 0)}" for k in ("SM_S", "SM_P", "CPK", "CPV", "FWV", "ROT")))
+        print("   lead g%-4d " % gg + " ".join(f"{k}={(ev(k, gg) or 0) - (ev('SM_S', 200) or 0)}" for k in ("SM_S", "SM_P", "CPK", "CPV", "FWV", "ROT", "VR_OK", "P_OK", "PV_ISS", "S_ISS")))
 
 
 if __name__ == "__main__":

@@ -199,11 +199,14 @@ __device__ __noinline__ void fa_wd_fail(uint32_t bar_off, uint32_t parity) {
   }
   __trap();
 }
+// The limit is read once per blocked wait, before the spin (the asm "memory" clobbers would
+// otherwise reload it from global memory on every iteration).
 __device__ __forceinline__ void fwait(uint32_t bar, uint32_t parity, uint32_t bar0) {
   if (mbar_try(bar, parity)) return;
+  const long long lim = g_fa_wd_lim;
   const long long t0 = clock64();
   while (!mbar_try(bar, parity)) {
-    if (clock64() - t0 > g_fa_wd_lim) fa_wd_fail((bar - bar0) / 8, parity);
+    if (clock64() - t0 > lim) fa_wd_fail((bar - bar0) / 8, parity);
   }
 }
 
@@ -1031,7 +1034,8 @@ constexpr int kPtEvents = 32, kPtIdx = 1024;
 enum {
   PT_S_ISS = 0, PT_PV_ISS, PT_KF_OK, PT_VR_OK, PT_P_OK, PT_SM_S, PT_SM_P, PT_CPK, PT_CPV, PT_FWV, PT_ROT,   // per tile
   PT_ITEM = 12, PT_Q_START, PT_Q_FREE, PT_Q_END, PT_EPI_O, PT_EPI_END, PT_QR_OK, PT_OF_OK, PT_END,           // per item
-  PT_KR_FW = 21, PT_S_MMA = 22, PT_PV_MMA = 23, PT_S_FENCE = 24, PT_ROT_PRE = 25, PT_ROT_KR = 26, PT_ROT_RR = 27   // per tile
+  PT_KR_FW = 21, PT_S_MMA = 22, PT_PV_MMA = 23, PT_S_FENCE = 24, PT_ROT_PRE = 25, PT_ROT_KR = 26, PT_ROT_RR = 27,   // per tile
+  PT_ROT9 = 28, PT_ROT10 = 29, PT_ROT11 = 30
 };
 #if PR_TRACE
 #define PT(ev, i)                                                                                      \
@@ -1081,9 +1085,10 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
 // wait on a barrier that collects arrivals from both CTAs (cluster-scope acquire)
 __device__ __forceinline__ void cwait(uint32_t bar, uint32_t parity, uint32_t bar0) {
   if (mbar_try_cl(bar, parity)) return;
+  const long long lim = fa::g_fa_wd_lim;
   const long long t0 = clock64();
   while (!mbar_try_cl(bar, parity)) {
-    if (clock64() - t0 > fa::g_fa_wd_lim) fa::fa_wd_fail((bar - bar0) / 8, parity);
+    if (clock64() - t0 > lim) fa::fa_wd_fail((bar - bar0) / 8, parity);
   }
 }
 __device__ __forceinline__ void cluster_sync_all() {
@@ -1526,6 +1531,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) arrive_cl(lbar(B_KF + ks), 1);
           if (lt == 0) PT(PT_ROT, g);
+          if (lt == 32) PT(PT_ROT9, g);
+          if (lt == 64) PT(PT_ROT10, g);
+          if (lt == 96) PT(PT_ROT11, g);
           if (dbg && c8 == 0) {
             const TileSeg tg = tile_segments<BN>(p, w, u);
 #pragma unroll
@@ -1739,7 +1747,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           if (did) {
             t_idle = 0;
-          } else {   // both queues blocked: back off briefly instead of spinning on the SMSP
+          } else {   // both queues blocked: back off instead of spinning on the SMSP (the
+                     // sleep plus the watchdog check's global load make a ~0.5K clk backoff;
+                     // a tight test_wait poll slows the rotation / softmax warps of this
+                     // sub-partition, a suspending in-order issuer measured slower too)
             __nanosleep(32);
             if (t_idle == 0) t_idle = clock64();
             else if (clock64() - t_idle > fa::g_fa_wd_lim) fa::fa_wd_fail(B_P, v_g);
@@ -1838,11 +1849,11 @@ int fa_watchdog_read(unsigned long long* out, int n) {
   return 0;
 }
 
-// DSC_FA=8 selects the CTA-pair kernel (v8), default: the single-CTA v7 kernel
+// Default: the CTA-pair kernel (v8); DSC_FA=7 selects the single-CTA v7 kernel (A/B runs)
 static bool pair_kernel_on() {
   static const bool on = [] {
     const char* e = std::getenv("DSC_FA");
-    return e && e[0] == '8';
+    return !(e && e[0] == '7');
   }();
   return on;
 }

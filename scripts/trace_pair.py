@@ -22,7 +22,7 @@ from paper_2605_01858_b200 import dscache as _D  # noqa: E402
 NE, NI = 32, 1024
 EV = dict(S_ISS=0, PV_ISS=1, KF_OK=2, VR_OK=3, P_OK=4, SM_S=5, SM_P=6, CPK=7, CPV=8, FWV=9, ROT=10,
           ITEM=12, Q_START=13, Q_FREE=14, Q_END=15, EPI_O=16, EPI_END=17, QR_OK=18, OF_OK=19, END=20, KR_FW=21,
-          S_MMA=22, PV_MMA=23, S_FENCE=24, ROT_PRE=25, ROT_KR=26, ROT_RR=27)
+          S_MMA=22, PV_MMA=23, S_FENCE=24, ROT_PRE=25, ROT_KR=26, ROT_RR=27, ROT9=28, ROT10=29, ROT11=30)
 
 
 def main():
@@ -151,6 +151,21 @@ def main():
             d_.append(x - y)
     if d_:
         print(f"leader softmax P(g) -> S(g+1) seen: median {st.median(d_):7.0f}")
+    print("   g: PV(g-3)end S_start S_end | ROT8..11 lead | ROT8..11 peer | P_lead")
+    for gg in range(200, 212):
+        def q(e, tt):
+            x = int(tt[EV[e], gg])
+            return x - int(t[EV["SM_S"], 200]) if x else None
+        pv3 = ev("PV_ISS", gg - 3) - ev("SM_S", 200) if ev("PV_ISS", gg - 3) is not None else None
+        print(f"   {gg}: {pv3} {q('KF_OK', t)} {q('S_ISS', t)} | {q('ROT', t)} {q('ROT9', t)} {q('ROT10', t)} {q('ROT11', t)} | "
+              f"{q('ROT', tp)} {q('ROT9', tp)} {q('ROT10', tp)} {q('ROT11', tp)} | {q('SM_P', t)}")
+    print("   g   : S_ISS  PV_ISS | P_lead  ROT_l  ROT_p  FWV_l  FWV_p | S gate: PV(g-3) / KF")
+    for gg in range(200, 216):
+        def q(e, tt):
+            x = int(tt[EV[e], gg]) if gg < NI else 0
+            return x - int(t[EV["SM_S"], 200]) if x else None
+        pv3 = ev("PV_ISS", gg - 3) - ev("SM_S", 200) if ev("PV_ISS", gg - 3) is not None else None
+        print(f"   {gg}: {q('S_ISS', t)} {q('PV_ISS', t)} | {q('SM_P', t)} {q('ROT', t)} {q('ROT', tp)} {q('FWV', t)} {q('FWV', tp)} | {pv3}")
     for gg in range(200, 204):
         print("   peer g%-4d " % gg + " ".join(f"{k}={(evp(k, gg) or 0) - (evp('SM_S', 200) or 0)}" for k in ("SM_S", "SM_P", "CPK", "CPV", "FWV", "ROT")))
         print("   lead g%-4d " % gg + " ".join(f"{k}={(ev(k, gg) or 0) - (ev('SM_S', 200) or 0)}" for k in ("SM_S", "SM_P", "CPK", "CPV", "FWV", "ROT", "VR_OK", "P_OK", "PV_ISS", "S_ISS")))

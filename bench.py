@@ -52,8 +52,16 @@ def peaks():
 
 
 # ----------------------------------------------------------------------------- workload arithmetic
+# the attention kernel the library runs (attn_fa.cu): v8 = the CTA-pair kernel (default), v7 with DSC_FA=7
+FA_VER = "7" if os.environ.get("DSC_FA", "")[:1] == "7" else "8"
+FA_KERNEL = {"8": "attn_pair_kernel (v8: tcgen05.mma.cta_group::2 CTA-pair rotate-on-load GQA flash attention)",
+             "7": "attn_fa_kernel (v7 tcgen05 rotate-on-load GQA flash attention)"}[FA_VER]
+
+
 def traffic_key(args, world: int) -> str:
     key = f"{args.config}|{args.mode}|{args.api}|boost{args.boost:g}|world{world}|layerseq{int(args.layer_seq)}"
+    if FA_VER == "8" and args.mode != "decode":   # v8 captures are keyed apart from the v7 ones
+        key = "v8|" + key
     if getattr(args, "approx", 0):
         key += f"|approx{args.approx}"
     if getattr(args, "instant_frames", None):
@@ -438,7 +446,7 @@ def run_ours(args, cfg, world, rank, local):
         "frames_per_s_per_stream": round(value / cfg.num_streams, 3),
         "attention_tflops_per_gpu_step": round(step_tflops, 2),
         "attention_pct_peak_step": round(100 * step_tflops / pk["bf16_tflops"], 2),
-        "roofline": {"bound": "tensor", "kernel": "attn_fa_kernel (v7 tcgen05 rotate-on-load GQA flash attention)",
+        "roofline": {"bound": "tensor", "kernel": FA_KERNEL,
                      "achieved": round(achieved, 2) if achieved else None, "peak": pk["bf16_tflops"],
                      "peak_source": pk["source"] + " bf16 burst", "unit": "TFLOP/s",
                      "frac": round(achieved / pk["bf16_tflops"], 4) if achieved else None,

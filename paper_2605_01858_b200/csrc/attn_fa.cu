@@ -1360,20 +1360,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int c8 = lt & 7;             // frequencies 8*c8 .. 8*c8+7
     const int rg = lt >> 3;            // key rows rg*4 .. rg*4+3 of this CTA's half
     const float4* __restrict__ rp = p.rope_pairs;
-    float2 cth[4], sth[4];             // R(theta_f) = table entry of id 1
-    float2 rkc[3][4], rks[3][4];       // R(k theta_f), k = 1, 2, 3 (ids 1..3)
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float4 t = rp[32 * (k + 1) + 4 * c8 + j];
-        rkc[k][j] = make_float2(t.x, t.y);
-        rks[k][j] = make_float2(t.z, t.w);
-      }
+    float2 cth[4], sth[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      cth[j] = rkc[0][j];
-      sth[j] = rks[0][j];
+      const float4 t = rp[32 + 4 * c8 + j];
+      cth[j] = make_float2(t.x, t.y);
+      sth[j] = make_float2(t.z, t.w);
     }
     auto prep_q = [&](int kq) {
       const ItemRec rq = load_rec(recs, kq);
@@ -1530,7 +1522,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (lt == 0) PT(PT_ROT_KR, g);
           if (!PR_ABL_ROT) {
             if (__all_sync(0xffffffffu, consec))
-              rotate4_consec<kKHalf>(tile, rg * 4, c8, rkc, rks, pre);
+              rotate4_consec<kKHalf>(tile, rg * 4, c8, cth, sth, pre);
             else if (rg * 4 < nh)   // rows >= nh are never read by the MMA
               rotate_rows<1, kKHalf>(tile, rg * 4, c8, rp, cth, sth, kpos, pre, max(p0, 0));
           }

@@ -317,12 +317,13 @@ __device__ __forceinline__ void rotate_rows(uint32_t tile, int r0, int c8, const
 }
 
 // rotate_rows for 4 rows r0 .. r0+3 with CONSECUTIVE ids p0 .. p0+3 (a window tile: no
-// per-row branches).  Row k's (cos, sin) = R(p0) R(k theta), from the table entry of p0 and
-// the entries of ids 1, 2, 3 (rk[k-1]): the four rows are independent chains (ILP), not a
-// recurrence through the previous row.
+// per-row branches): (cs, sn) start at the table entry of p0 and advance by R(theta) per row
 template <int HI>
-__device__ __forceinline__ void rotate4_consec(uint32_t tile, int r0, int c8, const float2 (&rc)[3][4],
-                                               const float2 (&rs)[3][4], const float4 (&pre)[4]) {
+__device__ __forceinline__ void rotate4_consec(uint32_t tile, int r0, int c8, const float2 (&cth)[4],
+                                               const float2 (&sth)[4], const float4 (&pre)[4]) {
+  float2 cs[4], sn[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) { cs[j] = make_float2(pre[j].x, pre[j].y); sn[j] = make_float2(pre[j].z, pre[j].w); }
   uint4 lo[4], hi[4];
   uint32_t addr[4];
 #pragma unroll
@@ -332,27 +333,22 @@ __device__ __forceinline__ void rotate4_consec(uint32_t tile, int r0, int c8, co
     lo[k] = lds128(addr[k]);
     hi[k] = lds128(addr[k] + HI);
   }
-  float2 cs[4][4], sn[4][4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    cs[0][j] = make_float2(pre[j].x, pre[j].y);
-    sn[0][j] = make_float2(pre[j].z, pre[j].w);
-  }
-#pragma unroll
-  for (int k = 1; k < 4; ++k)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      cs[k][j] = __ffma2_rn(cs[0][j], rc[k - 1][j], __fmul2_rn(make_float2(-sn[0][j].x, -sn[0][j].y), rs[k - 1][j]));
-      sn[k][j] = __ffma2_rn(sn[0][j], rc[k - 1][j], __fmul2_rn(cs[0][j], rs[k - 1][j]));
-    }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
+    if (k > 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 nc = __ffma2_rn(cs[j], cth[j], __fmul2_rn(make_float2(-sn[j].x, -sn[j].y), sth[j]));
+        sn[j] = __ffma2_rn(sn[j], cth[j], __fmul2_rn(cs[j], sth[j]));
+        cs[j] = nc;
+      }
+    }
     uint32_t ol[4], oh[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float2 av = bf2(get_w(lo[k], j)), bv = bf2(get_w(hi[k], j));
-      const float2 yl = __ffma2_rn(av, cs[k][j], __fmul2_rn(make_float2(-bv.x, -bv.y), sn[k][j]));   // a cos - b sin
-      const float2 yh = __ffma2_rn(av, sn[k][j], __fmul2_rn(bv, cs[k][j]));                        // a sin + b cos
+      const float2 yl = __ffma2_rn(av, cs[j], __fmul2_rn(make_float2(-bv.x, -bv.y), sn[j]));   // a cos - b sin
+      const float2 yh = __ffma2_rn(av, sn[j], __fmul2_rn(bv, cs[j]));                        // a sin + b cos
       ol[j] = pack_bf16(yl.x, yl.y);
       oh[j] = pack_bf16(yh.x, yh.y);
     }

@@ -988,7 +988,12 @@ constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + NQB * kQBytes;
 constexpr int OFF_V = OFF_K + KST * kKBytes;
 constexpr int OFF_BAR = OFF_V + VST * kVBytes;
-constexpr int NSB = 3;                    // S buffers in TMEM
+// TMEM: NSB S buffers + NOB O buffers of 128 columns (PR_NOB = 1: S[3], O; 2: S[2], O[2])
+#ifndef PR_NOB
+#define PR_NOB 1
+#endif
+constexpr int NOB = PR_NOB;
+constexpr int NSB = 4 - NOB;
 enum {
   B_QR = 0,             // [2] Q buffer ready (leader: 4 warps x 2 CTAs)
   B_QF = B_QR + 2,      // [2] Q buffer free (commit after its item's last QK^T)
@@ -1000,9 +1005,9 @@ enum {
   B_VE = B_VR + VST,    // [VST] V stage free = PV done (commit)
   B_S = B_VE + VST,     // [NSB] S buffer ready (commit)
   B_P = B_S + NSB,      // [NSB] P ready (leader: 8 softmax warps x 2 CTAs)
-  B_O = B_P + NSB,      // O final for its item (commit)
-  B_OF = B_O + 1,       // O read out (leader: 4 warps x 2 CTAs)
-  B_LR = B_OF + 1,      // [2] (l, m) of an item's rows written (256 softmax threads)
+  B_O = B_P + NSB,      // [NOB] O final for its item (commit)
+  B_OF = B_O + NOB,     // [NOB] O read out (leader: 4 warps x 2 CTAs)
+  B_LR = B_OF + NOB,      // [2] (l, m) of an item's rows written (256 softmax threads)
   B_LF = B_LR + 2,      // [2] ... read by the epilogue (128)
   B_N = B_LF + 2
 };
@@ -1191,8 +1196,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(bar(B_S + i), 1);
       mbar_init(bar(B_P + i), 16);
     }
-    mbar_init(bar(B_O), 1);
-    mbar_init(bar(B_OF), 8);
+    for (int i = 0; i < NOB; ++i) {
+      mbar_init(bar(B_O + i), 1);
+      mbar_init(bar(B_OF + i), 8);
+    }
     for (int i = 0; i < KST; ++i) {
       mbar_init(bar(B_KR + i), 1);
       mbar_init(bar(B_KF + i), 8);
@@ -1239,7 +1246,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int rloc = quarter * 32 + lane;
     const int c0 = 64 * hc;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t tO = tO_base + lane_off + (uint32_t)c0;
+    const uint32_t tO0 = tO_base + lane_off + (uint32_t)c0;
     const float sl2 = p.scale_log2;
     const float2 scale2 = make_float2(sl2, sl2);
     int g = 0;
@@ -1254,6 +1261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int qi = valid_row ? rglob / p.grp : 0;
       const int lim = valid_row ? p.q_pos0 + qi : -1;
       const bool warp_dead = __all_sync(0xffffffffu, !valid_row);   // same for both halves of a quarter
+      const uint32_t tO = tO0 + (uint32_t)((kk % NOB) * 128);
       float m = -INFINITY;
       float2 lsum2 = make_float2(0.f, 0.f);
       uint32_t r[64];
@@ -1405,10 +1413,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const float lsum = lm0.x + lm1.x;
       const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
       const bool part = p.n_splits > 1 || p.split_only >= 0;
-      fwait(bar(B_O), ke & 1, bar0);
+      fwait(bar(B_O + ke % NOB), (ke / NOB) & 1, bar0);
       if (lt == 0) PT(PT_EPI_O, ke);
       tc_fence_after();
-      const uint32_t tO = tO_base + ((uint32_t)((lt >> 5) * 32) << 16);
+      const uint32_t tO = tO_base + (uint32_t)((ke % NOB) * 128) + ((uint32_t)((lt >> 5) * 32) << 16);
       uint32_t r[64];
       if (!part) {
         uint32_t pk[64];   // O / l as bf16 pairs: the O columns leave TMEM before any store
@@ -1425,7 +1433,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) arrive_cl(lbar(B_OF), 1);   // O may take item ke + 1
+        if (lane == 0) arrive_cl(lbar(B_OF + ke % NOB), 1);   // this O buffer may take item ke + NOB
         if (valid_row && !PR_ABL_EPI) {
           const bool peers = p.n_peers > 0;
           int oq = qi + p.o_rot;   // o_rot = 0 unless ring-ordered output (o_rows > 0)
@@ -1455,7 +1463,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (hf == 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) arrive_cl(lbar(B_OF), 1);
+            if (lane == 0) arrive_cl(lbar(B_OF + ke % NOB), 1);
           }
           if (!valid_row) continue;
           float4* dst = reinterpret_cast<float4*>(p.ws_o + (slot * rows + orow) * 128 + 64 * hf);
@@ -1695,7 +1703,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       auto ready_pv = [&](int k, int jj, int g) {
         if (!mbar_test(bar(B_VR + g % VST), (g / VST) & 1)) return false;
         if (!mbar_test(bar(B_P + g % NSB), (g / NSB) & 1)) return false;
-        return !(jj == 0 && k >= 1) || mbar_test(bar(B_OF), (k - 1) & 1);
+        return !(jj == 0 && k >= NOB) || mbar_test(bar(B_OF + k % NOB), ((k - NOB) / NOB) & 1);
       };
       auto issue_pv = [&](const MI& m, int k, int jj, int g) {
         const int vs = g % VST, sb = g % NSB;
@@ -1703,7 +1711,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const int nu = width_of(m, jj);
         const uint64_t dv = sdesc(sbase + OFF_V + vs * kVBytes, 16, 1024);
-        const uint32_t d = tO_base, a = tmem + (uint32_t)(sb * 128);
+        const uint32_t d = tO_base + (uint32_t)((k % NOB) * 128), a = tmem + (uint32_t)(sb * 128);
         const uint32_t acc = jj > 0 ? 1u : 0u;
         if (nu == BN) {
           mma2_pv8(d, a, dv, IPV, acc);
@@ -1714,7 +1722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (lane == 0) PT(PT_PV_MMA, g);
         commit2_w(bar(B_VE + vs));
-        if (jj + 1 == m.n) commit2_w(bar(B_O));
+        if (jj + 1 == m.n) commit2_w(bar(B_O + k % NOB));
         if (lane == 0) PT(PT_PV_ISS, g);
       };
       // Two cursors over the same tile sequence, each issued as soon as its operands are
@@ -1727,7 +1735,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         long long t_idle = 0;
         while (v_k < n_my) {
           bool did = false;
-          if (s_k < n_my && s_g <= v_g + 2 && ready_s(s_k, s_jj, s_g)) {
+          if (s_k < n_my && s_g <= v_g + (NSB - 1) && ready_s(s_k, s_jj, s_g)) {
             issue_s(s_m, s_k, s_jj, s_g);
             ++s_g;
             if (++s_jj == s_m.n) {

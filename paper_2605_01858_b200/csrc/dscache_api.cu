@@ -29,7 +29,10 @@
 #define DSC_STAGE_MIN 2LL
 #endif
 #ifndef DSC_SPLIT_DIV
-#define DSC_SPLIT_DIV 2   // measured vs 1: c4 +13.5%, c2 +24%, kvsplit +4.5% (3: c4 -5%)
+// v8 (two-SM clusters, num_sms / 2 of them): 4 = 37 items measured best vs 2 (74): c2 +3.5 %,
+// c4 +4.6 %, context split +6.7 %, kvsplit +1.3 %, c5 0; 6 / 8 lose 3-18 % except kvsplit
+// (+3 %) (profiles/r2c/ab_split_div_*.txt).  v7 (single-SM CTAs) measured 2 best.
+#define DSC_SPLIT_DIV 4
 #endif
 
 namespace {

@@ -26,7 +26,7 @@
 // (problem, kv head, m-block) items cannot fill the SMs
 // DSC_STAGE_MIN: the build is staged when it has at least DSC_STAGE_MIN * num_sms items
 #ifndef DSC_STAGE_MIN
-#define DSC_STAGE_MIN 2LL
+#define DSC_STAGE_MIN 1LL   // v8: 1 measured c4 +4.5 % vs 2, c2 / c3 / c5 unchanged (profiles/r2c/ab_ogrp_stage.txt)
 #endif
 #ifndef DSC_SPLIT_DIV
 // v8 (two-SM clusters, num_sms / 2 of them): 4 = 37 items measured best vs 2 (74): c2 +3.5 %,

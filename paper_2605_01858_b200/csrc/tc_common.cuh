@@ -159,7 +159,8 @@ __host__ __device__ __forceinline__ Item decode_item(const PT& p, int idx) {
   w.mb = p.n_mblocks - 1 - rest / (p.P * p.Hkv);
 #elif DSC_ORDER == 2   // longest-first inside groups of kOrderGroup (problem, head) pairs (L2 reuse)
 #ifndef DSC_OGRP
-#define DSC_OGRP 74   // measured: 74 +0.3-0.8%, 37 +0.3%, 296 -2.8% vs 148 (c5)
+#define DSC_OGRP 37   // v8 (74 clusters): 37 measured c3 +1.5 % vs 74, c5 / c2 / c4 within noise, 148 -1 to -2 %
+                      // (profiles/r2c/ab_ogrp_stage.txt); v7 (148 CTAs) measured 74 best
 #endif
   constexpr int kOrderGroup = DSC_OGRP;
   const int nph = p.P * p.Hkv;

@@ -383,6 +383,28 @@ dscache_status dscache_copy_ring(dscache_t h, int32_t stream_idx, int32_t layer,
 dscache_status dscache_copy_sink(dscache_t h, int32_t stream_idx, int32_t layer,
                                  void* k_host, void* v_host);
 
+/* Checkpoint restore (SURVEY §5 checkpoint / resume; "bit-exact round trip").
+ * The streaming state of a handle is the host counters of each layer plus the device ring and
+ * sink slabs (everything later steps read is U, A and the frame counter).
+ * A checkpoint is dscache_get_state + dscache_copy_ring + dscache_copy_sink for every
+ * (stream, layer); a handle created with the same config and given these three calls resumes
+ * with results bit-identical to the uninterrupted handle's (same kernels, same inputs).
+ * restore_ring : HOST [Hkv][R][d] each, the layout dscache_copy_ring writes; also refreshes the
+ *                mirror rows R..R+127 (create's layout).  Synchronous: waits for the device
+ *                before and after, so no queued kernel reads half-replaced rows.
+ * restore_sink : HOST [Hkv][A][d] each (no-op when A = 0).  Synchronous.
+ * set_state    : the counters of `layer`: frames_seen (>= 0) and sink_filled (0/1) as
+ *                dscache_get_state reported them; the last evicted frame follows from the
+ *                closed form (Eq. 6).  The approximate instant cache (NEXT-3) restarts its
+ *                reuse chain: the next dscache_build_instant_approx refreshes (exact rows).
+ * Errors: E_ARG (null, out of range), E_STATE (frames without a sink, sink_filled = 0 when
+ * A = 0), E_CUDA. */
+dscache_status dscache_restore_ring(dscache_t h, int32_t stream_idx, int32_t layer,
+                                    const void* k_host, const void* v_host);
+dscache_status dscache_restore_sink(dscache_t h, int32_t stream_idx, int32_t layer,
+                                    const void* k_host, const void* v_host);
+dscache_status dscache_set_state(dscache_t h, int32_t layer, int64_t frames_seen, int32_t sink_filled);
+
 /* Debug exports (K7).  build_pos / attend_pos: NULL = off, else DEVICE int32
  * buffers of num_streams * num_layers * dscache_debug_len(h) entries, one block of
  * dscache_debug_len(h) per (stream, layer) ([S][N][len], int32), which the attention and

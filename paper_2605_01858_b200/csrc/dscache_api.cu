@@ -1187,6 +1187,61 @@ dscache_status dscache_copy_sink(dscache_t h, int32_t s_idx, int32_t layer, void
   return copy_rows(h, s_idx, layer, h->sink_k, h->sink_v, h->cfg.sink_tokens, h->cfg.sink_tokens, kh, vh);
 }
 
+// rows per head [rows] uploaded into a device layout with `pitch_rows` rows per head (inverse
+// of copy_rows); mirror = also write slots [0, min(rows, kMirror)) to rows [rows, rows + ...)
+static dscache_status upload_rows(dscache_t h, int s_idx, int layer, void* dk, void* dv, int rows, int pitch_rows,
+                                  bool mirror, const void* kh, const void* vh) {
+  if (!h || !kh || !vh) return fail(DSCACHE_E_ARG, "null argument");
+  const dscache_config& c = h->cfg;
+  if (s_idx < 0 || s_idx >= c.num_streams || layer < 0 || layer >= c.num_layers)
+    return fail(DSCACHE_E_ARG, "stream/layer out of range");
+  DeviceGuard dg(c.device);
+  const size_t row_bytes = (size_t)c.head_dim * h->elem;
+  const size_t off = ((size_t)s_idx * c.num_layers + layer) * c.num_kv_heads * pitch_rows * row_bytes;
+  DSC_CUDA(cudaDeviceSynchronize());   // no kernel of any stream may still read the rows replaced
+  for (int which = 0; which < 2; ++which) {
+    char* dst = (char*)(which ? dv : dk) + off;
+    const void* src = which ? vh : kh;
+    DSC_CUDA(cudaMemcpy2D(dst, pitch_rows * row_bytes, src, rows * row_bytes, rows * row_bytes, c.num_kv_heads,
+                          cudaMemcpyHostToDevice));
+    const int nm = std::min(rows, dsc::kMirror);
+    if (mirror && nm > 0)
+      DSC_CUDA(cudaMemcpy2D(dst + rows * row_bytes, pitch_rows * row_bytes, src, rows * row_bytes, nm * row_bytes,
+                            c.num_kv_heads, cudaMemcpyHostToDevice));
+  }
+  DSC_CUDA(cudaDeviceSynchronize());
+  return DSCACHE_OK;
+}
+
+dscache_status dscache_restore_ring(dscache_t h, int32_t s_idx, int32_t layer, const void* kh, const void* vh) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  return upload_rows(h, s_idx, layer, h->ring_k, h->ring_v, h->R, h->Rp, true, kh, vh);
+}
+
+dscache_status dscache_restore_sink(dscache_t h, int32_t s_idx, int32_t layer, const void* kh, const void* vh) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  if (h->cfg.sink_tokens == 0) return DSCACHE_OK;
+  return upload_rows(h, s_idx, layer, h->sink_k, h->sink_v, h->cfg.sink_tokens, h->cfg.sink_tokens, false, kh, vh);
+}
+
+dscache_status dscache_set_state(dscache_t h, int32_t layer, int64_t frames_seen, int32_t sink_filled) {
+  if (!h) return fail(DSCACHE_E_ARG, "null handle");
+  const dscache_config& c = h->cfg;
+  if (layer < 0 || layer >= c.num_layers) return fail(DSCACHE_E_ARG, "layer out of range");
+  if (frames_seen < 0 || (sink_filled != 0 && sink_filled != 1))
+    return fail(DSCACHE_E_ARG, "frames_seen must be >= 0 and sink_filled 0 or 1");
+  if (c.sink_tokens == 0 && !sink_filled) return fail(DSCACHE_E_STATE, "A = 0: the sink is always filled");
+  if (frames_seen > 0 && !sink_filled) return fail(DSCACHE_E_STATE, "frames cannot precede the sink");
+  // ids stay below max_position for any frames_seen: create bounded A + W + max(C + q_max, tpf)
+  h->frames[layer] = frames_seen;
+  h->sink_filled[layer] = sink_filled;
+  const int64_t ev = frames_seen - 1 - c.instant_frames - c.past_frames;   // dropped at the latest append (Eq. 6)
+  h->last_evicted[layer] = ev >= 0 ? ev : -1;
+  h->approx_last[layer] = -1;   // the approximate cache's reuse chain restarts with a refresh
+  h->approx_ring[layer] = nullptr;
+  return DSCACHE_OK;
+}
+
 int32_t dscache_debug_len(dscache_t h) {
   if (!h) return 0;
   return h->cfg.sink_tokens + h->R + 2 * std::max(h->C, h->cfg.max_query_tokens);   // per problem

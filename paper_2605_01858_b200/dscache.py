@@ -59,6 +59,7 @@ EXPORTS = ["dscache_create", "dscache_destroy", "dscache_append_frame", "dscache
            "dscache_append_past", "dscache_build_instant_ext", "dscache_attend_ext", "dscache_decode_ext",
            "dscache_attend", "dscache_update_attend", "dscache_decode", "dscache_build_instant_newest",
            "dscache_instant_approx_rows", "dscache_build_instant_approx", "dscache_decode_sampled", "dscache_step", "dscache_get_state", "dscache_copy_ring", "dscache_copy_sink",
+           "dscache_restore_ring", "dscache_restore_sink", "dscache_set_state",
            "dscache_set_debug", "dscache_debug_len", "dscache_set_trace", "dscache_profile", "dscache_profile_read",
            "dscache_attn_impl", "dscache_watchdog_read", "dscache_last_error", "dscache_attend_partial", "dscache_combine_partials",
            "dscache_build_instant_boost", "dscache_attend_boost", "dscache_attend_peers",
@@ -93,6 +94,9 @@ def load_library(path: str = LIB_PATH):
         "dscache_get_state": ([P, I32, ctypes.POINTER(State)], I32),
         "dscache_copy_ring": ([P, I32, I32, P, P], I32),
         "dscache_copy_sink": ([P, I32, I32, P, P], I32),
+        "dscache_restore_ring": ([P, I32, I32, P, P], I32),
+        "dscache_restore_sink": ([P, I32, I32, P, P], I32),
+        "dscache_set_state": ([P, I32, I64, I32], I32),
         "dscache_set_debug": ([P, P, P, I32], I32),
         "dscache_debug_len": ([P], I32),
         "dscache_set_trace": ([P, P, I32], I32),
@@ -560,6 +564,52 @@ class DSCache:
         v = torch.empty(shape, dtype=self.torch_dtype)
         _check(_lib.dscache_copy_sink(self._h, stream_idx, layer, _ptr(k), _ptr(v)))
         return k, v
+
+    # ------------------------------------------------------------------ checkpoint / resume
+    def restore_ring(self, stream_idx: int, layer: int, k: torch.Tensor, v: torch.Tensor):
+        """Upload a ring snapshot ([Hkv][R][d] host tensors, as copy_ring returns them)."""
+        c = self.cfg
+        shape = (c.num_kv_heads, self.R, c.head_dim)
+        for t in (k, v):
+            if tuple(t.shape) != shape or t.dtype != self.torch_dtype or t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"ring snapshot must be contiguous host {self.torch_dtype} {shape}")
+        _check(_lib.dscache_restore_ring(self._h, stream_idx, layer, _ptr(k), _ptr(v)))
+
+    def restore_sink(self, stream_idx: int, layer: int, k: torch.Tensor, v: torch.Tensor):
+        """Upload a sink snapshot ([Hkv][A][d] host tensors, as copy_sink returns them)."""
+        c = self.cfg
+        shape = (c.num_kv_heads, c.sink_tokens, c.head_dim)
+        for t in (k, v):
+            if tuple(t.shape) != shape or t.dtype != self.torch_dtype or t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"sink snapshot must be contiguous host {self.torch_dtype} {shape}")
+        _check(_lib.dscache_restore_sink(self._h, stream_idx, layer, _ptr(k), _ptr(v)))
+
+    def set_state(self, layer: int, frames_seen: int, sink_filled: int):
+        _check(_lib.dscache_set_state(self._h, layer, int(frames_seen), int(sink_filled)))
+
+    def snapshot(self) -> bytes:
+        """The whole streaming state as one flat little-endian blob (checkpoint.pack)."""
+        from . import checkpoint
+        c = self.cfg
+        counters = [(self.state(l)["frames_seen"], self.state(l)["sink_filled"]) for l in range(c.num_layers)]
+        slabs = {}
+        for s in range(c.num_streams):
+            for l in range(c.num_layers):
+                slabs[(s, l)] = self.copy_sink(s, l) + self.copy_ring(s, l)
+        return checkpoint.pack(c, self.R, counters, slabs)
+
+    def restore(self, blob: bytes):
+        """Resume from snapshot(): the config must match this handle's field for field."""
+        from . import checkpoint
+        counters, slabs = checkpoint.unpack(blob, self.cfg, self.R)
+        c = self.cfg
+        for s in range(c.num_streams):
+            for l in range(c.num_layers):
+                sk, sv, rk, rv = slabs[(s, l)]
+                self.restore_sink(s, l, sk, sv)
+                self.restore_ring(s, l, rk, rv)
+        for l, (f, sf) in enumerate(counters):
+            self.set_state(l, f, sf)
 
     def debug_len(self) -> int:
         return int(_lib.dscache_debug_len(self._h))

@@ -91,6 +91,15 @@ def test_snapshot_restore_resumes_bit_exact(lib, name, t_snap, fused):
         assert torch.equal(oa, ob), f"O differs {t_snap + t} steps in"
     for l in range(cfg.num_layers):
         assert b.state(l) == a.state(l)
+    # decode (NEXT-2) over the resumed cache, dense and with the 0.5 FPS past stride
+    S, N, Hq, Hkv, d = cfg.num_streams, cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim
+    n_self = cfg.query_tokens + 5
+    dt = a.torch_dtype
+    ks = torch.randn((S, N, n_self, Hkv, d), generator=gen, device=dev).to(dt)
+    vs = torch.randn((S, N, n_self, Hkv, d), generator=gen, device=dev).to(dt)
+    q = torch.randn((S, N, 1, Hq, d), generator=gen, device=dev).to(dt)
+    for stride in (1, 2):
+        assert torch.equal(a.decode(q, ks, vs, past_stride=stride), b.decode(q, ks, vs, past_stride=stride))
 
 
 def test_restore_rejects_other_config(lib):

@@ -82,3 +82,7 @@ def test_null_arguments():
     assert lib.dscache_create(None, None) == -1
     assert lib.dscache_append_frame(None, 0, 1, None, None, 4, None) == -1
     assert lib.dscache_destroy(None) == -1
+    # checkpoint restore calls: null handle -> E_ARG before any device work
+    assert lib.dscache_restore_ring(None, 0, 0, None, None) == -1
+    assert lib.dscache_restore_sink(None, 0, 0, None, None) == -1
+    assert lib.dscache_set_state(None, 0, 0, 1) == -1

@@ -128,3 +128,53 @@ def test_set_state_validation(lib):
     lI, lU, tpf = cfg.instant_frames, cfg.past_frames, cfg.tokens_per_frame
     assert st["frames_seen"] == 9 and st["last_evicted_frame"] == 9 - 1 - lI - lU
     assert st["instant_tokens"] == lI * tpf and st["past_tokens"] == lU * tpf
+
+
+@pytest.mark.parametrize("t_snap", [2, 9])
+def test_snapshot_restore_external_instant_mode(lib, t_snap):
+    """Real-model mode (NEXT-1): U holds the caller's Eq. 5 K/V (append_past); a restored
+    handle resumes update_attend / build_instant_ext / attend_ext bit-identically."""
+    cfg = CASES["c2_multi"]
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(991 + t_snap)
+    S, N, tpf, Hq, Hkv, d, lI, nq = (cfg.num_streams, cfg.num_layers, cfg.tokens_per_frame, cfg.num_q_heads,
+                                     cfg.num_kv_heads, cfg.head_dim, cfg.instant_frames, cfg.query_tokens)
+    dt = torch.bfloat16
+
+    def r(*shape):
+        return (torch.randn(shape, generator=gen, device=dev) * cfg.scale).to(dt)
+
+    def advance(hs, t):
+        e = t - lI
+        if e >= 0:
+            kp, vp = r(S, N, tpf, Hkv, d), r(S, N, tpf, Hkv, d)
+            for h in hs:
+                h.append_past(kp, vp)
+        else:
+            for h in hs:
+                h.append_past(None, None)
+        C_t = min(t + 1, lI) * tpf
+        qi, ki, vi = r(S, N, C_t, Hq, d), r(S, N, C_t, Hkv, d), r(S, N, C_t, Hkv, d)
+        q, ks, vs = r(S, N, nq, Hq, d), r(S, N, nq, Hkv, d), r(S, N, nq, Hkv, d)
+        qu = r(S, N, tpf, Hq, d) if e >= 0 else None
+        res = []
+        for h in hs:
+            out = [h.build_instant_ext(qi, ki, vi).clone(), h.attend_ext(q, ks, vs, ki, vi).clone()]
+            if qu is not None:
+                out.append(h.update_attend(qu, active_frames=cfg.past_frames).clone())
+            res.append(out)
+        return res
+
+    a = D.DSCache.from_config(cfg, instant_source=D.INSTANT_EXTERNAL)
+    _sink(cfg, a, gen, dev)
+    for t in range(t_snap):
+        advance([a], t)
+    torch.cuda.synchronize()
+    b = D.DSCache.from_config(cfg, instant_source=D.INSTANT_EXTERNAL)
+    b.restore(a.snapshot())
+    for t in range(t_snap, t_snap + cfg.past_frames + lI + 2):
+        ra, rb = advance([a, b], t)
+        torch.cuda.synchronize()
+        for x, y in zip(ra, rb):
+            assert torch.equal(x, y), f"step {t}"
